@@ -1,0 +1,69 @@
+/*
+ * ps_b200.h -- C-ABI of the B200-native seeding hot path (libps_b200.so).
+ *
+ * Conventions:
+ *   - every pointer argument is a DEVICE pointer unless its name ends in _h;
+ *   - `stream` is a cudaStream_t passed as void* (torch's current stream);
+ *   - no allocation inside the hot path: callers pass outputs and workspaces;
+ *   - return 0 (PS_OK) or a status; the host shim maps statuses to the
+ *     reference's exceptions (ValueError for shapes / out-of-grid).
+ *   - results are deterministic run to run and independent of batch splits.
+ *
+ * Each entry point names the reference interface it replaces (file:line under
+ * /root/reference/pkg/src/planseed/).
+ */
+#ifndef PS_B200_H
+#define PS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PS_OK 0
+#define PS_ERR_OUT_OF_GRID 1
+#define PS_ERR_SHAPE 2
+#define PS_ERR_CUDA 3
+
+/* library identification: returns a static string, e.g. "ps_b200 sm_100a" */
+const char* ps_version(void);
+
+/* ====================== BASELINE profile (3-D, fp32) ======================= */
+
+/* ESDF construction: analytic signed distance to axis-aligned boxes, sampled on
+ * n[0] x n[1] x n[2] nodes (C-order), node (i,j,k) at origin + h*(i,j,k).
+ * boxes: (P, n_boxes, 6) lo/hi; out: (P, nx*ny*nz).  3-D form of
+ * _kernels.analytic_sdf (_kernels.py:60-83) + geometry.build_esdf (geometry.py:195-210). */
+int ps_esdf_build_boxes(const float* boxes, int P, int n_boxes, const int* n_h,
+                        const float* origin_h, float h, float cap, float* out, void* stream);
+
+/* Batched cost and gradient (no update): cost (B,), grad (B,T,7) with row 0 zero,
+ * clamped (B,) uint8.  Trajectory b reads ESDF esdf + (b / S) * esdf_stride.
+ * BL analogue of _kernels.cost_terms_batch (_kernels.py:165-312). */
+int ps_bl_cost(const float* q, int B, int T, int S, const float* esdf, long long esdf_stride,
+               const int* n_h, const float* origin_h, float h, const float* dh_h,
+               const float* base_h, const float* sph_h, const int* sph_link_h, int n_sph,
+               const float* weights_h, float* cost, float* grad, uint8_t* clamped, void* stream);
+
+/* Fused refinement: n_iters fixed gradient steps (row 0 pinned), then final cost,
+ * dense feasibility (waypoints + 4 interpolants per segment, d - r > 0) and
+ * clamped flags.  One warp per trajectory; state stays in registers.
+ * BL analogue of _kernels.optimize_batch (_kernels.py:315-431) +
+ * pipeline.planner_success (pipeline.py:139-157).
+ * weights_h = (w_coll, w_vel, w_acc, w_jerk, margin, eta).  T in {32, 64}. */
+int ps_bl_refine(const float* q_in, int B, int T, int S, const float* esdf,
+                 long long esdf_stride, const int* n_h, const float* origin_h, float h,
+                 const float* dh_h, const float* base_h, const float* sph_h,
+                 const int* sph_link_h, int n_sph, const float* weights_h, int n_iters,
+                 float* q_out, float* cost, uint8_t* feasible, uint8_t* clamped, void* stream);
+
+/* Best seed per problem: lowest-cost feasible seed, else lowest cost; ties to the
+ * lower index.  pipeline.select_best (pipeline.py:160-165).  best: (P,) int32. */
+int ps_select(const float* cost, const uint8_t* feasible, int P, int S, int32_t* best,
+              void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,88 @@
+"""ctypes binding of libps_b200.so (the C-ABI declared in include/ps_b200.h).
+
+The product path has no CPU fallback: if the library is missing or no CUDA device
+is visible, every entry point raises.  Tensors cross the boundary as raw device
+pointers plus sizes; torch is only the allocator and stream provider.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import numpy as np
+
+from . import build as _build
+
+PS_OK, PS_ERR_OUT_OF_GRID, PS_ERR_SHAPE, PS_ERR_CUDA = 0, 1, 2, 3
+
+_c_int, _c_ll, _c_f, _vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_float, ctypes.c_void_p
+
+# name -> argtypes ; every function returns int (status) unless listed in _RESTYPE
+_SIGS = {
+    "ps_version": [],
+    "ps_esdf_build_boxes": [_vp, _c_int, _c_int, _vp, _vp, _c_f, _c_f, _vp, _vp],
+    "ps_bl_cost": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,
+                   _c_int, _vp, _vp, _vp, _vp, _vp],
+    "ps_bl_refine": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,
+                     _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp],
+    "ps_select": [_vp, _vp, _c_int, _c_int, _vp, _vp],
+}
+_RESTYPE = {"ps_version": ctypes.c_char_p}
+
+_lib = None
+
+
+class PSError(RuntimeError):
+    pass
+
+
+def lib():
+    """Load (never build) the in-tree library; fail loudly if it is absent."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if not path.exists():
+            raise PSError(f"{path} is missing: run __graft_entry__.build() (no CPU fallback)")
+        L = ctypes.CDLL(str(path))
+        for name, args in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPE.get(name, ctypes.c_int)
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def check(status: int, what: str):
+    if status == PS_OK:
+        return
+    if status == PS_ERR_OUT_OF_GRID:
+        raise ValueError(f"{what}: trajectory collision points leave the ESDF extent")
+    if status == PS_ERR_SHAPE:
+        raise ValueError(f"{what}: bad shape or argument")
+    raise PSError(f"{what}: CUDA error (status {status})")
+
+
+def require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise PSError("no CUDA device visible: the B200 path has no CPU fallback")
+    return torch
+
+
+def ptr(t) -> int:
+    return t.data_ptr()
+
+
+def hptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

@@ -1,0 +1,143 @@
+"""BASELINE-profile refinement API over the C-ABI (batched over problems).
+
+Batched counterparts of the reference refiner / planner helpers:
+  esdf_build      ~ geometry.build_esdf / pipeline.build_planner_esdf  (geometry.py:195-210)
+  cost            ~ trajopt.evaluate_cost_batch                        (trajopt.py:105-119)
+  refine          ~ trajopt.optimize + pipeline.planner_success        (trajopt.py:140-177,
+                                                                        pipeline.py:139-157)
+  select          ~ pipeline.select_best                               (pipeline.py:160-165)
+
+Inputs may be numpy arrays or torch CUDA tensors; outputs are torch CUDA tensors.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .spec import BLCost, DHRobot, GridSpec
+
+
+def _dev(x, dtype=None):
+    torch = _lib.require_cuda()
+    dtype = dtype or torch.float32
+    if isinstance(x, torch.Tensor):
+        t = x if x.is_cuda else x.cuda()
+        return t.to(dtype).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device="cuda")
+
+
+@dataclass
+class RobotTables:
+    """Host float32/int32 tables copied into each kernel's parameter block."""
+
+    dh: np.ndarray
+    base: np.ndarray
+    sph: np.ndarray
+    link: np.ndarray
+
+    @classmethod
+    def of(cls, robot: DHRobot) -> "RobotTables":
+        return cls(dh=np.ascontiguousarray(robot.dh_table_f32()),
+                   base=np.ascontiguousarray(robot.base, dtype=np.float32),
+                   sph=np.ascontiguousarray(robot.sphere_table_f32()),
+                   link=np.ascontiguousarray(robot.sphere_link, dtype=np.int32))
+
+
+def _grid_args(grid: GridSpec):
+    n = np.array(grid.n, dtype=np.int32)
+    o = np.array(grid.origin, dtype=np.float32)
+    return n, o
+
+
+def esdf_build(boxes, grid: GridSpec = GridSpec(), stream=None):
+    """boxes (P, n_boxes, 6) -> ESDF values (P, nx, ny, nz) float32 on device."""
+    torch = _lib.require_cuda()
+    b = _dev(boxes)
+    if b.dim() != 3 or b.shape[2] != 6:
+        raise ValueError("boxes must be (P, n_boxes, 6)")
+    P = b.shape[0]
+    out = torch.empty((P,) + tuple(grid.n), dtype=torch.float32, device="cuda")
+    n, o = _grid_args(grid)
+    st = _lib.lib().ps_esdf_build_boxes(_lib.ptr(b), P, b.shape[1], _lib.hptr(n), _lib.hptr(o),
+                                        grid.h, grid.cap, _lib.ptr(out), _lib.stream_handle(stream))
+    _lib.check(st, "esdf_build")
+    return out
+
+
+def _esdf_stride(esdf, grid: GridSpec, n_problems: int) -> int:
+    if esdf.dim() == 3:
+        return 0                      # one ESDF shared by every problem
+    if esdf.shape[0] == 1:
+        return 0
+    if esdf.shape[0] < n_problems:
+        raise ValueError("need one ESDF per problem (or a single shared one)")
+    return grid.n_nodes
+
+
+def cost(q, esdf, S: int, robot: DHRobot, grid: GridSpec = GridSpec(), w: BLCost = BLCost(),
+         stream=None):
+    """Batched cost (B,), gradient (B,T,7) (row 0 zero) and clamped flags (B,)."""
+    torch = _lib.require_cuda()
+    qd = _dev(q)
+    B, T, D = qd.shape
+    if D != 7 or T not in (32, 64):
+        raise ValueError("q must be (B, 32|64, 7)")
+    e = _dev(esdf)
+    rt = RobotTables.of(robot)
+    n, o = _grid_args(grid)
+    wts = w.as_f32()
+    c = torch.empty(B, dtype=torch.float32, device="cuda")
+    g = torch.empty_like(qd)
+    cl = torch.empty(B, dtype=torch.uint8, device="cuda")
+    st = _lib.lib().ps_bl_cost(_lib.ptr(qd), B, T, S, _lib.ptr(e), _esdf_stride(e, grid, -(-B // S)),
+                               _lib.hptr(n), _lib.hptr(o), grid.h, _lib.hptr(rt.dh),
+                               _lib.hptr(rt.base), _lib.hptr(rt.sph), _lib.hptr(rt.link),
+                               len(rt.link), _lib.hptr(wts), _lib.ptr(c), _lib.ptr(g), _lib.ptr(cl),
+                               _lib.stream_handle(stream))
+    _lib.check(st, "bl_cost")
+    return c, g, cl.bool()
+
+
+def refine(q, esdf, S: int, robot: DHRobot, grid: GridSpec = GridSpec(), w: BLCost = BLCost(),
+           n_iters: int | None = None, stream=None, out=None):
+    """n_iters fixed steps + final cost, feasibility and clamped flags.
+
+    Returns (q_out (B,T,7), cost (B,), feasible (B,) bool, clamped (B,) bool)."""
+    torch = _lib.require_cuda()
+    qd = _dev(q)
+    B, T, D = qd.shape
+    if D != 7 or T not in (32, 64):
+        raise ValueError("q must be (B, 32|64, 7)")
+    n_iters = w.n_iters if n_iters is None else n_iters
+    e = _dev(esdf)
+    rt = RobotTables.of(robot)
+    n, o = _grid_args(grid)
+    wts = w.as_f32()
+    if out is None:
+        out = (torch.empty_like(qd), torch.empty(B, dtype=torch.float32, device="cuda"),
+               torch.empty(B, dtype=torch.uint8, device="cuda"),
+               torch.empty(B, dtype=torch.uint8, device="cuda"))
+    qo, c, f, cl = out
+    st = _lib.lib().ps_bl_refine(_lib.ptr(qd), B, T, S, _lib.ptr(e), _esdf_stride(e, grid, -(-B // S)),
+                                 _lib.hptr(n), _lib.hptr(o), grid.h, _lib.hptr(rt.dh),
+                                 _lib.hptr(rt.base), _lib.hptr(rt.sph), _lib.hptr(rt.link),
+                                 len(rt.link), _lib.hptr(wts), int(n_iters), _lib.ptr(qo),
+                                 _lib.ptr(c), _lib.ptr(f), _lib.ptr(cl), _lib.stream_handle(stream))
+    _lib.check(st, "bl_refine")
+    return qo, c, f, cl
+
+
+def select(cost_, feasible, S: int, stream=None, out=None):
+    """Best seed per problem (P,) int32: lowest-cost feasible, else lowest cost, ties low."""
+    torch = _lib.require_cuda()
+    c = _dev(cost_)
+    f = _dev(feasible, torch.uint8)
+    P = c.shape[0] // S
+    best = out if out is not None else torch.empty(P, dtype=torch.int32, device="cuda")
+    st = _lib.lib().ps_select(_lib.ptr(c), _lib.ptr(f), P, S, _lib.ptr(best),
+                              _lib.stream_handle(stream))
+    _lib.check(st, "select")
+    return best

@@ -1,0 +1,488 @@
+// BASELINE-profile refinement path: ESDF build, fused cost/gradient/fixed-step
+// refinement with dense feasibility, and best-seed selection.
+//
+// Compiled with --fmad=false: all fused multiply-adds are explicit fmaf() in the
+// canonical order of oracle/c/bl_oracle.c, so results are bit-identical to it.
+//
+// Layout: one warp per trajectory, lane l owns waypoints l*WPL .. l*WPL+WPL-1
+// (T = 32*WPL).  Robot, weights and grid geometry travel in the kernel parameter
+// block (__grid_constant__, constant bank broadcast); the trajectory state stays in
+// registers for all iterations; the per-problem ESDF (128^3 fp32 = 8 MiB) is read
+// through the read-only path with 8 scalar gathers per sphere lookup.
+#include "common.cuh"
+
+namespace ps {
+
+constexpr int NJ = 7;
+constexpr int MAX_SPH = 64;
+
+struct BLParams {
+    float dh[NJ][4];          // a, d, cos alpha, sin alpha
+    float base[3];
+    float sph[MAX_SPH][4];    // link-frame offset xyz, radius
+    int link_start[NJ + 1];   // spheres of link k: [link_start[k], link_start[k+1])
+    float w_coll, w_vel, w_acc, w_jerk, margin, eta;
+    int nx, ny, nz;
+    float ox, oy, oz, inv_h;
+    int B, T, S, n_iters;
+    long long esdf_stride;
+    const float* q_in;
+    const float* esdf;
+    float* q_out;
+    float* cost;
+    float* grad;
+    uint8_t* feasible;
+    uint8_t* clamped;
+};
+
+// World term of one configuration (canonical order, see bl_oracle.c:config_world).
+template <bool WANT_GRAD>
+__device__ __forceinline__ void config_world(const BLParams& P, const Grid& g, const float (&q)[NJ],
+                                             float& wc, float (&gq)[NJ], float& mc, bool& cl_any) {
+    f3 X{1.f, 0.f, 0.f}, Y{0.f, 1.f, 0.f}, Z{0.f, 0.f, 1.f};
+    f3 o{P.base[0], P.base[1], P.base[2]};
+    f3 tz[NJ], tm[NJ];
+    wc = 0.f;
+    mc = __int_as_float(0x7f800000);
+    cl_any = false;
+    const float m2w = -2.0f * P.w_coll;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) gq[j] = 0.f;
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) {
+        tz[k] = Z;
+        tm[k] = c_cross(o, Z);
+        float sn, cs;
+        c_sincos(q[k], sn, cs);
+        const float a = P.dh[k][0], dd = P.dh[k][1], ca = P.dh[k][2], sa = P.dh[k][3];
+        const float ac = a * cs, as = a * sn;
+        o.x = fmaf(ac, X.x, fmaf(as, Y.x, fmaf(dd, Z.x, o.x)));
+        o.y = fmaf(ac, X.y, fmaf(as, Y.y, fmaf(dd, Z.y, o.y)));
+        o.z = fmaf(ac, X.z, fmaf(as, Y.z, fmaf(dd, Z.z, o.z)));
+        f3 X1{fmaf(cs, X.x, sn * Y.x), fmaf(cs, X.y, sn * Y.y), fmaf(cs, X.z, sn * Y.z)};
+        f3 Y1{fmaf(cs, Y.x, -(sn * X.x)), fmaf(cs, Y.y, -(sn * X.y)), fmaf(cs, Y.z, -(sn * X.z))};
+        f3 Y2{fmaf(ca, Y1.x, sa * Z.x), fmaf(ca, Y1.y, sa * Z.y), fmaf(ca, Y1.z, sa * Z.z)};
+        f3 Z2{fmaf(ca, Z.x, -(sa * Y1.x)), fmaf(ca, Z.y, -(sa * Y1.y)), fmaf(ca, Z.z, -(sa * Y1.z))};
+        X = X1;
+        Y = Y2;
+        Z = Z2;
+        f3 S1{0.f, 0.f, 0.f}, S2{0.f, 0.f, 0.f};
+        const int s_end = P.link_start[k + 1];
+        for (int s = P.link_start[k]; s < s_end; ++s) {
+            const float lx = P.sph[s][0], ly = P.sph[s][1], lz = P.sph[s][2], r = P.sph[s][3];
+            f3 p{fmaf(X.x, lx, fmaf(Y.x, ly, fmaf(Z.x, lz, o.x))),
+                 fmaf(X.y, lx, fmaf(Y.y, ly, fmaf(Z.y, lz, o.y))),
+                 fmaf(X.z, lx, fmaf(Y.z, ly, fmaf(Z.z, lz, o.z)))};
+            f3 gr;
+            bool cl;
+            const float dv = c_trilinear(g, p, gr, cl);
+            cl_any |= cl;
+            mc = fminf(mc, dv - r);
+            const float hinge = (r + P.margin) - dv;
+            if (hinge > 0.f) {
+                wc = fmaf(P.w_coll * hinge, hinge, wc);
+                if (WANT_GRAD) {
+                    const float coef = m2w * hinge;
+                    f3 gp{coef * gr.x, coef * gr.y, coef * gr.z};
+                    f3 cr = c_cross(p, gp);
+                    S1.x = S1.x + cr.x; S1.y = S1.y + cr.y; S1.z = S1.z + cr.z;
+                    S2.x = S2.x + gp.x; S2.y = S2.y + gp.y; S2.z = S2.z + gp.z;
+                }
+            }
+        }
+        if (WANT_GRAD) {
+#pragma unroll
+            for (int j = 0; j <= k; ++j) {
+                float t = tz[j].x * S1.x;
+                t = fmaf(tz[j].y, S1.y, t);
+                t = fmaf(tz[j].z, S1.z, t);
+                t = fmaf(tm[j].x, S2.x, t);
+                t = fmaf(tm[j].y, S2.y, t);
+                t = fmaf(tm[j].z, S2.z, t);
+                gq[j] = gq[j] + t;
+            }
+        }
+    }
+}
+
+// 3-term stencil of D (numpy.gradient, planseed/trajopt.py:64-73) or D^T across the
+// warp's waypoints.  Missing neighbours are substituted by y_t (as the oracle does).
+template <int WPL, bool TRANSPOSE>
+__device__ __forceinline__ void stencil(const float (&y)[WPL], float (&out)[WPL], int lane, int T) {
+    const float up = __shfl_up_sync(PS_FULL, y[WPL - 1], 1);
+    const float dn = __shfl_down_sync(PS_FULL, y[0], 1);
+#pragma unroll
+    for (int w = 0; w < WPL; ++w) {
+        const int t = lane * WPL + w;
+        float ym = (w > 0) ? y[w > 0 ? w - 1 : 0] : (t == 0 ? y[w] : up);
+        float yp = (w < WPL - 1) ? y[w < WPL - 1 ? w + 1 : w] : (t == T - 1 ? y[w] : dn);
+        float cl, cs, cr;
+        cs = (t == 0) ? -1.f : (t == T - 1 ? 1.f : 0.f);
+        if (!TRANSPOSE) {
+            cl = (t == 0) ? 0.f : (t == T - 1 ? -1.f : -0.5f);
+            cr = (t == T - 1) ? 0.f : (t == 0 ? 1.f : 0.5f);
+        } else {
+            cl = (t == 0) ? 0.f : (t - 1 == 0 ? 1.f : 0.5f);
+            cr = (t == T - 1) ? 0.f : (t + 1 == T - 1 ? -1.f : -0.5f);
+        }
+        float r = cs * y[w];
+        r = fmaf(cl, ym, r);
+        r = fmaf(cr, yp, r);
+        out[w] = r;
+    }
+}
+
+// Smoothness cost per waypoint and (optionally) gradient, see bl_oracle.c:smooth_terms.
+template <int WPL, bool WANT_GRAD>
+__device__ __forceinline__ void smooth_terms(const BLParams& P, const float (&q)[WPL][NJ], int lane,
+                                             float (&sm)[WPL], float (&gs)[WPL][NJ]) {
+#pragma unroll
+    for (int w = 0; w < WPL; ++w) sm[w] = 0.f;
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) {
+        float y[WPL], v[WPL], a[WPL], jk[WPL];
+#pragma unroll
+        for (int w = 0; w < WPL; ++w) y[w] = q[w][k];
+        stencil<WPL, false>(y, v, lane, P.T);
+        stencil<WPL, false>(v, a, lane, P.T);
+        stencil<WPL, false>(a, jk, lane, P.T);
+#pragma unroll
+        for (int w = 0; w < WPL; ++w) {
+            float s = sm[w];
+            s = fmaf(P.w_vel, v[w] * v[w], s);
+            s = fmaf(P.w_acc, a[w] * a[w], s);
+            s = fmaf(P.w_jerk, jk[w] * jk[w], s);
+            sm[w] = s;
+        }
+        if (WANT_GRAD) {
+            float z[WPL], zz[WPL], tmp[WPL];
+#pragma unroll
+            for (int w = 0; w < WPL; ++w) z[w] = P.w_jerk * jk[w];
+            stencil<WPL, true>(z, tmp, lane, P.T);
+#pragma unroll
+            for (int w = 0; w < WPL; ++w) zz[w] = fmaf(P.w_acc, a[w], tmp[w]);
+            stencil<WPL, true>(zz, tmp, lane, P.T);
+#pragma unroll
+            for (int w = 0; w < WPL; ++w) z[w] = fmaf(P.w_vel, v[w], tmp[w]);
+            stencil<WPL, true>(z, tmp, lane, P.T);
+#pragma unroll
+            for (int w = 0; w < WPL; ++w) gs[w][k] = tmp[w];
+        }
+    }
+}
+
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v = fminf(v, __shfl_xor_sync(PS_FULL, v, off));
+    return v;
+}
+
+// MODE 0: refine (n_iters steps + final cost/flags).  MODE 1: cost + gradient only.
+template <int WPL, int MODE>
+__global__ void __launch_bounds__(128) bl_refine_kernel(const __grid_constant__ BLParams P) {
+    const int lane = threadIdx.x & 31;
+    const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (b >= P.B) return;  // whole warp exits together
+    Grid g;
+    g.v = P.esdf + (size_t)(b / P.S) * (size_t)P.esdf_stride;
+    g.nx = P.nx; g.ny = P.ny; g.nz = P.nz;
+    g.ox = P.ox; g.oy = P.oy; g.oz = P.oz; g.inv_h = P.inv_h;
+
+    float q[WPL][NJ];
+    const float* qb = P.q_in + (size_t)b * P.T * NJ;
+#pragma unroll
+    for (int w = 0; w < WPL; ++w)
+#pragma unroll
+        for (int k = 0; k < NJ; ++k) q[w][k] = qb[(lane * WPL + w) * NJ + k];
+
+    float sm[WPL], gs[WPL][NJ];
+    if constexpr (MODE == 1) {
+        float ct[WPL];
+        bool cl_lane = false;
+        smooth_terms<WPL, true>(P, q, lane, sm, gs);
+#pragma unroll
+        for (int w = 0; w < WPL; ++w) {
+            float wc, mc, gq[NJ];
+            bool cl;
+            config_world<true>(P, g, q[w], wc, gq, mc, cl);
+            cl_lane |= cl;
+            ct[w] = wc + sm[w];
+            const int t = lane * WPL + w;
+            float* gout = P.grad + ((size_t)b * P.T + t) * NJ;
+#pragma unroll
+            for (int k = 0; k < NJ; ++k) gout[k] = (t == 0) ? 0.f : fmaf(2.0f, gs[w][k], gq[k]);
+        }
+        float c = ct[0];
+#pragma unroll
+        for (int w = 1; w < WPL; ++w) c = c + ct[w];
+        c = warp_sum_butterfly(c);
+        const bool cl_any = __any_sync(PS_FULL, cl_lane);
+        if (lane == 0) {
+            P.cost[b] = c;
+            P.clamped[b] = cl_any ? 1 : 0;
+        }
+        return;
+    }
+
+    for (int it = 0; it < P.n_iters; ++it) {
+        float gw[WPL][NJ];
+#pragma unroll
+        for (int w = 0; w < WPL; ++w) {
+            float wc, mc;
+            bool cl;
+            config_world<true>(P, g, q[w], wc, gw[w], mc, cl);
+        }
+        smooth_terms<WPL, true>(P, q, lane, sm, gs);
+#pragma unroll
+        for (int w = 0; w < WPL; ++w) {
+            const int t = lane * WPL + w;
+            if (t != 0) {
+#pragma unroll
+                for (int k = 0; k < NJ; ++k) q[w][k] = fmaf(-P.eta, fmaf(2.0f, gs[w][k], gw[w][k]), q[w][k]);
+            }
+        }
+    }
+
+    // final cost, clearance and clamped flag at the waypoints
+    smooth_terms<WPL, false>(P, q, lane, sm, gs);
+    float ct[WPL];
+    float mc_lane = __int_as_float(0x7f800000);
+    bool cl_lane = false;
+#pragma unroll
+    for (int w = 0; w < WPL; ++w) {
+        float wc, mc, gq[NJ];
+        bool cl;
+        config_world<false>(P, g, q[w], wc, gq, mc, cl);
+        ct[w] = wc + sm[w];
+        mc_lane = fminf(mc_lane, mc);
+        cl_lane |= cl;
+    }
+    // dense check: 4 interpolants per segment (planseed/pipeline.py:139-157)
+    float qn[NJ];
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) qn[k] = __shfl_down_sync(PS_FULL, q[0][k], 1);
+#pragma unroll
+    for (int w = 0; w < WPL; ++w) {
+        const int t = lane * WPL + w;
+        if (t + 1 < P.T) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float f = (float)(i + 1) / 5.0f;
+                float qi[NJ], wc, mc, gq[NJ];
+                bool cl;
+#pragma unroll
+                for (int k = 0; k < NJ; ++k) {
+                    const float q1 = (w + 1 < WPL) ? q[w + 1 < WPL ? w + 1 : w][k] : qn[k];
+                    qi[k] = fmaf(f, q1 - q[w][k], q[w][k]);
+                }
+                config_world<false>(P, g, qi, wc, gq, mc, cl);
+                mc_lane = fminf(mc_lane, mc);
+                cl_lane |= cl;
+            }
+        }
+    }
+    float c = ct[0];
+#pragma unroll
+    for (int w = 1; w < WPL; ++w) c = c + ct[w];
+    c = warp_sum_butterfly(c);
+    const float mc_all = warp_min(mc_lane);
+    const bool cl_any = __any_sync(PS_FULL, cl_lane);
+    float* qo = P.q_out + (size_t)b * P.T * NJ;
+#pragma unroll
+    for (int w = 0; w < WPL; ++w)
+#pragma unroll
+        for (int k = 0; k < NJ; ++k) qo[(lane * WPL + w) * NJ + k] = q[w][k];
+    if (lane == 0) {
+        P.cost[b] = c;
+        P.feasible[b] = (mc_all > 0.f) ? 1 : 0;
+        P.clamped[b] = cl_any ? 1 : 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ESDF build: 4 consecutive z nodes per thread, float4 store (nz % 4 == 0).
+// ---------------------------------------------------------------------------
+constexpr int MAX_BOXES = 64;
+
+template <int VEC>
+__global__ void __launch_bounds__(256) esdf_boxes_kernel(const float* __restrict__ boxes, int n_boxes,
+                                                         int nx, int ny, int nz, float ox, float oy,
+                                                         float oz, float h, float cap,
+                                                         float* __restrict__ out) {
+    __shared__ float bc[MAX_BOXES][3], bh[MAX_BOXES][3];
+    const int p = blockIdx.y;
+    const float* bx = boxes + (size_t)p * n_boxes * 6;
+    for (int i = threadIdx.x; i < n_boxes * 3; i += blockDim.x) {
+        const int b = i / 3, a = i % 3;
+        const float lo = bx[b * 6 + a], hi = bx[b * 6 + 3 + a];
+        bc[b][a] = 0.5f * (lo + hi);
+        bh[b][a] = 0.5f * (hi - lo);
+    }
+    __syncthreads();
+    const long long n_nodes = (long long)nx * ny * nz;
+    const long long first = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * VEC;
+    if (first >= n_nodes) return;
+    const int k0 = (int)(first % nz);
+    const long long ij = first / nz;
+    const int j = (int)(ij % ny), i = (int)(ij / ny);
+    const float px = fmaf((float)i, h, ox), py = fmaf((float)j, h, oy);
+    float res[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+        const float pz = fmaf((float)(k0 + v), h, oz);
+        float best = cap;
+        for (int b = 0; b < n_boxes; ++b) {
+            const float qx = fabsf(px - bc[b][0]) - bh[b][0];
+            const float qy = fabsf(py - bc[b][1]) - bh[b][1];
+            const float qz = fabsf(pz - bc[b][2]) - bh[b][2];
+            const float ax = fmaxf(qx, 0.f), ay = fmaxf(qy, 0.f), az = fmaxf(qz, 0.f);
+            const float outside = sqrtf(fmaf(ax, ax, fmaf(ay, ay, az * az)));
+            const float inside = fminf(fmaxf(qx, fmaxf(qy, qz)), 0.f);
+            best = fminf(best, outside + inside);
+        }
+        res[v] = best;
+    }
+    float* o = out + (size_t)p * (size_t)n_nodes + first;
+    if (VEC == 4) {
+        *reinterpret_cast<float4*>(o) = make_float4(res[0], res[1], res[2], res[VEC > 3 ? 3 : 0]);
+    } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) o[v] = res[v];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// select_best: one warp per problem; lexicographic (infeasible, cost, index) min.
+// ---------------------------------------------------------------------------
+__global__ void select_kernel(const float* __restrict__ cost, const uint8_t* __restrict__ feas, int P,
+                              int S, int32_t* __restrict__ best) {
+    const int lane = threadIdx.x & 31;
+    const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (p >= P) return;
+    int bi = 0x7fffffff, bf = 2;
+    float bcst = 0.f;
+    for (int s = lane; s < S; s += 32) {
+        const int f = feas[(size_t)p * S + s] ? 0 : 1;
+        const float c = cost[(size_t)p * S + s];
+        if (f < bf || (f == bf && (c < bcst || (c == bcst && s < bi)))) {
+            bf = f; bcst = c; bi = s;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const int of = __shfl_xor_sync(PS_FULL, bf, off);
+        const float oc = __shfl_xor_sync(PS_FULL, bcst, off);
+        const int oi = __shfl_xor_sync(PS_FULL, bi, off);
+        if (of < bf || (of == bf && (oc < bcst || (oc == bcst && oi < bi)))) {
+            bf = of; bcst = oc; bi = oi;
+        }
+    }
+    if (lane == 0) best[p] = bi;
+}
+
+static int fill_params(BLParams& P, int B, int T, int S, const float* esdf, long long esdf_stride,
+                       const int* n_h, const float* origin_h, float h, const float* dh_h,
+                       const float* base_h, const float* sph_h, const int* sph_link_h, int n_sph,
+                       const float* w_h) {
+    if (B < 0 || S <= 0 || (T != 32 && T != 64) || n_sph < 0 || n_sph > MAX_SPH) return PS_ERR_SHAPE;
+    if (n_h[0] < 2 || n_h[1] < 2 || n_h[2] < 2) return PS_ERR_SHAPE;
+    for (int k = 0; k < NJ; ++k)
+        for (int i = 0; i < 4; ++i) P.dh[k][i] = dh_h[4 * k + i];
+    for (int i = 0; i < 3; ++i) P.base[i] = base_h[i];
+    for (int s = 0; s < n_sph; ++s)
+        for (int i = 0; i < 4; ++i) P.sph[s][i] = sph_h[4 * s + i];
+    // link ranges (table must be sorted by link)
+    int s = 0;
+    for (int k = 0; k < NJ; ++k) {
+        P.link_start[k] = s;
+        while (s < n_sph && sph_link_h[s] == k) ++s;
+    }
+    P.link_start[NJ] = s;
+    if (s != n_sph) return PS_ERR_SHAPE;
+    P.w_coll = w_h[0]; P.w_vel = w_h[1]; P.w_acc = w_h[2]; P.w_jerk = w_h[3];
+    P.margin = w_h[4]; P.eta = w_h[5];
+    P.nx = n_h[0]; P.ny = n_h[1]; P.nz = n_h[2];
+    P.ox = origin_h[0]; P.oy = origin_h[1]; P.oz = origin_h[2];
+    P.inv_h = 1.0f / h;
+    P.B = B; P.T = T; P.S = S;
+    P.esdf = esdf;
+    P.esdf_stride = esdf_stride;
+    return PS_OK;
+}
+
+template <int MODE>
+static int launch_bl(const BLParams& P, cudaStream_t st) {
+    if (P.B == 0) return PS_OK;
+    const int threads = 128;
+    const long long blocks = ((long long)P.B * 32 + threads - 1) / threads;
+    if (P.T == 32)
+        bl_refine_kernel<1, MODE><<<(unsigned)blocks, threads, 0, st>>>(P);
+    else
+        bl_refine_kernel<2, MODE><<<(unsigned)blocks, threads, 0, st>>>(P);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" int ps_bl_cost(const float* q, int B, int T, int S, const float* esdf, long long esdf_stride,
+                          const int* n_h, const float* origin_h, float h, const float* dh_h,
+                          const float* base_h, const float* sph_h, const int* sph_link_h, int n_sph,
+                          const float* weights_h, float* cost, float* grad, uint8_t* clamped,
+                          void* stream) {
+    BLParams P{};
+    int st = fill_params(P, B, T, S, esdf, esdf_stride, n_h, origin_h, h, dh_h, base_h, sph_h, sph_link_h,
+                         n_sph, weights_h);
+    if (st) return st;
+    P.q_in = q; P.cost = cost; P.grad = grad; P.clamped = clamped; P.n_iters = 0;
+    return launch_bl<1>(P, (cudaStream_t)stream);
+}
+
+extern "C" int ps_bl_refine(const float* q_in, int B, int T, int S, const float* esdf,
+                            long long esdf_stride, const int* n_h, const float* origin_h, float h,
+                            const float* dh_h, const float* base_h, const float* sph_h,
+                            const int* sph_link_h, int n_sph, const float* weights_h, int n_iters,
+                            float* q_out, float* cost, uint8_t* feasible, uint8_t* clamped,
+                            void* stream) {
+    BLParams P{};
+    int st = fill_params(P, B, T, S, esdf, esdf_stride, n_h, origin_h, h, dh_h, base_h, sph_h, sph_link_h,
+                         n_sph, weights_h);
+    if (st) return st;
+    if (n_iters < 0) return PS_ERR_SHAPE;
+    P.q_in = q_in; P.q_out = q_out; P.cost = cost; P.feasible = feasible; P.clamped = clamped;
+    P.n_iters = n_iters;
+    return launch_bl<0>(P, (cudaStream_t)stream);
+}
+
+extern "C" int ps_esdf_build_boxes(const float* boxes, int P, int n_boxes, const int* n_h,
+                                   const float* origin_h, float h, float cap, float* out, void* stream) {
+    if (P < 0 || n_boxes < 0 || n_boxes > MAX_BOXES) return PS_ERR_SHAPE;
+    if (P == 0) return PS_OK;
+    const long long n_nodes = (long long)n_h[0] * n_h[1] * n_h[2];
+    const int threads = 256;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_h[2] % 4 == 0) {
+        const long long blocks = (n_nodes / 4 + threads - 1) / threads;
+        esdf_boxes_kernel<4><<<dim3((unsigned)blocks, P), threads, 0, st>>>(
+            boxes, n_boxes, n_h[0], n_h[1], n_h[2], origin_h[0], origin_h[1], origin_h[2], h, cap, out);
+    } else {
+        const long long blocks = (n_nodes + threads - 1) / threads;
+        esdf_boxes_kernel<1><<<dim3((unsigned)blocks, P), threads, 0, st>>>(
+            boxes, n_boxes, n_h[0], n_h[1], n_h[2], origin_h[0], origin_h[1], origin_h[2], h, cap, out);
+    }
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+extern "C" int ps_select(const float* cost, const uint8_t* feasible, int P, int S, int32_t* best,
+                         void* stream) {
+    if (P < 0 || S <= 0) return PS_ERR_SHAPE;
+    if (P == 0) return PS_OK;
+    const int threads = 128;
+    const int blocks = (P * 32 + threads - 1) / threads;
+    select_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(cost, feasible, P, S, best);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}

@@ -1,0 +1,119 @@
+"""Seeded synthetic inputs for the BASELINE configs.
+
+The paper evaluates on the MpiNet scenes, which are absent; BASELINE.json's synthetic
+scenes stand in for them.  Every problem p is drawn from its own generator
+`default_rng([seed, p, stream])`, so a shard of problems [p0, p1) is identical no
+matter how many ranks split the batch (the world-size invariance the reference's
+data generator guarantees for worker counts, planseed/data.py:391-394).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .spec import (BOX_SIDE, DOF, GOAL_EXTENT, JOINT_LIMIT, N_BOXES, GridSpec)
+
+STREAM_PROBLEM = 11
+STREAM_BOXES = 12
+STREAM_IMAGE = 13
+STREAM_REFINE = 14
+
+
+def _rng(seed: int, p: int, stream: int) -> np.random.Generator:
+    return np.random.default_rng([int(seed), int(p), int(stream)])
+
+
+@dataclass
+class ProblemBatch:
+    """Problems [p0, p0+P) of a seeded batch, host arrays."""
+
+    p0: int
+    q_start: np.ndarray   # (P, 7) float32, radians
+    goal: np.ndarray      # (P, 7) float32: xyz (m) + unit quaternion (w, x, y, z)
+    boxes: np.ndarray     # (P, n_boxes, 6) float32: lo xyz, hi xyz
+    images: Optional[np.ndarray] = None   # (P, n_img, H, W) float32 depth, m
+
+    @property
+    def P(self) -> int:
+        return int(self.q_start.shape[0])
+
+
+def sample_q_start(rng) -> np.ndarray:
+    # U(-pi, pi)^7 clipped to the Franka-like limits (BASELINE config 0)
+    return np.clip(rng.uniform(-math.pi, math.pi, size=DOF), -JOINT_LIMIT, JOINT_LIMIT)
+
+
+def sample_goal(rng) -> np.ndarray:
+    xyz = rng.uniform(-GOAL_EXTENT, GOAL_EXTENT, size=3)
+    quat = rng.standard_normal(4)
+    quat /= np.linalg.norm(quat)
+    return np.concatenate([xyz, quat])
+
+
+def sample_boxes(rng, n_boxes: int = N_BOXES, grid: GridSpec = GridSpec()) -> np.ndarray:
+    side = rng.uniform(BOX_SIDE[0], BOX_SIDE[1], size=(n_boxes, 3))
+    lo = rng.uniform(0.0, 1.0, size=(n_boxes, 3)) * (grid.cube - side)
+    return np.concatenate([lo, lo + side], axis=1)
+
+
+def synth_depth_image(rng, h: int, w: int, n_rect: int) -> np.ndarray:
+    """Uniform background b ~ U(0.3, 2.0) m; n_rect axis-aligned pixel rectangles
+    with random corners at depths ~ U(0.3, 2.0); each pixel keeps the nearest depth."""
+    img = np.full((h, w), rng.uniform(0.3, 2.0))
+    for _ in range(n_rect):
+        ys = np.sort(rng.integers(0, h + 1, size=2))
+        xs = np.sort(rng.integers(0, w + 1, size=2))
+        depth = rng.uniform(0.3, 2.0)
+        sub = img[ys[0]:ys[1], xs[0]:xs[1]]
+        np.minimum(sub, depth, out=sub)
+    return img
+
+
+def make_problems(P: int, p0: int = 0, seed: int = 0, n_boxes: int = N_BOXES,
+                  image_shape=None, n_images: int = 1, n_rect: int = 5) -> ProblemBatch:
+    q = np.empty((P, DOF))
+    g = np.empty((P, 7))
+    boxes = np.empty((P, n_boxes, 6))
+    imgs = None
+    if image_shape is not None:
+        imgs = np.empty((P, n_images) + tuple(image_shape), dtype=np.float32)
+    for i in range(P):
+        p = p0 + i
+        r = _rng(seed, p, STREAM_PROBLEM)
+        q[i] = sample_q_start(r)
+        g[i] = sample_goal(r)
+        boxes[i] = sample_boxes(_rng(seed, p, STREAM_BOXES), n_boxes)
+        if imgs is not None:
+            ri = _rng(seed, p, STREAM_IMAGE)
+            for m in range(n_images):
+                imgs[i, m] = synth_depth_image(ri, image_shape[0], image_shape[1], n_rect)
+    return ProblemBatch(p0=p0, q_start=q.astype(np.float32), goal=g.astype(np.float32),
+                        boxes=boxes.astype(np.float32), images=imgs)
+
+
+def config0_problems(P: int = 1, p0: int = 0, seed: int = 0) -> ProblemBatch:
+    return make_problems(P, p0, seed, image_shape=(128, 128), n_images=1, n_rect=5)
+
+
+def config3_problems(P: int = 1024, p0: int = 0, seed: int = 0) -> ProblemBatch:
+    return make_problems(P, p0, seed, image_shape=(240, 320), n_images=2, n_rect=8)
+
+
+def refine_init(n_traj: int, t_len: int = 32, t0: int = 0, seed: int = 0,
+                noise: float = 0.2) -> np.ndarray:
+    """BASELINE config 2 seeds: straight line q_start -> q_goal (both uniform within the
+    limits) plus N(0, noise^2) on rows 1..T-1; row 0 is the start (pinned)."""
+    out = np.empty((n_traj, t_len, DOF))
+    alphas = np.linspace(0.0, 1.0, t_len)[:, None]
+    for i in range(n_traj):
+        r = _rng(seed, t0 + i, STREAM_REFINE)
+        qa = r.uniform(-JOINT_LIMIT, JOINT_LIMIT, size=DOF)
+        qb = r.uniform(-JOINT_LIMIT, JOINT_LIMIT, size=DOF)
+        tr = qa[None, :] + alphas * (qb - qa)[None, :]
+        tr[1:] += noise * r.standard_normal((t_len - 1, DOF))
+        out[i] = tr
+    return out.astype(np.float32)

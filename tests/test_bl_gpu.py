@@ -1,0 +1,150 @@
+"""GPU parity tests of the BASELINE-profile refinement path, through the C-ABI.
+
+The CUDA kernels follow the canonical fp32 operation order of oracle/c/bl_oracle.c,
+so the bar here is BIT-EXACT equality (trajectories, costs, gradients, flags,
+best-seed indices), not a tolerance.
+"""
+
+import numpy as np
+import pytest
+
+from paper_2410_16727_b200 import spec, synth
+
+pytestmark = pytest.mark.gpu
+
+RB = spec.make_bl_robot()
+COST = spec.BLCost()
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test without a CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def bl(torch_cuda):
+    from paper_2410_16727_b200 import bl as _bl
+    return _bl
+
+
+def _esdf(bl, oracle_lib, grid, P, seed, n_boxes=20):
+    rng = np.random.default_rng(seed)
+    boxes = np.stack([synth.sample_boxes(rng, n_boxes, grid) for _ in range(P)]).astype(np.float32)
+    dev = bl.esdf_build(boxes, grid)
+    return boxes, dev
+
+
+class TestEsdf:
+    def test_bitwise_vs_oracle_full_grid(self, bl, oracle_lib):
+        grid = spec.GridSpec()
+        boxes, dev = _esdf(bl, oracle_lib, grid, 1, 0)
+        ref = oracle_lib.esdf_build(boxes[0], grid)
+        assert np.array_equal(dev[0].cpu().numpy(), ref)
+
+    def test_bitwise_odd_grid_and_multi_problem(self, bl, oracle_lib):
+        grid = spec.GridSpec(n=(17, 9, 13), h=0.05, origin=(0.1, -0.2, 0.05), cube=0.85)
+        boxes, dev = _esdf(bl, oracle_lib, grid, 3, 1, n_boxes=5)
+        for p in range(3):
+            assert np.array_equal(dev[p].cpu().numpy(), oracle_lib.esdf_build(boxes[p], grid))
+
+    def test_no_boxes_is_cap(self, bl):
+        grid = spec.GridSpec(n=(8, 8, 8), h=0.1, cube=0.8)
+        dev = bl.esdf_build(np.zeros((2, 0, 6), np.float32), grid)
+        assert np.all(dev.cpu().numpy() == np.float32(grid.cap))
+
+
+class TestCost:
+    @pytest.mark.parametrize("T", [32, 64])
+    def test_bitwise_vs_oracle(self, bl, oracle_lib, T):
+        grid = spec.GridSpec()
+        P, S = 2, 16
+        _, dev = _esdf(bl, oracle_lib, grid, P, 2)
+        q = synth.refine_init(P * S, t_len=T, seed=3)
+        c, g, cl = bl.cost(q, dev, S, RB, grid, COST)
+        ps = oracle_lib.BLProblemSet(RB, grid, COST, dev.cpu().numpy(), grid.n_nodes)
+        rc, rg, rcl = oracle_lib.bl_cost(ps, q, S)
+        assert np.array_equal(c.cpu().numpy(), rc)
+        assert np.array_equal(g.cpu().numpy(), rg)
+        assert np.array_equal(cl.cpu().numpy(), rcl)
+
+
+class TestRefine:
+    def _run(self, bl, oracle_lib, grid, P, S, T, n_iters, seed, n_boxes=20, q=None):
+        _, dev = _esdf(bl, oracle_lib, grid, P, seed, n_boxes)
+        if q is None:
+            q = synth.refine_init(P * S, t_len=T, seed=seed + 1)
+        out = bl.refine(q, dev, S, RB, grid, COST, n_iters=n_iters)
+        ps = oracle_lib.BLProblemSet(RB, grid, COST, dev.cpu().numpy(), grid.n_nodes)
+        ref = oracle_lib.bl_refine(ps, q, S, n_iters)
+        return [o.cpu().numpy() for o in out], ref, q
+
+    @pytest.mark.parametrize("T", [32, 64])
+    def test_bitwise_vs_oracle(self, bl, oracle_lib, T):
+        got, ref, q = self._run(bl, oracle_lib, spec.GridSpec(), 4, 32, T, 10, 10)
+        assert np.array_equal(got[0], ref[0])
+        assert np.array_equal(got[1], ref[1])
+        assert np.array_equal(got[2].astype(bool), ref[2])
+        assert np.array_equal(got[3].astype(bool), ref[3])
+        assert np.array_equal(got[0][:, 0], q[:, 0])
+
+    def test_flags_mixed_and_select_exact(self, bl, oracle_lib):
+        # few small boxes -> a mix of feasible and colliding seeds
+        got, ref, _ = self._run(bl, oracle_lib, spec.GridSpec(), 8, 32, 32, 10, 20, n_boxes=3)
+        feas = ref[2]
+        assert 0 < feas.sum() < feas.size
+        best = bl.select(got[1], got[2], 32).cpu().numpy()
+        assert np.array_equal(best, oracle_lib.select(ref[1], ref[2], 32))
+
+    def test_config2_full_size_bitwise(self, bl, oracle_lib):
+        # BASELINE config 2: 2048 trajectories, one shared 128^3 ESDF, 10 iterations
+        grid = spec.GridSpec()
+        _, dev = _esdf(bl, oracle_lib, grid, 1, 30)
+        q = synth.refine_init(2048, seed=31)
+        got = [o.cpu().numpy() for o in bl.refine(q, dev[0], 2048, RB, grid, COST)]
+        ps = oracle_lib.BLProblemSet(RB, grid, COST, dev.cpu().numpy(), 0)
+        ref = oracle_lib.bl_refine(ps, q, 2048, 10)
+        assert np.array_equal(got[0], ref[0])
+        assert np.array_equal(got[1], ref[1])
+        assert np.array_equal(got[2].astype(bool), ref[2])
+
+    def test_deterministic_and_split_invariant(self, bl, oracle_lib):
+        grid = spec.GridSpec()
+        _, dev = _esdf(bl, oracle_lib, grid, 4, 40)
+        q = synth.refine_init(128, seed=41)
+        a = [o.cpu().numpy() for o in bl.refine(q, dev, 32, RB, grid, COST)]
+        b = [o.cpu().numpy() for o in bl.refine(q, dev, 32, RB, grid, COST)]
+        lo = [o.cpu().numpy() for o in bl.refine(q[:64], dev[:2], 32, RB, grid, COST)]
+        hi = [o.cpu().numpy() for o in bl.refine(q[64:], dev[2:], 32, RB, grid, COST)]
+        for i in range(4):
+            assert np.array_equal(a[i], b[i])
+            assert np.array_equal(a[i], np.concatenate([lo[i], hi[i]]))
+
+    def test_out_of_grid_flags(self, bl, oracle_lib):
+        grid = spec.GridSpec(n=(32, 32, 32), h=0.01, origin=(0.48, 0.48, 0.48), cube=0.32)
+        got, ref, _ = self._run(bl, oracle_lib, grid, 1, 32, 32, 3, 50, n_boxes=2)
+        assert ref[3].all()                       # a 0.32 m box cannot hold the arm
+        assert np.array_equal(got[3].astype(bool), ref[3])
+        assert np.array_equal(got[0], ref[0])
+
+    def test_empty_batch_and_bad_shapes(self, bl, torch_cuda):
+        grid = spec.GridSpec(n=(8, 8, 8), h=0.1, cube=0.8)
+        dev = bl.esdf_build(np.zeros((1, 1, 6), np.float32), grid)
+        q = np.zeros((0, 32, 7), np.float32)
+        out = bl.refine(q, dev, 4, RB, grid, COST)
+        assert out[0].shape == (0, 32, 7)
+        with pytest.raises(ValueError):
+            bl.refine(np.zeros((4, 48, 7), np.float32), dev, 4, RB, grid, COST)
+
+
+class TestSelect:
+    def test_matches_oracle_with_ties(self, bl, oracle_lib):
+        rng = np.random.default_rng(7)
+        for S in (1, 8, 32, 100):
+            P = 37
+            c = rng.integers(0, 4, size=P * S).astype(np.float32)
+            f = rng.random(P * S) < 0.15
+            got = bl.select(c, f.astype(np.uint8), S).cpu().numpy()
+            assert np.array_equal(got, oracle_lib.select(c, f, S))
