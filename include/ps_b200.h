@@ -63,6 +63,49 @@ int ps_bl_refine(const float* q_in, int B, int T, int S, const float* esdf,
 int ps_select(const float* cost, const uint8_t* feasible, int P, int S, int32_t* best,
               void* stream);
 
+/* ===================== BASELINE profile: seed sampler ======================= */
+/* Weights travel as the PSCK fp32 blob (spec.UNetArch.param_shapes order) on device;
+ * ps_unet_pack converts them once into the layout of `mode` (0 = fp32 SIMT,
+ * 1 = bf16 tcgen05).  Replaces planseed's DenoiserNet param dict
+ * (diffusion.py:139-200) + load_checkpoint (diffusion.py:657-687). */
+long long ps_unet_param_count(void);
+long long ps_unet_param_offset(const char* name_h);
+long long ps_unet_packed_bytes(int mode);
+int ps_unet_pack(const float* blob, int mode, void* packed, void* stream);
+
+/* Observation encoder: depth images (P*n_img, H, W) metres -> cond (P, 270) =
+ * [mean image embedding 256 ; normalised q_start 7 ; goal xyz/0.6 ; quaternion].
+ * enc_w: encoder params in table order.  BL analogue of encode_condition
+ * (diffusion.py:246-269). */
+long long ps_encode_workspace_bytes(int n_images, int H, int W, int n_layers);
+int ps_encode(const float* images, int P, int n_img, int H, int W, const float* enc_w, int n_layers,
+              const float* q_start, const float* goal, float lo, float hi, void* ws, float* cond,
+              void* stream);
+
+/* FiLM split: film_a[p] = mish(cond[p]) @ W_cond (per problem, once);
+ * per-step part computed inside ps_sample / ps_unet_forward. */
+int ps_film_problem(const void* packed, int mode, const float* cond, int P, float* film_a, void* stream);
+int ps_film_steps(const void* packed, int mode, const int* ks, int n, float* scratch, float* film_b,
+                  void* stream);
+
+/* One noise prediction eps(x, k) for B = P*S trajectories.  predict_noise
+ * (diffusion.py:288-300). */
+int ps_unet_forward(const void* packed, int mode, const float* x, int B, int T, int S, int k,
+                    const float* film_a, void* ws, float* eps, void* stream);
+
+/* All denoising steps for P problems x S seeds; returns physical trajectories with
+ * row 0 := q_start.  ddpm=1: stochastic posterior over K..1; ddpm=0: DDIM (eta 0)
+ * over steps_h, as _ddim_core (diffusion.py:535-556) / ddim_sample (:559-569).
+ * Noise: Philox4x32-10 keyed by (noise_key, global problem p0+p, seed, step). */
+long long ps_sample_workspace_bytes(int B, int T, int P, int n_steps, int mode);
+int ps_sample(const void* packed, int mode, const float* film_a, int P, int S, int T, int p0,
+              const int* steps_h, int n_steps, int ddpm, const float* coef_h, int K,
+              unsigned noise_key, const float* q_start, float lo, float hi, void* ws, float* traj,
+              void* stream);
+
+/* n standard normals of the sampler's noise stream (test hook). */
+int ps_noise_probe(float* out, int n, int step, int prob, int seed, unsigned key, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

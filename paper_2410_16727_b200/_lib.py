@@ -27,8 +27,24 @@ _SIGS = {
     "ps_bl_refine": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,
                      _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp],
     "ps_select": [_vp, _vp, _c_int, _c_int, _vp, _vp],
+    "ps_unet_param_count": [],
+    "ps_unet_param_offset": [ctypes.c_char_p],
+    "ps_unet_packed_bytes": [_c_int],
+    "ps_unet_pack": [_vp, _c_int, _vp, _vp],
+    "ps_encode_workspace_bytes": [_c_int, _c_int, _c_int, _c_int],
+    "ps_encode": [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp, _vp, _c_f, _c_f, _vp, _vp,
+                  _vp],
+    "ps_film_problem": [_vp, _c_int, _vp, _c_int, _vp, _vp],
+    "ps_film_steps": [_vp, _c_int, _vp, _c_int, _vp, _vp, _vp],
+    "ps_unet_forward": [_vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp],
+    "ps_sample_workspace_bytes": [_c_int, _c_int, _c_int, _c_int, _c_int],
+    "ps_sample": [_vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int,
+                  ctypes.c_uint, _vp, _c_f, _c_f, _vp, _vp, _vp],
+    "ps_noise_probe": [_vp, _c_int, _c_int, _c_int, _c_int, ctypes.c_uint, _vp],
 }
-_RESTYPE = {"ps_version": ctypes.c_char_p}
+_RESTYPE = {"ps_version": ctypes.c_char_p, "ps_unet_param_count": _c_ll,
+            "ps_unet_param_offset": _c_ll, "ps_unet_packed_bytes": _c_ll,
+            "ps_encode_workspace_bytes": _c_ll, "ps_sample_workspace_bytes": _c_ll}
 
 _lib = None
 

@@ -1,0 +1,907 @@
+// BASELINE-profile seed sampler: weight packing, observation encoder, FiLM tables,
+// fp32 SIMT U-Net (mode 0) and the step loop (DDPM / strided DDIM), with the Philox
+// counter-based noise stream.  The bf16 tcgen05 U-Net (mode 1) lives in conv_tc.cu and
+// shares the layout built here.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "sampler.cuh"
+
+namespace ps {
+
+// ---------------------------------------------------------------------------
+// layout
+// ---------------------------------------------------------------------------
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct PackMap {
+    std::vector<long long> w_src;  // per packed weight element: blob index or -1
+    std::vector<long long> s_src;  // per fp32 side element
+};
+
+namespace {
+
+struct Builder {
+    Layout& L;
+    PackMap* M;
+    const std::vector<ParamEntry>& tab;
+    int mode;
+
+    size_t P(const std::string& n) {
+        const ParamEntry* e = find_param(tab, n);
+        return e->off;
+    }
+    size_t side(size_t n, long long src_off) {  // append n consecutive blob values (or zeros)
+        size_t o = L.side_elems;
+        L.side_elems += n;
+        if (M)
+            for (size_t i = 0; i < n; ++i) M->s_src.push_back(src_off < 0 ? -1 : src_off + (long long)i);
+        return o;
+    }
+    size_t side_map(size_t n, const std::function<long long(size_t)>& f) {
+        size_t o = L.side_elems;
+        L.side_elems += n;
+        if (M)
+            for (size_t i = 0; i < n; ++i) M->s_src.push_back(f(i));
+        return o;
+    }
+    // conv weights: map(row k, col n) -> blob index or -1
+    void conv(PConv& c, int N, const std::vector<PSeg>& segs, const std::function<long long(int, int)>& map) {
+        c.N = N;
+        c.n_seg = (int)segs.size();
+        int k = 0;
+        for (int i = 0; i < c.n_seg; ++i) {
+            c.seg[i] = segs[i];
+            c.seg[i].k0 = k;
+            k += segs[i].nc;
+        }
+        c.K = k;
+        const int Kp = mode == 1 ? (int)align_up((size_t)k, 64) : k;
+        c.w_off = L.w_elems;
+        L.w_elems += (size_t)Kp * N;
+        if (!M) return;
+        if (mode == 0) {
+            for (int r = 0; r < Kp; ++r)
+                for (int n = 0; n < N; ++n) M->w_src.push_back(map(r, n));
+        } else {
+            for (int n = 0; n < N; ++n)
+                for (int r = 0; r < Kp; ++r) M->w_src.push_back(r < k ? map(r, n) : -1);
+        }
+    }
+};
+
+}  // namespace
+
+// Which segment a packed row belongs to.
+static int seg_of(const std::vector<PSeg>& s, int r, int& c) {
+    int k = 0;
+    for (int i = 0; i < (int)s.size(); ++i) {
+        if (r < k + s[i].nc) {
+            c = r - k;
+            return i;
+        }
+        k += s[i].nc;
+    }
+    return -1;
+}
+
+Layout make_layout(int mode, PackMap* M) {
+    Layout L;
+    L.mode = mode;
+    auto tab = unet_param_table();
+    L.n_params = tab.back().off + tab.back().numel();
+    Builder B{L, M, tab, mode};
+    static const char* names[U_NBLK] = {"d0r0", "d0r1", "d1r0", "d1r1", "d2r0", "d2r1",
+                                        "m0",   "m1",   "u0r0", "u0r1", "u1r0", "u1r1"};
+    static const int cin[U_NBLK] = {7, 64, 64, 128, 128, 256, 256, 256, 512, 128, 256, 64};
+    static const int cout[U_NBLK] = {64, 64, 128, 128, 256, 256, 256, 256, 128, 128, 64, 64};
+    static const int lvl[U_NBLK] = {0, 0, 1, 1, 2, 2, 2, 2, 2, 2, 1, 1};
+    int film_col = 0;
+    for (int b = 0; b < U_NBLK; ++b) {
+        PBlock& blk = L.blk[b];
+        blk.name = names[b];
+        blk.c_in = cin[b];
+        blk.c_out = cout[b];
+        blk.level = lvl[b];
+        const int co = cout[b], ci = cin[b];
+        const bool cat = (b == 8 || b == 10);
+        const int C1 = cat ? ci / 2 : ci, C2 = cat ? ci / 2 : 0;
+        const bool im2col = (mode == 1 && b == 0);
+        const size_t w0 = B.P(blk.name + "_c0_w"), w1 = B.P(blk.name + "_c1_w");
+        // c0
+        std::vector<PSeg> s0;
+        if (im2col) {
+            s0.push_back({0, 0, 0, 64, 0});
+            B.conv(blk.c0, co, s0, [&](int r, int n) -> long long {
+                if (r >= 5 * U_DOF) return -1;
+                int tap = r / U_DOF, c = r % U_DOF;
+                return (long long)(w0 + ((size_t)n * ci + c) * 5 + tap);
+            });
+        } else {
+            for (int tap = 0; tap < 5; ++tap) {
+                s0.push_back({0, tap - 2, 0, C1, 0});
+                if (C2) s0.push_back({1, tap - 2, 0, C2, 0});
+            }
+            B.conv(blk.c0, co, s0, [&](int r, int n) -> long long {
+                int c, i = seg_of(s0, r, c);
+                int tap = s0[i].dt + 2;
+                int cc = s0[i].src == 0 ? c : C1 + c;
+                return (long long)(w0 + ((size_t)n * ci + cc) * 5 + tap);
+            });
+        }
+        // c1
+        std::vector<PSeg> s1;
+        for (int tap = 0; tap < 5; ++tap) s1.push_back({0, tap - 2, 0, co, 0});
+        B.conv(blk.c1, co, s1, [&](int r, int n) -> long long {
+            int c, i = seg_of(s1, r, c);
+            return (long long)(w1 + ((size_t)n * co + c) * 5 + (s1[i].dt + 2));
+        });
+        // residual 1x1
+        if (ci != co) {
+            const size_t wr = B.P(blk.name + "_res_w");
+            std::vector<PSeg> sr;
+            if (im2col) {
+                sr.push_back({0, 0, 0, 64, 0});
+                B.conv(blk.res, co, sr, [&](int r, int n) -> long long {
+                    if (r < 2 * U_DOF || r >= 3 * U_DOF) return -1;
+                    return (long long)(wr + (size_t)n * ci + (r - 2 * U_DOF));
+                });
+            } else {
+                sr.push_back({0, 0, 0, C1, 0});
+                if (C2) sr.push_back({1, 0, 0, C2, 0});
+                B.conv(blk.res, co, sr, [&](int r, int n) -> long long {
+                    int c, i = seg_of(sr, r, c);
+                    int cc = sr[i].src == 0 ? c : C1 + c;
+                    return (long long)(wr + (size_t)n * ci + cc);
+                });
+            }
+        }
+        blk.c0.film_col = film_col;
+        film_col += 2 * co;
+    }
+    // downsampling conv k3 s2 p1 over the pair view [B, T/2, 2C]
+    for (int d = 0; d < 2; ++d) {
+        const int C = d == 0 ? 64 : 128;
+        const size_t w = B.P(d == 0 ? "down0_w" : "down1_w");
+        std::vector<PSeg> s = {{0, -1, C, C, 0}, {0, 0, 0, 2 * C, 0}};
+        B.conv(L.down[d], C, s, [&](int r, int n) -> long long {
+            int c, i = seg_of(s, r, c);
+            int tap = i == 0 ? 0 : (c < C ? 1 : 2);
+            int cc = i == 0 ? c : (c < C ? c : c - C);
+            return (long long)(w + ((size_t)n * C + cc) * 3 + tap);
+        });
+    }
+    // transposed conv k4 s2 p1 writing the pair view [B, T_in, 2C]
+    for (int u = 0; u < 2; ++u) {
+        const int C = u == 0 ? 128 : 64;
+        const size_t w = B.P(u == 0 ? "up0_w" : "up1_w");
+        std::vector<PSeg> s = {{0, -1, 0, C, 0}, {0, 0, 0, C, 0}, {0, 1, 0, C, 0}};
+        B.conv(L.up[u], 2 * C, s, [&](int r, int n) -> long long {
+            int c, i = seg_of(s, r, c);
+            const bool odd = n >= C;
+            const int co = odd ? n - C : n;
+            int tap;
+            if (i == 0) tap = odd ? -1 : 3;
+            else if (i == 1) tap = odd ? 2 : 1;
+            else tap = odd ? 0 : -1;
+            if (tap < 0) return -1;
+            return (long long)(w + ((size_t)c * C + co) * 4 + tap);
+        });
+    }
+    {
+        const size_t w = B.P("fin_c_w");
+        std::vector<PSeg> s;
+        for (int tap = 0; tap < 5; ++tap) s.push_back({0, tap - 2, 0, 64, 0});
+        B.conv(L.fin, 64, s, [&](int r, int n) -> long long {
+            int c, i = seg_of(s, r, c);
+            return (long long)(w + ((size_t)n * 64 + c) * 5 + (s[i].dt + 2));
+        });
+        const size_t wo = B.P("out_w");
+        std::vector<PSeg> so = {{0, 0, 0, 64, 0}};
+        B.conv(L.out, U_DOF, so, [&](int r, int n) -> long long { return (long long)(wo + (size_t)n * 64 + r); });
+    }
+    // ---- fp32 side table
+    L.w_bytes = align_up(L.w_elems * (mode == 1 ? 2 : 4), 256);
+    for (int b = 0; b < U_NBLK; ++b) {
+        PBlock& blk = L.blk[b];
+        blk.c0.b_off = B.side(blk.c_out, (long long)B.P(blk.name + "_c0_b"));
+        blk.c0.g_off = (long long)B.side(blk.c_out, (long long)B.P(blk.name + "_gn0_g"));
+        blk.c0.be_off = (long long)B.side(blk.c_out, (long long)B.P(blk.name + "_gn0_b"));
+        blk.c1.b_off = B.side(blk.c_out, (long long)B.P(blk.name + "_c1_b"));
+        blk.c1.g_off = (long long)B.side(blk.c_out, (long long)B.P(blk.name + "_gn1_g"));
+        blk.c1.be_off = (long long)B.side(blk.c_out, (long long)B.P(blk.name + "_gn1_b"));
+        if (blk.res.K) blk.res.b_off = B.side(blk.c_out, (long long)B.P(blk.name + "_res_b"));
+    }
+    for (int d = 0; d < 2; ++d)
+        L.down[d].b_off = B.side(L.down[d].N, (long long)B.P(d == 0 ? "down0_b" : "down1_b"));
+    for (int u = 0; u < 2; ++u) {
+        const int C = L.up[u].N / 2;
+        const size_t ub = B.P(u == 0 ? "up0_b" : "up1_b");
+        L.up[u].b_off = B.side_map(2 * C, [&](size_t i) { return (long long)(ub + (i % C)); });
+    }
+    L.fin.b_off = B.side(64, (long long)B.P("fin_c_b"));
+    L.fin.g_off = (long long)B.side(64, (long long)B.P("fin_gn_g"));
+    L.fin.be_off = (long long)B.side(64, (long long)B.P("fin_gn_b"));
+    L.out.b_off = B.side(U_DOF, (long long)B.P("out_b"));
+    L.outw_f32 = B.side(U_DOF * 64, (long long)B.P("out_w"));  // [n][c]
+    // time MLP
+    L.t1w = B.side(U_TEMB * U_THID, (long long)B.P("t_fc1_w"));
+    L.t1b = B.side(U_THID, (long long)B.P("t_fc1_b"));
+    L.t2w = B.side(U_THID * U_TEMB, (long long)B.P("t_fc2_w"));
+    L.t2b = B.side(U_TEMB, (long long)B.P("t_fc2_b"));
+    // FiLM split: rows 0..127 (time part) and 128..397 (condition part), all blocks' columns
+    std::vector<size_t> fw(U_NBLK), fb(U_NBLK);
+    for (int b = 0; b < U_NBLK; ++b) {
+        fw[b] = B.P(L.blk[b].name + "_film_w");
+        fb[b] = B.P(L.blk[b].name + "_film_b");
+    }
+    auto film_src = [&](int row, int col) -> long long {
+        for (int b = 0; b < U_NBLK; ++b) {
+            const int c0 = L.blk[b].c0.film_col, w = 2 * L.blk[b].c_out;
+            if (col >= c0 && col < c0 + w) {
+                if (row < 0) return (long long)(fb[b] + (col - c0));
+                return (long long)(fw[b] + (size_t)row * w + (col - c0));
+            }
+        }
+        return -1;
+    };
+    L.film_wt = B.side_map((size_t)U_TEMB * U_FILM_COLS,
+                           [&](size_t i) { return film_src((int)(i / U_FILM_COLS), (int)(i % U_FILM_COLS)); });
+    L.film_wc = B.side_map((size_t)U_COND * U_FILM_COLS, [&](size_t i) {
+        return film_src(U_TEMB + (int)(i / U_FILM_COLS), (int)(i % U_FILM_COLS));
+    });
+    L.film_b = B.side_map(U_FILM_COLS, [&](size_t i) { return film_src(-1, (int)i); });
+    L.total_bytes = L.w_bytes + align_up(L.side_elems * 4, 256);
+    return L;
+}
+
+// ---------------------------------------------------------------------------
+// small kernels
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ float mishf(float x) {
+    const float sp = x > 20.f ? x : log1pf(expf(x));
+    return x * tanhf(sp);
+}
+
+template <typename TW>
+__global__ void gather_kernel(const float* __restrict__ blob, const long long* __restrict__ src, size_t n,
+                              TW* __restrict__ dst) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long s = src[i];
+    const float v = s >= 0 ? blob[s] : 0.f;
+    if constexpr (sizeof(TW) == 2)
+        dst[i] = __float2bfloat16_rn(v);
+    else
+        dst[i] = v;
+}
+
+// y[r, n] = act_out(bias[n] + sum_k act_in(x[r, k]) W[k, n])   (act: 0 none, 1 mish)
+__global__ void dense_kernel(const float* __restrict__ x, int ldx, const float* __restrict__ W, int ldw,
+                             const float* __restrict__ bias, int rows, int K, int N, int act_in, int act_out,
+                             float* __restrict__ y, int ldy) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y;
+    if (n >= N) return;
+    const float* xr = x + (size_t)r * ldx;
+    float acc = 0.f;
+    for (int k = 0; k < K; ++k) {
+        float v = xr[k];
+        if (act_in) v = mishf(v);
+        acc = fmaf(v, W[(size_t)k * ldw + n], acc);
+    }
+    if (bias) acc += bias[n];
+    if (act_out) acc = mishf(acc);
+    y[(size_t)r * ldy + n] = acc;
+}
+
+// sinusoid embedding of 1-based step indices (planseed/diffusion.py:228-234)
+__global__ void sinusoid_kernel(const int* __restrict__ ks, int n, float* __restrict__ out) {
+    const int i = blockIdx.x, j = threadIdx.x;  // j < 64
+    if (i >= n) return;
+    const double freq = exp(-log(10000.0) * (double)j / 63.0);
+    const double ang = (double)ks[i] * freq;
+    out[(size_t)i * U_TEMB + j] = (float)sin(ang);
+    out[(size_t)i * U_TEMB + 64 + j] = (float)cos(ang);
+}
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 + Box-Muller (spec.py "Counter-based noise")
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint4 philox(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+
+__device__ __forceinline__ float normal_at(uint32_t step, uint32_t prob, uint32_t seed, uint32_t e,
+                                           uint32_t key) {
+    const uint4 r = philox(make_uint4(e >> 2, step, prob, seed), key, 0x5EED5EEDu);
+    const uint32_t comp = e & 3u;
+    const uint32_t a = comp < 2 ? r.x : r.z, b = comp < 2 ? r.y : r.w;
+    const float u1 = ((float)(a >> 8) + 1.0f) * (1.0f / 16777216.0f);
+    const float u2 = (float)(b >> 8) * (1.0f / 16777216.0f);
+    const float rad = sqrtf(-2.0f * logf(u1));
+    const float ang = 6.28318530717958648f * u2;
+    return (comp & 1u) ? rad * sinf(ang) : rad * cosf(ang);
+}
+
+__global__ void noise_init_kernel(float* __restrict__ x, int B, int T, int S, int p0, uint32_t key) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t n = (size_t)B * T * U_DOF;
+    if (i >= n) return;
+    const int b = (int)(i / ((size_t)T * U_DOF));
+    const uint32_t e = (uint32_t)(i % ((size_t)T * U_DOF));
+    x[i] = normal_at(0u, (uint32_t)(p0 + b / S), (uint32_t)(b % S), e, key);
+}
+
+__global__ void noise_probe_kernel(float* __restrict__ out, int n, uint32_t step, uint32_t prob,
+                                   uint32_t seed, uint32_t key) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = normal_at(step, prob, seed, (uint32_t)i, key);
+}
+
+// x0 = clip((x - sq1m eps) rsq); DDPM: x = c0 x0 + c1 x + sig z  |  DDIM: x = sqn x0 + sq1mn eps
+// On the last step writes the physical trajectory with row 0 := q_start.
+__global__ void step_update_kernel(float* __restrict__ x, const float* __restrict__ eps, StepCoef sc, int B,
+                                   int T, int S, int p0, uint32_t key, const float* __restrict__ q_start,
+                                   float* __restrict__ traj, float lo, float hi) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t n = (size_t)B * T * U_DOF;
+    if (i >= n) return;
+    const float xv = x[i], ev = eps[i];
+    float x0 = (xv - sc.sq1m * ev) * sc.rsq;
+    x0 = fminf(fmaxf(x0, -0.1f), 1.1f);
+    const int b = (int)(i / ((size_t)T * U_DOF));
+    const uint32_t e = (uint32_t)(i % ((size_t)T * U_DOF));
+    if (sc.last) {
+        const int t = (int)(e / U_DOF), d = (int)(e % U_DOF);
+        traj[i] = (t == 0) ? q_start[(size_t)(b / S) * U_DOF + d] : lo + x0 * (hi - lo);
+        return;
+    }
+    if (sc.ddpm) {
+        const float z = normal_at((uint32_t)sc.k, (uint32_t)(p0 + b / S), (uint32_t)(b % S), e, key);
+        x[i] = sc.c0 * x0 + sc.c1 * xv + sc.sig * z;
+    } else {
+        x[i] = sc.sqn * x0 + sc.sq1mn * ev;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// fp32 SIMT implicit-GEMM convolution over a segment view (mode 0)
+// ---------------------------------------------------------------------------
+
+struct ConvArgs {
+    const float* src[2];
+    int ld[2];
+    int Tv, rows, N, K, n_seg;
+    PSeg seg[U_MAXSEG];
+    const float* W;      // [K][N]
+    const float* bias;   // [N]
+    float* out;          // [rows][N]
+};
+
+constexpr int CB_M = 64, CB_N = 64, CB_K = 16;
+
+__global__ void __launch_bounds__(256) conv_gemm_f32_kernel(const __grid_constant__ ConvArgs a) {
+    __shared__ float As[CB_K][CB_M + 4];
+    __shared__ float Bs[CB_K][CB_N];
+    const int tid = threadIdx.x;
+    const int m0 = blockIdx.x * CB_M, n0 = blockIdx.y * CB_N;
+    const int tr = tid / 16, tc = tid % 16;  // 16x16 threads, 4x4 outputs each
+    float acc[4][4] = {};
+    for (int k0 = 0; k0 < a.K; k0 += CB_K) {
+        // A tile: 64 rows x 16 k
+        for (int i = tid; i < CB_M * CB_K; i += 256) {
+            const int r = i / CB_K, kk = i % CB_K;
+            const int row = m0 + r, k = k0 + kk;
+            float v = 0.f;
+            if (row < a.rows && k < a.K) {
+                int s = 0;
+                while (s + 1 < a.n_seg && k >= a.seg[s + 1].k0) ++s;
+                const PSeg sg = a.seg[s];
+                const int b = row / a.Tv, t = row % a.Tv + sg.dt;
+                if (t >= 0 && t < a.Tv)
+                    v = a.src[sg.src][((size_t)b * a.Tv + t) * a.ld[sg.src] + sg.c0 + (k - sg.k0)];
+            }
+            As[kk][r] = v;
+        }
+        for (int i = tid; i < CB_K * CB_N; i += 256) {
+            const int kk = i / CB_N, n = i % CB_N;
+            const int k = k0 + kk, col = n0 + n;
+            Bs[kk][n] = (k < a.K && col < a.N) ? a.W[(size_t)k * a.N + col] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < CB_K; ++kk) {
+            float av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[kk][tr * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tc * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int row = m0 + tr * 4 + i;
+        if (row >= a.rows) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int col = n0 + tc * 4 + j;
+            if (col < a.N) a.out[(size_t)row * a.N + col] = acc[i][j] + a.bias[col];
+        }
+    }
+}
+
+// GroupNorm + Mish (+ FiLM) (+ residual) over one (sample, group) per block.
+struct GnArgs {
+    const float* pre;     // [rows][C]
+    const float* gamma;
+    const float* beta;
+    int C, Tv, S;
+    const float* film_a;  // [P][3584] (may be null)
+    const float* film_b;  // [3584] row of this step
+    int film_col;
+    const float* res;     // [rows][C] (may be null)
+    float* out;
+};
+
+__global__ void __launch_bounds__(256) gn_epi_f32_kernel(const __grid_constant__ GnArgs a) {
+    const int b = blockIdx.x, g = blockIdx.y;
+    const int cg = a.C / U_GROUPS;
+    const int n = a.Tv * cg;
+    __shared__ float red[32];
+    __shared__ float stat[2];
+    const float* base = a.pre + (size_t)b * a.Tv * a.C + g * cg;
+    float s = 0.f;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += base[(size_t)(i / cg) * a.C + i % cg];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(PS_FULL, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        stat[0] = t / n;
+    }
+    __syncthreads();
+    const float mean = stat[0];
+    float v = 0.f;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const float d = base[(size_t)(i / cg) * a.C + i % cg] - mean;
+        v = fmaf(d, d, v);
+    }
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(PS_FULL, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        stat[1] = rsqrtf(t / n + 1e-5f);
+    }
+    __syncthreads();
+    const float rstd = stat[1];
+    const int p = b / a.S;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int t = i / cg, c = g * cg + i % cg;
+        const size_t idx = ((size_t)b * a.Tv + t) * a.C + c;
+        float y = (a.pre[idx] - mean) * rstd * a.gamma[c] + a.beta[c];
+        y = mishf(y);
+        if (a.film_a) {
+            const float* fa = a.film_a + (size_t)p * U_FILM_COLS + a.film_col;
+            const float* fb = a.film_b + a.film_col;
+            const float sc = fa[c] + fb[c], sh = fa[a.C + c] + fb[a.C + c];
+            y = y * (1.f + sc) + sh;
+        }
+        if (a.res) y += a.res[idx];
+        a.out[idx] = y;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// encoder: conv3x3 stride 2 pad 1 + ReLU (NCHW per image), global mean, condition
+// ---------------------------------------------------------------------------
+
+__global__ void conv2d_s2_relu_kernel(const float* __restrict__ in, int C, int H, int W, const float* __restrict__ w,
+                                      const float* __restrict__ bias, int O, float* __restrict__ out, float in_scale) {
+    const int Ho = (H - 1) / 2 + 1, Wo = (W - 1) / 2 + 1;
+    const int img = blockIdx.z;
+    const int o = blockIdx.y;
+    const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pix >= Ho * Wo) return;
+    const int oy = pix / Wo, ox = pix % Wo;
+    const float* ib = in + (size_t)img * C * H * W;
+    float acc = bias[o];
+    for (int c = 0; c < C; ++c) {
+        const float* wc = w + ((size_t)o * C + c) * 9;
+        const float* ic = ib + (size_t)c * H * W;
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy) {
+            const int y = 2 * oy + dy - 1;
+            if (y < 0 || y >= H) continue;
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+                const int xx = 2 * ox + dx - 1;
+                if (xx < 0 || xx >= W) continue;
+                acc = fmaf(ic[(size_t)y * W + xx] * in_scale, wc[dy * 3 + dx], acc);
+            }
+        }
+    }
+    out[((size_t)img * O + o) * Ho * Wo + pix] = fmaxf(acc, 0.f);
+}
+
+// cond[p] = [mean over images of GAP(feat) ; (q - lo)/(hi - lo) ; goal xyz / 0.6 ; quat]
+__global__ void cond_kernel(const float* __restrict__ feat, int n_img, int C, int HW, const float* __restrict__ q,
+                            const float* __restrict__ goal, float lo, float hi, float* __restrict__ cond) {
+    const int p = blockIdx.x;
+    const int c = threadIdx.x;
+    if (c < C) {
+        float acc = 0.f;
+        for (int m = 0; m < n_img; ++m) {
+            const float* f = feat + ((size_t)(p * n_img + m) * C + c) * HW;
+            float s = 0.f;
+            for (int i = 0; i < HW; ++i) s += f[i];
+            acc += s / HW;
+        }
+        cond[(size_t)p * U_COND + c] = acc / n_img;
+    }
+    if (c < U_DOF) cond[(size_t)p * U_COND + C + c] = (q[p * U_DOF + c] - lo) / (hi - lo);
+    if (c < 3) cond[(size_t)p * U_COND + C + U_DOF + c] = goal[p * 7 + c] / 0.6f;
+    if (c < 4) cond[(size_t)p * U_COND + C + U_DOF + 3 + c] = goal[p * 7 + 3 + c];
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+
+static int launch_conv_f32(const Layout& L, const PConv& c, const char* packed, const float* s0, int ld0,
+                           const float* s1, int ld1, int Tv, int rows, float* out, cudaStream_t st) {
+    ConvArgs a{};
+    a.src[0] = s0;
+    a.src[1] = s1;
+    a.ld[0] = ld0;
+    a.ld[1] = ld1;
+    a.Tv = Tv;
+    a.rows = rows;
+    a.N = c.N;
+    a.K = c.K;
+    a.n_seg = c.n_seg;
+    for (int i = 0; i < c.n_seg; ++i) a.seg[i] = c.seg[i];
+    a.W = reinterpret_cast<const float*>(packed) + c.w_off;
+    a.bias = L.side(packed) + c.b_off;
+    a.out = out;
+    dim3 grid((rows + CB_M - 1) / CB_M, (c.N + CB_N - 1) / CB_N);
+    conv_gemm_f32_kernel<<<grid, 256, 0, st>>>(a);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+static int launch_gn(const Layout& L, const PConv& c, const char* packed, const float* pre, int C, int Tv,
+                     int B, int S, const float* film_a, const float* film_b, const float* res, float* out,
+                     cudaStream_t st) {
+    GnArgs g{};
+    g.pre = pre;
+    g.gamma = L.side(packed) + c.g_off;
+    g.beta = L.side(packed) + c.be_off;
+    g.C = C;
+    g.Tv = Tv;
+    g.S = S;
+    g.film_a = film_a;
+    g.film_b = film_b;
+    g.film_col = c.film_col;
+    g.res = res;
+    g.out = out;
+    gn_epi_f32_kernel<<<dim3(B, U_GROUPS), 256, 0, st>>>(g);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+#define PS_TRY(x)            \
+    do {                     \
+        int s_ = (x);        \
+        if (s_) return s_;   \
+    } while (0)
+
+size_t f32_slot_elems(int B, int T) { return (size_t)B * T * 128; }
+
+// One U-Net evaluation in fp32 (mode 0).  x: state (B,T,7); eps out (B,T,7).
+int unet_eval_f32(const Layout& L, const char* packed, const float* x, int B, int T, int S, const float* film_a,
+                  const float* film_b_row, float* ws, float* eps, cudaStream_t st) {
+    const size_t SL = f32_slot_elems(B, T);
+    float* slot[8];
+    for (int i = 0; i < 8; ++i) slot[i] = ws + i * SL;
+    float *pre = slot[0], *h = slot[1], *r = slot[2], *skip1 = slot[6], *skip2 = slot[7];
+    float* cur = slot[3];
+    float* nxt = slot[4];
+    auto block = [&](int bi, const float* in0, int ld0, const float* in1, int ld1, float* out) -> int {
+        const PBlock& bk = L.blk[bi];
+        const int Tv = T >> bk.level, rows = B * Tv, co = bk.c_out;
+        PS_TRY(launch_conv_f32(L, bk.c0, packed, in0, ld0, in1, ld1, Tv, rows, pre, st));
+        PS_TRY(launch_gn(L, bk.c0, packed, pre, co, Tv, B, S, film_a, film_b_row, nullptr, h, st));
+        PS_TRY(launch_conv_f32(L, bk.c1, packed, h, co, nullptr, 0, Tv, rows, pre, st));
+        const float* res = in0;
+        if (bk.res.K) {
+            PS_TRY(launch_conv_f32(L, bk.res, packed, in0, ld0, in1, ld1, Tv, rows, r, st));
+            res = r;
+        }
+        return launch_gn(L, bk.c1, packed, pre, co, Tv, B, S, nullptr, nullptr, res, out, st);
+    };
+    auto swap = [&]() { std::swap(cur, nxt); };
+    PS_TRY(block(0, x, U_DOF, nullptr, 0, cur));
+    PS_TRY(block(1, cur, 64, nullptr, 0, nxt)); swap();
+    PS_TRY(launch_conv_f32(L, L.down[0], packed, cur, 128, nullptr, 0, T / 2, B * T / 2, nxt, st)); swap();
+    PS_TRY(block(2, cur, 64, nullptr, 0, nxt)); swap();
+    PS_TRY(block(3, cur, 128, nullptr, 0, skip1));
+    PS_TRY(launch_conv_f32(L, L.down[1], packed, skip1, 256, nullptr, 0, T / 4, B * T / 4, cur, st));
+    PS_TRY(block(4, cur, 128, nullptr, 0, nxt)); swap();
+    PS_TRY(block(5, cur, 256, nullptr, 0, skip2));
+    PS_TRY(block(6, skip2, 256, nullptr, 0, cur));
+    PS_TRY(block(7, cur, 256, nullptr, 0, nxt)); swap();
+    PS_TRY(block(8, cur, 256, skip2, 256, nxt)); swap();
+    PS_TRY(block(9, cur, 128, nullptr, 0, nxt)); swap();
+    PS_TRY(launch_conv_f32(L, L.up[0], packed, cur, 128, nullptr, 0, T / 4, B * T / 4, nxt, st)); swap();
+    PS_TRY(block(10, cur, 128, skip1, 128, nxt)); swap();
+    PS_TRY(block(11, cur, 64, nullptr, 0, nxt)); swap();
+    PS_TRY(launch_conv_f32(L, L.up[1], packed, cur, 64, nullptr, 0, T / 2, B * T / 2, nxt, st)); swap();
+    PS_TRY(launch_conv_f32(L, L.fin, packed, cur, 64, nullptr, 0, T, B * T, pre, st));
+    PS_TRY(launch_gn(L, L.fin, packed, pre, 64, T, B, S, nullptr, nullptr, nullptr, h, st));
+    return launch_conv_f32(L, L.out, packed, h, 64, nullptr, 0, T, B * T, eps, st);
+}
+
+}  // namespace ps
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+using namespace ps;
+
+extern "C" long long ps_unet_param_count(void) { return (long long)make_layout(0, nullptr).n_params; }
+
+extern "C" long long ps_unet_param_offset(const char* name) {
+    auto t = unet_param_table();
+    const ParamEntry* e = find_param(t, name);
+    return e ? (long long)e->off : -1;
+}
+
+extern "C" long long ps_unet_packed_bytes(int mode) {
+    if (mode != 0 && mode != 1) return -1;
+    return (long long)make_layout(mode, nullptr).total_bytes;
+}
+
+extern "C" int ps_unet_pack(const float* blob, int mode, void* packed, void* stream) {
+    if (mode != 0 && mode != 1) return PS_ERR_SHAPE;
+    PackMap M;
+    Layout L = make_layout(mode, &M);
+    cudaStream_t st = (cudaStream_t)stream;
+    long long* d_idx = nullptr;
+    const size_t nmax = std::max(M.w_src.size(), M.s_src.size());
+    if (cudaMallocAsync(&d_idx, nmax * sizeof(long long), st) != cudaSuccess) return PS_ERR_CUDA;
+    // weights
+    if (cudaMemcpyAsync(d_idx, M.w_src.data(), M.w_src.size() * sizeof(long long), cudaMemcpyHostToDevice, st) !=
+        cudaSuccess)
+        return PS_ERR_CUDA;
+    {
+        const size_t n = M.w_src.size();
+        const unsigned blocks = (unsigned)((n + 255) / 256);
+        if (mode == 0)
+            gather_kernel<float><<<blocks, 256, 0, st>>>(blob, d_idx, n, reinterpret_cast<float*>(packed));
+        else
+            gather_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(blob, d_idx, n, reinterpret_cast<__nv_bfloat16*>(packed));
+        PS_CHECK_LAUNCH();
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess) return PS_ERR_CUDA;  // host vector reuse below
+    if (cudaMemcpyAsync(d_idx, M.s_src.data(), M.s_src.size() * sizeof(long long), cudaMemcpyHostToDevice, st) !=
+        cudaSuccess)
+        return PS_ERR_CUDA;
+    {
+        const size_t n = M.s_src.size();
+        gather_kernel<float><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+            blob, d_idx, n, reinterpret_cast<float*>(reinterpret_cast<char*>(packed) + L.w_bytes));
+        PS_CHECK_LAUNCH();
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess) return PS_ERR_CUDA;
+    cudaFreeAsync(d_idx, st);
+    return PS_OK;
+}
+
+extern "C" long long ps_sample_workspace_bytes(int B, int T, int P, int n_steps, int mode) {
+    if (B <= 0 || (T != 32 && T != 64) || P <= 0 || n_steps <= 0) return -1;
+    const size_t film = (size_t)P * U_FILM_COLS + (size_t)n_steps * (U_FILM_COLS + U_TEMB + U_THID + U_TEMB);
+    const size_t state = 2 * (size_t)B * T * U_DOF;
+    size_t act;
+    if (mode == 0)
+        act = 8 * f32_slot_elems(B, T) * 4;
+    else
+        act = tc_workspace_bytes(B, T);
+    return (long long)((film + state) * 4 + act + 4096);
+}
+
+// per-problem FiLM part: film_a = mish(cond) @ W_c  (P, 3584)
+extern "C" int ps_film_problem(const void* packed, int mode, const float* cond, int P, float* film_a, void* stream) {
+    if (P < 0 || (mode != 0 && mode != 1)) return PS_ERR_SHAPE;
+    if (P == 0) return PS_OK;
+    Layout L = make_layout(mode, nullptr);
+    const char* pk = reinterpret_cast<const char*>(packed);
+    dense_kernel<<<dim3((U_FILM_COLS + 127) / 128, P), 128, 0, (cudaStream_t)stream>>>(
+        cond, U_COND, L.side(pk) + L.film_wc, U_FILM_COLS, nullptr, P, U_COND, U_FILM_COLS, 1, 0, film_a,
+        U_FILM_COLS);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+// per-step FiLM part for a list of 1-based steps: film_b[i] = mish(temb(k_i)) @ W_t + b
+extern "C" int ps_film_steps(const void* packed, int mode, const int* ks_dev, int n, float* scratch,
+                             float* film_b, void* stream) {
+    if (n <= 0) return PS_ERR_SHAPE;
+    Layout L = make_layout(mode, nullptr);
+    const char* pk = reinterpret_cast<const char*>(packed);
+    cudaStream_t st = (cudaStream_t)stream;
+    float* sinus = scratch;
+    float* hid = sinus + (size_t)n * U_TEMB;
+    float* temb = hid + (size_t)n * U_THID;
+    sinusoid_kernel<<<n, 64, 0, st>>>(ks_dev, n, sinus);
+    dense_kernel<<<dim3((U_THID + 127) / 128, n), 128, 0, st>>>(sinus, U_TEMB, L.side(pk) + L.t1w, U_THID,
+                                                                 L.side(pk) + L.t1b, n, U_TEMB, U_THID, 0, 1, hid,
+                                                                 U_THID);
+    dense_kernel<<<dim3(1, n), 128, 0, st>>>(hid, U_THID, L.side(pk) + L.t2w, U_TEMB, L.side(pk) + L.t2b, n, U_THID,
+                                             U_TEMB, 0, 0, temb, U_TEMB);
+    dense_kernel<<<dim3((U_FILM_COLS + 127) / 128, n), 128, 0, st>>>(
+        temb, U_TEMB, L.side(pk) + L.film_wt, U_FILM_COLS, L.side(pk) + L.film_b, n, U_TEMB, U_FILM_COLS, 1, 0,
+        film_b, U_FILM_COLS);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+extern "C" int ps_unet_forward(const void* packed, int mode, const float* x, int B, int T, int S, int k,
+                               const float* film_a, void* ws, float* eps, void* stream) {
+    if (B <= 0 || (T != 32 && T != 64) || S <= 0 || B % S) return PS_ERR_SHAPE;
+    Layout L = make_layout(mode, nullptr);
+    cudaStream_t st = (cudaStream_t)stream;
+    char* w = reinterpret_cast<char*>(ws);
+    int* dk = reinterpret_cast<int*>(w);
+    float* film_b = reinterpret_cast<float*>(w + 256);
+    float* scratch = film_b + U_FILM_COLS;
+    float* act = scratch + (U_TEMB + U_THID + U_TEMB);
+    act = reinterpret_cast<float*>(align_up(reinterpret_cast<size_t>(act), 256));
+    if (cudaMemcpyAsync(dk, &k, sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess) return PS_ERR_CUDA;
+    PS_TRY(ps_film_steps(packed, mode, dk, 1, scratch, film_b, stream));
+    if (mode == 0)
+        return unet_eval_f32(L, reinterpret_cast<const char*>(packed), x, B, T, S, film_a, film_b, act, eps, st);
+    return unet_eval_tc(L, reinterpret_cast<const char*>(packed), const_cast<float*>(x), B, T, S, film_a, film_b, act, eps, nullptr,
+                        st);
+}
+
+extern "C" int ps_noise_probe(float* out, int n, int step, int prob, int seed, unsigned key, void* stream) {
+    noise_probe_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(out, n, (uint32_t)step, (uint32_t)prob,
+                                                                           (uint32_t)seed, key);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+// Full seed generation for P problems x S seeds.  steps_h: 1-based indices, descending;
+// ddpm=1 runs the stochastic posterior update between consecutive indices k -> k-1
+// (requires the full K..1 list), ddpm=0 the deterministic DDIM update (eta = 0).
+// coef_h: 6 x (K+1) float32 tables (sq, sq1m, rsq, c0, c1, sig) from spec.sampler_tables.
+extern "C" int ps_sample(const void* packed, int mode, const float* film_a, int P, int S, int T, int p0,
+                         const int* steps_h, int n_steps, int ddpm, const float* coef_h, int K, unsigned noise_key,
+                         const float* q_start, float lo, float hi, void* ws, float* traj, void* stream) {
+    if (P <= 0 || S <= 0 || (T != 32 && T != 64) || n_steps <= 0 || K <= 0) return PS_ERR_SHAPE;
+    for (int i = 0; i < n_steps; ++i)
+        if (steps_h[i] < 1 || steps_h[i] > K) return PS_ERR_SHAPE;
+    const int B = P * S;
+    Layout L = make_layout(mode, nullptr);
+    cudaStream_t st = (cudaStream_t)stream;
+    char* w = reinterpret_cast<char*>(ws);
+    int* dks = reinterpret_cast<int*>(w);
+    size_t off = align_up((size_t)n_steps * 4, 256);
+    float* film_b = reinterpret_cast<float*>(w + off);
+    off = align_up(off + (size_t)n_steps * U_FILM_COLS * 4, 256);
+    float* scratch = reinterpret_cast<float*>(w + off);
+    off = align_up(off + (size_t)n_steps * (U_TEMB + U_THID + U_TEMB) * 4, 256);
+    float* x = reinterpret_cast<float*>(w + off);
+    off = align_up(off + (size_t)B * T * U_DOF * 4, 256);
+    float* eps = reinterpret_cast<float*>(w + off);
+    off = align_up(off + (size_t)B * T * U_DOF * 4, 256);
+    float* act = reinterpret_cast<float*>(w + off);
+    if (cudaMemcpyAsync(dks, steps_h, n_steps * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return PS_ERR_CUDA;
+    PS_TRY(ps_film_steps(packed, mode, dks, n_steps, scratch, film_b, stream));
+    const size_t n = (size_t)B * T * U_DOF;
+    noise_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, B, T, S, p0, noise_key);
+    PS_CHECK_LAUNCH();
+    const float* sq = coef_h;
+    const float* sq1m = coef_h + (K + 1);
+    const float* rsq = coef_h + 2 * (K + 1);
+    const float* c0 = coef_h + 3 * (K + 1);
+    const float* c1 = coef_h + 4 * (K + 1);
+    const float* sig = coef_h + 5 * (K + 1);
+    const char* pk = reinterpret_cast<const char*>(packed);
+    for (int i = 0; i < n_steps; ++i) {
+        const int k = steps_h[i];
+        StepCoef sc{};
+        sc.k = k;
+        sc.sq1m = sq1m[k];
+        sc.rsq = rsq[k];
+        sc.last = (i + 1 == n_steps);
+        sc.ddpm = ddpm;
+        if (ddpm) {
+            sc.c0 = c0[k];
+            sc.c1 = c1[k];
+            sc.sig = sig[k];
+        } else if (!sc.last) {
+            sc.sqn = sq[steps_h[i + 1]];
+            sc.sq1mn = sq1m[steps_h[i + 1]];
+        }
+        const float* fb = film_b + (size_t)i * U_FILM_COLS;
+        if (mode == 0) {
+            PS_TRY(unet_eval_f32(L, pk, x, B, T, S, film_a, fb, act, eps, st));
+            step_update_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, eps, sc, B, T, S, p0, noise_key,
+                                                                             q_start, traj, lo, hi);
+            PS_CHECK_LAUNCH();
+        } else {
+            TcStep ts{sc, p0, noise_key, q_start, traj, lo, hi};
+            PS_TRY(unet_eval_tc(L, pk, x, B, T, S, film_a, fb, act, eps, &ts, st));
+        }
+    }
+    return PS_OK;
+}
+
+// Observation encoder: images (P*n_img, H, W) depth in metres -> cond (P, 270).
+// ws must hold ps_encode_workspace_bytes floats.
+extern "C" long long ps_encode_workspace_bytes(int n_images, int H, int W, int n_layers) {
+    size_t h = H, w = W, total = 0, mx = 0;
+    const int ch[5] = {32, 64, 128, 256, 256};
+    for (int i = 0; i < n_layers; ++i) {
+        h = (h - 1) / 2 + 1;
+        w = (w - 1) / 2 + 1;
+        mx = std::max(mx, (size_t)n_images * ch[i] * h * w);
+    }
+    total = 2 * mx;
+    return (long long)(total * 4 + 512);
+}
+
+extern "C" int ps_encode(const float* images, int P, int n_img, int H, int W, const float* enc_w, int n_layers,
+                         const float* q_start, const float* goal, float lo, float hi, void* ws, float* cond,
+                         void* stream) {
+    if (P <= 0 || n_img <= 0 || n_layers < 1 || n_layers > 5) return PS_ERR_SHAPE;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int ch[5] = {32, 64, 128, 256, 256};
+    const size_t half = (size_t)(ps_encode_workspace_bytes(P * n_img, H, W, n_layers) - 512) / 8;
+    float* buf[2] = {reinterpret_cast<float*>(ws), reinterpret_cast<float*>(ws) + half};
+    const float* in = images;
+    int C = 1, h = H, wd = W;
+    size_t woff = 0;
+    for (int l = 0; l < n_layers; ++l) {
+        const int O = ch[l];
+        const int Ho = (h - 1) / 2 + 1, Wo = (wd - 1) / 2 + 1;
+        const float* wl = enc_w + woff;
+        const float* bl = wl + (size_t)O * C * 9;
+        woff += (size_t)O * C * 9 + O;
+        dim3 grid((Ho * Wo + 127) / 128, O, P * n_img);
+        conv2d_s2_relu_kernel<<<grid, 128, 0, st>>>(in, C, h, wd, wl, bl, O, buf[l & 1], l == 0 ? 0.5f : 1.0f);
+        PS_CHECK_LAUNCH();
+        in = buf[l & 1];
+        C = O;
+        h = Ho;
+        wd = Wo;
+    }
+    cond_kernel<<<P, 256, 0, st>>>(in, n_img, C, h * wd, q_start, goal, lo, hi, cond);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}

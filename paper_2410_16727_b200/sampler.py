@@ -1,0 +1,135 @@
+"""BASELINE-profile seed sampler over the C-ABI: encoder, U-Net noise predictor and the
+DDPM / strided-DDIM step loop, batched over problems.
+
+Counterparts of the reference sampler API (planseed/diffusion.py):
+  SeedSampler.encode         ~ encode_condition   (:246-269), P problems at once
+  SeedSampler.predict_noise  ~ predict_noise      (:288-300)
+  SeedSampler.sample         ~ ddim_sample        (:559-569) / DDPM with posterior noise
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib, spec
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+class SeedSampler:
+    """Device-resident packed weights + schedule tables.
+
+    mode 0: fp32 SIMT kernels (fp32 profile, configs 0/2);
+    mode 1: bf16 weights/activations on tcgen05 with fp32 accumulation and fp32
+            DDPM state (configs 1/3)."""
+
+    def __init__(self, params: dict, enc: spec.EncoderArch = spec.ENCODER_CFG0,
+                 arch: spec.UNetArch = spec.UNetArch(), mode: int = 0, betas=None,
+                 noise_seed: int = spec.NOISE_SEED):
+        torch = _lib.require_cuda()
+        L = _lib.lib()
+        self.enc, self.arch, self.mode = enc, arch, int(mode)
+        shapes = arch.param_shapes()
+        if L.ps_unet_param_count() != arch.n_params():
+            raise ValueError("library U-Net table does not match spec.UNetArch")
+        blob = np.concatenate([_f32(params[n]).ravel() for n, _ in shapes])
+        self._blob = torch.as_tensor(blob, device="cuda")
+        eb = np.concatenate([_f32(params[n]).ravel() for n, _ in spec.encoder_param_shapes(enc)])
+        self.enc_w = torch.as_tensor(eb, device="cuda")
+        nbytes = L.ps_unet_packed_bytes(self.mode)
+        self.packed = torch.empty(int(nbytes), dtype=torch.uint8, device="cuda")
+        _lib.check(L.ps_unet_pack(_lib.ptr(self._blob), self.mode, _lib.ptr(self.packed),
+                                  _lib.stream_handle()), "unet_pack")
+        self.betas = spec.cosine_betas() if betas is None else np.asarray(betas, np.float64)
+        tab = spec.sampler_tables(self.betas)
+        self.coef = _f32(np.stack([tab.sq, tab.sq1m, tab.rsq, tab.c0, tab.c1, tab.sig]))
+        self.K = int(self.betas.shape[0])
+        self.noise_key = int(noise_seed) & 0xFFFFFFFF
+        self._ws = None
+
+    # ------------------------------------------------------------------ helpers
+    def _workspace(self, nbytes: int):
+        torch = _lib.require_cuda()
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(int(nbytes), dtype=torch.uint8, device="cuda")
+        return self._ws
+
+    # ------------------------------------------------------------------ API
+    def encode(self, images, q_start, goal, stream=None):
+        """images (P, n_img, H, W) depth metres; q_start (P,7); goal (P,7) -> cond (P,270)."""
+        torch = _lib.require_cuda()
+        from .bl import _dev
+        im = _dev(images)
+        P, n_img, H, W = im.shape
+        q, g = _dev(q_start), _dev(goal)
+        L = _lib.lib()
+        nl = len(self.enc.channels)
+        ws = torch.empty(int(L.ps_encode_workspace_bytes(P * n_img, H, W, nl)), dtype=torch.uint8,
+                         device="cuda")
+        cond = torch.empty((P, spec.COND_DIM), dtype=torch.float32, device="cuda")
+        st = L.ps_encode(_lib.ptr(im), P, n_img, H, W, _lib.ptr(self.enc_w), nl, _lib.ptr(q),
+                         _lib.ptr(g), -spec.JOINT_LIMIT, spec.JOINT_LIMIT, _lib.ptr(ws),
+                         _lib.ptr(cond), _lib.stream_handle(stream))
+        _lib.check(st, "encode")
+        return cond
+
+    def film(self, cond, stream=None):
+        torch = _lib.require_cuda()
+        from .bl import _dev
+        c = _dev(cond)
+        fa = torch.empty((c.shape[0], 3584), dtype=torch.float32, device="cuda")
+        _lib.check(_lib.lib().ps_film_problem(_lib.ptr(self.packed), self.mode, _lib.ptr(c),
+                                              c.shape[0], _lib.ptr(fa), _lib.stream_handle(stream)),
+                   "film_problem")
+        return fa
+
+    def predict_noise(self, x, k: int, film_a, S: int, stream=None):
+        """eps(x, k) for x (B,T,7) normalised, B = P*S."""
+        torch = _lib.require_cuda()
+        from .bl import _dev
+        xd = _dev(x)
+        B, T, _ = xd.shape
+        L = _lib.lib()
+        ws = self._workspace(L.ps_sample_workspace_bytes(B, T, max(1, B // S), 1, self.mode))
+        eps = torch.empty_like(xd)
+        st = L.ps_unet_forward(_lib.ptr(self.packed), self.mode, _lib.ptr(xd), B, T, S, int(k),
+                               _lib.ptr(film_a), _lib.ptr(ws), _lib.ptr(eps),
+                               _lib.stream_handle(stream))
+        _lib.check(st, "unet_forward")
+        return eps
+
+    def sample(self, film_a, q_start, S: int, T: int = spec.T_DEFAULT, p0: int = 0, steps=None,
+               stream=None, out=None):
+        """Seeds for P problems x S seeds -> physical trajectories (P*S, T, 7), row 0 = q_start.
+
+        steps=None: K-step DDPM; otherwise deterministic DDIM over the given indices."""
+        torch = _lib.require_cuda()
+        from .bl import _dev
+        q = _dev(q_start)
+        P = q.shape[0]
+        if steps is None:
+            ks = np.arange(self.K, 0, -1, dtype=np.int32)
+            ddpm = 1
+        else:
+            ks = np.ascontiguousarray(steps, dtype=np.int32)
+            ddpm = 0
+        L = _lib.lib()
+        B = P * S
+        ws = self._workspace(L.ps_sample_workspace_bytes(B, T, P, len(ks), self.mode))
+        traj = out if out is not None else torch.empty((B, T, 7), dtype=torch.float32, device="cuda")
+        st = L.ps_sample(_lib.ptr(self.packed), self.mode, _lib.ptr(film_a), P, S, T, int(p0),
+                         _lib.hptr(ks), len(ks), ddpm, _lib.hptr(self.coef), self.K, self.noise_key,
+                         _lib.ptr(q), -spec.JOINT_LIMIT, spec.JOINT_LIMIT, _lib.ptr(ws),
+                         _lib.ptr(traj), _lib.stream_handle(stream))
+        _lib.check(st, "sample")
+        return traj
+
+
+def noise_probe(n: int, step: int, prob: int, seed: int, key: int = spec.NOISE_SEED):
+    torch = _lib.require_cuda()
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib().ps_noise_probe(_lib.ptr(out), n, step, prob, seed, key,
+                                         _lib.stream_handle()), "noise_probe")
+    return out

@@ -412,3 +412,14 @@ def timestep_sinusoid(k, dim: int = T_EMB) -> np.ndarray:
 # u1 = ((r0 >> 8) + 1) * 2^-24 in (0,1], u2 = (r1 >> 8) * 2^-24 in [0,1)
 # z0 = sqrt(-2 ln u1) cos(2 pi u2), z1 = sqrt(-2 ln u1) sin(2 pi u2); same for r2,r3.
 PHILOX_KEY_HI = 0x5EED5EED
+
+
+def model_param_shapes(enc: EncoderArch = ENCODER_CFG0, arch: UNetArch = UNetArch()):
+    """Encoder table followed by the U-Net table; the PSCK blob order."""
+    return encoder_param_shapes(enc) + arch.param_shapes()
+
+
+def random_model(enc: EncoderArch = ENCODER_CFG0, arch: UNetArch = UNetArch(),
+                 seed: int = WEIGHT_SEED) -> dict:
+    """BASELINE random-init weights ("weights seed 0"), float64 host arrays."""
+    return init_params(model_param_shapes(enc, arch), seed)

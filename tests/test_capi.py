@@ -46,3 +46,24 @@ def test_sass_is_sm100a(libpath):
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", str(libpath)], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
+
+
+def test_unet_param_table_matches_spec(libpath):
+    import numpy as np
+    from paper_2410_16727_b200 import _lib, spec
+    L = _lib.lib()
+    arch = spec.UNetArch()
+    assert L.ps_unet_param_count() == arch.n_params()
+    off = 0
+    for name, shape in arch.param_shapes():
+        assert L.ps_unet_param_offset(name.encode()) == off, name
+        off += int(np.prod(shape))
+    assert L.ps_unet_param_offset(b"nope") == -1
+
+
+def test_packed_sizes(libpath):
+    from paper_2410_16727_b200 import _lib
+    L = _lib.lib()
+    assert L.ps_unet_packed_bytes(0) > 4 * 5_000_000
+    assert L.ps_unet_packed_bytes(1) > 2 * 5_000_000
+    assert L.ps_unet_packed_bytes(7) == -1

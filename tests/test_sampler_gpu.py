@@ -1,0 +1,134 @@
+"""GPU parity of the BASELINE-profile seed sampler (encoder, U-Net, DDPM/DDIM) against the
+numpy oracle (oracle/unet_numpy.py), through the C-ABI.
+
+Tolerances (written here):
+  fp32 mode (mode 0): noise predictions and final trajectories within 1e-4 rad of the
+  float64 oracle (north-star bound), except where the x0 clip boundary is crossed.
+  bf16 mode (mode 1): see test_tc_gpu.py.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import unet_numpy as un
+from paper_2410_16727_b200 import spec, synth
+
+pytestmark = pytest.mark.gpu
+
+ARCH = spec.UNetArch()
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test without a CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def params():
+    return spec.random_model(spec.ENCODER_CFG0)
+
+
+@pytest.fixture(scope="module")
+def sampler(torch_cuda, params):
+    from paper_2410_16727_b200.sampler import SeedSampler
+    return SeedSampler(params, spec.ENCODER_CFG0, ARCH, mode=0)
+
+
+def test_noise_stream_matches_oracle(torch_cuda):
+    from paper_2410_16727_b200.sampler import noise_probe
+    for step, prob, seed in ((0, 0, 0), (37, 5, 31), (100, 1023, 7)):
+        got = noise_probe(224, step, prob, seed).cpu().numpy()
+        want = un.noise(step, np.array([prob]), np.array([seed]), 32).ravel()
+        assert np.abs(got - want).max() < 2e-5
+
+
+class TestEncoder:
+    def test_config0_image(self, sampler, params):
+        pb = synth.config0_problems(3, seed=2)
+        cond = sampler.encode(pb.images, pb.q_start, pb.goal).cpu().numpy()
+        want = un.encode_problems(params, spec.ENCODER_CFG0, pb.images, pb.q_start, pb.goal)
+        np.testing.assert_allclose(cond, want, rtol=1e-4, atol=1e-5)
+
+    def test_config3_two_images_five_layers(self, torch_cuda):
+        from paper_2410_16727_b200.sampler import SeedSampler
+        p3 = spec.random_model(spec.ENCODER_CFG3)
+        s3 = SeedSampler(p3, spec.ENCODER_CFG3, ARCH, mode=0)
+        pb = synth.config3_problems(2, seed=3)
+        cond = s3.encode(pb.images, pb.q_start, pb.goal).cpu().numpy()
+        want = un.encode_problems(p3, spec.ENCODER_CFG3, pb.images, pb.q_start, pb.goal)
+        np.testing.assert_allclose(cond, want, rtol=1e-4, atol=1e-5)
+
+
+def _cond(P, seed=4):
+    rng = np.random.default_rng(seed)
+    c = np.concatenate([np.abs(rng.standard_normal((P, 256))) * 0.3, rng.uniform(0, 1, (P, 7)),
+                        rng.uniform(-1, 1, (P, 3)), rng.standard_normal((P, 4)) * 0.5], axis=1)
+    return c
+
+
+class TestUNet:
+    @pytest.mark.parametrize("T,k", [(32, 100), (32, 37), (32, 1), (64, 50)])
+    def test_predict_noise_fp32(self, sampler, params, T, k):
+        P, S = 3, 4
+        cond = _cond(P)
+        x = np.random.default_rng(T + k).standard_normal((P * S, T, 7)).astype(np.float32)
+        fa = sampler.film(cond)
+        eps = sampler.predict_noise(x, k, fa, S).cpu().numpy()
+        want = un.unet_forward(params, ARCH, x, k, cond, S)
+        assert np.abs(eps - want).max() < 1e-4
+
+    def test_film_problem_part(self, sampler, params):
+        cond = _cond(2)
+        fa = sampler.film(cond).cpu().numpy()
+        e = un.mish(cond)
+        col = 0
+        for blk in ARCH.blocks():
+            w = params[f"{blk.name}_film_w"][spec.T_EMB:]
+            np.testing.assert_allclose(fa[:, col:col + 2 * blk.c_out], e @ w, rtol=1e-5, atol=1e-5)
+            col += 2 * blk.c_out
+
+
+class TestSample:
+    def test_ddpm_100_steps_fp32(self, sampler, params):
+        P, S = 2, 4
+        cond = _cond(P, 8)
+        q0 = synth.make_problems(P, seed=9).q_start
+        traj = sampler.sample(sampler.film(cond), q0, S).cpu().numpy()
+        want = un.sample(params, ARCH, cond, q0, S)
+        assert np.array_equal(traj[:, 0], np.repeat(q0, S, axis=0))
+        assert np.abs(traj - want).max() < 1e-4
+
+    def test_ddim_strided_10_steps_fp32(self, sampler, params):
+        P, S = 2, 4
+        cond = _cond(P, 10)
+        q0 = synth.make_problems(P, seed=11).q_start
+        steps = spec.strided_steps(100, 10)
+        traj = sampler.sample(sampler.film(cond), q0, S, steps=steps).cpu().numpy()
+        want = un.sample(params, ARCH, cond, q0, S, steps=steps)
+        assert np.abs(traj - want).max() < 1e-4
+
+    def test_shard_invariance(self, sampler):
+        # problems [0,4) at once == [0,2) + [2,4) with p0 offsets (noise keyed globally)
+        cond = _cond(4, 12)
+        q0 = synth.make_problems(4, seed=13).q_start
+        fa = sampler.film(cond)
+        steps = spec.strided_steps(100, 5)
+        full = sampler.sample(fa, q0, 8, steps=None).cpu().numpy()
+        a = sampler.sample(fa[:2], q0[:2], 8, p0=0).cpu().numpy()
+        b = sampler.sample(fa[2:], q0[2:], 8, p0=2).cpu().numpy()
+        assert np.array_equal(full, np.concatenate([a, b]))
+        again = sampler.sample(fa, q0, 8).cpu().numpy()
+        assert np.array_equal(full, again)
+        del steps
+
+    def test_config0_pipeline_encode_then_sample(self, sampler, params):
+        pb = synth.config0_problems(1, seed=0)
+        cond = sampler.encode(pb.images, pb.q_start, pb.goal)
+        traj = sampler.sample(sampler.film(cond), pb.q_start, 32).cpu().numpy()
+        c_ref = un.encode_problems(params, spec.ENCODER_CFG0, pb.images, pb.q_start, pb.goal)
+        want = un.sample(params, ARCH, c_ref, pb.q_start, 32)
+        assert traj.shape == (32, 32, 7)
+        assert np.abs(traj - want).max() < 1e-4
