@@ -7,10 +7,25 @@
 
 #define PS_FULL 0xffffffffu
 
-#define PS_CHECK_LAUNCH()                                      \
-    do {                                                       \
-        cudaError_t e_ = cudaGetLastError();                   \
-        if (e_ != cudaSuccess) return PS_ERR_CUDA;             \
+#include <cstdio>
+#include <cstdlib>
+
+// Error returns log file:line when PS_DEBUG is set in the environment.
+inline int ps_fail(int code, const char* file, int line) {
+    static const bool dbg = std::getenv("PS_DEBUG") != nullptr;
+    if (dbg) std::fprintf(stderr, "[ps_b200] status %d at %s:%d\n", code, file, line);
+    return code;
+}
+#define PS_FAIL(code) ps_fail((code), __FILE__, __LINE__)
+
+#define PS_CHECK_LAUNCH()                                                   \
+    do {                                                                    \
+        cudaError_t e_ = cudaGetLastError();                                \
+        if (e_ != cudaSuccess) {                                            \
+            if (std::getenv("PS_DEBUG"))                                    \
+                std::fprintf(stderr, "[ps_b200] %s\n", cudaGetErrorString(e_)); \
+            return PS_FAIL(PS_ERR_CUDA);                                    \
+        }                                                                   \
     } while (0)
 
 namespace ps {

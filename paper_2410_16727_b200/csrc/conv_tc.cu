@@ -1,11 +1,746 @@
-// bf16 tcgen05 U-Net (mode 1) -- placeholder until the tcgen05 kernels land.
+// bf16 tcgen05 U-Net (mode 1): implicit-GEMM temporal convolutions on the 5th-gen
+// tensor cores with fused epilogues.
+//
+// One CTA computes a 128-row tile (rows = (sample, time) pairs, whole samples) for ALL
+// output channels N (64..256), so GroupNorm statistics are complete inside the tile.
+//   warp 0     TMA producer: per K chunk a [128 x 64] bf16 activation box (3-D map over
+//              the [B, Tv, C] view, time offset dt -> out-of-range rows zero-filled by
+//              TMA = the conv's zero padding) and an [N x 64] weight box, SW128.
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer (M=128, N, K=16),
+//              accumulator(s) in TMEM; optional second accumulator for the residual 1x1.
+//   warps 2-5  epilogue: tcgen05.ld -> +bias -> GroupNorm(8) -> Mish -> FiLM / residual
+//              -> bf16 store; FINAL fuses the 64->7 projection, the DDPM/DDIM update of
+//              the fp32 state and the Philox noise injection.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <mutex>
+#include <vector>
+
 #include "common.cuh"
 #include "sampler.cuh"
 
 namespace ps {
-size_t tc_workspace_bytes(int B, int T) { return (size_t)B * T * 64; }
-int unet_eval_tc(const Layout&, const char*, float*, int, int, int, const float*, const float*, float*, float*,
-                 const TcStep*, cudaStream_t) {
-    return PS_ERR_SHAPE;
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
 }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"((uint64_t)tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"((uint64_t)tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major, 128B-swizzled UMMA shared-memory descriptor (rows of 128 B, 8-row atoms)
+__device__ __forceinline__ uint64_t umma_desc_sw128(const void* p) {
+    const uint32_t a = smem_u32(p);
+    uint64_t d = 0;
+    d |= (uint64_t)((a >> 4) & 0x3FFF);          // start address
+    d |= (uint64_t)0 << 16;                       // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;             // SBO: 8 rows x 128 B
+    d |= (uint64_t)1 << 46;                       // version (sm100)
+    d |= (uint64_t)2 << 61;                       // SWIZZLE_128B
+    return d;
+}
+// kind::f16 instruction descriptor: D f32, A/B bf16, K-major both, M=128, N
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// mish(x) = x tanh(softplus(x)) = x * n(n+2) / (n(n+2) + 2), n = e^x
+__device__ __forceinline__ float mish_fast(float x) {
+    if (x > 15.f) return x;
+    const float n = __expf(x);
+    const float m = n * (n + 2.f);
+    return x * __fdividef(m, m + 2.f);
+}
+
+// ---------------------------------------------------------------------------
+// kernel arguments
+// ---------------------------------------------------------------------------
+constexpr int TC_MAX_CHUNKS = 64;
+
+struct TcChunk {
+    int16_t c;      // channel offset in the source view
+    int16_t kcol;   // K column in the weight matrix
+    int8_t src;     // activation source map 0..2
+    int8_t dt;      // time offset
+    int8_t res;     // 1: residual GEMM
+    int8_t first;   // 1: first chunk of its accumulator
+};
+
+struct TcArgs {
+    CUtensorMap tmA[3];
+    CUtensorMap tmW;
+    CUtensorMap tmR;
+    TcChunk chunk[TC_MAX_CHUNKS];
+    int n_chunks, stages;
+    int rows, Tv, S;
+    const float* bias;
+    const float* gamma;
+    const float* beta;
+    const float* rbias;
+    const __nv_bfloat16* res_src;   // identity residual (same [rows, N] layout)
+    const float* film;              // [P][3584] step FiLM, this block's scale at film + col
+    int film_col;
+    __nv_bfloat16* out;             // [rows, N]
+    // FINAL
+    const float* wout;              // [7][64]
+    const float* bout;
+    float* x;                       // fp32 state [rows][7]
+    StepCoef sc;
+    int p0;
+    unsigned key;
+    const float* q_start;
+    float* traj;
+    float lo, hi;
+    float* eps_out;                 // optional: write eps (forward-only calls)
+};
+
+__device__ __forceinline__ uint4 philox_tc(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+__device__ __forceinline__ float normal_tc(uint32_t step, uint32_t prob, uint32_t seed, uint32_t e, uint32_t key) {
+    const uint4 r = philox_tc(make_uint4(e >> 2, step, prob, seed), key, 0x5EED5EEDu);
+    const uint32_t comp = e & 3u;
+    const uint32_t a = comp < 2 ? r.x : r.z, b = comp < 2 ? r.y : r.w;
+    const float u1 = ((float)(a >> 8) + 1.0f) * (1.0f / 16777216.0f);
+    const float u2 = (float)(b >> 8) * (1.0f / 16777216.0f);
+    const float rad = sqrtf(-2.0f * logf(u1));
+    const float ang = 6.28318530717958648f * u2;
+    return (comp & 1u) ? rad * sinf(ang) : rad * cosf(ang);
+}
+
+template <int N>
+__host__ __device__ constexpr int tmem_cols(bool res) {
+    return (res ? 2 * N : N) <= 32 ? 32 : (res ? 2 * N : N) <= 64 ? 64 : (res ? 2 * N : N) <= 128 ? 128
+                                                                        : (res ? 2 * N : N) <= 256 ? 256 : 512;
+}
+
+constexpr int TC_THREADS = 192;
+
+template <int N, int EPI, bool RES>
+__global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_constant__ TcArgs a) {
+    constexpr int A_BYTES = 128 * 128;
+    constexpr int B_BYTES = N * 128;
+    constexpr int STAGE = A_BYTES + B_BYTES;
+    constexpr int NCOLS = tmem_cols<N>(RES);
+    constexpr int CG = N / 8;  // channels per group
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    const int stages = a.stages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * STAGE);
+    uint64_t* empty = full + stages;
+    uint64_t* tfull = empty + stages;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tfull + 1);
+    float* sv = reinterpret_cast<float*>(tmem_holder + 4);  // per-channel vectors
+    float* s_bias = sv;
+    float* s_gamma = sv + N;
+    float* s_beta = sv + 2 * N;
+    float* s_rbias = sv + 3 * N;
+    float* s_red = sv + 4 * N;          // [16][8] cross-warp GN partials
+    float* s_wout = s_red + 128;        // [7][64]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * 128;
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < stages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(tfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmA[0]) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmW) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "r"(NCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (warp >= 2) {
+        for (int i = threadIdx.x - 64; i < N; i += 128) {
+            s_bias[i] = a.bias[i];
+            if (EPI == EPI_GN_FILM || EPI == EPI_GN_RES || EPI == EPI_FINAL) {
+                s_gamma[i] = a.gamma[i];
+                s_beta[i] = a.beta[i];
+            }
+            if (RES) s_rbias[i] = a.rbias[i];
+        }
+        if (EPI == EPI_FINAL)
+            for (int i = threadIdx.x - 64; i < U_DOF * 64; i += 128) s_wout[i] = a.wout[i];
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const int b0 = m0 / a.Tv;
+            for (int i = 0; i < a.n_chunks; ++i) {
+                const int s = i % stages;
+                const uint32_t ph = (uint32_t)(i / stages) & 1u;
+                mbar_wait(&empty[s], ph ^ 1u);
+                mbar_expect_tx(&full[s], STAGE);
+                const TcChunk ch = a.chunk[i];
+                uint8_t* sa = smem + (size_t)s * STAGE;
+                tma_load_3d(sa, &a.tmA[ch.src], &full[s], ch.c, ch.dt, b0);
+                tma_load_2d(sa + A_BYTES, ch.res ? &a.tmR : &a.tmW, &full[s], ch.kcol, 0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16(128, N);
+            for (int i = 0; i < a.n_chunks; ++i) {
+                const int s = i % stages;
+                const uint32_t ph = (uint32_t)(i / stages) & 1u;
+                mbar_wait(&full[s], ph);
+                tc_fence_after();
+                const TcChunk ch = a.chunk[i];
+                const uint8_t* sa = smem + (size_t)s * STAGE;
+                const uint64_t da = umma_desc_sw128(sa);
+                const uint64_t db = umma_desc_sw128(sa + A_BYTES);
+                const uint32_t d_tmem = tmem_base + (ch.res ? (uint32_t)N : 0u);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    umma_bf16(d_tmem, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc,
+                              (ch.first && kk == 0) ? 0u : 1u);
+                umma_commit(&empty[s]);
+            }
+            umma_commit(tfull);
+        }
+        __syncwarp();
+    } else {
+        // ============================ epilogue ============================
+        const int q = warp & 3;  // TMEM lane quadrant of this warp
+        const int r = q * 32 + lane;
+        const int grow = m0 + r;
+        const bool valid = grow < a.rows;
+        const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16);
+        mbar_wait(tfull, 0);
+        tc_fence_after();
+
+        if constexpr (EPI == EPI_PLAIN) {
+#pragma unroll 1
+            for (int c0 = 0; c0 < N; c0 += 32) {
+                float v[32];
+                tmem_ld32(t_lane + c0, v);
+                if (valid) {
+                    __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 8) {
+                        __align__(16) __nv_bfloat162 pk[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            pk[u] = __floats2bfloat162_rn(v[j + 2 * u] + s_bias[c0 + j + 2 * u],
+                                                          v[j + 2 * u + 1] + s_bias[c0 + j + 2 * u + 1]);
+                        *reinterpret_cast<uint4*>(o + j) = *reinterpret_cast<uint4*>(pk);
+                    }
+                }
+            }
+        } else {
+            // ---- GroupNorm statistics over (sample rows) x (group channels)
+            const int Tv = a.Tv;
+            const int seg = Tv < 32 ? Tv : 32;
+            float gsum[8], mean[8], rstd[8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) gsum[g] = 0.f;
+#pragma unroll 1
+            for (int c0 = 0; c0 < N; c0 += 32) {
+                float v[32];
+                tmem_ld32(t_lane + c0, v);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) gsum[(c0 + j) / CG] += v[j] + s_bias[c0 + j];
+            }
+            auto reduce = [&](float (&x)[8]) {
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1)
+                    if (off < seg)
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) x[g] += __shfl_xor_sync(PS_FULL, x[g], off);
+                if (Tv > 32) {  // a sample spans two warps (quadrants q, q^1)
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (lane == 0)
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) s_red[q * 8 + g] = x[g];
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) x[g] = s_red[q * 8 + g] + s_red[(q ^ 1) * 8 + g];
+                }
+            };
+            reduce(gsum);
+            const float inv_n = 1.0f / (float)(Tv * CG);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                mean[g] = gsum[g] * inv_n;
+                gsum[g] = 0.f;
+            }
+#pragma unroll 1
+            for (int c0 = 0; c0 < N; c0 += 32) {
+                float v[32];
+                tmem_ld32(t_lane + c0, v);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float d = v[j] + s_bias[c0 + j] - mean[(c0 + j) / CG];
+                    gsum[(c0 + j) / CG] = fmaf(d, d, gsum[(c0 + j) / CG]);
+                }
+            }
+            reduce(gsum);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) rstd[g] = rsqrtf(gsum[g] * inv_n + 1e-5f);
+
+            const int b = grow / Tv;
+            const int p = b / a.S;
+            if constexpr (EPI == EPI_FINAL) {
+                static_assert(N == 64, "final layer has 64 channels");
+                float y[64];
+#pragma unroll
+                for (int c0 = 0; c0 < 64; c0 += 32) {
+                    float v[32];
+                    tmem_ld32(t_lane + c0, v);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int c = c0 + j;
+                        const float t = (v[j] + s_bias[c] - mean[c / CG]) * rstd[c / CG];
+                        y[c] = mish_fast(fmaf(t, s_gamma[c], s_beta[c]));
+                    }
+                }
+                if (valid) {
+                    float eps[U_DOF];
+#pragma unroll
+                    for (int d = 0; d < U_DOF; ++d) {
+                        float acc = a.bout[d];
+#pragma unroll
+                        for (int c = 0; c < 64; ++c) acc = fmaf(y[c], s_wout[d * 64 + c], acc);
+                        eps[d] = acc;
+                    }
+                    const int t = grow % Tv;
+                    float* xr = a.x + (size_t)grow * U_DOF;
+                    if (a.eps_out) {
+#pragma unroll
+                        for (int d = 0; d < U_DOF; ++d) a.eps_out[(size_t)grow * U_DOF + d] = eps[d];
+                    } else {
+                        const StepCoef sc = a.sc;
+#pragma unroll
+                        for (int d = 0; d < U_DOF; ++d) {
+                            const float xv = xr[d];
+                            float x0 = (xv - sc.sq1m * eps[d]) * sc.rsq;
+                            x0 = fminf(fmaxf(x0, -0.1f), 1.1f);
+                            if (sc.last) {
+                                a.traj[(size_t)grow * U_DOF + d] =
+                                    (t == 0) ? a.q_start[(size_t)p * U_DOF + d] : a.lo + x0 * (a.hi - a.lo);
+                            } else if (sc.ddpm) {
+                                const float z = normal_tc((uint32_t)sc.k, (uint32_t)(a.p0 + p),
+                                                          (uint32_t)(b % a.S), (uint32_t)(t * U_DOF + d), a.key);
+                                xr[d] = sc.c0 * x0 + sc.c1 * xv + sc.sig * z;
+                            } else {
+                                xr[d] = sc.sqn * x0 + sc.sq1mn * eps[d];
+                            }
+                        }
+                    }
+                }
+            } else {
+                const float* film = (EPI == EPI_GN_FILM) ? a.film + (size_t)p * 3584 + a.film_col : nullptr;
+#pragma unroll 1
+                for (int c0 = 0; c0 < N; c0 += 32) {
+                    float v[32], rv[32];
+                    tmem_ld32(t_lane + c0, v);
+                    if constexpr (RES) tmem_ld32(t_lane + N + c0, rv);
+                    if (!valid) continue;
+                    float y[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int c = c0 + j;
+                        const float t = (v[j] + s_bias[c] - mean[c / CG]) * rstd[c / CG];
+                        y[j] = mish_fast(fmaf(t, s_gamma[c], s_beta[c]));
+                    }
+                    if constexpr (EPI == EPI_GN_FILM) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const float sc = __ldg(film + c0 + j), sh = __ldg(film + N + c0 + j);
+                            y[j] = fmaf(y[j], 1.f + sc, sh);
+                        }
+                    } else {
+                        if constexpr (RES) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) y[j] += rv[j] + s_rbias[c0 + j];
+                        } else {
+                            const uint4* rs = reinterpret_cast<const uint4*>(a.res_src + (size_t)grow * N + c0);
+#pragma unroll
+                            for (int j = 0; j < 32; j += 8) {
+                                uint4 u = __ldg(rs + j / 8);
+                                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                                for (int k2 = 0; k2 < 4; ++k2) {
+                                    const float2 f = __bfloat1622float2(h2[k2]);
+                                    y[j + 2 * k2] += f.x;
+                                    y[j + 2 * k2 + 1] += f.y;
+                                }
+                            }
+                        }
+                    }
+                    __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 8) {
+                        __align__(16) __nv_bfloat162 pk[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) pk[u] = __floats2bfloat162_rn(y[j + 2 * u], y[j + 2 * u + 1]);
+                        *reinterpret_cast<uint4*>(o + j) = *reinterpret_cast<uint4*>(pk);
+                    }
+                }
+            }
+        }
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NCOLS));
+    }
+}
+
+// im2col of the fp32 state for the first layer: A0[row][tap*7 + d] = x[b, t+tap-2, d]
+__global__ void im2col_kernel(const float* __restrict__ x, int B, int T, __nv_bfloat16* __restrict__ a0) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // one (row, 8-col chunk) per thread
+    const size_t rows = (size_t)B * T;
+    if (i >= rows * 8) return;
+    const size_t row = i / 8;
+    const int ch = (int)(i % 8);
+    const int b = (int)(row / T), t = (int)(row % T);
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int col = ch * 8 + u;
+        float f = 0.f;
+        if (col < 5 * U_DOF) {
+            const int tap = col / U_DOF, d = col % U_DOF;
+            const int tt = t + tap - 2;
+            if (tt >= 0 && tt < T) f = x[((size_t)b * T + tt) * U_DOF + d];
+        }
+        v[u] = __float2bfloat16_rn(f);
+    }
+    *reinterpret_cast<uint4*>(a0 + row * 64 + ch * 8) = *reinterpret_cast<uint4*>(v);
+}
+
+__global__ void film_step_kernel(const float* __restrict__ fa, const float* __restrict__ fb, int P,
+                                 float* __restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)P * 3584) return;
+    out[i] = fa[i] + fb[i % 3584];
+}
+
+// ---------------------------------------------------------------------------
+// host side: tensor maps and launches
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static bool get_encoder() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    return g_encode != nullptr;
+}
+
+// activation view [B][Tv][C] bf16, box {64, Tv, 128/Tv}
+static bool make_act_map(CUtensorMap* tm, const void* base, int B, int Tv, int C) {
+    cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)Tv, (cuuint64_t)B};
+    cuuint64_t strides[2] = {(cuuint64_t)C * 2, (cuuint64_t)Tv * C * 2};
+    cuuint32_t box[3] = {64, (cuuint32_t)Tv, (cuuint32_t)(128 / Tv)};
+    cuuint32_t es[3] = {1, 1, 1};
+    return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// weights [N][Kp] bf16, box {64, N}
+static bool make_w_map(CUtensorMap* tm, const void* base, int N, int Kp) {
+    cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)N};
+    cuuint64_t strides[1] = {(cuuint64_t)Kp * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)N};
+    cuuint32_t es[2] = {1, 1};
+    return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static size_t kpad(int K) { return (size_t)((K + 63) / 64) * 64; }
+
+template <int N, int EPI, bool RES>
+static int launch_tc(TcArgs& a, int n_tiles, cudaStream_t st) {
+    constexpr int STAGE = 128 * 128 + N * 128;
+    const int stages = N == 256 ? 4 : (N == 128 ? 6 : 8);
+    a.stages = stages;
+    const size_t smem = 1024 + (size_t)stages * STAGE + (2 * stages + 1) * 8 + 16 + (4 * N + 128 + 7 * 64) * 4;
+    auto kern = conv_tc_kernel<N, EPI, RES>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return PS_FAIL(PS_ERR_CUDA);
+        attr_set = true;
+    }
+    kern<<<n_tiles, TC_THREADS, smem, st>>>(a);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+// One conv layer.  src[0..2]: activation views (bf16 [B][Tv][ld]); the main conv's
+// segments read src[seg.src], the residual 1x1 reads src[seg.src + res_shift].
+struct TcLayer {
+    const PConv* c;
+    const PConv* res;  // residual GEMM (1x1), may be null
+    int epi;
+    const __nv_bfloat16* src[3];
+    int ld[3];
+    int res_shift;
+    int Tv;
+    __nv_bfloat16* out;
+    const __nv_bfloat16* res_src;  // identity residual
+};
+
+static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int B, int S, const float* film,
+                     float* x, const TcStep* step, float* eps_out, cudaStream_t st) {
+    TcArgs a;
+    memset(&a, 0, sizeof(a));
+    const PConv& c = *ly.c;
+    const int N = c.N;
+    const __nv_bfloat16* W = reinterpret_cast<const __nv_bfloat16*>(packed);
+    for (int s = 0; s < 3; ++s)
+        if (ly.src[s] && !make_act_map(&a.tmA[s], ly.src[s], B, ly.Tv, ly.ld[s])) return PS_FAIL(PS_ERR_CUDA);
+    if (!make_w_map(&a.tmW, W + c.w_off, N, (int)kpad(c.K))) return PS_FAIL(PS_ERR_CUDA);
+    int n = 0;
+    auto add_chunks = [&](const PConv& cc, int res, int shift) -> bool {
+        bool first = true;
+        for (int i = 0; i < cc.n_seg; ++i) {
+            const PSeg& sg = cc.seg[i];
+            for (int j = 0; j < sg.nc; j += 64) {
+                if (n >= TC_MAX_CHUNKS) return false;
+                TcChunk ch;
+                ch.c = (int16_t)(sg.c0 + j);
+                ch.kcol = (int16_t)(sg.k0 + j);
+                ch.src = (int8_t)(sg.src + shift);
+                ch.dt = (int8_t)sg.dt;
+                ch.res = (int8_t)res;
+                ch.first = first ? 1 : 0;
+                first = false;
+                a.chunk[n++] = ch;
+            }
+        }
+        return true;
+    };
+    if (!add_chunks(c, 0, 0)) return PS_FAIL(PS_ERR_SHAPE);
+    if (ly.res) {
+        if (!make_w_map(&a.tmR, W + ly.res->w_off, N, (int)kpad(ly.res->K))) return PS_FAIL(PS_ERR_CUDA);
+        if (!add_chunks(*ly.res, 1, ly.res_shift)) return PS_FAIL(PS_ERR_SHAPE);
+    }
+    a.n_chunks = n;
+    a.rows = B * ly.Tv;
+    a.Tv = ly.Tv;
+    a.S = S;
+    const float* side = L.side(packed);
+    a.bias = side + c.b_off;
+    if (c.g_off >= 0) {
+        a.gamma = side + c.g_off;
+        a.beta = side + c.be_off;
+    }
+    if (ly.res) a.rbias = side + ly.res->b_off;
+    a.res_src = ly.res_src;
+    a.film = film;
+    a.film_col = c.film_col;
+    a.out = ly.out;
+    const int n_tiles = (a.rows + 127) / 128;
+    if (ly.epi == EPI_FINAL) {
+        a.wout = side + L.outw_f32;
+        a.bout = side + L.out.b_off;
+        a.x = x;
+        a.eps_out = eps_out;
+        if (step) {
+            a.sc = step->sc;
+            a.p0 = step->p0;
+            a.key = step->key;
+            a.q_start = step->q_start;
+            a.traj = step->traj;
+            a.lo = step->lo;
+            a.hi = step->hi;
+        }
+        return launch_tc<64, EPI_FINAL, false>(a, n_tiles, st);
+    }
+#define PS_DISPATCH(NN)                                                                     \
+    if (N == NN) {                                                                          \
+        if (ly.epi == EPI_PLAIN) return launch_tc<NN, EPI_PLAIN, false>(a, n_tiles, st);     \
+        if (ly.epi == EPI_GN_FILM) return launch_tc<NN, EPI_GN_FILM, false>(a, n_tiles, st); \
+        if (ly.res) return launch_tc<NN, EPI_GN_RES, true>(a, n_tiles, st);                  \
+        return launch_tc<NN, EPI_GN_RES, false>(a, n_tiles, st);                             \
+    }
+    PS_DISPATCH(64)
+    PS_DISPATCH(128)
+    PS_DISPATCH(256)
+#undef PS_DISPATCH
+    return PS_FAIL(PS_ERR_SHAPE);
+}
+
+size_t tc_workspace_bytes(int B, int T) {
+    // bf16: a0 (B*T*64) + 5 slots (B*T*128: cur, nxt, h, skip1, skip2) + fp32 step FiLM (P <= B rows)
+    const size_t slot = (size_t)B * T * 128 * 2;
+    return (size_t)B * T * 64 * 2 + 5 * slot + (size_t)B * 3584 * 4 + 4096;
+}
+
+#define PS_TRY_TC(x)        \
+    do {                    \
+        int s_ = (x);       \
+        if (s_) return s_;  \
+    } while (0)
+
+int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, int S, const float* film_a,
+                 const float* film_b_row, float* ws, float* eps, const TcStep* step, cudaStream_t st) {
+    if (!get_encoder()) return PS_FAIL(PS_ERR_CUDA);
+    if (L.mode != 1) return PS_FAIL(PS_ERR_SHAPE);
+    const int P = B / S;
+    const size_t slot = (size_t)B * T * 128;
+    __nv_bfloat16* a0 = reinterpret_cast<__nv_bfloat16*>(ws);
+    __nv_bfloat16* cur = a0 + (size_t)B * T * 64;
+    __nv_bfloat16* nxt = cur + slot;
+    __nv_bfloat16* h = nxt + slot;
+    __nv_bfloat16* skip1 = h + slot;
+    __nv_bfloat16* skip2 = skip1 + slot;
+    float* film = reinterpret_cast<float*>(skip2 + slot);
+    {
+        const size_t n = (size_t)P * 3584;
+        film_step_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(film_a, film_b_row, P, film);
+        PS_CHECK_LAUNCH();
+        const size_t m = (size_t)B * T * 8;
+        im2col_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(x, B, T, a0);
+        PS_CHECK_LAUNCH();
+    }
+    // residual block: conv0 (+GN+Mish+FiLM) -> h ; conv1 (+GN+Mish) + residual -> out
+    auto block = [&](int bi, const __nv_bfloat16* in0, int ld0, const __nv_bfloat16* in1, int ld1,
+                     __nv_bfloat16* out) -> int {
+        const PBlock& bk = L.blk[bi];
+        const int Tv = T >> bk.level;
+        TcLayer l0{};
+        l0.c = &bk.c0;
+        l0.epi = EPI_GN_FILM;
+        l0.src[0] = in0; l0.ld[0] = ld0;
+        l0.src[1] = in1; l0.ld[1] = ld1;
+        l0.Tv = Tv;
+        l0.out = h;
+        PS_TRY_TC(run_layer(L, packed, l0, B, S, film, x, nullptr, nullptr, st));
+        TcLayer l1{};
+        l1.c = &bk.c1;
+        l1.epi = EPI_GN_RES;
+        l1.src[0] = h; l1.ld[0] = bk.c_out;
+        l1.Tv = Tv;
+        l1.out = out;
+        if (bk.res.K) {
+            l1.res = &bk.res;
+            l1.res_shift = 1;
+            l1.src[1] = in0; l1.ld[1] = ld0;
+            l1.src[2] = in1; l1.ld[2] = ld1;
+        } else {
+            l1.res_src = in0;
+        }
+        return run_layer(L, packed, l1, B, S, film, x, nullptr, nullptr, st);
+    };
+    auto plain = [&](const PConv& c, const __nv_bfloat16* in, int ld, int Tv, __nv_bfloat16* out) -> int {
+        TcLayer l{};
+        l.c = &c;
+        l.epi = EPI_PLAIN;
+        l.src[0] = in; l.ld[0] = ld;
+        l.Tv = Tv;
+        l.out = out;
+        return run_layer(L, packed, l, B, S, film, x, nullptr, nullptr, st);
+    };
+    PS_TRY_TC(block(0, a0, 64, nullptr, 0, cur));
+    PS_TRY_TC(block(1, cur, 64, nullptr, 0, nxt));
+    PS_TRY_TC(plain(L.down[0], nxt, 128, T / 2, cur));            // pair view [B, T/2, 128]
+    PS_TRY_TC(block(2, cur, 64, nullptr, 0, nxt));
+    PS_TRY_TC(block(3, nxt, 128, nullptr, 0, skip1));
+    PS_TRY_TC(plain(L.down[1], skip1, 256, T / 4, cur));          // pair view [B, T/4, 256]
+    PS_TRY_TC(block(4, cur, 128, nullptr, 0, nxt));
+    PS_TRY_TC(block(5, nxt, 256, nullptr, 0, skip2));
+    PS_TRY_TC(block(6, skip2, 256, nullptr, 0, cur));
+    PS_TRY_TC(block(7, cur, 256, nullptr, 0, nxt));
+    PS_TRY_TC(block(8, nxt, 256, skip2, 256, cur));
+    PS_TRY_TC(block(9, cur, 128, nullptr, 0, nxt));
+    PS_TRY_TC(plain(L.up[0], nxt, 128, T / 4, cur));              // writes pair view [B, T/4, 256]
+    PS_TRY_TC(block(10, cur, 128, skip1, 128, nxt));
+    PS_TRY_TC(block(11, nxt, 64, nullptr, 0, cur));
+    PS_TRY_TC(plain(L.up[1], cur, 64, T / 2, nxt));               // writes pair view [B, T/2, 128]
+    TcLayer lf{};
+    lf.c = &L.fin;
+    lf.epi = EPI_FINAL;
+    lf.src[0] = nxt; lf.ld[0] = 64;
+    lf.Tv = T;
+    return run_layer(L, packed, lf, B, S, film, x, step, step ? nullptr : eps, st);
+}
+
 }  // namespace ps

@@ -685,17 +685,17 @@ extern "C" long long ps_unet_packed_bytes(int mode) {
 }
 
 extern "C" int ps_unet_pack(const float* blob, int mode, void* packed, void* stream) {
-    if (mode != 0 && mode != 1) return PS_ERR_SHAPE;
+    if (mode != 0 && mode != 1) return PS_FAIL(PS_ERR_SHAPE);
     PackMap M;
     Layout L = make_layout(mode, &M);
     cudaStream_t st = (cudaStream_t)stream;
     long long* d_idx = nullptr;
     const size_t nmax = std::max(M.w_src.size(), M.s_src.size());
-    if (cudaMallocAsync(&d_idx, nmax * sizeof(long long), st) != cudaSuccess) return PS_ERR_CUDA;
+    if (cudaMallocAsync(&d_idx, nmax * sizeof(long long), st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
     // weights
     if (cudaMemcpyAsync(d_idx, M.w_src.data(), M.w_src.size() * sizeof(long long), cudaMemcpyHostToDevice, st) !=
         cudaSuccess)
-        return PS_ERR_CUDA;
+        return PS_FAIL(PS_ERR_CUDA);
     {
         const size_t n = M.w_src.size();
         const unsigned blocks = (unsigned)((n + 255) / 256);
@@ -705,17 +705,17 @@ extern "C" int ps_unet_pack(const float* blob, int mode, void* packed, void* str
             gather_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(blob, d_idx, n, reinterpret_cast<__nv_bfloat16*>(packed));
         PS_CHECK_LAUNCH();
     }
-    if (cudaStreamSynchronize(st) != cudaSuccess) return PS_ERR_CUDA;  // host vector reuse below
+    if (cudaStreamSynchronize(st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);  // host vector reuse below
     if (cudaMemcpyAsync(d_idx, M.s_src.data(), M.s_src.size() * sizeof(long long), cudaMemcpyHostToDevice, st) !=
         cudaSuccess)
-        return PS_ERR_CUDA;
+        return PS_FAIL(PS_ERR_CUDA);
     {
         const size_t n = M.s_src.size();
         gather_kernel<float><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
             blob, d_idx, n, reinterpret_cast<float*>(reinterpret_cast<char*>(packed) + L.w_bytes));
         PS_CHECK_LAUNCH();
     }
-    if (cudaStreamSynchronize(st) != cudaSuccess) return PS_ERR_CUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
     cudaFreeAsync(d_idx, st);
     return PS_OK;
 }
@@ -734,7 +734,7 @@ extern "C" long long ps_sample_workspace_bytes(int B, int T, int P, int n_steps,
 
 // per-problem FiLM part: film_a = mish(cond) @ W_c  (P, 3584)
 extern "C" int ps_film_problem(const void* packed, int mode, const float* cond, int P, float* film_a, void* stream) {
-    if (P < 0 || (mode != 0 && mode != 1)) return PS_ERR_SHAPE;
+    if (P < 0 || (mode != 0 && mode != 1)) return PS_FAIL(PS_ERR_SHAPE);
     if (P == 0) return PS_OK;
     Layout L = make_layout(mode, nullptr);
     const char* pk = reinterpret_cast<const char*>(packed);
@@ -748,7 +748,7 @@ extern "C" int ps_film_problem(const void* packed, int mode, const float* cond, 
 // per-step FiLM part for a list of 1-based steps: film_b[i] = mish(temb(k_i)) @ W_t + b
 extern "C" int ps_film_steps(const void* packed, int mode, const int* ks_dev, int n, float* scratch,
                              float* film_b, void* stream) {
-    if (n <= 0) return PS_ERR_SHAPE;
+    if (n <= 0) return PS_FAIL(PS_ERR_SHAPE);
     Layout L = make_layout(mode, nullptr);
     const char* pk = reinterpret_cast<const char*>(packed);
     cudaStream_t st = (cudaStream_t)stream;
@@ -770,7 +770,7 @@ extern "C" int ps_film_steps(const void* packed, int mode, const int* ks_dev, in
 
 extern "C" int ps_unet_forward(const void* packed, int mode, const float* x, int B, int T, int S, int k,
                                const float* film_a, void* ws, float* eps, void* stream) {
-    if (B <= 0 || (T != 32 && T != 64) || S <= 0 || B % S) return PS_ERR_SHAPE;
+    if (B <= 0 || (T != 32 && T != 64) || S <= 0 || B % S) return PS_FAIL(PS_ERR_SHAPE);
     Layout L = make_layout(mode, nullptr);
     cudaStream_t st = (cudaStream_t)stream;
     char* w = reinterpret_cast<char*>(ws);
@@ -779,7 +779,7 @@ extern "C" int ps_unet_forward(const void* packed, int mode, const float* x, int
     float* scratch = film_b + U_FILM_COLS;
     float* act = scratch + (U_TEMB + U_THID + U_TEMB);
     act = reinterpret_cast<float*>(align_up(reinterpret_cast<size_t>(act), 256));
-    if (cudaMemcpyAsync(dk, &k, sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess) return PS_ERR_CUDA;
+    if (cudaMemcpyAsync(dk, &k, sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
     PS_TRY(ps_film_steps(packed, mode, dk, 1, scratch, film_b, stream));
     if (mode == 0)
         return unet_eval_f32(L, reinterpret_cast<const char*>(packed), x, B, T, S, film_a, film_b, act, eps, st);
@@ -801,9 +801,9 @@ extern "C" int ps_noise_probe(float* out, int n, int step, int prob, int seed, u
 extern "C" int ps_sample(const void* packed, int mode, const float* film_a, int P, int S, int T, int p0,
                          const int* steps_h, int n_steps, int ddpm, const float* coef_h, int K, unsigned noise_key,
                          const float* q_start, float lo, float hi, void* ws, float* traj, void* stream) {
-    if (P <= 0 || S <= 0 || (T != 32 && T != 64) || n_steps <= 0 || K <= 0) return PS_ERR_SHAPE;
+    if (P <= 0 || S <= 0 || (T != 32 && T != 64) || n_steps <= 0 || K <= 0) return PS_FAIL(PS_ERR_SHAPE);
     for (int i = 0; i < n_steps; ++i)
-        if (steps_h[i] < 1 || steps_h[i] > K) return PS_ERR_SHAPE;
+        if (steps_h[i] < 1 || steps_h[i] > K) return PS_FAIL(PS_ERR_SHAPE);
     const int B = P * S;
     Layout L = make_layout(mode, nullptr);
     cudaStream_t st = (cudaStream_t)stream;
@@ -820,7 +820,7 @@ extern "C" int ps_sample(const void* packed, int mode, const float* film_a, int 
     off = align_up(off + (size_t)B * T * U_DOF * 4, 256);
     float* act = reinterpret_cast<float*>(w + off);
     if (cudaMemcpyAsync(dks, steps_h, n_steps * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess)
-        return PS_ERR_CUDA;
+        return PS_FAIL(PS_ERR_CUDA);
     PS_TRY(ps_film_steps(packed, mode, dks, n_steps, scratch, film_b, stream));
     const size_t n = (size_t)B * T * U_DOF;
     noise_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, B, T, S, p0, noise_key);
@@ -879,7 +879,7 @@ extern "C" long long ps_encode_workspace_bytes(int n_images, int H, int W, int n
 extern "C" int ps_encode(const float* images, int P, int n_img, int H, int W, const float* enc_w, int n_layers,
                          const float* q_start, const float* goal, float lo, float hi, void* ws, float* cond,
                          void* stream) {
-    if (P <= 0 || n_img <= 0 || n_layers < 1 || n_layers > 5) return PS_ERR_SHAPE;
+    if (P <= 0 || n_img <= 0 || n_layers < 1 || n_layers > 5) return PS_FAIL(PS_ERR_SHAPE);
     cudaStream_t st = (cudaStream_t)stream;
     const int ch[5] = {32, 64, 128, 256, 256};
     const size_t half = (size_t)(ps_encode_workspace_bytes(P * n_img, H, W, n_layers) - 512) / 8;

@@ -106,9 +106,21 @@ class TestSample:
         cond = _cond(P, 10)
         q0 = synth.make_problems(P, seed=11).q_start
         steps = spec.strided_steps(100, 10)
-        traj = sampler.sample(sampler.film(cond), q0, S, steps=steps).cpu().numpy()
+        fa = sampler.film(cond)
+        traj = sampler.sample(fa, q0, S, steps=steps).cpu().numpy()
         want = un.sample(params, ARCH, cond, q0, S, steps=steps)
-        assert np.abs(traj - want).max() < 1e-4
+        # The deterministic strided update carries the first step's x0 error forward
+        # undamped, and the pinned squared-cosine schedule amplifies it by
+        # 1/sqrt(abar_100) ~ 2000.  Bound: 1e-4 rad x that
+        # conditioning, relative to the 1e-6 fp32 noise-prediction error -> 1e-2 rad.
+        rsq = spec.sampler_tables(spec.cosine_betas()).rsq
+        assert rsq[100] > 1000
+        assert np.abs(traj - want).max() < 1e-2
+        # every noise prediction on the strided path itself stays within 1e-4
+        x = np.random.default_rng(1).standard_normal((P * S, 32, 7)).astype(np.float32)
+        for k in steps:
+            eps = sampler.predict_noise(x, int(k), fa, S).cpu().numpy()
+            assert np.abs(eps - un.unet_forward(params, ARCH, x, int(k), cond, S)).max() < 1e-4
 
     def test_shard_invariance(self, sampler):
         # problems [0,4) at once == [0,2) + [2,4) with p0 offsets (noise keyed globally)
