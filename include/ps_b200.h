@@ -29,6 +29,9 @@ extern "C" {
 /* library identification: returns a static string, e.g. "ps_b200 sm_100a" */
 const char* ps_version(void);
 
+/* number of kernels this library has launched so far (instrumentation) */
+long long ps_launch_count(void);
+
 /* ====================== BASELINE profile (3-D, fp32) ======================= */
 
 /* ESDF construction: analytic signed distance to axis-aligned boxes, sampled on

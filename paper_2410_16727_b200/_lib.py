@@ -21,6 +21,7 @@ _c_int, _c_ll, _c_f, _vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_float, ctyp
 # name -> argtypes ; every function returns int (status) unless listed in _RESTYPE
 _SIGS = {
     "ps_version": [],
+    "ps_launch_count": [],
     "ps_esdf_build_boxes": [_vp, _c_int, _c_int, _vp, _vp, _c_f, _c_f, _vp, _vp],
     "ps_bl_cost": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,
                    _c_int, _vp, _vp, _vp, _vp, _vp],
@@ -42,7 +43,7 @@ _SIGS = {
                   ctypes.c_uint, _vp, _c_f, _c_f, _vp, _vp, _vp],
     "ps_noise_probe": [_vp, _c_int, _c_int, _c_int, _c_int, ctypes.c_uint, _vp],
 }
-_RESTYPE = {"ps_version": ctypes.c_char_p, "ps_unet_param_count": _c_ll,
+_RESTYPE = {"ps_version": ctypes.c_char_p, "ps_launch_count": _c_ll, "ps_unet_param_count": _c_ll,
             "ps_unet_param_offset": _c_ll, "ps_unet_packed_bytes": _c_ll,
             "ps_encode_workspace_bytes": _c_ll, "ps_sample_workspace_bytes": _c_ll}
 

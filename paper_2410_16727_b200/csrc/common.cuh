@@ -18,8 +18,17 @@ inline int ps_fail(int code, const char* file, int line) {
 }
 #define PS_FAIL(code) ps_fail((code), __FILE__, __LINE__)
 
+#include <atomic>
+// Every kernel launch site goes through PS_CHECK_LAUNCH, which counts it
+// (ps_launch_count() in the C-ABI; bench.py reports launches per step).
+inline std::atomic<long long>& ps_launch_counter() {
+    static std::atomic<long long> c{0};
+    return c;
+}
+
 #define PS_CHECK_LAUNCH()                                                   \
     do {                                                                    \
+        ps_launch_counter().fetch_add(1, std::memory_order_relaxed);        \
         cudaError_t e_ = cudaGetLastError();                                \
         if (e_ != cudaSuccess) {                                            \
             if (std::getenv("PS_DEBUG"))                                    \

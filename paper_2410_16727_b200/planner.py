@@ -1,0 +1,122 @@
+"""Batched BASELINE-profile planner: the seeding hot path end to end on one GPU.
+
+plan_batch() is the batched counterpart of planseed's plan_diffusion
+(pipeline.py:172-209) for P problems at once:
+
+  ESDF build (per-problem boxes)  ~ build_planner_esdf     pipeline.py:115-132
+  encode (depth images -> cond)   ~ encode_condition       diffusion.py:260-269
+  sample (DDPM / strided DDIM)    ~ ddim_sample            diffusion.py:559-569
+  refine (fixed-step) + flags     ~ optimize + planner_success  trajopt.py:140-177,
+                                                                 pipeline.py:139-157
+  select                          ~ select_best            pipeline.py:160-165
+
+All device buffers are preallocated for the maximum batch (no allocation in the
+hot path); inputs can be device tensors (device-resident mode) or host arrays
+(end-to-end mode: host->device copies and the result read-back are part of the call).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, bl, spec
+from .sampler import SeedSampler
+
+
+@dataclass
+class PlanBatchResult:
+    trajectories: object    # (P*S, T, 7) refined, physical radians
+    seeds: object           # (P*S, T, 7) sampler output
+    cost: object            # (P*S,)
+    feasible: object        # (P*S,) bool/uint8
+    clamped: object         # (P*S,)
+    best_index: object      # (P,) int32
+
+
+class BLPlanner:
+    def __init__(self, params: dict, enc: spec.EncoderArch = spec.ENCODER_CFG3,
+                 arch: spec.UNetArch = spec.UNetArch(), mode: int = 1, S: int = 32,
+                 T: int = spec.T_DEFAULT, robot: spec.DHRobot | None = None,
+                 grid: spec.GridSpec = spec.GridSpec(), cost: spec.BLCost = spec.BLCost(),
+                 steps=None, max_problems: int = 1024, n_images: int = 2,
+                 image_shape=(240, 320), n_boxes: int = spec.N_BOXES):
+        torch = _lib.require_cuda()
+        self.sampler = SeedSampler(params, enc, arch, mode=mode)
+        self.S, self.T = int(S), int(T)
+        self.robot = robot or spec.make_bl_robot()
+        self.grid, self.cost = grid, cost
+        self.steps = steps
+        self.Pmax = int(max_problems)
+        B = self.Pmax * self.S
+        dev = "cuda"
+        self.esdf = torch.empty((self.Pmax,) + tuple(grid.n), dtype=torch.float32, device=dev)
+        self.seeds = torch.empty((B, self.T, 7), dtype=torch.float32, device=dev)
+        self.out = (torch.empty((B, self.T, 7), dtype=torch.float32, device=dev),
+                    torch.empty(B, dtype=torch.float32, device=dev),
+                    torch.empty(B, dtype=torch.uint8, device=dev),
+                    torch.empty(B, dtype=torch.uint8, device=dev))
+        self.best = torch.empty(self.Pmax, dtype=torch.int32, device=dev)
+        # device copies of host inputs for the end-to-end path
+        self.d_images = torch.empty((self.Pmax, n_images) + tuple(image_shape), dtype=torch.float32,
+                                    device=dev)
+        self.d_q = torch.empty((self.Pmax, 7), dtype=torch.float32, device=dev)
+        self.d_goal = torch.empty((self.Pmax, 7), dtype=torch.float32, device=dev)
+        self.d_boxes = torch.empty((self.Pmax, n_boxes, 6), dtype=torch.float32, device=dev)
+        self.timing = {}
+
+    # ------------------------------------------------------------------ device
+    def plan_batch_device(self, images, q_start, goal, boxes, p0: int = 0, events=None):
+        """All inputs already on the device.  Returns PlanBatchResult of device tensors.
+        `events` (optional dict) receives CUDA events bracketing the sampler."""
+        torch = _lib.require_cuda()
+        P = int(q_start.shape[0])
+        if P > self.Pmax:
+            raise ValueError("batch larger than max_problems")
+        B = P * self.S
+        esdf = self.esdf[:P]
+        self._esdf_build(boxes, esdf)
+        cond = self.sampler.encode(images, q_start, goal)
+        fa = self.sampler.film(cond)
+        if events is not None:
+            events["sample_start"].record()
+        seeds = self.sampler.sample(fa, q_start, self.S, self.T, p0=p0, steps=self.steps,
+                                    out=self.seeds[:B])
+        if events is not None:
+            events["sample_end"].record()
+        out = tuple(o[:B] for o in self.out)
+        bl.refine(seeds, esdf, self.S, self.robot, self.grid, self.cost, out=out)
+        best = bl.select(out[1], out[2], self.S, out=self.best[:P])
+        return PlanBatchResult(out[0], seeds, out[1], out[2], out[3], best)
+
+    def _esdf_build(self, boxes, out):
+        n = np.array(self.grid.n, dtype=np.int32)
+        o = np.array(self.grid.origin, dtype=np.float32)
+        st = _lib.lib().ps_esdf_build_boxes(_lib.ptr(boxes), int(boxes.shape[0]), int(boxes.shape[1]),
+                                            _lib.hptr(n), _lib.hptr(o), self.grid.h, self.grid.cap,
+                                            _lib.ptr(out), _lib.stream_handle())
+        _lib.check(st, "esdf_build")
+
+    # ------------------------------------------------------------------ host
+    def plan_batch(self, images, q_start, goal, boxes, p0: int = 0):
+        """End-to-end call from host (ideally pinned) arrays: H2D copies, the device
+        pipeline, and a D2H read of trajectories, costs, flags and best indices."""
+        torch = _lib.require_cuda()
+        P = int(q_start.shape[0])
+        d_im, d_q, d_g, d_b = (self.d_images[:P], self.d_q[:P], self.d_goal[:P], self.d_boxes[:P])
+        for dst, src in ((d_im, images), (d_q, q_start), (d_g, goal), (d_b, boxes)):
+            dst.copy_(torch.as_tensor(src), non_blocking=True)
+        r = self.plan_batch_device(d_im, d_q, d_g, d_b, p0=p0)
+        host = PlanBatchResult(r.trajectories.to("cpu", non_blocking=True), None,
+                               r.cost.to("cpu", non_blocking=True),
+                               r.feasible.to("cpu", non_blocking=True),
+                               r.clamped.to("cpu", non_blocking=True),
+                               r.best_index.to("cpu", non_blocking=True))
+        torch.cuda.current_stream().synchronize()
+        return host
+
+    @staticmethod
+    def result_bytes(P: int, S: int, T: int) -> int:
+        B = P * S
+        return B * T * 7 * 4 + B * 4 + B + B + P * 4
