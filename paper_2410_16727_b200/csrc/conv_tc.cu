@@ -36,6 +36,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -175,45 +178,74 @@ __device__ __forceinline__ float normal_tc(uint32_t step, uint32_t prob, uint32_
     return (comp & 1u) ? rad * sinf(ang) : rad * cosf(ang);
 }
 
-template <int N>
-__host__ __device__ constexpr int tmem_cols(bool res) {
-    return (res ? 2 * N : N) <= 32 ? 32 : (res ? 2 * N : N) <= 64 ? 64 : (res ? 2 * N : N) <= 128 ? 128
-                                                                        : (res ? 2 * N : N) <= 256 ? 256 : 512;
+// columns of one accumulator buffer (main [+ residual])
+template <int N, bool RES>
+__host__ __device__ constexpr int acc_cols() { return RES ? 2 * N : N; }
+// double-buffer the accumulators when two fit in the 512 TMEM columns
+template <int N, bool RES>
+__host__ __device__ constexpr int n_accbuf() { return 2 * acc_cols<N, RES>() <= 512 ? 2 : 1; }
+template <int N, bool RES>
+__host__ __device__ constexpr int tmem_alloc_cols() {
+    return acc_cols<N, RES>() * n_accbuf<N, RES>() <= 32    ? 32
+           : acc_cols<N, RES>() * n_accbuf<N, RES>() <= 64  ? 64
+           : acc_cols<N, RES>() * n_accbuf<N, RES>() <= 128 ? 128
+           : acc_cols<N, RES>() * n_accbuf<N, RES>() <= 256 ? 256
+                                                            : 512;
 }
 
-constexpr int TC_THREADS = 192;
+constexpr int TC_EPI_WG = 2;                         // epilogue warpgroups
+constexpr int TC_THREADS = 64 + 128 * TC_EPI_WG;     // producer warp, MMA warp, epilogue
 
+template <int NV>
+__device__ __forceinline__ float sel(const float (&a)[NV], int i) {
+    float r = a[0];
+#pragma unroll
+    for (int k = 1; k < NV; ++k) r = (i == k) ? a[k] : r;
+    return r;
+}
+
+// Persistent: CTA c handles tiles c, c + gridDim.x, ...  The producer streams every
+// tile's K chunks through the smem ring; the MMA warp fills accumulator buffer j % NBUF
+// for local tile j; epilogue warpgroup j % 2 drains it and releases the buffer, so the
+// epilogue of one tile overlaps the MMAs (and loads) of the next.
 template <int N, int EPI, bool RES>
 __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_constant__ TcArgs a) {
     constexpr int A_BYTES = 128 * 128;
     constexpr int B_BYTES = N * 128;
     constexpr int STAGE = A_BYTES + B_BYTES;
-    constexpr int NCOLS = tmem_cols<N>(RES);
+    constexpr int ACC = acc_cols<N, RES>();
+    constexpr int NBUF = n_accbuf<N, RES>();
+    constexpr int NCOLS = tmem_alloc_cols<N, RES>();
     constexpr int CG = N / 8;  // channels per group
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     const int stages = a.stages;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * STAGE);
     uint64_t* empty = full + stages;
-    uint64_t* tfull = empty + stages;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tfull + 1);
-    float* sv = reinterpret_cast<float*>(tmem_holder + 4);  // per-channel vectors
+    uint64_t* tfull = empty + stages;   // [2]
+    uint64_t* tempty = tfull + 2;       // [2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* sv = reinterpret_cast<float*>(tmem_holder + 4);
     float* s_bias = sv;
     float* s_gamma = sv + N;
     float* s_beta = sv + 2 * N;
     float* s_rbias = sv + 3 * N;
-    float* s_red = sv + 4 * N;          // [16][8] cross-warp GN partials
-    float* s_wout = s_red + 128;        // [7][64]
+    float* s_red = sv + 4 * N;          // [2 WG][4 quadrants][8 groups]
+    float* s_wout = s_red + 64;         // [7][64]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * 128;
+    const int n_tiles = (a.rows + 127) / 128;
+    const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < stages; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
         }
-        mbar_init(tfull, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 128);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmA[0]) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmW) : "memory");
@@ -224,16 +256,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (warp >= 2) {
-        for (int i = threadIdx.x - 64; i < N; i += 128) {
+        for (int i = threadIdx.x - 64; i < N; i += 128 * TC_EPI_WG) {
             s_bias[i] = a.bias[i];
-            if (EPI == EPI_GN_FILM || EPI == EPI_GN_RES || EPI == EPI_FINAL) {
+            if (EPI != EPI_PLAIN) {
                 s_gamma[i] = a.gamma[i];
                 s_beta[i] = a.beta[i];
             }
             if (RES) s_rbias[i] = a.rbias[i];
         }
         if (EPI == EPI_FINAL)
-            for (int i = threadIdx.x - 64; i < U_DOF * 64; i += 128) s_wout[i] = a.wout[i];
+            for (int i = threadIdx.x - 64; i < U_DOF * 64; i += 128 * TC_EPI_WG) s_wout[i] = a.wout[i];
     }
     tc_fence_before();
     __syncthreads();
@@ -242,221 +274,254 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
 
     if (warp == 0) {
         if (lane == 0) {
-            const int b0 = m0 / a.Tv;
-            for (int i = 0; i < a.n_chunks; ++i) {
-                const int s = i % stages;
-                const uint32_t ph = (uint32_t)(i / stages) & 1u;
-                mbar_wait(&empty[s], ph ^ 1u);
-                mbar_expect_tx(&full[s], STAGE);
-                const TcChunk ch = a.chunk[i];
-                uint8_t* sa = smem + (size_t)s * STAGE;
-                tma_load_3d(sa, &a.tmA[ch.src], &full[s], ch.c, ch.dt, b0);
-                tma_load_2d(sa + A_BYTES, ch.res ? &a.tmR : &a.tmW, &full[s], ch.kcol, 0);
+            int it = 0;
+            for (int j = 0; j < my_tiles; ++j) {
+                const int tile = blockIdx.x + j * gridDim.x;
+                const int b0 = tile * 128 / a.Tv;
+                for (int i = 0; i < a.n_chunks; ++i, ++it) {
+                    const int s = it % stages;
+                    const uint32_t ph = (uint32_t)(it / stages) & 1u;
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    mbar_expect_tx(&full[s], STAGE);
+                    const TcChunk ch = a.chunk[i];
+                    uint8_t* sa = smem + (size_t)s * STAGE;
+                    tma_load_3d(sa, &a.tmA[ch.src], &full[s], ch.c, ch.dt, b0);
+                    tma_load_2d(sa + A_BYTES, ch.res ? &a.tmR : &a.tmW, &full[s], ch.kcol, 0);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_bf16(128, N);
-            for (int i = 0; i < a.n_chunks; ++i) {
-                const int s = i % stages;
-                const uint32_t ph = (uint32_t)(i / stages) & 1u;
-                mbar_wait(&full[s], ph);
+            int it = 0;
+            for (int j = 0; j < my_tiles; ++j) {
+                const int buf = j % NBUF;
+                const uint32_t use = (uint32_t)(j / NBUF);
+                mbar_wait(&tempty[buf], (use & 1u) ^ 1u);
                 tc_fence_after();
-                const TcChunk ch = a.chunk[i];
-                const uint8_t* sa = smem + (size_t)s * STAGE;
-                const uint64_t da = umma_desc_sw128(sa);
-                const uint64_t db = umma_desc_sw128(sa + A_BYTES);
-                const uint32_t d_tmem = tmem_base + (ch.res ? (uint32_t)N : 0u);
+                const uint32_t acc0 = tmem_base + (uint32_t)(buf * ACC);
+                for (int i = 0; i < a.n_chunks; ++i, ++it) {
+                    const int s = it % stages;
+                    const uint32_t ph = (uint32_t)(it / stages) & 1u;
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const TcChunk ch = a.chunk[i];
+                    const uint8_t* sa = smem + (size_t)s * STAGE;
+                    const uint64_t da = umma_desc_sw128(sa);
+                    const uint64_t db = umma_desc_sw128(sa + A_BYTES);
+                    const uint32_t d_tmem = acc0 + (ch.res ? (uint32_t)N : 0u);
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    umma_bf16(d_tmem, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc,
-                              (ch.first && kk == 0) ? 0u : 1u);
-                umma_commit(&empty[s]);
+                    for (int kk = 0; kk < 4; ++kk)
+                        umma_bf16(d_tmem, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc,
+                                  (ch.first && kk == 0) ? 0u : 1u);
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&tfull[buf]);
             }
-            umma_commit(tfull);
         }
         __syncwarp();
     } else {
         // ============================ epilogue ============================
-        const int q = warp & 3;  // TMEM lane quadrant of this warp
+        const int wg = (warp - 2) >> 2;   // warpgroup
+        const int q = warp & 3;           // TMEM lane quadrant of this warp
         const int r = q * 32 + lane;
-        const int grow = m0 + r;
-        const bool valid = grow < a.rows;
-        const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16);
-        mbar_wait(tfull, 0);
-        tc_fence_after();
+        const int Tv = a.Tv;
+        const int seg = Tv < 32 ? Tv : 32;
+        const float inv_n = 1.0f / (float)(Tv * CG);
+        float* red = s_red + wg * 32;
+        for (int j = wg; j < my_tiles; j += TC_EPI_WG) {
+            const int tile = blockIdx.x + j * gridDim.x;
+            const int buf = j % NBUF;
+            const uint32_t use = (uint32_t)(j / NBUF);
+            const int grow = tile * 128 + r;
+            const bool valid = grow < a.rows;
+            const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC);
+            mbar_wait(&tfull[buf], use & 1u);
+            tc_fence_after();
 
-        if constexpr (EPI == EPI_PLAIN) {
+            if constexpr (EPI == EPI_PLAIN) {
 #pragma unroll 1
-            for (int c0 = 0; c0 < N; c0 += 32) {
-                float v[32];
-                tmem_ld32(t_lane + c0, v);
-                if (valid) {
-                    __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
-#pragma unroll
-                    for (int j = 0; j < 32; j += 8) {
-                        __align__(16) __nv_bfloat162 pk[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            pk[u] = __floats2bfloat162_rn(v[j + 2 * u] + s_bias[c0 + j + 2 * u],
-                                                          v[j + 2 * u + 1] + s_bias[c0 + j + 2 * u + 1]);
-                        *reinterpret_cast<uint4*>(o + j) = *reinterpret_cast<uint4*>(pk);
-                    }
-                }
-            }
-        } else {
-            // ---- GroupNorm statistics over (sample rows) x (group channels)
-            const int Tv = a.Tv;
-            const int seg = Tv < 32 ? Tv : 32;
-            float gsum[8], mean[8], rstd[8];
-#pragma unroll
-            for (int g = 0; g < 8; ++g) gsum[g] = 0.f;
-#pragma unroll 1
-            for (int c0 = 0; c0 < N; c0 += 32) {
-                float v[32];
-                tmem_ld32(t_lane + c0, v);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) gsum[(c0 + j) / CG] += v[j] + s_bias[c0 + j];
-            }
-            auto reduce = [&](float (&x)[8]) {
-#pragma unroll
-                for (int off = 16; off >= 1; off >>= 1)
-                    if (off < seg)
-#pragma unroll
-                        for (int g = 0; g < 8; ++g) x[g] += __shfl_xor_sync(PS_FULL, x[g], off);
-                if (Tv > 32) {  // a sample spans two warps (quadrants q, q^1)
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (lane == 0)
-#pragma unroll
-                        for (int g = 0; g < 8; ++g) s_red[q * 8 + g] = x[g];
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-#pragma unroll
-                    for (int g = 0; g < 8; ++g) x[g] = s_red[q * 8 + g] + s_red[(q ^ 1) * 8 + g];
-                }
-            };
-            reduce(gsum);
-            const float inv_n = 1.0f / (float)(Tv * CG);
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                mean[g] = gsum[g] * inv_n;
-                gsum[g] = 0.f;
-            }
-#pragma unroll 1
-            for (int c0 = 0; c0 < N; c0 += 32) {
-                float v[32];
-                tmem_ld32(t_lane + c0, v);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float d = v[j] + s_bias[c0 + j] - mean[(c0 + j) / CG];
-                    gsum[(c0 + j) / CG] = fmaf(d, d, gsum[(c0 + j) / CG]);
-                }
-            }
-            reduce(gsum);
-#pragma unroll
-            for (int g = 0; g < 8; ++g) rstd[g] = rsqrtf(gsum[g] * inv_n + 1e-5f);
-
-            const int b = grow / Tv;
-            const int p = b / a.S;
-            if constexpr (EPI == EPI_FINAL) {
-                static_assert(N == 64, "final layer has 64 channels");
-                float y[64];
-#pragma unroll
-                for (int c0 = 0; c0 < 64; c0 += 32) {
+                for (int c0 = 0; c0 < N; c0 += 32) {
                     float v[32];
                     tmem_ld32(t_lane + c0, v);
+                    if (valid) {
+                        __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int c = c0 + j;
-                        const float t = (v[j] + s_bias[c] - mean[c / CG]) * rstd[c / CG];
-                        y[c] = mish_fast(fmaf(t, s_gamma[c], s_beta[c]));
-                    }
-                }
-                if (valid) {
-                    float eps[U_DOF];
+                        for (int jj = 0; jj < 32; jj += 8) {
+                            __align__(16) __nv_bfloat162 pk[4];
 #pragma unroll
-                    for (int d = 0; d < U_DOF; ++d) {
-                        float acc = a.bout[d];
-#pragma unroll
-                        for (int c = 0; c < 64; ++c) acc = fmaf(y[c], s_wout[d * 64 + c], acc);
-                        eps[d] = acc;
-                    }
-                    const int t = grow % Tv;
-                    float* xr = a.x + (size_t)grow * U_DOF;
-                    if (a.eps_out) {
-#pragma unroll
-                        for (int d = 0; d < U_DOF; ++d) a.eps_out[(size_t)grow * U_DOF + d] = eps[d];
-                    } else {
-                        const StepCoef sc = a.sc;
-#pragma unroll
-                        for (int d = 0; d < U_DOF; ++d) {
-                            const float xv = xr[d];
-                            float x0 = (xv - sc.sq1m * eps[d]) * sc.rsq;
-                            x0 = fminf(fmaxf(x0, -0.1f), 1.1f);
-                            if (sc.last) {
-                                a.traj[(size_t)grow * U_DOF + d] =
-                                    (t == 0) ? a.q_start[(size_t)p * U_DOF + d] : a.lo + x0 * (a.hi - a.lo);
-                            } else if (sc.ddpm) {
-                                const float z = normal_tc((uint32_t)sc.k, (uint32_t)(a.p0 + p),
-                                                          (uint32_t)(b % a.S), (uint32_t)(t * U_DOF + d), a.key);
-                                xr[d] = sc.c0 * x0 + sc.c1 * xv + sc.sig * z;
-                            } else {
-                                xr[d] = sc.sqn * x0 + sc.sq1mn * eps[d];
-                            }
+                            for (int u = 0; u < 4; ++u)
+                                pk[u] = __floats2bfloat162_rn(v[jj + 2 * u] + s_bias[c0 + jj + 2 * u],
+                                                              v[jj + 2 * u + 1] + s_bias[c0 + jj + 2 * u + 1]);
+                            *reinterpret_cast<uint4*>(o + jj) = *reinterpret_cast<uint4*>(pk);
                         }
                     }
                 }
             } else {
-                const float* film = (EPI == EPI_GN_FILM) ? a.film + (size_t)p * 3584 + a.film_col : nullptr;
-#pragma unroll 1
+                // ---- GroupNorm statistics over (sample rows) x (group channels)
+                float gsum[8], mean[8], rstd[8];
+#pragma unroll
+                for (int g = 0; g < 8; ++g) gsum[g] = 0.f;
+#pragma unroll
                 for (int c0 = 0; c0 < N; c0 += 32) {
-                    float v[32], rv[32];
+                    float v[32];
                     tmem_ld32(t_lane + c0, v);
-                    if constexpr (RES) tmem_ld32(t_lane + N + c0, rv);
-                    if (!valid) continue;
-                    float y[32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int c = c0 + j;
-                        const float t = (v[j] + s_bias[c] - mean[c / CG]) * rstd[c / CG];
-                        y[j] = mish_fast(fmaf(t, s_gamma[c], s_beta[c]));
+                    for (int jj = 0; jj < 32; ++jj) gsum[(c0 + jj) / CG] += v[jj] + s_bias[c0 + jj];
+                }
+                auto reduce = [&](float (&x)[8]) {
+#pragma unroll
+                    for (int off = 16; off >= 1; off >>= 1)
+                        if (off < seg)
+#pragma unroll
+                            for (int g = 0; g < 8; ++g) x[g] += __shfl_xor_sync(PS_FULL, x[g], off);
+                    if (Tv > 32) {  // a sample spans two warps (quadrants q, q^1)
+                        asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+                        if (lane == 0)
+#pragma unroll
+                            for (int g = 0; g < 8; ++g) red[q * 8 + g] = x[g];
+                        asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) x[g] = red[q * 8 + g] + red[(q ^ 1) * 8 + g];
                     }
-                    if constexpr (EPI == EPI_GN_FILM) {
+                };
+                reduce(gsum);
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const float sc = __ldg(film + c0 + j), sh = __ldg(film + N + c0 + j);
-                            y[j] = fmaf(y[j], 1.f + sc, sh);
+                for (int g = 0; g < 8; ++g) {
+                    mean[g] = gsum[g] * inv_n;
+                    gsum[g] = 0.f;
+                }
+#pragma unroll
+                for (int c0 = 0; c0 < N; c0 += 32) {
+                    float v[32];
+                    tmem_ld32(t_lane + c0, v);
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj) {
+                        const float d = v[jj] + s_bias[c0 + jj] - mean[(c0 + jj) / CG];
+                        gsum[(c0 + jj) / CG] = fmaf(d, d, gsum[(c0 + jj) / CG]);
+                    }
+                }
+                reduce(gsum);
+#pragma unroll
+                for (int g = 0; g < 8; ++g) rstd[g] = rsqrtf(gsum[g] * inv_n + 1e-5f);
+
+                const int b = grow / Tv;
+                const int p = b / a.S;
+                if constexpr (EPI == EPI_FINAL) {
+                    static_assert(N == 64, "final layer has 64 channels");
+                    float y[64];
+#pragma unroll
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
+                        float v[32];
+                        tmem_ld32(t_lane + c0, v);
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) {
+                            const int c = c0 + jj;
+                            const float t = (v[jj] + s_bias[c] - mean[c / CG]) * rstd[c / CG];
+                            y[c] = mish_fast(fmaf(t, s_gamma[c], s_beta[c]));
                         }
-                    } else {
-                        if constexpr (RES) {
+                    }
+                    if (valid) {
+                        float eps[U_DOF];
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) y[j] += rv[j] + s_rbias[c0 + j];
+                        for (int d = 0; d < U_DOF; ++d) {
+                            float acc = a.bout[d];
+#pragma unroll
+                            for (int c = 0; c < 64; ++c) acc = fmaf(y[c], s_wout[d * 64 + c], acc);
+                            eps[d] = acc;
+                        }
+                        const int t = grow % Tv;
+                        float* xr = a.x + (size_t)grow * U_DOF;
+                        if (a.eps_out) {
+#pragma unroll
+                            for (int d = 0; d < U_DOF; ++d) a.eps_out[(size_t)grow * U_DOF + d] = eps[d];
                         } else {
-                            const uint4* rs = reinterpret_cast<const uint4*>(a.res_src + (size_t)grow * N + c0);
+                            const StepCoef sc = a.sc;
 #pragma unroll
-                            for (int j = 0; j < 32; j += 8) {
-                                uint4 u = __ldg(rs + j / 8);
-                                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-                                for (int k2 = 0; k2 < 4; ++k2) {
-                                    const float2 f = __bfloat1622float2(h2[k2]);
-                                    y[j + 2 * k2] += f.x;
-                                    y[j + 2 * k2 + 1] += f.y;
+                            for (int d = 0; d < U_DOF; ++d) {
+                                const float xv = xr[d];
+                                float x0 = (xv - sc.sq1m * eps[d]) * sc.rsq;
+                                x0 = fminf(fmaxf(x0, -0.1f), 1.1f);
+                                if (sc.last) {
+                                    a.traj[(size_t)grow * U_DOF + d] =
+                                        (t == 0) ? a.q_start[(size_t)p * U_DOF + d] : a.lo + x0 * (a.hi - a.lo);
+                                } else if (sc.ddpm) {
+                                    const float z = normal_tc((uint32_t)sc.k, (uint32_t)(a.p0 + p),
+                                                              (uint32_t)(b % a.S), (uint32_t)(t * U_DOF + d), a.key);
+                                    xr[d] = sc.c0 * x0 + sc.c1 * xv + sc.sig * z;
+                                } else {
+                                    xr[d] = sc.sqn * x0 + sc.sq1mn * eps[d];
                                 }
                             }
                         }
                     }
-                    __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
+                } else {
+                    const float* film = (EPI == EPI_GN_FILM) ? a.film + (size_t)p * 3584 + a.film_col : nullptr;
+#pragma unroll 1
+                    for (int c0 = 0; c0 < N; c0 += 32) {
+                        float v[32], rv[32];
+                        tmem_ld32(t_lane + c0, v);
+                        if constexpr (RES) tmem_ld32(t_lane + N + c0, rv);
+                        if (!valid) continue;
+                        float y[32];
+                        if constexpr (CG >= 32) {
+                            const float mu = sel(mean, c0 / CG), rs = sel(rstd, c0 / CG);
 #pragma unroll
-                    for (int j = 0; j < 32; j += 8) {
-                        __align__(16) __nv_bfloat162 pk[4];
+                            for (int jj = 0; jj < 32; ++jj) {
+                                const int c = c0 + jj;
+                                y[jj] = mish_fast(fmaf((v[jj] + s_bias[c] - mu) * rs, s_gamma[c], s_beta[c]));
+                            }
+                        } else {
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) pk[u] = __floats2bfloat162_rn(y[j + 2 * u], y[j + 2 * u + 1]);
-                        *reinterpret_cast<uint4*>(o + j) = *reinterpret_cast<uint4*>(pk);
+                            for (int gq = 0; gq < 32 / CG; ++gq) {
+                                const int gi = c0 / CG + gq;
+                                const float mu = sel(mean, gi), rs = sel(rstd, gi);
+#pragma unroll
+                                for (int u = 0; u < CG; ++u) {
+                                    const int jj = gq * CG + u, c = c0 + jj;
+                                    y[jj] = mish_fast(fmaf((v[jj] + s_bias[c] - mu) * rs, s_gamma[c], s_beta[c]));
+                                }
+                            }
+                        }
+                        if constexpr (EPI == EPI_GN_FILM) {
+#pragma unroll
+                            for (int jj = 0; jj < 32; ++jj) {
+                                const float sc = __ldg(film + c0 + jj), sh = __ldg(film + N + c0 + jj);
+                                y[jj] = fmaf(y[jj], 1.f + sc, sh);
+                            }
+                        } else {
+                            if constexpr (RES) {
+#pragma unroll
+                                for (int jj = 0; jj < 32; ++jj) y[jj] += rv[jj] + s_rbias[c0 + jj];
+                            } else {
+                                const uint4* rs = reinterpret_cast<const uint4*>(a.res_src + (size_t)grow * N + c0);
+#pragma unroll
+                                for (int jj = 0; jj < 32; jj += 8) {
+                                    uint4 u = __ldg(rs + jj / 8);
+                                    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                                    for (int k2 = 0; k2 < 4; ++k2) {
+                                        const float2 f = __bfloat1622float2(h2[k2]);
+                                        y[jj + 2 * k2] += f.x;
+                                        y[jj + 2 * k2 + 1] += f.y;
+                                    }
+                                }
+                            }
+                        }
+                        __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
+#pragma unroll
+                        for (int jj = 0; jj < 32; jj += 8) {
+                            __align__(16) __nv_bfloat162 pk[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) pk[u] = __floats2bfloat162_rn(y[jj + 2 * u], y[jj + 2 * u + 1]);
+                            *reinterpret_cast<uint4*>(o + jj) = *reinterpret_cast<uint4*>(pk);
+                        }
                     }
                 }
             }
+            tc_fence_before();
+            mbar_arrive(&tempty[buf]);
         }
-        tc_fence_before();
     }
     __syncthreads();
     if (warp == 1) {
@@ -540,7 +605,7 @@ static int launch_tc(TcArgs& a, int n_tiles, cudaStream_t st) {
     constexpr int STAGE = 128 * 128 + N * 128;
     const int stages = N == 256 ? 4 : (N == 128 ? 6 : 8);
     a.stages = stages;
-    const size_t smem = 1024 + (size_t)stages * STAGE + (2 * stages + 1) * 8 + 16 + (4 * N + 128 + 7 * 64) * 4;
+    const size_t smem = 1024 + (size_t)stages * STAGE + (2 * stages + 4) * 8 + 16 + (4 * N + 64 + 7 * 64) * 4;
     auto kern = conv_tc_kernel<N, EPI, RES>;
     static bool attr_set = false;
     if (!attr_set) {
@@ -548,7 +613,14 @@ static int launch_tc(TcArgs& a, int n_tiles, cudaStream_t st) {
             return PS_FAIL(PS_ERR_CUDA);
         attr_set = true;
     }
-    kern<<<n_tiles, TC_THREADS, smem, st>>>(a);
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int grid = n_tiles < n_sm ? n_tiles : n_sm;
+    kern<<<grid, TC_THREADS, smem, st>>>(a);
     PS_CHECK_LAUNCH();
     return PS_OK;
 }
