@@ -108,10 +108,10 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 
 // mish(x) = x tanh(softplus(x)) = x * n(n+2) / (n(n+2) + 2), n = e^x
 __device__ __forceinline__ float mish_fast(float x) {
-    if (x > 15.f) return x;
-    const float n = __expf(x);
+    const float n = __expf(fminf(x, 15.f));
     const float m = n * (n + 2.f);
-    return x * __fdividef(m, m + 2.f);
+    const float y = x * __fdividef(m, m + 2.f);
+    return x > 15.f ? x : y;
 }
 
 // ---------------------------------------------------------------------------
@@ -194,6 +194,7 @@ __host__ __device__ constexpr int tmem_alloc_cols() {
 }
 
 constexpr int TC_EPI_WG = 2;                         // epilogue warpgroups
+constexpr int TC_FILM_P = 4;                         // FiLM rows staged per tile
 constexpr int TC_THREADS = 64 + 128 * TC_EPI_WG;     // producer warp, MMA warp, epilogue
 
 template <int NV>
@@ -217,6 +218,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
     constexpr int NBUF = n_accbuf<N, RES>();
     constexpr int NCOLS = tmem_alloc_cols<N, RES>();
     constexpr int CG = N / 8;  // channels per group
+    // single accumulator buffer: both epilogue warpgroups drain every tile, each taking
+    // half of the GroupNorm groups (NSPLIT = 2); otherwise warpgroups alternate tiles.
+    constexpr int NSPLIT = NBUF == 1 ? 2 : 1;
+    constexpr int NC = N / NSPLIT;   // columns per warpgroup
+    constexpr int NG = 8 / NSPLIT;   // groups per warpgroup
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     const int stages = a.stages;
@@ -230,8 +236,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
     float* s_gamma = sv + N;
     float* s_beta = sv + 2 * N;
     float* s_rbias = sv + 3 * N;
-    float* s_red = sv + 4 * N;          // [2 WG][4 quadrants][8 groups]
-    float* s_wout = s_red + 64;         // [7][64]
+    float* s_red = sv + 4 * N;          // [2 WG][4 quadrants][16]
+    float* s_wout = s_red + 128;        // [7][64]
+    float* s_film = s_wout + 7 * 64;    // [2 WG][TC_FILM_P][2N]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_tiles = (a.rows + 127) / 128;
@@ -244,7 +251,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 128);
+            mbar_init(&tempty[b], 128 * NSPLIT);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmA[0]) : "memory");
@@ -328,23 +335,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
         const int Tv = a.Tv;
         const int seg = Tv < 32 ? Tv : 32;
         const float inv_n = 1.0f / (float)(Tv * CG);
-        float* red = s_red + wg * 32;
-        for (int j = wg; j < my_tiles; j += TC_EPI_WG) {
+        float* red = s_red + wg * 64;
+        const int cbase = NSPLIT == 2 ? wg * NC : 0;   // first column of this warpgroup
+        const int j0 = NSPLIT == 2 ? 0 : wg;
+        const int jstep = NSPLIT == 2 ? 1 : TC_EPI_WG;
+        for (int j = j0; j < my_tiles; j += jstep) {
             const int tile = blockIdx.x + j * gridDim.x;
             const int buf = j % NBUF;
             const uint32_t use = (uint32_t)(j / NBUF);
             const int grow = tile * 128 + r;
             const bool valid = grow < a.rows;
-            const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC);
+            const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC + cbase);
             mbar_wait(&tfull[buf], use & 1u);
             tc_fence_after();
 
             if constexpr (EPI == EPI_PLAIN) {
 #pragma unroll 1
-                for (int c0 = 0; c0 < N; c0 += 32) {
+                for (int cc = 0; cc < NC; cc += 32) {
                     float v[32];
-                    tmem_ld32(t_lane + c0, v);
+                    tmem_ld32(t_lane + cc, v);
                     if (valid) {
+                        const int c0 = cbase + cc;
                         __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
 #pragma unroll
                         for (int jj = 0; jj < 32; jj += 8) {
@@ -358,57 +369,54 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
                     }
                 }
             } else {
-                // ---- GroupNorm statistics over (sample rows) x (group channels)
-                float gsum[8], mean[8], rstd[8];
+                // ---- GroupNorm statistics (local groups of this warpgroup), one pass
+                float s1[NG], s2[NG], mean[NG], rstd[NG];
 #pragma unroll
-                for (int g = 0; g < 8; ++g) gsum[g] = 0.f;
+                for (int g = 0; g < NG; ++g) s1[g] = s2[g] = 0.f;
 #pragma unroll
-                for (int c0 = 0; c0 < N; c0 += 32) {
+                for (int cc = 0; cc < NC; cc += 32) {
                     float v[32];
-                    tmem_ld32(t_lane + c0, v);
-#pragma unroll
-                    for (int jj = 0; jj < 32; ++jj) gsum[(c0 + jj) / CG] += v[jj] + s_bias[c0 + jj];
-                }
-                auto reduce = [&](float (&x)[8]) {
-#pragma unroll
-                    for (int off = 16; off >= 1; off >>= 1)
-                        if (off < seg)
-#pragma unroll
-                            for (int g = 0; g < 8; ++g) x[g] += __shfl_xor_sync(PS_FULL, x[g], off);
-                    if (Tv > 32) {  // a sample spans two warps (quadrants q, q^1)
-                        asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
-                        if (lane == 0)
-#pragma unroll
-                            for (int g = 0; g < 8; ++g) red[q * 8 + g] = x[g];
-                        asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
-#pragma unroll
-                        for (int g = 0; g < 8; ++g) x[g] = red[q * 8 + g] + red[(q ^ 1) * 8 + g];
-                    }
-                };
-                reduce(gsum);
-#pragma unroll
-                for (int g = 0; g < 8; ++g) {
-                    mean[g] = gsum[g] * inv_n;
-                    gsum[g] = 0.f;
-                }
-#pragma unroll
-                for (int c0 = 0; c0 < N; c0 += 32) {
-                    float v[32];
-                    tmem_ld32(t_lane + c0, v);
+                    tmem_ld32(t_lane + cc, v);
 #pragma unroll
                     for (int jj = 0; jj < 32; ++jj) {
-                        const float d = v[jj] + s_bias[c0 + jj] - mean[(c0 + jj) / CG];
-                        gsum[(c0 + jj) / CG] = fmaf(d, d, gsum[(c0 + jj) / CG]);
+                        const float xv = v[jj] + s_bias[cbase + cc + jj];
+                        s1[(cc + jj) / CG] += xv;
+                        s2[(cc + jj) / CG] = fmaf(xv, xv, s2[(cc + jj) / CG]);
                     }
                 }
-                reduce(gsum);
 #pragma unroll
-                for (int g = 0; g < 8; ++g) rstd[g] = rsqrtf(gsum[g] * inv_n + 1e-5f);
+                for (int off = 16; off >= 1; off >>= 1)
+                    if (off < seg)
+#pragma unroll
+                        for (int g = 0; g < NG; ++g) {
+                            s1[g] += __shfl_xor_sync(PS_FULL, s1[g], off);
+                            s2[g] += __shfl_xor_sync(PS_FULL, s2[g], off);
+                        }
+                if (Tv > 32) {  // a sample spans two warps (quadrants q, q^1)
+                    asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+                    if (lane == 0)
+#pragma unroll
+                        for (int g = 0; g < NG; ++g) {
+                            red[q * 16 + g] = s1[g];
+                            red[q * 16 + 8 + g] = s2[g];
+                        }
+                    asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        s1[g] = red[q * 16 + g] + red[(q ^ 1) * 16 + g];
+                        s2[g] = red[q * 16 + 8 + g] + red[(q ^ 1) * 16 + 8 + g];
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    mean[g] = s1[g] * inv_n;
+                    rstd[g] = rsqrtf(fmaxf(fmaf(s2[g], inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
+                }
 
                 const int b = grow / Tv;
                 const int p = b / a.S;
                 if constexpr (EPI == EPI_FINAL) {
-                    static_assert(N == 64, "final layer has 64 channels");
+                    static_assert(N == 64 && NSPLIT == 1, "final layer has 64 channels");
                     float y[64];
 #pragma unroll
                     for (int c0 = 0; c0 < 64; c0 += 32) {
@@ -456,48 +464,78 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
                         }
                     }
                 } else {
-                    const float* film = (EPI == EPI_GN_FILM) ? a.film + (size_t)p * 3584 + a.film_col : nullptr;
-#pragma unroll 1
-                    for (int c0 = 0; c0 < N; c0 += 32) {
-                        float v[32], rv[32];
-                        tmem_ld32(t_lane + c0, v);
-                        if constexpr (RES) tmem_ld32(t_lane + N + c0, rv);
-                        if (!valid) continue;
-                        float y[32];
-                        if constexpr (CG >= 32) {
-                            const float mu = sel(mean, c0 / CG), rs = sel(rstd, c0 / CG);
-#pragma unroll
-                            for (int jj = 0; jj < 32; ++jj) {
-                                const int c = c0 + jj;
-                                y[jj] = mish_fast(fmaf((v[jj] + s_bias[c] - mu) * rs, s_gamma[c], s_beta[c]));
+                    // FiLM (scale, shift) for the <= TC_FILM_P problems of this tile, staged in smem
+                    const float* film_row = nullptr;
+                    if constexpr (EPI == EPI_GN_FILM) {
+                        const int last_row = min(tile * 128 + 127, a.rows - 1);
+                        const int p_lo = (tile * 128 / Tv) / a.S, p_hi = (last_row / Tv) / a.S;
+                        float* sf = s_film + wg * (TC_FILM_P * 2 * N);
+                        if (p_hi - p_lo < TC_FILM_P) {
+                            asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+                            const int n = (p_hi - p_lo + 1) * 2 * N;
+                            for (int i = r; i < n; i += 128) {
+                                const int pp = p_lo + i / (2 * N), c = i % (2 * N);
+                                sf[i] = __ldg(a.film + (size_t)pp * 3584 + a.film_col + c);
                             }
+                            asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+                            film_row = sf + (p - p_lo) * 2 * N;
                         } else {
-#pragma unroll
-                            for (int gq = 0; gq < 32 / CG; ++gq) {
-                                const int gi = c0 / CG + gq;
-                                const float mu = sel(mean, gi), rs = sel(rstd, gi);
-#pragma unroll
-                                for (int u = 0; u < CG; ++u) {
-                                    const int jj = gq * CG + u, c = c0 + jj;
-                                    y[jj] = mish_fast(fmaf((v[jj] + s_bias[c] - mu) * rs, s_gamma[c], s_beta[c]));
-                                }
-                            }
+                            film_row = a.film + (size_t)p * 3584 + a.film_col;
                         }
-                        if constexpr (EPI == EPI_GN_FILM) {
-#pragma unroll
-                            for (int jj = 0; jj < 32; ++jj) {
-                                const float sc = __ldg(film + c0 + jj), sh = __ldg(film + N + c0 + jj);
-                                y[jj] = fmaf(y[jj], 1.f + sc, sh);
-                            }
-                        } else {
+                    }
+                    if (valid) {
+#pragma unroll 1
+                        for (int cc = 0; cc < NC; cc += 16) {
+                            const int c0 = cbase + cc;
+                            float v[32];
+                            // 16 columns per step keeps the register footprint below the cap
+                            uint32_t rr[16];
+                            asm volatile(
+                                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                                : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]),
+                                  "=r"(rr[6]), "=r"(rr[7]), "=r"(rr[8]), "=r"(rr[9]), "=r"(rr[10]), "=r"(rr[11]),
+                                  "=r"(rr[12]), "=r"(rr[13]), "=r"(rr[14]), "=r"(rr[15])
+                                : "r"(t_lane + cc));
                             if constexpr (RES) {
+                                uint32_t rq[16];
+                                asm volatile(
+                                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                                    : "=r"(rq[0]), "=r"(rq[1]), "=r"(rq[2]), "=r"(rq[3]), "=r"(rq[4]), "=r"(rq[5]),
+                                      "=r"(rq[6]), "=r"(rq[7]), "=r"(rq[8]), "=r"(rq[9]), "=r"(rq[10]), "=r"(rq[11]),
+                                      "=r"(rq[12]), "=r"(rq[13]), "=r"(rq[14]), "=r"(rq[15])
+                                    : "r"(t_lane + N + cc));
+                                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                                for (int jj = 0; jj < 32; ++jj) y[jj] += rv[jj] + s_rbias[c0 + jj];
+                                for (int jj = 0; jj < 16; ++jj) v[16 + jj] = __uint_as_float(rq[jj]);
                             } else {
-                                const uint4* rs = reinterpret_cast<const uint4*>(a.res_src + (size_t)grow * N + c0);
+                                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                            }
 #pragma unroll
-                                for (int jj = 0; jj < 32; jj += 8) {
-                                    uint4 u = __ldg(rs + jj / 8);
+                            for (int jj = 0; jj < 16; ++jj) v[jj] = __uint_as_float(rr[jj]);
+                            const int gi = cc / CG;
+                            const float mu = sel(mean, gi), rs = sel(rstd, gi);
+                            const float mu2 = CG < 16 ? sel(mean, gi + 1) : mu;
+                            const float rs2 = CG < 16 ? sel(rstd, gi + 1) : rs;
+                            float y[16];
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj) {
+                                const int c = c0 + jj;
+                                const bool hi = CG < 16 && jj >= CG;
+                                const float t = (v[jj] + s_bias[c] - (hi ? mu2 : mu)) * (hi ? rs2 : rs);
+                                y[jj] = mish_fast(fmaf(t, s_gamma[c], s_beta[c]));
+                            }
+                            if constexpr (EPI == EPI_GN_FILM) {
+#pragma unroll
+                                for (int jj = 0; jj < 16; ++jj)
+                                    y[jj] = fmaf(y[jj], 1.f + film_row[c0 + jj], film_row[N + c0 + jj]);
+                            } else if constexpr (RES) {
+#pragma unroll
+                                for (int jj = 0; jj < 16; ++jj) y[jj] += v[16 + jj] + s_rbias[c0 + jj];
+                            } else {
+                                const uint4* rsrc = reinterpret_cast<const uint4*>(a.res_src + (size_t)grow * N + c0);
+#pragma unroll
+                                for (int jj = 0; jj < 16; jj += 8) {
+                                    uint4 u = __ldg(rsrc + jj / 8);
                                     const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
                                     for (int k2 = 0; k2 < 4; ++k2) {
@@ -507,14 +545,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
                                     }
                                 }
                             }
-                        }
-                        __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
+                            __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
 #pragma unroll
-                        for (int jj = 0; jj < 32; jj += 8) {
-                            __align__(16) __nv_bfloat162 pk[4];
+                            for (int jj = 0; jj < 16; jj += 8) {
+                                __align__(16) __nv_bfloat162 pk[4];
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) pk[u] = __floats2bfloat162_rn(y[jj + 2 * u], y[jj + 2 * u + 1]);
-                            *reinterpret_cast<uint4*>(o + jj) = *reinterpret_cast<uint4*>(pk);
+                                for (int u = 0; u < 4; ++u) pk[u] = __floats2bfloat162_rn(y[jj + 2 * u], y[jj + 2 * u + 1]);
+                                *reinterpret_cast<uint4*>(o + jj) = *reinterpret_cast<uint4*>(pk);
+                            }
                         }
                     }
                 }
@@ -605,7 +643,8 @@ static int launch_tc(TcArgs& a, int n_tiles, cudaStream_t st) {
     constexpr int STAGE = 128 * 128 + N * 128;
     const int stages = N == 256 ? 4 : (N == 128 ? 6 : 8);
     a.stages = stages;
-    const size_t smem = 1024 + (size_t)stages * STAGE + (2 * stages + 4) * 8 + 16 + (4 * N + 64 + 7 * 64) * 4;
+    const size_t smem = 1024 + (size_t)stages * STAGE + (2 * stages + 4) * 8 + 16 +
+                        (4 * N + 128 + 7 * 64 + TC_EPI_WG * TC_FILM_P * 2 * N) * 4;
     auto kern = conv_tc_kernel<N, EPI, RES>;
     static bool attr_set = false;
     if (!attr_set) {

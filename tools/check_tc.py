@@ -23,3 +23,12 @@ for (P, S, T, k) in [(1, 16, 32, 50), (2, 8, 32, 100), (4, 32, 32, 3), (2, 4, 64
     d1 = e1 - want
     print(f"P{P} S{S} T{T} k{k}: fp32 max {np.abs(e0-want).max():.2e} | bf16 max {np.abs(d1).max():.3e} "
           f"rms {np.sqrt((d1**2).mean()):.3e} ref rms {np.sqrt((want**2).mean()):.3e}", flush=True)
+
+# multi-tile-per-CTA persistence check: bf16 vs fp32 SIMT at B=4096 (>148 tiles per layer)
+for P, S in [(128, 32), (1024, 32)]:
+    cond = np.concatenate([np.abs(rng.standard_normal((P, 256))) * 0.3, rng.uniform(0, 1, (P, 14))], 1)
+    x = rng.standard_normal((P * S, 32, 7)).astype(np.float32)
+    e0 = s0.predict_noise(x, 40, s0.film(cond), S).cpu().numpy()
+    e1 = s1.predict_noise(x, 40, s1.film(cond), S).cpu().numpy()
+    d = e1 - e0
+    print(f"P{P}: bf16 vs fp32 max {np.abs(d).max():.3e} rms {np.sqrt((d**2).mean()):.3e}", flush=True)
