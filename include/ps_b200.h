@@ -85,6 +85,16 @@ int ps_encode(const float* images, int P, int n_img, int H, int W, const float* 
               const float* q_start, const float* goal, float lo, float hi, void* ws, float* cond,
               void* stream);
 
+/* The same encoder on tcgen05 (bf16 activations, fp32 accumulation): layer 1 in
+ * fp32 SIMT, layers 2.. as segment GEMMs over the [img][H/2][2][W/2][2C] pair view.
+ * ps_encoder_pack packs the fp32 encoder blob (table order) once per image size. */
+long long ps_encoder_packed_bytes(int H, int W, int n_layers);
+int ps_encoder_pack(const float* blob, int H, int W, int n_layers, void* packed, void* stream);
+long long ps_encode_tc_workspace_bytes(int n_images, int H, int W, int n_layers);
+int ps_encode_tc(const float* images, int P, int n_img, int H, int W, const void* packed, int n_layers,
+                 const float* q_start, const float* goal, float lo, float hi, void* ws, float* cond,
+                 void* stream);
+
 /* FiLM split: film_a[p] = mish(cond[p]) @ W_cond (per problem, once);
  * per-step part computed inside ps_sample / ps_unet_forward. */
 int ps_film_problem(const void* packed, int mode, const float* cond, int P, float* film_a, void* stream);

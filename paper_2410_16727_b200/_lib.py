@@ -42,10 +42,16 @@ _SIGS = {
     "ps_sample": [_vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int,
                   ctypes.c_uint, _vp, _c_f, _c_f, _vp, _vp, _vp],
     "ps_noise_probe": [_vp, _c_int, _c_int, _c_int, _c_int, ctypes.c_uint, _vp],
+    "ps_encoder_packed_bytes": [_c_int, _c_int, _c_int],
+    "ps_encoder_pack": [_vp, _c_int, _c_int, _c_int, _vp, _vp],
+    "ps_encode_tc_workspace_bytes": [_c_int, _c_int, _c_int, _c_int],
+    "ps_encode_tc": [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp, _vp, _c_f, _c_f, _vp, _vp,
+                     _vp],
 }
 _RESTYPE = {"ps_version": ctypes.c_char_p, "ps_launch_count": _c_ll, "ps_unet_param_count": _c_ll,
             "ps_unet_param_offset": _c_ll, "ps_unet_packed_bytes": _c_ll,
-            "ps_encode_workspace_bytes": _c_ll, "ps_sample_workspace_bytes": _c_ll}
+            "ps_encode_workspace_bytes": _c_ll, "ps_sample_workspace_bytes": _c_ll,
+            "ps_encoder_packed_bytes": _c_ll, "ps_encode_tc_workspace_bytes": _c_ll}
 
 _lib = None
 

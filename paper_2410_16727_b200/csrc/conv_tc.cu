@@ -62,6 +62,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, ui
         "l"((uint64_t)tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+        : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -126,6 +134,8 @@ struct TcChunk {
     int8_t dt;      // time offset
     int8_t res;     // 1: residual GEMM
     int8_t first;   // 1: first chunk of its accumulator
+    int8_t dx;      // 2-D geometry: x-pair offset
+    int8_t par;     // 2-D geometry: row parity
 };
 
 struct TcArgs {
@@ -154,6 +164,9 @@ struct TcArgs {
     float* traj;
     float lo, hi;
     float* eps_out;                 // optional: write eps (forward-only calls)
+    // 2-D geometry (encoder): tile = ry output rows x wx output columns of one image
+    int geom;                       // 0: [B][Tv] samples, 1: 2-D image tiles
+    int Ho, Wo, Hp, wx, ry, tiles_x, tiles_y;
 };
 
 __device__ __forceinline__ uint4 philox_tc(uint4 c, uint32_t k0, uint32_t k1) {
@@ -241,7 +254,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
     float* s_film = s_wout + 7 * 64;    // [2 WG][TC_FILM_P][2N]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_tiles = (a.rows + 127) / 128;
+    const int n_tiles = a.geom ? a.rows : (a.rows + 127) / 128;   // geom 1: rows = #tiles
     const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
     if (warp == 0 && lane == 0) {
@@ -265,7 +278,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
     if (warp >= 2) {
         for (int i = threadIdx.x - 64; i < N; i += 128 * TC_EPI_WG) {
             s_bias[i] = a.bias[i];
-            if (EPI != EPI_PLAIN) {
+            if (EPI != EPI_PLAIN && EPI != EPI_RELU2D) {
                 s_gamma[i] = a.gamma[i];
                 s_beta[i] = a.beta[i];
             }
@@ -284,7 +297,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
             int it = 0;
             for (int j = 0; j < my_tiles; ++j) {
                 const int tile = blockIdx.x + j * gridDim.x;
-                const int b0 = tile * 128 / a.Tv;
+                const int b0 = a.geom ? 0 : tile * 128 / a.Tv;
+                int img = 0, y0 = 0, x0 = 0;
+                if (a.geom) {
+                    const int per_img = a.tiles_x * a.tiles_y;
+                    img = tile / per_img;
+                    const int tt = tile % per_img;
+                    y0 = (tt / a.tiles_x) * a.ry;
+                    x0 = (tt % a.tiles_x) * a.wx;
+                }
                 for (int i = 0; i < a.n_chunks; ++i, ++it) {
                     const int s = it % stages;
                     const uint32_t ph = (uint32_t)(it / stages) & 1u;
@@ -292,7 +313,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
                     mbar_expect_tx(&full[s], STAGE);
                     const TcChunk ch = a.chunk[i];
                     uint8_t* sa = smem + (size_t)s * STAGE;
-                    tma_load_3d(sa, &a.tmA[ch.src], &full[s], ch.c, ch.dt, b0);
+                    if (a.geom)
+                        tma_load_5d(sa, &a.tmA[ch.src], &full[s], ch.c, x0 + ch.dx, ch.par, y0 + ch.dt, img);
+                    else
+                        tma_load_3d(sa, &a.tmA[ch.src], &full[s], ch.c, ch.dt, b0);
                     tma_load_2d(sa + A_BYTES, ch.res ? &a.tmR : &a.tmW, &full[s], ch.kcol, 0);
                 }
             }
@@ -349,7 +373,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
             mbar_wait(&tfull[buf], use & 1u);
             tc_fence_after();
 
-            if constexpr (EPI == EPI_PLAIN) {
+            if constexpr (EPI == EPI_RELU2D) {
+                const int per_img = a.tiles_x * a.tiles_y;
+                const int img = tile / per_img, tt = tile % per_img;
+                const int y = (tt / a.tiles_x) * a.ry + r / a.wx, x = (tt % a.tiles_x) * a.wx + r % a.wx;
+                const bool ok = y < a.Ho && x < a.Wo;
+                __nv_bfloat16* o = a.out + (((size_t)img * a.Hp + y) * a.Wo + x) * N;
+#pragma unroll 1
+                for (int cc = 0; cc < NC; cc += 32) {
+                    float v[32];
+                    tmem_ld32(t_lane + cc, v);
+                    if (ok) {
+                        const int c0 = cbase + cc;
+#pragma unroll
+                        for (int jj = 0; jj < 32; jj += 8) {
+                            __align__(16) __nv_bfloat162 pk[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                pk[u] = __floats2bfloat162_rn(fmaxf(v[jj + 2 * u] + s_bias[c0 + jj + 2 * u], 0.f),
+                                                              fmaxf(v[jj + 2 * u + 1] + s_bias[c0 + jj + 2 * u + 1], 0.f));
+                            *reinterpret_cast<uint4*>(o + c0 + jj) = *reinterpret_cast<uint4*>(pk);
+                        }
+                    }
+                }
+            } else if constexpr (EPI == EPI_PLAIN) {
 #pragma unroll 1
                 for (int cc = 0; cc < NC; cc += 32) {
                     float v[32];
@@ -566,6 +613,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NCOLS));
     }
+}
+
+__global__ void gather_bf16_kernel(const float* __restrict__ blob, const long long* __restrict__ src, size_t n,
+                                   __nv_bfloat16* __restrict__ dst) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = __float2bfloat16_rn(src[i] >= 0 ? blob[src[i]] : 0.f);
+}
+__global__ void gather_f32_kernel(const float* __restrict__ blob, const long long* __restrict__ src, size_t n,
+                                  float* __restrict__ dst) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[i] >= 0 ? blob[src[i]] : 0.f;
 }
 
 // im2col of the fp32 state for the first layer: A0[row][tap*7 + d] = x[b, t+tap-2, d]
@@ -854,4 +912,316 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
     return run_layer(L, packed, lf, B, S, film, x, step, step ? nullptr : eps, st);
 }
 
+
+// ===========================================================================
+// Observation encoder on tcgen05: conv3x3 stride 2 pad 1 + ReLU as a segment GEMM
+// over the 5-D pair view [img][H/2][2][W/2][2C] of an NHWC bf16 activation.
+//   out[y][x] = sum_dy ( in[2y+dy-1][2x-1] W[.,.,dy,0] + in[2y+dy-1][2x..2x+1] W[.,.,dy,1..2] )
+// row 2y+dy-1 -> (pair y-1, parity 1) | (y, 0) | (y, 1); column pair x-1 (odd pixel)
+// and x (both pixels).  TMA zero-fills the top/left padding.
+// ===========================================================================
+constexpr int ENC_MAXL = 5;
+static const int ENC_CH[ENC_MAXL] = {32, 64, 128, 256, 256};
+
+struct EncLayerGeo {
+    int C, N;            // in / out channels
+    int Hin, Win, Hin_p; // input (Hin_p even, padded)
+    int Ho, Wo, Ho_p;    // output (Ho_p even for the next layer's pair view)
+    int wx, ry, tiles_x, tiles_y;
+    int n_chunks;
+    size_t w_off;        // bf16 offset in the packed encoder buffer
+    size_t b_off;        // fp32 bias offset in the side table (elements)
+};
+
+static void enc_geometry(int H, int W, int n_layers, EncLayerGeo* g) {
+    int h = H, w = W, c = 1;
+    size_t woff = 0, boff = 0;
+    for (int l = 0; l < n_layers; ++l) {
+        EncLayerGeo& e = g[l];
+        e.C = c;
+        e.N = ENC_CH[l];
+        e.Hin = h;
+        e.Win = w;
+        e.Hin_p = h + (h & 1);
+        e.Ho = (h - 1) / 2 + 1;
+        e.Wo = (w - 1) / 2 + 1;
+        e.Ho_p = e.Ho + (e.Ho & 1);
+        // tile shape: wx x ry = 128 minimising padding waste
+        int best_wx = 8;
+        double best = 1e30;
+        for (int wx = 4; wx <= 128; wx *= 2) {
+            const int ry = 128 / wx;
+            const double cover = (double)((e.Wo + wx - 1) / wx * wx) * ((e.Ho + ry - 1) / ry * ry);
+            if (cover < best - 1e-9) {
+                best = cover;
+                best_wx = wx;
+            }
+        }
+        e.wx = best_wx;
+        e.ry = 128 / best_wx;
+        e.tiles_x = (e.Wo + e.wx - 1) / e.wx;
+        e.tiles_y = (e.Ho + e.ry - 1) / e.ry;
+        const int segA = c == 32 ? 1 : c / 64, segB = 2 * c / 64;
+        e.n_chunks = l == 0 ? 0 : 3 * (segA + segB);
+        e.w_off = woff;
+        if (l > 0) woff += (size_t)e.N * e.n_chunks * 64;
+        e.b_off = boff;
+        boff += e.N;
+        h = e.Ho;
+        w = e.Wo;
+        c = e.N;
+    }
+}
+
+extern "C" long long ps_encoder_packed_bytes(int H, int W, int n_layers) {
+    if (n_layers < 2 || n_layers > ENC_MAXL) return -1;
+    EncLayerGeo g[ENC_MAXL];
+    enc_geometry(H, W, n_layers, g);
+    const EncLayerGeo& last = g[n_layers - 1];
+    const size_t wb = (last.w_off + (size_t)last.N * last.n_chunks * 64) * 2;
+    size_t side = 0;
+    for (int l = 0; l < n_layers; ++l) side += g[l].N;
+    side += 32 * 9;  // layer-1 weights (fp32)
+    return (long long)(((wb + 255) / 256) * 256 + side * 4);
+}
+
+// blob: encoder params in table order (fp32, device).  Layer 1 stays fp32 (SIMT);
+// layers 2.. are packed bf16 [N][chunks*64] in chunk order.
+extern "C" int ps_encoder_pack(const float* blob, int H, int W, int n_layers, void* packed, void* stream) {
+    if (n_layers < 2 || n_layers > ENC_MAXL) return PS_FAIL(PS_ERR_SHAPE);
+    EncLayerGeo g[ENC_MAXL];
+    enc_geometry(H, W, n_layers, g);
+    // blob offsets
+    size_t boff[ENC_MAXL], woff_blob[ENC_MAXL], o = 0;
+    for (int l = 0; l < n_layers; ++l) {
+        woff_blob[l] = o;
+        o += (size_t)g[l].N * g[l].C * 9;
+        boff[l] = o;
+        o += g[l].N;
+    }
+    std::vector<long long> wsrc, ssrc;
+    for (int l = 1; l < n_layers; ++l) {
+        const EncLayerGeo& e = g[l];
+        const int C = e.C;
+        // chunk list (same order as the launcher): dy -> segA chunks -> segB chunks
+        for (int n = 0; n < e.N; ++n) {
+            for (int dy = 0; dy < 3; ++dy) {
+                const int segA = C == 32 ? 1 : C / 64;
+                for (int ci = 0; ci < segA; ++ci)
+                    for (int k = 0; k < 64; ++k) {
+                        // pair x-1: channel index within the pair = (C==32 ? k : C + 64ci + k); odd pixel
+                        const int pc = C == 32 ? k : C + 64 * ci + k;
+                        if (pc < C) {
+                            wsrc.push_back(-1);
+                            continue;
+                        }
+                        const int c = pc - C;
+                        wsrc.push_back((long long)(woff_blob[l] + (((size_t)n * C + c) * 3 + dy) * 3 + 0));
+                    }
+                for (int ci = 0; ci < 2 * C / 64; ++ci)
+                    for (int k = 0; k < 64; ++k) {
+                        const int pc = 64 * ci + k;  // pair x: even pixel c (dx=1), odd pixel c (dx=2)
+                        const int dx = pc < C ? 1 : 2, c = pc < C ? pc : pc - C;
+                        wsrc.push_back((long long)(woff_blob[l] + (((size_t)n * C + c) * 3 + dy) * 3 + dx));
+                    }
+            }
+        }
+    }
+    for (int l = 0; l < n_layers; ++l)
+        for (int n = 0; n < g[l].N; ++n) ssrc.push_back((long long)(boff[l] + n));
+    for (int i = 0; i < 32 * 9; ++i) ssrc.push_back((long long)(woff_blob[0] + i));
+    const EncLayerGeo& last = g[n_layers - 1];
+    const size_t wb = ((last.w_off + (size_t)last.N * last.n_chunks * 64) * 2 + 255) / 256 * 256;
+    if (wsrc.size() * 2 > wb) return PS_FAIL(PS_ERR_SHAPE);
+    cudaStream_t st = (cudaStream_t)stream;
+    long long* d_idx = nullptr;
+    const size_t nmax = std::max(wsrc.size(), ssrc.size());
+    if (cudaMallocAsync(&d_idx, nmax * sizeof(long long), st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+    cudaMemcpyAsync(d_idx, wsrc.data(), wsrc.size() * sizeof(long long), cudaMemcpyHostToDevice, st);
+    gather_bf16_kernel<<<(unsigned)((wsrc.size() + 255) / 256), 256, 0, st>>>(
+        blob, d_idx, wsrc.size(), reinterpret_cast<__nv_bfloat16*>(packed));
+    PS_CHECK_LAUNCH();
+    if (cudaStreamSynchronize(st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+    cudaMemcpyAsync(d_idx, ssrc.data(), ssrc.size() * sizeof(long long), cudaMemcpyHostToDevice, st);
+    gather_f32_kernel<<<(unsigned)((ssrc.size() + 255) / 256), 256, 0, st>>>(
+        blob, d_idx, ssrc.size(), reinterpret_cast<float*>(reinterpret_cast<char*>(packed) + wb));
+    PS_CHECK_LAUNCH();
+    if (cudaStreamSynchronize(st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+    cudaFreeAsync(d_idx, st);
+    return PS_OK;
+}
+
+// layer 1 (1 -> 32 channels) in fp32 SIMT: one output pixel x 32 channels per thread,
+// input depth scaled by 1/2 (spec.DEPTH_SCALE), NHWC bf16 output with even-padded rows.
+__global__ void enc_l1_kernel(const float* __restrict__ img, int n_img, int H, int W, const float* __restrict__ w,
+                              const float* __restrict__ bias, int Ho, int Wo, int Ho_p,
+                              __nv_bfloat16* __restrict__ out) {
+    __shared__ float sw[32 * 9], sb[32];
+    for (int i = threadIdx.x; i < 32 * 9; i += blockDim.x) sw[i] = w[i];
+    for (int i = threadIdx.x; i < 32; i += blockDim.x) sb[i] = bias[i];
+    __syncthreads();
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t n = (size_t)n_img * Ho_p * Wo;
+    if (idx >= n) return;
+    const int x = (int)(idx % Wo), y = (int)((idx / Wo) % Ho_p), m = (int)(idx / ((size_t)Wo * Ho_p));
+    float acc[32];
+#pragma unroll
+    for (int o = 0; o < 32; ++o) acc[o] = sb[o];
+    if (y < Ho) {
+        const float* ib = img + (size_t)m * H * W;
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy) {
+            const int yy = 2 * y + dy - 1;
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+                const int xx = 2 * x + dx - 1;
+                const float v = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? ib[(size_t)yy * W + xx] * 0.5f : 0.f;
+#pragma unroll
+                for (int o = 0; o < 32; ++o) acc[o] = fmaf(v, sw[o * 9 + dy * 3 + dx], acc[o]);
+            }
+        }
+    }
+    __align__(16) __nv_bfloat162 pk[16];
+#pragma unroll
+    for (int o = 0; o < 16; ++o)
+        pk[o] = y < Ho ? __floats2bfloat162_rn(fmaxf(acc[2 * o], 0.f), fmaxf(acc[2 * o + 1], 0.f))
+                       : __floats2bfloat162_rn(0.f, 0.f);
+    uint4* dst = reinterpret_cast<uint4*>(out + idx * 32);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dst[i] = reinterpret_cast<uint4*>(pk)[i];
+}
+
+// global average pool of the last layer (NHWC bf16) averaged over each problem's images,
+// then the condition vector [emb ; (q-lo)/(hi-lo) ; goal xyz/0.6 ; quat]
+__global__ void enc_gap_cond_kernel(const __nv_bfloat16* __restrict__ feat, int n_img, int Ho, int Ho_p, int Wo,
+                                    const float* __restrict__ q, const float* __restrict__ goal, float lo, float hi,
+                                    float* __restrict__ cond) {
+    const int p = blockIdx.x, c = threadIdx.x;  // 256 threads
+    float acc = 0.f;
+    for (int m = 0; m < n_img; ++m) {
+        const __nv_bfloat16* f = feat + (size_t)(p * n_img + m) * Ho_p * Wo * 256 + c;
+        float s = 0.f;
+        for (int i = 0; i < Ho * Wo; ++i) s += __bfloat162float(f[(size_t)i * 256]);
+        acc += s / (float)(Ho * Wo);
+    }
+    cond[(size_t)p * U_COND + c] = acc / (float)n_img;
+    if (c < U_DOF) cond[(size_t)p * U_COND + 256 + c] = (q[p * U_DOF + c] - lo) / (hi - lo);
+    if (c < 3) cond[(size_t)p * U_COND + 256 + U_DOF + c] = goal[p * 7 + c] / 0.6f;
+    if (c < 4) cond[(size_t)p * U_COND + 256 + U_DOF + 3 + c] = goal[p * 7 + 3 + c];
+}
+
+// 5-D pair view of an NHWC bf16 tensor [img][Hp][W][C]: dims (2C, W/2, 2, Hp/2, img)
+static bool make_pair_map(CUtensorMap* tm, const void* base, int n_img, int Hp, int W, int C, int wx, int ry) {
+    cuuint64_t dims[5] = {(cuuint64_t)2 * C, (cuuint64_t)W / 2, 2, (cuuint64_t)Hp / 2, (cuuint64_t)n_img};
+    cuuint64_t strides[4] = {(cuuint64_t)2 * C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)2 * W * C * 2,
+                             (cuuint64_t)Hp * W * C * 2};
+    cuuint32_t box[5] = {64, (cuuint32_t)wx, 1, (cuuint32_t)ry, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+extern "C" long long ps_encode_tc_workspace_bytes(int n_images, int H, int W, int n_layers) {
+    if (n_layers < 2 || n_layers > ENC_MAXL) return -1;
+    EncLayerGeo g[ENC_MAXL];
+    enc_geometry(H, W, n_layers, g);
+    size_t mx = 0;
+    for (int l = 0; l < n_layers; ++l) mx = std::max(mx, (size_t)n_images * g[l].Ho_p * g[l].Wo * g[l].N);
+    return (long long)(2 * ((mx * 2 + 255) / 256 * 256));
+}
+
+extern "C" int ps_encode_tc(const float* images, int P, int n_img, int H, int W, const void* packed, int n_layers,
+                            const float* q_start, const float* goal, float lo, float hi, void* ws, float* cond,
+                            void* stream) {
+    if (P <= 0 || n_img <= 0 || n_layers < 2 || n_layers > ENC_MAXL || (W & 3)) return PS_FAIL(PS_ERR_SHAPE);
+    if (!get_encoder()) return PS_FAIL(PS_ERR_CUDA);
+    cudaStream_t st = (cudaStream_t)stream;
+    EncLayerGeo g[ENC_MAXL];
+    enc_geometry(H, W, n_layers, g);
+    for (int l = 1; l < n_layers; ++l)
+        if (g[l].Win & 1) return PS_FAIL(PS_ERR_SHAPE);
+    const int NI = P * n_img;
+    const size_t half = (size_t)(ps_encode_tc_workspace_bytes(NI, H, W, n_layers) / 2);
+    __nv_bfloat16* buf[2] = {reinterpret_cast<__nv_bfloat16*>(ws),
+                             reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(ws) + half)};
+    const EncLayerGeo& last = g[n_layers - 1];
+    const size_t wb = ((last.w_off + (size_t)last.N * last.n_chunks * 64) * 2 + 255) / 256 * 256;
+    const float* side = reinterpret_cast<const float*>(reinterpret_cast<const char*>(packed) + wb);
+    size_t bias_tot = 0;
+    for (int l = 0; l < n_layers; ++l) bias_tot += g[l].N;
+    const float* w1 = side + bias_tot;
+    {
+        const EncLayerGeo& e = g[0];
+        const size_t n = (size_t)NI * e.Ho_p * e.Wo;
+        enc_l1_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(images, NI, H, W, w1, side + e.b_off, e.Ho,
+                                                                    e.Wo, e.Ho_p, buf[0]);
+        PS_CHECK_LAUNCH();
+    }
+    const __nv_bfloat16* W16 = reinterpret_cast<const __nv_bfloat16*>(packed);
+    for (int l = 1; l < n_layers; ++l) {
+        const EncLayerGeo& e = g[l];
+        __nv_bfloat16* in = buf[(l - 1) & 1];
+        __nv_bfloat16* out = buf[l & 1];
+        if (e.Ho_p != e.Ho)  // zero the padding row the next layer's pair view reads
+            cudaMemsetAsync(out, 0, (size_t)NI * e.Ho_p * e.Wo * e.N * 2, st);
+        TcArgs a;
+        memset(&a, 0, sizeof(a));
+        if (!make_pair_map(&a.tmA[0], in, NI, e.Hin_p, e.Win, e.C, e.wx, e.ry)) return PS_FAIL(PS_ERR_CUDA);
+        if (!make_w_map(&a.tmW, W16 + e.w_off, e.N, e.n_chunks * 64)) return PS_FAIL(PS_ERR_CUDA);
+        int n = 0;
+        const int C = e.C;
+        for (int dy = 0; dy < 3; ++dy) {
+            const int par = dy == 1 ? 0 : 1, dt = dy == 0 ? -1 : 0;
+            const int segA = C == 32 ? 1 : C / 64;
+            for (int ci = 0; ci < segA; ++ci) {
+                TcChunk ch{};
+                ch.c = (int16_t)(C == 32 ? 0 : C + 64 * ci);
+                ch.kcol = (int16_t)(64 * n);
+                ch.dt = (int8_t)dt;
+                ch.par = (int8_t)par;
+                ch.dx = -1;
+                ch.first = n == 0;
+                a.chunk[n++] = ch;
+            }
+            for (int ci = 0; ci < 2 * C / 64; ++ci) {
+                TcChunk ch{};
+                ch.c = (int16_t)(64 * ci);
+                ch.kcol = (int16_t)(64 * n);
+                ch.dt = (int8_t)dt;
+                ch.par = (int8_t)par;
+                ch.dx = 0;
+                ch.first = n == 0;
+                a.chunk[n++] = ch;
+            }
+        }
+        if (n != e.n_chunks || n > TC_MAX_CHUNKS) return PS_FAIL(PS_ERR_SHAPE);
+        a.n_chunks = n;
+        a.geom = 1;
+        a.rows = NI * e.tiles_x * e.tiles_y;   // number of tiles
+        a.Tv = 1;
+        a.S = 1;
+        a.Ho = e.Ho;
+        a.Wo = e.Wo;
+        a.Hp = e.Ho_p;
+        a.wx = e.wx;
+        a.ry = e.ry;
+        a.tiles_x = e.tiles_x;
+        a.tiles_y = e.tiles_y;
+        a.bias = side + e.b_off;
+        a.out = out;
+        int s;
+        if (e.N == 64)
+            s = launch_tc<64, EPI_RELU2D, false>(a, a.rows, st);
+        else if (e.N == 128)
+            s = launch_tc<128, EPI_RELU2D, false>(a, a.rows, st);
+        else
+            s = launch_tc<256, EPI_RELU2D, false>(a, a.rows, st);
+        if (s) return s;
+    }
+    enc_gap_cond_kernel<<<P, 256, 0, st>>>(buf[(n_layers - 1) & 1], n_img, last.Ho, last.Ho_p, last.Wo, q_start, goal,
+                                           lo, hi, cond);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
 }  // namespace ps

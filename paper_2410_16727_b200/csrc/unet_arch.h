@@ -32,7 +32,7 @@ struct PSeg {
     int k0;    // first packed K row
 };
 
-enum Epi { EPI_PLAIN = 0, EPI_GN_FILM = 1, EPI_GN_RES = 2, EPI_FINAL = 3 };
+enum Epi { EPI_PLAIN = 0, EPI_GN_FILM = 1, EPI_GN_RES = 2, EPI_FINAL = 3, EPI_RELU2D = 4 };
 
 struct PConv {
     int K = 0, N = 0;

@@ -57,8 +57,24 @@ class SeedSampler:
         return self._ws
 
     # ------------------------------------------------------------------ API
+    def _enc_packed(self, H: int, W: int):
+        torch = _lib.require_cuda()
+        key = (H, W)
+        if getattr(self, "_encp", None) is None:
+            self._encp = {}
+        if key not in self._encp:
+            L = _lib.lib()
+            nl = len(self.enc.channels)
+            buf = torch.empty(int(L.ps_encoder_packed_bytes(H, W, nl)), dtype=torch.uint8, device="cuda")
+            _lib.check(L.ps_encoder_pack(_lib.ptr(self.enc_w), H, W, nl, _lib.ptr(buf),
+                                         _lib.stream_handle()), "encoder_pack")
+            self._encp[key] = buf
+        return self._encp[key]
+
     def encode(self, images, q_start, goal, stream=None):
-        """images (P, n_img, H, W) depth metres; q_start (P,7); goal (P,7) -> cond (P,270)."""
+        """images (P, n_img, H, W) depth metres; q_start (P,7); goal (P,7) -> cond (P,270).
+
+        mode 1 runs the tcgen05 encoder (bf16 activations), mode 0 the fp32 SIMT one."""
         torch = _lib.require_cuda()
         from .bl import _dev
         im = _dev(images)
@@ -66,6 +82,17 @@ class SeedSampler:
         q, g = _dev(q_start), _dev(goal)
         L = _lib.lib()
         nl = len(self.enc.channels)
+        if self.mode == 1:
+            packed = self._enc_packed(H, W)
+            nb = int(L.ps_encode_tc_workspace_bytes(P * n_img, H, W, nl))
+            if getattr(self, "_encws", None) is None or self._encws.numel() < nb:
+                self._encws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+            cond = torch.empty((P, spec.COND_DIM), dtype=torch.float32, device="cuda")
+            st = L.ps_encode_tc(_lib.ptr(im), P, n_img, H, W, _lib.ptr(packed), nl, _lib.ptr(q),
+                                _lib.ptr(g), -spec.JOINT_LIMIT, spec.JOINT_LIMIT, _lib.ptr(self._encws),
+                                _lib.ptr(cond), _lib.stream_handle(stream))
+            _lib.check(st, "encode_tc")
+            return cond
         ws = torch.empty(int(L.ps_encode_workspace_bytes(P * n_img, H, W, nl)), dtype=torch.uint8,
                          device="cuda")
         cond = torch.empty((P, spec.COND_DIM), dtype=torch.float32, device="cuda")

@@ -32,3 +32,15 @@ for P, S in [(128, 32), (1024, 32)]:
     e1 = s1.predict_noise(x, 40, s1.film(cond), S).cpu().numpy()
     d = e1 - e0
     print(f"P{P}: bf16 vs fp32 max {np.abs(d).max():.3e} rms {np.sqrt((d**2).mean()):.3e}", flush=True)
+
+# tcgen05 encoder vs fp32 SIMT encoder vs oracle
+from paper_2410_16727_b200 import synth
+for enc, maker in ((spec.ENCODER_CFG0, synth.config0_problems), (spec.ENCODER_CFG3, synth.config3_problems)):
+    pe = spec.random_model(enc)
+    a0, a1 = SeedSampler(pe, enc, mode=0), SeedSampler(pe, enc, mode=1)
+    pb = maker(3, seed=1)
+    c0 = a0.encode(pb.images, pb.q_start, pb.goal).cpu().numpy()
+    c1 = a1.encode(pb.images, pb.q_start, pb.goal).cpu().numpy()
+    want = un.encode_problems(pe, enc, pb.images, pb.q_start, pb.goal)
+    print(f"encoder {len(enc.channels)}L: fp32 max {np.abs(c0-want).max():.2e} | bf16 max {np.abs(c1-want).max():.3e}"
+          f" rel {np.abs(c1-want)[:, :256].max() / np.abs(want[:, :256]).max():.3e}", flush=True)
