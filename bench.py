@@ -191,13 +191,14 @@ def main():
     import numpy as np
 
     from paper_2410_16727_b200 import _lib, spec, synth
+    from paper_2410_16727_b200 import dist as psd
     from paper_2410_16727_b200.planner import BLPlanner
 
     # weak scaling: every rank plans its own `--problems` problems (global indices
     # [rank*P, (rank+1)*P)); the whole job is P*N problems.
     P, S, T = args.problems, args.seeds, args.horizon
     P_all = P * world
-    p0 = rank * P
+    p0, _ = psd.shard(rank, world, P)
     steps = None if args.schedule == "ddpm100" else spec.strided_steps(100, 10)
     mode = 1 if args.mode == "bf16" else 0
     params = spec.random_model(spec.ENCODER_CFG3)
@@ -211,21 +212,9 @@ def main():
     d_goal, d_boxes = h_goal.to(dev), h_boxes.to(dev)
 
     # gather buffers (rank 0 receives every rank's trajectories, costs, flags, best)
-    gbufs = None
-    if world > 1 and rank == 0:
-        gbufs = [[torch.empty((world,) + shp, dtype=dt, device=dev)]
-                 for shp, dt in (((P * S, T, 7), torch.float32), ((P * S,), torch.float32),
-                                 ((P * S,), torch.uint8), ((P,), torch.int32))]
-
     def gather(r):
         # the only collective: final results of every rank to rank 0 (NCCL gather)
-        if world == 1:
-            return
-        for i, t in enumerate((r.trajectories, r.cost, r.feasible, r.best_index)):
-            if rank == 0:
-                dist.gather(t.contiguous(), list(gbufs[i][0].unbind(0)), dst=0)
-            else:
-                dist.gather(t.contiguous(), None, dst=0)
+        psd.gather_to_rank0([r.trajectories, r.cost, r.feasible, r.best_index], rank, world)
 
     ev = {"sample_start": torch.cuda.Event(enable_timing=True),
           "sample_end": torch.cuda.Event(enable_timing=True)}
