@@ -119,6 +119,49 @@ int ps_sample(const void* packed, int mode, const float* film_a, int P, int S, i
 /* n standard normals of the sampler's noise stream (test hook). */
 int ps_noise_probe(float* out, int n, int step, int prob, int seed, unsigned key, void* stream);
 
+/* ============ Reference profile: planseed's own planar / FC / DDIM path ============
+ * dtype 0 = float64 (parity with planseed), 1 = float32.  Argument lists follow the
+ * numba kernels' 18 positional args (src/_kernels.py:165-176, built by _kernel_args,
+ * src/trajopt.py:89-98); host arrays end in _h, the grid and the (T,T) jerk operators
+ * are device arrays of `dtype`. */
+#define PS_REF_ARM_ARGS                                                                   \
+    const double *lengths_h, double basex, double basey, const double *fracs_h, int M,   \
+        const long long *pair_a_h, const long long *pair_b_h, int n_pairs,               \
+        const void *grid, int nx, int ny, double gox, double goy, double gh,             \
+        double goal_x, double goal_y, double goal_th, const double *weights_h,           \
+        double d_act, double d_self, const void *jerk_mat, const void *jerk_quad
+
+/* _kernels.cost_terms_batch (src/_kernels.py:165-312) */
+int ps_ref_cost_terms(int dtype, const void* qs, int S, int T, int D, PS_REF_ARM_ARGS, int want_grad,
+                      void* terms, void* totals, void* grads, uint8_t* clamped, void* stream);
+/* _kernels.optimize_batch (src/_kernels.py:315-431) */
+int ps_ref_optimize(int dtype, const void* seeds, int S, int T, int D, int n_iters, double momentum,
+                    double armijo_c, double shrink, int max_backtracks, double alpha0, double alpha_max,
+                    PS_REF_ARM_ARGS, void* x_out, void* terms, void* totals, uint8_t* frozen,
+                    long long* n_accepted, void* stream);
+/* pipeline.build_planner_esdf (src/pipeline.py:101-132): discs at the scan's hit points */
+int ps_ref_planner_esdf(const double* depths, int n_rays, double sx, double sy, double heading, double fov,
+                        double max_range, double r_disc, double cap, double ox, double oy, double h, int nx,
+                        int ny, double* out, void* stream);
+/* pipeline.planner_success (src/pipeline.py:139-157), float64, one flag per seed */
+int ps_ref_planner_success(const double* trajs, int S, int T, int D, PS_REF_ARM_ARGS, double delta_t,
+                           double delta_r_deg, int interp, uint8_t* ok, void* stream);
+/* pipeline.select_best (src/pipeline.py:160-165) over float64 costs */
+int ps_ref_select(const double* cost, const uint8_t* ok, int P, int S, int* best, void* stream);
+/* denoiser / encoder building blocks (src/diffusion.py:207-300, autodiff.py:226-251) */
+int ps_ref_linear(const double* x, int ldx, const double* W, const double* b, int R, int K, int N, int act,
+                  double* y, int ldy, void* stream);
+int ps_ref_film(double* h, const double* scale, const double* shift, int R, int N, void* stream);
+int ps_ref_conv1d_silu(const double* x, int C, int L, const double* w, const double* b, int O, int K,
+                       int stride, double* y, void* stream);
+int ps_ref_sinusoid(double k, int half, double* out, void* stream);
+int ps_ref_div(const double* x, int n, double d, double* y, void* stream);
+/* DDIM step (src/diffusion.py:547-555) and denormalise + row-0 pin (:559-569) */
+int ps_ref_ddim_update(double* x, const double* eps, int n, double ab, double ab_next, int has_next,
+                       double clip_lo, double clip_hi, double* x0_out, void* stream);
+int ps_ref_denorm_pin(const double* x0, int B, int T, int D, const double* lo, const double* hi,
+                      const double* q0, double* traj, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,6 +17,11 @@ from . import build as _build
 PS_OK, PS_ERR_OUT_OF_GRID, PS_ERR_SHAPE, PS_ERR_CUDA = 0, 1, 2, 3
 
 _c_int, _c_ll, _c_f, _vp = ctypes.c_int, ctypes.c_longlong, ctypes.c_float, ctypes.c_void_p
+_c_d = ctypes.c_double
+# lengths, basex, basey, fracs, M, pair_a, pair_b, n_pairs, grid, nx, ny, gox, goy, gh,
+# goal_x, goal_y, goal_th, weights, d_act, d_self, jerk_mat, jerk_quad
+_REF_ARM = [_vp, _c_d, _c_d, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _c_int, _c_d, _c_d, _c_d,
+            _c_d, _c_d, _c_d, _vp, _c_d, _c_d, _vp, _vp]
 
 # name -> argtypes ; every function returns int (status) unless listed in _RESTYPE
 _SIGS = {
@@ -42,6 +47,21 @@ _SIGS = {
     "ps_sample": [_vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int,
                   ctypes.c_uint, _vp, _c_f, _c_f, _vp, _vp, _vp],
     "ps_noise_probe": [_vp, _c_int, _c_int, _c_int, _c_int, ctypes.c_uint, _vp],
+    "ps_ref_cost_terms": [_c_int, _vp, _c_int, _c_int, _c_int] + _REF_ARM + [_c_int, _vp, _vp, _vp, _vp,
+                                                                          _vp],
+    "ps_ref_optimize": [_c_int, _vp, _c_int, _c_int, _c_int, _c_int, _c_d, _c_d, _c_d, _c_int, _c_d, _c_d]
+                       + _REF_ARM + [_vp, _vp, _vp, _vp, _vp, _vp],
+    "ps_ref_planner_esdf": [_vp, _c_int, _c_d, _c_d, _c_d, _c_d, _c_d, _c_d, _c_d, _c_d, _c_d, _c_d, _c_int,
+                            _c_int, _vp, _vp],
+    "ps_ref_planner_success": [_vp, _c_int, _c_int, _c_int] + _REF_ARM + [_c_d, _c_d, _c_int, _vp, _vp],
+    "ps_ref_select": [_vp, _vp, _c_int, _c_int, _vp, _vp],
+    "ps_ref_linear": [_vp, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
+    "ps_ref_film": [_vp, _vp, _vp, _c_int, _c_int, _vp],
+    "ps_ref_conv1d_silu": [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp],
+    "ps_ref_sinusoid": [_c_d, _c_int, _vp, _vp],
+    "ps_ref_div": [_vp, _c_int, _c_d, _vp, _vp],
+    "ps_ref_ddim_update": [_vp, _vp, _c_int, _c_d, _c_d, _c_int, _c_d, _c_d, _vp, _vp],
+    "ps_ref_denorm_pin": [_vp, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp],
     "ps_encoder_packed_bytes": [_c_int, _c_int, _c_int],
     "ps_encoder_pack": [_vp, _c_int, _c_int, _c_int, _vp, _vp],
     "ps_encode_tc_workspace_bytes": [_c_int, _c_int, _c_int, _c_int],

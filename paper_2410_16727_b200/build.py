@@ -17,7 +17,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 BASE = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-diag-suppress", "128",
         "-I", str(PKG.parent / "include")]
 # Files whose arithmetic must match the canonical-fp32 oracle bit for bit.
-NO_FMAD = {"bl_refine.cu"}
+NO_FMAD = {"bl_refine.cu", "ref_kernels.cu"}
 
 
 def nvcc() -> str:

@@ -1,0 +1,768 @@
+// Reference-profile ("ref") kernels: planseed's own planar arm, 5-term cost, momentum +
+// Armijo optimiser, FC denoiser, scan encoder, scan-derived ESDF and planner_success,
+// on the GPU behind the numba/numpy signatures.  Templated on the scalar type: the
+// double instantiation is the parity mode against planseed itself (compiled with
+// --fmad=false and the reference's evaluation order, so results agree to ~1e-13), the
+// float instantiation the fast mode.
+//
+// Reference: src/_kernels.py:18-57 (_wrap, _bilinear), :165-312 (cost_terms_batch),
+// :315-431 (optimize_batch); src/diffusion.py:207-300 (features, encoder, denoiser);
+// src/pipeline.py:101-157 (planner ESDF, planner_success).
+#include <cuda_bf16.h>
+
+#include <cmath>
+
+#include "common.cuh"
+
+namespace ps {
+namespace ref {
+
+constexpr int MAXD = 8;        // joints
+constexpr int MAXM = 8;        // points per link
+constexpr int MAXP = MAXD * MAXM;
+constexpr int MAXPAIR = 512;
+constexpr int MAXT = 64;       // waypoints
+
+template <typename F>
+struct ArmGrid {
+    int D, M, n_pairs;
+    F lengths[MAXD];
+    F fracs[MAXM];
+    F basex, basey;
+    short pair_a[MAXPAIR], pair_b[MAXPAIR];
+    const F* grid;
+    int nx, ny;
+    F gox, goy, gh;
+    F goal_x, goal_y, goal_th;
+    F w[5];
+    F d_act, d_self;
+    const F* jerk_mat;   // (T,T)
+    const F* jerk_quad;  // (T,T)
+};
+
+// Python float modulo (CPython float_rem): sign follows the divisor.
+template <typename F>
+__device__ __forceinline__ F py_mod(F a, F b) {
+    F m = fmod(a, b);
+    if (m != F(0)) {
+        if ((b < F(0)) != (m < F(0))) m += b;
+    } else {
+        m = copysign(F(0), b);
+    }
+    return m;
+}
+
+template <typename F>
+__device__ __forceinline__ F wrap(F th) {
+    const F pi = F(3.141592653589793238462643383279502884);
+    return pi - py_mod(pi - th, F(2) * pi);
+}
+
+template <typename F>
+__device__ __forceinline__ F floorT(F x) { return floor(x); }
+
+// _bilinear (src/_kernels.py:23-57), same expression order
+template <typename F>
+__device__ void bilinear(const ArmGrid<F>& A, F x, F y, F& d, F& dgx, F& dgy, bool& clamped) {
+    const int nx = A.nx, ny = A.ny;
+    const F gx = (x - A.gox) / A.gh;
+    const F gy = (y - A.goy) / A.gh;
+    clamped = gx < F(0) || gx > F(nx - 1) || gy < F(0) || gy > F(ny - 1);
+    // int(np.floor(gx)) then clamp; guard the conversion for far-out points
+    F fx = floorT(gx), fy = floorT(gy);
+    int i = fx < F(0) ? -1 : (fx > F(nx) ? nx : (int)fx);
+    int j = fy < F(0) ? -1 : (fy > F(ny) ? ny : (int)fy);
+    if (i < 0) i = 0; else if (i > nx - 2) i = nx - 2;
+    if (j < 0) j = 0; else if (j > ny - 2) j = ny - 2;
+    F tx = gx - F(i), ty = gy - F(j);
+    if (tx < F(0)) tx = F(0); else if (tx > F(1)) tx = F(1);
+    if (ty < F(0)) ty = F(0); else if (ty > F(1)) ty = F(1);
+    const F* v = A.grid;
+    const F v00 = v[(size_t)i * ny + j], v10 = v[(size_t)(i + 1) * ny + j];
+    const F v01 = v[(size_t)i * ny + j + 1], v11 = v[(size_t)(i + 1) * ny + j + 1];
+    d = v00 * (1 - tx) * (1 - ty) + v10 * tx * (1 - ty) + v01 * (1 - tx) * ty + v11 * tx * ty;
+    dgx = ((v10 - v00) * (1 - ty) + (v11 - v01) * ty) / A.gh;
+    dgy = ((v01 - v00) * (1 - tx) + (v11 - v10) * tx) / A.gh;
+}
+
+// Per-warp scratch in shared memory for one seed.
+template <typename F>
+struct SeedScratch {
+    F world[MAXT][MAXP];   // per (t, p) world-term contributions (0 when inactive)
+    F self_[MAXT];
+    F smooth[MAXD][MAXT];
+    F goal_pos, goal_rot;
+    int clamped;
+};
+
+// One waypoint (lane-owned): world + self + goal terms and the joint gradient
+// (goal-rot part, then the backward accumulation), as cost_terms_batch does.
+template <typename F>
+__device__ void waypoint_terms(const ArmGrid<F>& A, const F* q, int t, int T, bool want_grad,
+                               SeedScratch<F>& sc, F* gq) {
+    const int D = A.D, M = A.M, P = D * M;
+    F ox[MAXD + 1], oy[MAXD + 1], px[MAXP], py[MAXP], gpx[MAXP], gpy[MAXP], cth[MAXD];
+    F th = 0;
+    ox[0] = A.basex;
+    oy[0] = A.basey;
+    for (int k = 0; k < D; ++k) {
+        th += q[k];
+        cth[k] = th;
+        const F c = cos(th), si = sin(th);
+        for (int i = 0; i < M; ++i) {
+            const int p = k * M + i;
+            px[p] = ox[k] + A.fracs[i] * A.lengths[k] * c;
+            py[p] = oy[k] + A.fracs[i] * A.lengths[k] * si;
+        }
+        ox[k + 1] = ox[k] + A.lengths[k] * c;
+        oy[k + 1] = oy[k] + A.lengths[k] * si;
+    }
+    for (int p = 0; p < P; ++p) gpx[p] = gpy[p] = 0;
+    bool any_point_grad = false;
+    const F w_gp = A.w[0], w_gr = A.w[1], w_self = A.w[3], w_world = A.w[4];
+    for (int p = 0; p < P; ++p) sc.world[t][p] = 0;
+    if (w_world > F(0)) {
+        for (int p = 0; p < P; ++p) {
+            F dv, dgx, dgy;
+            bool cl;
+            bilinear(A, px[p], py[p], dv, dgx, dgy, cl);
+            if (cl) sc.clamped = 1;
+            const F hinge = A.d_act - dv;
+            if (hinge > F(0)) {
+                sc.world[t][p] = w_world * hinge * hinge;
+                if (want_grad) {
+                    gpx[p] += F(-2.0) * w_world * hinge * dgx;
+                    gpy[p] += F(-2.0) * w_world * hinge * dgy;
+                    any_point_grad = true;
+                }
+            }
+        }
+    }
+    sc.self_[t] = 0;
+    if (w_self > F(0) && A.n_pairs > 0) {
+        F best = F(1e300 > 3e38 && sizeof(F) == 4 ? 3.0e38 : 1e300);
+        int best_i = 0;
+        for (int e = 0; e < A.n_pairs; ++e) {
+            const int a = A.pair_a[e], b = A.pair_b[e];
+            const F dx = px[a] - px[b], dy = py[a] - py[b];
+            const F dd = dx * dx + dy * dy;
+            if (dd < best) {
+                best = dd;
+                best_i = e;
+            }
+        }
+        const F mind = sqrt(best);
+        const F hinge = A.d_self - mind;
+        if (hinge > F(0)) {
+            sc.self_[t] = w_self * hinge * hinge;
+            if (want_grad && mind > F(1e-12)) {
+                const int a = A.pair_a[best_i], b = A.pair_b[best_i];
+                const F scale = F(-2.0) * w_self * hinge / mind;
+                gpx[a] += scale * (px[a] - px[b]);
+                gpy[a] += scale * (py[a] - py[b]);
+                gpx[b] += -scale * (px[a] - px[b]);
+                gpy[b] += -scale * (py[a] - py[b]);
+                any_point_grad = true;
+            }
+        }
+    }
+    for (int k = 0; k < D; ++k) gq[k] = 0;
+    F ee_gx = 0, ee_gy = 0;
+    if (t == T - 1) {
+        const F ex = ox[D] - A.goal_x, ey = oy[D] - A.goal_y;
+        sc.goal_pos = w_gp * (ex * ex + ey * ey);
+        const F dth = wrap(cth[D - 1] - A.goal_th);
+        sc.goal_rot = w_gr * dth * dth;
+        if (want_grad) {
+            ee_gx = F(2.0) * w_gp * ex;
+            ee_gy = F(2.0) * w_gp * ey;
+            for (int k = 0; k < D; ++k) gq[k] += F(2.0) * w_gr * dth;
+        }
+    }
+    if (want_grad && (any_point_grad || ee_gx != F(0) || ee_gy != F(0))) {
+        F acc = ee_gy * ox[D] - ee_gx * oy[D];
+        F bx = ee_gx, by = ee_gy;
+        for (int k = D - 1; k >= 0; --k) {
+            for (int i = 0; i < M; ++i) {
+                const int p = k * M + i;
+                acc += gpy[p] * px[p] - gpx[p] * py[p];
+                bx += gpx[p];
+                by += gpy[p];
+            }
+            gq[k] += acc - ox[k] * by + oy[k] * bx;
+        }
+    }
+}
+
+// Full cost of one seed by one warp.  q: smem (T, D).  grad (optional): smem (T, D).
+// Returns total (all lanes), writes terms[5] (lane 0) and clamped.
+template <typename F>
+__device__ F seed_cost(const ArmGrid<F>& A, const F* q, int T, bool want_grad, SeedScratch<F>& sc, F* grad,
+                       F* terms, int& clamped) {
+    const int lane = threadIdx.x & 31;
+    const int D = A.D, P = A.D * A.M;
+    if (lane == 0) {
+        sc.clamped = 0;
+        sc.goal_pos = sc.goal_rot = 0;
+    }
+    __syncwarp();
+    for (int t = lane; t < T; t += 32) {
+        F gq[MAXD];
+        waypoint_terms(A, q + t * D, t, T, want_grad, sc, gq);
+        if (want_grad)
+            for (int k = 0; k < D; ++k) grad[t * D + k] = gq[k];
+    }
+    __syncwarp();
+    // smoothness: y = J q per (k, r); gradient w_sm * (2 J^T J q)
+    const F w_sm = A.w[2];
+    if (w_sm > F(0)) {
+        for (int idx = lane; idx < D * T; idx += 32) {
+            const int k = idx / T, r = idx % T;
+            F y = 0;
+            for (int c = 0; c < T; ++c) y += A.jerk_mat[r * T + c] * q[c * D + k];
+            sc.smooth[k][r] = w_sm * y * y;
+        }
+        __syncwarp();
+        if (want_grad) {
+            for (int idx = lane; idx < D * T; idx += 32) {
+                const int k = idx / T, r = idx % T;
+                F g = 0;
+                for (int c = 0; c < T; ++c) g += A.jerk_quad[r * T + c] * q[c * D + k];
+                grad[r * D + k] += w_sm * g;
+            }
+        }
+    }
+    __syncwarp();
+    F total = 0;
+    if (lane == 0) {
+        F tw = 0, ts = 0, tsm = 0;
+        for (int t = 0; t < T; ++t)
+            for (int p = 0; p < P; ++p) tw += sc.world[t][p];
+        for (int t = 0; t < T; ++t) ts += sc.self_[t];
+        if (w_sm > F(0))
+            for (int k = 0; k < D; ++k)
+                for (int r = 0; r < T; ++r) tsm += sc.smooth[k][r];
+        terms[0] = sc.goal_pos;
+        terms[1] = sc.goal_rot;
+        terms[2] = tsm;
+        terms[3] = ts;
+        terms[4] = tw;
+        total = terms[0] + terms[1] + terms[2] + terms[3] + terms[4];
+    }
+    if (want_grad)
+        for (int k = lane; k < D; k += 32) grad[k] = 0;  // row 0 pinned
+    __syncwarp();
+    clamped = sc.clamped;
+    return __shfl_sync(PS_FULL, total, 0);
+}
+
+template <typename F>
+struct SeedSmem {
+    SeedScratch<F> sc;
+    F q[MAXT * MAXD];
+    F g[MAXT * MAXD];
+    F v[MAXT * MAXD];
+    F cand[MAXT * MAXD];
+    F terms[5];
+};
+
+template <typename F>
+__global__ void __launch_bounds__(32) cost_kernel(const __grid_constant__ ArmGrid<F> A, const F* __restrict__ qs, int S,
+                                                  int T, int want_grad, F* terms_out, F* totals, F* grads,
+                                                  uint8_t* clamped) {
+    extern __shared__ __align__(16) uint8_t smraw[];
+    SeedSmem<F>& sm = *reinterpret_cast<SeedSmem<F>*>(smraw);
+    const int s = blockIdx.x, lane = threadIdx.x;
+    const int n = T * A.D;
+    for (int i = lane; i < n; i += 32) sm.q[i] = qs[(size_t)s * n + i];
+    __syncwarp();
+    int cl;
+    const F tot = seed_cost(A, sm.q, T, want_grad != 0, sm.sc, sm.g, sm.terms, cl);
+    __syncwarp();
+    if (lane == 0) {
+        for (int i = 0; i < 5; ++i) terms_out[s * 5 + i] = sm.terms[i];
+        totals[s] = tot;
+        clamped[s] = (uint8_t)(cl ? 1 : 0);
+    }
+    for (int i = lane; i < n; i += 32) grads[(size_t)s * n + i] = want_grad ? sm.g[i] : F(0);
+}
+
+// optimize_batch (src/_kernels.py:315-431): one warp per seed, identical control flow.
+template <typename F>
+__global__ void __launch_bounds__(32) optimize_kernel(const __grid_constant__ ArmGrid<F> A, const F* __restrict__ seeds,
+                                                      int S, int T, int n_iters, F momentum, F armijo_c, F shrink,
+                                                      int max_backtracks, F alpha0, F alpha_max, F* x_out,
+                                                      F* terms_out, F* totals, uint8_t* frozen_out,
+                                                      long long* n_acc_out) {
+    extern __shared__ __align__(16) uint8_t smraw[];
+    SeedSmem<F>& sm = *reinterpret_cast<SeedSmem<F>*>(smraw);
+    const int s = blockIdx.x, lane = threadIdx.x;
+    const int n = T * A.D;
+    for (int i = lane; i < n; i += 32) {
+        sm.q[i] = seeds[(size_t)s * n + i];
+        sm.v[i] = 0;
+    }
+    __syncwarp();
+    F alpha = alpha0;
+    bool frozen = false;
+    long long n_acc = 0;
+    int cl;
+    F f = seed_cost(A, sm.q, T, true, sm.sc, sm.g, sm.terms, cl);
+    const F INF = F(INFINITY);
+    for (int it = 0; it < n_iters; ++it) {
+        if (frozen) break;  // a frozen seed never changes again (the batch loop skips it)
+        if (it > 0) {
+            F dummy_terms[5];
+            (void)dummy_terms;
+            seed_cost(A, sm.q, T, true, sm.sc, sm.g, sm.terms, cl);
+        }
+        __syncwarp();
+        // gmax and vzero (order-independent)
+        F gmax = 0;
+        bool vzero = true;
+        for (int i = lane; i < n; i += 32) {
+            const F ag = fabs(sm.g[i]);
+            if (ag > gmax) gmax = ag;
+            if (sm.v[i] != F(0)) vzero = false;
+        }
+        for (int off = 16; off; off >>= 1) gmax = fmax(gmax, __shfl_xor_sync(PS_FULL, gmax, off));
+        vzero = __all_sync(PS_FULL, vzero);
+        if (gmax < F(1e-12)) {
+            frozen = true;
+            continue;
+        }
+        bool fresh = vzero;
+        for (int i = lane; i < n; i += 32) sm.v[i] = momentum * sm.v[i] - sm.g[i];
+        __syncwarp();
+        F dd = 0;
+        if (lane == 0)
+            for (int i = 0; i < n; ++i) dd += sm.g[i] * sm.v[i];
+        dd = __shfl_sync(PS_FULL, dd, 0);
+        if (dd >= F(0)) {
+            fresh = true;
+            for (int i = lane; i < n; i += 32) sm.v[i] = -sm.g[i];
+            __syncwarp();
+            dd = 0;
+            if (lane == 0)
+                for (int i = 0; i < n; ++i) dd -= sm.g[i] * sm.g[i];
+            dd = __shfl_sync(PS_FULL, dd, 0);
+        }
+        F a = alpha * F(2.0);
+        if (a > alpha_max) a = alpha_max;
+        bool accepted = false;
+        F fc = 0;
+        for (int bt = 0; bt < max_backtracks; ++bt) {
+            for (int i = lane; i < n; i += 32) sm.cand[i] = sm.q[i] + a * sm.v[i];
+            __syncwarp();
+            int clc;
+            F totc = seed_cost(A, sm.cand, T, false, sm.sc, sm.g + 0 /*unused*/, sm.terms, clc);
+            fc = clc ? INF : totc;
+            if (fc <= f + armijo_c * a * dd) {
+                accepted = true;
+                break;
+            }
+            a *= shrink;
+        }
+        if (accepted) {
+            for (int i = lane; i < n; i += 32) sm.q[i] = sm.q[i] + a * sm.v[i];
+            f = fc;
+            alpha = a;
+            n_acc += 1;
+        } else {
+            for (int i = lane; i < n; i += 32) sm.v[i] = 0;
+            if (fresh) frozen = true;
+        }
+        __syncwarp();
+    }
+    const F tot = seed_cost(A, sm.q, T, false, sm.sc, sm.g, sm.terms, cl);
+    for (int i = lane; i < n; i += 32) x_out[(size_t)s * n + i] = sm.q[i];
+    if (lane == 0) {
+        for (int i = 0; i < 5; ++i) terms_out[s * 5 + i] = sm.terms[i];
+        totals[s] = tot;
+        frozen_out[s] = frozen ? 1 : 0;
+        n_acc_out[s] = n_acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// scan-derived planner ESDF (src/pipeline.py:101-132; geometry.py:130-152, :270-276)
+// ---------------------------------------------------------------------------
+__global__ void planner_esdf_kernel(const double* __restrict__ depths, int n_rays, double sx, double sy,
+                                    double heading, double fov, double max_range, double r_disc, double cap,
+                                    double ox, double oy, double h, int nx, int ny, double* __restrict__ out) {
+    __shared__ double cx[1024], cy[1024];
+    __shared__ int n_hit;
+    if (threadIdx.x == 0) {
+        // np.linspace(-fov/2, fov/2, n) then hit filter (depth < max_range - 1e-9), in ray order
+        int m = 0;
+        const double start = -fov / 2, stop = fov / 2;
+        const double step = (stop - start) / (double)(n_rays - 1);
+        for (int i = 0; i < n_rays && m < 1024; ++i) {
+            const double d = depths[i];
+            if (d < max_range - 1e-9) {
+                const double lin = (i == n_rays - 1) ? stop : start + (double)i * step;
+                const double ang = heading + lin;
+                cx[m] = sx + d * cos(ang);
+                cy[m] = sy + d * sin(ang);
+                ++m;
+            }
+        }
+        n_hit = m;
+    }
+    __syncthreads();
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nx * ny) return;
+    const int i = idx / ny, j = idx % ny;
+    const double x = ox + h * (double)i, y = oy + h * (double)j;
+    double best = cap;
+    if (n_hit > 0) {
+        double mn = INFINITY;
+        for (int k = 0; k < n_hit; ++k) {
+            const double dc = hypot(x - cx[k], y - cy[k]) - r_disc;
+            mn = fmin(mn, dc);
+        }
+        best = fmin(best, mn);
+    }
+    out[idx] = best;
+}
+
+// planner_success (src/pipeline.py:139-157): one thread per seed.
+__global__ void planner_success_kernel(const __grid_constant__ ArmGrid<double> A, const double* __restrict__ trajs,
+                                       int S, int T, double delta_t, double delta_r_deg, int interp,
+                                       uint8_t* __restrict__ ok) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= S) return;
+    const int D = A.D, M = A.M;
+    const double* tr = trajs + (size_t)s * T * D;
+    double dmin = INFINITY;
+    for (int f = 0; f <= interp; ++f) {
+        const double fr = f == 0 ? 0.0 : (double)f / (double)(interp + 1);
+        const int rows = f == 0 ? T : T - 1;
+        for (int t = 0; t < rows; ++t) {
+            double q[MAXD], th = 0, lx[MAXD], ly[MAXD], cx = 0, cy = 0;
+            for (int k = 0; k < D; ++k) q[k] = f == 0 ? tr[t * D + k] : tr[t * D + k] + fr * (tr[(t + 1) * D + k] - tr[t * D + k]);
+            for (int k = 0; k < D; ++k) {
+                th += q[k];
+                lx[k] = A.lengths[k] * cos(th);
+                ly[k] = A.lengths[k] * sin(th);
+            }
+            for (int k = 0; k < D; ++k) {
+                cx += lx[k];
+                cy += ly[k];
+                const double prex = cx - lx[k], prey = cy - ly[k];  // cumsum(lx) - lx
+                for (int i = 0; i < M; ++i) {
+                    const double px = A.basex + prex + A.fracs[i] * lx[k];
+                    const double py = A.basey + prey + A.fracs[i] * ly[k];
+                    double d, gx, gy;
+                    bool cl;
+                    bilinear(A, px, py, d, gx, gy, cl);
+                    dmin = fmin(dmin, d);
+                }
+            }
+        }
+    }
+    bool good = dmin > 0.0;
+    if (good) {
+        double th = 0, x = 0, y = 0;
+        for (int k = 0; k < D; ++k) {
+            th += tr[(T - 1) * D + k];
+            x += A.lengths[k] * cos(th);
+            y += A.lengths[k] * sin(th);
+        }
+        x += A.basex;
+        y += A.basey;
+        const double terr = hypot(x - A.goal_x, y - A.goal_y);
+        const double aerr = fabs(wrap(th - A.goal_th)) * (180.0 / 3.141592653589793238462643383279502884);
+        good = terr <= delta_t && aerr <= delta_r_deg;
+    }
+    ok[s] = good ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// FC denoiser (src/diffusion.py:272-300) and scan encoder (:246-269), fp64
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double silu(double x) { return x * (1.0 / (1.0 + exp(-x))); }
+
+// y[r, n] = act(b[n] + sum_k x[r, k] W[k, n]); W (K, N) row-major ("in, out")
+__global__ void linear_f64_kernel(const double* __restrict__ x, int ldx, const double* __restrict__ W,
+                                  const double* __restrict__ b, int R, int K, int N, int act,
+                                  double* __restrict__ y, int ldy) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+    if (n >= N || r >= R) return;
+    double acc = 0;
+    const double* xr = x + (size_t)r * ldx;
+    for (int k = 0; k < K; ++k) acc += xr[k] * W[(size_t)k * N + n];
+    acc += b[n];
+    y[(size_t)r * ldy + n] = act ? silu(acc) : acc;
+}
+
+// h = h * (1 + scale) + shift, scale/shift rows broadcast (mod is shared by the batch)
+__global__ void film_f64_kernel(double* __restrict__ h, const double* __restrict__ scale,
+                                const double* __restrict__ shift, int R, int N) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+    if (n >= N || r >= R) return;
+    double& v = h[(size_t)r * N + n];
+    v = v * (1.0 + scale[n]) + shift[n];
+}
+
+// conv1d valid, stride s: (C_in, L) x (C_out, C_in, K) -> silu -> (C_out, Lo); one block
+__global__ void conv1d_silu_kernel(const double* __restrict__ x, int C, int L, const double* __restrict__ w,
+                                   const double* __restrict__ b, int O, int Kk, int stride,
+                                   double* __restrict__ y) {
+    const int Lo = (L - Kk) / stride + 1;
+    for (int idx = threadIdx.x; idx < O * Lo; idx += blockDim.x) {
+        const int o = idx / Lo, j = idx % Lo;
+        double acc = 0;
+        for (int c = 0; c < C; ++c)
+            for (int t = 0; t < Kk; ++t) acc += w[((size_t)o * C + c) * Kk + t] * x[(size_t)c * L + j * stride + t];
+        y[idx] = silu(acc + b[o]);
+    }
+}
+
+// DDIM update (src/diffusion.py:547-555) on the normalised state
+__global__ void ddim_update_kernel(double* __restrict__ x, const double* __restrict__ eps, int n, double ab,
+                                   double ab_next, int has_next, double clip_lo, double clip_hi,
+                                   double* __restrict__ x0_out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double x0 = (x[i] - sqrt(1.0 - ab) * eps[i]) / sqrt(ab);
+    x0 = fmin(fmax(x0, clip_lo), clip_hi);
+    x0_out[i] = x0;
+    if (has_next) x[i] = sqrt(ab_next) * x0 + sqrt(1.0 - ab_next) * eps[i];
+}
+
+}  // namespace ref
+}  // namespace ps
+
+using namespace ps;
+using namespace ps::ref;
+
+template <typename F>
+static int fill_arm(ArmGrid<F>& A, int D, const double* lengths_h, double basex, double basey, const double* fracs_h,
+                    int M, const long long* pa_h, const long long* pb_h, int n_pairs, const void* grid, int nx,
+                    int ny, double gox, double goy, double gh, double goal_x, double goal_y, double goal_th,
+                    const double* w_h, double d_act, double d_self, const void* jm, const void* jq) {
+    if (D < 1 || D > MAXD || M < 1 || M > MAXM || n_pairs < 0 || n_pairs > MAXPAIR || nx < 2 || ny < 2)
+        return PS_FAIL(PS_ERR_SHAPE);
+    A.D = D;
+    A.M = M;
+    A.n_pairs = n_pairs;
+    for (int k = 0; k < D; ++k) A.lengths[k] = (F)lengths_h[k];
+    for (int i = 0; i < M; ++i) A.fracs[i] = (F)fracs_h[i];
+    A.basex = (F)basex;
+    A.basey = (F)basey;
+    for (int e = 0; e < n_pairs; ++e) {
+        if (pa_h[e] < 0 || pa_h[e] >= D * M || pb_h[e] < 0 || pb_h[e] >= D * M) return PS_FAIL(PS_ERR_SHAPE);
+        A.pair_a[e] = (short)pa_h[e];
+        A.pair_b[e] = (short)pb_h[e];
+    }
+    A.grid = reinterpret_cast<const F*>(grid);
+    A.nx = nx;
+    A.ny = ny;
+    A.gox = (F)gox;
+    A.goy = (F)goy;
+    A.gh = (F)gh;
+    A.goal_x = (F)goal_x;
+    A.goal_y = (F)goal_y;
+    A.goal_th = (F)goal_th;
+    for (int i = 0; i < 5; ++i) A.w[i] = (F)w_h[i];
+    A.d_act = (F)d_act;
+    A.d_self = (F)d_self;
+    A.jerk_mat = reinterpret_cast<const F*>(jm);
+    A.jerk_quad = reinterpret_cast<const F*>(jq);
+    return PS_OK;
+}
+
+#define REF_ARM_ARGS                                                                                             \
+    const double *lengths_h, double basex, double basey, const double *fracs_h, int M, const long long *pair_a_h, \
+        const long long *pair_b_h, int n_pairs, const void *grid, int nx, int ny, double gox, double goy,         \
+        double gh, double goal_x, double goal_y, double goal_th, const double *weights_h, double d_act,          \
+        double d_self, const void *jerk_mat, const void *jerk_quad
+#define REF_ARM_PASS                                                                                            \
+    lengths_h, basex, basey, fracs_h, M, pair_a_h, pair_b_h, n_pairs, grid, nx, ny, gox, goy, gh, goal_x, goal_y, \
+        goal_th, weights_h, d_act, d_self, jerk_mat, jerk_quad
+
+template <typename F>
+static int ref_cost(const void* qs, int S, int T, int D, REF_ARM_ARGS, int want_grad, void* terms, void* totals,
+                    void* grads, uint8_t* clamped, cudaStream_t st) {
+    ArmGrid<F> A;
+    int e = fill_arm(A, D, REF_ARM_PASS);
+    if (e) return e;
+    if (T < 2 || T > MAXT || S < 0) return PS_FAIL(PS_ERR_SHAPE);
+    if (S == 0) return PS_OK;
+    const size_t smem = sizeof(SeedSmem<F>);
+    auto k = cost_kernel<F>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<S, 32, smem, st>>>(A, (const F*)qs, S, T, want_grad, (F*)terms, (F*)totals, (F*)grads, clamped);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+template <typename F>
+static int ref_opt(const void* seeds, int S, int T, int D, int n_iters, double momentum, double armijo_c,
+                   double shrink, int max_bt, double alpha0, double alpha_max, REF_ARM_ARGS, void* x_out, void* terms,
+                   void* totals, uint8_t* frozen, long long* n_acc, cudaStream_t st) {
+    ArmGrid<F> A;
+    int e = fill_arm(A, D, REF_ARM_PASS);
+    if (e) return e;
+    if (T < 2 || T > MAXT || S < 0 || n_iters < 0) return PS_FAIL(PS_ERR_SHAPE);
+    if (S == 0) return PS_OK;
+    const size_t smem = sizeof(SeedSmem<F>);
+    auto k = optimize_kernel<F>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<S, 32, smem, st>>>(A, (const F*)seeds, S, T, n_iters, (F)momentum, (F)armijo_c, (F)shrink, max_bt, (F)alpha0,
+                           (F)alpha_max, (F*)x_out, (F*)terms, (F*)totals, frozen, n_acc);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+extern "C" int ps_ref_cost_terms(int dtype, const void* qs, int S, int T, int D, REF_ARM_ARGS, int want_grad,
+                                 void* terms, void* totals, void* grads, uint8_t* clamped, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == 0)
+        return ref_cost<double>(qs, S, T, D, REF_ARM_PASS, want_grad, terms, totals, grads, clamped, st);
+    if (dtype == 1)
+        return ref_cost<float>(qs, S, T, D, REF_ARM_PASS, want_grad, terms, totals, grads, clamped, st);
+    return PS_FAIL(PS_ERR_SHAPE);
+}
+
+extern "C" int ps_ref_optimize(int dtype, const void* seeds, int S, int T, int D, int n_iters, double momentum,
+                               double armijo_c, double shrink, int max_backtracks, double alpha0, double alpha_max,
+                               REF_ARM_ARGS, void* x_out, void* terms, void* totals, uint8_t* frozen,
+                               long long* n_accepted, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == 0)
+        return ref_opt<double>(seeds, S, T, D, n_iters, momentum, armijo_c, shrink, max_backtracks, alpha0, alpha_max,
+                               REF_ARM_PASS, x_out, terms, totals, frozen, n_accepted, st);
+    if (dtype == 1)
+        return ref_opt<float>(seeds, S, T, D, n_iters, momentum, armijo_c, shrink, max_backtracks, alpha0, alpha_max,
+                              REF_ARM_PASS, x_out, terms, totals, frozen, n_accepted, st);
+    return PS_FAIL(PS_ERR_SHAPE);
+}
+
+extern "C" int ps_ref_planner_esdf(const double* depths, int n_rays, double sx, double sy, double heading, double fov,
+                                   double max_range, double r_disc, double cap, double ox, double oy, double h,
+                                   int nx, int ny, double* out, void* stream) {
+    if (n_rays < 2 || n_rays > 1024 || nx < 2 || ny < 2) return PS_FAIL(PS_ERR_SHAPE);
+    const int n = nx * ny;
+    planner_esdf_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        depths, n_rays, sx, sy, heading, fov, max_range, r_disc, cap, ox, oy, h, nx, ny, out);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+extern "C" int ps_ref_planner_success(const double* trajs, int S, int T, int D, REF_ARM_ARGS, double delta_t,
+                                      double delta_r_deg, int interp, uint8_t* ok, void* stream) {
+    ArmGrid<double> A;
+    int e = fill_arm(A, D, REF_ARM_PASS);
+    if (e) return e;
+    if (S == 0) return PS_OK;
+    planner_success_kernel<<<(S + 63) / 64, 64, 0, (cudaStream_t)stream>>>(A, trajs, S, T, delta_t, delta_r_deg,
+                                                                            interp, ok);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+extern "C" int ps_ref_linear(const double* x, int ldx, const double* W, const double* b, int R, int K, int N, int act,
+                             double* y, int ldy, void* stream) {
+    if (R <= 0 || K <= 0 || N <= 0) return PS_FAIL(PS_ERR_SHAPE);
+    linear_f64_kernel<<<dim3((N + 127) / 128, R), 128, 0, (cudaStream_t)stream>>>(x, ldx, W, b, R, K, N, act, y, ldy);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+extern "C" int ps_ref_film(double* h, const double* scale, const double* shift, int R, int N, void* stream) {
+    film_f64_kernel<<<dim3((N + 127) / 128, R), 128, 0, (cudaStream_t)stream>>>(h, scale, shift, R, N);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+extern "C" int ps_ref_conv1d_silu(const double* x, int C, int L, const double* w, const double* b, int O, int K,
+                                  int stride, double* y, void* stream) {
+    if (L < K) return PS_FAIL(PS_ERR_SHAPE);
+    conv1d_silu_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(x, C, L, w, b, O, K, stride, y);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+extern "C" int ps_ref_ddim_update(double* x, const double* eps, int n, double ab, double ab_next, int has_next,
+                                  double clip_lo, double clip_hi, double* x0_out, void* stream) {
+    ddim_update_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(x, eps, n, ab, ab_next, has_next, clip_lo,
+                                                                           clip_hi, x0_out);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// small elementwise helpers of the ref sampler (fp64)
+// ---------------------------------------------------------------------------
+namespace ps {
+namespace ref {
+// sinusoid of a 1-based step (src/diffusion.py:228-234): freq_i = exp(-ln(1e4) i / max(half-1, 1))
+__global__ void sinusoid_f64_kernel(double k, int half, double* __restrict__ out) {
+    const int i = threadIdx.x;
+    if (i >= half) return;
+    const double freq = exp(-log(10000.0) * (double)i / (double)(half > 1 ? half - 1 : 1));
+    const double ang = k * freq;
+    out[i] = sin(ang);
+    out[half + i] = cos(ang);
+}
+__global__ void div_f64_kernel(const double* __restrict__ x, int n, double d, double* __restrict__ y) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = x[i] / d;
+}
+// traj = lo + x0 * (hi - lo); row 0 := q0  (src/diffusion.py:559-569, arm.py:200-201)
+__global__ void denorm_pin_kernel(const double* __restrict__ x0, int B, int T, int D, const double* __restrict__ lo,
+                                  const double* __restrict__ hi, const double* __restrict__ q0,
+                                  double* __restrict__ traj) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * T * D) return;
+    const int d = i % D, t = (i / D) % T;
+    traj[i] = t == 0 ? q0[d] : lo[d] + x0[i] * (hi[d] - lo[d]);
+}
+// select_best (src/pipeline.py:160-165) over fp64 costs, one thread per problem
+__global__ void select_f64_kernel(const double* __restrict__ cost, const uint8_t* __restrict__ ok, int P, int S,
+                                  int* __restrict__ best) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    bool any = false;
+    for (int s = 0; s < S; ++s) any |= ok[p * S + s] != 0;
+    int bi = -1;
+    double bc = 0;
+    for (int s = 0; s < S; ++s) {
+        if (any && !ok[p * S + s]) continue;
+        const double c = cost[p * S + s];
+        if (bi < 0 || c < bc) {
+            bi = s;
+            bc = c;
+        }
+    }
+    best[p] = bi;
+}
+}  // namespace ref
+}  // namespace ps
+
+extern "C" int ps_ref_sinusoid(double k, int half, double* out, void* stream) {
+    if (half < 1 || half > 1024) return PS_FAIL(PS_ERR_SHAPE);
+    sinusoid_f64_kernel<<<1, half, 0, (cudaStream_t)stream>>>(k, half, out);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+extern "C" int ps_ref_div(const double* x, int n, double d, double* y, void* stream) {
+    div_f64_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(x, n, d, y);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+extern "C" int ps_ref_denorm_pin(const double* x0, int B, int T, int D, const double* lo, const double* hi,
+                                 const double* q0, double* traj, void* stream) {
+    const int n = B * T * D;
+    denorm_pin_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(x0, B, T, D, lo, hi, q0, traj);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+extern "C" int ps_ref_select(const double* cost, const uint8_t* ok, int P, int S, int* best, void* stream) {
+    if (P <= 0 || S <= 0) return PS_FAIL(PS_ERR_SHAPE);
+    select_f64_kernel<<<(P + 63) / 64, 64, 0, (cudaStream_t)stream>>>(cost, ok, P, S, best);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}

@@ -1,0 +1,357 @@
+"""Drop-in for planseed.diffusion's sampler API on the GPU (src/diffusion.py).
+
+Weights are the reference's own: `create_net` draws them exactly like planseed
+(same rng, same order, same fan-in rule, zero biases and FiLM) and the PSCK
+checkpoint format is read/written byte-compatibly, so a planseed checkpoint loads
+here and vice versa.  The forward passes run in float64 CUDA kernels
+(`ps_ref_linear`, `ps_ref_conv1d_silu`, `ps_ref_film`, `ps_ref_ddim_update`, ...);
+input feature vectors (11 + 4 scalars) are formed on the host as the reference does.
+"""
+
+from __future__ import annotations
+
+import json
+import struct
+from dataclasses import asdict, dataclass
+from pathlib import Path
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+
+from .. import _lib
+from .types import WORKSPACE, Rect
+
+CKPT_MAGIC = b"PSCK"
+X0_CLIP = (-0.1, 1.1)
+
+
+@dataclass(frozen=True)
+class NoiseSchedule:
+    betas: np.ndarray
+
+    @property
+    def K(self) -> int:
+        return self.betas.shape[0]
+
+    @property
+    def alpha_bars(self) -> np.ndarray:
+        return np.cumprod(1.0 - self.betas)
+
+    def alpha_bar(self, k):
+        return self.alpha_bars[np.asarray(k) - 1]
+
+
+def make_schedule(K: int = 100, beta_start: float = 1e-3, beta_end: float = 8e-2) -> NoiseSchedule:
+    if K < 2:
+        raise ValueError("need at least 2 diffusion steps")
+    if not (0.0 < beta_start < beta_end < 1.0):
+        raise ValueError("betas must satisfy 0 < beta_start < beta_end < 1")
+    return NoiseSchedule(betas=np.linspace(beta_start, beta_end, K))
+
+
+@dataclass(frozen=True)
+class ArchConfig:
+    """src/diffusion.py:84-120."""
+
+    t_len: int = 32
+    dof: int = 7
+    n_rays: int = 256
+    scan_channels: Tuple[int, ...] = (8, 16, 16)
+    scan_kernels: Tuple[int, ...] = (5, 5, 3)
+    scan_strides: Tuple[int, ...] = (2, 2, 2)
+    scan_embed: int = 64
+    problem_embed: int = 32
+    pose_embed: int = 32
+    t_embed: int = 32
+    embed_hidden: int = 64
+    hidden: int = 512
+    n_hidden: int = 3
+    joint_lo: Tuple[float, ...] = (-2.8973,) * 7
+    joint_hi: Tuple[float, ...] = (2.8973,) * 7
+    bounds_lo: Tuple[float, float] = WORKSPACE.lo
+    bounds_hi: Tuple[float, float] = WORKSPACE.hi
+    max_range: float = 2.0 * WORKSPACE.diagonal
+
+    @property
+    def cond_dim(self) -> int:
+        return self.scan_embed + self.problem_embed + self.pose_embed
+
+    @property
+    def x_dim(self) -> int:
+        return self.t_len * self.dof
+
+    def conv_out_len(self) -> int:
+        n = self.n_rays
+        for kk, ss in zip(self.scan_kernels, self.scan_strides):
+            n = (n - kk) // ss + 1
+        return n
+
+    def lo_hi(self):
+        return np.array(self.joint_lo), np.array(self.joint_hi)
+
+
+def arch_for_arm(arm, bounds: Rect = WORKSPACE, **overrides) -> ArchConfig:
+    base = dict(dof=arm.dof, joint_lo=tuple(arm.lo.tolist()), joint_hi=tuple(arm.hi.tolist()),
+                bounds_lo=tuple(bounds.lo), bounds_hi=tuple(bounds.hi), max_range=2.0 * bounds.diagonal)
+    base.update(overrides)
+    return ArchConfig(**base)
+
+
+@dataclass
+class DenoiserNet:
+    config: ArchConfig
+    params: Dict[str, np.ndarray]
+    init_seed: int = 0
+
+
+def _param_shapes(cfg) -> List[Tuple[str, Tuple[int, ...]]]:
+    """Parameter table in planseed's order (src/diffusion.py:146-182)."""
+    shapes = []
+    c_prev = 1
+    for i, (c, k) in enumerate(zip(cfg.scan_channels, cfg.scan_kernels)):
+        shapes += [(f"scan_conv{i}_w", (c, c_prev, k)), (f"scan_conv{i}_b", (c,))]
+        c_prev = c
+    flat = cfg.scan_channels[-1] * cfg.conv_out_len()
+    shapes += [("scan_fc_w", (flat, cfg.scan_embed)), ("scan_fc_b", (cfg.scan_embed,)),
+               ("prob_fc1_w", (cfg.dof + 4, cfg.embed_hidden)), ("prob_fc1_b", (cfg.embed_hidden,)),
+               ("prob_fc2_w", (cfg.embed_hidden, cfg.problem_embed)), ("prob_fc2_b", (cfg.problem_embed,)),
+               ("pose_fc1_w", (4, cfg.embed_hidden)), ("pose_fc1_b", (cfg.embed_hidden,)),
+               ("pose_fc2_w", (cfg.embed_hidden, cfg.pose_embed)), ("pose_fc2_b", (cfg.pose_embed,)),
+               ("t_fc1_w", (cfg.t_embed, cfg.embed_hidden)), ("t_fc1_b", (cfg.embed_hidden,)),
+               ("t_fc2_w", (cfg.embed_hidden, cfg.t_embed)), ("t_fc2_b", (cfg.t_embed,))]
+    d_in = cfg.x_dim + cfg.cond_dim + cfg.t_embed
+    mod_in = cfg.cond_dim + cfg.t_embed
+    for i in range(cfg.n_hidden):
+        shapes += [(f"trunk{i}_w", (d_in, cfg.hidden)), (f"trunk{i}_b", (cfg.hidden,)),
+                   (f"trunk{i}_scale_w", (mod_in, cfg.hidden)), (f"trunk{i}_scale_b", (cfg.hidden,)),
+                   (f"trunk{i}_shift_w", (mod_in, cfg.hidden)), (f"trunk{i}_shift_b", (cfg.hidden,))]
+        d_in = cfg.hidden
+    shapes += [("trunk_out_w", (d_in, cfg.x_dim)), ("trunk_out_b", (cfg.x_dim,))]
+    return shapes
+
+
+def create_net(cfg: ArchConfig, seed: int = 0) -> DenoiserNet:
+    """Uniform fan-in init, identical draws to planseed (src/diffusion.py:185-200)."""
+    rng = np.random.default_rng(seed)
+    params = {}
+    for name, shape in _param_shapes(cfg):
+        if name.endswith("_b") or "_scale_" in name or "_shift_" in name:
+            params[name] = np.zeros(shape)
+        else:
+            fan_in = int(np.prod(shape[:-1])) if name.endswith("fc_w") or "trunk" in name \
+                or "fc1" in name or "fc2" in name else int(np.prod(shape[1:]))
+            bound = 1.0 / np.sqrt(max(fan_in, 1))
+            params[name] = rng.uniform(-bound, bound, size=shape)
+    return DenoiserNet(config=cfg, params=params, init_seed=seed)
+
+
+def _host_params(net) -> Dict[str, np.ndarray]:
+    return {k: np.asarray(getattr(v, "data", v), dtype=np.float64) for k, v in net.params.items()}
+
+
+def _dev_params(net):
+    """Device float64 copies of the weights, cached on the net object."""
+    torch = _lib.require_cuda()
+    cache = getattr(net, "_ps_dev", None)
+    if cache is None:
+        cache = {k: torch.as_tensor(np.ascontiguousarray(v), device="cuda")
+                 for k, v in _host_params(net).items()}
+        try:
+            object.__setattr__(net, "_ps_dev", cache)
+        except Exception:
+            pass
+    return cache
+
+
+# ----------------------------------------------------------------------------- features
+def _norm_pos(cfg, p):
+    lo = np.array(cfg.bounds_lo)
+    return (np.asarray(p, dtype=np.float64) - lo) / (np.array(cfg.bounds_hi) - lo)
+
+
+def problem_features(cfg, q0, goal) -> np.ndarray:
+    lo, hi = cfg.lo_hi()
+    q0n = (np.asarray(q0, dtype=np.float64) - lo) / (hi - lo)
+    g = _norm_pos(cfg, goal.pos)
+    return np.concatenate([q0n, [g[0], g[1], np.cos(goal.theta), np.sin(goal.theta)]])
+
+
+def pose_features(cfg, pose) -> np.ndarray:
+    p = _norm_pos(cfg, pose.position)
+    return np.array([p[0], p[1], np.cos(pose.heading), np.sin(pose.heading)])
+
+
+def ddim_steps(K: int, n_steps: int) -> np.ndarray:
+    """src/diffusion.py:520-526 (numpy round-half-even)."""
+    if n_steps > K:
+        raise ValueError("n_steps cannot exceed K")
+    if n_steps == 1:
+        return np.array([K], dtype=np.int64)
+    return np.round(np.linspace(K, 1, n_steps)).astype(np.int64)
+
+
+# ----------------------------------------------------------------------------- forward
+def _linear(x, W, b, act: int, out=None):
+    torch = _lib.require_cuda()
+    R, K = x.shape
+    N = W.shape[1]
+    y = out if out is not None else torch.empty((R, N), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().ps_ref_linear(_lib.ptr(x), x.stride(0), _lib.ptr(W), _lib.ptr(b), R, K, N, act,
+                                        _lib.ptr(y), y.stride(0), _lib.stream_handle()), "linear")
+    return y
+
+
+def _mlp2(p, prefix, x):
+    return _linear(_linear(x, p[f"{prefix}_fc1_w"], p[f"{prefix}_fc1_b"], 1),
+                   p[f"{prefix}_fc2_w"], p[f"{prefix}_fc2_b"], 0)
+
+
+def condition_device(net, depths, prob_feats, pose_feats):
+    """condition_graph (src/diffusion.py:246-257) for one observation -> (1, cond_dim) device."""
+    torch = _lib.require_cuda()
+    cfg, p = net.config, _dev_params(net)
+    L = _lib.lib()
+    d = torch.as_tensor(np.asarray(depths, dtype=np.float64), device="cuda").contiguous()
+    h = torch.empty_like(d)
+    _lib.check(L.ps_ref_div(_lib.ptr(d), d.numel(), float(cfg.max_range), _lib.ptr(h),
+                            _lib.stream_handle()), "scan_features")
+    C, Ln = 1, cfg.n_rays
+    for i, (c, kk, ss) in enumerate(zip(cfg.scan_channels, cfg.scan_kernels, cfg.scan_strides)):
+        lo = (Ln - kk) // ss + 1
+        y = torch.empty(c * lo, dtype=torch.float64, device="cuda")
+        _lib.check(L.ps_ref_conv1d_silu(_lib.ptr(h), C, Ln, _lib.ptr(p[f"scan_conv{i}_w"]),
+                                        _lib.ptr(p[f"scan_conv{i}_b"]), c, kk, ss, _lib.ptr(y),
+                                        _lib.stream_handle()), "conv1d")
+        h, C, Ln = y, c, lo
+    scan_emb = _linear(h.view(1, -1), p["scan_fc_w"], p["scan_fc_b"], 0)
+    pf = torch.as_tensor(np.asarray(prob_feats, dtype=np.float64)[None], device="cuda")
+    qf = torch.as_tensor(np.asarray(pose_feats, dtype=np.float64)[None], device="cuda")
+    return torch.cat([scan_emb, _mlp2(p, "prob", pf), _mlp2(p, "pose", qf)], dim=1)
+
+
+def encode_condition(net, scan, q0, goal) -> np.ndarray:
+    """src/diffusion.py:260-269."""
+    cfg = net.config
+    c = condition_device(net, scan.depths, problem_features(cfg, q0, goal), pose_features(cfg, scan.pose))
+    return c.cpu().numpy()[0]
+
+
+def predict_noise_device(net, x, k: int, cond):
+    """predict_noise_graph (src/diffusion.py:272-285); x (B,T,D) device f64, cond (1,C) device."""
+    torch = _lib.require_cuda()
+    cfg, p = net.config, _dev_params(net)
+    L = _lib.lib()
+    B = x.shape[0]
+    half = cfg.t_embed // 2
+    tf = torch.empty((1, cfg.t_embed), dtype=torch.float64, device="cuda")
+    _lib.check(L.ps_ref_sinusoid(float(k), half, _lib.ptr(tf), _lib.stream_handle()), "sinusoid")
+    t_emb = _mlp2(p, "t", tf)
+    mod = torch.cat([cond, t_emb], dim=1)
+    h = torch.cat([x.reshape(B, cfg.x_dim), cond.expand(B, -1), t_emb.expand(B, -1)], dim=1).contiguous()
+    for i in range(cfg.n_hidden):
+        h = _linear(h, p[f"trunk{i}_w"], p[f"trunk{i}_b"], 1)
+        sc = _linear(mod, p[f"trunk{i}_scale_w"], p[f"trunk{i}_scale_b"], 0)
+        sh = _linear(mod, p[f"trunk{i}_shift_w"], p[f"trunk{i}_shift_b"], 0)
+        _lib.check(L.ps_ref_film(_lib.ptr(h), _lib.ptr(sc), _lib.ptr(sh), B, h.shape[1],
+                                 _lib.stream_handle()), "film")
+    return _linear(h, p["trunk_out_w"], p["trunk_out_b"], 0).view(B, cfg.t_len, cfg.dof)
+
+
+def predict_noise(net, x_k, k, cond, K: int = 100) -> np.ndarray:
+    """src/diffusion.py:288-300: x_k (T,D) or (B,T,D), one cond row broadcast."""
+    torch = _lib.require_cuda()
+    x = np.asarray(x_k, dtype=np.float64)
+    single = x.ndim == 2
+    if single:
+        x = x[None]
+    if np.ndim(k) != 0:
+        raise ValueError("per-row step indices are not supported by the drop-in sampler")
+    c = np.atleast_2d(np.asarray(cond, dtype=np.float64))
+    if c.shape[0] != 1:
+        raise ValueError("one condition row per call (the reference broadcasts a single row)")
+    xd = torch.as_tensor(x, device="cuda")
+    cd = torch.as_tensor(c, device="cuda")
+    out = predict_noise_device(net, xd, int(k), cd).cpu().numpy()
+    return out[0] if single else out
+
+
+def ddim_sample_device(net, schedule, cond, x_K, q0, arm, n_steps: int = 5):
+    """_ddim_core + ddim_sample (src/diffusion.py:535-569) on device float64."""
+    torch = _lib.require_cuda()
+    L = _lib.lib()
+    ks = ddim_steps(schedule.K, n_steps)
+    x = torch.as_tensor(np.array(x_K, dtype=np.float64), device="cuda")
+    single = x.dim() == 2
+    if single:
+        x = x[None]
+    x = x.contiguous()
+    cd = torch.as_tensor(np.atleast_2d(np.asarray(cond, dtype=np.float64)), device="cuda")
+    x0 = torch.empty_like(x)
+    n = x.numel()
+    for i, k in enumerate(ks):
+        ab = float(schedule.alpha_bar(int(k)))
+        eps = predict_noise_device(net, x, int(k), cd)
+        has_next = i + 1 < len(ks)
+        ab_next = float(schedule.alpha_bar(int(ks[i + 1]))) if has_next else 1.0
+        _lib.check(L.ps_ref_ddim_update(_lib.ptr(x), _lib.ptr(eps), n, ab, ab_next, int(has_next),
+                                        X0_CLIP[0], X0_CLIP[1], _lib.ptr(x0), _lib.stream_handle()),
+                   "ddim_update")
+    B, T, D = x0.shape
+    lo = torch.as_tensor(np.asarray(arm.lo, dtype=np.float64), device="cuda")
+    hi = torch.as_tensor(np.asarray(arm.hi, dtype=np.float64), device="cuda")
+    q = torch.as_tensor(np.asarray(q0, dtype=np.float64), device="cuda")
+    traj = torch.empty_like(x0)
+    _lib.check(L.ps_ref_denorm_pin(_lib.ptr(x0), B, T, D, _lib.ptr(lo), _lib.ptr(hi), _lib.ptr(q),
+                                   _lib.ptr(traj), _lib.stream_handle()), "denormalize")
+    return traj[0] if single else traj
+
+
+def ddim_sample(net, schedule, cond, x_K, q0, arm, n_steps: int = 5) -> np.ndarray:
+    """src/diffusion.py:559-569: denoise x_K (T,D) or (B,T,D); row 0 pinned to q0."""
+    return ddim_sample_device(net, schedule, cond, x_K, q0, arm, n_steps).cpu().numpy()
+
+
+# ----------------------------------------------------------------------------- checkpoints
+def save_checkpoint(path, net, schedule, meta: Optional[dict] = None):
+    """PSCK: magic, u64 header length, sorted-key JSON, little-endian f64 blob (src/diffusion.py:635-651)."""
+    names = [n for n, _ in _param_shapes(net.config)]
+    hp = _host_params(net)
+    header = {"format": 1, "arch": asdict(net.config), "init_seed": net.init_seed,
+              "schedule": {"betas": [float(x) for x in np.asarray(schedule.betas).ravel()]},
+              "meta": meta or {},
+              "params": [{"name": n, "shape": list(hp[n].shape)} for n in names]}
+    blob = b"".join(np.ascontiguousarray(hp[n], dtype="<f8").tobytes() for n in names)
+    head = json.dumps(header, sort_keys=True).encode()
+    with open(path, "wb") as f:
+        f.write(CKPT_MAGIC)
+        f.write(struct.pack("<Q", len(head)))
+        f.write(head)
+        f.write(blob)
+
+
+def load_checkpoint(path):
+    """src/diffusion.py:657-687."""
+    path = Path(path)
+    if not path.exists():
+        raise FileNotFoundError(f"checkpoint not found: {path}")
+    with open(path, "rb") as f:
+        if f.read(4) != CKPT_MAGIC:
+            raise ValueError(f"{path} is not a checkpoint file")
+        (hlen,) = struct.unpack("<Q", f.read(8))
+        header = json.loads(f.read(hlen).decode())
+        blob = f.read()
+    arch = header["arch"]
+    for key in ("scan_channels", "scan_kernels", "scan_strides", "joint_lo", "joint_hi", "bounds_lo",
+                "bounds_hi"):
+        arch[key] = tuple(arch[key])
+    cfg = ArchConfig(**arch)
+    params, off = {}, 0
+    for spec_ in header["params"]:
+        shape = tuple(spec_["shape"])
+        n = int(np.prod(shape))
+        params[spec_["name"]] = np.frombuffer(blob, dtype="<f8", count=n, offset=off).reshape(shape).copy()
+        off += n * 8
+    if off != len(blob):
+        raise ValueError(f"checkpoint blob size mismatch in {path}")
+    net = DenoiserNet(config=cfg, params=params, init_seed=header.get("init_seed", 0))
+    return net, NoiseSchedule(betas=np.array(header["schedule"]["betas"])), header.get("meta", {})

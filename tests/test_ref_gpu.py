@@ -1,0 +1,142 @@
+"""GPU parity of the ref-profile drop-in (paper_2410_16727_b200.ref) against planseed's
+own outputs (golden fixtures from tools/make_golden.py) -- the reference's sampler,
+refiner and planner API, called the way planseed's callers call it.
+
+Bars: float64 mode within 1e-9 (relative, values) of planseed; flags, clamped,
+frozen, accept counts, successes and best index exactly equal."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+@pytest.fixture(scope="module")
+def ref():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test without a CUDA device")
+    from paper_2410_16727_b200 import ref as r
+    return r
+
+
+def _weights(ref, w):
+    return ref.trajopt.CostWeights(*[float(x) for x in w])
+
+
+def _grid(ref, z):
+    v = z["esdf_values"]
+    return ref.types.SdfGrid(origin=z["esdf_origin"], h=float(z["esdf_h"]), nx=v.shape[0], ny=v.shape[1],
+                             values=v)
+
+
+def _close(a, b, rtol=1e-9, atol=1e-11):
+    np.testing.assert_allclose(a, b, rtol=rtol, atol=atol)
+
+
+@pytest.mark.parametrize("case", [f"c{i}" for i in range(6)])
+def test_cost_terms_batch(ref, case):
+    z = np.load(GOLD / f"ref_cost_{case}.npz")
+    arm = ref.types.default_arm()
+    goal = ref.types.Pose2((z["goal"][0], z["goal"][1]), z["goal"][2])
+    terms, totals, grads, clamped = ref.trajopt.cost_terms_batch_device(arm, _grid(ref, z), goal, z["trajs"],
+                                                                         _weights(ref, z["w"]), True)
+    _close(totals.cpu().numpy(), z["totals"])
+    _close(terms.cpu().numpy(), z["terms"])
+    _close(grads.cpu().numpy(), z["grads"], rtol=1e-8, atol=1e-9)
+    assert np.array_equal(clamped.cpu().numpy().astype(bool), z["clamped"])
+
+
+def test_cost_fp32_mode(ref):
+    z = np.load(GOLD / "ref_cost_c1.npz")
+    arm = ref.types.default_arm()
+    goal = ref.types.Pose2((z["goal"][0], z["goal"][1]), z["goal"][2])
+    _, totals, _, _ = ref.trajopt.cost_terms_batch_device(arm, _grid(ref, z), goal, z["trajs"],
+                                                          _weights(ref, z["w"]), True, dtype="fp32")
+    np.testing.assert_allclose(totals.cpu().numpy(), z["totals"], rtol=1e-4)
+
+
+def test_optimize_batch(ref):
+    z = np.load(GOLD / "ref_optimize.npz")
+    arm = ref.types.default_arm()
+    goal = ref.types.Pose2((z["goal"][0], z["goal"][1]), z["goal"][2])
+    res = ref.trajopt.optimize(arm, _grid(ref, z), goal, list(z["seeds"]), int(z["n_iters"]),
+                               _weights(ref, z["w"]))
+    x = np.stack([r.trajectory for r in res])
+    _close(x, z["x"], rtol=1e-8, atol=1e-9)
+    _close(np.array([r.cost for r in res]), z["totals"], rtol=1e-8)
+    assert [r.converged for r in res] == list(z["frozen"])
+    assert [r.n_accepted for r in res] == list(z["n_acc"])
+    assert all(np.array_equal(r.trajectory[0], s[0]) for r, s in zip(res, z["seeds"]))
+
+
+def test_optimize_errors(ref):
+    z = np.load(GOLD / "ref_optimize.npz")
+    arm = ref.types.default_arm()
+    goal = ref.types.Pose2((0.1, 0.5), 0.0)
+    g = _grid(ref, z)
+    with pytest.raises(ValueError):
+        ref.trajopt.optimize(arm, g, goal, list(z["seeds"]), 0, ref.trajopt.CostWeights())
+    with pytest.raises(ValueError):
+        ref.trajopt.optimize(arm, g, goal, [], 5, ref.trajopt.CostWeights())
+    tiny = ref.types.SdfGrid(origin=np.array([-0.1, -0.1]), h=0.05, nx=5, ny=5, values=np.ones((5, 5)))
+    with pytest.raises(ValueError, match="ESDF extent"):
+        ref.trajopt.evaluate_cost(arm, tiny, goal, np.zeros((32, 7)), ref.trajopt.CostWeights())
+
+
+def _scan(ref, z):
+    p = z["pose"]
+    pose = ref.types.SensorPose(position=(p[0], p[1]), heading=p[2], fov=p[3], max_range=p[4], n_rays=int(p[5]))
+    return ref.types.DepthScan(pose=pose, depths=z["depths"])
+
+
+def test_sampler_encode_predict_ddim(ref):
+    from golden_net import golden_net
+    z = np.load(GOLD / "ref_sampler.npz")
+    arm = ref.types.default_arm()
+    net = golden_net(arm)
+    goal = ref.types.Pose2((z["goal"][0], z["goal"][1]), z["goal"][2])
+    cond = ref.diffusion.encode_condition(net, _scan(ref, z), z["q0"], goal)
+    _close(cond, z["cond"], rtol=1e-10, atol=1e-12)
+    eps = ref.diffusion.predict_noise(net, z["x"], int(z["k"]), z["cond"])
+    _close(eps, z["eps"], rtol=1e-9, atol=1e-10)
+    sched = ref.diffusion.NoiseSchedule(betas=z["betas"])
+    traj = ref.diffusion.ddim_sample(net, sched, z["cond"], z["x_K"], z["q0"], arm, n_steps=5)
+    _close(traj, z["traj"], rtol=1e-9, atol=1e-9)
+    assert np.array_equal(traj[:, 0], np.repeat(z["q0"][None], traj.shape[0], 0))
+
+
+def test_plan_diffusion_end_to_end(ref):
+    from golden_net import golden_net
+    z = np.load(GOLD / "ref_plan.npz")
+    arm = ref.types.default_arm()
+    net = golden_net(arm)
+    goal = ref.types.Pose2((z["goal"][0], z["goal"][1]), z["goal"][2])
+    req = ref.pipeline.PlanRequest(q_start=z["q0"], goal=goal, scan=_scan(ref, z), n_trajs=int(z["n_trajs"]),
+                                   n_iters=int(z["n_iters"]), n_denoising=5, seed=int(z["seed"]))
+    res = ref.pipeline.plan_diffusion(arm, net, ref.diffusion.make_schedule(), req)
+    esdf = ref.pipeline.build_planner_esdf(req.bounds, req.scan, req.esdf_cell)
+    _close(esdf.values, z["esdf_values"], rtol=1e-12, atol=1e-13)
+    _close(res.seed_trajectories, z["seed_trajectories"], rtol=1e-9, atol=1e-9)
+    _close(np.array([r.cost for r in res.results]), z["costs"], rtol=1e-8)
+    _close(np.stack([r.trajectory for r in res.results]), z["trajs"], rtol=1e-8, atol=1e-8)
+    assert res.successes == list(z["successes"])
+    assert res.best_index == int(z["best_index"])
+    loose = [ref.pipeline.planner_success(arm, esdf, goal, t, 0.2, 30.0) for t in z["trajs"]]
+    assert loose == list(z["loose_success"])
+    assert res.esdf_time > 0 and res.plan_time > 0
+
+
+def test_select_best_tie_rules(ref):
+    R = ref.trajopt.OptResult
+    mk = lambda cs: [R(trajectory=None, cost=c, breakdown={}, iterations=1, converged=False) for c in cs]
+    sb = ref.pipeline.select_best
+    assert sb(mk([3.0]), [False]) == 0
+    assert sb(mk([1.0, 5.0]), [False, True]) == 1
+    assert sb(mk([2.0, 1.0, 1.0]), [False] * 3) == 1
+    assert sb(mk([0.5, 3.0, 2.0, 9.0]), [False, True, True, True]) == 2
+    with pytest.raises(ValueError):
+        sb([], [])

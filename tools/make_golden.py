@@ -1,0 +1,165 @@
+"""Generate golden input/output fixtures from the reference package (planseed, imported
+from /root/reference/pkg/src in the build container) for the ref-profile parity tests.
+
+    PYTHONPATH=/root/reference/pkg/src python tools/make_golden.py
+
+Writes tests/golden/ref_*.npz.  The GPU box has no /root/reference, so the tests there
+compare the CUDA drop-in against these files; tests/test_golden_cpu.py re-runs this
+generator in the container and checks the committed files are what planseed produces.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+REF = Path("/root/reference/pkg/src")
+if str(REF) not in sys.path:
+    sys.path.insert(0, str(REF))
+
+from planseed import _kernels  # noqa: E402
+from planseed.arm import Pose2, default_arm, fk_pose  # noqa: E402
+from planseed.diffusion import (arch_for_arm, create_net, ddim_sample, encode_condition,  # noqa: E402
+                                make_schedule, predict_noise)
+from planseed.geometry import (Box, Circle, SdfGrid, SensorPose, World, build_esdf,  # noqa: E402
+                               render_depth_scan)
+from planseed.pipeline import PlanRequest, build_planner_esdf, plan_diffusion, planner_success  # noqa: E402
+from planseed.trajopt import (CostWeights, _kernel_args, evaluate_cost_batch, linear_seed,  # noqa: E402
+                              optimize)
+
+ARM = default_arm()
+T = 32
+
+
+def linear_grid(a=1.0, bx=0.25, by=-0.4):
+    h, n = 0.01, 201
+    xs = -1.0 + h * np.arange(n)
+    gx, gy = np.meshgrid(xs, xs, indexing="ij")
+    return SdfGrid(origin=np.array([-1.0, -1.0]), h=h, nx=n, ny=n, values=a + bx * gx + by * gy)
+
+
+def random_trajs(rng, n, scale=0.8):
+    out = []
+    for _ in range(n):
+        q0 = rng.uniform(-1.2, 1.2, size=7)
+        q1 = rng.uniform(-1.2, 1.2, size=7)
+        tr = q0 + np.linspace(0, 1, T)[:, None] * (q1 - q0)
+        tr += scale * 0.1 * rng.standard_normal((T, 7))
+        tr[0] = q0
+        out.append(tr)
+    return np.stack(out)
+
+
+def esdf_dict(e, prefix="esdf"):
+    return {f"{prefix}_values": e.values, f"{prefix}_origin": np.asarray(e.origin), f"{prefix}_h": np.float64(e.h)}
+
+
+def w_arr(w):
+    return np.array([w.w_goal_pos, w.w_goal_rot, w.w_smooth, w.w_self, w.w_world, w.d_act, w.d_self])
+
+
+def gen_cost():
+    cases = {}
+    world = World([Circle(center=(0.45, 0.15), radius=0.2), Box(lo=(-0.6, -0.7), hi=(-0.2, -0.35))])
+    grids = {"real": build_esdf(world, 0.01), "linear": linear_grid()}
+    ws = {"default": CostWeights(), "all": CostWeights(d_act=0.15, d_self=0.4),
+          "world": CostWeights(w_goal_pos=0, w_goal_rot=0, w_smooth=0, w_self=0, d_act=1.5)}
+    rng = np.random.default_rng(16)
+    goal = Pose2(position=(0.3, 0.25), theta=0.7)
+    i = 0
+    for gname, g in grids.items():
+        for wname, w in ws.items():
+            trajs = random_trajs(rng, 6)
+            terms, totals, grads, clamped = _kernels.cost_terms_batch(trajs, *_kernel_args(ARM, g, goal, w, T), True)
+            cases[f"c{i}"] = dict(trajs=trajs, goal=np.array([*goal.pos, goal.theta]), w=w_arr(w),
+                                  terms=terms, totals=totals, grads=grads, clamped=clamped,
+                                  grid=gname, **esdf_dict(g))
+            i += 1
+    return cases
+
+
+def gen_optimize():
+    esdf = build_esdf(World([Circle(center=(0.4, 0.3), radius=0.15)]), 0.01)
+    rng = np.random.default_rng(20)
+    q0 = np.array([0.4, -0.3, 0.5, -0.2, 0.3, 0.1, -0.2])
+    goal = Pose2(position=(0.1, 0.55), theta=1.2)
+    seeds = np.stack([linear_seed(ARM, q0, goal, rng) for _ in range(6)])
+    w = CostWeights()
+    x, terms, totals, frozen, nacc = _kernels.optimize_batch(
+        seeds.copy(), 40, 0.9, 1e-4, 0.5, 40, 1.0, 4.0, *_kernel_args(ARM, esdf, goal, w, T))
+    return dict(seeds=seeds, goal=np.array([*goal.pos, goal.theta]), w=w_arr(w), n_iters=np.int64(40), x=x,
+                terms=terms, totals=totals, frozen=frozen, n_acc=nacc, **esdf_dict(esdf))
+
+
+def scene():
+    world = World([Circle(center=(0.35, 0.2), radius=0.12), Box(lo=(0.55, -0.35), hi=(0.7, 0.1)),
+                   Circle(center=(-0.3, 0.45), radius=0.1)])
+    pose = SensorPose(position=(-0.6, 0.2), heading=-0.15)
+    return world, render_depth_scan(world, pose)
+
+
+def net_and_cond():
+    cfg = arch_for_arm(ARM)
+    net = create_net(cfg, seed=3)
+    rng = np.random.default_rng(5)
+    for name, p in net.params.items():           # exercise every path (FiLM, biases)
+        p.data[:] = p.data + 0.02 * rng.standard_normal(p.data.shape)
+    return net
+
+
+def gen_sampler():
+    net = net_and_cond()
+    world, scan = scene()
+    q0 = np.array([0.3, -0.5, 0.6, -0.4, 0.2, 0.3, -0.1])
+    goal = Pose2(position=(0.45, 0.5), theta=0.9)
+    cond = encode_condition(net, scan, q0, goal)
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((5, T, 7))
+    eps = predict_noise(net, x, 37, cond)
+    sched = make_schedule()
+    x_K = rng.standard_normal((6, T, 7))
+    traj = ddim_sample(net, sched, cond, x_K, q0, ARM, n_steps=5)
+    # weights are not stored: the tests rebuild them with the drop-in create_net(seed=3)
+    # plus the same seeded perturbation (create_net parity is pinned in test_golden_cpu.py)
+    params = {}
+    return dict(depths=scan.depths, pose=np.array([*scan.pose.position, scan.pose.heading, scan.pose.fov,
+                                                   scan.pose.max_range, scan.pose.n_rays]),
+                q0=q0, goal=np.array([*goal.pos, goal.theta]), cond=cond, x=x, k=np.int64(37), eps=eps,
+                x_K=x_K, traj=traj, betas=sched.betas, **params)
+
+
+def gen_plan():
+    net = net_and_cond()
+    world, scan = scene()
+    q0 = np.array([0.3, -0.5, 0.6, -0.4, 0.2, 0.3, -0.1])
+    goal = fk_pose(ARM, np.array([0.9, 0.4, -0.3, 0.5, 0.2, -0.4, 0.1]))
+    req = PlanRequest(q_start=q0, goal=goal, scan=scan, n_trajs=8, n_iters=25, n_denoising=5, seed=11)
+    res = plan_diffusion(ARM, net, make_schedule(), req)
+    esdf = build_planner_esdf(req.bounds, scan, req.esdf_cell)
+    succ_cases = np.stack([r.trajectory for r in res.results])
+    ps = np.array([planner_success(ARM, esdf, goal, t, 0.2, 30.0) for t in succ_cases])  # looser thresholds
+    return dict(depths=scan.depths, pose=np.array([*scan.pose.position, scan.pose.heading, scan.pose.fov,
+                                                   scan.pose.max_range, scan.pose.n_rays]),
+                q0=q0, goal=np.array([*goal.pos, goal.theta]), seed=np.int64(req.seed),
+                n_trajs=np.int64(req.n_trajs), n_iters=np.int64(req.n_iters), esdf_values=esdf.values,
+                best_index=np.int64(res.best_index), trajectory=res.trajectory,
+                costs=np.array([r.cost for r in res.results]),
+                trajs=np.stack([r.trajectory for r in res.results]), successes=np.array(res.successes),
+                seed_trajectories=res.seed_trajectories, loose_success=ps)
+
+
+def main(out_dir: Path = ROOT / "tests" / "golden"):
+    out_dir.mkdir(parents=True, exist_ok=True)
+    for name, c in gen_cost().items():
+        np.savez_compressed(out_dir / f"ref_cost_{name}.npz", **c)
+    np.savez_compressed(out_dir / "ref_optimize.npz", **gen_optimize())
+    np.savez_compressed(out_dir / "ref_sampler.npz", **gen_sampler())
+    np.savez_compressed(out_dir / "ref_plan.npz", **gen_plan())
+    return out_dir
+
+
+if __name__ == "__main__":
+    print(main())
