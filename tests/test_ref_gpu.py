@@ -40,7 +40,7 @@ def _close(a, b, rtol=1e-9, atol=1e-11):
     np.testing.assert_allclose(a, b, rtol=rtol, atol=atol)
 
 
-@pytest.mark.parametrize("case", [f"c{i}" for i in range(6)])
+@pytest.mark.parametrize("case", [f"c{i}" for i in range(7)])
 def test_cost_terms_batch(ref, case):
     z = np.load(GOLD / f"ref_cost_{case}.npz")
     arm = ref.types.default_arm()
@@ -74,6 +74,15 @@ def test_optimize_batch(ref):
     assert [r.converged for r in res] == list(z["frozen"])
     assert [r.n_accepted for r in res] == list(z["n_acc"])
     assert all(np.array_equal(r.trajectory[0], s[0]) for r, s in zip(res, z["seeds"]))
+    # already-optimal seed freezes (planseed tests/test_trajopt.py:162-169), others do not
+    goal_b = ref.types.Pose2((z["b_goal"][0], z["b_goal"][1]), z["b_goal"][2])
+    gb = ref.types.SdfGrid(origin=z["b_esdf_origin"], h=float(z["b_esdf_h"]), nx=z["b_esdf_values"].shape[0],
+                           ny=z["b_esdf_values"].shape[1], values=z["b_esdf_values"])
+    rb = ref.trajopt.optimize(arm, gb, goal_b, list(z["b_seeds"]), 25, _weights(ref, z["w"]))
+    assert [r.converged for r in rb] == list(z["b_frozen"]) and any(z["b_frozen"]) and not all(z["b_frozen"])
+    assert [r.n_accepted for r in rb] == list(z["b_n_acc"])
+    _close(np.stack([r.trajectory for r in rb]), z["b_x"], rtol=1e-7, atol=1e-7)
+    assert np.array_equal(rb[0].trajectory, z["b_seeds"][0])
 
 
 def test_optimize_errors(ref):
@@ -130,6 +139,8 @@ def test_plan_diffusion_end_to_end(ref):
     assert res.best_index == int(z["best_index"])
     loose = [ref.pipeline.planner_success(arm, esdf, goal, t, 0.2, 30.0) for t in z["trajs"]]
     assert loose == list(z["loose_success"])
+    coll = ref.pipeline.planner_success_batch(arm, esdf, goal, z["coll_trajs"], 10.0, 360.0)
+    assert list(coll) == list(z["coll_success"]) and any(coll) and not all(coll)
     assert res.esdf_time > 0 and res.plan_time > 0
 
 

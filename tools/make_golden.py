@@ -78,6 +78,14 @@ def gen_cost():
                                   terms=terms, totals=totals, grads=grads, clamped=clamped,
                                   grid=gname, **esdf_dict(g))
             i += 1
+    # out-of-extent points: clamped flags set, values from the clamped edge patch
+    tiny = SdfGrid(origin=np.array([-0.1, -0.1]), h=0.05, nx=5, ny=5,
+                   values=np.random.default_rng(3).uniform(0.0, 0.2, (5, 5)))
+    trajs = random_trajs(rng, 4)
+    w = CostWeights(d_act=0.3)
+    terms, totals, grads, clamped = _kernels.cost_terms_batch(trajs, *_kernel_args(ARM, tiny, goal, w, T), True)
+    cases["c6"] = dict(trajs=trajs, goal=np.array([*goal.pos, goal.theta]), w=w_arr(w), terms=terms,
+                       totals=totals, grads=grads, clamped=clamped, grid="tiny", **esdf_dict(tiny))
     return cases
 
 
@@ -90,8 +98,17 @@ def gen_optimize():
     w = CostWeights()
     x, terms, totals, frozen, nacc = _kernels.optimize_batch(
         seeds.copy(), 40, 0.9, 1e-4, 0.5, 40, 1.0, 4.0, *_kernel_args(ARM, esdf, goal, w, T))
+    # second case: an already optimal seed (constant at a pose whose FK is the goal, empty
+    # world) freezes; mixed with linear seeds that do not
+    esdf0 = build_esdf(World([]), 0.01)
+    goal0 = fk_pose(ARM, q0)
+    seeds0 = np.stack([np.tile(q0, (T, 1))] + [linear_seed(ARM, q0, goal0, rng) for _ in range(3)])
+    x0, terms0, totals0, frozen0, nacc0 = _kernels.optimize_batch(
+        seeds0.copy(), 25, 0.9, 1e-4, 0.5, 40, 1.0, 4.0, *_kernel_args(ARM, esdf0, goal0, w, T))
     return dict(seeds=seeds, goal=np.array([*goal.pos, goal.theta]), w=w_arr(w), n_iters=np.int64(40), x=x,
-                terms=terms, totals=totals, frozen=frozen, n_acc=nacc, **esdf_dict(esdf))
+                terms=terms, totals=totals, frozen=frozen, n_acc=nacc, **esdf_dict(esdf),
+                b_seeds=seeds0, b_goal=np.array([*goal0.pos, goal0.theta]), b_x=x0, b_totals=totals0,
+                b_frozen=frozen0, b_n_acc=nacc0, **esdf_dict(esdf0, "b_esdf"))
 
 
 def scene():
@@ -141,6 +158,10 @@ def gen_plan():
     esdf = build_planner_esdf(req.bounds, scan, req.esdf_cell)
     succ_cases = np.stack([r.trajectory for r in res.results])
     ps = np.array([planner_success(ARM, esdf, goal, t, 0.2, 30.0) for t in succ_cases])  # looser thresholds
+    # collision-only verdicts (goal thresholds that always pass): mixed flags
+    rng = np.random.default_rng(12)
+    coll = np.concatenate([succ_cases, random_trajs(rng, 12, scale=0.3)])
+    pc = np.array([planner_success(ARM, esdf, goal, t, 10.0, 360.0) for t in coll])
     return dict(depths=scan.depths, pose=np.array([*scan.pose.position, scan.pose.heading, scan.pose.fov,
                                                    scan.pose.max_range, scan.pose.n_rays]),
                 q0=q0, goal=np.array([*goal.pos, goal.theta]), seed=np.int64(req.seed),
@@ -148,7 +169,7 @@ def gen_plan():
                 best_index=np.int64(res.best_index), trajectory=res.trajectory,
                 costs=np.array([r.cost for r in res.results]),
                 trajs=np.stack([r.trajectory for r in res.results]), successes=np.array(res.successes),
-                seed_trajectories=res.seed_trajectories, loose_success=ps)
+                seed_trajectories=res.seed_trajectories, loose_success=ps, coll_trajs=coll, coll_success=pc)
 
 
 def main(out_dir: Path = ROOT / "tests" / "golden"):
