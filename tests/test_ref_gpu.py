@@ -154,3 +154,30 @@ def test_select_best_tie_rules(ref):
     assert sb(mk([0.5, 3.0, 2.0, 9.0]), [False, True, True, True]) == 2
     with pytest.raises(ValueError):
         sb([], [])
+
+
+def test_integration_binding_stub(ref):
+    """tools/planseed_kernels_b200.py called with planseed's raw
+    18-argument convention reproduces the golden numba outputs."""
+    import sys
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+    import planseed_kernels_b200 as kb
+    from paper_2410_16727_b200.ref.trajopt import _jerk_quad, jerk_matrix
+    arm = ref.types.default_arm()
+    pa, pb = ref.types.nonadjacent_point_pairs(arm)
+    z = np.load(GOLD / "ref_cost_c1.npz")
+    w = z["w"]
+    raw = (arm.lengths, 0.0, 0.0, arm.point_fractions(), pa, pb, z["esdf_values"], float(z["esdf_origin"][0]),
+           float(z["esdf_origin"][1]), float(z["esdf_h"]), float(z["goal"][0]), float(z["goal"][1]),
+           float(z["goal"][2]), w[:5], float(w[5]), float(w[6]), jerk_matrix(32), _jerk_quad(32))
+    terms, totals, grads, clamped = kb.cost_terms_batch(z["trajs"], *raw, True)
+    _close(totals, z["totals"])
+    _close(grads, z["grads"], rtol=1e-8, atol=1e-9)
+    o = np.load(GOLD / "ref_optimize.npz")
+    w = o["w"]
+    raw = (arm.lengths, 0.0, 0.0, arm.point_fractions(), pa, pb, o["esdf_values"], float(o["esdf_origin"][0]),
+           float(o["esdf_origin"][1]), float(o["esdf_h"]), float(o["goal"][0]), float(o["goal"][1]),
+           float(o["goal"][2]), w[:5], float(w[5]), float(w[6]), jerk_matrix(32), _jerk_quad(32))
+    x, _, tot, frozen, nacc = kb.optimize_batch(o["seeds"], int(o["n_iters"]), 0.9, 1e-4, 0.5, 40, 1.0, 4.0, *raw)
+    _close(x, o["x"], rtol=1e-7, atol=1e-7)
+    assert list(frozen) == list(o["frozen"]) and list(nacc) == list(o["n_acc"])
