@@ -15,112 +15,15 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <mutex>
 #include <vector>
 
 #include "common.cuh"
 #include "sampler.cuh"
+#include "tc_ptx.cuh"
 
 namespace ps {
-
-// ---------------------------------------------------------------------------
-// PTX wrappers
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1, int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
-            smem_u32(dst)),
-        "l"((uint64_t)tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-            smem_u32(dst)),
-        "l"((uint64_t)tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1, int c2,
-                                            int c3, int c4) {
-    asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], "
-        "[%2];" ::"r"(smem_u32(dst)),
-        "l"((uint64_t)tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-        : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// K-major, 128B-swizzled UMMA shared-memory descriptor (rows of 128 B, 8-row atoms)
-__device__ __forceinline__ uint64_t umma_desc_sw128(const void* p) {
-    const uint32_t a = smem_u32(p);
-    uint64_t d = 0;
-    d |= (uint64_t)((a >> 4) & 0x3FFF);          // start address
-    d |= (uint64_t)0 << 16;                       // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;             // SBO: 8 rows x 128 B
-    d |= (uint64_t)1 << 46;                       // version (sm100)
-    d |= (uint64_t)2 << 61;                       // SWIZZLE_128B
-    return d;
-}
-// kind::f16 instruction descriptor: D f32, A/B bf16, K-major both, M=128, N
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-    uint32_t r[32];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-// mish(x) = x tanh(softplus(x)) = x * n(n+2) / (n(n+2) + 2), n = e^x
-__device__ __forceinline__ float mish_fast(float x) {
-    const float n = __expf(fminf(x, 15.f));
-    const float m = n * (n + 2.f);
-    const float y = x * __fdividef(m, m + 2.f);
-    return x > 15.f ? x : y;
-}
 
 // ---------------------------------------------------------------------------
 // kernel arguments
@@ -167,29 +70,8 @@ struct TcArgs {
     // 2-D geometry (encoder): tile = ry output rows x wx output columns of one image
     int geom;                       // 0: [B][Tv] samples, 1: 2-D image tiles
     int Ho, Wo, Hp, wx, ry, tiles_x, tiles_y;
+    int dbg;                        // PS_TC_DBG: 1 = skip epilogue math, 2 = skip MMAs
 };
-
-__device__ __forceinline__ uint4 philox_tc(uint4 c, uint32_t k0, uint32_t k1) {
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
-        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
-        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
-        k0 += 0x9E3779B9u;
-        k1 += 0xBB67AE85u;
-    }
-    return c;
-}
-__device__ __forceinline__ float normal_tc(uint32_t step, uint32_t prob, uint32_t seed, uint32_t e, uint32_t key) {
-    const uint4 r = philox_tc(make_uint4(e >> 2, step, prob, seed), key, 0x5EED5EEDu);
-    const uint32_t comp = e & 3u;
-    const uint32_t a = comp < 2 ? r.x : r.z, b = comp < 2 ? r.y : r.w;
-    const float u1 = ((float)(a >> 8) + 1.0f) * (1.0f / 16777216.0f);
-    const float u2 = (float)(b >> 8) * (1.0f / 16777216.0f);
-    const float rad = sqrtf(-2.0f * logf(u1));
-    const float ang = 6.28318530717958648f * u2;
-    return (comp & 1u) ? rad * sinf(ang) : rad * cosf(ang);
-}
 
 // columns of one accumulator buffer (main [+ residual])
 template <int N, bool RES>
@@ -209,14 +91,6 @@ __host__ __device__ constexpr int tmem_alloc_cols() {
 constexpr int TC_EPI_WG = 2;                         // epilogue warpgroups
 constexpr int TC_FILM_P = 4;                         // FiLM rows staged per tile
 constexpr int TC_THREADS = 64 + 128 * TC_EPI_WG;     // producer warp, MMA warp, epilogue
-
-template <int NV>
-__device__ __forceinline__ float sel(const float (&a)[NV], int i) {
-    float r = a[0];
-#pragma unroll
-    for (int k = 1; k < NV; ++k) r = (i == k) ? a[k] : r;
-    return r;
-}
 
 // Persistent: CTA c handles tiles c, c + gridDim.x, ...  The producer streams every
 // tile's K chunks through the smem ring; the MMA warp fills accumulator buffer j % NBUF
@@ -341,10 +215,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
                     const uint64_t da = umma_desc_sw128(sa);
                     const uint64_t db = umma_desc_sw128(sa + A_BYTES);
                     const uint32_t d_tmem = acc0 + (ch.res ? (uint32_t)N : 0u);
+                    if (!(a.dbg & 2)) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        umma_bf16(d_tmem, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc,
-                                  (ch.first && kk == 0) ? 0u : 1u);
+                        for (int kk = 0; kk < 4; ++kk)
+                            umma_bf16(d_tmem, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc,
+                                      (ch.first && kk == 0) ? 0u : 1u);
+                    }
                     umma_commit(&empty[s]);
                 }
                 umma_commit(&tfull[buf]);
@@ -373,7 +249,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) conv_tc_kernel(const __grid_con
             mbar_wait(&tfull[buf], use & 1u);
             tc_fence_after();
 
-            if constexpr (EPI == EPI_RELU2D) {
+            if (a.dbg & 1) {
+                // debug: drain without epilogue work
+            } else if constexpr (EPI == EPI_RELU2D) {
                 const int per_img = a.tiles_x * a.tiles_y;
                 const int img = tile / per_img, tt = tile % per_img;
                 const int y = (tt / a.tiles_x) * a.ry + r / a.wx, x = (tt % a.tiles_x) * a.wx + r % a.wx;
@@ -710,6 +588,8 @@ static int launch_tc(TcArgs& a, int n_tiles, cudaStream_t st) {
             return PS_FAIL(PS_ERR_CUDA);
         attr_set = true;
     }
+    static const int dbg = std::getenv("PS_TC_DBG") ? std::atoi(std::getenv("PS_TC_DBG")) : 0;
+    a.dbg = dbg;
     static int n_sm = 0;
     if (!n_sm) {
         int dev = 0;
@@ -722,58 +602,594 @@ static int launch_tc(TcArgs& a, int n_tiles, cudaStream_t st) {
     return PS_OK;
 }
 
+// ===========================================================================
+// U-Net layers: (time, sample)-ordered tiles with one activation load per channel
+// chunk.  Tile rows are r = t * nb + s (nb = 128 / Tv samples), so a conv tap dt is
+// a uniform shift of dt * nb rows: each 64-channel activation chunk is loaded ONCE
+// per tile as a [(Tv + 4) x nb] box whose two halo rows on each side are TMA
+// zero-fill (the conv's zero padding), and the 1..5 taps that read it issue their
+// MMAs from shifted smem descriptors (SW128 base-offset field set for row shifts that
+// are not multiples of 8).  Weights stream through a separate ring, one [N x 64] box
+// per (tap, chunk).
+// ===========================================================================
+constexpr int UT_MAXG = 24;   // activation chunk groups per tile
+constexpr int UT_MAXTAP = 64;
+
+struct UtGroup {
+    int16_t c;      // channel offset in the source view
+    int8_t src;     // activation map
+    int8_t ntap;    // taps reading this chunk
+    int16_t tap0;   // index of its first tap
+};
+struct UtTap {
+    int16_t kcol;   // weight K column
+    int8_t dt;      // time shift
+    int8_t res;     // residual accumulator
+    int8_t first;   // first MMA into its accumulator
+};
+
+struct UtArgs {
+    CUtensorMap tmA[3];
+    CUtensorMap tmW;
+    CUtensorMap tmR;
+    UtGroup grp[UT_MAXG];
+    UtTap tap[UT_MAXTAP];
+    int n_grp, n_tap;
+    int sa_stages, sb_stages;
+    int B, Tv, nb, S;
+    const float* bias;
+    const float* gamma;
+    const float* beta;
+    const float* rbias;
+    const __nv_bfloat16* res_src;
+    const float* film;
+    int film_col;
+    __nv_bfloat16* out;
+    const float* wout;
+    const float* bout;
+    float* x;
+    StepCoef sc;
+    int p0;
+    unsigned key;
+    const float* q_start;
+    float* traj;
+    float lo, hi;
+    float* eps_out;
+    int dbg;
+};
+
+// SW128 K-major descriptor for a matrix starting `row` rows into a 1024-B aligned slot
+// (measured on B200: the MMA applies the SW128 XOR pattern from absolute smem address
+// bits, so a row-shifted start needs no base-offset field; setting it breaks results)
+__device__ __forceinline__ uint64_t umma_desc_sw128_rows(const void* slot, int row) {
+    const uint32_t a = smem_u32(slot) + (uint32_t)row * 128u;
+    uint64_t d = 0;
+    d |= (uint64_t)((a >> 4) & 0x3FFF);
+    d |= (uint64_t)(1024 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+template <int N, int EPI, bool RES>
+__global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_constant__ UtArgs a) {
+    constexpr int B_BYTES = N * 128;
+    constexpr int ACC = acc_cols<N, RES>();
+    constexpr int NBUF = n_accbuf<N, RES>();
+    constexpr int NCOLS = tmem_alloc_cols<N, RES>();
+    constexpr int CG = N / 8;
+    // both warpgroups drain every tile (each half of the GroupNorm groups); FINAL needs all
+    // 64 channels per row for the 64->7 projection, so its warpgroups alternate tiles
+    constexpr int NSPLIT = EPI == EPI_FINAL ? 1 : 2;
+    constexpr int NC = N / NSPLIT;
+    constexpr int NG = 8 / NSPLIT;
+    extern __shared__ __align__(1024) uint8_t smem_dyn[];
+    // SW128 tiles need 1024-B alignment; offset within the shared array (keeps LDS/STS)
+    uint8_t* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
+    const int Tv = a.Tv, nb = a.nb;
+    const int A_BYTES = (Tv + 4) * nb * 128;
+    const int SA = a.sa_stages, SB = a.sb_stages;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + (size_t)SA * A_BYTES;
+    uint64_t* a_full = reinterpret_cast<uint64_t*>(sB + (size_t)SB * B_BYTES);
+    uint64_t* a_empty = a_full + SA;
+    uint64_t* b_full = a_empty + SA;
+    uint64_t* b_empty = b_full + SB;
+    uint64_t* tfull = b_empty + SB;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* s_bias = reinterpret_cast<float*>(tmem_holder + 4);
+    float* s_gamma = s_bias + N;
+    float* s_beta = s_gamma + N;
+    float* s_rbias = s_beta + N;
+    float* s_wout = s_rbias + N;                 // [7][64]
+    float* s_red = s_wout + 7 * 64;              // [WG][4 quadrants][16 samples][2*NG]
+    float* s_film = s_red + TC_EPI_WG * 4 * 16 * 16;  // [WG][TC_FILM_P][2N]
+    UtGroup* s_grp = reinterpret_cast<UtGroup*>(s_film + TC_EPI_WG * TC_FILM_P * 2 * N);
+    UtTap* s_tap = reinterpret_cast<UtTap*>(s_grp + UT_MAXG);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_tiles = (a.B + nb - 1) / nb;
+    const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < SA; ++i) {
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_empty[i], 1);
+        }
+        for (int i = 0; i < SB; ++i) {
+            mbar_init(&b_full[i], 1);
+            mbar_init(&b_empty[i], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 128 * NSPLIT);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmA[0]) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmW) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "r"(NCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (warp >= 2) {
+        for (int i = threadIdx.x - 64; i < N; i += 128 * TC_EPI_WG) {
+            s_bias[i] = a.bias[i];
+            if (EPI != EPI_PLAIN) {
+                s_gamma[i] = a.gamma[i];
+                s_beta[i] = a.beta[i];
+            }
+            if (RES) s_rbias[i] = a.rbias[i];
+        }
+        if (EPI == EPI_FINAL)
+            for (int i = threadIdx.x - 64; i < U_DOF * 64; i += 128 * TC_EPI_WG) s_wout[i] = a.wout[i];
+        for (int i = threadIdx.x - 64; i < a.n_grp; i += 128 * TC_EPI_WG) s_grp[i] = a.grp[i];
+        for (int i = threadIdx.x - 64; i < a.n_tap; i += 128 * TC_EPI_WG) s_tap[i] = a.tap[i];
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int sa = 0, sb = 0;
+            uint32_t pa = 0, pb = 0;   // phase bits of the A / B rings
+            const int n_grp = a.n_grp;
+            for (int j = 0; j < my_tiles; ++j) {
+                const int b0 = (blockIdx.x + j * gridDim.x) * nb;
+                for (int g = 0; g < n_grp; ++g) {
+                    const UtGroup gr = s_grp[g];
+                    mbar_wait(&a_empty[sa], pa ^ 1u);
+                    if (a.dbg & 8) {
+                        mbar_arrive(&a_full[sa]);
+                    } else {
+                        mbar_expect_tx(&a_full[sa], (uint32_t)A_BYTES);
+                        tma_load_3d(sA + (size_t)sa * A_BYTES, &a.tmA[gr.src], &a_full[sa], gr.c, b0, -2);
+                    }
+                    if (++sa == SA) { sa = 0; pa ^= 1u; }
+                    for (int k = 0; k < gr.ntap; ++k) {
+                        const UtTap tp = s_tap[gr.tap0 + k];
+                        mbar_wait(&b_empty[sb], pb ^ 1u);
+                        if (a.dbg & 16) {
+                            mbar_arrive(&b_full[sb]);
+                        } else {
+                            mbar_expect_tx(&b_full[sb], (uint32_t)B_BYTES);
+                            tma_load_2d(sB + (size_t)sb * B_BYTES, tp.res ? &a.tmR : &a.tmW, &b_full[sb], tp.kcol, 0);
+                        }
+                        if (++sb == SB) { sb = 0; pb ^= 1u; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16(128, N);
+            int sa = 0, sb = 0;
+            uint32_t pa = 0, pb = 0;
+            const int n_grp = a.n_grp;
+            const bool do_mma = !(a.dbg & 2);
+            const uint64_t dA0 = umma_desc_sw128(sA), dB0 = umma_desc_sw128(sB);
+            const uint64_t a_step = (uint64_t)(A_BYTES >> 4), b_step = (uint64_t)(B_BYTES >> 4);
+            const uint64_t row_step = (uint64_t)((nb * 128) >> 4);
+            int buf = 0;
+            uint32_t tph = 0;
+            for (int j = 0; j < my_tiles; ++j) {
+                mbar_wait(&tempty[buf], tph ^ 1u);
+                tc_fence_after();
+                const uint32_t acc0 = tmem_base + (uint32_t)(buf * ACC);
+                for (int g = 0; g < n_grp; ++g) {
+                    const UtGroup gr = s_grp[g];
+                    mbar_wait(&a_full[sa], pa);
+                    const uint64_t dA = dA0 + (uint64_t)sa * a_step;
+                    for (int k = 0; k < gr.ntap; ++k) {
+                        const UtTap tp = s_tap[gr.tap0 + k];
+                        mbar_wait(&b_full[sb], pb);
+                        tc_fence_after();
+                        const uint64_t da = dA + (uint64_t)(2 + tp.dt) * row_step;
+                        const uint64_t db = dB0 + (uint64_t)sb * b_step;
+                        const uint32_t d_tmem = acc0 + (tp.res ? (uint32_t)N : 0u);
+                        if (do_mma) {
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                umma_bf16(d_tmem, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc,
+                                          (tp.first && kk == 0) ? 0u : 1u);
+                        }
+                        umma_commit(&b_empty[sb]);
+                        if (++sb == SB) { sb = 0; pb ^= 1u; }
+                    }
+                    umma_commit(&a_empty[sa]);
+                    if (++sa == SA) { sa = 0; pa ^= 1u; }
+                }
+                umma_commit(&tfull[buf]);
+                if (++buf == NBUF) { buf = 0; tph ^= 1u; }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ============================ epilogue ============================
+        const int wg = (warp - 2) >> 2;
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        const int t = r / nb, sl = r % nb;   // tile row = (time, sample)
+        const float inv_n = 1.0f / (float)(Tv * CG);
+        float* red = s_red + wg * (4 * 16 * 16);
+        const int cbase = NSPLIT == 2 ? wg * NC : 0;
+        const int j0 = NSPLIT == 2 ? 0 : wg;
+        const int jstep = NSPLIT == 2 ? 1 : TC_EPI_WG;
+        for (int j = j0; j < my_tiles; j += jstep) {
+            const int tile = blockIdx.x + j * gridDim.x;
+            const int buf = j % NBUF;
+            const int b = tile * nb + sl;
+            const bool valid = b < a.B;
+            const int grow = b * Tv + t;
+            const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC + cbase);
+            mbar_wait(&tfull[buf], (uint32_t)(j / NBUF) & 1u);
+            tc_fence_after();
+
+            if (a.dbg & 1) {
+            } else if constexpr (EPI == EPI_PLAIN) {
+#pragma unroll 1
+                for (int cc = 0; cc < NC; cc += 32) {
+                    float v[32];
+                    tmem_ld32(t_lane + cc, v);
+                    if (valid) {
+                        const int c0 = cbase + cc;
+                        __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
+#pragma unroll
+                        for (int jj = 0; jj < 32; jj += 8) {
+                            __align__(16) __nv_bfloat162 pk[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                pk[u] = __floats2bfloat162_rn(v[jj + 2 * u] + s_bias[c0 + jj + 2 * u],
+                                                              v[jj + 2 * u + 1] + s_bias[c0 + jj + 2 * u + 1]);
+                            *reinterpret_cast<uint4*>(o + jj) = *reinterpret_cast<uint4*>(pk);
+                        }
+                    }
+                }
+            } else {
+                // ---- GroupNorm statistics: rows of one sample share `sl` across all 4 warps
+                float s1[NG], s2[NG], mean[NG], rstd[NG];
+#pragma unroll
+                for (int g = 0; g < NG; ++g) s1[g] = s2[g] = 0.f;
+#pragma unroll
+                for (int cc = 0; cc < NC; cc += 32) {
+                    float v[32];
+                    tmem_ld32(t_lane + cc, v);
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj) {
+                        const float xv = v[jj] + s_bias[cbase + cc + jj];
+                        s1[(cc + jj) / CG] += xv;
+                        s2[(cc + jj) / CG] = fmaf(xv, xv, s2[(cc + jj) / CG]);
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1)
+                    if (off >= nb)
+#pragma unroll
+                        for (int g = 0; g < NG; ++g) {
+                            s1[g] += __shfl_xor_sync(PS_FULL, s1[g], off);
+                            s2[g] += __shfl_xor_sync(PS_FULL, s2[g], off);
+                        }
+                asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+                if (lane < nb)
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        red[(q * 16 + sl) * 16 + g] = s1[g];
+                        red[(q * 16 + sl) * 16 + 8 + g] = s2[g];
+                    }
+                asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    float a1 = 0.f, a2 = 0.f;
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) {
+                        a1 += red[(qq * 16 + sl) * 16 + g];
+                        a2 += red[(qq * 16 + sl) * 16 + 8 + g];
+                    }
+                    mean[g] = a1 * inv_n;
+                    rstd[g] = rsqrtf(fmaxf(fmaf(a2, inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
+                }
+
+                const int p = b / a.S;
+                if constexpr (EPI == EPI_FINAL) {
+                    static_assert(N == 64 && NSPLIT == 1, "final layer has 64 channels");
+                    float y[64];
+#pragma unroll
+                    for (int c0 = 0; c0 < 64; c0 += 32) {
+                        float v[32];
+                        tmem_ld32(t_lane + c0, v);
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) {
+                            const int c = c0 + jj;
+                            const float tt = (v[jj] + s_bias[c] - mean[c / CG]) * rstd[c / CG];
+                            y[c] = mish_fast(fmaf(tt, s_gamma[c], s_beta[c]));
+                        }
+                    }
+                    if (valid) {
+                        float eps[U_DOF];
+#pragma unroll
+                        for (int d = 0; d < U_DOF; ++d) {
+                            float acc = a.bout[d];
+#pragma unroll
+                            for (int c = 0; c < 64; ++c) acc = fmaf(y[c], s_wout[d * 64 + c], acc);
+                            eps[d] = acc;
+                        }
+                        float* xr = a.x + (size_t)grow * U_DOF;
+                        if (a.eps_out) {
+#pragma unroll
+                            for (int d = 0; d < U_DOF; ++d) a.eps_out[(size_t)grow * U_DOF + d] = eps[d];
+                        } else {
+                            const StepCoef sc = a.sc;
+#pragma unroll
+                            for (int d = 0; d < U_DOF; ++d) {
+                                const float xv = xr[d];
+                                float x0 = (xv - sc.sq1m * eps[d]) * sc.rsq;
+                                x0 = fminf(fmaxf(x0, -0.1f), 1.1f);
+                                if (sc.last) {
+                                    a.traj[(size_t)grow * U_DOF + d] =
+                                        (t == 0) ? a.q_start[(size_t)p * U_DOF + d] : a.lo + x0 * (a.hi - a.lo);
+                                } else if (sc.ddpm) {
+                                    const float z = normal_tc((uint32_t)sc.k, (uint32_t)(a.p0 + p),
+                                                              (uint32_t)(b % a.S), (uint32_t)(t * U_DOF + d), a.key);
+                                    xr[d] = sc.c0 * x0 + sc.c1 * xv + sc.sig * z;
+                                } else {
+                                    xr[d] = sc.sqn * x0 + sc.sq1mn * eps[d];
+                                }
+                            }
+                        }
+                    }
+                } else {
+                    // per-tile FiLM rows staged as (1 + scale, shift) for this warpgroup's columns
+                    const float* fs1 = nullptr;
+                    const float* fsh = nullptr;
+                    if constexpr (EPI == EPI_GN_FILM) {
+                        const int b_last = min(tile * nb + nb - 1, a.B - 1);
+                        const int p_lo = (tile * nb) / a.S, p_hi = b_last / a.S;
+                        float* sf = s_film + wg * (TC_FILM_P * 2 * N);
+                        if (p_hi - p_lo < TC_FILM_P) {
+                            const int n = (p_hi - p_lo + 1) * 2 * NC;
+                            for (int i = r; i < n; i += 128) {
+                                const int pp = i / (2 * NC), w = i % (2 * NC);
+                                const int c = cbase + (w < NC ? w : w - NC);
+                                const float v = __ldg(a.film + (size_t)(p_lo + pp) * 3584 + a.film_col +
+                                                      (w < NC ? c : N + c));
+                                sf[pp * 2 * NC + w] = w < NC ? 1.f + v : v;
+                            }
+                            asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+                            fs1 = sf + (p - p_lo) * 2 * NC;
+                            fsh = fs1 + NC;
+                        }
+                    }
+                    float nmr[NG];
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) nmr[g] = -mean[g] * rstd[g];
+                    if (valid) {
+#pragma unroll 1
+                        for (int cc = 0; cc < NC; cc += 16) {
+                            const int c0 = cbase + cc;
+                            uint32_t rr[16], rq[16];
+                            tmem_ld16(t_lane + cc, rr);
+                            if constexpr (RES) tmem_ld16(t_lane + N + cc, rq);
+                            tmem_wait_ld();
+                            const int gi = cc / CG;
+                            const float rs = sel(rstd, gi), nm = sel(nmr, gi);
+                            const float rs2 = CG < 16 ? sel(rstd, gi + 1) : rs;
+                            const float nm2 = CG < 16 ? sel(nmr, gi + 1) : nm;
+                            float y[16];
+#pragma unroll
+                            for (int jj = 0; jj < 16; jj += 4) {
+                                const float4 bi = *reinterpret_cast<const float4*>(s_bias + c0 + jj);
+                                const float4 ga = *reinterpret_cast<const float4*>(s_gamma + c0 + jj);
+                                const float4 be = *reinterpret_cast<const float4*>(s_beta + c0 + jj);
+                                const float bv[4] = {bi.x, bi.y, bi.z, bi.w}, gv[4] = {ga.x, ga.y, ga.z, ga.w},
+                                            ev[4] = {be.x, be.y, be.z, be.w};
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const bool hi = CG < 16 && (jj + u) >= CG;
+                                    const float xv = __uint_as_float(rr[jj + u]) + bv[u];
+                                    const float tt = fmaf(xv, hi ? rs2 : rs, hi ? nm2 : nm);
+                                    y[jj + u] = mish8(fmaf(tt, gv[u], ev[u]));
+                                }
+                            }
+                            if constexpr (EPI == EPI_GN_FILM) {
+                                if (fs1) {
+#pragma unroll
+                                    for (int jj = 0; jj < 16; jj += 4) {
+                                        const float4 m1 = *reinterpret_cast<const float4*>(fs1 + cc + jj);
+                                        const float4 sh = *reinterpret_cast<const float4*>(fsh + cc + jj);
+                                        y[jj] = fmaf(y[jj], m1.x, sh.x);
+                                        y[jj + 1] = fmaf(y[jj + 1], m1.y, sh.y);
+                                        y[jj + 2] = fmaf(y[jj + 2], m1.z, sh.z);
+                                        y[jj + 3] = fmaf(y[jj + 3], m1.w, sh.w);
+                                    }
+                                } else {
+                                    const float* fr = a.film + (size_t)p * 3584 + a.film_col;
+#pragma unroll
+                                    for (int jj = 0; jj < 16; ++jj)
+                                        y[jj] = fmaf(y[jj], 1.f + __ldg(fr + c0 + jj), __ldg(fr + N + c0 + jj));
+                                }
+                            } else if constexpr (RES) {
+#pragma unroll
+                                for (int jj = 0; jj < 16; ++jj) y[jj] += __uint_as_float(rq[jj]) + s_rbias[c0 + jj];
+                            } else {
+                                const uint4* rsrc = reinterpret_cast<const uint4*>(a.res_src + (size_t)grow * N + c0);
+#pragma unroll
+                                for (int jj = 0; jj < 16; jj += 8) {
+                                    uint4 u = __ldg(rsrc + jj / 8);
+                                    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                                    for (int k2 = 0; k2 < 4; ++k2) {
+                                        const float2 f = __bfloat1622float2(h2[k2]);
+                                        y[jj + 2 * k2] += f.x;
+                                        y[jj + 2 * k2 + 1] += f.y;
+                                    }
+                                }
+                            }
+                            __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
+#pragma unroll
+                            for (int jj = 0; jj < 16; jj += 8) {
+                                __align__(16) __nv_bfloat162 pk[4];
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) pk[u] = __floats2bfloat162_rn(y[jj + 2 * u], y[jj + 2 * u + 1]);
+                                *reinterpret_cast<uint4*>(o + jj) = *reinterpret_cast<uint4*>(pk);
+                            }
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[buf]);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NCOLS));
+    }
+}
+
+// activation view [B][Tv][C] bf16 read in (time, sample) order: dims (C, B, Tv), box {64, nb, Tv+4}
+static bool make_ts_map(CUtensorMap* tm, const void* base, int B, int Tv, int C) {
+    const int nb = 128 / Tv;
+    cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)B, (cuuint64_t)Tv};
+    cuuint64_t strides[2] = {(cuuint64_t)Tv * C * 2, (cuuint64_t)C * 2};
+    cuuint32_t box[3] = {64, (cuuint32_t)nb, (cuuint32_t)(Tv + 4)};
+    cuuint32_t es[3] = {1, 1, 1};
+    return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int N, int EPI, bool RES>
+static int launch_ut(UtArgs& a, cudaStream_t st) {
+    const int A_BYTES = (a.Tv + 4) * a.nb * 128;
+    constexpr int B_BYTES = N * 128;
+    const size_t vec = (size_t)(4 * N + 7 * 64 + TC_EPI_WG * 4 * 16 * 16 + TC_EPI_WG * TC_FILM_P * 2 * N) * 4 +
+                       UT_MAXG * sizeof(UtGroup) + UT_MAXTAP * sizeof(UtTap) + 64;
+    const size_t budget = 225 * 1024 - vec - 2048;
+    a.sa_stages = 3;
+    a.sb_stages = (int)std::min<size_t>(8, (budget - (size_t)a.sa_stages * A_BYTES) / B_BYTES);
+    if (a.sb_stages < 2) return PS_FAIL(PS_ERR_SHAPE);
+    const size_t smem = 1024 + (size_t)a.sa_stages * A_BYTES + (size_t)a.sb_stages * B_BYTES +
+                        (2 * (a.sa_stages + a.sb_stages) + 4) * 8 + 16 + vec;
+    auto kern = unet_tc_kernel<N, EPI, RES>;
+    static int set_bytes = 0;
+    if ((int)smem > set_bytes) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return PS_FAIL(PS_ERR_CUDA);
+        set_bytes = (int)smem;
+    }
+    static const int dbg = std::getenv("PS_TC_DBG") ? std::atoi(std::getenv("PS_TC_DBG")) : 0;
+    a.dbg = dbg;
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int n_tiles = (a.B + a.nb - 1) / a.nb;
+    const int grid = n_tiles < n_sm ? n_tiles : n_sm;
+    kern<<<grid, TC_THREADS, smem, st>>>(a);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
 // One conv layer.  src[0..2]: activation views (bf16 [B][Tv][ld]); the main conv's
 // segments read src[seg.src], the residual 1x1 reads src[seg.src + res_shift].
 struct TcLayer {
     const PConv* c;
-    const PConv* res;  // residual GEMM (1x1), may be null
+    const PConv* res;
     int epi;
     const __nv_bfloat16* src[3];
     int ld[3];
     int res_shift;
     int Tv;
     __nv_bfloat16* out;
-    const __nv_bfloat16* res_src;  // identity residual
+    const __nv_bfloat16* res_src;
 };
 
 static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int B, int S, const float* film,
                      float* x, const TcStep* step, float* eps_out, cudaStream_t st) {
-    TcArgs a;
+    UtArgs a;
     memset(&a, 0, sizeof(a));
     const PConv& c = *ly.c;
     const int N = c.N;
     const __nv_bfloat16* W = reinterpret_cast<const __nv_bfloat16*>(packed);
     for (int s = 0; s < 3; ++s)
-        if (ly.src[s] && !make_act_map(&a.tmA[s], ly.src[s], B, ly.Tv, ly.ld[s])) return PS_FAIL(PS_ERR_CUDA);
+        if (ly.src[s] && !make_ts_map(&a.tmA[s], ly.src[s], B, ly.Tv, ly.ld[s])) return PS_FAIL(PS_ERR_CUDA);
     if (!make_w_map(&a.tmW, W + c.w_off, N, (int)kpad(c.K))) return PS_FAIL(PS_ERR_CUDA);
-    int n = 0;
-    auto add_chunks = [&](const PConv& cc, int res, int shift) -> bool {
-        bool first = true;
+    if (ly.res && !make_w_map(&a.tmR, W + ly.res->w_off, N, (int)kpad(ly.res->K))) return PS_FAIL(PS_ERR_CUDA);
+    // group taps by the activation chunk they read: (src, channel offset)
+    struct Tmp { int src, c; std::vector<UtTap> taps; };
+    std::vector<Tmp> groups;
+    bool first_main = true, first_res = true;
+    auto add = [&](const PConv& cc, int res, int shift) {
         for (int i = 0; i < cc.n_seg; ++i) {
             const PSeg& sg = cc.seg[i];
             for (int j = 0; j < sg.nc; j += 64) {
-                if (n >= TC_MAX_CHUNKS) return false;
-                TcChunk ch;
-                ch.c = (int16_t)(sg.c0 + j);
-                ch.kcol = (int16_t)(sg.k0 + j);
-                ch.src = (int8_t)(sg.src + shift);
-                ch.dt = (int8_t)sg.dt;
-                ch.res = (int8_t)res;
-                ch.first = first ? 1 : 0;
-                first = false;
-                a.chunk[n++] = ch;
+                const int src = sg.src + shift, ch = sg.c0 + j;
+                Tmp* gp = nullptr;
+                for (auto& g : groups)
+                    if (g.src == src && g.c == ch) gp = &g;
+                if (!gp) {
+                    groups.push_back(Tmp{src, ch, {}});
+                    gp = &groups.back();
+                }
+                UtTap tp;
+                tp.kcol = (int16_t)(sg.k0 + j);
+                tp.dt = (int8_t)sg.dt;
+                tp.res = (int8_t)res;
+                tp.first = 0;
+                gp->taps.push_back(tp);
             }
         }
-        return true;
     };
-    if (!add_chunks(c, 0, 0)) return PS_FAIL(PS_ERR_SHAPE);
-    if (ly.res) {
-        if (!make_w_map(&a.tmR, W + ly.res->w_off, N, (int)kpad(ly.res->K))) return PS_FAIL(PS_ERR_CUDA);
-        if (!add_chunks(*ly.res, 1, ly.res_shift)) return PS_FAIL(PS_ERR_SHAPE);
+    add(c, 0, 0);
+    if (ly.res) add(*ly.res, 1, ly.res_shift);
+    if ((int)groups.size() > UT_MAXG) return PS_FAIL(PS_ERR_SHAPE);
+    int nt = 0;
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        UtGroup& g = a.grp[gi];
+        g.c = (int16_t)groups[gi].c;
+        g.src = (int8_t)groups[gi].src;
+        g.ntap = (int8_t)groups[gi].taps.size();
+        g.tap0 = (int16_t)nt;
+        for (auto tp : groups[gi].taps) {
+            if (nt >= UT_MAXTAP) return PS_FAIL(PS_ERR_SHAPE);
+            bool& f = tp.res ? first_res : first_main;
+            tp.first = f ? 1 : 0;
+            f = false;
+            a.tap[nt++] = tp;
+        }
     }
-    a.n_chunks = n;
-    a.rows = B * ly.Tv;
+    a.n_grp = (int)groups.size();
+    a.n_tap = nt;
+    a.B = B;
     a.Tv = ly.Tv;
+    a.nb = 128 / ly.Tv;
     a.S = S;
     const float* side = L.side(packed);
     a.bias = side + c.b_off;
@@ -786,7 +1202,6 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
     a.film = film;
     a.film_col = c.film_col;
     a.out = ly.out;
-    const int n_tiles = (a.rows + 127) / 128;
     if (ly.epi == EPI_FINAL) {
         a.wout = side + L.outw_f32;
         a.bout = side + L.out.b_off;
@@ -801,14 +1216,14 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
             a.lo = step->lo;
             a.hi = step->hi;
         }
-        return launch_tc<64, EPI_FINAL, false>(a, n_tiles, st);
+        return launch_ut<64, EPI_FINAL, false>(a, st);
     }
-#define PS_DISPATCH(NN)                                                                     \
-    if (N == NN) {                                                                          \
-        if (ly.epi == EPI_PLAIN) return launch_tc<NN, EPI_PLAIN, false>(a, n_tiles, st);     \
-        if (ly.epi == EPI_GN_FILM) return launch_tc<NN, EPI_GN_FILM, false>(a, n_tiles, st); \
-        if (ly.res) return launch_tc<NN, EPI_GN_RES, true>(a, n_tiles, st);                  \
-        return launch_tc<NN, EPI_GN_RES, false>(a, n_tiles, st);                             \
+#define PS_DISPATCH(NN)                                                                   \
+    if (N == NN) {                                                                        \
+        if (ly.epi == EPI_PLAIN) return launch_ut<NN, EPI_PLAIN, false>(a, st);           \
+        if (ly.epi == EPI_GN_FILM) return launch_ut<NN, EPI_GN_FILM, false>(a, st);       \
+        if (ly.res) return launch_ut<NN, EPI_GN_RES, true>(a, st);                        \
+        return launch_ut<NN, EPI_GN_RES, false>(a, st);                                   \
     }
     PS_DISPATCH(64)
     PS_DISPATCH(128)
@@ -818,7 +1233,6 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
 }
 
 size_t tc_workspace_bytes(int B, int T) {
-    // bf16: a0 (B*T*64) + 5 slots (B*T*128: cur, nxt, h, skip1, skip2) + fp32 step FiLM (P <= B rows)
     const size_t slot = (size_t)B * T * 128 * 2;
     return (size_t)B * T * 64 * 2 + 5 * slot + (size_t)B * 3584 * 4 + 4096;
 }
@@ -850,7 +1264,6 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
         im2col_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(x, B, T, a0);
         PS_CHECK_LAUNCH();
     }
-    // residual block: conv0 (+GN+Mish+FiLM) -> h ; conv1 (+GN+Mish) + residual -> out
     auto block = [&](int bi, const __nv_bfloat16* in0, int ld0, const __nv_bfloat16* in1, int ld1,
                      __nv_bfloat16* out) -> int {
         const PBlock& bk = L.blk[bi];
@@ -911,7 +1324,6 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
     lf.Tv = T;
     return run_layer(L, packed, lf, B, S, film, x, step, step ? nullptr : eps, st);
 }
-
 
 // ===========================================================================
 // Observation encoder on tcgen05: conv3x3 stride 2 pad 1 + ReLU as a segment GEMM
