@@ -671,12 +671,14 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_rows(const void* slot, int r
     return d;
 }
 
-template <int N, int EPI, bool RES>
+// MB = M-blocks (128 rows) per tile: every weight stage feeds MB x 4 MMAs.
+template <int N, int EPI, bool RES, int MB>
 __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_constant__ UtArgs a) {
     constexpr int B_BYTES = N * 128;
-    constexpr int ACC = acc_cols<N, RES>();
-    constexpr int NBUF = n_accbuf<N, RES>();
-    constexpr int NCOLS = tmem_alloc_cols<N, RES>();
+    constexpr int ACC1 = acc_cols<N, RES>();          // columns of one M-block
+    constexpr int ACC = MB * ACC1;                     // columns of one tile
+    constexpr int NBUF = 2 * ACC <= 512 ? 2 : 1;
+    constexpr int NCOLS = NBUF * ACC <= 32 ? 32 : NBUF * ACC <= 64 ? 64 : NBUF * ACC <= 128 ? 128 : NBUF * ACC <= 256 ? 256 : 512;
     constexpr int CG = N / 8;
     // both warpgroups drain every tile (each half of the GroupNorm groups); FINAL needs all
     // 64 channels per row for the 64->7 projection, so its warpgroups alternate tiles
@@ -703,8 +705,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
     float* s_beta = s_gamma + N;
     float* s_rbias = s_beta + N;
     float* s_wout = s_rbias + N;                 // [7][64]
-    float* s_red = s_wout + 7 * 64;              // [WG][4 quadrants][16 samples][2*NG]
-    float* s_film = s_red + TC_EPI_WG * 4 * 16 * 16;  // [WG][TC_FILM_P][2N]
+    float* s_red = s_wout + 7 * 64;              // [WG][4 quadrants][32 samples][16]
+    float* s_film = s_red + TC_EPI_WG * 4 * 32 * 16;  // [WG][TC_FILM_P][2N]
     UtGroup* s_grp = reinterpret_cast<UtGroup*>(s_film + TC_EPI_WG * TC_FILM_P * 2 * N);
     UtTap* s_tap = reinterpret_cast<UtTap*>(s_grp + UT_MAXG);
 
@@ -813,9 +815,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
                         const uint32_t d_tmem = acc0 + (tp.res ? (uint32_t)N : 0u);
                         if (do_mma) {
 #pragma unroll
-                            for (int kk = 0; kk < 4; ++kk)
-                                umma_bf16(d_tmem, da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc,
-                                          (tp.first && kk == 0) ? 0u : 1u);
+                            for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+                                for (int kk = 0; kk < 4; ++kk)
+                                    umma_bf16(d_tmem + (uint32_t)(mb * ACC1), da + (uint64_t)(mb * 128 * 128 / 16 + kk * 2),
+                                              db + (uint64_t)(kk * 2), idesc, (tp.first && kk == 0) ? 0u : 1u);
                         }
                         umma_commit(&b_empty[sb]);
                         if (++sb == SB) { sb = 0; pb ^= 1u; }
@@ -833,9 +837,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
         const int wg = (warp - 2) >> 2;
         const int q = warp & 3;
         const int r = q * 32 + lane;
-        const int t = r / nb, sl = r % nb;   // tile row = (time, sample)
+        const int t0 = r / nb, sl = r % nb;  // tile row = (time, sample); M-block mb adds 128/nb steps
+        const int tstep = 128 / nb;
         const float inv_n = 1.0f / (float)(Tv * CG);
-        float* red = s_red + wg * (4 * 16 * 16);
+        float* red = s_red + wg * (4 * 32 * 16);
         const int cbase = NSPLIT == 2 ? wg * NC : 0;
         const int j0 = NSPLIT == 2 ? 0 : wg;
         const int jstep = NSPLIT == 2 ? 1 : TC_EPI_WG;
@@ -844,28 +849,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
             const int buf = j % NBUF;
             const int b = tile * nb + sl;
             const bool valid = b < a.B;
-            const int grow = b * Tv + t;
-            const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC + cbase);
+            const uint32_t t_lane0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC + cbase);
             mbar_wait(&tfull[buf], (uint32_t)(j / NBUF) & 1u);
             tc_fence_after();
 
             if (a.dbg & 1) {
             } else if constexpr (EPI == EPI_PLAIN) {
 #pragma unroll 1
-                for (int cc = 0; cc < NC; cc += 32) {
-                    float v[32];
-                    tmem_ld32(t_lane + cc, v);
-                    if (valid) {
-                        const int c0 = cbase + cc;
-                        __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
+                for (int mb = 0; mb < MB; ++mb) {
+                    const int grow = b * Tv + t0 + mb * tstep;
+                    const uint32_t t_lane = t_lane0 + (uint32_t)(mb * ACC1);
+#pragma unroll 1
+                    for (int cc = 0; cc < NC; cc += 32) {
+                        float v[32];
+                        tmem_ld32(t_lane + cc, v);
+                        if (valid) {
+                            const int c0 = cbase + cc;
+                            __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
 #pragma unroll
-                        for (int jj = 0; jj < 32; jj += 8) {
-                            __align__(16) __nv_bfloat162 pk[4];
+                            for (int jj = 0; jj < 32; jj += 8) {
+                                __align__(16) __nv_bfloat162 pk[4];
 #pragma unroll
-                            for (int u = 0; u < 4; ++u)
-                                pk[u] = __floats2bfloat162_rn(v[jj + 2 * u] + s_bias[c0 + jj + 2 * u],
-                                                              v[jj + 2 * u + 1] + s_bias[c0 + jj + 2 * u + 1]);
-                            *reinterpret_cast<uint4*>(o + jj) = *reinterpret_cast<uint4*>(pk);
+                                for (int u = 0; u < 4; ++u)
+                                    pk[u] = __floats2bfloat162_rn(v[jj + 2 * u] + s_bias[c0 + jj + 2 * u],
+                                                                  v[jj + 2 * u + 1] + s_bias[c0 + jj + 2 * u + 1]);
+                                *reinterpret_cast<uint4*>(o + jj) = *reinterpret_cast<uint4*>(pk);
+                            }
                         }
                     }
                 }
@@ -875,16 +884,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
 #pragma unroll
                 for (int g = 0; g < NG; ++g) s1[g] = s2[g] = 0.f;
 #pragma unroll
-                for (int cc = 0; cc < NC; cc += 32) {
-                    float v[32];
-                    tmem_ld32(t_lane + cc, v);
+                for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-                    for (int jj = 0; jj < 32; ++jj) {
-                        const float xv = v[jj] + s_bias[cbase + cc + jj];
-                        s1[(cc + jj) / CG] += xv;
-                        s2[(cc + jj) / CG] = fmaf(xv, xv, s2[(cc + jj) / CG]);
+                    for (int cc = 0; cc < NC; cc += 32) {
+                        float v[32];
+                        tmem_ld32(t_lane0 + (uint32_t)(mb * ACC1) + cc, v);
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) {
+                            const float xv = v[jj] + s_bias[cbase + cc + jj];
+                            s1[(cc + jj) / CG] += xv;
+                            s2[(cc + jj) / CG] = fmaf(xv, xv, s2[(cc + jj) / CG]);
+                        }
                     }
-                }
 #pragma unroll
                 for (int off = 16; off >= 1; off >>= 1)
                     if (off >= nb)
@@ -897,8 +908,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
                 if (lane < nb)
 #pragma unroll
                     for (int g = 0; g < NG; ++g) {
-                        red[(q * 16 + sl) * 16 + g] = s1[g];
-                        red[(q * 16 + sl) * 16 + 8 + g] = s2[g];
+                        red[(q * 32 + sl) * 16 + g] = s1[g];
+                        red[(q * 32 + sl) * 16 + 8 + g] = s2[g];
                     }
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
 #pragma unroll
@@ -906,8 +917,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
                     float a1 = 0.f, a2 = 0.f;
 #pragma unroll
                     for (int qq = 0; qq < 4; ++qq) {
-                        a1 += red[(qq * 16 + sl) * 16 + g];
-                        a2 += red[(qq * 16 + sl) * 16 + 8 + g];
+                        a1 += red[(qq * 32 + sl) * 16 + g];
+                        a2 += red[(qq * 32 + sl) * 16 + 8 + g];
                     }
                     mean[g] = a1 * inv_n;
                     rstd[g] = rsqrtf(fmaxf(fmaf(a2, inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
@@ -915,7 +926,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
 
                 const int p = b / a.S;
                 if constexpr (EPI == EPI_FINAL) {
-                    static_assert(N == 64 && NSPLIT == 1, "final layer has 64 channels");
+                    static_assert(N == 64 && NSPLIT == 1 && MB == 1, "final layer has 64 channels");
+                    const int t = t0;
+                    const int grow = b * Tv + t;
+                    const uint32_t t_lane = t_lane0;
                     float y[64];
 #pragma unroll
                     for (int c0 = 0; c0 < 64; c0 += 32) {
@@ -986,7 +1000,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
                     float nmr[NG];
 #pragma unroll
                     for (int g = 0; g < NG; ++g) nmr[g] = -mean[g] * rstd[g];
-                    if (valid) {
+                    // no early-out on `valid`: tcgen05.ld is .sync.aligned and lanes of one warp
+                    // belong to different samples, so only global accesses are predicated
+                    {
+#pragma unroll 1
+                      for (int mb = 0; mb < MB; ++mb) {
+                        const int grow = b * Tv + t0 + mb * tstep;
+                        const uint32_t t_lane = t_lane0 + (uint32_t)(mb * ACC1);
 #pragma unroll 1
                         for (int cc = 0; cc < NC; cc += 16) {
                             const int c0 = cbase + cc;
@@ -1015,7 +1035,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
                                 }
                             }
                             if constexpr (EPI == EPI_GN_FILM) {
-                                if (fs1) {
+                                if (fs1 && valid) {
 #pragma unroll
                                     for (int jj = 0; jj < 16; jj += 4) {
                                         const float4 m1 = *reinterpret_cast<const float4*>(fs1 + cc + jj);
@@ -1025,7 +1045,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
                                         y[jj + 2] = fmaf(y[jj + 2], m1.z, sh.z);
                                         y[jj + 3] = fmaf(y[jj + 3], m1.w, sh.w);
                                     }
-                                } else {
+                                } else if (valid) {
                                     const float* fr = a.film + (size_t)p * 3584 + a.film_col;
 #pragma unroll
                                     for (int jj = 0; jj < 16; ++jj)
@@ -1038,7 +1058,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
                                 const uint4* rsrc = reinterpret_cast<const uint4*>(a.res_src + (size_t)grow * N + c0);
 #pragma unroll
                                 for (int jj = 0; jj < 16; jj += 8) {
-                                    uint4 u = __ldg(rsrc + jj / 8);
+                                    uint4 u = valid ? __ldg(rsrc + jj / 8) : make_uint4(0u, 0u, 0u, 0u);
                                     const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
                                     for (int k2 = 0; k2 < 4; ++k2) {
@@ -1048,15 +1068,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
                                     }
                                 }
                             }
-                            __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
+                            if (valid) {
+                                __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
 #pragma unroll
-                            for (int jj = 0; jj < 16; jj += 8) {
-                                __align__(16) __nv_bfloat162 pk[4];
+                                for (int jj = 0; jj < 16; jj += 8) {
+                                    __align__(16) __nv_bfloat162 pk[4];
 #pragma unroll
-                                for (int u = 0; u < 4; ++u) pk[u] = __floats2bfloat162_rn(y[jj + 2 * u], y[jj + 2 * u + 1]);
-                                *reinterpret_cast<uint4*>(o + jj) = *reinterpret_cast<uint4*>(pk);
+                                    for (int u = 0; u < 4; ++u)
+                                        pk[u] = __floats2bfloat162_rn(y[jj + 2 * u], y[jj + 2 * u + 1]);
+                                    *reinterpret_cast<uint4*>(o + jj) = *reinterpret_cast<uint4*>(pk);
+                                }
                             }
                         }
+                      }
                     }
                 }
             }
@@ -1072,8 +1096,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
 }
 
 // activation view [B][Tv][C] bf16 read in (time, sample) order: dims (C, B, Tv), box {64, nb, Tv+4}
-static bool make_ts_map(CUtensorMap* tm, const void* base, int B, int Tv, int C) {
-    const int nb = 128 / Tv;
+static bool make_ts_map(CUtensorMap* tm, const void* base, int B, int Tv, int C, int nb) {
     cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)B, (cuuint64_t)Tv};
     cuuint64_t strides[2] = {(cuuint64_t)Tv * C * 2, (cuuint64_t)C * 2};
     cuuint32_t box[3] = {64, (cuuint32_t)nb, (cuuint32_t)(Tv + 4)};
@@ -1083,19 +1106,19 @@ static bool make_ts_map(CUtensorMap* tm, const void* base, int B, int Tv, int C)
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int N, int EPI, bool RES>
+template <int N, int EPI, bool RES, int MB>
 static int launch_ut(UtArgs& a, cudaStream_t st) {
     const int A_BYTES = (a.Tv + 4) * a.nb * 128;
     constexpr int B_BYTES = N * 128;
-    const size_t vec = (size_t)(4 * N + 7 * 64 + TC_EPI_WG * 4 * 16 * 16 + TC_EPI_WG * TC_FILM_P * 2 * N) * 4 +
+    const size_t vec = (size_t)(4 * N + 7 * 64 + TC_EPI_WG * 4 * 32 * 16 + TC_EPI_WG * TC_FILM_P * 2 * N) * 4 +
                        UT_MAXG * sizeof(UtGroup) + UT_MAXTAP * sizeof(UtTap) + 64;
     const size_t budget = 225 * 1024 - vec - 2048;
-    a.sa_stages = 3;
+    a.sa_stages = 3 * (size_t)A_BYTES <= 110 * 1024 ? 3 : 2;
     a.sb_stages = (int)std::min<size_t>(8, (budget - (size_t)a.sa_stages * A_BYTES) / B_BYTES);
     if (a.sb_stages < 2) return PS_FAIL(PS_ERR_SHAPE);
     const size_t smem = 1024 + (size_t)a.sa_stages * A_BYTES + (size_t)a.sb_stages * B_BYTES +
                         (2 * (a.sa_stages + a.sb_stages) + 4) * 8 + 16 + vec;
-    auto kern = unet_tc_kernel<N, EPI, RES>;
+    auto kern = unet_tc_kernel<N, EPI, RES, MB>;
     static int set_bytes = 0;
     if ((int)smem > set_bytes) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -1112,8 +1135,12 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     }
     const int n_tiles = (a.B + a.nb - 1) / a.nb;
     const int grid = n_tiles < n_sm ? n_tiles : n_sm;
+    static const bool trace = std::getenv("PS_DEBUG") && std::atoi(std::getenv("PS_DEBUG")) >= 2;
+    if (trace) std::fprintf(stderr, "[ps_b200] unet_tc N=%d EPI=%d RES=%d MB=%d B=%d Tv=%d nb=%d grid=%d groups=%d taps=%d\n",
+                            N, EPI, (int)RES, MB, a.B, a.Tv, a.nb, grid, a.n_grp, a.n_tap);
     kern<<<grid, TC_THREADS, smem, st>>>(a);
     PS_CHECK_LAUNCH();
+    if (trace && cudaStreamSynchronize(st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
     return PS_OK;
 }
 
@@ -1138,8 +1165,14 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
     const PConv& c = *ly.c;
     const int N = c.N;
     const __nv_bfloat16* W = reinterpret_cast<const __nv_bfloat16*>(packed);
+    // two M-blocks per tile where the TMEM budget still allows double buffering
+    const int MBv = (ly.epi != EPI_FINAL && (N == 64 || (N == 128 && !ly.res))) ? 2 : 1;
+    const int nb = MBv * 128 / ly.Tv;
     for (int s = 0; s < 3; ++s)
-        if (ly.src[s] && !make_ts_map(&a.tmA[s], ly.src[s], B, ly.Tv, ly.ld[s])) return PS_FAIL(PS_ERR_CUDA);
+        // maps span >= nb samples (the workspace is padded to TC_MIN_B): a TMA box larger than
+        // the tensor extent never completes its transaction
+        if (ly.src[s] && !make_ts_map(&a.tmA[s], ly.src[s], std::max(B, nb), ly.Tv, ly.ld[s], nb))
+            return PS_FAIL(PS_ERR_CUDA);
     if (!make_w_map(&a.tmW, W + c.w_off, N, (int)kpad(c.K))) return PS_FAIL(PS_ERR_CUDA);
     if (ly.res && !make_w_map(&a.tmR, W + ly.res->w_off, N, (int)kpad(ly.res->K))) return PS_FAIL(PS_ERR_CUDA);
     // group taps by the activation chunk they read: (src, channel offset)
@@ -1189,7 +1222,7 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
     a.n_tap = nt;
     a.B = B;
     a.Tv = ly.Tv;
-    a.nb = 128 / ly.Tv;
+    a.nb = nb;
     a.S = S;
     const float* side = L.side(packed);
     a.bias = side + c.b_off;
@@ -1216,25 +1249,28 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
             a.lo = step->lo;
             a.hi = step->hi;
         }
-        return launch_ut<64, EPI_FINAL, false>(a, st);
+        return launch_ut<64, EPI_FINAL, false, 1>(a, st);
     }
-#define PS_DISPATCH(NN)                                                                   \
-    if (N == NN) {                                                                        \
-        if (ly.epi == EPI_PLAIN) return launch_ut<NN, EPI_PLAIN, false>(a, st);           \
-        if (ly.epi == EPI_GN_FILM) return launch_ut<NN, EPI_GN_FILM, false>(a, st);       \
-        if (ly.res) return launch_ut<NN, EPI_GN_RES, true>(a, st);                        \
-        return launch_ut<NN, EPI_GN_RES, false>(a, st);                                   \
+#define PS_DISPATCH(NN, MBR, MBN)                                                            \
+    if (N == NN) {                                                                           \
+        if (ly.epi == EPI_PLAIN) return launch_ut<NN, EPI_PLAIN, false, MBN>(a, st);         \
+        if (ly.epi == EPI_GN_FILM) return launch_ut<NN, EPI_GN_FILM, false, MBN>(a, st);     \
+        if (ly.res) return launch_ut<NN, EPI_GN_RES, true, MBR>(a, st);                      \
+        return launch_ut<NN, EPI_GN_RES, false, MBN>(a, st);                                 \
     }
-    PS_DISPATCH(64)
-    PS_DISPATCH(128)
-    PS_DISPATCH(256)
+    PS_DISPATCH(64, 2, 2)
+    PS_DISPATCH(128, 1, 2)
+    PS_DISPATCH(256, 1, 1)
 #undef PS_DISPATCH
     return PS_FAIL(PS_ERR_SHAPE);
 }
 
+constexpr int TC_MIN_B = 64;   // activation slots are padded to at least this many samples
+
 size_t tc_workspace_bytes(int B, int T) {
-    const size_t slot = (size_t)B * T * 128 * 2;
-    return (size_t)B * T * 64 * 2 + 5 * slot + (size_t)B * 3584 * 4 + 4096;
+    const size_t Bp = (size_t)std::max(B, TC_MIN_B);
+    const size_t slot = Bp * T * 128 * 2;
+    return Bp * T * 64 * 2 + 5 * slot + (size_t)B * 3584 * 4 + 4096;
 }
 
 #define PS_TRY_TC(x)        \
@@ -1248,9 +1284,10 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
     if (!get_encoder()) return PS_FAIL(PS_ERR_CUDA);
     if (L.mode != 1) return PS_FAIL(PS_ERR_SHAPE);
     const int P = B / S;
-    const size_t slot = (size_t)B * T * 128;
+    const size_t Bp = (size_t)std::max(B, TC_MIN_B);
+    const size_t slot = Bp * T * 128;
     __nv_bfloat16* a0 = reinterpret_cast<__nv_bfloat16*>(ws);
-    __nv_bfloat16* cur = a0 + (size_t)B * T * 64;
+    __nv_bfloat16* cur = a0 + Bp * T * 64;
     __nv_bfloat16* nxt = cur + slot;
     __nv_bfloat16* h = nxt + slot;
     __nv_bfloat16* skip1 = h + slot;

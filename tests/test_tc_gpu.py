@@ -105,3 +105,16 @@ def test_tc_encoder_vs_oracle(cfg):
     emb_err = np.abs(got[:, :256] - want[:, :256]).max() / np.abs(want[:, :256]).max()
     assert emb_err < 1e-2
     np.testing.assert_allclose(got[:, 256:], want[:, 256:], rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("P,S,T", [(1, 4, 32), (3, 5, 32), (2, 2, 64), (1, 16, 32)])
+def test_partial_tiles_odd_batches(samplers, params, P, S, T):
+    # batches that do not fill a tile: lanes of one warp hold different samples, so the
+    # epilogue must keep tcgen05.ld convergent and predicate only global accesses
+    _, s1 = samplers
+    cond = _cond(P, 17)
+    x = np.random.default_rng(P * S).standard_normal((P * S, T, 7)).astype(np.float32)
+    eps = s1.predict_noise(x, 33, s1.film(cond), S).cpu().numpy()
+    want = un.unet_forward(params, ARCH, x, 33, cond, S)
+    d = eps - want
+    assert np.sqrt((d ** 2).mean()) / np.sqrt((want ** 2).mean()) < 2e-2
