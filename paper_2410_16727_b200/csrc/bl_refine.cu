@@ -9,6 +9,8 @@
 // block (__grid_constant__, constant bank broadcast); the trajectory state stays in
 // registers for all iterations; the per-problem ESDF (128^3 fp32 = 8 MiB) is read
 // through the read-only path with 8 scalar gathers per sphere lookup.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace ps {
@@ -352,6 +354,85 @@ __global__ void __launch_bounds__(256) esdf_boxes_kernel(const float* __restrict
 }
 
 // ---------------------------------------------------------------------------
+// ESDF build with exact box culling: one warp per (x, y) column, lanes along z.
+// For a column, lb_b = sqrt(ax^2 + ay^2) (same fp32 ops as the full SDF, without the z
+// term) is a lower bound of box b's distance at every node of the column (monotone
+// rounding), and equals the distance whenever it is > 0.  Boxes are visited in
+// ascending lb order and the scan stops once lb > 0 && lb >= best, which cannot change
+// the minimum: results are bit-identical to the all-boxes loop (fminf is order-free).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) esdf_cull_kernel(const float* __restrict__ boxes, int n_boxes, int nx, int ny,
+                                                        int nz, float ox, float oy, float oz, float h, float cap,
+                                                        float* __restrict__ out) {
+    __shared__ float bc[32][3], bh[32][3];
+    __shared__ float s_lb[8][32];
+    __shared__ int s_id[8][32];
+    const int p = blockIdx.y;
+    const float* bx = boxes + (size_t)p * n_boxes * 6;
+    for (int i = threadIdx.x; i < n_boxes * 3; i += blockDim.x) {
+        const int b = i / 3, a = i % 3;
+        const float lo = bx[b * 6 + a], hi = bx[b * 6 + 3 + a];
+        bc[b][a] = 0.5f * (lo + hi);
+        bh[b][a] = 0.5f * (hi - lo);
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long n_nodes = (long long)nx * ny * nz;
+    const int n_col = nx * ny;
+    for (int col = blockIdx.x * 8 + warp; col < n_col; col += gridDim.x * 8) {
+        const int i = col / ny, j = col % ny;
+        const float px = fmaf((float)i, h, ox), py = fmaf((float)j, h, oy);
+        float lb = __int_as_float(0x7f800000);
+        int id = lane;
+        if (lane < n_boxes) {
+            const float qx = fabsf(px - bc[lane][0]) - bh[lane][0];
+            const float qy = fabsf(py - bc[lane][1]) - bh[lane][1];
+            const float ax = fmaxf(qx, 0.f), ay = fmaxf(qy, 0.f);
+            lb = sqrtf(fmaf(ax, ax, ay * ay));
+        }
+        // bitonic sort of (lb, id) across the warp, ascending
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+            for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                const float olb = __shfl_xor_sync(PS_FULL, lb, jj);
+                const int oid = __shfl_xor_sync(PS_FULL, id, jj);
+                const bool up = ((lane & k) == 0);
+                const bool lower = (lane & jj) == 0;
+                const bool o_less = (olb < lb) || (olb == lb && oid < id);
+                const bool take = lower ? (up ? o_less : !o_less) : (up ? !o_less : o_less);
+                if (take) {
+                    lb = olb;
+                    id = oid;
+                }
+            }
+        }
+        s_lb[warp][lane] = lb;
+        s_id[warp][lane] = id;
+        __syncwarp();
+        float* o = out + (size_t)p * (size_t)n_nodes + (size_t)col * nz;
+        for (int k = lane; k < nz; k += 32) {
+            const float pz = fmaf((float)k, h, oz);
+            float best = cap;
+            for (int e = 0; e < n_boxes; ++e) {
+                const float l = s_lb[warp][e];
+                if (l > 0.f && l >= best) break;
+                const int b = s_id[warp][e];
+                const float qx = fabsf(px - bc[b][0]) - bh[b][0];
+                const float qy = fabsf(py - bc[b][1]) - bh[b][1];
+                const float qz = fabsf(pz - bc[b][2]) - bh[b][2];
+                const float ax = fmaxf(qx, 0.f), ay = fmaxf(qy, 0.f), az = fmaxf(qz, 0.f);
+                const float outside = sqrtf(fmaf(ax, ax, fmaf(ay, ay, az * az)));
+                const float inside = fminf(fmaxf(qx, fmaxf(qy, qz)), 0.f);
+                best = fminf(best, outside + inside);
+            }
+            o[k] = best;
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // select_best: one warp per problem; lexicographic (infeasible, cost, index) min.
 // ---------------------------------------------------------------------------
 __global__ void select_kernel(const float* __restrict__ cost, const uint8_t* __restrict__ feas, int P,
@@ -463,7 +544,12 @@ extern "C" int ps_esdf_build_boxes(const float* boxes, int P, int n_boxes, const
     const long long n_nodes = (long long)n_h[0] * n_h[1] * n_h[2];
     const int threads = 256;
     cudaStream_t st = (cudaStream_t)stream;
-    if (n_h[2] % 4 == 0) {
+    if (n_boxes <= 32) {
+        const int n_col = n_h[0] * n_h[1];
+        const int blocks = std::min((n_col + 7) / 8, 4096);
+        esdf_cull_kernel<<<dim3((unsigned)blocks, P), 256, 0, st>>>(
+            boxes, n_boxes, n_h[0], n_h[1], n_h[2], origin_h[0], origin_h[1], origin_h[2], h, cap, out);
+    } else if (n_h[2] % 4 == 0) {
         const long long blocks = (n_nodes / 4 + threads - 1) / threads;
         esdf_boxes_kernel<4><<<dim3((unsigned)blocks, P), threads, 0, st>>>(
             boxes, n_boxes, n_h[0], n_h[1], n_h[2], origin_h[0], origin_h[1], origin_h[2], h, cap, out);

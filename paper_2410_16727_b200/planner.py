@@ -67,9 +67,11 @@ class BLPlanner:
         self.timing = {}
 
     # ------------------------------------------------------------------ device
-    def plan_batch_device(self, images, q_start, goal, boxes, p0: int = 0, events=None):
+    def plan_batch_device(self, images, q_start, goal, boxes, p0: int = 0, events=None, images_ready=None):
         """All inputs already on the device.  Returns PlanBatchResult of device tensors.
-        `events` (optional dict) receives CUDA events bracketing the sampler."""
+        `events` (optional dict) receives CUDA events bracketing the sampler;
+        `images_ready` (optional CUDA event) is waited on before the encoder, so an image
+        upload on another stream overlaps the ESDF build."""
         torch = _lib.require_cuda()
         P = int(q_start.shape[0])
         if P > self.Pmax:
@@ -77,6 +79,8 @@ class BLPlanner:
         B = P * self.S
         esdf = self.esdf[:P]
         self._esdf_build(boxes, esdf)
+        if images_ready is not None:
+            torch.cuda.current_stream().wait_event(images_ready)
         cond = self.sampler.encode(images, q_start, goal)
         fa = self.sampler.film(cond)
         if events is not None:
@@ -101,19 +105,28 @@ class BLPlanner:
     # ------------------------------------------------------------------ host
     def plan_batch(self, images, q_start, goal, boxes, p0: int = 0):
         """End-to-end call from host (ideally pinned) arrays: H2D copies, the device
-        pipeline, and a D2H read of trajectories, costs, flags and best indices."""
+        pipeline, and a D2H read of trajectories, costs, flags and best indices.  The
+        image upload runs on a side stream, overlapped with the ESDF build."""
         torch = _lib.require_cuda()
         P = int(q_start.shape[0])
         d_im, d_q, d_g, d_b = (self.d_images[:P], self.d_q[:P], self.d_goal[:P], self.d_boxes[:P])
-        for dst, src in ((d_im, images), (d_q, q_start), (d_g, goal), (d_b, boxes)):
+        main = torch.cuda.current_stream()
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream()
+            self._img_ev = torch.cuda.Event()
+        for dst, src in ((d_q, q_start), (d_g, goal), (d_b, boxes)):
             dst.copy_(torch.as_tensor(src), non_blocking=True)
-        r = self.plan_batch_device(d_im, d_q, d_g, d_b, p0=p0)
+        self._copy_stream.wait_stream(main)          # buffers free from the previous call
+        with torch.cuda.stream(self._copy_stream):
+            d_im.copy_(torch.as_tensor(images), non_blocking=True)
+            self._img_ev.record()
+        r = self.plan_batch_device(d_im, d_q, d_g, d_b, p0=p0, images_ready=self._img_ev)
         host = PlanBatchResult(r.trajectories.to("cpu", non_blocking=True), None,
                                r.cost.to("cpu", non_blocking=True),
                                r.feasible.to("cpu", non_blocking=True),
                                r.clamped.to("cpu", non_blocking=True),
                                r.best_index.to("cpu", non_blocking=True))
-        torch.cuda.current_stream().synchronize()
+        main.synchronize()
         return host
 
     @staticmethod
