@@ -628,6 +628,9 @@ struct UtTap {
     int8_t first;   // first MMA into its accumulator
 };
 
+constexpr int UT_EPI_WG = 2;                       // U-Net epilogue warpgroups
+constexpr int UT_THREADS = 64 + 128 * UT_EPI_WG;
+
 struct UtArgs {
     CUtensorMap tmA[3];
     CUtensorMap tmW;
@@ -673,7 +676,7 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_rows(const void* slot, int r
 
 // MB = M-blocks (128 rows) per tile: every weight stage feeds MB x 4 MMAs.
 template <int N, int EPI, bool RES, int MB>
-__global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_constant__ UtArgs a) {
+__global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_constant__ UtArgs a) {
     constexpr int B_BYTES = N * 128;
     constexpr int ACC1 = acc_cols<N, RES>();          // columns of one M-block
     constexpr int ACC = MB * ACC1;                     // columns of one tile
@@ -682,7 +685,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
     constexpr int CG = N / 8;
     // both warpgroups drain every tile (each half of the GroupNorm groups); FINAL needs all
     // 64 channels per row for the 64->7 projection, so its warpgroups alternate tiles
-    constexpr int NSPLIT = EPI == EPI_FINAL ? 1 : 2;
+    constexpr int NSPLIT = EPI == EPI_FINAL ? 1 : UT_EPI_WG;
     constexpr int NC = N / NSPLIT;
     constexpr int NG = 8 / NSPLIT;
     extern __shared__ __align__(1024) uint8_t smem_dyn[];
@@ -705,9 +708,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
     float* s_beta = s_gamma + N;
     float* s_rbias = s_beta + N;
     float* s_wout = s_rbias + N;                 // [7][64]
-    float* s_red = s_wout + 7 * 64;              // [WG][4 quadrants][32 samples][16]
-    float* s_film = s_red + TC_EPI_WG * 4 * 32 * 16;  // [WG][TC_FILM_P][2N]
-    UtGroup* s_grp = reinterpret_cast<UtGroup*>(s_film + TC_EPI_WG * TC_FILM_P * 2 * N);
+    float* s_red = s_wout + 7 * 64;              // [WG][4 quadrants][32 samples][2*NG]
+    float* s_film = s_red + UT_EPI_WG * 4 * 32 * 2 * NG;  // [WG][TC_FILM_P][2*NC]
+    UtGroup* s_grp = reinterpret_cast<UtGroup*>(s_film + UT_EPI_WG * TC_FILM_P * 2 * NC);
     UtTap* s_tap = reinterpret_cast<UtTap*>(s_grp + UT_MAXG);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -725,7 +728,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 128 * NSPLIT);
+            mbar_init(&tempty[b], 128 * NSPLIT);   // FINAL: one warpgroup per tile
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmA[0]) : "memory");
@@ -737,7 +740,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (warp >= 2) {
-        for (int i = threadIdx.x - 64; i < N; i += 128 * TC_EPI_WG) {
+        for (int i = threadIdx.x - 64; i < N; i += 128 * UT_EPI_WG) {
             s_bias[i] = a.bias[i];
             if (EPI != EPI_PLAIN) {
                 s_gamma[i] = a.gamma[i];
@@ -746,9 +749,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
             if (RES) s_rbias[i] = a.rbias[i];
         }
         if (EPI == EPI_FINAL)
-            for (int i = threadIdx.x - 64; i < U_DOF * 64; i += 128 * TC_EPI_WG) s_wout[i] = a.wout[i];
-        for (int i = threadIdx.x - 64; i < a.n_grp; i += 128 * TC_EPI_WG) s_grp[i] = a.grp[i];
-        for (int i = threadIdx.x - 64; i < a.n_tap; i += 128 * TC_EPI_WG) s_tap[i] = a.tap[i];
+            for (int i = threadIdx.x - 64; i < U_DOF * 64; i += 128 * UT_EPI_WG) s_wout[i] = a.wout[i];
+        for (int i = threadIdx.x - 64; i < a.n_grp; i += 128 * UT_EPI_WG) s_grp[i] = a.grp[i];
+        for (int i = threadIdx.x - 64; i < a.n_tap; i += 128 * UT_EPI_WG) s_tap[i] = a.tap[i];
     }
     tc_fence_before();
     __syncthreads();
@@ -840,11 +843,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
         const int t0 = r / nb, sl = r % nb;  // tile row = (time, sample); M-block mb adds 128/nb steps
         const int tstep = 128 / nb;
         const float inv_n = 1.0f / (float)(Tv * CG);
-        float* red = s_red + wg * (4 * 32 * 16);
-        const int cbase = NSPLIT == 2 ? wg * NC : 0;
-        const int j0 = NSPLIT == 2 ? 0 : wg;
-        const int jstep = NSPLIT == 2 ? 1 : TC_EPI_WG;
-        for (int j = j0; j < my_tiles; j += jstep) {
+        float* red = s_red + wg * (4 * 32 * 2 * NG);
+        const int cbase = NSPLIT > 1 ? wg * NC : 0;   // first column of this warpgroup
+        // NSPLIT > 1: every warpgroup drains every tile; FINAL (NSPLIT 1): warpgroups 0/1
+        // alternate tiles (one per TMEM buffer -- a third waiter would alias barrier phases)
+        const int j0 = NSPLIT > 1 ? 0 : wg;
+        const int jstep = NSPLIT > 1 ? 1 : 2;
+        for (int j = (NSPLIT == 1 && wg >= 2) ? my_tiles : j0; j < my_tiles; j += jstep) {
             const int tile = blockIdx.x + j * gridDim.x;
             const int buf = j % NBUF;
             const int b = tile * nb + sl;
@@ -859,15 +864,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
                 for (int mb = 0; mb < MB; ++mb) {
                     const int grow = b * Tv + t0 + mb * tstep;
                     const uint32_t t_lane = t_lane0 + (uint32_t)(mb * ACC1);
+                    constexpr int PC = NC < 32 ? NC : 32;
 #pragma unroll 1
-                    for (int cc = 0; cc < NC; cc += 32) {
-                        float v[32];
-                        tmem_ld32(t_lane + cc, v);
+                    for (int cc = 0; cc < NC; cc += PC) {
+                        float v[PC];
+                        if constexpr (PC == 32) {
+                            tmem_ld32(t_lane + cc, v);
+                        } else {
+                            uint32_t rr[16];
+                            tmem_ld16(t_lane + cc, rr);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj) v[jj] = __uint_as_float(rr[jj]);
+                        }
                         if (valid) {
                             const int c0 = cbase + cc;
                             __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
 #pragma unroll
-                            for (int jj = 0; jj < 32; jj += 8) {
+                            for (int jj = 0; jj < PC; jj += 8) {
                                 __align__(16) __nv_bfloat162 pk[4];
 #pragma unroll
                                 for (int u = 0; u < 4; ++u)
@@ -883,14 +897,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
                 float s1[NG], s2[NG], mean[NG], rstd[NG];
 #pragma unroll
                 for (int g = 0; g < NG; ++g) s1[g] = s2[g] = 0.f;
+                constexpr int SC = NC < 32 ? NC : 32;   // stats chunk width
 #pragma unroll
                 for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
-                    for (int cc = 0; cc < NC; cc += 32) {
-                        float v[32];
-                        tmem_ld32(t_lane0 + (uint32_t)(mb * ACC1) + cc, v);
+                    for (int cc = 0; cc < NC; cc += SC) {
+                        float v[SC];
+                        if constexpr (SC == 32) {
+                            tmem_ld32(t_lane0 + (uint32_t)(mb * ACC1) + cc, v);
+                        } else {
+                            uint32_t rr[16];
+                            tmem_ld16(t_lane0 + (uint32_t)(mb * ACC1) + cc, rr);
+                            tmem_wait_ld();
 #pragma unroll
-                        for (int jj = 0; jj < 32; ++jj) {
+                            for (int jj = 0; jj < 16; ++jj) v[jj] = __uint_as_float(rr[jj]);
+                        }
+#pragma unroll
+                        for (int jj = 0; jj < SC; ++jj) {
                             const float xv = v[jj] + s_bias[cbase + cc + jj];
                             s1[(cc + jj) / CG] += xv;
                             s2[(cc + jj) / CG] = fmaf(xv, xv, s2[(cc + jj) / CG]);
@@ -908,8 +931,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
                 if (lane < nb)
 #pragma unroll
                     for (int g = 0; g < NG; ++g) {
-                        red[(q * 32 + sl) * 16 + g] = s1[g];
-                        red[(q * 32 + sl) * 16 + 8 + g] = s2[g];
+                        red[(q * 32 + sl) * 2 * NG + g] = s1[g];
+                        red[(q * 32 + sl) * 2 * NG + NG + g] = s2[g];
                     }
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
 #pragma unroll
@@ -917,8 +940,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
                     float a1 = 0.f, a2 = 0.f;
 #pragma unroll
                     for (int qq = 0; qq < 4; ++qq) {
-                        a1 += red[(qq * 32 + sl) * 16 + g];
-                        a2 += red[(qq * 32 + sl) * 16 + 8 + g];
+                        a1 += red[(qq * 32 + sl) * 2 * NG + g];
+                        a2 += red[(qq * 32 + sl) * 2 * NG + NG + g];
                     }
                     mean[g] = a1 * inv_n;
                     rstd[g] = rsqrtf(fmaxf(fmaf(a2, inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
@@ -982,7 +1005,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) unet_tc_kernel(const __grid_con
                     if constexpr (EPI == EPI_GN_FILM) {
                         const int b_last = min(tile * nb + nb - 1, a.B - 1);
                         const int p_lo = (tile * nb) / a.S, p_hi = b_last / a.S;
-                        float* sf = s_film + wg * (TC_FILM_P * 2 * N);
+                        float* sf = s_film + wg * (TC_FILM_P * 2 * NC);
                         if (p_hi - p_lo < TC_FILM_P) {
                             const int n = (p_hi - p_lo + 1) * 2 * NC;
                             for (int i = r; i < n; i += 128) {
@@ -1110,7 +1133,11 @@ template <int N, int EPI, bool RES, int MB>
 static int launch_ut(UtArgs& a, cudaStream_t st) {
     const int A_BYTES = (a.Tv + 4) * a.nb * 128;
     constexpr int B_BYTES = N * 128;
-    const size_t vec = (size_t)(4 * N + 7 * 64 + TC_EPI_WG * 4 * 32 * 16 + TC_EPI_WG * TC_FILM_P * 2 * N) * 4 +
+    // the kernel's shared layout (unet_tc_kernel): per-channel vectors, w_out, GN partials,
+    // staged FiLM, tap tables
+    constexpr int NSPLIT_ = EPI == EPI_FINAL ? 1 : UT_EPI_WG;
+    constexpr int NG_ = 8 / NSPLIT_, NC_ = N / NSPLIT_;
+    const size_t vec = (size_t)(4 * N + 7 * 64 + UT_EPI_WG * 4 * 32 * 2 * NG_ + UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
                        UT_MAXG * sizeof(UtGroup) + UT_MAXTAP * sizeof(UtTap) + 64;
     const size_t budget = 225 * 1024 - vec - 2048;
     a.sa_stages = 3 * (size_t)A_BYTES <= 110 * 1024 ? 3 : 2;
@@ -1138,7 +1165,7 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     static const bool trace = std::getenv("PS_DEBUG") && std::atoi(std::getenv("PS_DEBUG")) >= 2;
     if (trace) std::fprintf(stderr, "[ps_b200] unet_tc N=%d EPI=%d RES=%d MB=%d B=%d Tv=%d nb=%d grid=%d groups=%d taps=%d\n",
                             N, EPI, (int)RES, MB, a.B, a.Tv, a.nb, grid, a.n_grp, a.n_tap);
-    kern<<<grid, TC_THREADS, smem, st>>>(a);
+    kern<<<grid, UT_THREADS, smem, st>>>(a);
     PS_CHECK_LAUNCH();
     if (trace && cudaStreamSynchronize(st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
     return PS_OK;
