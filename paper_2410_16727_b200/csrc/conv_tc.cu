@@ -504,13 +504,15 @@ __global__ void gather_f32_kernel(const float* __restrict__ blob, const long lon
     if (i < n) dst[i] = src[i] >= 0 ? blob[src[i]] : 0.f;
 }
 
-// im2col of the fp32 state for the first layer: A0[row][tap*7 + d] = x[b, t+tap-2, d]
+// im2col of the fp32 state for the first layer: A0[row][tap*7 + d] = x[b, t+tap-2, d].
+// Thread i writes the i-th 16-B chunk of A0 (8 chunks per 128-B row), so a warp stores
+// 512 contiguous bytes; x reads hit L1 (each row's 35 inputs are reused by 5 rows).
 __global__ void im2col_kernel(const float* __restrict__ x, int B, int T, __nv_bfloat16* __restrict__ a0) {
-    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // one (row, 8-col chunk) per thread
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const size_t rows = (size_t)B * T;
     if (i >= rows * 8) return;
-    const size_t row = i / 8;
-    const int ch = (int)(i % 8);
+    const size_t row = i >> 3;
+    const int ch = (int)(i & 7);
     const int b = (int)(row / T), t = (int)(row % T);
     __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
@@ -518,13 +520,13 @@ __global__ void im2col_kernel(const float* __restrict__ x, int B, int T, __nv_bf
         const int col = ch * 8 + u;
         float f = 0.f;
         if (col < 5 * U_DOF) {
-            const int tap = col / U_DOF, d = col % U_DOF;
+            const int tap = col / U_DOF, d = col - tap * U_DOF;
             const int tt = t + tap - 2;
-            if (tt >= 0 && tt < T) f = x[((size_t)b * T + tt) * U_DOF + d];
+            if (tt >= 0 && tt < T) f = __ldg(x + ((size_t)b * T + tt) * U_DOF + d);
         }
         v[u] = __float2bfloat16_rn(f);
     }
-    *reinterpret_cast<uint4*>(a0 + row * 64 + ch * 8) = *reinterpret_cast<uint4*>(v);
+    reinterpret_cast<uint4*>(a0)[i] = *reinterpret_cast<uint4*>(v);
 }
 
 __global__ void film_step_kernel(const float* __restrict__ fa, const float* __restrict__ fb, int P,
@@ -953,33 +955,52 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     const int t = t0;
                     const int grow = b * Tv + t;
                     const uint32_t t_lane = t_lane0;
-                    float y[64];
+                    // 64 -> 7 projection accumulated chunk by chunk (no y[64] live range)
+                    float eps[U_DOF];
 #pragma unroll
-                    for (int c0 = 0; c0 < 64; c0 += 32) {
-                        float v[32];
-                        tmem_ld32(t_lane + c0, v);
+                    for (int d = 0; d < U_DOF; ++d) eps[d] = a.bout[d];
 #pragma unroll
-                        for (int jj = 0; jj < 32; ++jj) {
+                    for (int c0 = 0; c0 < 64; c0 += 16) {
+                        uint32_t rr[16];
+                        tmem_ld16(t_lane + c0, rr);
+                        tmem_wait_ld();
+                        float y[16];
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) {
                             const int c = c0 + jj;
-                            const float tt = (v[jj] + s_bias[c] - mean[c / CG]) * rstd[c / CG];
-                            y[c] = mish_fast(fmaf(tt, s_gamma[c], s_beta[c]));
+                            const float xv = __uint_as_float(rr[jj]) + s_bias[c];
+                            const float tt = fmaf(xv, rstd[c / CG], -mean[c / CG] * rstd[c / CG]);
+                            y[jj] = mish8(fmaf(tt, s_gamma[c], s_beta[c]));
                         }
+#pragma unroll
+                        for (int d = 0; d < U_DOF; ++d)
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj) eps[d] = fmaf(y[jj], s_wout[d * 64 + c0 + jj], eps[d]);
                     }
                     if (valid) {
-                        float eps[U_DOF];
-#pragma unroll
-                        for (int d = 0; d < U_DOF; ++d) {
-                            float acc = a.bout[d];
-#pragma unroll
-                            for (int c = 0; c < 64; ++c) acc = fmaf(y[c], s_wout[d * 64 + c], acc);
-                            eps[d] = acc;
-                        }
                         float* xr = a.x + (size_t)grow * U_DOF;
                         if (a.eps_out) {
 #pragma unroll
                             for (int d = 0; d < U_DOF; ++d) a.eps_out[(size_t)grow * U_DOF + d] = eps[d];
                         } else {
                             const StepCoef sc = a.sc;
+                            // noise: one Philox call per block of 4 consecutive elements of the row
+                            float z[U_DOF];
+                            if (!sc.last && sc.ddpm) {
+                                const uint32_t e0 = (uint32_t)(t * U_DOF);
+#pragma unroll
+                                for (int d = 0; d < U_DOF; ++d) z[d] = 0.f;
+                                const uint32_t blk_lo = e0 >> 2, blk_hi = (e0 + U_DOF - 1) >> 2;
+                                for (uint32_t blk = blk_lo; blk <= blk_hi; ++blk) {
+                                    float n4[4];
+                                    normal4_tc((uint32_t)sc.k, (uint32_t)(a.p0 + p), (uint32_t)(b % a.S), blk, a.key, n4);
+#pragma unroll
+                                    for (int u = 0; u < 4; ++u) {
+                                        const int d = (int)(blk * 4 + u) - (int)e0;
+                                        if (d >= 0 && d < U_DOF) z[d] = n4[u];
+                                    }
+                                }
+                            }
 #pragma unroll
                             for (int d = 0; d < U_DOF; ++d) {
                                 const float xv = xr[d];
@@ -989,9 +1010,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                                     a.traj[(size_t)grow * U_DOF + d] =
                                         (t == 0) ? a.q_start[(size_t)p * U_DOF + d] : a.lo + x0 * (a.hi - a.lo);
                                 } else if (sc.ddpm) {
-                                    const float z = normal_tc((uint32_t)sc.k, (uint32_t)(a.p0 + p),
-                                                              (uint32_t)(b % a.S), (uint32_t)(t * U_DOF + d), a.key);
-                                    xr[d] = sc.c0 * x0 + sc.c1 * xv + sc.sig * z;
+                                    xr[d] = sc.c0 * x0 + sc.c1 * xv + sc.sig * z[d];
                                 } else {
                                     xr[d] = sc.sqn * x0 + sc.sq1mn * eps[d];
                                 }
