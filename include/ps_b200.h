@@ -159,6 +159,25 @@ int ps_ref_div(const double* x, int n, double d, double* y, void* stream);
 /* DDIM step (src/diffusion.py:547-555) and denormalise + row-0 pin (:559-569) */
 int ps_ref_ddim_update(double* x, const double* eps, int n, double ab, double ab_next, int has_next,
                        double clip_lo, double clip_hi, double* x0_out, void* stream);
+/* DDIM step after guidance: x = sqrt(ab_next) x0 + sqrt(1 - ab_next) eps (src/diffusion.py:553-555) */
+int ps_ref_ddim_next(double* x, const double* x0, const double* eps, int n, double ab_next, void* stream);
+/* guided_ddim_sample's guide() for the planner cost (src/diffusion.py:598-617 with
+ * evaluate_cost_batch, src/trajopt.py:105-119): n_grad descent steps with <= max_halvings
+ * halvings on x0_hat (S,T,D), in place; one cooperative launch.  flags: 2*S ints of
+ * workspace; err: 2+S ints, err[0]=1 if an evaluation left the ESDF (the reference raises
+ * ValueError there), err[2+s] = seed s out of grid in that evaluation. */
+int ps_ref_guide(int dtype, void* x, int S, int T, int D, PS_REF_ARM_ARGS, const void* arm_lo,
+                 const void* arm_span, const void* net_span, int n_grad, double alpha_guide, int max_halvings,
+                 int* flags, int* err, void* stream);
+/* trajopt.metrics + retime (src/trajopt.py:209-272) with traj_min_clearance against the
+ * ground-truth analytic world (src/_kernels.py:60-162), one row per trajectory:
+ * out (S,6) = [min clearance, translation error, angle error (deg), motion time, max jerk, dt].
+ * circles (nc,3), boxes (nb,4), jerk_mat (T,T), vel/acc/jerk (D) are device pointers. */
+int ps_ref_metrics(const double* trajs, int S, int T, int D, const double* lengths_h, double basex, double basey,
+                   const double* fracs_h, int M, const double* circles, int nc, const double* boxes, int nb,
+                   double cap, double goal_x, double goal_y, double goal_th, const double* jerk_mat,
+                   const double* vel, const double* acc, const double* jerk, int interp, double* out,
+                   void* stream);
 int ps_ref_denorm_pin(const double* x0, int B, int T, int D, const double* lo, const double* hi,
                       const double* q0, double* traj, void* stream);
 

@@ -61,6 +61,11 @@ _SIGS = {
     "ps_ref_sinusoid": [_c_d, _c_int, _vp, _vp],
     "ps_ref_div": [_vp, _c_int, _c_d, _vp, _vp],
     "ps_ref_ddim_update": [_vp, _vp, _c_int, _c_d, _c_d, _c_int, _c_d, _c_d, _vp, _vp],
+    "ps_ref_ddim_next": [_vp, _vp, _vp, _c_int, _c_d, _vp],
+    "ps_ref_guide": [_c_int, _vp, _c_int, _c_int, _c_int] + _REF_ARM + [_vp, _vp, _vp, _c_int, _c_d, _c_int, _vp,
+                                                                     _vp, _vp],
+    "ps_ref_metrics": [_vp, _c_int, _c_int, _c_int, _vp, _c_d, _c_d, _vp, _c_int, _vp, _c_int, _vp, _c_int, _c_d,
+                       _c_d, _c_d, _c_d, _vp, _vp, _vp, _vp, _c_int, _vp, _vp],
     "ps_ref_denorm_pin": [_vp, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp],
     "ps_encoder_packed_bytes": [_c_int, _c_int, _c_int],
     "ps_encoder_pack": [_vp, _c_int, _c_int, _c_int, _vp, _vp],

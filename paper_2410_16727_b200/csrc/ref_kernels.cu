@@ -10,6 +10,8 @@
 // src/pipeline.py:101-157 (planner ESDF, planner_success).
 #include <cuda_bf16.h>
 
+#include <cooperative_groups.h>
+
 #include <cmath>
 
 #include "common.cuh"
@@ -385,6 +387,249 @@ __global__ void __launch_bounds__(32) optimize_kernel(const __grid_constant__ Ar
 }
 
 // ---------------------------------------------------------------------------
+// Cost guidance of one DDIM sub-step (guided_ddim_sample's `guide`, src/diffusion.py:598-617),
+// fused for the planner cost (evaluate_cost_batch, src/trajopt.py:105-119).  One warp per
+// seed, all seeds in one cooperative grid: the reference evaluates the whole batch at every
+// halving while ANY seed still backtracks (phantom candidates of finished seeds included),
+// and raises at the first evaluation that leaves the ESDF, so each evaluation ends in a grid
+// barrier that exchanges {clamped, remaining} over all seeds.
+//   x (S,T,D) normalised x0_hat, updated in place; q = arm_lo + x * arm_span (arm.denormalize);
+//   g_norm = grad * net_span; cand = x - step * g_norm.
+//   flags: 2*S ints (double-buffered exchange); err: 2 + S ints
+//   (err[0] = 1 if an evaluation was clamped, err[1] = its index, err[2+s] = seed s clamped).
+// ---------------------------------------------------------------------------
+template <typename F>
+__global__ void __launch_bounds__(32) guide_kernel(const __grid_constant__ ArmGrid<F> A, F* __restrict__ x, int S,
+                                                   int T, const F* __restrict__ arm_lo,
+                                                   const F* __restrict__ arm_span, const F* __restrict__ net_span,
+                                                   int n_grad, F alpha_guide, int max_halvings,
+                                                   int* __restrict__ flags, int* __restrict__ err) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) uint8_t smraw[];
+    SeedSmem<F>& sm = *reinterpret_cast<SeedSmem<F>*>(smraw);
+    const int s = blockIdx.x, lane = threadIdx.x;
+    const int D = A.D, n = T * D;
+    F* xs = sm.q;      // x (normalised)
+    F* gn = sm.v;      // g_norm
+    F* cx = sm.cand;   // candidate (normalised)
+    F* qd = sm.g;      // denormalised evaluation point; later the cost gradient
+    __shared__ F grad_buf[MAXT * MAXD];
+    for (int i = lane; i < n; i += 32) xs[i] = x[(size_t)s * n + i];
+    if (s == 0 && lane == 0) err[0] = 0;
+    __syncwarp();
+    int n_eval = 0;
+    // exchange: publish (remaining | clamped<<1), barrier, OR over all seeds
+    auto exchange = [&](bool remaining, bool clamped, bool& any_rem, bool& any_cl) {
+        int* buf = flags + (n_eval & 1) * S;
+        if (lane == 0) buf[s] = (remaining ? 1 : 0) | (clamped ? 2 : 0);
+        __threadfence();
+        grid.sync();
+        int acc = 0;
+        for (int j = lane; j < S; j += 32) acc |= __ldcg(buf + j);
+        for (int off = 16; off; off >>= 1) acc |= __shfl_xor_sync(PS_FULL, acc, off);
+        any_rem = (acc & 1) != 0;
+        any_cl = (acc & 2) != 0;
+        if (any_cl && s == 0) {
+            for (int j = lane; j < S; j += 32) err[2 + j] = (__ldcg(buf + j) & 2) ? 1 : 0;
+            if (lane == 0) {
+                err[1] = n_eval;
+                err[0] = 1;
+            }
+        }
+        ++n_eval;
+    };
+    for (int it = 0; it < n_grad; ++it) {
+        for (int i = lane; i < n; i += 32) qd[i] = arm_lo[i % D] + xs[i] * arm_span[i % D];
+        __syncwarp();
+        int cl;
+        const F cost = seed_cost(A, qd, T, true, sm.sc, grad_buf, sm.terms, cl);
+        __syncwarp();
+        bool any_rem, any_cl;
+        exchange(true, cl != 0, any_rem, any_cl);
+        if (any_cl) return;
+        for (int i = lane; i < n; i += 32) gn[i] = grad_buf[i] * net_span[i % D];
+        __syncwarp();
+        F step = alpha_guide;
+        bool remaining = true;
+        any_rem = true;
+        for (int h = 0; h < max_halvings; ++h) {
+            if (!any_rem) break;
+            for (int i = lane; i < n; i += 32) {
+                cx[i] = xs[i] - step * gn[i];
+                qd[i] = arm_lo[i % D] + cx[i] * arm_span[i % D];
+            }
+            __syncwarp();
+            int clc;
+            const F nc = seed_cost(A, qd, T, true, sm.sc, grad_buf, sm.terms, clc);
+            __syncwarp();
+            const bool improved = remaining && (nc < cost);
+            if (improved)
+                for (int i = lane; i < n; i += 32) xs[i] = cx[i];
+            remaining = remaining && !improved;
+            if (remaining) step = step * F(0.5);
+            __syncwarp();
+            exchange(remaining, clc != 0, any_rem, any_cl);
+            if (any_cl) return;
+        }
+    }
+    for (int i = lane; i < n; i += 32) x[(size_t)s * n + i] = xs[i];
+}
+
+// x = sqrt(ab_next) * x0 + sqrt(1 - ab_next) * eps (the DDIM step after guidance, src/diffusion.py:553-555)
+__global__ void ddim_next_kernel(double* __restrict__ x, const double* __restrict__ x0,
+                                 const double* __restrict__ eps, int n, double ab_next) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    x[i] = sqrt(ab_next) * x0[i] + sqrt(1.0 - ab_next) * eps[i];
+}
+
+// ---------------------------------------------------------------------------
+// Ground-truth trajectory metrics (trajopt.metrics / retime, src/trajopt.py:209-272;
+// _kernels.analytic_sdf / config_clearance / traj_min_clearance, src/_kernels.py:60-162).
+// One warp per trajectory: lanes stride over the T + (T-1)*interp configurations for the
+// analytic clearance (min is order-independent), then the end pose, the retime scale from
+// the numpy.gradient stencils (products by +-0.5/1 are exact, so v, a, j are bit-exact)
+// and max |J q| / dt^3.
+// ---------------------------------------------------------------------------
+struct GTWorld {
+    const double* circles;   // (nc, 3): cx, cy, r
+    const double* boxes;     // (nb, 4): lox, loy, hix, hiy
+    int nc, nb;
+    double cap;
+};
+
+__device__ double analytic_sdf(const GTWorld& W, double x, double y) {
+    double best = W.cap;
+    for (int k = 0; k < W.nc; ++k) {
+        const double dx = x - W.circles[3 * k], dy = y - W.circles[3 * k + 1];
+        const double d = sqrt(dx * dx + dy * dy) - W.circles[3 * k + 2];
+        if (d < best) best = d;
+    }
+    for (int k = 0; k < W.nb; ++k) {
+        const double* b = W.boxes + 4 * k;
+        const double cx = 0.5 * (b[0] + b[2]), cy = 0.5 * (b[1] + b[3]);
+        const double qx = fabs(x - cx) - 0.5 * (b[2] - b[0]);
+        const double qy = fabs(y - cy) - 0.5 * (b[3] - b[1]);
+        const double ax = qx > 0.0 ? qx : 0.0, ay = qy > 0.0 ? qy : 0.0;
+        double inside = qx > qy ? qx : qy;
+        if (inside > 0.0) inside = 0.0;
+        const double d = sqrt(ax * ax + ay * ay) + inside;
+        if (d < best) best = d;
+    }
+    return best;
+}
+
+__device__ double config_clearance(const ArmGrid<double>& A, const GTWorld& W, const double* q) {
+    double best = W.cap, th = 0.0, px = A.basex, py = A.basey;
+    for (int k = 0; k < A.D; ++k) {
+        th += q[k];
+        const double c = cos(th), s = sin(th);
+        for (int i = 0; i < A.M; ++i) {
+            const double x = px + A.fracs[i] * A.lengths[k] * c;
+            const double y = py + A.fracs[i] * A.lengths[k] * s;
+            const double v = analytic_sdf(W, x, y);
+            if (v < best) best = v;
+        }
+        px += A.lengths[k] * c;
+        py += A.lengths[k] * s;
+    }
+    return best;
+}
+
+__global__ void __launch_bounds__(32) metrics_kernel(const __grid_constant__ ArmGrid<double> A, const GTWorld W,
+                                                     const double* __restrict__ trajs, int S, int T, int interp,
+                                                     const double* __restrict__ vel, const double* __restrict__ acc,
+                                                     const double* __restrict__ jerk, double* __restrict__ out) {
+    __shared__ double q[MAXT * MAXD], v[MAXT * MAXD], a[MAXT * MAXD], j[MAXT * MAXD];
+    const int s = blockIdx.x, lane = threadIdx.x, D = A.D, n = T * D;
+    const double* tr = trajs + (size_t)s * n;
+    for (int i = lane; i < n; i += 32) q[i] = tr[i];
+    __syncwarp();
+    // clearance over waypoints + interpolants (traj_min_clearance)
+    const int per = interp + 1, n_cfg = (T - 1) * per + 1;
+    double best = W.cap;
+    for (int c = lane; c < n_cfg; c += 32) {
+        const int t = c / per, i = c % per;
+        double qc[MAXD];
+        if (i == 0) {
+            for (int k = 0; k < D; ++k) qc[k] = q[t * D + k];
+        } else {
+            const double f = (double)i / (double)per;
+            for (int k = 0; k < D; ++k) qc[k] = q[t * D + k] + f * (q[(t + 1) * D + k] - q[t * D + k]);
+        }
+        const double cv = config_clearance(A, W, qc);
+        if (cv < best) best = cv;
+    }
+    for (int off = 16; off; off >>= 1) best = fmin(best, __shfl_xor_sync(PS_FULL, best, off));
+    // numpy.gradient stencil applied three times (diff_matrix, src/trajopt.py:64-73)
+    auto grad1 = [&](const double* x, double* y) {
+        for (int idx = lane; idx < n; idx += 32) {
+            const int r = idx / D, k = idx % D;
+            double val;
+            if (r == 0) val = -1.0 * x[k] + 1.0 * x[D + k];
+            else if (r == T - 1) val = -1.0 * x[(T - 2) * D + k] + 1.0 * x[(T - 1) * D + k];
+            else val = -0.5 * x[(r - 1) * D + k] + 0.5 * x[(r + 1) * D + k];
+            y[idx] = val;
+        }
+        __syncwarp();
+    };
+    grad1(q, v);
+    grad1(v, a);
+    grad1(a, j);
+    // dt = max(max(vmax/vl), sqrt(max(amax/al)), cbrt(max(jmax/jl))) (retime, src/trajopt.py:209-229)
+    double rv = 0.0, ra = 0.0, rj = 0.0;
+    if (lane < D) {
+        double vm = 0.0, am = 0.0, jm = 0.0;
+        for (int r = 0; r < T; ++r) {
+            vm = fmax(vm, fabs(v[r * D + lane]));
+            am = fmax(am, fabs(a[r * D + lane]));
+            jm = fmax(jm, fabs(j[r * D + lane]));
+        }
+        rv = vm / vel[lane];
+        ra = am / acc[lane];
+        rj = jm / jerk[lane];
+    }
+    for (int off = 16; off; off >>= 1) {
+        rv = fmax(rv, __shfl_xor_sync(PS_FULL, rv, off));
+        ra = fmax(ra, __shfl_xor_sync(PS_FULL, ra, off));
+        rj = fmax(rj, __shfl_xor_sync(PS_FULL, rj, off));
+    }
+    const double dt = fmax(fmax(rv, sqrt(ra)), cbrt(rj));
+    const double motion_time = dt * (double)(T - 1);
+    // max |jerk_matrix @ traj| / dt^3 (dense J as the reference forms it)
+    double mj = 0.0;
+    for (int idx = lane; idx < n; idx += 32) {
+        const int r = idx / D, k = idx % D;
+        double y = 0.0;
+        for (int c = 0; c < T; ++c) y += A.jerk_mat[r * T + c] * q[c * D + k];
+        mj = fmax(mj, fabs(y));
+    }
+    for (int off = 16; off; off >>= 1) mj = fmax(mj, __shfl_xor_sync(PS_FULL, mj, off));
+    if (lane == 0) {
+        // end pose (fk_pose, src/arm.py:118-125) and its errors against the goal
+        double th = 0.0, ex = A.basex, ey = A.basey;
+        const double* qe = q + (T - 1) * D;
+        for (int k = 0; k < D; ++k) {
+            th += qe[k];
+            ex += A.lengths[k] * cos(th);
+            ey += A.lengths[k] * sin(th);
+        }
+        const double pi = 3.141592653589793238462643383279502884;
+        const double end_th = wrap(th);
+        const double terr = hypot(ex - A.goal_x, ey - A.goal_y);
+        const double aerr = fabs(wrap(end_th - A.goal_th)) * (180.0 / pi);
+        double* o = out + (size_t)s * 6;
+        o[0] = best;
+        o[1] = terr;
+        o[2] = aerr;
+        o[3] = motion_time;
+        o[4] = motion_time > 0.0 ? mj / (dt * dt * dt) : 0.0;
+        o[5] = dt;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // scan-derived planner ESDF (src/pipeline.py:101-132; geometry.py:130-152, :270-276)
 // ---------------------------------------------------------------------------
 __global__ void planner_esdf_kernel(const double* __restrict__ depths, int n_rays, double sx, double sy,
@@ -612,6 +857,82 @@ static int ref_opt(const void* seeds, int S, int T, int D, int n_iters, double m
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<S, 32, smem, st>>>(A, (const F*)seeds, S, T, n_iters, (F)momentum, (F)armijo_c, (F)shrink, max_bt, (F)alpha0,
                            (F)alpha_max, (F*)x_out, (F*)terms, (F*)totals, frozen, n_acc);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+template <typename F>
+static int ref_guide(void* x, int S, int T, int D, REF_ARM_ARGS, const double* arm_lo_d, const double* arm_span_d,
+                     const double* net_span_d, int n_grad, double alpha_guide, int max_halvings, int* flags, int* err,
+                     cudaStream_t st) {
+    ArmGrid<F> A;
+    int e = fill_arm(A, D, REF_ARM_PASS);
+    if (e) return e;
+    if (T < 2 || T > MAXT || S < 0 || n_grad < 0 || max_halvings < 0) return PS_FAIL(PS_ERR_SHAPE);
+    if (S == 0 || n_grad == 0) return PS_OK;
+    const size_t smem = sizeof(SeedSmem<F>);
+    auto k = guide_kernel<F>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0, dev = 0, n_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32, smem);
+    if ((long long)per_sm * n_sm < S) return PS_FAIL(PS_ERR_SHAPE);  // all seeds must be co-resident
+    F* xp = (F*)x;
+    const F* lo = (const F*)arm_lo_d;
+    const F* sp = (const F*)arm_span_d;
+    const F* ns = (const F*)net_span_d;
+    F ag = (F)alpha_guide;
+    void* args[] = {(void*)&A, (void*)&xp, (void*)&S, (void*)&T, (void*)&lo, (void*)&sp, (void*)&ns,
+                    (void*)&n_grad, (void*)&ag, (void*)&max_halvings, (void*)&flags, (void*)&err};
+    ps_launch_counter().fetch_add(1, std::memory_order_relaxed);
+    if (cudaLaunchCooperativeKernel((const void*)k, dim3(S), dim3(32), args, smem, st) != cudaSuccess)
+        return PS_FAIL(PS_ERR_CUDA);
+    return PS_OK;
+}
+
+extern "C" int ps_ref_guide(int dtype, void* x, int S, int T, int D, REF_ARM_ARGS, const void* arm_lo,
+                            const void* arm_span, const void* net_span, int n_grad, double alpha_guide,
+                            int max_halvings, int* flags, int* err, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == 0)
+        return ref_guide<double>(x, S, T, D, REF_ARM_PASS, (const double*)arm_lo, (const double*)arm_span,
+                                 (const double*)net_span, n_grad, alpha_guide, max_halvings, flags, err, st);
+    if (dtype == 1)
+        return ref_guide<float>(x, S, T, D, REF_ARM_PASS, (const double*)arm_lo, (const double*)arm_span,
+                                (const double*)net_span, n_grad, alpha_guide, max_halvings, flags, err, st);
+    return PS_FAIL(PS_ERR_SHAPE);
+}
+
+extern "C" int ps_ref_metrics(const double* trajs, int S, int T, int D, const double* lengths_h, double basex,
+                              double basey, const double* fracs_h, int M, const double* circles, int nc,
+                              const double* boxes, int nb, double cap, double goal_x, double goal_y, double goal_th,
+                              const double* jerk_mat, const double* vel, const double* acc, const double* jerk,
+                              int interp, double* out, void* stream) {
+    if (D < 1 || D > MAXD || M < 1 || M > MAXM || T < 2 || T > MAXT || S < 0 || interp < 0 || nc < 0 || nb < 0)
+        return PS_FAIL(PS_ERR_SHAPE);
+    if (S == 0) return PS_OK;
+    ArmGrid<double> A{};
+    A.D = D;
+    A.M = M;
+    for (int k = 0; k < D; ++k) A.lengths[k] = lengths_h[k];
+    for (int i = 0; i < M; ++i) A.fracs[i] = fracs_h[i];
+    A.basex = basex;
+    A.basey = basey;
+    A.goal_x = goal_x;
+    A.goal_y = goal_y;
+    A.goal_th = goal_th;
+    A.jerk_mat = jerk_mat;
+    GTWorld W{circles, boxes, nc, nb, cap};
+    metrics_kernel<<<S, 32, 0, (cudaStream_t)stream>>>(A, W, trajs, S, T, interp, vel, acc, jerk, out);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+extern "C" int ps_ref_ddim_next(double* x, const double* x0, const double* eps, int n, double ab_next,
+                                void* stream) {
+    if (n <= 0) return PS_FAIL(PS_ERR_SHAPE);
+    ddim_next_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(x, x0, eps, n, ab_next);
     PS_CHECK_LAUNCH();
     return PS_OK;
 }

@@ -311,6 +311,135 @@ def ddim_sample(net, schedule, cond, x_K, q0, arm, n_steps: int = 5) -> np.ndarr
     return ddim_sample_device(net, schedule, cond, x_K, q0, arm, n_steps).cpu().numpy()
 
 
+class PlannerCost:
+    """The planner's guidance cost, `evaluate_cost_batch(arm, esdf, goal, trajs, w)` ->
+    (totals, grads) (src/pipeline.py:190-192).  Callable on host arrays exactly like the
+    reference's closure; `guided_ddim_sample` recognises it and runs the whole guidance
+    (n_grad descent steps x halvings over all seeds) as one fused GPU launch per sub-step."""
+
+    def __init__(self, arm, esdf, goal, w=None, dtype: str = "fp64"):
+        from .trajopt import CostWeights
+        self.arm, self.esdf, self.goal = arm, esdf, goal
+        self.w = w if w is not None else CostWeights()
+        self.dtype = dtype
+
+    def __call__(self, trajs):
+        from .trajopt import evaluate_cost_batch
+        totals, grads, _ = evaluate_cost_batch(self.arm, self.esdf, self.goal, trajs, self.w, dtype=self.dtype)
+        return totals, grads
+
+
+def _guide_device(cost: PlannerCost, arm, net, x0, n_grad, alpha_guide, max_halvings, ws):
+    """One fused `ps_ref_guide` launch on x0 (B,T,D) device f64, in place; raises the
+    reference's ValueError when an evaluation leaves the ESDF (src/trajopt.py:116-118)."""
+    torch = _lib.require_cuda()
+    from .trajopt import _DT, _ArmArgs
+    B, T, D = x0.shape
+    A = _ArmArgs(cost.arm, cost.esdf, cost.goal, cost.w, T, "fp64")
+    lo, hi = net.config.lo_hi()
+    arm_lo = ws["arm_lo"]
+    flags = torch.empty(2 * B, dtype=torch.int32, device="cuda")
+    err = torch.zeros(2 + B, dtype=torch.int32, device="cuda")
+    st = _lib.lib().ps_ref_guide(_DT["fp64"], _lib.ptr(x0), B, T, D, *A.args, _lib.ptr(arm_lo),
+                                 _lib.ptr(ws["arm_span"]), _lib.ptr(ws["net_span"]), int(n_grad),
+                                 float(alpha_guide), int(max_halvings), _lib.ptr(flags), _lib.ptr(err),
+                                 _lib.stream_handle())
+    _lib.check(st, "guide")
+    e = err.cpu().numpy()
+    if e[0]:
+        raise ValueError("trajectory collision points leave the ESDF extent "
+                         f"(seeds {np.nonzero(e[2:])[0].tolist()})")
+
+
+def _guide_host(cost_fn, arm, span, x0_hat, n_grad, alpha_guide, max_halvings):
+    """guide() of src/diffusion.py:598-617 for an arbitrary user cost_fn (a host callable):
+    the same loop, with the user's function evaluated on host arrays."""
+    from .types import denormalize
+    batched = x0_hat.ndim == 3
+    x = x0_hat if batched else x0_hat[None]
+    for _ in range(n_grad):
+        costs, grads = cost_fn(denormalize(arm, x))
+        g_norm = grads * span
+        step = np.full(x.shape[0], alpha_guide)
+        remaining = np.ones(x.shape[0], dtype=bool)
+        for _ in range(max_halvings):
+            if not remaining.any():
+                break
+            cand = x - step[:, None, None] * g_norm
+            new_costs, _ = cost_fn(denormalize(arm, cand))
+            improved = remaining & (new_costs < costs)
+            x = np.where(improved[:, None, None], cand, x)
+            remaining = remaining & ~improved
+            step = np.where(remaining, step * 0.5, step)
+    return x if batched else x[0]
+
+
+def guided_ddim_sample_device(net, schedule, cond, x_K, q0, arm, cost_fn, n_steps: int = 5,
+                              k_guide_frac: float = 0.6, n_grad: int = 20, alpha_guide: float = 1.0,
+                              max_halvings: int = 8):
+    """guided_ddim_sample (src/diffusion.py:572-628) -> (device traj, log)."""
+    torch = _lib.require_cuda()
+    L = _lib.lib()
+    ks = ddim_steps(schedule.K, n_steps)
+    xin = np.array(x_K, dtype=np.float64)
+    single = xin.ndim == 2
+    x = torch.as_tensor(xin[None] if single else xin, device="cuda").contiguous()
+    cd = torch.as_tensor(np.atleast_2d(np.asarray(cond, dtype=np.float64)), device="cuda")
+    lo, hi = net.config.lo_hi()
+    span = hi - lo
+    k_guide = k_guide_frac * schedule.K
+    fused = isinstance(cost_fn, PlannerCost)
+    ws = {"arm_lo": torch.as_tensor(np.asarray(arm.lo, dtype=np.float64), device="cuda"),
+          "arm_span": torch.as_tensor(np.asarray(arm.hi - arm.lo, dtype=np.float64), device="cuda"),
+          "net_span": torch.as_tensor(np.asarray(span, dtype=np.float64), device="cuda")}
+    log: List[Tuple[int, bool]] = []
+    x0 = torch.empty_like(x)
+    n = x.numel()
+    for i, k in enumerate(ks):
+        ab = float(schedule.alpha_bar(int(k)))
+        eps = predict_noise_device(net, x, int(k), cd)
+        has_next = i + 1 < len(ks)
+        ab_next = float(schedule.alpha_bar(int(ks[i + 1]))) if has_next else 1.0
+        guided = False
+        if has_next:
+            guided = bool(k < k_guide and alpha_guide != 0.0)
+            log.append((int(k), guided))
+        if not guided:
+            _lib.check(L.ps_ref_ddim_update(_lib.ptr(x), _lib.ptr(eps), n, ab, ab_next, int(has_next),
+                                            X0_CLIP[0], X0_CLIP[1], _lib.ptr(x0), _lib.stream_handle()),
+                       "ddim_update")
+            continue
+        _lib.check(L.ps_ref_ddim_update(_lib.ptr(x), _lib.ptr(eps), n, ab, ab_next, 0, X0_CLIP[0],
+                                        X0_CLIP[1], _lib.ptr(x0), _lib.stream_handle()), "ddim_update")
+        if fused:
+            _guide_device(cost_fn, arm, net, x0, n_grad, alpha_guide, max_halvings, ws)
+        else:
+            xh = _guide_host(cost_fn, arm, span, x0.cpu().numpy(), n_grad, alpha_guide, max_halvings)
+            x0.copy_(torch.as_tensor(np.ascontiguousarray(xh), device="cuda"))
+        _lib.check(L.ps_ref_ddim_next(_lib.ptr(x), _lib.ptr(x0), _lib.ptr(eps), n, ab_next,
+                                      _lib.stream_handle()), "ddim_next")
+    log.append((int(ks[-1]), False))
+    B, T, D = x0.shape
+    hi_t = torch.as_tensor(np.asarray(arm.hi, dtype=np.float64), device="cuda")
+    q = torch.as_tensor(np.asarray(q0, dtype=np.float64), device="cuda")
+    traj = torch.empty_like(x0)
+    _lib.check(L.ps_ref_denorm_pin(_lib.ptr(x0), B, T, D, _lib.ptr(ws["arm_lo"]), _lib.ptr(hi_t), _lib.ptr(q),
+                                   _lib.ptr(traj), _lib.stream_handle()), "denormalize")
+    return (traj[0] if single else traj), log
+
+
+def guided_ddim_sample(net, schedule, cond, x_K, q0, arm, cost_fn, n_steps: int = 5,
+                       k_guide_frac: float = 0.6, n_grad: int = 20, alpha_guide: float = 1.0,
+                       max_halvings: int = 8):
+    """src/diffusion.py:572-628: DDIM with cost-gradient descent on the intermediate x0_hat
+    for sub-steps with k < k_guide_frac*K (never the last).  Returns (trajectories, log).
+    With a `PlannerCost` the guidance is one fused GPU launch per guided sub-step; any other
+    callable is evaluated on host arrays, as the reference does."""
+    traj, log = guided_ddim_sample_device(net, schedule, cond, x_K, q0, arm, cost_fn, n_steps,
+                                          k_guide_frac, n_grad, alpha_guide, max_halvings)
+    return traj.cpu().numpy(), log
+
+
 # ----------------------------------------------------------------------------- checkpoints
 def save_checkpoint(path, net, schedule, meta: Optional[dict] = None):
     """PSCK: magic, u64 header length, sorted-key JSON, little-endian f64 blob (src/diffusion.py:635-651)."""

@@ -16,7 +16,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from .. import _lib
-from .diffusion import ddim_sample_device, encode_condition
+from .diffusion import PlannerCost, ddim_sample_device, encode_condition, guided_ddim_sample_device
 from .trajopt import CostWeights, OptResult, _ArmArgs, _grid_device, optimize
 from .types import WORKSPACE, Pose2, Rect, SdfGrid
 
@@ -141,8 +141,6 @@ def select_best(results: Sequence[OptResult], successes: Sequence[bool]) -> int:
 def plan_diffusion(arm, net, schedule, req: PlanRequest, weights: CostWeights = CostWeights(),
                    guidance: Optional[GuidanceParams] = None) -> PlanResult:
     """src/pipeline.py:172-209."""
-    if guidance is not None and guidance.alpha_guide != 0.0:
-        raise NotImplementedError("cost-guided sampling (SURVEY §8(f) rank 2) is not built yet")
     torch = _lib.require_cuda()
     t0 = time.perf_counter()
     esdf = build_planner_esdf(req.bounds, req.scan, req.esdf_cell)
@@ -152,8 +150,15 @@ def plan_diffusion(arm, net, schedule, req: PlanRequest, weights: CostWeights = 
     rng = np.random.default_rng(req.seed)
     cond = encode_condition(net, req.scan, req.q_start, req.goal)
     x_K = rng.standard_normal((req.n_trajs, net.config.t_len, net.config.dof))
-    seeds = ddim_sample_device(net, schedule, cond, x_K, req.q_start, arm,
-                               n_steps=req.n_denoising).cpu().numpy()
+    if guidance is not None and guidance.alpha_guide != 0.0:
+        cost_fn = PlannerCost(arm, esdf, req.goal, weights)
+        seeds, _ = guided_ddim_sample_device(net, schedule, cond, x_K, req.q_start, arm, cost_fn,
+                                             n_steps=req.n_denoising, k_guide_frac=guidance.k_guide_frac,
+                                             n_grad=guidance.n_grad, alpha_guide=guidance.alpha_guide)
+        seeds = seeds.cpu().numpy()
+    else:
+        seeds = ddim_sample_device(net, schedule, cond, x_K, req.q_start, arm,
+                                   n_steps=req.n_denoising).cpu().numpy()
     results = optimize(arm, esdf, req.goal, list(seeds), req.n_iters, weights)
     successes = [bool(s) for s in planner_success_batch(arm, esdf, req.goal,
                                                         np.stack([r.trajectory for r in results]),

@@ -217,3 +217,93 @@ def optimize(arm, esdf, goal, seeds: Sequence[np.ndarray], n_iters: int, w: Cost
                       breakdown=dict(zip(TERM_NAMES, terms[s].tolist())), iterations=n_iters,
                       converged=bool(frozen[s]), n_accepted=int(nacc[s]))
             for s in range(stack.shape[0])]
+
+
+# ----------------------------------------------------------------------------- ground truth
+@dataclass
+class TrajectoryMetrics:
+    """src/trajopt.py:49-57."""
+
+    success: bool
+    plan_time: float
+    max_jerk: float
+    motion_time: float
+    translation_error: float
+    angle_error_deg: float
+    collision_free: bool
+
+
+def success_flag(collision_free: bool, translation_error: float, angle_error_deg: float,
+                 delta_t: float, delta_r_deg: float) -> bool:
+    """src/trajopt.py:232-236."""
+    return bool(collision_free and translation_error <= delta_t and angle_error_deg <= delta_r_deg)
+
+
+def metrics_device(arm, gt_world, goal, trajs, interp_per_seg: int = 4):
+    """Raw `ps_ref_metrics` call: (S,6) device f64 rows [clearance, translation error,
+    angle error deg, motion time, max jerk, dt] for trajectories (S,T,D)."""
+    torch = _lib.require_cuda()
+    t = trajs if isinstance(trajs, torch.Tensor) else torch.as_tensor(np.asarray(trajs, dtype=np.float64),
+                                                                        device="cuda")
+    t = t.to(torch.float64).contiguous()
+    S, T, D = t.shape
+    keep = [np.ascontiguousarray(arm.lengths, dtype=np.float64),
+            np.ascontiguousarray(arm.point_fractions(), dtype=np.float64)]
+    dev = lambda a, shape: torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(shape)),
+                                           device="cuda")
+    circ = dev(gt_world.circle_arr, (-1, 3))
+    box = dev(gt_world.box_arr, (-1, 4))
+    lims = [dev(arm.vel_limit, (-1,)), dev(arm.acc_limit, (-1,)), dev(arm.jerk_limit, (-1,))]
+    jm = _device(jerk_matrix(T), "fp64", key=("jm", T, "fp64"))
+    out = torch.empty((S, 6), dtype=torch.float64, device="cuda")
+    st = _lib.lib().ps_ref_metrics(_lib.ptr(t), S, T, D, _lib.hptr(keep[0]), float(arm.base[0]),
+                                   float(arm.base[1]), _lib.hptr(keep[1]), len(keep[1]), _lib.ptr(circ),
+                                   circ.shape[0], _lib.ptr(box), box.shape[0], float(gt_world.sdf_cap),
+                                   float(goal.pos[0]), float(goal.pos[1]), float(goal.theta), _lib.ptr(jm),
+                                   *[_lib.ptr(x) for x in lims], int(interp_per_seg), _lib.ptr(out),
+                                   _lib.stream_handle())
+    _lib.check(st, "metrics")
+    return out
+
+
+def retime(arm, traj) -> Tuple[float, np.ndarray]:
+    """src/trajopt.py:209-229: uniform waypoint spacing meeting the velocity /
+    acceleration / jerk limits -> (motion_time, per-waypoint timestamps)."""
+    from .types import Rect, World
+    traj = np.asarray(traj, dtype=np.float64)
+    T = traj.shape[0]
+    dt = float(metrics_device(arm, World((), Rect((-1.0, -1.0), (1.0, 1.0))), _ZeroPose(), traj[None])[0, 5])
+    return dt * (T - 1), dt * np.arange(T)
+
+
+class _ZeroPose:
+    pos = np.zeros(2)
+    theta = 0.0
+
+
+def metrics_batch(arm, gt_world, goal, trajs, plan_time=0.0, delta_t: float = 0.005,
+                  delta_r_deg: float = 2.86, interp_per_seg: int = 4) -> List[TrajectoryMetrics]:
+    """metrics() over a stack (S,T,D) in one launch; plan_time scalar or per trajectory."""
+    m = metrics_device(arm, gt_world, goal, trajs, interp_per_seg).cpu().numpy()
+    pt = np.broadcast_to(np.asarray(plan_time, dtype=np.float64), (m.shape[0],))
+    out = []
+    for s in range(m.shape[0]):
+        cf = bool(m[s, 0] > 0.0)
+        out.append(TrajectoryMetrics(success=success_flag(cf, float(m[s, 1]), float(m[s, 2]), delta_t, delta_r_deg),
+                                     plan_time=float(pt[s]), max_jerk=float(m[s, 4]), motion_time=float(m[s, 3]),
+                                     translation_error=float(m[s, 1]), angle_error_deg=float(m[s, 2]),
+                                     collision_free=cf))
+    return out
+
+
+def metrics(arm, gt_world, goal, traj, plan_time: float = 0.0, delta_t: float = 0.005,
+            delta_r_deg: float = 2.86, interp_per_seg: int = 4) -> TrajectoryMetrics:
+    """src/trajopt.py:239-272: judge a trajectory against ground-truth geometry."""
+    return metrics_batch(arm, gt_world, goal, np.asarray(traj, dtype=np.float64)[None], plan_time, delta_t,
+                         delta_r_deg, interp_per_seg)[0]
+
+
+def traj_min_clearance(arm, gt_world, traj, interp_per_seg: int = 4) -> float:
+    """_kernels.traj_min_clearance (src/_kernels.py:144-162) for one trajectory."""
+    return float(metrics_device(arm, gt_world, _ZeroPose(), np.asarray(traj, dtype=np.float64)[None],
+                                interp_per_seg)[0, 0].item())

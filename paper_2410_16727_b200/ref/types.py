@@ -58,10 +58,17 @@ class ArmModel:
     hi: np.ndarray
     base: np.ndarray = field(default_factory=lambda: np.zeros(2))
     points_per_link: int = 4
+    vel_limit: np.ndarray = None
+    acc_limit: np.ndarray = None
+    jerk_limit: np.ndarray = None
 
     def __post_init__(self):
         for n in ("lengths", "lo", "hi", "base"):
             object.__setattr__(self, n, np.asarray(getattr(self, n), dtype=np.float64))
+        d = self.lengths.shape[0]
+        for n, v in (("vel_limit", 2.1), ("acc_limit", 15.0), ("jerk_limit", 7500.0)):   # src/arm.py:48-53
+            cur = getattr(self, n)
+            object.__setattr__(self, n, np.full(d, v) if cur is None else np.asarray(cur, dtype=np.float64))
         if np.any(self.lengths <= 0):
             raise ValueError("link lengths must be positive")
         if np.any(self.lo >= self.hi):
@@ -136,3 +143,34 @@ class SensorPose:
 class DepthScan:
     pose: SensorPose
     depths: np.ndarray
+
+
+@dataclass(frozen=True)
+class Circle:
+    center: Tuple[float, float]
+    radius: float
+
+
+@dataclass(frozen=True)
+class Box:
+    lo: Tuple[float, float]
+    hi: Tuple[float, float]
+
+
+class World:
+    """Ground-truth obstacle world (src/geometry.py:72-99): the flat circle / box arrays
+    and the empty-world distance cap the metric kernels read."""
+
+    def __init__(self, obstacles=(), bounds: Rect = WORKSPACE):
+        self.obstacles = tuple(obstacles)
+        self.bounds = bounds
+        cs = [o for o in self.obstacles if isinstance(o, Circle)]
+        bs = [o for o in self.obstacles if isinstance(o, Box)]
+        self.circle_arr = (np.array([[c.center[0], c.center[1], c.radius] for c in cs], dtype=np.float64)
+                           if cs else np.zeros((0, 3)))
+        self.box_arr = (np.array([[b.lo[0], b.lo[1], b.hi[0], b.hi[1]] for b in bs], dtype=np.float64)
+                        if bs else np.zeros((0, 4)))
+
+    @property
+    def sdf_cap(self) -> float:
+        return self.bounds.diagonal

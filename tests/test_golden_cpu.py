@@ -14,7 +14,7 @@ GOLD = ROOT / "tests" / "golden"
 
 def test_fixtures_present():
     names = sorted(p.name for p in GOLD.glob("ref_*.npz"))
-    assert "ref_optimize.npz" in names and "ref_sampler.npz" in names and "ref_plan.npz" in names
+    assert {"ref_optimize.npz", "ref_sampler.npz", "ref_plan.npz", "ref_guided.npz"} <= set(names)
     assert sum(n.startswith("ref_cost_") for n in names) == 7
     z = np.load(GOLD / "ref_cost_c0.npz")
     assert z["trajs"].shape == (6, 32, 7) and z["grads"].shape == (6, 32, 7)

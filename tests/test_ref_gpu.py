@@ -181,3 +181,94 @@ def test_integration_binding_stub(ref):
     x, _, tot, frozen, nacc = kb.optimize_batch(o["seeds"], int(o["n_iters"]), 0.9, 1e-4, 0.5, 40, 1.0, 4.0, *raw)
     _close(x, o["x"], rtol=1e-7, atol=1e-7)
     assert list(frozen) == list(o["frozen"]) and list(nacc) == list(o["n_acc"])
+
+
+def test_guided_ddim_sample(ref):
+    """guided_ddim_sample (src/diffusion.py:572-628): the planner cost runs as one fused
+    cooperative launch per guided sub-step, a user callable on host arrays; trajectories,
+    step logs, the out-of-extent raise and guided plan_diffusion match planseed."""
+    from golden_net import golden_net
+    zs = np.load(GOLD / "ref_sampler.npz")
+    z = np.load(GOLD / "ref_guided.npz")
+    arm = ref.types.default_arm()
+    net = golden_net(arm)
+    goal = ref.types.Pose2((z["goal"][0], z["goal"][1]), z["goal"][2])
+    scan = _scan(ref, zs)
+    cond = ref.diffusion.encode_condition(net, scan, z["q0"], goal)
+    sched = ref.diffusion.make_schedule()
+    req = ref.pipeline.PlanRequest(q_start=z["q0"], goal=goal, scan=scan)
+    esdf = ref.pipeline.build_planner_esdf(req.bounds, scan, 0.01)
+    cost = ref.diffusion.PlannerCost(arm, esdf, goal)
+    traj, log = ref.diffusion.guided_ddim_sample(net, sched, cond, z["x_K"], z["q0"], arm, cost, n_steps=5,
+                                                 n_grad=4, alpha_guide=0.5)
+    assert [list(map(int, e)) for e in log] == z["log"].tolist()
+    _close(traj, z["traj"], rtol=1e-8, atol=1e-8)
+    traj10, log10 = ref.diffusion.guided_ddim_sample(net, sched, cond, z["x_K"][:3], z["q0"], arm, cost,
+                                                     n_steps=10, n_grad=2, alpha_guide=1.0, k_guide_frac=0.9)
+    assert [list(map(int, e)) for e in log10] == z["log10"].tolist()
+    _close(traj10, z["traj10"], rtol=1e-8, atol=1e-8)
+    # single (T,D) input and alpha 0 == unguided (tests/test_diffusion.py:385-389)
+    t1, _ = ref.diffusion.guided_ddim_sample(net, sched, cond, z["x_K"][0], z["q0"], arm, cost, n_steps=5,
+                                             n_grad=4, alpha_guide=0.5)
+    assert t1.shape == (32, 7)
+    plain = ref.diffusion.ddim_sample(net, sched, cond, z["x_K"], z["q0"], arm, n_steps=5)
+    g0, _ = ref.diffusion.guided_ddim_sample(net, sched, cond, z["x_K"], z["q0"], arm, cost, alpha_guide=0.0)
+    assert np.array_equal(plain, g0)
+    # a user cost callable (host arrays), as in tests/test_diffusion.py:365-410
+    target = z["target"]
+
+    def quad(t):
+        d = t - target
+        return np.sum(d.reshape(d.shape[0], -1) ** 2, axis=1), 2.0 * d
+
+    tq, _ = ref.diffusion.guided_ddim_sample(net, sched, cond, z["x_K"][:4], z["q0"], arm, quad, n_steps=5,
+                                             n_grad=3, alpha_guide=0.5)
+    _close(tq, z["trajq"], rtol=1e-8, atol=1e-8)
+    # out-of-extent evaluation raises the reference's ValueError, naming the same seeds
+    small = ref.types.SdfGrid(origin=np.array([-0.3, -0.3]), h=0.01, nx=61, ny=61, values=z["small_values"])
+    with pytest.raises(ValueError) as ei:
+        ref.diffusion.guided_ddim_sample(net, sched, cond, z["x_K"], z["q0"], arm,
+                                         ref.diffusion.PlannerCost(arm, small, goal), n_steps=5, n_grad=2)
+    assert str(ei.value) == str(z["err"])
+    # guided plan_diffusion (src/pipeline.py:189-197)
+    req = ref.pipeline.PlanRequest(q_start=z["q0"], goal=goal, scan=scan, n_trajs=8, n_iters=10, n_denoising=5,
+                                   seed=int(z["plan_seed"]))
+    res = ref.pipeline.plan_diffusion(arm, net, sched, req,
+                                      guidance=ref.pipeline.GuidanceParams(alpha_guide=0.5, n_grad=3))
+    _close(res.seed_trajectories, z["plan_seeds"], rtol=1e-8, atol=1e-8)
+    _close(np.array([r.cost for r in res.results]), z["plan_costs"], rtol=1e-7)
+    assert res.best_index == int(z["plan_best"])
+    _close(res.trajectory, z["plan_traj"], rtol=1e-7, atol=1e-7)
+
+
+def test_metrics_retime_clearance(ref):
+    """trajopt.metrics / retime / traj_min_clearance (src/trajopt.py:209-272,
+    src/_kernels.py:60-162) in one launch per batch against planseed's values; flags exact."""
+    z = np.load(GOLD / "ref_metrics.npz")
+    arm = ref.types.default_arm()
+    T = ref.types
+    goal = T.Pose2((z["goal"][0], z["goal"][1]), z["goal"][2])
+
+    def world(circles, boxes):
+        obs = [T.Circle((c[0], c[1]), c[2]) for c in circles] + [T.Box((b[0], b[1]), (b[2], b[3])) for b in boxes]
+        return T.World(obs)
+
+    worlds = [world(z["circles"], z["boxes"]), world(np.zeros((0, 3)), z["wall_boxes"])]
+    trajs = z["trajs"]
+    want = z["metrics"].reshape(2, len(trajs), 6)
+    for wi, w in enumerate(worlds):
+        ms = ref.trajopt.metrics_batch(arm, w, goal, trajs, plan_time=0.25)
+        got = np.array([[m.success, m.collision_free, m.translation_error, m.angle_error_deg, m.motion_time,
+                         m.max_jerk] for m in ms], dtype=np.float64)
+        assert np.array_equal(got[:, :2], want[wi][:, :2]), wi
+        _close(got[:, 2:], want[wi][:, 2:], rtol=1e-11, atol=1e-12)
+        assert all(m.plan_time == 0.25 for m in ms)
+    assert want[0][:, 0].any() and not want[0][:, 1].all()       # mixed verdicts
+    one = ref.trajopt.metrics(arm, worlds[0], goal, trajs[0])
+    assert one.success
+    cl = [ref.trajopt.traj_min_clearance(arm, worlds[0], t) for t in trajs]
+    _close(np.array(cl), z["clearance"], rtol=1e-12, atol=1e-13)
+    rt = [ref.trajopt.retime(arm, t)[0] for t in trajs]
+    _close(np.array(rt), z["motion_time"], rtol=1e-12, atol=0)
+    mt, stamps = ref.trajopt.retime(arm, np.tile(np.linspace(-1, 1, 7), (32, 1)))   # constant: zero time
+    assert mt == 0.0 and np.all(stamps == 0.0)

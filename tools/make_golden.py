@@ -172,6 +172,85 @@ def gen_plan():
                 seed_trajectories=res.seed_trajectories, loose_success=ps, coll_trajs=coll, coll_success=pc)
 
 
+def gen_guided():
+    """guided_ddim_sample with the planner cost (fused path), with a user quadratic cost
+    (host-callable path), plan_diffusion with guidance, and an out-of-extent raise."""
+    from planseed.diffusion import guided_ddim_sample
+    from planseed.pipeline import GuidanceParams
+    net = net_and_cond()
+    world, scan = scene()
+    q0 = np.array([0.3, -0.5, 0.6, -0.4, 0.2, 0.3, -0.1])
+    goal = fk_pose(ARM, np.array([0.9, 0.4, -0.3, 0.5, 0.2, -0.4, 0.1]))
+    cond = encode_condition(net, scan, q0, goal)
+    sched = make_schedule()
+    esdf = build_planner_esdf(PlanRequest(q_start=q0, goal=goal, scan=scan).bounds, scan, 0.01)
+    w = CostWeights()
+
+    def cost_fn(trajs):
+        totals, grads, _ = evaluate_cost_batch(ARM, esdf, goal, trajs, w)
+        return totals, grads
+
+    rng = np.random.default_rng(21)
+    x_K = rng.standard_normal((6, T, 7))
+    traj, log = guided_ddim_sample(net, sched, cond, x_K, q0, ARM, cost_fn, n_steps=5, n_grad=4,
+                                   alpha_guide=0.5)
+    traj10, log10 = guided_ddim_sample(net, sched, cond, x_K[:3], q0, ARM, cost_fn, n_steps=10, n_grad=2,
+                                       alpha_guide=1.0, k_guide_frac=0.9)
+    target = rng.uniform(-0.5, 0.5, size=(T, 7))
+
+    def quad(trajs):
+        d = trajs - target
+        return np.sum(d.reshape(d.shape[0], -1) ** 2, axis=1), 2.0 * d
+
+    trajq, _ = guided_ddim_sample(net, sched, cond, x_K[:4], q0, ARM, quad, n_steps=5, n_grad=3, alpha_guide=0.5)
+    # out-of-extent: a grid covering only part of the arm's reach
+    small = SdfGrid(origin=np.array([-0.3, -0.3]), h=0.01, nx=61, ny=61,
+                    values=np.random.default_rng(4).uniform(0.05, 0.2, (61, 61)))
+    try:
+        guided_ddim_sample(net, sched, cond, x_K, q0, ARM,
+                           lambda t: evaluate_cost_batch(ARM, small, goal, t, w)[:2], n_steps=5, n_grad=2)
+        err = ""
+    except ValueError as e:
+        err = str(e)
+    req = PlanRequest(q_start=q0, goal=goal, scan=scan, n_trajs=8, n_iters=10, n_denoising=5, seed=13)
+    res = plan_diffusion(ARM, net, sched, req, guidance=GuidanceParams(alpha_guide=0.5, n_grad=3))
+    return dict(q0=q0, goal=np.array([*goal.pos, goal.theta]), x_K=x_K, traj=traj,
+                log=np.array(log, dtype=np.int64), traj10=traj10, log10=np.array(log10, dtype=np.int64),
+                target=target, trajq=trajq, small_values=small.values, err=np.array(err),
+                plan_seed=np.int64(req.seed), plan_best=np.int64(res.best_index), plan_traj=res.trajectory,
+                plan_seeds=res.seed_trajectories, plan_costs=np.array([r.cost for r in res.results]))
+
+
+def gen_metrics():
+    """trajopt.metrics / retime / traj_min_clearance on a mixed batch: collision-free and
+    colliding trajectories, a constant one, a thin wall only the interpolants catch."""
+    from planseed.trajopt import metrics, retime
+    from planseed._kernels import traj_min_clearance
+    world = World([Circle(center=(0.45, 0.15), radius=0.12), Box(lo=(-0.6, -0.7), hi=(-0.2, -0.35)),
+                   Box(lo=(0.2, 0.55), hi=(0.3, 0.9))])
+    rng = np.random.default_rng(30)
+    trajs = list(random_trajs(rng, 20, scale=0.5))
+    trajs.append(np.tile(rng.uniform(-1, 1, 7) * 0.3, (T, 1)))
+    qa = np.zeros(7)
+    qa[0] = np.pi / 2
+    trajs.append(np.linspace(0, 1, T)[:, None] * (np.zeros(7) - qa) + qa)
+    trajs = np.stack(trajs)
+    goal = fk_pose(ARM, trajs[0, -1])
+    wall = World([Box(lo=(0.2, -0.8), hi=(0.24, 0.8))])
+    cols = []
+    for w in (world, wall):
+        for t in trajs:
+            m = metrics(ARM, w, goal, t, plan_time=0.25)
+            cols.append([m.success, m.collision_free, m.translation_error, m.angle_error_deg, m.motion_time,
+                         m.max_jerk])
+    clear = np.array([traj_min_clearance(t, 4, ARM.lengths, 0.0, 0.0, ARM.point_fractions(), world.circle_arr,
+                                         world.box_arr, world.sdf_cap) for t in trajs])
+    rt = np.array([retime(ARM, t)[0] for t in trajs])
+    return dict(trajs=trajs, goal=np.array([*goal.pos, goal.theta]), circles=world.circle_arr,
+                boxes=world.box_arr, wall_boxes=wall.box_arr, metrics=np.array(cols, dtype=np.float64),
+                clearance=clear, motion_time=rt)
+
+
 def main(out_dir: Path = ROOT / "tests" / "golden"):
     out_dir.mkdir(parents=True, exist_ok=True)
     for name, c in gen_cost().items():
@@ -179,6 +258,8 @@ def main(out_dir: Path = ROOT / "tests" / "golden"):
     np.savez_compressed(out_dir / "ref_optimize.npz", **gen_optimize())
     np.savez_compressed(out_dir / "ref_sampler.npz", **gen_sampler())
     np.savez_compressed(out_dir / "ref_plan.npz", **gen_plan())
+    np.savez_compressed(out_dir / "ref_guided.npz", **gen_guided())
+    np.savez_compressed(out_dir / "ref_metrics.npz", **gen_metrics())
     return out_dir
 
 
