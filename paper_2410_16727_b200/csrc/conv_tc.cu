@@ -504,29 +504,16 @@ __global__ void gather_f32_kernel(const float* __restrict__ blob, const long lon
     if (i < n) dst[i] = src[i] >= 0 ? blob[src[i]] : 0.f;
 }
 
-// im2col of the fp32 state for the first layer: A0[row][tap*7 + d] = x[b, t+tap-2, d].
-// Thread i writes the i-th 16-B chunk of A0 (8 chunks per 128-B row), so a warp stores
-// 512 contiguous bytes; x reads hit L1 (each row's 35 inputs are reused by 5 rows).
-__global__ void im2col_kernel(const float* __restrict__ x, int B, int T, __nv_bfloat16* __restrict__ a0) {
+// bf16 view of the fp32 state for the first layer: xb[row] = (x[row][0..6], 0), 16 B per
+// row; the first layer's taps are row shifts of this view inside the MMA descriptors.
+__global__ void xb_kernel(const float* __restrict__ x, size_t rows, __nv_bfloat16* __restrict__ xb) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const size_t rows = (size_t)B * T;
-    if (i >= rows * 8) return;
-    const size_t row = i >> 3;
-    const int ch = (int)(i & 7);
-    const int b = (int)(row / T), t = (int)(row % T);
+    if (i >= rows) return;
     __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        const int col = ch * 8 + u;
-        float f = 0.f;
-        if (col < 5 * U_DOF) {
-            const int tap = col / U_DOF, d = col - tap * U_DOF;
-            const int tt = t + tap - 2;
-            if (tt >= 0 && tt < T) f = __ldg(x + ((size_t)b * T + tt) * U_DOF + d);
-        }
-        v[u] = __float2bfloat16_rn(f);
-    }
-    reinterpret_cast<uint4*>(a0)[i] = *reinterpret_cast<uint4*>(v);
+    for (int u = 0; u < U_DOF; ++u) v[u] = __float2bfloat16_rn(__ldg(x + i * U_DOF + u));
+    v[7] = __float2bfloat16_rn(0.f);
+    reinterpret_cast<uint4*>(xb)[i] = *reinterpret_cast<uint4*>(v);
 }
 
 __global__ void film_step_kernel(const float* __restrict__ fa, const float* __restrict__ fb, int P,
@@ -622,6 +609,7 @@ struct UtGroup {
     int8_t src;     // activation map
     int8_t ntap;    // taps reading this chunk
     int16_t tap0;   // index of its first tap
+    int8_t xb;      // 1: the 8-channel bf16 state view (no swizzle, 16-B rows)
 };
 struct UtTap {
     int16_t kcol;   // weight K column
@@ -676,6 +664,18 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_rows(const void* slot, int r
     return d;
 }
 
+// no-swizzle K-major descriptor over 16-B rows in (time, sample) order: core matrices are
+// 8 consecutive rows (SBO = 128 B to the next 8 rows); LBO = nb * 16 B steps K by one time shift
+__device__ __forceinline__ uint64_t xb_desc(const void* base, int nb) {
+    const uint32_t a = smem_u32(base);
+    uint64_t d = 0;
+    d |= (uint64_t)((a >> 4) & 0x3FFF);
+    d |= (uint64_t)(((uint32_t)nb * 16u) >> 4) << 16;   // LBO: K direction
+    d |= (uint64_t)(128 >> 4) << 32;                     // SBO: M direction
+    d |= (uint64_t)1 << 46;
+    return d;                                            // layout type 0: SWIZZLE_NONE
+}
+
 // MB = M-blocks (128 rows) per tile: every weight stage feeds MB x 4 MMAs.
 template <int N, int EPI, bool RES, int MB>
 __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_constant__ UtArgs a) {
@@ -683,11 +683,15 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     constexpr int ACC1 = acc_cols<N, RES>();          // columns of one M-block
     constexpr int ACC = MB * ACC1;                     // columns of one tile
     constexpr int NBUF = 2 * ACC <= 512 ? 2 : 1;
-    constexpr int NCOLS = NBUF * ACC <= 32 ? 32 : NBUF * ACC <= 64 ? 64 : NBUF * ACC <= 128 ? 128 : NBUF * ACC <= 256 ? 256 : 512;
+    constexpr bool FIN = EPI == EPI_FINAL;
+    // FINAL: the 64->7 projection runs on the tensor core from a bf16 tile in smem into
+    // 16 extra TMEM columns after the accumulators
+    constexpr int PROJ_COL = NBUF * ACC;
+    constexpr int NUSED = NBUF * ACC + (FIN ? 16 : 0);
+    constexpr int NCOLS = NUSED <= 32 ? 32 : NUSED <= 64 ? 64 : NUSED <= 128 ? 128 : NUSED <= 256 ? 256 : 512;
     constexpr int CG = N / 8;
-    // both warpgroups drain every tile (each half of the GroupNorm groups); FINAL needs all
-    // 64 channels per row for the 64->7 projection, so its warpgroups alternate tiles
-    constexpr int NSPLIT = EPI == EPI_FINAL ? 1 : UT_EPI_WG;
+    // both warpgroups drain every tile, each half of the channels / GroupNorm groups
+    constexpr int NSPLIT = UT_EPI_WG;
     constexpr int NC = N / NSPLIT;
     constexpr int NG = 8 / NSPLIT;
     extern __shared__ __align__(1024) uint8_t smem_dyn[];
@@ -698,13 +702,19 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     const int SA = a.sa_stages, SB = a.sb_stages;
     uint8_t* sA = smem;
     uint8_t* sB = smem + (size_t)SA * A_BYTES;
-    uint64_t* a_full = reinterpret_cast<uint64_t*>(sB + (size_t)SB * B_BYTES);
+    // FINAL only: projection A tiles [2][128 x 64] bf16 SW128, W_out^T [16 x 64] bf16 SW128,
+    // per-tile noise [2][128 x 7]
+    uint8_t* sP = sB + (size_t)SB * B_BYTES;
+    uint8_t* sWo = sP + (FIN ? 2 * 16384 : 0);
+    float* sZ = reinterpret_cast<float*>(sWo + (FIN ? 2048 : 0));
+    uint64_t* a_full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sZ) + (FIN ? 2 * 128 * U_DOF * 4 : 0));
     uint64_t* a_empty = a_full + SA;
     uint64_t* b_full = a_empty + SA;
     uint64_t* b_empty = b_full + SB;
     uint64_t* tfull = b_empty + SB;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* pbar = tempty + 2;                 // FINAL: projection MMA done
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(pbar + 2);
     float* s_bias = reinterpret_cast<float*>(tmem_holder + 4);
     float* s_gamma = s_bias + N;
     float* s_beta = s_gamma + N;
@@ -730,8 +740,9 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 128 * NSPLIT);   // FINAL: one warpgroup per tile
+            mbar_init(&tempty[b], 128 * NSPLIT);
         }
+        mbar_init(pbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmA[0]) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmW) : "memory");
@@ -750,8 +761,19 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             }
             if (RES) s_rbias[i] = a.rbias[i];
         }
-        if (EPI == EPI_FINAL)
-            for (int i = threadIdx.x - 64; i < U_DOF * 64; i += 128 * UT_EPI_WG) s_wout[i] = a.wout[i];
+        if constexpr (FIN) {
+            // W_out^T as the projection's B operand: row n = joint (7 used of 16), K = 64 channels,
+            // 16-B chunk j of row n at chunk position j ^ (n & 7) (SW128, absolute-address swizzle)
+            for (int i = threadIdx.x - 64; i < 16 * 8; i += 128 * UT_EPI_WG) {
+                const int n = i >> 3, jc = i & 7;
+                __align__(16) __nv_bfloat16 w8[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) w8[u] = __float2bfloat16_rn(n < U_DOF ? a.wout[n * 64 + jc * 8 + u] : 0.f);
+                *reinterpret_cast<uint4*>(sWo + n * 128 + ((jc ^ (n & 7)) << 4)) = *reinterpret_cast<uint4*>(w8);
+            }
+            if (threadIdx.x - 64 < U_DOF) s_wout[threadIdx.x - 64] = a.bout[threadIdx.x - 64];
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
         for (int i = threadIdx.x - 64; i < a.n_grp; i += 128 * UT_EPI_WG) s_grp[i] = a.grp[i];
         for (int i = threadIdx.x - 64; i < a.n_tap; i += 128 * UT_EPI_WG) s_tap[i] = a.tap[i];
     }
@@ -759,6 +781,11 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    // programmatic dependent launch: the prologue above overlapped the previous layer's
+    // tail; wait for it before any global read or write of activations, then let the next
+    // layer's CTAs launch (they become resident only as this kernel's CTAs exit)
+    pdl_wait();
+    pdl_launch_dependents();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -773,7 +800,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     if (a.dbg & 8) {
                         mbar_arrive(&a_full[sa]);
                     } else {
-                        mbar_expect_tx(&a_full[sa], (uint32_t)A_BYTES);
+                        mbar_expect_tx(&a_full[sa], (uint32_t)(gr.xb ? (Tv + 5) * nb * 16 : A_BYTES));
                         tma_load_3d(sA + (size_t)sa * A_BYTES, &a.tmA[gr.src], &a_full[sa], gr.c, b0, -2);
                     }
                     if (++sa == SA) { sa = 0; pa ^= 1u; }
@@ -818,7 +845,22 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                         const uint64_t da = dA + (uint64_t)(2 + tp.dt) * row_step;
                         const uint64_t db = dB0 + (uint64_t)sb * b_step;
                         const uint32_t d_tmem = acc0 + (tp.res ? (uint32_t)N : 0u);
-                        if (do_mma) {
+                        if (gr.xb) {
+                            // state view: no-swizzle K-major, 16-B rows; a K=16 MMA reads two
+                            // 8-channel core-matrix columns LBO = one time step apart, so the
+                            // 5 taps are 3 MMAs (shifts -2/-1, 0/1, 2/3) and the 1x1 residual one
+                            const uint64_t dX = xb_desc(sA + (size_t)sa * A_BYTES, nb);
+                            const int nk = tp.res ? 1 : 3;
+                            if (do_mma)
+#pragma unroll
+                                for (int mb = 0; mb < MB; ++mb)
+                                    for (int kk = 0; kk < nk; ++kk) {
+                                        const int sh = tp.res ? 0 : 2 * kk - 2;
+                                        umma_bf16(d_tmem + (uint32_t)(mb * ACC1),
+                                                  dX + (uint64_t)((((2 + sh) * nb + mb * 128) * 16) >> 4),
+                                                  db + (uint64_t)(kk * 2), idesc, (tp.first && kk == 0) ? 0u : 1u);
+                                    }
+                        } else if (do_mma) {
 #pragma unroll
                             for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
@@ -849,9 +891,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         const int cbase = NSPLIT > 1 ? wg * NC : 0;   // first column of this warpgroup
         // NSPLIT > 1: every warpgroup drains every tile; FINAL (NSPLIT 1): warpgroups 0/1
         // alternate tiles (one per TMEM buffer -- a third waiter would alias barrier phases)
-        const int j0 = NSPLIT > 1 ? 0 : wg;
-        const int jstep = NSPLIT > 1 ? 1 : 2;
-        for (int j = (NSPLIT == 1 && wg >= 2) ? my_tiles : j0; j < my_tiles; j += jstep) {
+        for (int j = 0; j < my_tiles; ++j) {
             const int tile = blockIdx.x + j * gridDim.x;
             const int buf = j % NBUF;
             const int b = tile * nb + sl;
@@ -951,72 +991,104 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
 
                 const int p = b / a.S;
                 if constexpr (EPI == EPI_FINAL) {
-                    static_assert(N == 64 && NSPLIT == 1 && MB == 1, "final layer has 64 channels");
+                    static_assert(N == 64 && NSPLIT == 2 && MB == 1, "final layer has 64 channels");
                     const int t = t0;
                     const int grow = b * Tv + t;
-                    const uint32_t t_lane = t_lane0;
-                    // 64 -> 7 projection accumulated chunk by chunk (no y[64] live range)
-                    float eps[U_DOF];
+                    uint8_t* sPb = sP + (j & 1) * 16384;
+                    float* sZb = sZ + (j & 1) * (128 * U_DOF);
+                    // y = Mish(GN(acc + bias)) for this warpgroup's 32 channels -> bf16 projection tile
 #pragma unroll
-                    for (int d = 0; d < U_DOF; ++d) eps[d] = a.bout[d];
-#pragma unroll
-                    for (int c0 = 0; c0 < 64; c0 += 16) {
+                    for (int cc = 0; cc < NC; cc += 16) {
+                        const int c0 = cbase + cc;
                         uint32_t rr[16];
-                        tmem_ld16(t_lane + c0, rr);
+                        tmem_ld16(t_lane0 + cc, rr);
                         tmem_wait_ld();
-                        float y[16];
+                        const int gi = cc / CG;
+                        __align__(16) __nv_bfloat162 pk[8];
 #pragma unroll
-                        for (int jj = 0; jj < 16; ++jj) {
-                            const int c = c0 + jj;
-                            const float xv = __uint_as_float(rr[jj]) + s_bias[c];
-                            const float tt = fmaf(xv, rstd[c / CG], -mean[c / CG] * rstd[c / CG]);
-                            y[jj] = mish8(fmaf(tt, s_gamma[c], s_beta[c]));
+                        for (int jj = 0; jj < 16; jj += 2) {
+                            float yv[2];
+#pragma unroll
+                            for (int u = 0; u < 2; ++u) {
+                                const int c = c0 + jj + u;
+                                const int g = gi + (jj + u) / CG;
+                                const float xv = __uint_as_float(rr[jj + u]) + s_bias[c];
+                                const float tt = fmaf(xv, sel(rstd, g), -sel(mean, g) * sel(rstd, g));
+                                yv[u] = mish8(fmaf(tt, s_gamma[c], s_beta[c]));
+                            }
+                            pk[jj / 2] = __floats2bfloat162_rn(yv[0], yv[1]);
                         }
-#pragma unroll
-                        for (int d = 0; d < U_DOF; ++d)
-#pragma unroll
-                            for (int jj = 0; jj < 16; ++jj) eps[d] = fmaf(y[jj], s_wout[d * 64 + c0 + jj], eps[d]);
+                        const int jc = c0 >> 3;
+                        *reinterpret_cast<uint4*>(sPb + r * 128 + (((jc) ^ (r & 7)) << 4)) =
+                            *reinterpret_cast<const uint4*>(&pk[0]);
+                        *reinterpret_cast<uint4*>(sPb + r * 128 + (((jc + 1) ^ (r & 7)) << 4)) =
+                            *reinterpret_cast<const uint4*>(&pk[4]);
                     }
-                    if (valid) {
-                        float* xr = a.x + (size_t)grow * U_DOF;
-                        if (a.eps_out) {
+                    tc_fence_before();
+                    mbar_arrive(&tempty[buf]);   // accumulator drained: the next tile's MMAs may start
+                    const StepCoef sc = a.sc;
+                    const bool noisy = !a.eps_out && !sc.last && sc.ddpm;
+                    if (noisy) {
+                        // the tile's Philox blocks (nb samples x Tv*7/4), spread over both warpgroups
+                        const int per = Tv * U_DOF / 4;
+                        for (int i = threadIdx.x - 64; i < nb * per; i += 128 * UT_EPI_WG) {
+                            const int s2 = i / per, blk = i - s2 * per;
+                            const int b2 = tile * nb + s2;
+                            float n4[4] = {0.f, 0.f, 0.f, 0.f};
+                            if (b2 < a.B)
+                                normal4_tc((uint32_t)sc.k, (uint32_t)(a.p0 + b2 / a.S), (uint32_t)(b2 % a.S),
+                                           (uint32_t)blk, a.key, n4);
+                            *reinterpret_cast<float4*>(sZb + s2 * Tv * U_DOF + blk * 4) =
+                                make_float4(n4[0], n4[1], n4[2], n4[3]);
+                        }
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    asm volatile("bar.sync 3, 256;" ::: "memory");
+                    if (wg == 0) {
+                        if (threadIdx.x == 64) {
+                            tc_fence_after();
+                            constexpr uint32_t idp = idesc_bf16(128, 16);
+                            const uint64_t dP = umma_desc_sw128(sPb), dW = umma_desc_sw128(sWo);
 #pragma unroll
-                            for (int d = 0; d < U_DOF; ++d) a.eps_out[(size_t)grow * U_DOF + d] = eps[d];
-                        } else {
-                            const StepCoef sc = a.sc;
-                            // noise: one Philox call per block of 4 consecutive elements of the row
-                            float z[U_DOF];
-                            if (!sc.last && sc.ddpm) {
-                                const uint32_t e0 = (uint32_t)(t * U_DOF);
+                            for (int kk = 0; kk < 4; ++kk)
+                                umma_bf16(tmem_base + (uint32_t)PROJ_COL, dP + (uint64_t)(kk * 2),
+                                          dW + (uint64_t)(kk * 2), idp, kk > 0 ? 1u : 0u);
+                            umma_commit(pbar);
+                        }
+                        __syncwarp();
+                        mbar_wait(pbar, (uint32_t)j & 1u);
+                        tc_fence_after();
+                        uint32_t pr[16];
+                        tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)PROJ_COL, pr);
+                        tmem_wait_ld();
+                        float eps[U_DOF];
 #pragma unroll
-                                for (int d = 0; d < U_DOF; ++d) z[d] = 0.f;
-                                const uint32_t blk_lo = e0 >> 2, blk_hi = (e0 + U_DOF - 1) >> 2;
-                                for (uint32_t blk = blk_lo; blk <= blk_hi; ++blk) {
-                                    float n4[4];
-                                    normal4_tc((uint32_t)sc.k, (uint32_t)(a.p0 + p), (uint32_t)(b % a.S), blk, a.key, n4);
+                        for (int d = 0; d < U_DOF; ++d) eps[d] = __uint_as_float(pr[d]) + s_wout[d];
+                        if (valid) {
+                            float* xr = a.x + (size_t)grow * U_DOF;
+                            if (a.eps_out) {
 #pragma unroll
-                                    for (int u = 0; u < 4; ++u) {
-                                        const int d = (int)(blk * 4 + u) - (int)e0;
-                                        if (d >= 0 && d < U_DOF) z[d] = n4[u];
+                                for (int d = 0; d < U_DOF; ++d) a.eps_out[(size_t)grow * U_DOF + d] = eps[d];
+                            } else {
+                                const float* zr = sZb + sl * Tv * U_DOF + t * U_DOF;
+#pragma unroll
+                                for (int d = 0; d < U_DOF; ++d) {
+                                    const float xv = xr[d];
+                                    float x0 = (xv - sc.sq1m * eps[d]) * sc.rsq;
+                                    x0 = fminf(fmaxf(x0, -0.1f), 1.1f);
+                                    if (sc.last) {
+                                        a.traj[(size_t)grow * U_DOF + d] =
+                                            (t == 0) ? a.q_start[(size_t)p * U_DOF + d] : a.lo + x0 * (a.hi - a.lo);
+                                    } else if (sc.ddpm) {
+                                        xr[d] = sc.c0 * x0 + sc.c1 * xv + sc.sig * zr[d];
+                                    } else {
+                                        xr[d] = sc.sqn * x0 + sc.sq1mn * eps[d];
                                     }
                                 }
                             }
-#pragma unroll
-                            for (int d = 0; d < U_DOF; ++d) {
-                                const float xv = xr[d];
-                                float x0 = (xv - sc.sq1m * eps[d]) * sc.rsq;
-                                x0 = fminf(fmaxf(x0, -0.1f), 1.1f);
-                                if (sc.last) {
-                                    a.traj[(size_t)grow * U_DOF + d] =
-                                        (t == 0) ? a.q_start[(size_t)p * U_DOF + d] : a.lo + x0 * (a.hi - a.lo);
-                                } else if (sc.ddpm) {
-                                    xr[d] = sc.c0 * x0 + sc.c1 * xv + sc.sig * z[d];
-                                } else {
-                                    xr[d] = sc.sqn * x0 + sc.sq1mn * eps[d];
-                                }
-                            }
                         }
                     }
+                    continue;   // tempty already released
                 } else {
                     // per-tile FiLM rows staged as (1 + scale, shift) for this warpgroup's columns
                     const float* fs1 = nullptr;
@@ -1148,22 +1220,36 @@ static bool make_ts_map(CUtensorMap* tm, const void* base, int B, int Tv, int C,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// bf16 state view [B][Tv][8] in (time, sample) order, no swizzle: box {8, nb, Tv+5}
+// (time shifts -2..+3: the MMA pairing taps 2/3 also reads the zero-weight shift +3, whose
+// rows must be zero-filled by TMA, not stale shared memory -- NaN * 0 = NaN)
+static bool make_xb_map(CUtensorMap* tm, const void* base, int B, int Tv, int nb) {
+    cuuint64_t dims[3] = {8, (cuuint64_t)B, (cuuint64_t)Tv};
+    cuuint64_t strides[2] = {(cuuint64_t)Tv * 16, 16};
+    cuuint32_t box[3] = {8, (cuuint32_t)nb, (cuuint32_t)(Tv + 5)};
+    cuuint32_t es[3] = {1, 1, 1};
+    return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int N, int EPI, bool RES, int MB>
 static int launch_ut(UtArgs& a, cudaStream_t st) {
     const int A_BYTES = (a.Tv + 4) * a.nb * 128;
     constexpr int B_BYTES = N * 128;
     // the kernel's shared layout (unet_tc_kernel): per-channel vectors, w_out, GN partials,
     // staged FiLM, tap tables
-    constexpr int NSPLIT_ = EPI == EPI_FINAL ? 1 : UT_EPI_WG;
+    constexpr int NSPLIT_ = UT_EPI_WG;
     constexpr int NG_ = 8 / NSPLIT_, NC_ = N / NSPLIT_;
     const size_t vec = (size_t)(4 * N + 7 * 64 + UT_EPI_WG * 4 * 32 * 2 * NG_ + UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
                        UT_MAXG * sizeof(UtGroup) + UT_MAXTAP * sizeof(UtTap) + 64;
-    const size_t budget = 225 * 1024 - vec - 2048;
+    const size_t fin = EPI == EPI_FINAL ? 2 * 16384 + 2048 + 2 * 128 * U_DOF * 4 : 0;
+    const size_t budget = 225 * 1024 - vec - 2048 - fin;
     a.sa_stages = 3 * (size_t)A_BYTES <= 110 * 1024 ? 3 : 2;
     a.sb_stages = (int)std::min<size_t>(8, (budget - (size_t)a.sa_stages * A_BYTES) / B_BYTES);
     if (a.sb_stages < 2) return PS_FAIL(PS_ERR_SHAPE);
-    const size_t smem = 1024 + (size_t)a.sa_stages * A_BYTES + (size_t)a.sb_stages * B_BYTES +
-                        (2 * (a.sa_stages + a.sb_stages) + 4) * 8 + 16 + vec;
+    const size_t smem = 1024 + (size_t)a.sa_stages * A_BYTES + (size_t)a.sb_stages * B_BYTES + fin +
+                        (2 * (a.sa_stages + a.sb_stages) + 6) * 8 + 16 + vec;
     auto kern = unet_tc_kernel<N, EPI, RES, MB>;
     static int set_bytes = 0;
     if ((int)smem > set_bytes) {
@@ -1184,8 +1270,10 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     static const bool trace = std::getenv("PS_DEBUG") && std::atoi(std::getenv("PS_DEBUG")) >= 2;
     if (trace) std::fprintf(stderr, "[ps_b200] unet_tc N=%d EPI=%d RES=%d MB=%d B=%d Tv=%d nb=%d grid=%d groups=%d taps=%d\n",
                             N, EPI, (int)RES, MB, a.B, a.Tv, a.nb, grid, a.n_grp, a.n_tap);
-    kern<<<grid, UT_THREADS, smem, st>>>(a);
-    PS_CHECK_LAUNCH();
+    {
+        const int e_ = launch_pdl(kern, dim3(grid), dim3(UT_THREADS), smem, st, a);
+        if (e_) return e_;
+    }
     if (trace && cudaStreamSynchronize(st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
     return PS_OK;
 }
@@ -1202,6 +1290,7 @@ struct TcLayer {
     int Tv;
     __nv_bfloat16* out;
     const __nv_bfloat16* res_src;
+    int xb_src = -1;   // source index that is the 8-channel bf16 state view
 };
 
 static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int B, int S, const float* film,
@@ -1217,7 +1306,8 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
     for (int s = 0; s < 3; ++s)
         // maps span >= nb samples (the workspace is padded to TC_MIN_B): a TMA box larger than
         // the tensor extent never completes its transaction
-        if (ly.src[s] && !make_ts_map(&a.tmA[s], ly.src[s], std::max(B, nb), ly.Tv, ly.ld[s], nb))
+        if (ly.src[s] && !(s == ly.xb_src ? make_xb_map(&a.tmA[s], ly.src[s], std::max(B, nb), ly.Tv, nb)
+                                          : make_ts_map(&a.tmA[s], ly.src[s], std::max(B, nb), ly.Tv, ly.ld[s], nb)))
             return PS_FAIL(PS_ERR_CUDA);
     if (!make_w_map(&a.tmW, W + c.w_off, N, (int)kpad(c.K))) return PS_FAIL(PS_ERR_CUDA);
     if (ly.res && !make_w_map(&a.tmR, W + ly.res->w_off, N, (int)kpad(ly.res->K))) return PS_FAIL(PS_ERR_CUDA);
@@ -1256,6 +1346,7 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
         g.src = (int8_t)groups[gi].src;
         g.ntap = (int8_t)groups[gi].taps.size();
         g.tap0 = (int16_t)nt;
+        g.xb = (int8_t)(groups[gi].src == ly.xb_src ? 1 : 0);
         for (auto tp : groups[gi].taps) {
             if (nt >= UT_MAXTAP) return PS_FAIL(PS_ERR_SHAPE);
             bool& f = tp.res ? first_res : first_main;
@@ -1343,8 +1434,8 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
         const size_t n = (size_t)P * 3584;
         film_step_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(film_a, film_b_row, P, film);
         PS_CHECK_LAUNCH();
-        const size_t m = (size_t)B * T * 8;
-        im2col_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(x, B, T, a0);
+        const size_t m = (size_t)B * T;
+        xb_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(x, m, a0);
         PS_CHECK_LAUNCH();
     }
     auto block = [&](int bi, const __nv_bfloat16* in0, int ld0, const __nv_bfloat16* in1, int ld1,
@@ -1358,6 +1449,7 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
         l0.src[1] = in1; l0.ld[1] = ld1;
         l0.Tv = Tv;
         l0.out = h;
+        if (bi == 0) l0.xb_src = 0;
         PS_TRY_TC(run_layer(L, packed, l0, B, S, film, x, nullptr, nullptr, st));
         TcLayer l1{};
         l1.c = &bk.c1;
@@ -1370,6 +1462,7 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
             l1.res_shift = 1;
             l1.src[1] = in0; l1.ld[1] = ld0;
             l1.src[2] = in1; l1.ld[2] = ld1;
+            if (bi == 0) l1.xb_src = 1;
         } else {
             l1.res_src = in0;
         }

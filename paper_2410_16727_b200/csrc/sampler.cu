@@ -114,10 +114,13 @@ Layout make_layout(int mode, PackMap* M) {
         // c0
         std::vector<PSeg> s0;
         if (im2col) {
+            // first layer reads the bf16 state view [B][T][8]: K column 8*j + c is channel c at
+            // time shift j - 2 (j = 0..5; j = 5 and c = 7 are zero), consumed as 3 K=16 MMAs whose
+            // two 8-channel core-matrix columns are consecutive time shifts
             s0.push_back({0, 0, 0, 64, 0});
             B.conv(blk.c0, co, s0, [&](int r, int n) -> long long {
-                if (r >= 5 * U_DOF) return -1;
-                int tap = r / U_DOF, c = r % U_DOF;
+                const int tap = r / 8, c = r % 8;
+                if (tap >= 5 || c >= U_DOF) return -1;
                 return (long long)(w0 + ((size_t)n * ci + c) * 5 + tap);
             });
         } else {
@@ -146,8 +149,8 @@ Layout make_layout(int mode, PackMap* M) {
             if (im2col) {
                 sr.push_back({0, 0, 0, 64, 0});
                 B.conv(blk.res, co, sr, [&](int r, int n) -> long long {
-                    if (r < 2 * U_DOF || r >= 3 * U_DOF) return -1;
-                    return (long long)(wr + (size_t)n * ci + (r - 2 * U_DOF));
+                    if (r >= U_DOF) return -1;   // shift 0, channels 0..6 (one K=16 MMA)
+                    return (long long)(wr + (size_t)n * ci + r);
                 });
             } else {
                 sr.push_back({0, 0, 0, C1, 0});

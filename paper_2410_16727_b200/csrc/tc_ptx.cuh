@@ -54,6 +54,31 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* tm, ui
         "l"((uint64_t)tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
         : "memory");
 }
+// programmatic dependent launch (griddepcontrol): no-ops for a normal launch
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// launch with cudaLaunchAttributeProgrammaticStreamSerialization: the kernel may start
+// while the previous kernel on the stream drains; it must call pdl_wait() before touching
+// memory the previous kernels produce or consume
+template <typename Kern, typename Arg>
+static inline int launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const Arg& a) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    static const bool no_pdl = std::getenv("PS_NO_PDL") != nullptr;
+    cfg.numAttrs = no_pdl ? 0 : 1;
+    ps_launch_counter().fetch_add(1, std::memory_order_relaxed);
+    if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+    return PS_OK;
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
