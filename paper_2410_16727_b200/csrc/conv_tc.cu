@@ -618,17 +618,19 @@ struct UtTap {
     int8_t first;   // first MMA into its accumulator
 };
 
-constexpr int UT_EPI_WG = 2;                       // U-Net epilogue warpgroups
+constexpr int UT_EPI_WG = 4;                       // U-Net epilogue warpgroups
 constexpr int UT_THREADS = 64 + 128 * UT_EPI_WG;
 
 struct UtArgs {
     CUtensorMap tmA[3];
     CUtensorMap tmW;
     CUtensorMap tmR;
+    CUtensorMap tmO;   // output view [B][Tv][N], (time, sample)-ordered boxes {16, nb, 128/nb}
     UtGroup grp[UT_MAXG];
     UtTap tap[UT_MAXTAP];
     int n_grp, n_tap;
     int sa_stages, sb_stages;
+    int resident;   // 1: every tap's weight box stays in B stage <tap> for the whole kernel
     int B, Tv, nb, S;
     const float* bias;
     const float* gamma;
@@ -707,7 +709,10 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     uint8_t* sP = sB + (size_t)SB * B_BYTES;
     uint8_t* sWo = sP + (FIN ? 2 * 16384 : 0);
     float* sZ = reinterpret_cast<float*>(sWo + (FIN ? 2048 : 0));
-    uint64_t* a_full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sZ) + (FIN ? 2 * 128 * U_DOF * 4 : 0));
+    // output staging (non-FINAL): per warpgroup two [128 rows x 16 ch] bf16 buffers that
+    // TMA-store 16-channel column slabs of the tile (coalesced writes off the LSU path)
+    uint8_t* sOut = reinterpret_cast<uint8_t*>(sZ) + (FIN ? 2 * 128 * U_DOF * 4 : 0);
+    uint64_t* a_full = reinterpret_cast<uint64_t*>(sOut + (FIN ? 0 : UT_EPI_WG * 2 * 4096));
     uint64_t* a_empty = a_full + SA;
     uint64_t* b_full = a_empty + SA;
     uint64_t* b_empty = b_full + SB;
@@ -740,7 +745,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 128 * NSPLIT);
+            mbar_init(&tempty[b], 4 * NSPLIT);   // one arrival per epilogue warp
         }
         mbar_init(pbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -792,6 +797,13 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             int sa = 0, sb = 0;
             uint32_t pa = 0, pb = 0;   // phase bits of the A / B rings
             const int n_grp = a.n_grp;
+            const bool resident = a.resident != 0;
+            if (resident && my_tiles > 0)
+                for (int t = 0; t < a.n_tap; ++t) {   // weights loaded once, reused by every tile
+                    const UtTap tp = s_tap[t];
+                    mbar_expect_tx(&b_full[t], (uint32_t)B_BYTES);
+                    tma_load_2d(sB + (size_t)t * B_BYTES, tp.res ? &a.tmR : &a.tmW, &b_full[t], tp.kcol, 0);
+                }
             for (int j = 0; j < my_tiles; ++j) {
                 const int b0 = (blockIdx.x + j * gridDim.x) * nb;
                 for (int g = 0; g < n_grp; ++g) {
@@ -804,6 +816,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                         tma_load_3d(sA + (size_t)sa * A_BYTES, &a.tmA[gr.src], &a_full[sa], gr.c, b0, -2);
                     }
                     if (++sa == SA) { sa = 0; pa ^= 1u; }
+                    if (resident) continue;
                     for (int k = 0; k < gr.ntap; ++k) {
                         const UtTap tp = s_tap[gr.tap0 + k];
                         mbar_wait(&b_empty[sb], pb ^ 1u);
@@ -825,6 +838,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             uint32_t pa = 0, pb = 0;
             const int n_grp = a.n_grp;
             const bool do_mma = !(a.dbg & 2);
+            const bool resident = a.resident != 0;
             const uint64_t dA0 = umma_desc_sw128(sA), dB0 = umma_desc_sw128(sB);
             const uint64_t a_step = (uint64_t)(A_BYTES >> 4), b_step = (uint64_t)(B_BYTES >> 4);
             const uint64_t row_step = (uint64_t)((nb * 128) >> 4);
@@ -840,10 +854,11 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     const uint64_t dA = dA0 + (uint64_t)sa * a_step;
                     for (int k = 0; k < gr.ntap; ++k) {
                         const UtTap tp = s_tap[gr.tap0 + k];
-                        mbar_wait(&b_full[sb], pb);
+                        const int bs = resident ? gr.tap0 + k : sb;   // resident: stage = tap
+                        mbar_wait(&b_full[bs], resident ? 0u : pb);
                         tc_fence_after();
                         const uint64_t da = dA + (uint64_t)(2 + tp.dt) * row_step;
-                        const uint64_t db = dB0 + (uint64_t)sb * b_step;
+                        const uint64_t db = dB0 + (uint64_t)bs * b_step;
                         const uint32_t d_tmem = acc0 + (tp.res ? (uint32_t)N : 0u);
                         if (gr.xb) {
                             // state view: no-swizzle K-major, 16-B rows; a K=16 MMA reads two
@@ -868,8 +883,10 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                                     umma_bf16(d_tmem + (uint32_t)(mb * ACC1), da + (uint64_t)(mb * 128 * 128 / 16 + kk * 2),
                                               db + (uint64_t)(kk * 2), idesc, (tp.first && kk == 0) ? 0u : 1u);
                         }
-                        umma_commit(&b_empty[sb]);
-                        if (++sb == SB) { sb = 0; pb ^= 1u; }
+                        if (!resident) {
+                            umma_commit(&b_empty[sb]);
+                            if (++sb == SB) { sb = 0; pb ^= 1u; }
+                        }
                     }
                     umma_commit(&a_empty[sa]);
                     if (++sa == SA) { sa = 0; pa ^= 1u; }
@@ -889,10 +906,30 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         const float inv_n = 1.0f / (float)(Tv * CG);
         float* red = s_red + wg * (4 * 32 * 2 * NG);
         const int cbase = NSPLIT > 1 ? wg * NC : 0;   // first column of this warpgroup
+        const bool leader = ((threadIdx.x - 64) & 127) == 0;
+        uint32_t ob = 0;   // staging buffer counter of this warpgroup
+        int cur_tile = 0;
+        // 16 channels of this thread's row -> staging buffer -> TMA store of the warpgroup's
+        // [128 x 16] slab.  The leader waits for the previous store to finish reading the other
+        // buffer before the barrier, so the next slab can be written right after it.
+        auto stage_store = [&](const __nv_bfloat162* pk, int c0, int mb) {
+            uint8_t* so = sOut + (size_t)(wg * 2 + (ob & 1u)) * 4096;
+            *reinterpret_cast<uint4*>(so + r * 32) = reinterpret_cast<const uint4*>(pk)[0];
+            *reinterpret_cast<uint4*>(so + r * 32 + 16) = reinterpret_cast<const uint4*>(pk)[1];
+            fence_proxy_async_smem();
+            if (leader) bulk_wait_read0();
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+            if (leader) {
+                tma_store_3d(&a.tmO, so, c0, cur_tile * nb, mb * (128 / nb));
+                bulk_commit();
+            }
+            ++ob;
+        };
         // NSPLIT > 1: every warpgroup drains every tile; FINAL (NSPLIT 1): warpgroups 0/1
         // alternate tiles (one per TMEM buffer -- a third waiter would alias barrier phases)
         for (int j = 0; j < my_tiles; ++j) {
             const int tile = blockIdx.x + j * gridDim.x;
+            cur_tile = tile;
             const int buf = j % NBUF;
             const int b = tile * nb + sl;
             const bool valid = b < a.B;
@@ -919,17 +956,16 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
 #pragma unroll
                             for (int jj = 0; jj < 16; ++jj) v[jj] = __uint_as_float(rr[jj]);
                         }
-                        if (valid) {
+                        {
                             const int c0 = cbase + cc;
-                            __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
 #pragma unroll
-                            for (int jj = 0; jj < PC; jj += 8) {
-                                __align__(16) __nv_bfloat162 pk[4];
+                            for (int h = 0; h < PC; h += 16) {
+                                __align__(16) __nv_bfloat162 pk[8];
 #pragma unroll
-                                for (int u = 0; u < 4; ++u)
-                                    pk[u] = __floats2bfloat162_rn(v[jj + 2 * u] + s_bias[c0 + jj + 2 * u],
-                                                                  v[jj + 2 * u + 1] + s_bias[c0 + jj + 2 * u + 1]);
-                                *reinterpret_cast<uint4*>(o + jj) = *reinterpret_cast<uint4*>(pk);
+                                for (int u = 0; u < 8; ++u)
+                                    pk[u] = __floats2bfloat162_rn(v[h + 2 * u] + s_bias[c0 + h + 2 * u],
+                                                                  v[h + 2 * u + 1] + s_bias[c0 + h + 2 * u + 1]);
+                                stage_store(pk, c0 + h, mb);
                             }
                         }
                     }
@@ -991,7 +1027,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
 
                 const int p = b / a.S;
                 if constexpr (EPI == EPI_FINAL) {
-                    static_assert(N == 64 && NSPLIT == 2 && MB == 1, "final layer has 64 channels");
+                    static_assert(N == 64 && NC % 16 == 0 && MB == 1, "final layer has 64 channels");
                     const int t = t0;
                     const int grow = b * Tv + t;
                     uint8_t* sPb = sP + (j & 1) * 16384;
@@ -1025,7 +1061,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                             *reinterpret_cast<const uint4*>(&pk[4]);
                     }
                     tc_fence_before();
-                    mbar_arrive(&tempty[buf]);   // accumulator drained: the next tile's MMAs may start
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[buf]);   // accumulator drained: the next tile's MMAs may start
                     const StepCoef sc = a.sc;
                     const bool noisy = !a.eps_out && !sc.last && sc.ddpm;
                     if (noisy) {
@@ -1043,7 +1080,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                         }
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    asm volatile("bar.sync 3, 256;" ::: "memory");
+                    asm volatile("bar.sync 5, %0;" ::"r"(128 * UT_EPI_WG) : "memory");
                     if (wg == 0) {
                         if (threadIdx.x == 64) {
                             tc_fence_after();
@@ -1182,16 +1219,11 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                                     }
                                 }
                             }
-                            if (valid) {
-                                __nv_bfloat16* o = a.out + (size_t)grow * N + c0;
+                                {
+                                __align__(16) __nv_bfloat162 pk[8];
 #pragma unroll
-                                for (int jj = 0; jj < 16; jj += 8) {
-                                    __align__(16) __nv_bfloat162 pk[4];
-#pragma unroll
-                                    for (int u = 0; u < 4; ++u)
-                                        pk[u] = __floats2bfloat162_rn(y[jj + 2 * u], y[jj + 2 * u + 1]);
-                                    *reinterpret_cast<uint4*>(o + jj) = *reinterpret_cast<uint4*>(pk);
-                                }
+                                for (int u = 0; u < 8; ++u) pk[u] = __floats2bfloat162_rn(y[2 * u], y[2 * u + 1]);
+                                stage_store(pk, c0, mb);
                             }
                         }
                       }
@@ -1199,8 +1231,10 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[buf]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
         }
+        if (!FIN && leader) bulk_wait0();   // output stores complete before the grid ends
     }
     __syncthreads();
     if (warp == 1) {
@@ -1217,6 +1251,17 @@ static bool make_ts_map(CUtensorMap* tm, const void* base, int B, int Tv, int C,
     cuuint32_t es[3] = {1, 1, 1};
     return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// output [B][Tv][N] bf16 written in (time, sample)-ordered 16-channel slabs: box {16, nb, 128/nb}
+static bool make_out_map(CUtensorMap* tm, void* base, int B, int Tv, int N, int nb) {
+    cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)B, (cuuint64_t)Tv};
+    cuuint64_t strides[2] = {(cuuint64_t)Tv * N * 2, (cuuint64_t)N * 2};
+    cuuint32_t box[3] = {16, (cuuint32_t)nb, (cuuint32_t)(128 / nb)};
+    cuuint32_t es[3] = {1, 1, 1};
+    return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1243,11 +1288,18 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     constexpr int NG_ = 8 / NSPLIT_, NC_ = N / NSPLIT_;
     const size_t vec = (size_t)(4 * N + 7 * 64 + UT_EPI_WG * 4 * 32 * 2 * NG_ + UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
                        UT_MAXG * sizeof(UtGroup) + UT_MAXTAP * sizeof(UtTap) + 64;
-    const size_t fin = EPI == EPI_FINAL ? 2 * 16384 + 2048 + 2 * 128 * U_DOF * 4 : 0;
+    const size_t fin = EPI == EPI_FINAL ? 2 * 16384 + 2048 + 2 * 128 * U_DOF * 4 : (size_t)UT_EPI_WG * 2 * 4096;
     const size_t budget = 225 * 1024 - vec - 2048 - fin;
     a.sa_stages = 3 * (size_t)A_BYTES <= 110 * 1024 ? 3 : 2;
-    a.sb_stages = (int)std::min<size_t>(8, (budget - (size_t)a.sa_stages * A_BYTES) / B_BYTES);
-    if (a.sb_stages < 2) return PS_FAIL(PS_ERR_SHAPE);
+    const int sb_fit = (int)((budget - (size_t)a.sa_stages * A_BYTES) / B_BYTES);
+    // small layers keep all their weights resident (one box per tap), the rest stream them
+    a.resident = a.n_tap <= std::min(sb_fit, 12) ? 1 : 0;
+    static const bool no_res = std::getenv("PS_NO_RESIDENT") != nullptr;
+    if (no_res) a.resident = 0;
+    a.sb_stages = a.resident ? a.n_tap : std::min(8, sb_fit);
+    if (a.resident)   // spend the smem the weight ring no longer needs on activation stages
+        a.sa_stages = (int)std::max<size_t>(a.sa_stages, std::min<size_t>(4, (budget - (size_t)a.n_tap * B_BYTES) / A_BYTES));
+    if (a.sb_stages < 2 && !a.resident) return PS_FAIL(PS_ERR_SHAPE);
     const size_t smem = 1024 + (size_t)a.sa_stages * A_BYTES + (size_t)a.sb_stages * B_BYTES + fin +
                         (2 * (a.sa_stages + a.sb_stages) + 6) * 8 + 16 + vec;
     auto kern = unet_tc_kernel<N, EPI, RES, MB>;
@@ -1310,6 +1362,8 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
                                           : make_ts_map(&a.tmA[s], ly.src[s], std::max(B, nb), ly.Tv, ly.ld[s], nb)))
             return PS_FAIL(PS_ERR_CUDA);
     if (!make_w_map(&a.tmW, W + c.w_off, N, (int)kpad(c.K))) return PS_FAIL(PS_ERR_CUDA);
+    if (ly.epi != EPI_FINAL && !make_out_map(&a.tmO, ly.out, std::max(B, nb), ly.Tv, N, nb))
+        return PS_FAIL(PS_ERR_CUDA);
     if (ly.res && !make_w_map(&a.tmR, W + ly.res->w_off, N, (int)kpad(ly.res->K))) return PS_FAIL(PS_ERR_CUDA);
     // group taps by the activation chunk they read: (src, channel offset)
     struct Tmp { int src, c; std::vector<UtTap> taps; };
