@@ -626,6 +626,7 @@ struct UtArgs {
     CUtensorMap tmW;
     CUtensorMap tmR;
     CUtensorMap tmO;   // output view [B][Tv][N], (time, sample)-ordered boxes {16, nb, 128/nb}
+    CUtensorMap tmRes; // identity residual view, same geometry as tmO
     UtGroup grp[UT_MAXG];
     UtTap tap[UT_MAXTAP];
     int n_grp, n_tap;
@@ -719,7 +720,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     uint64_t* tfull = b_empty + SB;
     uint64_t* tempty = tfull + 2;
     uint64_t* pbar = tempty + 2;                 // FINAL: projection MMA done
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(pbar + 2);
+    uint64_t* rbar = pbar + 2;                   // identity residual slabs: [WG][2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(rbar + 2 * UT_EPI_WG);
     float* s_bias = reinterpret_cast<float*>(tmem_holder + 4);
     float* s_gamma = s_bias + N;
     float* s_beta = s_gamma + N;
@@ -748,6 +750,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             mbar_init(&tempty[b], 4 * NSPLIT);   // one arrival per epilogue warp
         }
         mbar_init(pbar, 1);
+        for (int i = 0; i < 2 * UT_EPI_WG; ++i) mbar_init(&rbar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmA[0]) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmW) : "memory");
@@ -925,6 +928,48 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             }
             ++ob;
         };
+        // identity residual (GN_RES without a projection): the residual slab is TMA-loaded into
+        // the staging buffer one slab ahead; the thread adds its row and writes the output back
+        // in place, and the same buffer is TMA-stored
+        constexpr bool IDRES = EPI == EPI_GN_RES && !RES;
+        const int n_slab = MB * (NC / 16);
+        auto res_load = [&](uint32_t o, int tile_, int slab) {
+            const int mb_ = slab / (NC / 16), c_ = cbase + (slab % (NC / 16)) * 16;
+            uint64_t* bar = &rbar[wg * 2 + (o & 1u)];
+            mbar_expect_tx(bar, 4096u);
+            tma_load_3d(sOut + (size_t)(wg * 2 + (o & 1u)) * 4096, &a.tmRes, bar, c_, tile_ * nb, mb_ * (128 / nb));
+        };
+        auto stage_store_res = [&](float* y, int c0, int mb, int j_, int slab) {
+            const uint32_t bi = ob & 1u;
+            uint8_t* so = sOut + (size_t)(wg * 2 + bi) * 4096;
+            mbar_wait(&rbar[wg * 2 + bi], (ob >> 1) & 1u);
+            const uint4 q0 = *reinterpret_cast<const uint4*>(so + r * 32);
+            const uint4 q1 = *reinterpret_cast<const uint4*>(so + r * 32 + 16);
+            const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&q0);
+            const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&q1);
+            __align__(16) __nv_bfloat162 pk[8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float2 f0 = __bfloat1622float2(h0[u]), f1 = __bfloat1622float2(h1[u]);
+                pk[u] = __floats2bfloat162_rn(y[2 * u] + f0.x, y[2 * u + 1] + f0.y);
+                pk[4 + u] = __floats2bfloat162_rn(y[8 + 2 * u] + f1.x, y[8 + 2 * u + 1] + f1.y);
+            }
+            *reinterpret_cast<uint4*>(so + r * 32) = reinterpret_cast<const uint4*>(pk)[0];
+            *reinterpret_cast<uint4*>(so + r * 32 + 16) = reinterpret_cast<const uint4*>(pk)[1];
+            fence_proxy_async_smem();
+            if (leader) {
+                bulk_wait_read0();   // the other buffer's store has been read out: prefetch into it
+                if (slab + 1 < n_slab) res_load(ob + 1, cur_tile, slab + 1);
+                else if (j_ + 1 < my_tiles) res_load(ob + 1, cur_tile + (int)gridDim.x, 0);
+            }
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+            if (leader) {
+                tma_store_3d(&a.tmO, so, c0, cur_tile * nb, mb * (128 / nb));
+                bulk_commit();
+            }
+            ++ob;
+        };
+        if (IDRES && leader && my_tiles > 0) res_load(0, blockIdx.x, 0);
         // NSPLIT > 1: every warpgroup drains every tile; FINAL (NSPLIT 1): warpgroups 0/1
         // alternate tiles (one per TMEM buffer -- a third waiter would alias barrier phases)
         for (int j = 0; j < my_tiles; ++j) {
@@ -1206,18 +1251,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
 #pragma unroll
                                 for (int jj = 0; jj < 16; ++jj) y[jj] += __uint_as_float(rq[jj]) + s_rbias[c0 + jj];
                             } else {
-                                const uint4* rsrc = reinterpret_cast<const uint4*>(a.res_src + (size_t)grow * N + c0);
-#pragma unroll
-                                for (int jj = 0; jj < 16; jj += 8) {
-                                    uint4 u = valid ? __ldg(rsrc + jj / 8) : make_uint4(0u, 0u, 0u, 0u);
-                                    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-                                    for (int k2 = 0; k2 < 4; ++k2) {
-                                        const float2 f = __bfloat1622float2(h2[k2]);
-                                        y[jj + 2 * k2] += f.x;
-                                        y[jj + 2 * k2 + 1] += f.y;
-                                    }
-                                }
+                                stage_store_res(y, c0, mb, j, mb * (NC / 16) + cc / 16);
+                                continue;
                             }
                                 {
                                 __align__(16) __nv_bfloat162 pk[8];
@@ -1301,7 +1336,7 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
         a.sa_stages = (int)std::max<size_t>(a.sa_stages, std::min<size_t>(4, (budget - (size_t)a.n_tap * B_BYTES) / A_BYTES));
     if (a.sb_stages < 2 && !a.resident) return PS_FAIL(PS_ERR_SHAPE);
     const size_t smem = 1024 + (size_t)a.sa_stages * A_BYTES + (size_t)a.sb_stages * B_BYTES + fin +
-                        (2 * (a.sa_stages + a.sb_stages) + 6) * 8 + 16 + vec;
+                        (2 * (a.sa_stages + a.sb_stages) + 6 + 2 * UT_EPI_WG) * 8 + 16 + vec;
     auto kern = unet_tc_kernel<N, EPI, RES, MB>;
     static int set_bytes = 0;
     if ((int)smem > set_bytes) {
@@ -1363,6 +1398,8 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
             return PS_FAIL(PS_ERR_CUDA);
     if (!make_w_map(&a.tmW, W + c.w_off, N, (int)kpad(c.K))) return PS_FAIL(PS_ERR_CUDA);
     if (ly.epi != EPI_FINAL && !make_out_map(&a.tmO, ly.out, std::max(B, nb), ly.Tv, N, nb))
+        return PS_FAIL(PS_ERR_CUDA);
+    if (ly.res_src && !make_out_map(&a.tmRes, const_cast<__nv_bfloat16*>(ly.res_src), std::max(B, nb), ly.Tv, N, nb))
         return PS_FAIL(PS_ERR_CUDA);
     if (ly.res && !make_w_map(&a.tmR, W + ly.res->w_off, N, (int)kpad(ly.res->K))) return PS_FAIL(PS_ERR_CUDA);
     // group taps by the activation chunk they read: (src, channel offset)
