@@ -685,7 +685,9 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     constexpr int B_BYTES = N * 128;
     constexpr int ACC1 = acc_cols<N, RES>();          // columns of one M-block
     constexpr int ACC = MB * ACC1;                     // columns of one tile
-    constexpr int NBUF = 2 * ACC <= 512 ? 2 : 1;
+    // TMEM accumulator buffers: up to 4, so the commit -> epilogue -> release round trip of a
+    // tile hides behind the MMAs of the following tiles even when a tile's K loop is short
+    constexpr int NBUF = 4 * ACC <= 512 ? 4 : 2 * ACC <= 512 ? 2 : 1;
     constexpr bool FIN = EPI == EPI_FINAL;
     // FINAL: the 64->7 projection runs on the tensor core from a bf16 tile in smem into
     // 16 extra TMEM columns after the accumulators
@@ -718,8 +720,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     uint64_t* b_full = a_empty + SA;
     uint64_t* b_empty = b_full + SB;
     uint64_t* tfull = b_empty + SB;
-    uint64_t* tempty = tfull + 2;
-    uint64_t* pbar = tempty + 2;                 // FINAL: projection MMA done
+    uint64_t* tempty = tfull + 4;
+    uint64_t* pbar = tempty + 4;                 // FINAL: projection MMA done
     uint64_t* rbar = pbar + 2;                   // identity residual slabs: [WG][2]
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(rbar + 2 * UT_EPI_WG);
     float* s_bias = reinterpret_cast<float*>(tmem_holder + 4);
@@ -745,7 +747,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             mbar_init(&b_full[i], 1);
             mbar_init(&b_empty[i], 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < 4; ++b) {
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 4 * NSPLIT);   // one arrival per epilogue warp
         }
@@ -835,7 +837,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {   // the whole warp runs the issue loop; elect.sync picks the issuing lane
             constexpr uint32_t idesc = idesc_bf16(128, N);
             int sa = 0, sb = 0;
             uint32_t pa = 0, pb = 0;
@@ -874,7 +876,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                                 for (int mb = 0; mb < MB; ++mb)
                                     for (int kk = 0; kk < nk; ++kk) {
                                         const int sh = tp.res ? 0 : 2 * kk - 2;
-                                        umma_bf16(d_tmem + (uint32_t)(mb * ACC1),
+                                        umma_bf16_w(d_tmem + (uint32_t)(mb * ACC1),
                                                   dX + (uint64_t)((((2 + sh) * nb + mb * 128) * 16) >> 4),
                                                   db + (uint64_t)(kk * 2), idesc, (tp.first && kk == 0) ? 0u : 1u);
                                     }
@@ -883,18 +885,18 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                             for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk)
-                                    umma_bf16(d_tmem + (uint32_t)(mb * ACC1), da + (uint64_t)(mb * 128 * 128 / 16 + kk * 2),
+                                    umma_bf16_w(d_tmem + (uint32_t)(mb * ACC1), da + (uint64_t)(mb * 128 * 128 / 16 + kk * 2),
                                               db + (uint64_t)(kk * 2), idesc, (tp.first && kk == 0) ? 0u : 1u);
                         }
                         if (!resident) {
-                            umma_commit(&b_empty[sb]);
+                            umma_commit_w(&b_empty[sb]);
                             if (++sb == SB) { sb = 0; pb ^= 1u; }
                         }
                     }
-                    umma_commit(&a_empty[sa]);
+                    umma_commit_w(&a_empty[sa]);
                     if (++sa == SA) { sa = 0; pa ^= 1u; }
                 }
-                umma_commit(&tfull[buf]);
+                umma_commit_w(&tfull[buf]);
                 if (++buf == NBUF) { buf = 0; tph ^= 1u; }
             }
         }
@@ -1336,7 +1338,7 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
         a.sa_stages = (int)std::max<size_t>(a.sa_stages, std::min<size_t>(4, (budget - (size_t)a.n_tap * B_BYTES) / A_BYTES));
     if (a.sb_stages < 2 && !a.resident) return PS_FAIL(PS_ERR_SHAPE);
     const size_t smem = 1024 + (size_t)a.sa_stages * A_BYTES + (size_t)a.sb_stages * B_BYTES + fin +
-                        (2 * (a.sa_stages + a.sb_stages) + 6 + 2 * UT_EPI_WG) * 8 + 16 + vec;
+                        (2 * (a.sa_stages + a.sb_stages) + 10 + 2 * UT_EPI_WG) * 8 + 16 + vec;
     auto kern = unet_tc_kernel<N, EPI, RES, MB>;
     static int set_bytes = 0;
     if ((int)smem > set_bytes) {
