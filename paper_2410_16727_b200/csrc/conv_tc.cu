@@ -89,7 +89,7 @@ __host__ __device__ constexpr int tmem_alloc_cols() {
 }
 
 constexpr int TC_EPI_WG = 2;                         // epilogue warpgroups
-constexpr int TC_FILM_P = 4;                         // FiLM rows staged per tile
+constexpr int TC_FILM_P = 2;                         // FiLM rows (problems) staged per tile
 constexpr int TC_THREADS = 64 + 128 * TC_EPI_WG;     // producer warp, MMA warp, epilogue
 
 // Persistent: CTA c handles tiles c, c + gridDim.x, ...  The producer streams every
@@ -722,16 +722,16 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     uint64_t* tfull = b_empty + SB;
     uint64_t* tempty = tfull + 4;
     uint64_t* pbar = tempty + 4;                 // FINAL: projection MMA done
-    uint64_t* rbar = pbar + 2;                   // identity residual slabs: [WG][2]
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(rbar + 2 * UT_EPI_WG);
+    uint64_t* rbar = pbar + 2;                   // identity residual slabs: [epilogue warp][2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(rbar + 8 * UT_EPI_WG);
     float* s_bias = reinterpret_cast<float*>(tmem_holder + 4);
     float* s_gamma = s_bias + N;
     float* s_beta = s_gamma + N;
     float* s_rbias = s_beta + N;
     float* s_wout = s_rbias + N;                 // [7][64]
-    float* s_red = s_wout + 7 * 64;              // [WG][4 quadrants][32 samples][2*NG]
-    float* s_film = s_red + UT_EPI_WG * 4 * 32 * 2 * NG;  // [WG][TC_FILM_P][2*NC]
-    UtGroup* s_grp = reinterpret_cast<UtGroup*>(s_film + UT_EPI_WG * TC_FILM_P * 2 * NC);
+    float* s_red = s_wout + 7 * 64;              // [2 tile parity][WG][4 quadrants][32 samples][2*NG]
+    float* s_film = s_red + 2 * UT_EPI_WG * 4 * 32 * 2 * NG;  // [2 tile parity][WG][TC_FILM_P][2*NC]
+    UtGroup* s_grp = reinterpret_cast<UtGroup*>(s_film + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC);
     UtTap* s_tap = reinterpret_cast<UtTap*>(s_grp + UT_MAXG);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             mbar_init(&tempty[b], 4 * NSPLIT);   // one arrival per epilogue warp
         }
         mbar_init(pbar, 1);
-        for (int i = 0; i < 2 * UT_EPI_WG; ++i) mbar_init(&rbar[i], 1);
+        for (int i = 0; i < 8 * UT_EPI_WG; ++i) mbar_init(&rbar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmA[0]) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmW) : "memory");
@@ -911,42 +911,44 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         const float inv_n = 1.0f / (float)(Tv * CG);
         float* red = s_red + wg * (4 * 32 * 2 * NG);
         const int cbase = NSPLIT > 1 ? wg * NC : 0;   // first column of this warpgroup
-        const bool leader = ((threadIdx.x - 64) & 127) == 0;
-        uint32_t ob = 0;   // staging buffer counter of this warpgroup
+        const int ew = warp - 2;                       // epilogue warp 0..4*WG-1
+        const int t_w = (q * 32) / nb;                 // first time row of this warp's 32 rows
+        uint32_t ob = 0;   // staging buffer counter of this warp
         int cur_tile = 0;
-        // 16 channels of this thread's row -> staging buffer -> TMA store of the warpgroup's
-        // [128 x 16] slab.  The leader waits for the previous store to finish reading the other
-        // buffer before the barrier, so the next slab can be written right after it.
+        // 16 channels of this thread's row -> the warp's staging buffer (1 KB) -> TMA store of
+        // the warp's [32 rows x 16 ch] box; lane 0 first waits until the store from the other
+        // buffer has been read out, so the next slab can be written right after __syncwarp
         auto stage_store = [&](const __nv_bfloat162* pk, int c0, int mb) {
-            uint8_t* so = sOut + (size_t)(wg * 2 + (ob & 1u)) * 4096;
-            *reinterpret_cast<uint4*>(so + r * 32) = reinterpret_cast<const uint4*>(pk)[0];
-            *reinterpret_cast<uint4*>(so + r * 32 + 16) = reinterpret_cast<const uint4*>(pk)[1];
+            uint8_t* so = sOut + (size_t)(ew * 2 + (ob & 1u)) * 1024;
+            *reinterpret_cast<uint4*>(so + lane * 32) = reinterpret_cast<const uint4*>(pk)[0];
+            *reinterpret_cast<uint4*>(so + lane * 32 + 16) = reinterpret_cast<const uint4*>(pk)[1];
             fence_proxy_async_smem();
-            if (leader) bulk_wait_read0();
-            asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
-            if (leader) {
-                tma_store_3d(&a.tmO, so, c0, cur_tile * nb, mb * (128 / nb));
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_3d(&a.tmO, so, c0, cur_tile * nb, mb * (128 / nb) + t_w);
                 bulk_commit();
             }
             ++ob;
         };
-        // identity residual (GN_RES without a projection): the residual slab is TMA-loaded into
-        // the staging buffer one slab ahead; the thread adds its row and writes the output back
-        // in place, and the same buffer is TMA-stored
+        // identity residual (GN_RES without a projection): the warp's residual box is TMA-loaded
+        // into its staging buffer one slab ahead; each lane adds its row and writes the output
+        // back in place, and the same buffer is TMA-stored
         constexpr bool IDRES = EPI == EPI_GN_RES && !RES;
         const int n_slab = MB * (NC / 16);
         auto res_load = [&](uint32_t o, int tile_, int slab) {
             const int mb_ = slab / (NC / 16), c_ = cbase + (slab % (NC / 16)) * 16;
-            uint64_t* bar = &rbar[wg * 2 + (o & 1u)];
-            mbar_expect_tx(bar, 4096u);
-            tma_load_3d(sOut + (size_t)(wg * 2 + (o & 1u)) * 4096, &a.tmRes, bar, c_, tile_ * nb, mb_ * (128 / nb));
+            uint64_t* bar = &rbar[ew * 2 + (o & 1u)];
+            mbar_expect_tx(bar, 1024u);
+            tma_load_3d(sOut + (size_t)(ew * 2 + (o & 1u)) * 1024, &a.tmRes, bar, c_, tile_ * nb,
+                        mb_ * (128 / nb) + t_w);
         };
         auto stage_store_res = [&](float* y, int c0, int mb, int j_, int slab) {
             const uint32_t bi = ob & 1u;
-            uint8_t* so = sOut + (size_t)(wg * 2 + bi) * 4096;
-            mbar_wait(&rbar[wg * 2 + bi], (ob >> 1) & 1u);
-            const uint4 q0 = *reinterpret_cast<const uint4*>(so + r * 32);
-            const uint4 q1 = *reinterpret_cast<const uint4*>(so + r * 32 + 16);
+            uint8_t* so = sOut + (size_t)(ew * 2 + bi) * 1024;
+            mbar_wait(&rbar[ew * 2 + bi], (ob >> 1) & 1u);
+            const uint4 q0 = *reinterpret_cast<const uint4*>(so + lane * 32);
+            const uint4 q1 = *reinterpret_cast<const uint4*>(so + lane * 32 + 16);
             const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&q0);
             const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&q1);
             __align__(16) __nv_bfloat162 pk[8];
@@ -956,22 +958,22 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                 pk[u] = __floats2bfloat162_rn(y[2 * u] + f0.x, y[2 * u + 1] + f0.y);
                 pk[4 + u] = __floats2bfloat162_rn(y[8 + 2 * u] + f1.x, y[8 + 2 * u + 1] + f1.y);
             }
-            *reinterpret_cast<uint4*>(so + r * 32) = reinterpret_cast<const uint4*>(pk)[0];
-            *reinterpret_cast<uint4*>(so + r * 32 + 16) = reinterpret_cast<const uint4*>(pk)[1];
+            *reinterpret_cast<uint4*>(so + lane * 32) = reinterpret_cast<const uint4*>(pk)[0];
+            *reinterpret_cast<uint4*>(so + lane * 32 + 16) = reinterpret_cast<const uint4*>(pk)[1];
             fence_proxy_async_smem();
-            if (leader) {
+            if (lane == 0) {
                 bulk_wait_read0();   // the other buffer's store has been read out: prefetch into it
                 if (slab + 1 < n_slab) res_load(ob + 1, cur_tile, slab + 1);
                 else if (j_ + 1 < my_tiles) res_load(ob + 1, cur_tile + (int)gridDim.x, 0);
             }
-            asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
-            if (leader) {
-                tma_store_3d(&a.tmO, so, c0, cur_tile * nb, mb * (128 / nb));
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_3d(&a.tmO, so, c0, cur_tile * nb, mb * (128 / nb) + t_w);
                 bulk_commit();
             }
             ++ob;
         };
-        if (IDRES && leader && my_tiles > 0) res_load(0, blockIdx.x, 0);
+        if (IDRES && lane == 0 && my_tiles > 0) res_load(0, blockIdx.x, 0);
         // NSPLIT > 1: every warpgroup drains every tile; FINAL (NSPLIT 1): warpgroups 0/1
         // alternate tiles (one per TMEM buffer -- a third waiter would alias barrier phases)
         for (int j = 0; j < my_tiles; ++j) {
@@ -1052,21 +1054,40 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                             s1[g] += __shfl_xor_sync(PS_FULL, s1[g], off);
                             s2[g] += __shfl_xor_sync(PS_FULL, s2[g], off);
                         }
-                asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+                // partials of the 4 warps -> smem (double-buffered by tile parity, so one barrier
+                // suffices); the tile's FiLM rows are staged before the same barrier
+                float* redj = red + (j & 1) * (UT_EPI_WG * 4 * 32 * 2 * NG);
                 if (lane < nb)
 #pragma unroll
                     for (int g = 0; g < NG; ++g) {
-                        red[(q * 32 + sl) * 2 * NG + g] = s1[g];
-                        red[(q * 32 + sl) * 2 * NG + NG + g] = s2[g];
+                        redj[(q * 32 + sl) * 2 * NG + g] = s1[g];
+                        redj[(q * 32 + sl) * 2 * NG + NG + g] = s2[g];
                     }
+                bool film_staged = false;
+                if constexpr (EPI == EPI_GN_FILM) {
+                    const int b_last = min(tile * nb + nb - 1, a.B - 1);
+                    const int p_lo = (tile * nb) / a.S, p_hi = b_last / a.S;
+                    float* sf = s_film + ((j & 1) * UT_EPI_WG + wg) * (TC_FILM_P * 2 * NC);
+                    if (p_hi - p_lo < TC_FILM_P) {
+                        const int n = (p_hi - p_lo + 1) * 2 * NC;
+                        for (int i = r; i < n; i += 128) {
+                            const int pp = i / (2 * NC), w = i % (2 * NC);
+                            const int c = cbase + (w < NC ? w : w - NC);
+                            const float v = __ldg(a.film + (size_t)(p_lo + pp) * 3584 + a.film_col +
+                                                  (w < NC ? c : N + c));
+                            sf[pp * 2 * NC + w] = w < NC ? 1.f + v : v;
+                        }
+                        film_staged = true;
+                    }
+                }
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
                     float a1 = 0.f, a2 = 0.f;
 #pragma unroll
                     for (int qq = 0; qq < 4; ++qq) {
-                        a1 += red[(qq * 32 + sl) * 2 * NG + g];
-                        a2 += red[(qq * 32 + sl) * 2 * NG + NG + g];
+                        a1 += redj[(qq * 32 + sl) * 2 * NG + g];
+                        a2 += redj[(qq * 32 + sl) * 2 * NG + NG + g];
                     }
                     mean[g] = a1 * inv_n;
                     rstd[g] = rsqrtf(fmaxf(fmaf(a2, inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
@@ -1178,20 +1199,9 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     const float* fs1 = nullptr;
                     const float* fsh = nullptr;
                     if constexpr (EPI == EPI_GN_FILM) {
-                        const int b_last = min(tile * nb + nb - 1, a.B - 1);
-                        const int p_lo = (tile * nb) / a.S, p_hi = b_last / a.S;
-                        float* sf = s_film + wg * (TC_FILM_P * 2 * NC);
-                        if (p_hi - p_lo < TC_FILM_P) {
-                            const int n = (p_hi - p_lo + 1) * 2 * NC;
-                            for (int i = r; i < n; i += 128) {
-                                const int pp = i / (2 * NC), w = i % (2 * NC);
-                                const int c = cbase + (w < NC ? w : w - NC);
-                                const float v = __ldg(a.film + (size_t)(p_lo + pp) * 3584 + a.film_col +
-                                                      (w < NC ? c : N + c));
-                                sf[pp * 2 * NC + w] = w < NC ? 1.f + v : v;
-                            }
-                            asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
-                            fs1 = sf + (p - p_lo) * 2 * NC;
+                        if (film_staged) {
+                            const int p_lo = (tile * nb) / a.S;
+                            fs1 = s_film + ((j & 1) * UT_EPI_WG + wg) * (TC_FILM_P * 2 * NC) + (p - p_lo) * 2 * NC;
                             fsh = fs1 + NC;
                         }
                     }
@@ -1271,7 +1281,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
         }
-        if (!FIN && leader) bulk_wait0();   // output stores complete before the grid ends
+        if (!FIN && lane == 0) bulk_wait0();   // output stores complete before the grid ends
     }
     __syncthreads();
     if (warp == 1) {
@@ -1291,11 +1301,11 @@ static bool make_ts_map(CUtensorMap* tm, const void* base, int B, int Tv, int C,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// output [B][Tv][N] bf16 written in (time, sample)-ordered 16-channel slabs: box {16, nb, 128/nb}
+// output [B][Tv][N] bf16 written in (time, sample)-ordered 16-channel slabs: box {16, nb, 32/nb}
 static bool make_out_map(CUtensorMap* tm, void* base, int B, int Tv, int N, int nb) {
     cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)B, (cuuint64_t)Tv};
     cuuint64_t strides[2] = {(cuuint64_t)Tv * N * 2, (cuuint64_t)N * 2};
-    cuuint32_t box[3] = {16, (cuuint32_t)nb, (cuuint32_t)(128 / nb)};
+    cuuint32_t box[3] = {16, (cuuint32_t)nb, (cuuint32_t)(32 / nb)};   // one epilogue warp's 32 rows
     cuuint32_t es[3] = {1, 1, 1};
     return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -1323,7 +1333,7 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     // staged FiLM, tap tables
     constexpr int NSPLIT_ = UT_EPI_WG;
     constexpr int NG_ = 8 / NSPLIT_, NC_ = N / NSPLIT_;
-    const size_t vec = (size_t)(4 * N + 7 * 64 + UT_EPI_WG * 4 * 32 * 2 * NG_ + UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
+    const size_t vec = (size_t)(4 * N + 7 * 64 + 2 * UT_EPI_WG * 4 * 32 * 2 * NG_ + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
                        UT_MAXG * sizeof(UtGroup) + UT_MAXTAP * sizeof(UtTap) + 64;
     const size_t fin = EPI == EPI_FINAL ? 2 * 16384 + 2048 + 2 * 128 * U_DOF * 4 : (size_t)UT_EPI_WG * 2 * 4096;
     const size_t budget = 225 * 1024 - vec - 2048 - fin;
@@ -1333,12 +1343,17 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     a.resident = a.n_tap <= std::min(sb_fit, 12) ? 1 : 0;
     static const bool no_res = std::getenv("PS_NO_RESIDENT") != nullptr;
     if (no_res) a.resident = 0;
-    a.sb_stages = a.resident ? a.n_tap : std::min(8, sb_fit);
-    if (a.resident)   // spend the smem the weight ring no longer needs on activation stages
+    if (a.resident) {   // spend the smem the weight ring no longer needs on activation stages
+        a.sb_stages = a.n_tap;
         a.sa_stages = (int)std::max<size_t>(a.sa_stages, std::min<size_t>(4, (budget - (size_t)a.n_tap * B_BYTES) / A_BYTES));
+    } else {            // streamed weights: two activation stages, as deep a weight ring as fits, then a third A stage
+        a.sa_stages = 2;
+        a.sb_stages = (int)std::min<size_t>(8, (budget - 2 * (size_t)A_BYTES) / B_BYTES);
+        if (a.sb_stages >= 4 && budget >= 3 * (size_t)A_BYTES + (size_t)a.sb_stages * B_BYTES) a.sa_stages = 3;
+    }
     if (a.sb_stages < 2 && !a.resident) return PS_FAIL(PS_ERR_SHAPE);
     const size_t smem = 1024 + (size_t)a.sa_stages * A_BYTES + (size_t)a.sb_stages * B_BYTES + fin +
-                        (2 * (a.sa_stages + a.sb_stages) + 10 + 2 * UT_EPI_WG) * 8 + 16 + vec;
+                        (2 * (a.sa_stages + a.sb_stages) + 10 + 8 * UT_EPI_WG) * 8 + 16 + vec;
     auto kern = unet_tc_kernel<N, EPI, RES, MB>;
     static int set_bytes = 0;
     if ((int)smem > set_bytes) {
