@@ -172,9 +172,12 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // mish(x) = x - 2x / (n^2 + 2n + 2), n = e^min(x, 15)   (8 instructions; for x > 15 the
 // correction underflows below fp32 resolution, so no branch/select is needed)
 __device__ __forceinline__ float mish8(float x) {
-    const float n = ex2_approx(fminf(x, 15.f) * 1.4426950408889634f);
-    const float d = fmaf(n, n + 2.f, 2.f);
-    return fmaf(x * -2.f, rcp_approx(d), x);
+    // mish(x) = x - 2x / (n (n + 2) + 2), n = e^x, as x + x * r with r = 1 / (-d/2) = -2/d:
+    // -d/2 = n * (-(n + 2)/2) - 1.  6 ops (2 on the SFU).  No clamp needed: n = inf gives
+    // -d/2 = -inf, r = -0 and mish = x; n = 0 gives r = -1 and mish = 0.
+    const float n = ex2_approx(x * 1.4426950408889634f);
+    const float m = fmaf(n, -0.5f, -1.f);
+    return fmaf(x, rcp_approx(fmaf(n, m, -1.f)), x);
 }
 
 
