@@ -364,9 +364,10 @@ __global__ void __launch_bounds__(256) esdf_boxes_kernel(const float* __restrict
 __global__ void __launch_bounds__(256) esdf_cull_kernel(const float* __restrict__ boxes, int n_boxes, int nx, int ny,
                                                         int nz, float ox, float oy, float oz, float h, float cap,
                                                         float* __restrict__ out) {
+    // per warp, the column's boxes sorted by their xy lower bound, with the column-constant
+    // parts of the box distance (ax, ay, max(qx, qy)) precomputed
+    __shared__ float s_lb[8][32], s_cz[8][32], s_hz[8][32], s_ax[8][32], s_ay[8][32], s_mq[8][32];
     __shared__ float bc[32][3], bh[32][3];
-    __shared__ float s_lb[8][32];
-    __shared__ int s_id[8][32];
     const int p = blockIdx.y;
     const float* bx = boxes + (size_t)p * n_boxes * 6;
     for (int i = threadIdx.x; i < n_boxes * 3; i += blockDim.x) {
@@ -407,26 +408,46 @@ __global__ void __launch_bounds__(256) esdf_cull_kernel(const float* __restrict_
                 }
             }
         }
-        s_lb[warp][lane] = lb;
-        s_id[warp][lane] = id;
+        if (lane < n_boxes) {
+            const float qx = fabsf(px - bc[id][0]) - bh[id][0];
+            const float qy = fabsf(py - bc[id][1]) - bh[id][1];
+            s_lb[warp][lane] = lb;
+            s_cz[warp][lane] = bc[id][2];
+            s_hz[warp][lane] = bh[id][2];
+            s_ax[warp][lane] = fmaxf(qx, 0.f);
+            s_ay[warp][lane] = fmaxf(qy, 0.f);
+            s_mq[warp][lane] = fmaxf(qx, qy);   // fmaxf is exact: max(qx, qy, qz) in any order
+        }
         __syncwarp();
         float* o = out + (size_t)p * (size_t)n_nodes + (size_t)col * nz;
-        for (int k = lane; k < nz; k += 32) {
-            const float pz = fmaf((float)k, h, oz);
-            float best = cap;
+        // each lane owns 4 nodes (k = lane + 32 m) and walks the sorted boxes once for all of
+        // them; it stops when the next box's lower bound is positive and >= every node's best
+        // (evaluating a box past a node's own stop point cannot lower that node's minimum)
+        for (int k0 = 0; k0 < nz; k0 += 128) {
+            float pz[4], best[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                pz[m] = fmaf((float)(k0 + lane + 32 * m), h, oz);
+                best[m] = cap;
+            }
             for (int e = 0; e < n_boxes; ++e) {
                 const float l = s_lb[warp][e];
-                if (l > 0.f && l >= best) break;
-                const int b = s_id[warp][e];
-                const float qx = fabsf(px - bc[b][0]) - bh[b][0];
-                const float qy = fabsf(py - bc[b][1]) - bh[b][1];
-                const float qz = fabsf(pz - bc[b][2]) - bh[b][2];
-                const float ax = fmaxf(qx, 0.f), ay = fmaxf(qy, 0.f), az = fmaxf(qz, 0.f);
-                const float outside = sqrtf(fmaf(ax, ax, fmaf(ay, ay, az * az)));
-                const float inside = fminf(fmaxf(qx, fmaxf(qy, qz)), 0.f);
-                best = fminf(best, outside + inside);
+                const float bmax = fmaxf(fmaxf(best[0], best[1]), fmaxf(best[2], best[3]));
+                if (l > 0.f && l >= bmax) break;
+                const float cz = s_cz[warp][e], hz = s_hz[warp][e];
+                const float ax = s_ax[warp][e], ay = s_ay[warp][e], mq = s_mq[warp][e];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const float qz = fabsf(pz[m] - cz) - hz;
+                    const float az = fmaxf(qz, 0.f);
+                    const float outside = sqrtf(fmaf(ax, ax, fmaf(ay, ay, az * az)));
+                    const float inside = fminf(fmaxf(mq, qz), 0.f);
+                    best[m] = fminf(best[m], outside + inside);
+                }
             }
-            o[k] = best;
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+                if (k0 + lane + 32 * m < nz) o[k0 + lane + 32 * m] = best[m];
         }
         __syncwarp();
     }

@@ -801,6 +801,52 @@ extern "C" int ps_noise_probe(float* out, int n, int step, int prob, int seed, u
 // ddpm=1 runs the stochastic posterior update between consecutive indices k -> k-1
 // (requires the full K..1 list), ddpm=0 the deterministic DDIM update (eta = 0).
 // coef_h: 6 x (K+1) float32 tables (sq, sq1m, rsq, c0, c1, sig) from spec.sampler_tables.
+// ---- graph cache of the denoising loop
+static uint64_t hash_bytes(const void* p, size_t n) {
+    const unsigned char* c = static_cast<const unsigned char*>(p);
+    uint64_t h = 1469598103934665603ull;
+    for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 1099511628211ull;
+    return h;
+}
+struct SampleKey {
+    const void* packed; const float* film_a; const float* q_start; void* ws; float* traj;
+    int mode, P, S, T, p0, n_steps, ddpm, K;
+    unsigned noise_key;
+    float lo, hi;
+    cudaStream_t stream;
+    uint64_t steps_hash, coef_hash;
+    bool operator==(const SampleKey& o) const {
+        return packed == o.packed && film_a == o.film_a && q_start == o.q_start && ws == o.ws && traj == o.traj &&
+               mode == o.mode && P == o.P && S == o.S && T == o.T && p0 == o.p0 && n_steps == o.n_steps &&
+               ddpm == o.ddpm && K == o.K && noise_key == o.noise_key && lo == o.lo && hi == o.hi &&
+               stream == o.stream && steps_hash == o.steps_hash && coef_hash == o.coef_hash;
+    }
+};
+struct SampleGraph {
+    SampleKey key{};
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    long long n_kernels = 0;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    void reset() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        exec = nullptr;
+        graph = nullptr;
+        key = SampleKey{};
+        n_kernels = 0;
+    }
+};
+static SampleGraph& sample_graph() {
+    static SampleGraph g;
+    return g;
+}
+static int sample_loop(const void* packed, int mode, const float* film_a, const float* film_b, const float* coef_h,
+                       int K, const int* steps_h, int n_steps, int ddpm, int B, int T, int S, int p0,
+                       unsigned noise_key, const float* q_start, float lo, float hi, float* x, float* eps,
+                       float* act, float* traj, size_t n, cudaStream_t st);
+
 extern "C" int ps_sample(const void* packed, int mode, const float* film_a, int P, int S, int T, int p0,
                          const int* steps_h, int n_steps, int ddpm, const float* coef_h, int K, unsigned noise_key,
                          const float* q_start, float lo, float hi, void* ws, float* traj, void* stream) {
@@ -826,6 +872,67 @@ extern "C" int ps_sample(const void* packed, int mode, const float* film_a, int 
         return PS_FAIL(PS_ERR_CUDA);
     PS_TRY(ps_film_steps(packed, mode, dks, n_steps, scratch, film_b, stream));
     const size_t n = (size_t)B * T * U_DOF;
+    // The denoising loop (noise init + n_steps x ~31 launches) is captured once into a CUDA
+    // graph and replayed while every argument that shapes it is unchanged: at small batch the
+    // host cost of building ~31 launches per step (tensor maps, argument blocks) dominates.
+    SampleKey key{};
+    key.packed = packed; key.film_a = film_a; key.q_start = q_start; key.ws = ws; key.traj = traj;
+    key.mode = mode; key.P = P; key.S = S; key.T = T; key.p0 = p0; key.n_steps = n_steps; key.ddpm = ddpm;
+    key.K = K; key.noise_key = noise_key; key.lo = lo; key.hi = hi; key.stream = st;
+    key.steps_hash = hash_bytes(steps_h, (size_t)n_steps * sizeof(int));
+    key.coef_hash = hash_bytes(coef_h, (size_t)6 * (K + 1) * sizeof(float));
+    static const bool use_graph = std::getenv("PS_NO_GRAPH") == nullptr;
+    auto run_direct = [&]() {
+        return sample_loop(packed, mode, film_a, film_b, coef_h, K, steps_h, n_steps, ddpm, B, T, S, p0, noise_key,
+                           q_start, lo, hi, x, eps, act, traj, n, st);
+    };
+    if (!use_graph) return run_direct();
+    SampleGraph& G = sample_graph();
+    // graphs run on a private stream ordered after / before the caller's stream by events
+    // (the caller may be on the legacy default stream, which cannot be captured)
+    if (!G.side) {
+        if (cudaStreamCreateWithFlags(&G.side, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&G.ev_in, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&G.ev_out, cudaEventDisableTiming) != cudaSuccess)
+            return PS_FAIL(PS_ERR_CUDA);
+    }
+    key.stream = G.side;
+    auto launch_graph = [&]() -> int {
+        if (cudaEventRecord(G.ev_in, st) != cudaSuccess || cudaStreamWaitEvent(G.side, G.ev_in, 0) != cudaSuccess ||
+            cudaGraphLaunch(G.exec, G.side) != cudaSuccess || cudaEventRecord(G.ev_out, G.side) != cudaSuccess ||
+            cudaStreamWaitEvent(st, G.ev_out, 0) != cudaSuccess)
+            return PS_FAIL(PS_ERR_CUDA);
+        ps_launch_counter().fetch_add(G.n_kernels, std::memory_order_relaxed);
+        return PS_OK;
+    };
+    if (G.exec && G.key == key) return launch_graph();
+    G.reset();
+    const long long launches0 = ps_launch_counter().load();
+    if (cudaStreamBeginCapture(G.side, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return run_direct();
+    const int body = sample_loop(packed, mode, film_a, film_b, coef_h, K, steps_h, n_steps, ddpm, B, T, S, p0,
+                                 noise_key, q_start, lo, hi, x, eps, act, traj, n, G.side);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(G.side, &g);
+    if (body != PS_OK || e != cudaSuccess || cudaGraphInstantiate(&G.exec, g, 0) != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        G.reset();
+        cudaGetLastError();
+        if (body != PS_OK && e == cudaSuccess) return body;
+        return run_direct();   // capture not possible here: run the loop directly
+    }
+    G.graph = g;
+    G.key = key;
+    G.n_kernels = ps_launch_counter().load() - launches0;
+    ps_launch_counter().fetch_sub(G.n_kernels, std::memory_order_relaxed);   // counted when launched
+    return launch_graph();
+}
+
+// the denoising loop of ps_sample (captured into a graph by the caller)
+static int sample_loop(const void* packed, int mode, const float* film_a, const float* film_b, const float* coef_h,
+                       int K, const int* steps_h, int n_steps, int ddpm, int B, int T, int S, int p0,
+                       unsigned noise_key, const float* q_start, float lo, float hi, float* x, float* eps,
+                       float* act, float* traj, size_t n, cudaStream_t st) {
+    Layout L = make_layout(mode, nullptr);
     noise_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, B, T, S, p0, noise_key);
     PS_CHECK_LAUNCH();
     const float* sq = coef_h;

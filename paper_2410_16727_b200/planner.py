@@ -58,6 +58,7 @@ class BLPlanner:
                     torch.empty(B, dtype=torch.uint8, device=dev),
                     torch.empty(B, dtype=torch.uint8, device=dev))
         self.best = torch.empty(self.Pmax, dtype=torch.int32, device=dev)
+        self.film_a = torch.empty((self.Pmax, 3584), dtype=torch.float32, device=dev)
         # device copies of host inputs for the end-to-end path
         self.d_images = torch.empty((self.Pmax, n_images) + tuple(image_shape), dtype=torch.float32,
                                     device=dev)
@@ -82,7 +83,7 @@ class BLPlanner:
         if images_ready is not None:
             torch.cuda.current_stream().wait_event(images_ready)
         cond = self.sampler.encode(images, q_start, goal)
-        fa = self.sampler.film(cond)
+        fa = self.sampler.film(cond, out=self.film_a[:P])
         if events is not None:
             events["sample_start"].record()
         seeds = self.sampler.sample(fa, q_start, self.S, self.T, p0=p0, steps=self.steps,

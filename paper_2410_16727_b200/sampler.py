@@ -102,11 +102,13 @@ class SeedSampler:
         _lib.check(st, "encode")
         return cond
 
-    def film(self, cond, stream=None):
+    def film(self, cond, stream=None, out=None):
+        """Per-problem FiLM part (P, 3584); `out` reuses a caller buffer (keeping the sampler's
+        arguments stable lets ps_sample replay its captured CUDA graph)."""
         torch = _lib.require_cuda()
         from .bl import _dev
         c = _dev(cond)
-        fa = torch.empty((c.shape[0], 3584), dtype=torch.float32, device="cuda")
+        fa = out if out is not None else torch.empty((c.shape[0], 3584), dtype=torch.float32, device="cuda")
         _lib.check(_lib.lib().ps_film_problem(_lib.ptr(self.packed), self.mode, _lib.ptr(c),
                                               c.shape[0], _lib.ptr(fa), _lib.stream_handle(stream)),
                    "film_problem")

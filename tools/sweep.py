@@ -1,0 +1,119 @@
+"""BASELINE.json config 4: the config-3 pipeline swept over problems x seeds x horizon x
+schedule on one GPU.  Device-resident inputs; problems beyond one planner's capacity run
+as consecutive chunks (noise and inputs are keyed by the global problem index, so a chunked
+run equals an unchunked one).  Per combination: trajectories/s, p50/p99 ms per planning
+call (a batched call plans all P problems, so this is the per-problem latency), the
+amortised ms per problem, and the sampler's tensor roofline fraction.
+
+    python tools/sweep.py [--quick] [--out profiles/r01_sweep.json]
+"""
+from __future__ import annotations
+
+import argparse
+import itertools
+import json
+import statistics
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2410_16727_b200 import spec, synth  # noqa: E402
+from paper_2410_16727_b200.planner import BLPlanner  # noqa: E402
+
+
+def peaks():
+    try:
+        mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return mp.get("bf16_tflops_sustained") or mp["bf16_tflops"]
+    except Exception:
+        return 1400.0
+
+
+def run_combo(params, P, S, T, sched, budget_s, base_pb, chunk_cap):
+    steps = None if sched == "ddpm100" else spec.strided_steps(100, 10)
+    chunk = max(1, min(P, chunk_cap // S))
+    planner = BLPlanner(params, spec.ENCODER_CFG3, mode=1, S=S, T=T, steps=steps, max_problems=chunk)
+    dev = torch.device("cuda")
+    # inputs of the first `chunk` problems (tiled for larger P; the noise stays keyed by p0)
+    n = min(chunk, base_pb.q_start.shape[0])
+    rep = (chunk + n - 1) // n
+    imgs = torch.as_tensor(np.concatenate([base_pb.images[:n]] * rep)[:chunk], device=dev)
+    q = torch.as_tensor(np.concatenate([base_pb.q_start[:n]] * rep)[:chunk], device=dev)
+    g = torch.as_tensor(np.concatenate([base_pb.goal[:n]] * rep)[:chunk], device=dev)
+    bx = torch.as_tensor(np.concatenate([base_pb.boxes[:n]] * rep)[:chunk], device=dev)
+    ev = {"sample_start": torch.cuda.Event(enable_timing=True), "sample_end": torch.cuda.Event(enable_timing=True)}
+
+    def call(events=None):
+        samp = 0.0
+        for c0 in range(0, P, chunk):
+            m = min(chunk, P - c0)
+            planner.plan_batch_device(imgs[:m], q[:m], g[:m], bx[:m], p0=c0, events=events)
+            if events is not None:
+                events["sample_end"].synchronize()
+                samp += events["sample_start"].elapsed_time(events["sample_end"])
+        return samp
+
+    call()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    call()
+    torch.cuda.synchronize()
+    est = time.perf_counter() - t0
+    reps = int(max(3, min(20, budget_s / max(est, 1e-4))))
+    ms, samp = [], []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        s_ms = call(ev)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        samp.append(s_ms)
+    ms.sort()
+    p50 = statistics.median(ms)
+    p99 = ms[min(len(ms) - 1, int(round(0.99 * (len(ms) - 1))))]
+    n_eval = 100 if steps is None else len(steps)
+    flops = P * S * n_eval * spec.UNetArch().flops_per_traj_step(T) + P * n_eval * spec.UNetArch().film_flops()
+    s_ms = statistics.median(samp)
+    del planner
+    torch.cuda.empty_cache()
+    return {"problems": P, "seeds": S, "horizon": T, "schedule": sched, "chunk": chunk, "reps": reps,
+            "traj_per_s": P * S / (p50 / 1e3), "p50_ms_per_call": p50, "p99_ms_per_call": p99,
+            "amortised_ms_per_problem": p50 / P, "sampler_ms": s_ms,
+            "sampler_tflops": flops / (s_ms / 1e3) / 1e12, "sampler_frac_of_sustained_bf16": flops / (s_ms / 1e3) / 1e12 / peaks()}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--budget", type=float, default=4.0, help="seconds of timed calls per combination")
+    ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "sweep.json"))
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    params = spec.random_model(spec.ENCODER_CFG3)
+    base = synth.config3_problems(256, p0=0, seed=0)
+    Ps = [1, 16, 256, 4096, 16384] if not args.quick else [1, 256]
+    Ss = [8, 32, 128] if not args.quick else [32]
+    Ts = [32, 64]
+    scheds = ["ddim10", "ddpm100"]
+    rows = []
+    for sched, T, S, P in itertools.product(scheds, Ts, Ss, Ps):
+        # the largest ddpm100 combinations take minutes per call: cap trajectories for ddpm100
+        if sched == "ddpm100" and P * S * (T // 32) > 1024 * 128:
+            continue
+        cap = 65536 if T == 32 else 32768
+        r = run_combo(params, P, S, T, sched, args.budget, base, cap)
+        print(json.dumps(r), flush=True)
+        rows.append(r)
+    Path(args.out).parent.mkdir(parents=True, exist_ok=True)
+    Path(args.out).write_text(json.dumps({"device": torch.cuda.get_device_name(0), "rows": rows}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
