@@ -792,8 +792,18 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     // programmatic dependent launch: the prologue above overlapped the previous layer's
-    // tail; wait for it before any global read or write of activations, then let the next
-    // layer's CTAs launch (they become resident only as this kernel's CTAs exit)
+    // tail.  The producer first sends the first tile's weight boxes (no kernel writes
+    // weights), then every thread waits for the previous grid before touching activations,
+    // and the next layer's CTAs may launch (they become resident as this kernel's CTAs exit)
+    int pre = 0;   // weight boxes issued before the dependency wait (stages 0..pre-1)
+    if (warp == 0 && lane == 0 && my_tiles > 0 && !(a.dbg & (16 | 64))) {
+        pre = a.resident ? a.n_tap : (a.n_tap < SB ? a.n_tap : SB);
+        for (int t = 0; t < pre; ++t) {
+            const UtTap tp = s_tap[t];
+            mbar_expect_tx(&b_full[t], (uint32_t)B_BYTES);
+            tma_load_2d(sB + (size_t)t * B_BYTES, tp.res ? &a.tmR : &a.tmW, &b_full[t], tp.kcol, 0);
+        }
+    }
     pdl_wait();
     pdl_launch_dependents();
 
@@ -804,11 +814,12 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             const int n_grp = a.n_grp;
             const bool resident = a.resident != 0;
             if (resident && my_tiles > 0)
-                for (int t = 0; t < a.n_tap; ++t) {   // weights loaded once, reused by every tile
+                for (int t = pre; t < a.n_tap; ++t) {   // weights loaded once, reused by every tile
                     const UtTap tp = s_tap[t];
                     mbar_expect_tx(&b_full[t], (uint32_t)B_BYTES);
                     tma_load_2d(sB + (size_t)t * B_BYTES, tp.res ? &a.tmR : &a.tmW, &b_full[t], tp.kcol, 0);
                 }
+            int issued = 0;   // streamed weight boxes counted from the start of the kernel
             for (int j = 0; j < my_tiles; ++j) {
                 const int b0 = (blockIdx.x + j * gridDim.x) * nb;
                 for (int g = 0; g < n_grp; ++g) {
@@ -822,8 +833,12 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     }
                     if (++sa == SA) { sa = 0; pa ^= 1u; }
                     if (resident) continue;
-                    for (int k = 0; k < gr.ntap; ++k) {
+                    for (int k = 0; k < gr.ntap; ++k, ++issued) {
                         const UtTap tp = s_tap[gr.tap0 + k];
+                        if (issued < pre) {   // sent before the dependency wait
+                            if (++sb == SB) { sb = 0; pb ^= 1u; }
+                            continue;
+                        }
                         mbar_wait(&b_empty[sb], pb ^ 1u);
                         if (a.dbg & 16) {
                             mbar_arrive(&b_full[sb]);
