@@ -354,12 +354,12 @@ __global__ void __launch_bounds__(256) esdf_boxes_kernel(const float* __restrict
 }
 
 // ---------------------------------------------------------------------------
-// ESDF build with exact box culling: one warp per (x, y) column, lanes along z.
-// For a column, lb_b = sqrt(ax^2 + ay^2) (same fp32 ops as the full SDF, without the z
-// term) is a lower bound of box b's distance at every node of the column (monotone
-// rounding), and equals the distance whenever it is > 0.  Boxes are visited in
-// ascending lb order and the scan stops once lb > 0 && lb >= best, which cannot change
-// the minimum: results are bit-identical to the all-boxes loop (fminf is order-free).
+// ESDF build with exact box culling: one warp per (x, y) column, lanes along z (4 nodes
+// each).  For a column, lb_b = fmaf(ax, ax, ay*ay) (the squared-distance FMA chain without
+// the z term) bounds every node's squared distance term from below (monotone rounding).
+// Boxes are visited in ascending lb order and the walk stops once lb > 0 && lb >= every
+// node's running min of the squared term, which cannot change any minimum; the sqrtf is
+// taken once per node.  Results are bit-identical to the all-boxes loop (see below).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) esdf_cull_kernel(const float* __restrict__ boxes, int n_boxes, int nx, int ny,
                                                         int nz, float ox, float oy, float oz, float h, float cap,
@@ -383,13 +383,15 @@ __global__ void __launch_bounds__(256) esdf_cull_kernel(const float* __restrict_
     for (int col = blockIdx.x * 8 + warp; col < n_col; col += gridDim.x * 8) {
         const int i = col / ny, j = col % ny;
         const float px = fmaf((float)i, h, ox), py = fmaf((float)j, h, oy);
+        // column lower bound in squared form: every node's fmaf(ax,ax, fmaf(ay,ay, az*az)) is
+        // >= fmaf(ax,ax, ay*ay) (monotone rounding), and sqrtf is monotone
         float lb = __int_as_float(0x7f800000);
         int id = lane;
         if (lane < n_boxes) {
             const float qx = fabsf(px - bc[lane][0]) - bh[lane][0];
             const float qy = fabsf(py - bc[lane][1]) - bh[lane][1];
             const float ax = fmaxf(qx, 0.f), ay = fmaxf(qy, 0.f);
-            lb = sqrtf(fmaf(ax, ax, ay * ay));
+            lb = fmaf(ax, ax, ay * ay);
         }
         // bitonic sort of (lb, id) across the warp, ascending
 #pragma unroll
@@ -420,34 +422,55 @@ __global__ void __launch_bounds__(256) esdf_cull_kernel(const float* __restrict_
         }
         __syncwarp();
         float* o = out + (size_t)p * (size_t)n_nodes + (size_t)col * nz;
-        // each lane owns 4 nodes (k = lane + 32 m) and walks the sorted boxes once for all of
-        // them; it stops when the next box's lower bound is positive and >= every node's best
-        // (evaluating a box past a node's own stop point cannot lower that node's minimum)
+        // Each lane owns 4 adjacent nodes (k = 4 lane + m).  Per box d_b = sqrtf(X_b) + min(max q, 0):
+        // a box containing the node has X_b = 0 and d_b = max q < 0, any other box has
+        // d_b = sqrtf(X_b).  So min_b d_b = min(sqrtf(min_b X_b), min of the negative max q),
+        // bit-identical to the per-box sum (sqrtf is correctly rounded and monotone, x + 0 = x),
+        // with one sqrtf per node.  The walk over the sorted boxes stops once the next box's
+        // squared xy bound is positive and >= every node's min X.
         for (int k0 = 0; k0 < nz; k0 += 128) {
-            float pz[4], best[4];
+            float pz[4], mx[4], mi[4];
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
-                pz[m] = fmaf((float)(k0 + lane + 32 * m), h, oz);
-                best[m] = cap;
+                pz[m] = fmaf((float)(k0 + 4 * lane + m), h, oz);   // 4 adjacent nodes: tight walk
+                mx[m] = __int_as_float(0x7f800000);
+                mi[m] = __int_as_float(0x7f800000);
             }
+            // z-aware bound of the lane's 4 nodes: their z distance to the box is at least
+            // |mid - cz| - hz - 1.5 h (minus slack for the rounding of the node coordinates)
+            const float pmid = fmaf((float)(k0 + 4 * lane) + 1.5f, h, oz);
+            const float zslack = fmaf(1.5f, h, 1e-5f);
             for (int e = 0; e < n_boxes; ++e) {
                 const float l = s_lb[warp][e];
-                const float bmax = fmaxf(fmaxf(best[0], best[1]), fmaxf(best[2], best[3]));
+                const float bmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
                 if (l > 0.f && l >= bmax) break;
                 const float cz = s_cz[warp][e], hz = s_hz[warp][e];
                 const float ax = s_ax[warp][e], ay = s_ay[warp][e], mq = s_mq[warp][e];
+                const float azl = fmaxf(fabsf(pmid - cz) - hz - zslack, 0.f);
+                const float lbz = fmaf(ax, ax, fmaf(ay, ay, azl * azl));
+                if (lbz > 0.f && lbz >= bmax) continue;   // cannot lower any of the 4 minima
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
                     const float qz = fabsf(pz[m] - cz) - hz;
                     const float az = fmaxf(qz, 0.f);
-                    const float outside = sqrtf(fmaf(ax, ax, fmaf(ay, ay, az * az)));
-                    const float inside = fminf(fmaxf(mq, qz), 0.f);
-                    best[m] = fminf(best[m], outside + inside);
+                    mx[m] = fminf(mx[m], fmaf(ax, ax, fmaf(ay, ay, az * az)));
+                    mi[m] = fminf(mi[m], fmaxf(mq, qz));
                 }
             }
+            float res[4];
 #pragma unroll
-            for (int m = 0; m < 4; ++m)
-                if (k0 + lane + 32 * m < nz) o[k0 + lane + 32 * m] = best[m];
+            for (int m = 0; m < 4; ++m) {
+                res[m] = fminf(cap, sqrtf(mx[m]));
+                if (mi[m] < 0.f) res[m] = fminf(res[m], mi[m]);
+            }
+            const int kk = k0 + 4 * lane;
+            if (kk + 3 < nz && (nz & 3) == 0) {
+                *reinterpret_cast<float4*>(o + kk) = make_float4(res[0], res[1], res[2], res[3]);
+            } else {
+#pragma unroll
+                for (int m = 0; m < 4; ++m)
+                    if (kk + m < nz) o[kk + m] = res[m];
+            }
         }
         __syncwarp();
     }
@@ -567,7 +590,9 @@ extern "C" int ps_esdf_build_boxes(const float* boxes, int P, int n_boxes, const
     cudaStream_t st = (cudaStream_t)stream;
     if (n_boxes <= 32) {
         const int n_col = n_h[0] * n_h[1];
-        const int blocks = std::min((n_col + 7) / 8, 4096);
+        // a few blocks per problem, each looping over many columns: the per-block box setup
+        // and launch cost are amortised (one column per warp made them dominate)
+        const int blocks = std::max(1, std::min((n_col + 7) / 8, P >= 64 ? 16 : 2048 / std::max(P, 1)));
         esdf_cull_kernel<<<dim3((unsigned)blocks, P), 256, 0, st>>>(
             boxes, n_boxes, n_h[0], n_h[1], n_h[2], origin_h[0], origin_h[1], origin_h[2], h, cap, out);
     } else if (n_h[2] % 4 == 0) {
