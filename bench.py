@@ -293,10 +293,11 @@ def main():
     s_ms = statistics.median(sample_ms)
     peaks = _peaks()
     achieved = flops / (s_ms / 1000.0) / 1e12
+    traffic, traffic_src = _traffic(n_evals, P, S, T)
     roof = {"bound": "tensor", "kernel": "ps_sample (bf16 tcgen05 U-Net, 100 steps)",
             "achieved": achieved, "peak": peaks["bf16"], "unit": "TFLOP/s",
             "frac": achieved / peaks["bf16"], "peak_source": peaks["source"],
-            "traffic": None, "sampler_ms": s_ms, "sampler_share": s_ms / ms}
+            "traffic": traffic, "traffic_source": traffic_src, "sampler_ms": s_ms, "sampler_share": s_ms / ms}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -319,6 +320,17 @@ def main():
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _traffic(n_evals, P, S, T):
+    """DRAM bytes of one sampler call: the per-forward dram__bytes_read + write of an ncu
+    --set full capture of one U-Net forward at this workload (committed under profiles/),
+    times the denoising steps.  None when no capture of this workload is committed."""
+    cands = sorted((ROOT / "profiles").glob("*_unet_traffic.json"))
+    if not cands or (P, S, T) != (1024, 32, 32):
+        return None, None
+    d = json.loads(cands[-1].read_text())
+    return d["dram_bytes_per_forward"] * n_evals, f"{cands[-1].name} x {n_evals} forwards"
 
 
 def _peaks():

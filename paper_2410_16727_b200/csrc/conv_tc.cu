@@ -551,10 +551,10 @@ static bool make_act_map(CUtensorMap* tm, const void* base, int B, int Tv, int C
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 // weights [N][Kp] bf16, box {64, N}
-static bool make_w_map(CUtensorMap* tm, const void* base, int N, int Kp) {
+static bool make_w_map(CUtensorMap* tm, const void* base, int N, int Kp, int box_rows = 0) {
     cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)N};
     cuuint64_t strides[1] = {(cuuint64_t)Kp * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)N};
+    cuuint32_t box[2] = {64, (cuuint32_t)(box_rows ? box_rows : N)};
     cuuint32_t es[2] = {1, 1};
     return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -680,9 +680,12 @@ __device__ __forceinline__ uint64_t xb_desc(const void* base, int nb) {
 }
 
 // MB = M-blocks (128 rows) per tile: every weight stage feeds MB x 4 MMAs.
-template <int N, int EPI, bool RES, int MB>
+// PAIR: CTA pairs (cluster of 2, cta_group::2): the two CTAs hold adjacent 128-row tiles
+// and HALF of every weight box each; the leader issues M=256 MMAs over both CTAs' smem
+// (half the weight bytes per SM, in shared memory traffic and in L2 reads).
+template <int N, int EPI, bool RES, int MB, bool PAIR>
 __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_constant__ UtArgs a) {
-    constexpr int B_BYTES = N * 128;
+    constexpr int B_BYTES = PAIR ? N * 64 : N * 128;   // this CTA's share of a weight stage
     constexpr int ACC1 = acc_cols<N, RES>();          // columns of one M-block
     constexpr int ACC = MB * ACC1;                     // columns of one tile
     // TMEM accumulator buffers: up to 4, so the commit -> epilogue -> release round trip of a
@@ -736,7 +739,16 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_tiles = (a.B + nb - 1) / nb;
-    const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    // tile sequence: single CTAs stride over tiles; pairs stride over tile pairs, rank r of
+    // the pair takes tile 2 * pair + r (a phantom tile past the end when n_tiles is odd:
+    // its loads are zero-filled and its stores clipped)
+    const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
+    const bool leader = crank == 0;
+    const int n_units = PAIR ? (n_tiles + 1) / 2 : n_tiles;
+    const int unit0 = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+    const int ustride = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
+    const int my_tiles = unit0 < n_units ? (n_units - 1 - unit0) / ustride + 1 : 0;
+    auto tile_of = [&](int j) { return PAIR ? 2 * (unit0 + j * ustride) + (int)crank : unit0 + j * ustride; };
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < SA; ++i) {
@@ -749,7 +761,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         }
         for (int b = 0; b < 4; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4 * NSPLIT);   // one arrival per epilogue warp
+            mbar_init(&tempty[b], (PAIR ? 2 : 1) * 4 * NSPLIT);   // one arrival per epilogue warp (both CTAs)
         }
         mbar_init(pbar, 1);
         for (int i = 0; i < 8 * UT_EPI_WG; ++i) mbar_init(&rbar[i], 1);
@@ -758,9 +770,15 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmW) : "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                     "r"(NCOLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                         "r"(NCOLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                         "r"(NCOLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     if (warp >= 2) {
         for (int i = threadIdx.x - 64; i < N; i += 128 * UT_EPI_WG) {
@@ -789,8 +807,22 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) cluster_sync_all();   // both CTAs' barriers initialised before any remote signal
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    // weight box of tap t into B stage `stage` (this CTA's half for pairs); the leader's
+    // b_full counts both halves
+    auto load_w = [&](int stage, int t) {
+        const UtTap tp = s_tap[t];
+        const CUtensorMap* tm = tp.res ? &a.tmR : &a.tmW;
+        if constexpr (PAIR) {
+            if (leader) mbar_expect_tx(&b_full[stage], (uint32_t)(2 * B_BYTES));
+            tma_load_2d_cg2(sB + (size_t)stage * B_BYTES, tm, leader_addr(&b_full[stage]), tp.kcol, (int)crank * (N / 2));
+        } else {
+            mbar_expect_tx(&b_full[stage], (uint32_t)B_BYTES);
+            tma_load_2d(sB + (size_t)stage * B_BYTES, tm, &b_full[stage], tp.kcol, 0);
+        }
+    };
     // programmatic dependent launch: the prologue above overlapped the previous layer's
     // tail.  The producer first sends the first tile's weight boxes (no kernel writes
     // weights), then every thread waits for the previous grid before touching activations,
@@ -798,11 +830,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     int pre = 0;   // weight boxes issued before the dependency wait (stages 0..pre-1)
     if (warp == 0 && lane == 0 && my_tiles > 0 && !(a.dbg & (16 | 64))) {
         pre = a.resident ? a.n_tap : (a.n_tap < SB ? a.n_tap : SB);
-        for (int t = 0; t < pre; ++t) {
-            const UtTap tp = s_tap[t];
-            mbar_expect_tx(&b_full[t], (uint32_t)B_BYTES);
-            tma_load_2d(sB + (size_t)t * B_BYTES, tp.res ? &a.tmR : &a.tmW, &b_full[t], tp.kcol, 0);
-        }
+        for (int t = 0; t < pre; ++t) load_w(t, t);
     }
     pdl_wait();
     pdl_launch_dependents();
@@ -814,19 +842,18 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             const int n_grp = a.n_grp;
             const bool resident = a.resident != 0;
             if (resident && my_tiles > 0)
-                for (int t = pre; t < a.n_tap; ++t) {   // weights loaded once, reused by every tile
-                    const UtTap tp = s_tap[t];
-                    mbar_expect_tx(&b_full[t], (uint32_t)B_BYTES);
-                    tma_load_2d(sB + (size_t)t * B_BYTES, tp.res ? &a.tmR : &a.tmW, &b_full[t], tp.kcol, 0);
-                }
+                for (int t = pre; t < a.n_tap; ++t) load_w(t, t);   // weights loaded once, reused by every tile
             int issued = 0;   // streamed weight boxes counted from the start of the kernel
             for (int j = 0; j < my_tiles; ++j) {
-                const int b0 = (blockIdx.x + j * gridDim.x) * nb;
+                const int b0 = tile_of(j) * nb;
                 for (int g = 0; g < n_grp; ++g) {
                     const UtGroup gr = s_grp[g];
                     mbar_wait(&a_empty[sa], pa ^ 1u);
                     if (a.dbg & 8) {
                         mbar_arrive(&a_full[sa]);
+                    } else if constexpr (PAIR) {   // (pairs never use the 8-channel state view)
+                        if (leader) mbar_expect_tx(&a_full[sa], (uint32_t)(2 * A_BYTES));
+                        tma_load_3d_cg2(sA + (size_t)sa * A_BYTES, &a.tmA[gr.src], leader_addr(&a_full[sa]), gr.c, b0, -2);
                     } else {
                         mbar_expect_tx(&a_full[sa], (uint32_t)(gr.xb ? (Tv + 5) * nb * 16 : A_BYTES));
                         tma_load_3d(sA + (size_t)sa * A_BYTES, &a.tmA[gr.src], &a_full[sa], gr.c, b0, -2);
@@ -843,8 +870,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                         if (a.dbg & 16) {
                             mbar_arrive(&b_full[sb]);
                         } else {
-                            mbar_expect_tx(&b_full[sb], (uint32_t)B_BYTES);
-                            tma_load_2d(sB + (size_t)sb * B_BYTES, tp.res ? &a.tmR : &a.tmW, &b_full[sb], tp.kcol, 0);
+                            load_w(sb, gr.tap0 + k);
                         }
                         if (++sb == SB) { sb = 0; pb ^= 1u; }
                     }
@@ -852,8 +878,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             }
         }
     } else if (warp == 1) {
-        {   // the whole warp runs the issue loop; elect.sync picks the issuing lane
-            constexpr uint32_t idesc = idesc_bf16(128, N);
+        if (leader) {   // the whole warp runs the issue loop; elect.sync picks the issuing lane
+            constexpr uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, N);
             int sa = 0, sb = 0;
             uint32_t pa = 0, pb = 0;
             const int n_grp = a.n_grp;
@@ -864,6 +890,14 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             const uint64_t row_step = (uint64_t)((nb * 128) >> 4);
             int buf = 0;
             uint32_t tph = 0;
+            auto mma_ = [&](uint32_t d, uint64_t da_, uint64_t db_, uint32_t id, uint32_t acc) {
+                if constexpr (PAIR) umma_bf16_w2(d, da_, db_, id, acc);
+                else umma_bf16_w(d, da_, db_, id, acc);
+            };
+            auto commit_ = [&](uint64_t* bar) {
+                if constexpr (PAIR) umma_commit_w2(bar);
+                else umma_commit_w(bar);
+            };
             for (int j = 0; j < my_tiles; ++j) {
                 mbar_wait(&tempty[buf], tph ^ 1u);
                 tc_fence_after();
@@ -891,7 +925,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                                 for (int mb = 0; mb < MB; ++mb)
                                     for (int kk = 0; kk < nk; ++kk) {
                                         const int sh = tp.res ? 0 : 2 * kk - 2;
-                                        umma_bf16_w(d_tmem + (uint32_t)(mb * ACC1),
+                                        mma_(d_tmem + (uint32_t)(mb * ACC1),
                                                   dX + (uint64_t)((((2 + sh) * nb + mb * 128) * 16) >> 4),
                                                   db + (uint64_t)(kk * 2), idesc, (tp.first && kk == 0) ? 0u : 1u);
                                     }
@@ -900,18 +934,18 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                             for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk)
-                                    umma_bf16_w(d_tmem + (uint32_t)(mb * ACC1), da + (uint64_t)(mb * 128 * 128 / 16 + kk * 2),
+                                    mma_(d_tmem + (uint32_t)(mb * ACC1), da + (uint64_t)(mb * 128 * 128 / 16 + kk * 2),
                                               db + (uint64_t)(kk * 2), idesc, (tp.first && kk == 0) ? 0u : 1u);
                         }
                         if (!resident) {
-                            umma_commit_w(&b_empty[sb]);
+                            commit_(&b_empty[sb]);
                             if (++sb == SB) { sb = 0; pb ^= 1u; }
                         }
                     }
-                    umma_commit_w(&a_empty[sa]);
+                    commit_(&a_empty[sa]);
                     if (++sa == SA) { sa = 0; pa ^= 1u; }
                 }
-                umma_commit_w(&tfull[buf]);
+                commit_(&tfull[buf]);
                 if (++buf == NBUF) { buf = 0; tph ^= 1u; }
             }
         }
@@ -979,7 +1013,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             if (lane == 0) {
                 bulk_wait_read0();   // the other buffer's store has been read out: prefetch into it
                 if (slab + 1 < n_slab) res_load(ob + 1, cur_tile, slab + 1);
-                else if (j_ + 1 < my_tiles) res_load(ob + 1, cur_tile + (int)gridDim.x, 0);
+                else if (j_ + 1 < my_tiles) res_load(ob + 1, tile_of(j_ + 1), 0);
             }
             __syncwarp();
             if (lane == 0) {
@@ -988,11 +1022,11 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             }
             ++ob;
         };
-        if (IDRES && lane == 0 && my_tiles > 0) res_load(0, blockIdx.x, 0);
+        if (IDRES && lane == 0 && my_tiles > 0) res_load(0, tile_of(0), 0);
         // NSPLIT > 1: every warpgroup drains every tile; FINAL (NSPLIT 1): warpgroups 0/1
         // alternate tiles (one per TMEM buffer -- a third waiter would alias barrier phases)
         for (int j = 0; j < my_tiles; ++j) {
-            const int tile = blockIdx.x + j * gridDim.x;
+            const int tile = tile_of(j);
             cur_tile = tile;
             const int buf = j % NBUF;
             const int b = tile * nb + sl;
@@ -1294,12 +1328,21 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[buf]);
+            if (lane == 0) {
+                if (PAIR && !leader) mbar_arrive_remote(leader_addr(&tempty[buf]));
+                else mbar_arrive(&tempty[buf]);
+            }
         }
         if (!FIN && lane == 0) bulk_wait0();   // output stores complete before the grid ends
     }
     __syncthreads();
-    if (warp == 1) {
+    if constexpr (PAIR) {
+        cluster_sync_all();   // the pair's MMAs, remote arrivals and TMA completions are done
+        if (warp == 1) {
+            tc_fence_after();
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NCOLS));
+        }
+    } else if (warp == 1) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NCOLS));
     }
@@ -1340,10 +1383,10 @@ static bool make_xb_map(CUtensorMap* tm, const void* base, int B, int Tv, int nb
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int N, int EPI, bool RES, int MB>
+template <int N, int EPI, bool RES, int MB, bool PAIR>
 static int launch_ut(UtArgs& a, cudaStream_t st) {
     const int A_BYTES = (a.Tv + 4) * a.nb * 128;
-    constexpr int B_BYTES = N * 128;
+    constexpr int B_BYTES = PAIR ? N * 64 : N * 128;
     // the kernel's shared layout (unet_tc_kernel): per-channel vectors, w_out, GN partials,
     // staged FiLM, tap tables
     constexpr int NSPLIT_ = UT_EPI_WG;
@@ -1369,7 +1412,7 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     if (a.sb_stages < 2 && !a.resident) return PS_FAIL(PS_ERR_SHAPE);
     const size_t smem = 1024 + (size_t)a.sa_stages * A_BYTES + (size_t)a.sb_stages * B_BYTES + fin +
                         (2 * (a.sa_stages + a.sb_stages) + 10 + 8 * UT_EPI_WG) * 8 + 16 + vec;
-    auto kern = unet_tc_kernel<N, EPI, RES, MB>;
+    auto kern = unet_tc_kernel<N, EPI, RES, MB, PAIR>;
     static int set_bytes = 0;
     if ((int)smem > set_bytes) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -1385,12 +1428,15 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     }
     const int n_tiles = (a.B + a.nb - 1) / a.nb;
-    const int grid = n_tiles < n_sm ? n_tiles : n_sm;
+    const int n_units = PAIR ? (n_tiles + 1) / 2 : n_tiles;
+    const int units = n_units < (PAIR ? n_sm / 2 : n_sm) ? n_units : (PAIR ? n_sm / 2 : n_sm);
+    const int grid = PAIR ? 2 * units : units;
     static const bool trace = std::getenv("PS_DEBUG") && std::atoi(std::getenv("PS_DEBUG")) >= 2;
     if (trace) std::fprintf(stderr, "[ps_b200] unet_tc N=%d EPI=%d RES=%d MB=%d B=%d Tv=%d nb=%d grid=%d groups=%d taps=%d\n",
                             N, EPI, (int)RES, MB, a.B, a.Tv, a.nb, grid, a.n_grp, a.n_tap);
     {
-        const int e_ = launch_pdl(kern, dim3(grid), dim3(UT_THREADS), smem, st, a);
+        const int e_ = PAIR ? launch_pdl_pair(kern, dim3(grid), dim3(UT_THREADS), smem, st, a)
+                            : launch_pdl(kern, dim3(grid), dim3(UT_THREADS), smem, st, a);
         if (e_) return e_;
     }
     if (trace && cudaStreamSynchronize(st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
@@ -1428,12 +1474,16 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
         if (ly.src[s] && !(s == ly.xb_src ? make_xb_map(&a.tmA[s], ly.src[s], std::max(B, nb), ly.Tv, nb)
                                           : make_ts_map(&a.tmA[s], ly.src[s], std::max(B, nb), ly.Tv, ly.ld[s], nb)))
             return PS_FAIL(PS_ERR_CUDA);
-    if (!make_w_map(&a.tmW, W + c.w_off, N, (int)kpad(c.K))) return PS_FAIL(PS_ERR_CUDA);
+    // CTA pairs for the N = 256 layers (PS_NO_PAIR=1 disables): each CTA loads half of every weight box
+    static const bool no_pair = std::getenv("PS_NO_PAIR") != nullptr;
+    const bool pair = !no_pair && N == 256 && ly.epi != EPI_FINAL;
+    if (!make_w_map(&a.tmW, W + c.w_off, N, (int)kpad(c.K), pair ? N / 2 : 0)) return PS_FAIL(PS_ERR_CUDA);
     if (ly.epi != EPI_FINAL && !make_out_map(&a.tmO, ly.out, std::max(B, nb), ly.Tv, N, nb))
         return PS_FAIL(PS_ERR_CUDA);
     if (ly.res_src && !make_out_map(&a.tmRes, const_cast<__nv_bfloat16*>(ly.res_src), std::max(B, nb), ly.Tv, N, nb))
         return PS_FAIL(PS_ERR_CUDA);
-    if (ly.res && !make_w_map(&a.tmR, W + ly.res->w_off, N, (int)kpad(ly.res->K))) return PS_FAIL(PS_ERR_CUDA);
+    if (ly.res && !make_w_map(&a.tmR, W + ly.res->w_off, N, (int)kpad(ly.res->K), pair ? N / 2 : 0))
+        return PS_FAIL(PS_ERR_CUDA);
     // group taps by the activation chunk they read: (src, channel offset)
     struct Tmp { int src, c; std::vector<UtTap> taps; };
     std::vector<Tmp> groups;
@@ -1509,18 +1559,24 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
             a.lo = step->lo;
             a.hi = step->hi;
         }
-        return launch_ut<64, EPI_FINAL, false, 1>(a, st);
+        return launch_ut<64, EPI_FINAL, false, 1, false>(a, st);
     }
-#define PS_DISPATCH(NN, MBR, MBN)                                                            \
-    if (N == NN) {                                                                           \
-        if (ly.epi == EPI_PLAIN) return launch_ut<NN, EPI_PLAIN, false, MBN>(a, st);         \
-        if (ly.epi == EPI_GN_FILM) return launch_ut<NN, EPI_GN_FILM, false, MBN>(a, st);     \
-        if (ly.res) return launch_ut<NN, EPI_GN_RES, true, MBR>(a, st);                      \
-        return launch_ut<NN, EPI_GN_RES, false, MBN>(a, st);                                 \
+#define PS_DISPATCH(NN, MBR, MBN, PR)                                                                  \
+    if (N == NN) {                                                                                     \
+        if (PR && pair) {                                                                              \
+            if (ly.epi == EPI_PLAIN) return launch_ut<NN, EPI_PLAIN, false, MBN, PR>(a, st);            \
+            if (ly.epi == EPI_GN_FILM) return launch_ut<NN, EPI_GN_FILM, false, MBN, PR>(a, st);        \
+            if (ly.res) return launch_ut<NN, EPI_GN_RES, true, MBR, PR>(a, st);                         \
+            return launch_ut<NN, EPI_GN_RES, false, MBN, PR>(a, st);                                    \
+        }                                                                                              \
+        if (ly.epi == EPI_PLAIN) return launch_ut<NN, EPI_PLAIN, false, MBN, false>(a, st);             \
+        if (ly.epi == EPI_GN_FILM) return launch_ut<NN, EPI_GN_FILM, false, MBN, false>(a, st);         \
+        if (ly.res) return launch_ut<NN, EPI_GN_RES, true, MBR, false>(a, st);                          \
+        return launch_ut<NN, EPI_GN_RES, false, MBN, false>(a, st);                                     \
     }
-    PS_DISPATCH(64, 2, 2)
-    PS_DISPATCH(128, 1, 2)
-    PS_DISPATCH(256, 1, 1)
+    PS_DISPATCH(64, 2, 2, false)
+    PS_DISPATCH(128, 1, 2, false)
+    PS_DISPATCH(256, 1, 1, true)
 #undef PS_DISPATCH
     return PS_FAIL(PS_ERR_SHAPE);
 }
