@@ -1474,9 +1474,11 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
         if (ly.src[s] && !(s == ly.xb_src ? make_xb_map(&a.tmA[s], ly.src[s], std::max(B, nb), ly.Tv, nb)
                                           : make_ts_map(&a.tmA[s], ly.src[s], std::max(B, nb), ly.Tv, ly.ld[s], nb)))
             return PS_FAIL(PS_ERR_CUDA);
-    // CTA pairs for the N = 256 layers (PS_NO_PAIR=1 disables): each CTA loads half of every weight box
+    // CTA pairs for the weight-heavy layers (K >= 1024; PS_NO_PAIR=1 disables): each CTA loads half of
+    // every weight box and the leader issues M = 256 MMAs over both CTAs
     static const bool no_pair = std::getenv("PS_NO_PAIR") != nullptr;
-    const bool pair = !no_pair && N == 256 && ly.epi != EPI_FINAL;
+    const int k_total = c.K + (ly.res ? ly.res->K : 0);
+    const bool pair = !no_pair && k_total >= 1024 && ly.epi != EPI_FINAL;   // weight-heavy layers
     if (!make_w_map(&a.tmW, W + c.w_off, N, (int)kpad(c.K), pair ? N / 2 : 0)) return PS_FAIL(PS_ERR_CUDA);
     if (ly.epi != EPI_FINAL && !make_out_map(&a.tmO, ly.out, std::max(B, nb), ly.Tv, N, nb))
         return PS_FAIL(PS_ERR_CUDA);
@@ -1574,8 +1576,8 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
         if (ly.res) return launch_ut<NN, EPI_GN_RES, true, MBR, false>(a, st);                          \
         return launch_ut<NN, EPI_GN_RES, false, MBN, false>(a, st);                                     \
     }
-    PS_DISPATCH(64, 2, 2, false)
-    PS_DISPATCH(128, 1, 2, false)
+    PS_DISPATCH(64, 2, 2, true)
+    PS_DISPATCH(128, 1, 2, true)
     PS_DISPATCH(256, 1, 1, true)
 #undef PS_DISPATCH
     return PS_FAIL(PS_ERR_SHAPE);
