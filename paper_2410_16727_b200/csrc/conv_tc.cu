@@ -1088,11 +1088,22 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
 #pragma unroll
                             for (int jj = 0; jj < 16; ++jj) v[jj] = __uint_as_float(rr[jj]);
                         }
+                        // packed: channel pairs (2c, 2c+1) share a group (CG >= 8)
+                        float2 a1[NG], a2[NG];
 #pragma unroll
-                        for (int jj = 0; jj < SC; ++jj) {
-                            const float xv = v[jj] + s_bias[cbase + cc + jj];
-                            s1[(cc + jj) / CG] += xv;
-                            s2[(cc + jj) / CG] = fmaf(xv, xv, s2[(cc + jj) / CG]);
+                        for (int g = 0; g < NG; ++g) a1[g] = a2[g] = f2(0.f, 0.f);
+#pragma unroll
+                        for (int jj = 0; jj < SC; jj += 2) {
+                            const int g = (cc + jj) / CG;
+                            const float2 bb = *reinterpret_cast<const float2*>(s_bias + cbase + cc + jj);
+                            const float2 xv = fadd2(f2(v[jj], v[jj + 1]), bb);
+                            a1[g] = fadd2(a1[g], xv);
+                            a2[g] = ffma2(xv, xv, a2[g]);
+                        }
+#pragma unroll
+                        for (int g = 0; g < NG; ++g) {
+                            s1[g] += a1[g].x + a1[g].y;
+                            s2[g] += a2[g].x + a2[g].y;
                         }
                     }
 #pragma unroll
@@ -1281,15 +1292,15 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                                 const float4 bi = *reinterpret_cast<const float4*>(s_bias + c0 + jj);
                                 const float4 ga = *reinterpret_cast<const float4*>(s_gamma + c0 + jj);
                                 const float4 be = *reinterpret_cast<const float4*>(s_beta + c0 + jj);
-                                const float bv[4] = {bi.x, bi.y, bi.z, bi.w}, gv[4] = {ga.x, ga.y, ga.z, ga.w},
-                                            ev[4] = {be.x, be.y, be.z, be.w};
-#pragma unroll
-                                for (int u = 0; u < 4; ++u) {
-                                    const bool hi = CG < 16 && (jj + u) >= CG;
-                                    const float xv = __uint_as_float(rr[jj + u]) + bv[u];
-                                    const float tt = fmaf(xv, hi ? rs2 : rs, hi ? nm2 : nm);
-                                    y[jj + u] = mish8(fmaf(tt, gv[u], ev[u]));
-                                }
+                                // packed pairs: (jj, jj+1) and (jj+2, jj+3) lie in one group each
+                                const bool hi = CG < 16 && jj >= CG;
+                                const float2 rsv = hi ? f2(rs2, rs2) : f2(rs, rs), nmv = hi ? f2(nm2, nm2) : f2(nm, nm);
+                                const float2 x0 = fadd2(f2(__uint_as_float(rr[jj]), __uint_as_float(rr[jj + 1])), f2(bi.x, bi.y));
+                                const float2 x1 = fadd2(f2(__uint_as_float(rr[jj + 2]), __uint_as_float(rr[jj + 3])), f2(bi.z, bi.w));
+                                const float2 z0 = ffma2(ffma2(x0, rsv, nmv), f2(ga.x, ga.y), f2(be.x, be.y));
+                                const float2 z1 = ffma2(ffma2(x1, rsv, nmv), f2(ga.z, ga.w), f2(be.z, be.w));
+                                const float2 y0 = mish2(z0), y1 = mish2(z1);
+                                y[jj] = y0.x; y[jj + 1] = y0.y; y[jj + 2] = y1.x; y[jj + 3] = y1.y;
                             }
                             if constexpr (EPI == EPI_GN_FILM) {
                                 if (fs1 && valid) {
@@ -1297,10 +1308,9 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                                     for (int jj = 0; jj < 16; jj += 4) {
                                         const float4 m1 = *reinterpret_cast<const float4*>(fs1 + cc + jj);
                                         const float4 sh = *reinterpret_cast<const float4*>(fsh + cc + jj);
-                                        y[jj] = fmaf(y[jj], m1.x, sh.x);
-                                        y[jj + 1] = fmaf(y[jj + 1], m1.y, sh.y);
-                                        y[jj + 2] = fmaf(y[jj + 2], m1.z, sh.z);
-                                        y[jj + 3] = fmaf(y[jj + 3], m1.w, sh.w);
+                                        const float2 u0 = ffma2(f2(y[jj], y[jj + 1]), f2(m1.x, m1.y), f2(sh.x, sh.y));
+                                        const float2 u1 = ffma2(f2(y[jj + 2], y[jj + 3]), f2(m1.z, m1.w), f2(sh.z, sh.w));
+                                        y[jj] = u0.x; y[jj + 1] = u0.y; y[jj + 2] = u1.x; y[jj + 3] = u1.y;
                                     }
                                 } else if (valid) {
                                     const float* fr = a.film + (size_t)p * 3584 + a.film_col;

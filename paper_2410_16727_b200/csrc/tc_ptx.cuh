@@ -245,6 +245,25 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 // mish(x) = x - 2x / (n^2 + 2n + 2), n = e^min(x, 15)   (8 instructions; for x > 15 the
 // correction underflows below fp32 resolution, so no branch/select is needed)
+// packed fp32 (sm_100 FFMA2 / FADD2 / FMUL2): two lanes of math per instruction
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+// mish8 on a pair (see mish8): the SFU ops stay scalar, the rest is packed
+__device__ __forceinline__ float2 mish2(float2 z) {
+    const float2 zl = fmul2(z, f2(1.4426950408889634f, 1.4426950408889634f));
+    float2 n;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(n.x) : "f"(zl.x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(n.y) : "f"(zl.y));
+    const float2 m = ffma2(n, f2(-0.5f, -0.5f), f2(-1.f, -1.f));
+    const float2 d = ffma2(n, m, f2(-1.f, -1.f));
+    float2 r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.x) : "f"(d.x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r.y) : "f"(d.y));
+    return ffma2(z, r, z);
+}
+
 __device__ __forceinline__ float mish8(float x) {
     // mish(x) = x - 2x / (n (n + 2) + 2), n = e^x, as x + x * r with r = 1 / (-d/2) = -2/d:
     // -d/2 = n * (-(n + 2)/2) - 1.  6 ops (2 on the SFU).  No clamp needed: n = inf gives
