@@ -1476,7 +1476,16 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
     const int N = c.N;
     const __nv_bfloat16* W = reinterpret_cast<const __nv_bfloat16*>(packed);
     // two M-blocks per tile where the TMEM budget still allows double buffering
-    const int MBv = (ly.epi != EPI_FINAL && (N == 64 || (N == 128 && !ly.res))) ? 2 : 1;
+    // two M-blocks per tile where the TMEM budget allows double buffering, unless the batch is
+    // too small to give every SM a tile (small batches are latency-bound: more, smaller tiles)
+    static int n_sm_rl = 0;
+    if (!n_sm_rl) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm_rl, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const bool small = (long long)B * ly.Tv < 256LL * n_sm_rl;
+    const int MBv = (!small && ly.epi != EPI_FINAL && (N == 64 || (N == 128 && !ly.res))) ? 2 : 1;
     const int nb = MBv * 128 / ly.Tv;
     for (int s = 0; s < 3; ++s)
         // maps span >= nb samples (the workspace is padded to TC_MIN_B): a TMA box larger than
@@ -1573,23 +1582,27 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
         }
         return launch_ut<64, EPI_FINAL, false, 1, false>(a, st);
     }
-#define PS_DISPATCH(NN, MBR, MBN, PR)                                                                  \
-    if (N == NN) {                                                                                     \
-        if (PR && pair) {                                                                              \
-            if (ly.epi == EPI_PLAIN) return launch_ut<NN, EPI_PLAIN, false, MBN, PR>(a, st);            \
-            if (ly.epi == EPI_GN_FILM) return launch_ut<NN, EPI_GN_FILM, false, MBN, PR>(a, st);        \
-            if (ly.res) return launch_ut<NN, EPI_GN_RES, true, MBR, PR>(a, st);                         \
-            return launch_ut<NN, EPI_GN_RES, false, MBN, PR>(a, st);                                    \
-        }                                                                                              \
-        if (ly.epi == EPI_PLAIN) return launch_ut<NN, EPI_PLAIN, false, MBN, false>(a, st);             \
-        if (ly.epi == EPI_GN_FILM) return launch_ut<NN, EPI_GN_FILM, false, MBN, false>(a, st);         \
-        if (ly.res) return launch_ut<NN, EPI_GN_RES, true, MBR, false>(a, st);                          \
-        return launch_ut<NN, EPI_GN_RES, false, MBN, false>(a, st);                                     \
+#define PS_LAUNCH4(NN, MBR, MBN, PR)                                                                   \
+    {                                                                                                  \
+        if (ly.epi == EPI_PLAIN) return launch_ut<NN, EPI_PLAIN, false, MBN, PR>(a, st);                \
+        if (ly.epi == EPI_GN_FILM) return launch_ut<NN, EPI_GN_FILM, false, MBN, PR>(a, st);            \
+        if (ly.res) return launch_ut<NN, EPI_GN_RES, true, MBR, PR>(a, st);                             \
+        return launch_ut<NN, EPI_GN_RES, false, MBN, PR>(a, st);                                        \
     }
-    PS_DISPATCH(64, 2, 2, true)
-    PS_DISPATCH(128, 1, 2, true)
-    PS_DISPATCH(256, 1, 1, true)
+#define PS_DISPATCH(NN, MBR, MBN)                                                                      \
+    if (N == NN) {                                                                                     \
+        if (MBv == 1) {                                                                                \
+            if (pair) PS_LAUNCH4(NN, 1, 1, true)                                                       \
+            PS_LAUNCH4(NN, 1, 1, false)                                                                \
+        }                                                                                              \
+        if (pair) PS_LAUNCH4(NN, MBR, MBN, true)                                                       \
+        PS_LAUNCH4(NN, MBR, MBN, false)                                                                \
+    }
+    PS_DISPATCH(64, 2, 2)
+    PS_DISPATCH(128, 1, 2)
+    PS_DISPATCH(256, 1, 1)
 #undef PS_DISPATCH
+#undef PS_LAUNCH4
     return PS_FAIL(PS_ERR_SHAPE);
 }
 
