@@ -683,8 +683,11 @@ __device__ __forceinline__ uint64_t xb_desc(const void* base, int nb) {
 // PAIR: CTA pairs (cluster of 2, cta_group::2): the two CTAs hold adjacent 128-row tiles
 // and HALF of every weight box each; the leader issues M=256 MMAs over both CTAs' smem
 // (half the weight bytes per SM, in shared memory traffic and in L2 reads).
-template <int N, int EPI, bool RES, int MB, bool PAIR>
+// SPLIT: N-split for latency-bound small batches: a work item is (tile, channel slice of N
+// = NF / SPLIT channels, whole GroupNorm groups); the template N is the slice width.
+template <int N, int EPI, bool RES, int MB, bool PAIR, int SPLIT>
 __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_constant__ UtArgs a) {
+    constexpr int NF = N * SPLIT;   // the layer's output channels
     constexpr int B_BYTES = PAIR ? N * 64 : N * 128;   // this CTA's share of a weight stage
     constexpr int ACC1 = acc_cols<N, RES>();          // columns of one M-block
     constexpr int ACC = MB * ACC1;                     // columns of one tile
@@ -697,11 +700,11 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     constexpr int PROJ_COL = NBUF * ACC;
     constexpr int NUSED = NBUF * ACC + (FIN ? 16 : 0);
     constexpr int NCOLS = NUSED <= 32 ? 32 : NUSED <= 64 ? 64 : NUSED <= 128 ? 128 : NUSED <= 256 ? 256 : 512;
-    constexpr int CG = N / 8;
+    constexpr int CG = NF / 8;   // channels per GroupNorm group (of the full layer)
     // both warpgroups drain every tile, each half of the channels / GroupNorm groups
     constexpr int NSPLIT = UT_EPI_WG;
     constexpr int NC = N / NSPLIT;
-    constexpr int NG = 8 / NSPLIT;
+    constexpr int NG = 8 / (SPLIT * NSPLIT);
     extern __shared__ __align__(1024) uint8_t smem_dyn[];
     // SW128 tiles need 1024-B alignment; offset within the shared array (keeps LDS/STS)
     uint8_t* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
@@ -728,10 +731,10 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     uint64_t* rbar = pbar + 2;                   // identity residual slabs: [epilogue warp][2]
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(rbar + 8 * UT_EPI_WG);
     float* s_bias = reinterpret_cast<float*>(tmem_holder + 4);
-    float* s_gamma = s_bias + N;
-    float* s_beta = s_gamma + N;
-    float* s_rbias = s_beta + N;
-    float* s_wout = s_rbias + N;                 // [7][64]
+    float* s_gamma = s_bias + NF;
+    float* s_beta = s_gamma + NF;
+    float* s_rbias = s_beta + NF;
+    float* s_wout = s_rbias + NF;                // [7][64]
     float* s_red = s_wout + 7 * 64;              // [2 tile parity][WG][4 quadrants][32 samples][2*NG]
     float* s_film = s_red + 2 * UT_EPI_WG * 4 * 32 * 2 * NG;  // [2 tile parity][WG][TC_FILM_P][2*NC]
     UtGroup* s_grp = reinterpret_cast<UtGroup*>(s_film + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC);
@@ -744,11 +747,16 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     // its loads are zero-filled and its stores clipped)
     const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
     const bool leader = crank == 0;
-    const int n_units = PAIR ? (n_tiles + 1) / 2 : n_tiles;
+    // work items: (tile or tile pair) x channel slice
+    const int n_units = (PAIR ? (n_tiles + 1) / 2 : n_tiles) * SPLIT;
     const int unit0 = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
     const int ustride = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
     const int my_tiles = unit0 < n_units ? (n_units - 1 - unit0) / ustride + 1 : 0;
-    auto tile_of = [&](int j) { return PAIR ? 2 * (unit0 + j * ustride) + (int)crank : unit0 + j * ustride; };
+    auto tile_of = [&](int j) {
+        const int u = (unit0 + j * ustride) / SPLIT;
+        return PAIR ? 2 * u + (int)crank : u;
+    };
+    auto slice_of = [&](int j) { return (unit0 + j * ustride) % SPLIT; };
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < SA; ++i) {
@@ -781,7 +789,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         }
     }
     if (warp >= 2) {
-        for (int i = threadIdx.x - 64; i < N; i += 128 * UT_EPI_WG) {
+        for (int i = threadIdx.x - 64; i < NF; i += 128 * UT_EPI_WG) {
             s_bias[i] = a.bias[i];
             if (EPI != EPI_PLAIN) {
                 s_gamma[i] = a.gamma[i];
@@ -812,15 +820,16 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     const uint32_t tmem_base = *tmem_holder;
     // weight box of tap t into B stage `stage` (this CTA's half for pairs); the leader's
     // b_full counts both halves
-    auto load_w = [&](int stage, int t) {
+    auto load_w = [&](int stage, int t, int slice) {
         const UtTap tp = s_tap[t];
         const CUtensorMap* tm = tp.res ? &a.tmR : &a.tmW;
         if constexpr (PAIR) {
             if (leader) mbar_expect_tx(&b_full[stage], (uint32_t)(2 * B_BYTES));
-            tma_load_2d_cg2(sB + (size_t)stage * B_BYTES, tm, leader_addr(&b_full[stage]), tp.kcol, (int)crank * (N / 2));
+            tma_load_2d_cg2(sB + (size_t)stage * B_BYTES, tm, leader_addr(&b_full[stage]), tp.kcol,
+                            slice * N + (int)crank * (N / 2));
         } else {
             mbar_expect_tx(&b_full[stage], (uint32_t)B_BYTES);
-            tma_load_2d(sB + (size_t)stage * B_BYTES, tm, &b_full[stage], tp.kcol, 0);
+            tma_load_2d(sB + (size_t)stage * B_BYTES, tm, &b_full[stage], tp.kcol, slice * N);
         }
     };
     // programmatic dependent launch: the prologue above overlapped the previous layer's
@@ -830,7 +839,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     int pre = 0;   // weight boxes issued before the dependency wait (stages 0..pre-1)
     if (warp == 0 && lane == 0 && my_tiles > 0 && !(a.dbg & (16 | 64))) {
         pre = a.resident ? a.n_tap : (a.n_tap < SB ? a.n_tap : SB);
-        for (int t = 0; t < pre; ++t) load_w(t, t);
+        for (int t = 0; t < pre; ++t) load_w(t, t, slice_of(0));
     }
     pdl_wait();
     pdl_launch_dependents();
@@ -842,7 +851,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             const int n_grp = a.n_grp;
             const bool resident = a.resident != 0;
             if (resident && my_tiles > 0)
-                for (int t = pre; t < a.n_tap; ++t) load_w(t, t);   // weights loaded once, reused by every tile
+                for (int t = pre; t < a.n_tap; ++t) load_w(t, t, 0);   // weights loaded once, reused by every tile
             int issued = 0;   // streamed weight boxes counted from the start of the kernel
             for (int j = 0; j < my_tiles; ++j) {
                 const int b0 = tile_of(j) * nb;
@@ -870,7 +879,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                         if (a.dbg & 16) {
                             mbar_arrive(&b_full[sb]);
                         } else {
-                            load_w(sb, gr.tap0 + k);
+                            load_w(sb, gr.tap0 + k, slice_of(j));
                         }
                         if (++sb == SB) { sb = 0; pb ^= 1u; }
                     }
@@ -961,9 +970,13 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         float* red = s_red + wg * (4 * 32 * 2 * NG);
         const int cbase = NSPLIT > 1 ? wg * NC : 0;   // first column of this warpgroup
         const int ew = warp - 2;                       // epilogue warp 0..4*WG-1
+        const float* s_bias_all = s_bias;
+        const float* s_gamma_all = s_gamma;
+        const float* s_beta_all = s_beta;
+        const float* s_rbias_all = s_rbias;
         const int t_w = (q * 32) / nb;                 // first time row of this warp's 32 rows
         uint32_t ob = 0;   // staging buffer counter of this warp
-        int cur_tile = 0;
+        int cur_tile = 0, cur_noff = 0;
         // 16 channels of this thread's row -> the warp's staging buffer (1 KB) -> TMA store of
         // the warp's [32 rows x 16 ch] box; lane 0 first waits until the store from the other
         // buffer has been read out, so the next slab can be written right after __syncwarp
@@ -975,7 +988,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
             if (lane == 0) {
-                tma_store_3d(&a.tmO, so, c0, cur_tile * nb, mb * (128 / nb) + t_w);
+                tma_store_3d(&a.tmO, so, c0 + cur_noff, cur_tile * nb, mb * (128 / nb) + t_w);
                 bulk_commit();
             }
             ++ob;
@@ -985,8 +998,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         // back in place, and the same buffer is TMA-stored
         constexpr bool IDRES = EPI == EPI_GN_RES && !RES;
         const int n_slab = MB * (NC / 16);
-        auto res_load = [&](uint32_t o, int tile_, int slab) {
-            const int mb_ = slab / (NC / 16), c_ = cbase + (slab % (NC / 16)) * 16;
+        auto res_load = [&](uint32_t o, int tile_, int slab, int noff_) {
+            const int mb_ = slab / (NC / 16), c_ = noff_ + cbase + (slab % (NC / 16)) * 16;
             uint64_t* bar = &rbar[ew * 2 + (o & 1u)];
             mbar_expect_tx(bar, 1024u);
             tma_load_3d(sOut + (size_t)(ew * 2 + (o & 1u)) * 1024, &a.tmRes, bar, c_, tile_ * nb,
@@ -1012,22 +1025,28 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             fence_proxy_async_smem();
             if (lane == 0) {
                 bulk_wait_read0();   // the other buffer's store has been read out: prefetch into it
-                if (slab + 1 < n_slab) res_load(ob + 1, cur_tile, slab + 1);
-                else if (j_ + 1 < my_tiles) res_load(ob + 1, tile_of(j_ + 1), 0);
+                if (slab + 1 < n_slab) res_load(ob + 1, cur_tile, slab + 1, cur_noff);
+                else if (j_ + 1 < my_tiles) res_load(ob + 1, tile_of(j_ + 1), 0, slice_of(j_ + 1) * N);
             }
             __syncwarp();
             if (lane == 0) {
-                tma_store_3d(&a.tmO, so, c0, cur_tile * nb, mb * (128 / nb) + t_w);
+                tma_store_3d(&a.tmO, so, c0 + cur_noff, cur_tile * nb, mb * (128 / nb) + t_w);
                 bulk_commit();
             }
             ++ob;
         };
-        if (IDRES && lane == 0 && my_tiles > 0) res_load(0, tile_of(0), 0);
+        if (IDRES && lane == 0 && my_tiles > 0) res_load(0, tile_of(0), 0, slice_of(0) * N);
         // NSPLIT > 1: every warpgroup drains every tile; FINAL (NSPLIT 1): warpgroups 0/1
         // alternate tiles (one per TMEM buffer -- a third waiter would alias barrier phases)
         for (int j = 0; j < my_tiles; ++j) {
             const int tile = tile_of(j);
             cur_tile = tile;
+            cur_noff = slice_of(j) * N;
+            // this item's channel slice of the per-channel vectors
+            const float* s_bias = s_bias_all + cur_noff;
+            const float* s_gamma = s_gamma_all + cur_noff;
+            const float* s_beta = s_beta_all + cur_noff;
+            const float* s_rbias = s_rbias_all + cur_noff;
             const int buf = j % NBUF;
             const int b = tile * nb + sl;
             const bool valid = b < a.B;
@@ -1133,8 +1152,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                         for (int i = r; i < n; i += 128) {
                             const int pp = i / (2 * NC), w = i % (2 * NC);
                             const int c = cbase + (w < NC ? w : w - NC);
-                            const float v = __ldg(a.film + (size_t)(p_lo + pp) * 3584 + a.film_col +
-                                                  (w < NC ? c : N + c));
+                            const float v = __ldg(a.film + (size_t)(p_lo + pp) * 3584 + a.film_col + cur_noff +
+                                                  (w < NC ? c : NF + c));
                             sf[pp * 2 * NC + w] = w < NC ? 1.f + v : v;
                         }
                         film_staged = true;
@@ -1313,10 +1332,10 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                                         y[jj] = u0.x; y[jj + 1] = u0.y; y[jj + 2] = u1.x; y[jj + 3] = u1.y;
                                     }
                                 } else if (valid) {
-                                    const float* fr = a.film + (size_t)p * 3584 + a.film_col;
+                                    const float* fr = a.film + (size_t)p * 3584 + a.film_col + cur_noff;
 #pragma unroll
                                     for (int jj = 0; jj < 16; ++jj)
-                                        y[jj] = fmaf(y[jj], 1.f + __ldg(fr + c0 + jj), __ldg(fr + N + c0 + jj));
+                                        y[jj] = fmaf(y[jj], 1.f + __ldg(fr + c0 + jj), __ldg(fr + NF + c0 + jj));
                                 }
                             } else if constexpr (RES) {
 #pragma unroll
@@ -1393,22 +1412,22 @@ static bool make_xb_map(CUtensorMap* tm, const void* base, int B, int Tv, int nb
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int N, int EPI, bool RES, int MB, bool PAIR>
+template <int N, int EPI, bool RES, int MB, bool PAIR, int SPLIT>
 static int launch_ut(UtArgs& a, cudaStream_t st) {
     const int A_BYTES = (a.Tv + 4) * a.nb * 128;
     constexpr int B_BYTES = PAIR ? N * 64 : N * 128;
     // the kernel's shared layout (unet_tc_kernel): per-channel vectors, w_out, GN partials,
     // staged FiLM, tap tables
     constexpr int NSPLIT_ = UT_EPI_WG;
-    constexpr int NG_ = 8 / NSPLIT_, NC_ = N / NSPLIT_;
-    const size_t vec = (size_t)(4 * N + 7 * 64 + 2 * UT_EPI_WG * 4 * 32 * 2 * NG_ + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
+    constexpr int NG_ = 8 / (SPLIT * NSPLIT_), NC_ = N / NSPLIT_;
+    const size_t vec = (size_t)(4 * N * SPLIT + 7 * 64 + 2 * UT_EPI_WG * 4 * 32 * 2 * NG_ + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
                        UT_MAXG * sizeof(UtGroup) + UT_MAXTAP * sizeof(UtTap) + 64;
     const size_t fin = EPI == EPI_FINAL ? 2 * 16384 + 2048 + 2 * 128 * U_DOF * 4 : (size_t)UT_EPI_WG * 2 * 4096;
     const size_t budget = 225 * 1024 - vec - 2048 - fin;
     a.sa_stages = 3 * (size_t)A_BYTES <= 110 * 1024 ? 3 : 2;
     const int sb_fit = (int)((budget - (size_t)a.sa_stages * A_BYTES) / B_BYTES);
     // small layers keep all their weights resident (one box per tap), the rest stream them
-    a.resident = a.n_tap <= std::min(sb_fit, 12) ? 1 : 0;
+    a.resident = (SPLIT == 1 && a.n_tap <= std::min(sb_fit, 12)) ? 1 : 0;   // one slice per kernel only
     static const bool no_res = std::getenv("PS_NO_RESIDENT") != nullptr;
     if (no_res) a.resident = 0;
     if (a.resident) {   // spend the smem the weight ring no longer needs on activation stages
@@ -1422,7 +1441,7 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     if (a.sb_stages < 2 && !a.resident) return PS_FAIL(PS_ERR_SHAPE);
     const size_t smem = 1024 + (size_t)a.sa_stages * A_BYTES + (size_t)a.sb_stages * B_BYTES + fin +
                         (2 * (a.sa_stages + a.sb_stages) + 10 + 8 * UT_EPI_WG) * 8 + 16 + vec;
-    auto kern = unet_tc_kernel<N, EPI, RES, MB, PAIR>;
+    auto kern = unet_tc_kernel<N, EPI, RES, MB, PAIR, SPLIT>;
     static int set_bytes = 0;
     if ((int)smem > set_bytes) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -1438,7 +1457,7 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     }
     const int n_tiles = (a.B + a.nb - 1) / a.nb;
-    const int n_units = PAIR ? (n_tiles + 1) / 2 : n_tiles;
+    const int n_units = (PAIR ? (n_tiles + 1) / 2 : n_tiles) * SPLIT;
     const int units = n_units < (PAIR ? n_sm / 2 : n_sm) ? n_units : (PAIR ? n_sm / 2 : n_sm);
     const int grid = PAIR ? 2 * units : units;
     static const bool trace = std::getenv("PS_DEBUG") && std::atoi(std::getenv("PS_DEBUG")) >= 2;
@@ -1498,12 +1517,18 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
     static const bool no_pair = std::getenv("PS_NO_PAIR") != nullptr;
     const int k_total = c.K + (ly.res ? ly.res->K : 0);
     const bool pair = !no_pair && k_total >= 1024 && ly.epi != EPI_FINAL;   // weight-heavy layers
-    if (!make_w_map(&a.tmW, W + c.w_off, N, (int)kpad(c.K), pair ? N / 2 : 0)) return PS_FAIL(PS_ERR_CUDA);
+    // small batches: N-split the N >= 128 layers into two channel slices (whole GroupNorm
+    // groups), doubling the CTAs per tile and halving each CTA's weight stream and MMA chain
+    static const bool no_split = std::getenv("PS_NO_SPLIT") != nullptr;
+    const bool tiny = 2LL * ((long long)B * ly.Tv + 127) / 128 <= n_sm_rl;   // both slices still fit on the SMs
+    const int split = (!no_split && tiny && N >= 128 && ly.epi != EPI_FINAL) ? 2 : 1;
+    const int wrows = N / split / (pair ? 2 : 1);
+    if (!make_w_map(&a.tmW, W + c.w_off, N, (int)kpad(c.K), wrows)) return PS_FAIL(PS_ERR_CUDA);
     if (ly.epi != EPI_FINAL && !make_out_map(&a.tmO, ly.out, std::max(B, nb), ly.Tv, N, nb))
         return PS_FAIL(PS_ERR_CUDA);
     if (ly.res_src && !make_out_map(&a.tmRes, const_cast<__nv_bfloat16*>(ly.res_src), std::max(B, nb), ly.Tv, N, nb))
         return PS_FAIL(PS_ERR_CUDA);
-    if (ly.res && !make_w_map(&a.tmR, W + ly.res->w_off, N, (int)kpad(ly.res->K), pair ? N / 2 : 0))
+    if (ly.res && !make_w_map(&a.tmR, W + ly.res->w_off, N, (int)kpad(ly.res->K), wrows))
         return PS_FAIL(PS_ERR_CUDA);
     // group taps by the activation chunk they read: (src, channel offset)
     struct Tmp { int src, c; std::vector<UtTap> taps; };
@@ -1580,23 +1605,27 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
             a.lo = step->lo;
             a.hi = step->hi;
         }
-        return launch_ut<64, EPI_FINAL, false, 1, false>(a, st);
+        return launch_ut<64, EPI_FINAL, false, 1, false, 1>(a, st);
     }
-#define PS_LAUNCH4(NN, MBR, MBN, PR)                                                                   \
+#define PS_LAUNCH4(NN, MBR, MBN, PR, SP)                                                               \
     {                                                                                                  \
-        if (ly.epi == EPI_PLAIN) return launch_ut<NN, EPI_PLAIN, false, MBN, PR>(a, st);                \
-        if (ly.epi == EPI_GN_FILM) return launch_ut<NN, EPI_GN_FILM, false, MBN, PR>(a, st);            \
-        if (ly.res) return launch_ut<NN, EPI_GN_RES, true, MBR, PR>(a, st);                             \
-        return launch_ut<NN, EPI_GN_RES, false, MBN, PR>(a, st);                                        \
+        if (ly.epi == EPI_PLAIN) return launch_ut<NN / SP, EPI_PLAIN, false, MBN, PR, SP>(a, st);       \
+        if (ly.epi == EPI_GN_FILM) return launch_ut<NN / SP, EPI_GN_FILM, false, MBN, PR, SP>(a, st);   \
+        if (ly.res) return launch_ut<NN / SP, EPI_GN_RES, true, MBR, PR, SP>(a, st);                    \
+        return launch_ut<NN / SP, EPI_GN_RES, false, MBN, PR, SP>(a, st);                               \
     }
 #define PS_DISPATCH(NN, MBR, MBN)                                                                      \
     if (N == NN) {                                                                                     \
         if (MBv == 1) {                                                                                \
-            if (pair) PS_LAUNCH4(NN, 1, 1, true)                                                       \
-            PS_LAUNCH4(NN, 1, 1, false)                                                                \
+            if (split == 2) {                                                                          \
+                if (pair) PS_LAUNCH4(NN, 1, 1, true, 2)                                                \
+                PS_LAUNCH4(NN, 1, 1, false, 2)                                                         \
+            }                                                                                          \
+            if (pair) PS_LAUNCH4(NN, 1, 1, true, 1)                                                    \
+            PS_LAUNCH4(NN, 1, 1, false, 1)                                                             \
         }                                                                                              \
-        if (pair) PS_LAUNCH4(NN, MBR, MBN, true)                                                       \
-        PS_LAUNCH4(NN, MBR, MBN, false)                                                                \
+        if (pair) PS_LAUNCH4(NN, MBR, MBN, true, 1)                                                    \
+        PS_LAUNCH4(NN, MBR, MBN, false, 1)                                                             \
     }
     PS_DISPATCH(64, 2, 2)
     PS_DISPATCH(128, 1, 2)
