@@ -1290,11 +1290,11 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     // no early-out on `valid`: tcgen05.ld is .sync.aligned and lanes of one warp
                     // belong to different samples, so only global accesses are predicated
                     {
-#pragma unroll 1
+#pragma unroll
                       for (int mb = 0; mb < MB; ++mb) {
                         const int grow = b * Tv + t0 + mb * tstep;
                         const uint32_t t_lane = t_lane0 + (uint32_t)(mb * ACC1);
-#pragma unroll 1
+#pragma unroll
                         for (int cc = 0; cc < NC; cc += 16) {
                             const int c0 = cbase + cc;
                             uint32_t rr[16], rq[16];
@@ -1672,7 +1672,7 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
         PS_CHECK_LAUNCH();
     }
     auto block = [&](int bi, const __nv_bfloat16* in0, int ld0, const __nv_bfloat16* in1, int ld1,
-                     __nv_bfloat16* out) -> int {
+                     __nv_bfloat16* out, __nv_bfloat16* res_tmp = nullptr) -> int {
         const PBlock& bk = L.blk[bi];
         const int Tv = T >> bk.level;
         TcLayer l0{};
@@ -1690,7 +1690,19 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
         l1.src[0] = h; l1.ld[0] = bk.c_out;
         l1.Tv = Tv;
         l1.out = out;
-        if (bk.res.K) {
+        if (bk.res.K && bk.c_out == 256 && !in1 && res_tmp) {
+            // a 256-wide residual projection would need a second 256-column accumulator (512
+            // TMEM columns, no double buffering): run it as its own 1x1 conv into a free slot
+            // and let c1 add it as an identity residual
+            TcLayer lr{};
+            lr.c = &bk.res;
+            lr.epi = EPI_PLAIN;
+            lr.src[0] = in0; lr.ld[0] = ld0;
+            lr.Tv = Tv;
+            lr.out = res_tmp;
+            PS_TRY_TC(run_layer(L, packed, lr, B, S, film, x, nullptr, nullptr, st));
+            l1.res_src = res_tmp;
+        } else if (bk.res.K) {
             l1.res = &bk.res;
             l1.res_shift = 1;
             l1.src[1] = in0; l1.ld[1] = ld0;
@@ -1716,7 +1728,7 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
     PS_TRY_TC(block(2, cur, 64, nullptr, 0, nxt));
     PS_TRY_TC(block(3, nxt, 128, nullptr, 0, skip1));
     PS_TRY_TC(plain(L.down[1], skip1, 256, T / 4, cur));          // pair view [B, T/4, 256]
-    PS_TRY_TC(block(4, cur, 128, nullptr, 0, nxt));
+    PS_TRY_TC(block(4, cur, 128, nullptr, 0, nxt, skip2));   // skip2 is free until block 5 writes it
     PS_TRY_TC(block(5, nxt, 256, nullptr, 0, skip2));
     PS_TRY_TC(block(6, skip2, 256, nullptr, 0, cur));
     PS_TRY_TC(block(7, cur, 256, nullptr, 0, nxt));
