@@ -92,7 +92,9 @@ def lib():
         path = _build.LIB
         if not path.exists():
             raise PSError(f"{path} is missing: run __graft_entry__.build() (no CPU fallback)")
-        L = ctypes.CDLL(str(path))
+        import os
+        alt = os.environ.get("PS_LIB_OVERRIDE")   # A/B timing of an alternative build (tools only)
+        L = ctypes.CDLL(alt if alt else str(path))
         for name, args in _SIGS.items():
             fn = getattr(L, name)
             fn.argtypes = args
