@@ -1093,6 +1093,10 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
 #pragma unroll
                 for (int g = 0; g < NG; ++g) s1[g] = s2[g] = 0.f;
                 constexpr int SC = NC < 32 ? NC : 32;   // stats chunk width
+                // KEEP: narrow warpgroup slices keep the biased accumulator values in registers
+                // between the statistics and the normalise pass (no second TMEM read / bias add)
+                constexpr bool KEEP = (EPI == EPI_GN_FILM || (EPI == EPI_GN_RES && !RES)) && SC == 16 && NC == 16;
+                float kv[KEEP ? MB : 1][16];
 #pragma unroll
                 for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
@@ -1116,6 +1120,10 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                             const int g = (cc + jj) / CG;
                             const float2 bb = *reinterpret_cast<const float2*>(s_bias + cbase + cc + jj);
                             const float2 xv = fadd2(f2(v[jj], v[jj + 1]), bb);
+                            if constexpr (KEEP) {
+                                kv[KEEP ? mb : 0][(jj) & 15] = xv.x;
+                                kv[KEEP ? mb : 0][(jj + 1) & 15] = xv.y;
+                            }
                             a1[g] = fadd2(a1[g], xv);
                             a2[g] = ffma2(xv, xv, a2[g]);
                         }
@@ -1298,9 +1306,11 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                         for (int cc = 0; cc < NC; cc += 16) {
                             const int c0 = cbase + cc;
                             uint32_t rr[16], rq[16];
-                            tmem_ld16(t_lane + cc, rr);
-                            if constexpr (RES) tmem_ld16(t_lane + N + cc, rq);
-                            tmem_wait_ld();
+                            if constexpr (!KEEP) {
+                                tmem_ld16(t_lane + cc, rr);
+                                if constexpr (RES) tmem_ld16(t_lane + N + cc, rq);
+                                tmem_wait_ld();
+                            }
                             const int gi = cc / CG;
                             const float rs = sel(rstd, gi), nm = sel(nmr, gi);
                             const float rs2 = CG < 16 ? sel(rstd, gi + 1) : rs;
@@ -1314,8 +1324,14 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                                 // packed pairs: (jj, jj+1) and (jj+2, jj+3) lie in one group each
                                 const bool hi = CG < 16 && jj >= CG;
                                 const float2 rsv = hi ? f2(rs2, rs2) : f2(rs, rs), nmv = hi ? f2(nm2, nm2) : f2(nm, nm);
-                                const float2 x0 = fadd2(f2(__uint_as_float(rr[jj]), __uint_as_float(rr[jj + 1])), f2(bi.x, bi.y));
-                                const float2 x1 = fadd2(f2(__uint_as_float(rr[jj + 2]), __uint_as_float(rr[jj + 3])), f2(bi.z, bi.w));
+                                float2 x0, x1;
+                                if constexpr (KEEP) {
+                                    x0 = f2(kv[KEEP ? mb : 0][jj], kv[KEEP ? mb : 0][jj + 1]);
+                                    x1 = f2(kv[KEEP ? mb : 0][jj + 2], kv[KEEP ? mb : 0][jj + 3]);
+                                } else {
+                                    x0 = fadd2(f2(__uint_as_float(rr[jj]), __uint_as_float(rr[jj + 1])), f2(bi.x, bi.y));
+                                    x1 = fadd2(f2(__uint_as_float(rr[jj + 2]), __uint_as_float(rr[jj + 3])), f2(bi.z, bi.w));
+                                }
                                 const float2 z0 = ffma2(ffma2(x0, rsv, nmv), f2(ga.x, ga.y), f2(be.x, be.y));
                                 const float2 z1 = ffma2(ffma2(x1, rsv, nmv), f2(ga.z, ga.w), f2(be.z, be.w));
                                 const float2 y0 = mish2(z0), y1 = mish2(z1);
