@@ -139,6 +139,10 @@ int ps_ref_optimize(int dtype, const void* seeds, int S, int T, int D, int n_ite
                     double armijo_c, double shrink, int max_backtracks, double alpha0, double alpha_max,
                     PS_REF_ARM_ARGS, void* x_out, void* terms, void* totals, uint8_t* frozen,
                     long long* n_accepted, void* stream);
+/* geometry.render_depth_scan / _ray_hits (src/geometry.py:279-329): first hit distance of
+ * each of the sensor's n_rays rays against circles (nc,3) and boxes (nb,4), max_range if none */
+int ps_ref_render_scan(const double* circles, int nc, const double* boxes, int nb, double px, double py,
+                       double heading, double fov, int n_rays, double max_range, double* depths, void* stream);
 /* pipeline.build_planner_esdf (src/pipeline.py:101-132): discs at the scan's hit points */
 int ps_ref_planner_esdf(const double* depths, int n_rays, double sx, double sy, double heading, double fov,
                         double max_range, double r_disc, double cap, double ox, double oy, double h, int nx,

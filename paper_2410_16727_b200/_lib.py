@@ -53,6 +53,7 @@ _SIGS = {
                        + _REF_ARM + [_vp, _vp, _vp, _vp, _vp, _vp],
     "ps_ref_planner_esdf": [_vp, _c_int, _c_d, _c_d, _c_d, _c_d, _c_d, _c_d, _c_d, _c_d, _c_d, _c_d, _c_int,
                             _c_int, _vp, _vp],
+    "ps_ref_render_scan": [_vp, _c_int, _vp, _c_int, _c_d, _c_d, _c_d, _c_d, _c_int, _c_d, _vp, _vp],
     "ps_ref_planner_success": [_vp, _c_int, _c_int, _c_int] + _REF_ARM + [_c_d, _c_d, _c_int, _vp, _vp],
     "ps_ref_select": [_vp, _vp, _c_int, _c_int, _vp, _vp],
     "ps_ref_linear": [_vp, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp],

@@ -630,6 +630,63 @@ __global__ void __launch_bounds__(32) metrics_kernel(const __grid_constant__ Arm
 }
 
 // ---------------------------------------------------------------------------
+// Observation synthesis: geometry.render_depth_scan / _ray_hits (src/geometry.py:279-329),
+// one thread per ray, the reference's expressions in the reference's order (fp64).
+// ---------------------------------------------------------------------------
+__global__ void render_scan_kernel(const double* __restrict__ circles, int nc, const double* __restrict__ boxes,
+                                   int nb, double px, double py, double heading, double fov, int n_rays,
+                                   double max_range, double* __restrict__ depths) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_rays) return;
+    // pose.ray_angles(): heading + np.linspace(-fov/2, fov/2, n_rays)
+    const double start = -fov / 2, stop = fov / 2;
+    const double step = (stop - start) / (double)(n_rays - 1);
+    const double lin = (i == n_rays - 1) ? stop : (double)i * step + start;
+    const double ang = heading + lin;
+    const double dx = cos(ang), dy = sin(ang);
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    double t_best = max_range;
+    if (nc > 0) {
+        double tmin = inf;
+        for (int k = 0; k < nc; ++k) {
+            const double mx = circles[3 * k] - px, my = circles[3 * k + 1] - py, r = circles[3 * k + 2];
+            const double b = dx * mx + dy * my;
+            const double cc = mx * mx + my * my - r * r;
+            const double disc = b * b - cc;
+            const bool ok = disc >= 0;
+            const double sq = sqrt(ok ? disc : 0.0);
+            double t1 = b - sq, t2 = b + sq;
+            t1 = (ok && t1 > 1e-12) ? t1 : inf;
+            t2 = (ok && t2 > 1e-12) ? t2 : inf;
+            tmin = fmin(tmin, fmin(t1, t2));
+        }
+        t_best = fmin(t_best, tmin);
+    }
+    if (nb > 0) {
+        double tmin = inf;
+        const bool par_x = fabs(dx) < 1e-300, par_y = fabs(dy) < 1e-300;
+        for (int k = 0; k < nb; ++k) {
+            const double* bx = boxes + 4 * k;
+            const double tx1 = (bx[0] - px) / dx, tx2 = (bx[2] - px) / dx;
+            const double ty1 = (bx[1] - py) / dy, ty2 = (bx[3] - py) / dy;
+            const bool in_x = (px >= bx[0]) && (px <= bx[2]);
+            const bool in_y = (py >= bx[1]) && (py <= bx[3]);
+            const double tx_lo = par_x ? (in_x ? -inf : inf) : fmin(tx1, tx2);
+            const double tx_hi = par_x ? (in_x ? inf : -inf) : fmax(tx1, tx2);
+            const double ty_lo = par_y ? (in_y ? -inf : inf) : fmin(ty1, ty2);
+            const double ty_hi = par_y ? (in_y ? inf : -inf) : fmax(ty1, ty2);
+            const double t_near = fmax(tx_lo, ty_lo), t_far = fmin(tx_hi, ty_hi);
+            const bool hit = t_near <= t_far;
+            double t = t_near > 1e-12 ? t_near : t_far;   // origin inside -> exit point
+            t = (hit && t > 1e-12) ? t : inf;
+            tmin = fmin(tmin, t);
+        }
+        t_best = fmin(t_best, tmin);
+    }
+    depths[i] = fmin(t_best, max_range);
+}
+
+// ---------------------------------------------------------------------------
 // scan-derived planner ESDF (src/pipeline.py:101-132; geometry.py:130-152, :270-276)
 // ---------------------------------------------------------------------------
 __global__ void planner_esdf_kernel(const double* __restrict__ depths, int n_rays, double sx, double sy,
@@ -959,6 +1016,17 @@ extern "C" int ps_ref_optimize(int dtype, const void* seeds, int S, int T, int D
         return ref_opt<float>(seeds, S, T, D, n_iters, momentum, armijo_c, shrink, max_backtracks, alpha0, alpha_max,
                               REF_ARM_PASS, x_out, terms, totals, frozen, n_accepted, st);
     return PS_FAIL(PS_ERR_SHAPE);
+}
+
+extern "C" int ps_ref_render_scan(const double* circles, int nc, const double* boxes, int nb, double px, double py,
+                                  double heading, double fov, int n_rays, double max_range, double* depths,
+                                  void* stream) {
+    if (n_rays < 2 || nc < 0 || nb < 0) return PS_FAIL(PS_ERR_SHAPE);
+    render_scan_kernel<<<(n_rays + 127) / 128, 128, 0, (cudaStream_t)stream>>>(circles, nc, boxes, nb, px, py,
+                                                                                heading, fov, n_rays, max_range,
+                                                                                depths);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
 }
 
 extern "C" int ps_ref_planner_esdf(const double* depths, int n_rays, double sx, double sy, double heading, double fov,

@@ -174,3 +174,22 @@ class World:
     @property
     def sdf_cap(self) -> float:
         return self.bounds.diagonal
+
+
+def render_depth_scan(world, pose):
+    """geometry.render_depth_scan (src/geometry.py:326-329): the sensor's fan of rays cast
+    against the world on the GPU (`ps_ref_render_scan`, fp64); depth = first hit, max_range
+    otherwise.  Accepts planseed's World / SensorPose or this module's."""
+    from .. import _lib
+    torch = _lib.require_cuda()
+    dev = lambda a, w: torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1, w)),
+                                       device="cuda")
+    circ, box = dev(world.circle_arr, 3), dev(world.box_arr, 4)
+    n = int(pose.n_rays)
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = _lib.lib().ps_ref_render_scan(_lib.ptr(circ), circ.shape[0], _lib.ptr(box), box.shape[0],
+                                       float(pose.position[0]), float(pose.position[1]), float(pose.heading),
+                                       float(pose.fov), n, float(pose.max_range), _lib.ptr(out),
+                                       _lib.stream_handle())
+    _lib.check(st, "render_depth_scan")
+    return DepthScan(pose=pose, depths=out.cpu().numpy())

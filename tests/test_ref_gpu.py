@@ -272,3 +272,22 @@ def test_metrics_retime_clearance(ref):
     _close(np.array(rt), z["motion_time"], rtol=1e-12, atol=0)
     mt, stamps = ref.trajopt.retime(arm, np.tile(np.linspace(-1, 1, 7), (32, 1)))   # constant: zero time
     assert mt == 0.0 and np.all(stamps == 0.0)
+
+
+def test_render_depth_scan(ref):
+    """geometry.render_depth_scan / _ray_hits (src/geometry.py:279-329) on the GPU against
+    planseed's depths: axis-parallel rays, origins inside a box / circle, empty world."""
+    z = np.load(GOLD / "ref_scans.npz")
+    T = ref.types
+    for wi in range(3):
+        circles, boxes = z[f"w{wi}_circles"], z[f"w{wi}_boxes"]
+        obs = [T.Circle((c[0], c[1]), c[2]) for c in circles] + [T.Box((b[0], b[1]), (b[2], b[3])) for b in boxes]
+        w = T.World(obs)
+        for pi in range(5):
+            p = z[f"pose{pi}"]
+            pose = T.SensorPose(position=(p[0], p[1]), heading=p[2], fov=p[3], n_rays=int(p[4]), max_range=p[5])
+            got = T.render_depth_scan(w, pose).depths
+            want = z[f"w{wi}_p{pi}"]
+            assert got.shape == want.shape
+            assert np.array_equal(got == pose.max_range, want == pose.max_range), (wi, pi)
+            _close(got, want, rtol=1e-12, atol=1e-12)

@@ -251,6 +251,30 @@ def gen_metrics():
                 clearance=clear, motion_time=rt)
 
 
+def gen_scans():
+    """geometry.render_depth_scan over mixed worlds and poses: axis-parallel central rays
+    (dy = 0 exactly), an origin inside a box and inside a circle, an empty world."""
+    rng = np.random.default_rng(40)
+    worlds = [World([Circle(center=(0.35, 0.2), radius=0.12), Box(lo=(0.55, -0.35), hi=(0.7, 0.1)),
+                     Circle(center=(-0.3, 0.45), radius=0.1), Box(lo=(-0.8, -0.9), hi=(-0.5, -0.6))]),
+              World([]),
+              World([Box(lo=(-0.2, -0.2), hi=(0.2, 0.2)), Circle(center=(0.6, 0.6), radius=0.3)])]
+    poses = [SensorPose(position=(-0.6, 0.2), heading=-0.15),
+             SensorPose(position=(-0.9, 0.0), heading=0.0, n_rays=257),              # central ray dy == 0
+             SensorPose(position=(0.0, 0.0), heading=np.pi / 2, n_rays=65, fov=np.pi),
+             SensorPose(position=(0.6, 0.62), heading=1.0, n_rays=33),               # inside the circle (w2)
+             SensorPose(position=(0.1, -0.1), heading=-2.5, n_rays=31, fov=1.2)]     # inside the box (w2)
+    out = {}
+    for wi, w in enumerate(worlds):
+        out[f"w{wi}_circles"] = w.circle_arr
+        out[f"w{wi}_boxes"] = w.box_arr
+        for pi, pz in enumerate(poses):
+            out[f"w{wi}_p{pi}"] = render_depth_scan(w, pz).depths
+    for pi, pz in enumerate(poses):
+        out[f"pose{pi}"] = np.array([pz.position[0], pz.position[1], pz.heading, pz.fov, pz.n_rays, pz.max_range])
+    return out
+
+
 def main(out_dir: Path = ROOT / "tests" / "golden"):
     out_dir.mkdir(parents=True, exist_ok=True)
     for name, c in gen_cost().items():
@@ -260,6 +284,7 @@ def main(out_dir: Path = ROOT / "tests" / "golden"):
     np.savez_compressed(out_dir / "ref_plan.npz", **gen_plan())
     np.savez_compressed(out_dir / "ref_guided.npz", **gen_guided())
     np.savez_compressed(out_dir / "ref_metrics.npz", **gen_metrics())
+    np.savez_compressed(out_dir / "ref_scans.npz", **gen_scans())
     return out_dir
 
 
