@@ -41,6 +41,12 @@ long long ps_launch_count(void);
 int ps_esdf_build_boxes(const float* boxes, int P, int n_boxes, const int* n_h,
                         const float* origin_h, float h, float cap, float* out, void* stream);
 
+/* Same, with a choice of layout: 0 = C order (as above), 1 = 4x4x4 bricks (64 contiguous
+ * floats per brick, bricks in C order; every extent a multiple of 4).  The planner keeps its
+ * per-problem ESDFs bricked: a refinement lookup's 8 corners share one or two cache lines. */
+int ps_esdf_build_boxes_layout(const float* boxes, int P, int n_boxes, const int* n_h,
+                               const float* origin_h, float h, float cap, float* out, int layout, void* stream);
+
 /* Batched cost and gradient (no update): cost (B,), grad (B,T,7) with row 0 zero,
  * clamped (B,) uint8.  Trajectory b reads ESDF esdf + (b / S) * esdf_stride.
  * BL analogue of _kernels.cost_terms_batch (_kernels.py:165-312). */
@@ -60,6 +66,13 @@ int ps_bl_refine(const float* q_in, int B, int T, int S, const float* esdf,
                  const float* dh_h, const float* base_h, const float* sph_h,
                  const int* sph_link_h, int n_sph, const float* weights_h, int n_iters,
                  float* q_out, float* cost, uint8_t* feasible, uint8_t* clamped, void* stream);
+
+/* ps_bl_refine over an ESDF in `layout` (see ps_esdf_build_boxes_layout); identical results. */
+int ps_bl_refine_layout(const float* q_in, int B, int T, int S, const float* esdf, long long esdf_stride,
+                        int layout, const int* n_h, const float* origin_h, float h, const float* dh_h,
+                        const float* base_h, const float* sph_h, const int* sph_link_h, int n_sph,
+                        const float* weights_h, int n_iters, float* q_out, float* cost, uint8_t* feasible,
+                        uint8_t* clamped, void* stream);
 
 /* Best seed per problem: lowest-cost feasible seed, else lowest cost; ties to the
  * lower index.  pipeline.select_best (pipeline.py:160-165).  best: (P,) int32. */

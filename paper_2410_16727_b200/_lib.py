@@ -28,6 +28,9 @@ _SIGS = {
     "ps_version": [],
     "ps_launch_count": [],
     "ps_esdf_build_boxes": [_vp, _c_int, _c_int, _vp, _vp, _c_f, _c_f, _vp, _vp],
+    "ps_esdf_build_boxes_layout": [_vp, _c_int, _c_int, _vp, _vp, _c_f, _c_f, _vp, _c_int, _vp],
+    "ps_bl_refine_layout": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _c_int, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,
+                            _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp],
     "ps_bl_cost": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,
                    _c_int, _vp, _vp, _vp, _vp, _vp],
     "ps_bl_refine": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,

@@ -52,19 +52,34 @@ def _grid_args(grid: GridSpec):
     return n, o
 
 
-def esdf_build(boxes, grid: GridSpec = GridSpec(), stream=None):
-    """boxes (P, n_boxes, 6) -> ESDF values (P, nx, ny, nz) float32 on device."""
+ESDF_C_ORDER, ESDF_BRICKED = 0, 1
+
+
+def esdf_build(boxes, grid: GridSpec = GridSpec(), stream=None, layout: int = ESDF_C_ORDER, out=None):
+    """boxes (P, n_boxes, 6) -> ESDF values (P, nx, ny, nz) float32 on device.  With
+    layout=ESDF_BRICKED the same values are stored in 4x4x4 bricks (the planner's layout;
+    see ps_esdf_build_boxes_layout) and the tensor's index order is not (x, y, z)."""
     torch = _lib.require_cuda()
     b = _dev(boxes)
     if b.dim() != 3 or b.shape[2] != 6:
         raise ValueError("boxes must be (P, n_boxes, 6)")
     P = b.shape[0]
-    out = torch.empty((P,) + tuple(grid.n), dtype=torch.float32, device="cuda")
+    if out is None:
+        out = torch.empty((P,) + tuple(grid.n), dtype=torch.float32, device="cuda")
     n, o = _grid_args(grid)
-    st = _lib.lib().ps_esdf_build_boxes(_lib.ptr(b), P, b.shape[1], _lib.hptr(n), _lib.hptr(o),
-                                        grid.h, grid.cap, _lib.ptr(out), _lib.stream_handle(stream))
+    st = _lib.lib().ps_esdf_build_boxes_layout(_lib.ptr(b), P, b.shape[1], _lib.hptr(n), _lib.hptr(o),
+                                               grid.h, grid.cap, _lib.ptr(out), int(layout),
+                                               _lib.stream_handle(stream))
     _lib.check(st, "esdf_build")
     return out
+
+
+def unbrick(esdf_bricked, grid: GridSpec = GridSpec()):
+    """(P, nx, ny, nz)-shaped bricked storage -> C-order values (test / inspection helper)."""
+    nx, ny, nz = grid.n
+    P = esdf_bricked.shape[0]
+    v = esdf_bricked.reshape(P, nx // 4, ny // 4, nz // 4, 4, 4, 4)
+    return v.permute(0, 1, 4, 2, 5, 3, 6).reshape(P, nx, ny, nz)
 
 
 def _esdf_stride(esdf, grid: GridSpec, n_problems: int) -> int:
@@ -102,7 +117,7 @@ def cost(q, esdf, S: int, robot: DHRobot, grid: GridSpec = GridSpec(), w: BLCost
 
 
 def refine(q, esdf, S: int, robot: DHRobot, grid: GridSpec = GridSpec(), w: BLCost = BLCost(),
-           n_iters: int | None = None, stream=None, out=None):
+           n_iters: int | None = None, stream=None, out=None, esdf_layout: int = ESDF_C_ORDER):
     """n_iters fixed steps + final cost, feasibility and clamped flags.
 
     Returns (q_out (B,T,7), cost (B,), feasible (B,) bool, clamped (B,) bool)."""
@@ -121,11 +136,11 @@ def refine(q, esdf, S: int, robot: DHRobot, grid: GridSpec = GridSpec(), w: BLCo
                torch.empty(B, dtype=torch.uint8, device="cuda"),
                torch.empty(B, dtype=torch.uint8, device="cuda"))
     qo, c, f, cl = out
-    st = _lib.lib().ps_bl_refine(_lib.ptr(qd), B, T, S, _lib.ptr(e), _esdf_stride(e, grid, -(-B // S)),
-                                 _lib.hptr(n), _lib.hptr(o), grid.h, _lib.hptr(rt.dh),
-                                 _lib.hptr(rt.base), _lib.hptr(rt.sph), _lib.hptr(rt.link),
-                                 len(rt.link), _lib.hptr(wts), int(n_iters), _lib.ptr(qo),
-                                 _lib.ptr(c), _lib.ptr(f), _lib.ptr(cl), _lib.stream_handle(stream))
+    st = _lib.lib().ps_bl_refine_layout(_lib.ptr(qd), B, T, S, _lib.ptr(e), _esdf_stride(e, grid, -(-B // S)),
+                                        int(esdf_layout), _lib.hptr(n), _lib.hptr(o), grid.h, _lib.hptr(rt.dh),
+                                        _lib.hptr(rt.base), _lib.hptr(rt.sph), _lib.hptr(rt.link),
+                                        len(rt.link), _lib.hptr(wts), int(n_iters), _lib.ptr(qo),
+                                        _lib.ptr(c), _lib.ptr(f), _lib.ptr(cl), _lib.stream_handle(stream))
     _lib.check(st, "bl_refine")
     return qo, c, f, cl
 

@@ -27,6 +27,7 @@ struct BLParams {
     int nx, ny, nz;
     float ox, oy, oz, inv_h;
     int B, T, S, n_iters;
+    int esdf_brick;           // ESDF layout: 0 C order, 1 4^3 bricks
     long long esdf_stride;
     const float* q_in;
     const float* esdf;
@@ -189,6 +190,7 @@ __global__ void __launch_bounds__(128) bl_refine_kernel(const __grid_constant__ 
     g.v = P.esdf + (size_t)(b / P.S) * (size_t)P.esdf_stride;
     g.nx = P.nx; g.ny = P.ny; g.nz = P.nz;
     g.ox = P.ox; g.oy = P.oy; g.oz = P.oz; g.inv_h = P.inv_h;
+    g.brick = P.esdf_brick;
 
     float q[WPL][NJ];
     const float* qb = P.q_in + (size_t)b * P.T * NJ;
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__(256) esdf_boxes_kernel(const float* __restrict
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) esdf_cull_kernel(const float* __restrict__ boxes, int n_boxes, int nx, int ny,
                                                         int nz, float ox, float oy, float oz, float h, float cap,
-                                                        float* __restrict__ out) {
+                                                        float* __restrict__ out, int brick) {
     // per warp, the column's boxes sorted by their xy lower bound, with the column-constant
     // parts of the box distance (ax, ay, max(qx, qy)) precomputed
     __shared__ float s_lb[8][32], s_cz[8][32], s_hz[8][32], s_ax[8][32], s_ay[8][32], s_mq[8][32];
@@ -464,7 +466,11 @@ __global__ void __launch_bounds__(256) esdf_cull_kernel(const float* __restrict_
                 if (mi[m] < 0.f) res[m] = fminf(res[m], mi[m]);
             }
             const int kk = k0 + 4 * lane;
-            if (kk + 3 < nz && (nz & 3) == 0) {
+            if (brick) {   // 4 nodes = one brick row (k..k+3, k % 4 == 0)
+                if (kk < nz)
+                    *reinterpret_cast<float4*>(out + (size_t)p * (size_t)n_nodes + esdf_brick_index(i, j, kk, ny, nz)) =
+                        make_float4(res[0], res[1], res[2], res[3]);
+            } else if (kk + 3 < nz && (nz & 3) == 0) {
                 *reinterpret_cast<float4*>(o + kk) = make_float4(res[0], res[1], res[2], res[3]);
             } else {
 #pragma unroll
@@ -571,19 +577,34 @@ extern "C" int ps_bl_refine(const float* q_in, int B, int T, int S, const float*
                             const int* sph_link_h, int n_sph, const float* weights_h, int n_iters,
                             float* q_out, float* cost, uint8_t* feasible, uint8_t* clamped,
                             void* stream) {
+    return ps_bl_refine_layout(q_in, B, T, S, esdf, esdf_stride, 0, n_h, origin_h, h, dh_h, base_h, sph_h,
+                               sph_link_h, n_sph, weights_h, n_iters, q_out, cost, feasible, clamped, stream);
+}
+
+extern "C" int ps_bl_refine_layout(const float* q_in, int B, int T, int S, const float* esdf,
+                                   long long esdf_stride, int layout, const int* n_h, const float* origin_h,
+                                   float h, const float* dh_h, const float* base_h, const float* sph_h,
+                                   const int* sph_link_h, int n_sph, const float* weights_h, int n_iters,
+                                   float* q_out, float* cost, uint8_t* feasible, uint8_t* clamped,
+                                   void* stream) {
     BLParams P{};
     int st = fill_params(P, B, T, S, esdf, esdf_stride, n_h, origin_h, h, dh_h, base_h, sph_h, sph_link_h,
                          n_sph, weights_h);
     if (st) return st;
+    if (layout < 0 || layout > 1 || (layout == 1 && ((n_h[0] & 3) || (n_h[1] & 3) || (n_h[2] & 3))))
+        return PS_ERR_SHAPE;
+    P.esdf_brick = layout;
     if (n_iters < 0) return PS_ERR_SHAPE;
     P.q_in = q_in; P.q_out = q_out; P.cost = cost; P.feasible = feasible; P.clamped = clamped;
     P.n_iters = n_iters;
     return launch_bl<0>(P, (cudaStream_t)stream);
 }
 
-extern "C" int ps_esdf_build_boxes(const float* boxes, int P, int n_boxes, const int* n_h,
-                                   const float* origin_h, float h, float cap, float* out, void* stream) {
-    if (P < 0 || n_boxes < 0 || n_boxes > MAX_BOXES) return PS_ERR_SHAPE;
+extern "C" int ps_esdf_build_boxes_layout(const float* boxes, int P, int n_boxes, const int* n_h,
+                                          const float* origin_h, float h, float cap, float* out, int layout,
+                                          void* stream) {
+    if (P < 0 || n_boxes < 0 || n_boxes > MAX_BOXES || layout < 0 || layout > 1) return PS_ERR_SHAPE;
+    if (layout == 1 && (n_boxes > 32 || (n_h[0] & 3) || (n_h[1] & 3) || (n_h[2] & 3))) return PS_ERR_SHAPE;
     if (P == 0) return PS_OK;
     const long long n_nodes = (long long)n_h[0] * n_h[1] * n_h[2];
     const int threads = 256;
@@ -594,7 +615,7 @@ extern "C" int ps_esdf_build_boxes(const float* boxes, int P, int n_boxes, const
         // and launch cost are amortised (one column per warp made them dominate)
         const int blocks = std::max(1, std::min((n_col + 7) / 8, P >= 64 ? 16 : 2048 / std::max(P, 1)));
         esdf_cull_kernel<<<dim3((unsigned)blocks, P), 256, 0, st>>>(
-            boxes, n_boxes, n_h[0], n_h[1], n_h[2], origin_h[0], origin_h[1], origin_h[2], h, cap, out);
+            boxes, n_boxes, n_h[0], n_h[1], n_h[2], origin_h[0], origin_h[1], origin_h[2], h, cap, out, layout);
     } else if (n_h[2] % 4 == 0) {
         const long long blocks = (n_nodes / 4 + threads - 1) / threads;
         esdf_boxes_kernel<4><<<dim3((unsigned)blocks, P), threads, 0, st>>>(
@@ -606,6 +627,11 @@ extern "C" int ps_esdf_build_boxes(const float* boxes, int P, int n_boxes, const
     }
     PS_CHECK_LAUNCH();
     return PS_OK;
+}
+
+extern "C" int ps_esdf_build_boxes(const float* boxes, int P, int n_boxes, const int* n_h,
+                                   const float* origin_h, float h, float cap, float* out, void* stream) {
+    return ps_esdf_build_boxes_layout(boxes, P, n_boxes, n_h, origin_h, h, cap, out, 0, stream);
 }
 
 extern "C" int ps_select(const float* cost, const uint8_t* feasible, int P, int S, int32_t* best,

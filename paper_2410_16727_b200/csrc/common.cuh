@@ -75,7 +75,18 @@ struct Grid {
     const float* __restrict__ v;
     int nx, ny, nz;
     float ox, oy, oz, inv_h;
+    int brick;   // 0: C order (z fastest); 1: 4x4x4 bricks (see esdf_brick_index)
 };
+
+// 4x4x4-brick layout of an (nx, ny, nz) grid with all extents multiples of 4: brick
+// (i/4, j/4, k/4) in C order, 64 contiguous floats per brick, node (i&3, j&3, k&3) at
+// 16 (i&3) + 4 (j&3) + (k&3).  A trilinear cell's 8 corners then share one or two 128-B
+// lines most of the time (C order: four lines 256 B / 64 KB apart), so a problem's ESDF
+// working set takes a fraction of the L2 lines.
+__host__ __device__ __forceinline__ size_t esdf_brick_index(int i, int j, int k, int ny, int nz) {
+    return (((size_t)(i >> 2) * (size_t)(ny >> 2) + (size_t)(j >> 2)) * (size_t)(nz >> 2) + (size_t)(k >> 2)) * 64 +
+           (size_t)((i & 3) * 16 + (j & 3) * 4 + (k & 3));
+}
 
 // Trilinear value + in-cell analytic gradient + clamp flag; generalises
 // planseed/_kernels.py:_bilinear (:23-57) to 3-D.  Manual fp32 weights, never
@@ -92,11 +103,23 @@ __device__ __forceinline__ float c_trilinear(const Grid& g, const f3& p, f3& gra
     float tx = fminf(fmaxf(ux - fi, 0.f), 1.f);
     float ty = fminf(fmaxf(uy - fj, 0.f), 1.f);
     float tz = fminf(fmaxf(uz - fk, 0.f), 1.f);
-    const size_t sy = (size_t)g.nz, sx = (size_t)g.ny * (size_t)g.nz;
-    const float* v = g.v + ((size_t)(int)fi * sx + (size_t)(int)fj * sy + (size_t)(int)fk);
-    float v000 = __ldg(v), v001 = __ldg(v + 1), v010 = __ldg(v + sy), v011 = __ldg(v + sy + 1);
-    float v100 = __ldg(v + sx), v101 = __ldg(v + sx + 1), v110 = __ldg(v + sx + sy),
-          v111 = __ldg(v + sx + sy + 1);
+    const float* v;
+    size_t sx, sy, sz;
+    if (g.brick) {   // neighbour steps stay inside a brick unless the cell sits on its edge
+        const int ii = (int)fi, jj = (int)fj, kk = (int)fk;
+        v = g.v + esdf_brick_index(ii, jj, kk, g.ny, g.nz);
+        sz = (kk & 3) == 3 ? 61 : 1;
+        sy = (jj & 3) == 3 ? (size_t)(g.nz >> 2) * 64 - 12 : 4;
+        sx = (ii & 3) == 3 ? (size_t)(g.ny >> 2) * (size_t)(g.nz >> 2) * 64 - 48 : 16;
+    } else {
+        sz = 1;
+        sy = (size_t)g.nz;
+        sx = (size_t)g.ny * (size_t)g.nz;
+        v = g.v + ((size_t)(int)fi * sx + (size_t)(int)fj * sy + (size_t)(int)fk);
+    }
+    float v000 = __ldg(v), v001 = __ldg(v + sz), v010 = __ldg(v + sy), v011 = __ldg(v + sy + sz);
+    float v100 = __ldg(v + sx), v101 = __ldg(v + sx + sz), v110 = __ldg(v + sx + sy),
+          v111 = __ldg(v + sx + sy + sz);
     float z00 = v001 - v000, z01 = v011 - v010, z10 = v101 - v100, z11 = v111 - v110;
     float c00 = fmaf(tz, z00, v000), c01 = fmaf(tz, z01, v010);
     float c10 = fmaf(tz, z10, v100), c11 = fmaf(tz, z11, v110);

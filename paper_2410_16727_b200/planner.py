@@ -17,6 +17,7 @@ hot path); inputs can be device tensors (device-resident mode) or host arrays
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -52,6 +53,10 @@ class BLPlanner:
         B = self.Pmax * self.S
         dev = "cuda"
         self.esdf = torch.empty((self.Pmax,) + tuple(grid.n), dtype=torch.float32, device=dev)
+        # per-problem ESDFs in 4^3 bricks (PS_ESDF_CORDER=1: C order): each refinement lookup's 8
+        # corners share one or two cache lines, so the 1024 ESDFs' working set fits L2 far better
+        bricks_ok = all(v % 4 == 0 for v in grid.n) and n_boxes <= 32
+        self.esdf_layout = bl.ESDF_BRICKED if bricks_ok and not os.environ.get("PS_ESDF_CORDER") else bl.ESDF_C_ORDER
         self.seeds = torch.empty((B, self.T, 7), dtype=torch.float32, device=dev)
         self.out = (torch.empty((B, self.T, 7), dtype=torch.float32, device=dev),
                     torch.empty(B, dtype=torch.float32, device=dev),
@@ -91,17 +96,12 @@ class BLPlanner:
         if events is not None:
             events["sample_end"].record()
         out = tuple(o[:B] for o in self.out)
-        bl.refine(seeds, esdf, self.S, self.robot, self.grid, self.cost, out=out)
+        bl.refine(seeds, esdf, self.S, self.robot, self.grid, self.cost, out=out, esdf_layout=self.esdf_layout)
         best = bl.select(out[1], out[2], self.S, out=self.best[:P])
         return PlanBatchResult(out[0], seeds, out[1], out[2], out[3], best)
 
     def _esdf_build(self, boxes, out):
-        n = np.array(self.grid.n, dtype=np.int32)
-        o = np.array(self.grid.origin, dtype=np.float32)
-        st = _lib.lib().ps_esdf_build_boxes(_lib.ptr(boxes), int(boxes.shape[0]), int(boxes.shape[1]),
-                                            _lib.hptr(n), _lib.hptr(o), self.grid.h, self.grid.cap,
-                                            _lib.ptr(out), _lib.stream_handle())
-        _lib.check(st, "esdf_build")
+        bl.esdf_build(boxes, self.grid, layout=self.esdf_layout, out=out)
 
     # ------------------------------------------------------------------ host
     def plan_batch(self, images, q_start, goal, boxes, p0: int = 0):
