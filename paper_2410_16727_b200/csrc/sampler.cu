@@ -284,22 +284,41 @@ __global__ void gather_kernel(const float* __restrict__ blob, const long long* _
 }
 
 // y[r, n] = act_out(bias[n] + sum_k act_in(x[r, k]) W[k, n])   (act: 0 none, 1 mish)
+// A block owns DENSE_RB rows x 128 columns: the rows' (activated) inputs are staged in smem
+// once, every W element read from L2 feeds DENSE_RB FMAs.  Same k order per output as a
+// plain loop.
+constexpr int DENSE_RB = 8;
+constexpr int DENSE_KMAX = 512;
 __global__ void dense_kernel(const float* __restrict__ x, int ldx, const float* __restrict__ W, int ldw,
                              const float* __restrict__ bias, int rows, int K, int N, int act_in, int act_out,
                              float* __restrict__ y, int ldy) {
+    __shared__ float xs[DENSE_RB][DENSE_KMAX];
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
-    const int r = blockIdx.y;
-    if (n >= N) return;
-    const float* xr = x + (size_t)r * ldx;
-    float acc = 0.f;
-    for (int k = 0; k < K; ++k) {
-        float v = xr[k];
-        if (act_in) v = mishf(v);
-        acc = fmaf(v, W[(size_t)k * ldw + n], acc);
+    const int r0 = blockIdx.y * DENSE_RB;
+    const int nr = min(DENSE_RB, rows - r0);
+    for (int i = threadIdx.x; i < nr * K; i += blockDim.x) {
+        const int rr = i / K, k = i - rr * K;
+        const float v = x[(size_t)(r0 + rr) * ldx + k];
+        xs[rr][k] = act_in ? mishf(v) : v;
     }
-    if (bias) acc += bias[n];
-    if (act_out) acc = mishf(acc);
-    y[(size_t)r * ldy + n] = acc;
+    __syncthreads();
+    if (n >= N) return;
+    float acc[DENSE_RB];
+#pragma unroll
+    for (int rr = 0; rr < DENSE_RB; ++rr) acc[rr] = 0.f;
+    for (int k = 0; k < K; ++k) {
+        const float wv = __ldg(W + (size_t)k * ldw + n);
+#pragma unroll
+        for (int rr = 0; rr < DENSE_RB; ++rr) acc[rr] = fmaf(xs[rr][k], wv, acc[rr]);
+    }
+#pragma unroll
+    for (int rr = 0; rr < DENSE_RB; ++rr) {
+        if (rr >= nr) break;
+        float v = acc[rr];
+        if (bias) v += bias[n];
+        if (act_out) v = mishf(v);
+        y[(size_t)(r0 + rr) * ldy + n] = v;
+    }
 }
 
 // sinusoid embedding of 1-based step indices (planseed/diffusion.py:228-234)
@@ -741,7 +760,7 @@ extern "C" int ps_film_problem(const void* packed, int mode, const float* cond, 
     if (P == 0) return PS_OK;
     Layout L = make_layout(mode, nullptr);
     const char* pk = reinterpret_cast<const char*>(packed);
-    dense_kernel<<<dim3((U_FILM_COLS + 127) / 128, P), 128, 0, (cudaStream_t)stream>>>(
+    dense_kernel<<<dim3((U_FILM_COLS + 127) / 128, (P + DENSE_RB - 1) / DENSE_RB), 128, 0, (cudaStream_t)stream>>>(
         cond, U_COND, L.side(pk) + L.film_wc, U_FILM_COLS, nullptr, P, U_COND, U_FILM_COLS, 1, 0, film_a,
         U_FILM_COLS);
     PS_CHECK_LAUNCH();
@@ -759,12 +778,12 @@ extern "C" int ps_film_steps(const void* packed, int mode, const int* ks_dev, in
     float* hid = sinus + (size_t)n * U_TEMB;
     float* temb = hid + (size_t)n * U_THID;
     sinusoid_kernel<<<n, 64, 0, st>>>(ks_dev, n, sinus);
-    dense_kernel<<<dim3((U_THID + 127) / 128, n), 128, 0, st>>>(sinus, U_TEMB, L.side(pk) + L.t1w, U_THID,
+    dense_kernel<<<dim3((U_THID + 127) / 128, (n + DENSE_RB - 1) / DENSE_RB), 128, 0, st>>>(sinus, U_TEMB, L.side(pk) + L.t1w, U_THID,
                                                                  L.side(pk) + L.t1b, n, U_TEMB, U_THID, 0, 1, hid,
                                                                  U_THID);
-    dense_kernel<<<dim3(1, n), 128, 0, st>>>(hid, U_THID, L.side(pk) + L.t2w, U_TEMB, L.side(pk) + L.t2b, n, U_THID,
+    dense_kernel<<<dim3(1, (n + DENSE_RB - 1) / DENSE_RB), 128, 0, st>>>(hid, U_THID, L.side(pk) + L.t2w, U_TEMB, L.side(pk) + L.t2b, n, U_THID,
                                              U_TEMB, 0, 0, temb, U_TEMB);
-    dense_kernel<<<dim3((U_FILM_COLS + 127) / 128, n), 128, 0, st>>>(
+    dense_kernel<<<dim3((U_FILM_COLS + 127) / 128, (n + DENSE_RB - 1) / DENSE_RB), 128, 0, st>>>(
         temb, U_TEMB, L.side(pk) + L.film_wt, U_FILM_COLS, L.side(pk) + L.film_b, n, U_TEMB, U_FILM_COLS, 1, 0,
         film_b, U_FILM_COLS);
     PS_CHECK_LAUNCH();
