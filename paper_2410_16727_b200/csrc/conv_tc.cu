@@ -528,7 +528,7 @@ __global__ void film_step_kernel(const float* __restrict__ fa, const float* __re
 // ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
-static bool get_encoder() {
+bool get_encoder() {
     static std::once_flag once;
     std::call_once(once, [] {
         cudaDriverEntryPointQueryResult q;
@@ -551,7 +551,7 @@ static bool make_act_map(CUtensorMap* tm, const void* base, int B, int Tv, int C
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 // weights [N][Kp] bf16, box {64, N}
-static bool make_w_map(CUtensorMap* tm, const void* base, int N, int Kp, int box_rows = 0) {
+bool make_w_map(CUtensorMap* tm, const void* base, int N, int Kp, int box_rows) {
     cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)N};
     cuuint64_t strides[1] = {(cuuint64_t)Kp * 2};
     cuuint32_t box[2] = {64, (cuuint32_t)(box_rows ? box_rows : N)};
@@ -1394,7 +1394,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
 }
 
 // activation view [B][Tv][C] bf16 read in (time, sample) order: dims (C, B, Tv), box {64, nb, Tv+4}
-static bool make_ts_map(CUtensorMap* tm, const void* base, int B, int Tv, int C, int nb) {
+bool make_ts_map(CUtensorMap* tm, const void* base, int B, int Tv, int C, int nb) {
     cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)B, (cuuint64_t)Tv};
     cuuint64_t strides[2] = {(cuuint64_t)Tv * C * 2, (cuuint64_t)C * 2};
     cuuint32_t box[3] = {64, (cuuint32_t)nb, (cuuint32_t)(Tv + 4)};
@@ -1418,7 +1418,7 @@ static bool make_out_map(CUtensorMap* tm, void* base, int B, int Tv, int N, int 
 // bf16 state view [B][Tv][8] in (time, sample) order, no swizzle: box {8, nb, Tv+5}
 // (time shifts -2..+3: the MMA pairing taps 2/3 also reads the zero-weight shift +3, whose
 // rows must be zero-filled by TMA, not stale shared memory -- NaN * 0 = NaN)
-static bool make_xb_map(CUtensorMap* tm, const void* base, int B, int Tv, int nb) {
+bool make_xb_map(CUtensorMap* tm, const void* base, int B, int Tv, int nb) {
     cuuint64_t dims[3] = {8, (cuuint64_t)B, (cuuint64_t)Tv};
     cuuint64_t strides[2] = {(cuuint64_t)Tv * 16, 16};
     cuuint32_t box[3] = {8, (cuuint32_t)nb, (cuuint32_t)(Tv + 5)};
@@ -1488,20 +1488,6 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     return PS_OK;
 }
 
-// One conv layer.  src[0..2]: activation views (bf16 [B][Tv][ld]); the main conv's
-// segments read src[seg.src], the residual 1x1 reads src[seg.src + res_shift].
-struct TcLayer {
-    const PConv* c;
-    const PConv* res;
-    int epi;
-    const __nv_bfloat16* src[3];
-    int ld[3];
-    int res_shift;
-    int Tv;
-    __nv_bfloat16* out;
-    const __nv_bfloat16* res_src;
-    int xb_src = -1;   // source index that is the 8-channel bf16 state view
-};
 
 static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int B, int S, const float* film,
                      float* x, const TcStep* step, float* eps_out, cudaStream_t st) {
@@ -1665,30 +1651,28 @@ size_t tc_workspace_bytes(int B, int T) {
         if (s_) return s_;  \
     } while (0)
 
-int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, int S, const float* film_a,
-                 const float* film_b_row, float* ws, float* eps, const TcStep* step, cudaStream_t st) {
-    if (!get_encoder()) return PS_FAIL(PS_ERR_CUDA);
-    if (L.mode != 1) return PS_FAIL(PS_ERR_SHAPE);
-    const int P = B / S;
+UnetSlots unet_slots(void* ws, int B, int T) {
     const size_t Bp = (size_t)std::max(B, TC_MIN_B);
     const size_t slot = Bp * T * 128;
-    __nv_bfloat16* a0 = reinterpret_cast<__nv_bfloat16*>(ws);
-    __nv_bfloat16* cur = a0 + Bp * T * 64;
-    __nv_bfloat16* nxt = cur + slot;
-    __nv_bfloat16* h = nxt + slot;
-    __nv_bfloat16* skip1 = h + slot;
-    __nv_bfloat16* skip2 = skip1 + slot;
-    float* film = reinterpret_cast<float*>(skip2 + slot);
-    {
-        const size_t n = (size_t)P * 3584;
-        film_step_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(film_a, film_b_row, P, film);
-        PS_CHECK_LAUNCH();
-        const size_t m = (size_t)B * T;
-        xb_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(x, m, a0);
-        PS_CHECK_LAUNCH();
-    }
+    UnetSlots u;
+    u.a0 = reinterpret_cast<__nv_bfloat16*>(ws);
+    u.cur = u.a0 + Bp * T * 64;
+    u.nxt = u.cur + slot;
+    u.h = u.nxt + slot;
+    u.skip1 = u.h + slot;
+    u.skip2 = u.skip1 + slot;
+    u.film = reinterpret_cast<float*>(u.skip2 + slot);
+    return u;
+}
+
+// The forward's 29 (30 with split_res256) layers in execution order.  split_res256: the
+// 256-wide residual projection of d2r0 runs as its own 1x1 conv into a free slot (the
+// layered kernels would otherwise need 512 TMEM columns for c1); the persistent small-batch
+// kernel keeps it fused.
+void unet_layer_list(const Layout& L, int T, const UnetSlots& u, bool split_res256, std::vector<TcLayer>& out) {
+    out.clear();
     auto block = [&](int bi, const __nv_bfloat16* in0, int ld0, const __nv_bfloat16* in1, int ld1,
-                     __nv_bfloat16* out, __nv_bfloat16* res_tmp = nullptr) -> int {
+                     __nv_bfloat16* dst, __nv_bfloat16* res_tmp = nullptr) {
         const PBlock& bk = L.blk[bi];
         const int Tv = T >> bk.level;
         TcLayer l0{};
@@ -1697,26 +1681,23 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
         l0.src[0] = in0; l0.ld[0] = ld0;
         l0.src[1] = in1; l0.ld[1] = ld1;
         l0.Tv = Tv;
-        l0.out = h;
+        l0.out = u.h;
         if (bi == 0) l0.xb_src = 0;
-        PS_TRY_TC(run_layer(L, packed, l0, B, S, film, x, nullptr, nullptr, st));
+        out.push_back(l0);
         TcLayer l1{};
         l1.c = &bk.c1;
         l1.epi = EPI_GN_RES;
-        l1.src[0] = h; l1.ld[0] = bk.c_out;
+        l1.src[0] = u.h; l1.ld[0] = bk.c_out;
         l1.Tv = Tv;
-        l1.out = out;
-        if (bk.res.K && bk.c_out == 256 && !in1 && res_tmp) {
-            // a 256-wide residual projection would need a second 256-column accumulator (512
-            // TMEM columns, no double buffering): run it as its own 1x1 conv into a free slot
-            // and let c1 add it as an identity residual
+        l1.out = dst;
+        if (bk.res.K && bk.c_out == 256 && !in1 && res_tmp && split_res256) {
             TcLayer lr{};
             lr.c = &bk.res;
             lr.epi = EPI_PLAIN;
             lr.src[0] = in0; lr.ld[0] = ld0;
             lr.Tv = Tv;
             lr.out = res_tmp;
-            PS_TRY_TC(run_layer(L, packed, lr, B, S, film, x, nullptr, nullptr, st));
+            out.push_back(lr);
             l1.res_src = res_tmp;
         } else if (bk.res.K) {
             l1.res = &bk.res;
@@ -1727,39 +1708,66 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
         } else {
             l1.res_src = in0;
         }
-        return run_layer(L, packed, l1, B, S, film, x, nullptr, nullptr, st);
+        out.push_back(l1);
     };
-    auto plain = [&](const PConv& c, const __nv_bfloat16* in, int ld, int Tv, __nv_bfloat16* out) -> int {
+    auto plain = [&](const PConv& c, const __nv_bfloat16* in, int ld, int Tv, __nv_bfloat16* dst) {
         TcLayer l{};
         l.c = &c;
         l.epi = EPI_PLAIN;
         l.src[0] = in; l.ld[0] = ld;
         l.Tv = Tv;
-        l.out = out;
-        return run_layer(L, packed, l, B, S, film, x, nullptr, nullptr, st);
+        l.out = dst;
+        out.push_back(l);
     };
-    PS_TRY_TC(block(0, a0, 64, nullptr, 0, cur));
-    PS_TRY_TC(block(1, cur, 64, nullptr, 0, nxt));
-    PS_TRY_TC(plain(L.down[0], nxt, 128, T / 2, cur));            // pair view [B, T/2, 128]
-    PS_TRY_TC(block(2, cur, 64, nullptr, 0, nxt));
-    PS_TRY_TC(block(3, nxt, 128, nullptr, 0, skip1));
-    PS_TRY_TC(plain(L.down[1], skip1, 256, T / 4, cur));          // pair view [B, T/4, 256]
-    PS_TRY_TC(block(4, cur, 128, nullptr, 0, nxt, skip2));   // skip2 is free until block 5 writes it
-    PS_TRY_TC(block(5, nxt, 256, nullptr, 0, skip2));
-    PS_TRY_TC(block(6, skip2, 256, nullptr, 0, cur));
-    PS_TRY_TC(block(7, cur, 256, nullptr, 0, nxt));
-    PS_TRY_TC(block(8, nxt, 256, skip2, 256, cur));
-    PS_TRY_TC(block(9, cur, 128, nullptr, 0, nxt));
-    PS_TRY_TC(plain(L.up[0], nxt, 128, T / 4, cur));              // writes pair view [B, T/4, 256]
-    PS_TRY_TC(block(10, cur, 128, skip1, 128, nxt));
-    PS_TRY_TC(block(11, nxt, 64, nullptr, 0, cur));
-    PS_TRY_TC(plain(L.up[1], cur, 64, T / 2, nxt));               // writes pair view [B, T/2, 128]
+    block(0, u.a0, 64, nullptr, 0, u.cur);
+    block(1, u.cur, 64, nullptr, 0, u.nxt);
+    plain(L.down[0], u.nxt, 128, T / 2, u.cur);            // pair view [B, T/2, 128]
+    block(2, u.cur, 64, nullptr, 0, u.nxt);
+    block(3, u.nxt, 128, nullptr, 0, u.skip1);
+    plain(L.down[1], u.skip1, 256, T / 4, u.cur);          // pair view [B, T/4, 256]
+    block(4, u.cur, 128, nullptr, 0, u.nxt, u.skip2);   // skip2 is free until block 5 writes it
+    block(5, u.nxt, 256, nullptr, 0, u.skip2);
+    block(6, u.skip2, 256, nullptr, 0, u.cur);
+    block(7, u.cur, 256, nullptr, 0, u.nxt);
+    block(8, u.nxt, 256, u.skip2, 256, u.cur);
+    block(9, u.cur, 128, nullptr, 0, u.nxt);
+    plain(L.up[0], u.nxt, 128, T / 4, u.cur);              // writes pair view [B, T/4, 256]
+    block(10, u.cur, 128, u.skip1, 128, u.nxt);
+    block(11, u.nxt, 64, nullptr, 0, u.cur);
+    plain(L.up[1], u.cur, 64, T / 2, u.nxt);               // writes pair view [B, T/2, 128]
     TcLayer lf{};
     lf.c = &L.fin;
     lf.epi = EPI_FINAL;
-    lf.src[0] = nxt; lf.ld[0] = 64;
+    lf.src[0] = u.nxt; lf.ld[0] = 64;
     lf.Tv = T;
-    return run_layer(L, packed, lf, B, S, film, x, step, step ? nullptr : eps, st);
+    out.push_back(lf);
+}
+
+int tc_xb(const float* x, size_t rows, __nv_bfloat16* xb, cudaStream_t st) {
+    xb_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(x, rows, xb);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, int S, const float* film_a,
+                 const float* film_b_row, float* ws, float* eps, const TcStep* step, cudaStream_t st) {
+    if (!get_encoder()) return PS_FAIL(PS_ERR_CUDA);
+    if (L.mode != 1) return PS_FAIL(PS_ERR_SHAPE);
+    const int P = B / S;
+    const UnetSlots u = unet_slots(ws, B, T);
+    {
+        const size_t n = (size_t)P * 3584;
+        film_step_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(film_a, film_b_row, P, u.film);
+        PS_CHECK_LAUNCH();
+        PS_TRY_TC(tc_xb(x, (size_t)B * T, u.a0, st));
+    }
+    std::vector<TcLayer> layers;
+    unet_layer_list(L, T, u, true, layers);
+    for (const TcLayer& ly : layers) {
+        const bool fin = ly.epi == EPI_FINAL;
+        PS_TRY_TC(run_layer(L, packed, ly, B, S, u.film, x, fin ? step : nullptr, fin && !step ? eps : nullptr, st));
+    }
+    return PS_OK;
 }
 
 // ===========================================================================

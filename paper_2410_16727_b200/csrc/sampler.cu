@@ -805,6 +805,12 @@ extern "C" int ps_unet_forward(const void* packed, int mode, const float* x, int
     PS_TRY(ps_film_steps(packed, mode, dk, 1, scratch, film_b, stream));
     if (mode == 0)
         return unet_eval_f32(L, reinterpret_cast<const char*>(packed), x, B, T, S, film_a, film_b, act, eps, st);
+    if (unet_persist_eligible(B, T)) {
+        const StepCoef sc{};
+        PS_TRY(unet_persist_prepare(L, reinterpret_cast<const char*>(packed), act, B, T, &sc, 1));
+        return unet_persist_launch(L, reinterpret_cast<const char*>(packed), act, const_cast<float*>(x), B, T, S, 0, 0u,
+                                   film_a, film_b, 1, nullptr, nullptr, 0.f, 0.f, eps, st);
+    }
     return unet_eval_tc(L, reinterpret_cast<const char*>(packed), const_cast<float*>(x), B, T, S, film_a, film_b, act, eps, nullptr,
                         st);
 }
@@ -820,6 +826,34 @@ extern "C" int ps_noise_probe(float* out, int n, int step, int prob, int seed, u
 // ddpm=1 runs the stochastic posterior update between consecutive indices k -> k-1
 // (requires the full K..1 list), ddpm=0 the deterministic DDIM update (eta = 0).
 // coef_h: 6 x (K+1) float32 tables (sq, sq1m, rsq, c0, c1, sig) from spec.sampler_tables.
+// per-step coefficients of the denoising loop (steps_h: 1-based indices, descending)
+static void step_coefs(const float* coef_h, int K, const int* steps_h, int n_steps, int ddpm, std::vector<StepCoef>& out) {
+    const float* sq = coef_h;
+    const float* sq1m = coef_h + (K + 1);
+    const float* rsq = coef_h + 2 * (K + 1);
+    const float* c0 = coef_h + 3 * (K + 1);
+    const float* c1 = coef_h + 4 * (K + 1);
+    const float* sig = coef_h + 5 * (K + 1);
+    out.assign(n_steps, StepCoef{});
+    for (int i = 0; i < n_steps; ++i) {
+        const int k = steps_h[i];
+        StepCoef& sc = out[i];
+        sc.k = k;
+        sc.sq1m = sq1m[k];
+        sc.rsq = rsq[k];
+        sc.last = (i + 1 == n_steps);
+        sc.ddpm = ddpm;
+        if (ddpm) {
+            sc.c0 = c0[k];
+            sc.c1 = c1[k];
+            sc.sig = sig[k];
+        } else if (!sc.last) {
+            sc.sqn = sq[steps_h[i + 1]];
+            sc.sq1mn = sq1m[steps_h[i + 1]];
+        }
+    }
+}
+
 // ---- graph cache of the denoising loop
 static uint64_t hash_bytes(const void* p, size_t n) {
     const unsigned char* c = static_cast<const unsigned char*>(p);
@@ -829,7 +863,7 @@ static uint64_t hash_bytes(const void* p, size_t n) {
 }
 struct SampleKey {
     const void* packed; const float* film_a; const float* q_start; void* ws; float* traj;
-    int mode, P, S, T, p0, n_steps, ddpm, K;
+    int mode, P, S, T, p0, n_steps, ddpm, K, persist;
     unsigned noise_key;
     float lo, hi;
     cudaStream_t stream;
@@ -837,7 +871,7 @@ struct SampleKey {
     bool operator==(const SampleKey& o) const {
         return packed == o.packed && film_a == o.film_a && q_start == o.q_start && ws == o.ws && traj == o.traj &&
                mode == o.mode && P == o.P && S == o.S && T == o.T && p0 == o.p0 && n_steps == o.n_steps &&
-               ddpm == o.ddpm && K == o.K && noise_key == o.noise_key && lo == o.lo && hi == o.hi &&
+               ddpm == o.ddpm && K == o.K && persist == o.persist && noise_key == o.noise_key && lo == o.lo && hi == o.hi &&
                stream == o.stream && steps_hash == o.steps_hash && coef_hash == o.coef_hash;
     }
 };
@@ -891,13 +925,18 @@ extern "C" int ps_sample(const void* packed, int mode, const float* film_a, int 
         return PS_FAIL(PS_ERR_CUDA);
     PS_TRY(ps_film_steps(packed, mode, dks, n_steps, scratch, film_b, stream));
     const size_t n = (size_t)B * T * U_DOF;
+    if (mode == 1 && unet_persist_eligible(B, T)) {
+        std::vector<StepCoef> scs;
+        step_coefs(coef_h, K, steps_h, n_steps, ddpm, scs);
+        PS_TRY(unet_persist_prepare(L, reinterpret_cast<const char*>(packed), act, B, T, scs.data(), n_steps));
+    }
     // The denoising loop (noise init + n_steps x ~31 launches) is captured once into a CUDA
     // graph and replayed while every argument that shapes it is unchanged: at small batch the
     // host cost of building ~31 launches per step (tensor maps, argument blocks) dominates.
     SampleKey key{};
     key.packed = packed; key.film_a = film_a; key.q_start = q_start; key.ws = ws; key.traj = traj;
     key.mode = mode; key.P = P; key.S = S; key.T = T; key.p0 = p0; key.n_steps = n_steps; key.ddpm = ddpm;
-    key.K = K; key.noise_key = noise_key; key.lo = lo; key.hi = hi; key.stream = st;
+    key.K = K; key.persist = mode == 1 && unet_persist_eligible(B, T); key.noise_key = noise_key; key.lo = lo; key.hi = hi; key.stream = st;
     key.steps_hash = hash_bytes(steps_h, (size_t)n_steps * sizeof(int));
     key.coef_hash = hash_bytes(coef_h, (size_t)6 * (K + 1) * sizeof(float));
     static const bool use_graph = std::getenv("PS_NO_GRAPH") == nullptr;
@@ -954,29 +993,14 @@ static int sample_loop(const void* packed, int mode, const float* film_a, const 
     Layout L = make_layout(mode, nullptr);
     noise_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, B, T, S, p0, noise_key);
     PS_CHECK_LAUNCH();
-    const float* sq = coef_h;
-    const float* sq1m = coef_h + (K + 1);
-    const float* rsq = coef_h + 2 * (K + 1);
-    const float* c0 = coef_h + 3 * (K + 1);
-    const float* c1 = coef_h + 4 * (K + 1);
-    const float* sig = coef_h + 5 * (K + 1);
     const char* pk = reinterpret_cast<const char*>(packed);
+    if (mode == 1 && unet_persist_eligible(B, T))   // one persistent launch for every step
+        return unet_persist_launch(L, pk, act, x, B, T, S, p0, noise_key, film_a, film_b, n_steps, q_start, traj, lo,
+                                   hi, nullptr, st);
+    std::vector<StepCoef> scs;
+    step_coefs(coef_h, K, steps_h, n_steps, ddpm, scs);
     for (int i = 0; i < n_steps; ++i) {
-        const int k = steps_h[i];
-        StepCoef sc{};
-        sc.k = k;
-        sc.sq1m = sq1m[k];
-        sc.rsq = rsq[k];
-        sc.last = (i + 1 == n_steps);
-        sc.ddpm = ddpm;
-        if (ddpm) {
-            sc.c0 = c0[k];
-            sc.c1 = c1[k];
-            sc.sig = sig[k];
-        } else if (!sc.last) {
-            sc.sqn = sq[steps_h[i + 1]];
-            sc.sq1mn = sq1m[steps_h[i + 1]];
-        }
+        const StepCoef& sc = scs[i];
         const float* fb = film_b + (size_t)i * U_FILM_COLS;
         if (mode == 0) {
             PS_TRY(unet_eval_f32(L, pk, x, B, T, S, film_a, fb, act, eps, st));

@@ -2,7 +2,10 @@
 #pragma once
 #include <cuda_bf16.h>
 
+#include <cuda.h>
+
 #include <functional>
+#include <vector>
 
 #include "unet_arch.h"
 
@@ -45,6 +48,44 @@ struct TcStep {
     float* traj;
     float lo, hi;
 };
+
+// One conv layer of the tcgen05 U-Net.  src[0..2]: activation views (bf16 [B][Tv][ld]); the
+// main conv's segments read src[seg.src], the residual 1x1 reads src[seg.src + res_shift].
+struct TcLayer {
+    const PConv* c;
+    const PConv* res;
+    int epi;
+    const __nv_bfloat16* src[3];
+    int ld[3];
+    int res_shift;
+    int Tv;
+    __nv_bfloat16* out;
+    const __nv_bfloat16* res_src;
+    int xb_src = -1;   // source index that is the 8-channel bf16 state view
+};
+
+// activation slots of the tcgen05 workspace (tc_workspace_bytes)
+struct UnetSlots {
+    __nv_bfloat16 *a0, *cur, *nxt, *h, *skip1, *skip2;
+    float* film;
+};
+UnetSlots unet_slots(void* ws, int B, int T);
+void unet_layer_list(const Layout& L, int T, const UnetSlots& u, bool split_res256, std::vector<TcLayer>& out);
+int tc_xb(const float* x, size_t rows, __nv_bfloat16* xb, cudaStream_t st);
+
+// tensor maps (conv_tc.cu)
+bool get_encoder();
+bool make_ts_map(CUtensorMap* tm, const void* base, int B, int Tv, int C, int nb);
+bool make_xb_map(CUtensorMap* tm, const void* base, int B, int Tv, int nb);
+bool make_w_map(CUtensorMap* tm, const void* base, int N, int Kp, int box_rows = 0);
+
+// persistent small-batch sampler (unet_small.cu)
+bool unet_persist_eligible(int B, int T);
+int unet_persist_prepare(const Layout& L, const char* packed, void* ws, int B, int T, const StepCoef* sc_h,
+                         int n_steps);
+int unet_persist_launch(const Layout& L, const char* packed, void* ws, float* x, int B, int T, int S, int p0,
+                        unsigned key, const float* film_a, const float* film_b, int n_steps, const float* q_start,
+                        float* traj, float lo, float hi, float* eps_out, cudaStream_t st);
 
 size_t tc_workspace_bytes(int B, int T);
 int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, int S, const float* film_a,

@@ -1,0 +1,999 @@
+// Persistent small-batch U-Net sampler (north star "at small batch it
+// becomes a persistent fused per-step kernel"): ONE launch runs every denoising step of
+// ps_sample -- all 28 conv layers of every step plus the fused DDPM posterior -- for batches
+// whose layers cannot fill the GPU with the layered kernels (conv_tc.cu), where each layer's
+// launch / fill / drain latency (~7 us) is most of its time.
+//
+// Work: a unit is (128-row tile in (time, sample) order, output-channel slice of whole
+// GroupNorm groups: 16 channels, 32 for the 256-wide layers, all 64 for the final layer).
+// CTA c owns units c, c + grid, ... of every layer.  Roles per CTA (256 threads):
+//   warp 0  weight producer: streams the unit's weight slice ([ns x 64] TMA boxes, packed
+//           8 KB per ring stage) and runs ahead across units and layers -- weights do not
+//           depend on activations, so the next layer's slice arrives while this layer computes;
+//   warp 1  MMA issuer (tcgen05, M = 128, N = ns, TMEM accumulators double-buffered);
+//   warp 2  activation producer: waits until every unit of the previous layer has published
+//           (a monotone completion counter in global memory, acquire), then TMA-loads the
+//           tile's 64-channel chunks with the conv halo (tap shifts are descriptor row shifts,
+//           as in conv_tc.cu);
+//   warps 4-7 epilogue: bias, GroupNorm (per-sample statistics over the tile's rows),
+//           Mish, FiLM (per-problem + per-step parts added on the fly), residual (second
+//           accumulator or the block input), bf16 store; the final layer adds the 64 -> 7
+//           projection, x0 clip, DDPM posterior + Philox noise (or DDIM / denormalise), and
+//           writes the next step's bf16 state view.  One release-add per unit publishes it.
+// Every layer waits for the whole previous layer, so the buffer reuse of the layered
+// forward (unet_layer_list) stays race-free.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "sampler.cuh"
+#include "tc_ptx.cuh"
+
+namespace ps {
+
+constexpr int US_MAXG = 24;
+constexpr int US_MAXT = 64;
+constexpr int US_MAXL = 32;
+constexpr int US_THREADS = 256;
+constexpr int US_SA = 4;             // activation stages (a multiple of US_AB)
+constexpr int US_A_BYTES = 24576;    // >= (Tv + 4) * nb * 128 for every layer (T = 32, 64)
+constexpr int US_SB = 12;            // weight stages (a multiple of US_BB)
+constexpr int US_B_BYTES = 8192;     // 64 / ns tap boxes of [ns x 64] bf16 per stage
+// stages are released in batches (one tcgen05.commit per batch): the tensor pipe processes
+// commits one after another at ~0.25 us each, which dominated small units' MMA phase
+constexpr int US_AB = 2;             // activation stages per release batch
+constexpr int US_BB = 4;             // weight stages per release batch
+constexpr int US_RED = 2 * 4 * 16 * 16;   // GN partials [unit parity][warp][sample][2 * groups]
+
+struct UsGroup {
+    int16_t c;      // channel offset in the source view
+    int8_t src;     // activation map
+    int8_t ntap;    // taps reading this chunk
+    int16_t tap0;   // first tap
+    int8_t xb;      // 8-channel bf16 state view (no swizzle)
+    int8_t pad;
+};
+struct UsTap {
+    int16_t kcol;   // weight K column
+    int16_t aoff;   // A descriptor offset of the time shift: (2 + dt) * nb * 128 B, in 16-B units
+    int8_t dt;      // time shift
+    int8_t res;     // residual accumulator
+    int8_t first;   // first MMA into its accumulator
+    int8_t pad;
+};
+
+// per-layer tensor maps (global memory; TMA reads them through its own descriptor cache)
+struct __align__(64) UsMaps {
+    CUtensorMap tmA[3];
+    CUtensorMap tmW;
+    CUtensorMap tmR;
+};
+// per-layer scalars; copied to shared memory with the group / tap tables at kernel start
+// (with ~220 KB of shared memory in use the L1 holds little, and every table read from L2
+// would cost ~0.5 us on the critical path)
+struct UsHdr {
+    int n_grp, n_tap, grp0, tap0;   // tables: entries [grp0, grp0 + n_grp) / [tap0, tap0 + n_tap)
+    int epi, res, N, ns, n_slices, Tv, nb, units, film_col, pad_;
+    const float* bias;
+    const float* gamma;
+    const float* beta;
+    const float* rbias;
+    const __nv_bfloat16* res_src;   // identity residual [B][Tv][N]
+    __nv_bfloat16* out;             // [B][Tv][N]
+};
+// per-unit parameters staged by the prefetch warp: bias / gamma / beta / rbias slices, the
+// tile's FiLM rows as (1 + scale, shift), and the step's coefficients
+constexpr int US_FILM_P = 16;                         // problems per tile (nb <= 16)
+constexpr int US_VEC_FILM = 256;
+constexpr int US_VEC_SC = US_VEC_FILM + US_FILM_P * 64;
+constexpr int US_VEC = US_VEC_SC + 16;
+
+struct UsArgs {
+    const UsMaps* maps;
+    const UsHdr* hdr;
+    const UsGroup* grp;
+    const UsTap* tap;
+    int n_layers, n_grp_all, n_tap_all;
+    int B, T, S, p0;
+    unsigned key;
+    int n_steps;
+    const StepCoef* sc;     // [n_steps]
+    const float* film_a;    // [P][3584] per-problem FiLM part
+    const float* film_b;    // [n_steps][3584] per-step part
+    float* x;               // fp32 state [B][T][7]
+    __nv_bfloat16* xb;      // its bf16 view [B][T][8]
+    const float* wout;      // [7][64]
+    const float* bout;
+    const float* q_start;
+    float* traj;
+    float lo, hi;
+    float* eps_out;         // forward-only: write eps, no update
+    unsigned* done;         // units published since launch (zeroed before the launch)
+    int dbg;
+    unsigned long long* trace;   // debug (PS_PERSIST_TRACE): [cta][unit][8] globaltimer stamps + MMA-warp cycle counters
+    int trace_cap;               // units per CTA in the trace
+};
+
+__device__ __forceinline__ void us_stamp(const UsArgs& a, int j, int ev) {
+    if (a.trace && j < a.trace_cap) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[((size_t)blockIdx.x * a.trace_cap + j) * 20 + ev] = t;
+    }
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_gpu(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// no-swizzle K-major descriptor over the 16-B rows of the bf16 state view in (time, sample)
+// order: core matrices are 8 consecutive rows (SBO 128 B), LBO = one time step (nb rows)
+__device__ __forceinline__ uint64_t xb_desc_us(const void* base, int nb) {
+    const uint32_t a = smem_u32(base);
+    uint64_t d = 0;
+    d |= (uint64_t)((a >> 4) & 0x3FFF);
+    d |= (uint64_t)(((uint32_t)nb * 16u) >> 4) << 16;
+    d |= (uint64_t)(128 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
+// mbarrier wait without the suspend-time hint (pure try_wait spin): on the persistent
+// kernel's latency-bound chains a suspended waiter wakes late
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void us_wait(uint64_t* b, uint32_t parity, bool spin) {
+    if (spin) mbar_wait_spin(b, parity);
+    else mbar_wait(b, parity);
+}
+
+__device__ __forceinline__ void store_bf16_row(__nv_bfloat16* dst, const float* y, int n) {
+    for (int c = 0; c < n; c += 8) {
+        __align__(16) __nv_bfloat162 pk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pk[u] = __floats2bfloat162_rn(y[c + 2 * u], y[c + 2 * u + 1]);
+        *reinterpret_cast<uint4*>(dst + c) = *reinterpret_cast<const uint4*>(pk);
+    }
+}
+
+// TMEM -> registers: NS fp32 columns starting at taddr
+template <int NS>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[NS]) {
+#pragma unroll
+    for (int cc = 0; cc < NS; cc += 16) {
+        uint32_t rr[16];
+        tmem_ld16(taddr + (uint32_t)cc, rr);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[cc + j] = __uint_as_float(rr[j]);
+    }
+}
+
+// GroupNorm statistics of NGS groups (CG channels each) of this thread's row, reduced over the
+// rows of its sample: lanes sharing `sl` in the warp (xor offsets >= nb), then the 4 warps
+// through shared memory (one named barrier; `red` is double-buffered by unit parity)
+template <int NS, int NGS>
+__device__ __forceinline__ void gn_stats(const float (&v)[NS], int nb, int sl, int lane, int ew, float* red,
+                                         float inv_n, float (&mean)[NGS], float (&rstd)[NGS]) {
+    constexpr int CG = NS / NGS;
+    float s1[NGS], s2[NGS];
+#pragma unroll
+    for (int g = 0; g < NGS; ++g) {
+        s1[g] = s2[g] = 0.f;
+#pragma unroll
+        for (int c = 0; c < CG; ++c) {
+            s1[g] += v[g * CG + c];
+            s2[g] = fmaf(v[g * CG + c], v[g * CG + c], s2[g]);
+        }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1)
+        if (off >= nb)
+#pragma unroll
+            for (int g = 0; g < NGS; ++g) {
+                s1[g] += __shfl_xor_sync(PS_FULL, s1[g], off);
+                s2[g] += __shfl_xor_sync(PS_FULL, s2[g], off);
+            }
+    if (lane < nb)
+#pragma unroll
+        for (int g = 0; g < NGS; ++g) {
+            red[(ew * 16 + sl) * 16 + g] = s1[g];
+            red[(ew * 16 + sl) * 16 + 8 + g] = s2[g];
+        }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+    for (int g = 0; g < NGS; ++g) {
+        float a1 = 0.f, a2 = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            a1 += red[(w * 16 + sl) * 16 + g];
+            a2 += red[(w * 16 + sl) * 16 + 8 + g];
+        }
+        mean[g] = a1 * inv_n;
+        rstd[g] = rsqrtf(fmaxf(fmaf(a2, inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
+    }
+}
+
+// epilogue of one unit of a non-final layer (NS channels, NGS GroupNorm groups in the slice);
+// vec: this unit's staged parameters
+template <int NS, int NGS>
+__device__ __forceinline__ void us_epilogue(const UsArgs& a, const UsHdr& H, int tile, int slice, uint32_t taddr,
+                                            float* red, const float* vec, int r, int lane, int ew) {
+    const int Tv = H.Tv, nb = H.nb, N = H.N, epi = H.epi;
+    const int n0 = slice * NS;
+    const int t0 = r / nb, sl = r % nb;
+    const int b = tile * nb + sl;
+    const bool valid = b < a.B;
+    const size_t grow = (size_t)(valid ? b : 0) * Tv + t0;
+    // identity residual (written by an earlier layer on another SM): issued first, read
+    // through L2, so its latency overlaps the statistics
+    uint4 rq[NS / 8];
+    const bool idres = epi == EPI_GN_RES && !H.res;
+    if (idres && valid) {
+        const uint4* rs = reinterpret_cast<const uint4*>(H.res_src + grow * N + n0);
+#pragma unroll
+        for (int i = 0; i < NS / 8; ++i) rq[i] = __ldcg(rs + i);
+    }
+    float v[NS];
+    tmem_ld_cols<NS>(taddr, v);
+#pragma unroll
+    for (int c = 0; c < NS; ++c) v[c] += vec[c];
+    if (epi == EPI_PLAIN) {
+        if (valid) store_bf16_row(H.out + grow * N + n0, v, NS);
+        return;
+    }
+    constexpr int CG = NS / NGS;
+    float mean[NGS], rstd[NGS];
+    gn_stats<NS, NGS>(v, nb, sl, lane, ew, red, 1.0f / (float)(Tv * CG), mean, rstd);
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+        const int g = c / CG;
+        const float tt = fmaf(v[c], rstd[g], -mean[g] * rstd[g]);
+        v[c] = mish8(fmaf(tt, vec[64 + c], vec[128 + c]));
+    }
+    if (epi == EPI_GN_FILM) {
+        const int pp = (valid ? b : tile * nb) / a.S - (tile * nb) / a.S;
+        const float* f = vec + US_VEC_FILM + pp * 2 * NS;
+#pragma unroll
+        for (int c = 0; c < NS; ++c) v[c] = fmaf(v[c], f[c], f[NS + c]);
+    } else if (H.res) {
+        float q[NS];
+        tmem_ld_cols<NS>(taddr + (uint32_t)NS, q);
+#pragma unroll
+        for (int c = 0; c < NS; ++c) v[c] += q[c] + vec[192 + c];
+    } else if (valid) {
+#pragma unroll
+        for (int i = 0; i < NS / 8; ++i) {
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&rq[i]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float2 f = __bfloat1622float2(h[u]);
+                v[8 * i + 2 * u] += f.x;
+                v[8 * i + 2 * u + 1] += f.y;
+            }
+        }
+    }
+    if (valid) store_bf16_row(H.out + grow * N + n0, v, NS);
+}
+
+// final layer: conv + GN + Mish over all 64 channels, 64 -> 7 projection (bf16 operands, fp32
+// sums, as the layered kernel's tensor-core projection), then the sampler update of the row
+__device__ __forceinline__ void us_final(const UsArgs& a, const UsHdr& H, int tile, uint32_t taddr, float* red,
+                                         const float* vec, const float* s_wout, const float* s_bout, int r, int lane,
+                                         int ew) {
+    const int Tv = H.Tv, nb = H.nb;
+    const int t = r / nb, sl = r % nb;
+    const int b = tile * nb + sl;
+    const bool valid = b < a.B;
+    const size_t grow = (size_t)(valid ? b : 0) * Tv + t;
+    float xv[U_DOF];   // the row's state, loaded early (L2) to overlap the statistics
+    if (!a.eps_out)
+#pragma unroll
+        for (int d = 0; d < U_DOF; ++d) xv[d] = __ldcg(a.x + grow * U_DOF + d);
+    float v[64];
+    tmem_ld_cols<64>(taddr, v);
+#pragma unroll
+    for (int c = 0; c < 64; ++c) v[c] += vec[c];
+    float mean[8], rstd[8];
+    gn_stats<64, 8>(v, nb, sl, lane, ew, red, 1.0f / (float)(Tv * 8), mean, rstd);
+    float eps[U_DOF];
+#pragma unroll
+    for (int d = 0; d < U_DOF; ++d) eps[d] = 0.f;
+#pragma unroll
+    for (int c = 0; c < 64; ++c) {
+        const int g = c / 8;
+        const float tt = fmaf(v[c], rstd[g], -mean[g] * rstd[g]);
+        const float y = __bfloat162float(__float2bfloat16_rn(mish8(fmaf(tt, vec[64 + c], vec[128 + c]))));
+#pragma unroll
+        for (int d = 0; d < U_DOF; ++d) eps[d] = fmaf(y, s_wout[d * 64 + c], eps[d]);
+    }
+#pragma unroll
+    for (int d = 0; d < U_DOF; ++d) eps[d] += s_bout[d];
+    if (!valid) return;
+    if (a.eps_out) {
+#pragma unroll
+        for (int d = 0; d < U_DOF; ++d) a.eps_out[grow * U_DOF + d] = eps[d];
+        return;
+    }
+    const StepCoef sc = *reinterpret_cast<const StepCoef*>(vec + US_VEC_SC);
+    // this row's 7 noise elements e = 7 t + d of sample b: Philox blocks e / 4 (2 or 3 of them)
+    float z[12];
+    const int e0 = t * U_DOF, blk0 = e0 >> 2, off = e0 & 3;
+    if (sc.ddpm && !sc.last) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float n4[4] = {0.f, 0.f, 0.f, 0.f};
+            if (k < 2 || off > 1)
+                normal4_tc((uint32_t)sc.k, (uint32_t)(a.p0 + b / a.S), (uint32_t)(b % a.S), (uint32_t)(blk0 + k), a.key, n4);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) z[4 * k + i] = n4[i];
+        }
+    }
+    float* xr = a.x + grow * U_DOF;
+    __align__(16) __nv_bfloat16 xv8[8];
+#pragma unroll
+    for (int d = 0; d < U_DOF; ++d) {
+        float x0 = (xv[d] - sc.sq1m * eps[d]) * sc.rsq;
+        x0 = fminf(fmaxf(x0, -0.1f), 1.1f);
+        float xn;
+        if (sc.last) {
+            const int p = b / a.S;
+            a.traj[grow * U_DOF + d] = (t == 0) ? a.q_start[(size_t)p * U_DOF + d] : a.lo + x0 * (a.hi - a.lo);
+            continue;
+        } else if (sc.ddpm) {
+            const float zd = off == 0 ? z[d] : off == 1 ? z[d + 1] : off == 2 ? z[d + 2] : z[d + 3];
+            xn = sc.c0 * x0 + sc.c1 * xv[d] + sc.sig * zd;
+        } else {
+            xn = sc.sqn * x0 + sc.sq1mn * eps[d];
+        }
+        xr[d] = xn;
+        xv8[d] = __float2bfloat16_rn(xn);
+    }
+    if (!sc.last) {
+        xv8[7] = __float2bfloat16_rn(0.f);
+        reinterpret_cast<uint4*>(a.xb)[grow] = *reinterpret_cast<const uint4*>(xv8);
+    }
+}
+
+__global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __grid_constant__ UsArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem_dyn[];
+    uint8_t* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
+    uint8_t* sA = smem;
+    uint8_t* sB = sA + US_SA * US_A_BYTES;
+    float* s_red = reinterpret_cast<float*>(sB + US_SB * US_B_BYTES);
+    float* s_wout = s_red + US_RED;
+    float* s_bout = s_wout + U_DOF * 64;
+    float* s_vec = s_bout + 8;                     // [2][US_VEC]
+    uint64_t* a_full = reinterpret_cast<uint64_t*>(s_vec + 2 * US_VEC);
+    uint64_t* a_empty = a_full + US_SA;
+    uint64_t* b_full = a_empty + US_SA;
+    uint64_t* b_empty = b_full + US_SB;
+    uint64_t* tfull = b_empty + US_SB;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* vfull = tempty + 2;
+    uint64_t* vempty = vfull + 2;
+    UsHdr* s_hdr = reinterpret_cast<UsHdr*>(vempty + 2);
+    UsGroup* s_grp = reinterpret_cast<UsGroup*>(s_hdr + a.n_layers);
+    UsTap* s_tap = reinterpret_cast<UsTap*>(s_grp + a.n_grp_all);
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(
+        (reinterpret_cast<uintptr_t>(s_tap + a.n_tap_all) + 15) & ~(uintptr_t)15);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool spin = (a.dbg & 32) != 0;
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < US_SA; ++i) {
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_empty[i], 1);
+        }
+        for (int i = 0; i < US_SB / US_BB; ++i) {
+            mbar_init(&b_full[i], US_BB);
+            mbar_init(&b_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+            mbar_init(&vfull[i], 1);
+            mbar_init(&vempty[i], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "r"(128));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    {   // layer tables -> shared memory
+        const int nh = a.n_layers * (int)(sizeof(UsHdr) / 4), ng = a.n_grp_all * (int)(sizeof(UsGroup) / 2),
+                  nt = a.n_tap_all * (int)(sizeof(UsTap) / 2);
+        for (int i = threadIdx.x; i < nh; i += US_THREADS)
+            reinterpret_cast<uint32_t*>(s_hdr)[i] = reinterpret_cast<const uint32_t*>(a.hdr)[i];
+        for (int i = threadIdx.x; i < ng; i += US_THREADS)
+            reinterpret_cast<uint16_t*>(s_grp)[i] = reinterpret_cast<const uint16_t*>(a.grp)[i];
+        for (int i = threadIdx.x; i < nt; i += US_THREADS)
+            reinterpret_cast<uint16_t*>(s_tap)[i] = reinterpret_cast<const uint16_t*>(a.tap)[i];
+    }
+    if (warp >= 4) {
+        // the projection's operands as the layered kernel sees them: bf16 weights
+        for (int i = threadIdx.x - 128; i < U_DOF * 64; i += 128)
+            s_wout[i] = __bfloat162float(__float2bfloat16_rn(a.wout[i]));
+        if (threadIdx.x - 128 < U_DOF) s_bout[threadIdx.x - 128] = a.bout[threadIdx.x - 128];
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+    const int G = (int)gridDim.x, c0 = (int)blockIdx.x;
+
+    if (warp == 0) {
+        // ---- weight producer: runs ahead over units and layers (bounded by the ring)
+        if (lane == 0) {
+            int sb = 0;
+            uint32_t pb = 0;
+            for (int s = 0; s < a.n_steps; ++s)
+                for (int l = 0; l < a.n_layers; ++l) {
+                    const UsHdr& H = s_hdr[l];
+                    const UsTap* tap = s_tap + H.tap0;
+                    const UsMaps* M = a.maps + l;
+                    const int units = H.units, ns = H.ns, n_sl = H.n_slices, n_tap = H.n_tap;
+                    const int tps = 64 / ns;
+                    for (int u = c0; u < units; u += G) {
+                        const int slice = u % n_sl;
+                        for (int t = 0; t < n_tap; t += tps) {
+                            if (sb % US_BB == 0) us_wait(&b_empty[sb / US_BB], pb ^ 1u, spin);
+                            const int n_in = min(tps, n_tap - t);
+                            if (a.dbg & 16) {   // knob: no weight traffic
+                                mbar_arrive(&b_full[sb / US_BB]);
+                                if (++sb == US_SB) { sb = 0; pb ^= 1u; }
+                                continue;
+                            }
+                            uint64_t* bf = &b_full[sb / US_BB];   // one full barrier per batch (US_BB arrivals)
+                            mbar_expect_tx(bf, (uint32_t)(n_in * ns * 128));
+                            for (int i = 0; i < n_in; ++i) {
+                                const UsTap tp = tap[t + i];
+                                tma_load_2d(sB + (size_t)sb * US_B_BYTES + i * ns * 128, tp.res ? &M->tmR : &M->tmW,
+                                            bf, tp.kcol, slice * ns);
+                            }
+                            if (++sb == US_SB) { sb = 0; pb ^= 1u; }
+                        }
+                    }
+                }
+            // complete the last batch (its full barrier counts US_BB stage arrivals)
+            for (; sb % US_BB != 0; ++sb) mbar_arrive(&b_full[sb / US_BB]);
+        }
+    } else if (warp == 2) {
+        // ---- activation producer: waits for the previous layer, then loads the tile's chunks
+        if (lane == 0) {
+            int sa = 0, ja = 0;
+            uint32_t pa = 0;
+            unsigned base = 0;   // units of all earlier (step, layer)s
+            for (int s = 0; s < a.n_steps; ++s)
+                for (int l = 0; l < a.n_layers; ++l) {
+                    const UsHdr& H = s_hdr[l];
+                    const UsGroup* grp = s_grp + H.grp0;
+                    const UsMaps* M = a.maps + l;
+                    const int units = H.units, n_sl = H.n_slices, nb = H.nb, Tv = H.Tv, n_grp = H.n_grp;
+                    if (c0 < units && base > 0) {
+                        // bounded: a unit that never publishes is a bug -- trap instead of hanging the GPU
+                        long long spins = 0;
+                        while (ld_acquire_gpu(a.done) < base)
+                            if (++spins > (1LL << 25)) __trap();
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                    }
+                    for (int u = c0; u < units; u += G, ++ja) {
+                        us_stamp(a, ja, 0);
+                        const int b0 = (u / n_sl) * nb;
+                        for (int g = 0; g < n_grp; ++g) {
+                            const UsGroup gr = grp[g];
+                            if (sa % US_AB == 0) us_wait(&a_empty[sa / US_AB], pa ^ 1u, spin);
+                            if (a.dbg & 8) {   // knob: no activation traffic
+                                mbar_arrive(&a_full[sa]);
+                                if (++sa == US_SA) { sa = 0; pa ^= 1u; }
+                                continue;
+                            }
+                            mbar_expect_tx(&a_full[sa], (uint32_t)(gr.xb ? (Tv + 5) * nb * 16 : (Tv + 4) * nb * 128));
+                            tma_load_3d(sA + (size_t)sa * US_A_BYTES, &M->tmA[gr.src], &a_full[sa], gr.c, b0, -2);
+                            if (++sa == US_SA) { sa = 0; pa ^= 1u; }
+                        }
+                    }
+                    base += (unsigned)units;
+                }
+        }
+    } else if (warp == 3) {
+        // ---- parameter prefetch: each unit's per-channel vectors, FiLM rows and step
+        // coefficients into a double-buffered staging area, ahead of the epilogue
+        int j = 0;
+        for (int s = 0; s < a.n_steps; ++s)
+            for (int l = 0; l < a.n_layers; ++l) {
+                const UsHdr& H = s_hdr[l];
+                const int units = H.units, n_sl = H.n_slices, ns = H.ns, nb = H.nb, N = H.N, epi = H.epi;
+                for (int u = c0; u < units; u += G, ++j) {
+                    const int vb = j & 1;
+                    us_wait(&vempty[vb], (((uint32_t)j >> 1) & 1u) ^ 1u, spin);
+                    if (lane == 0) us_stamp(a, j, 9);
+                    float* vec = s_vec + vb * US_VEC;
+                    const int tile = u / n_sl, n0 = (u % n_sl) * ns;
+                    for (int c = lane; c < ns; c += 32) {
+                        vec[c] = __ldg(H.bias + n0 + c);
+                        if (epi != EPI_PLAIN) {
+                            vec[64 + c] = __ldg(H.gamma + n0 + c);
+                            vec[128 + c] = __ldg(H.beta + n0 + c);
+                        }
+                        if (H.res) vec[192 + c] = __ldg(H.rbias + n0 + c);
+                    }
+                    if (epi == EPI_GN_FILM) {
+                        const int b_lo = tile * nb, b_hi = min(b_lo + nb, a.B) - 1;
+                        const int p_lo = b_lo / a.S, np = b_hi / a.S - p_lo + 1;
+                        const float* fb = a.film_b + (size_t)s * 3584 + H.film_col + n0;
+                        for (int i = lane; i < np * ns; i += 32) {
+                            const int pp = i / ns, c = i - pp * ns;
+                            const float* fa = a.film_a + (size_t)(p_lo + pp) * 3584 + H.film_col + n0;
+                            vec[US_VEC_FILM + pp * 2 * ns + c] = 1.f + (__ldg(fa + c) + __ldg(fb + c));
+                            vec[US_VEC_FILM + pp * 2 * ns + ns + c] = __ldg(fa + N + c) + __ldg(fb + N + c);
+                        }
+                    }
+                    if (epi == EPI_FINAL && !a.eps_out && lane < (int)(sizeof(StepCoef) / 4))
+                        vec[US_VEC_SC + lane] = __ldg(reinterpret_cast<const float*>(a.sc + s) + lane);
+                    __syncwarp();
+                    if (lane == 0) {
+                        us_stamp(a, j, 10);
+                        mbar_arrive(&vfull[vb]);
+                    }
+                }
+            }
+    } else if (warp == 1) {
+        // ---- MMA issuer (whole warp; elect.sync inside the issue wrappers -- measured faster
+        // than a lane-0 loop here too).  A single warp's dependent instruction chain: keep the
+        // per-tap path short (no divisions, descriptors as 32-bit address words + constant high
+        // words, one 8-B table load per tap, one full-barrier wait per weight batch)
+        int sa = 0, sb = 0, j = 0;
+        uint32_t pa = 0, pb = 0;
+        const uint32_t a_lo0 = smem_u32(sA) >> 4, b_lo0 = smem_u32(sB) >> 4;
+        const uint64_t hi_sw = umma_desc_sw128(sA) & ~(uint64_t)0x3FFF;   // SBO 1024, version, SWIZZLE_128B
+        const uint64_t hi_xb = ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);   // SBO 128, no swizzle
+        for (int s = 0; s < a.n_steps; ++s)
+            for (int l = 0; l < a.n_layers; ++l) {
+                const UsHdr& H = s_hdr[l];
+                const UsGroup* grp = s_grp + H.grp0;
+                const UsTap* tap = s_tap + H.tap0;
+                const int units = H.units, ns = H.ns, nb = H.nb, n_grp = H.n_grp;
+                const int tps = 64 / ns;
+                const uint32_t idesc = idesc_bf16(128, ns);
+                const uint32_t bstep = (uint32_t)(ns * 128) >> 4;
+                for (int u = c0; u < units; u += G, ++j) {
+                    const int buf = j & 1;
+                    us_wait(&tempty[buf], (((uint32_t)j >> 1) & 1u) ^ 1u, spin);
+                    tc_fence_after();
+                    const uint32_t acc0 = tmem_base + (uint32_t)(buf * 64);
+                    int in_st = 0;   // tap position inside the current weight stage
+                    for (int g = 0; g < n_grp; ++g) {
+                        const UsGroup gr = grp[g];
+                        us_wait(&a_full[sa], pa, spin);
+                        tc_fence_after();
+                        if (g == 0 && lane == 0) us_stamp(a, j, 1);
+                        const uint32_t a_lo = a_lo0 + (uint32_t)sa * (uint32_t)(US_A_BYTES >> 4);
+                        for (int k = 0; k < gr.ntap; ++k) {
+                            const UsTap tp = tap[gr.tap0 + k];
+                            if (in_st == 0 && sb % US_BB == 0) {   // a whole batch of stages lands together
+                                us_wait(&b_full[sb / US_BB], pb, spin);
+                                tc_fence_after();
+                            }
+                            const uint32_t b_lo = b_lo0 + (uint32_t)sb * (uint32_t)(US_B_BYTES >> 4) + (uint32_t)in_st * bstep;
+                            const uint32_t d_tmem = acc0 + (tp.res ? (uint32_t)ns : 0u);
+                            if (!(a.dbg & 2)) {
+                                if (gr.xb) {
+                                    // state view: a K=16 MMA covers two time shifts of 8 channels
+                                    // (LBO = one time step = nb rows of 16 B)
+                                    const uint64_t dX = hi_xb | ((uint64_t)nb << 16) | a_lo;
+                                    const int nk = tp.res ? 1 : 3;
+                                    for (int kk = 0; kk < nk; ++kk) {
+                                        const int sh = tp.res ? 0 : 2 * kk - 2;
+                                        umma_bf16_w(d_tmem, dX + (uint64_t)((2 + sh) * nb),
+                                                    (hi_sw | b_lo) + (uint64_t)(kk * 2), idesc, (tp.first && kk == 0) ? 0u : 1u);
+                                    }
+                                } else {
+                                    const uint64_t da = hi_sw | (uint64_t)(a_lo + (uint32_t)tp.aoff);
+                                    const uint64_t db = hi_sw | (uint64_t)b_lo;
+                                    umma_bf16_w(d_tmem, da, db, idesc, tp.first ? 0u : 1u);
+                                    umma_bf16_w(d_tmem, da + 2, db + 2, idesc, 1u);
+                                    umma_bf16_w(d_tmem, da + 4, db + 4, idesc, 1u);
+                                    umma_bf16_w(d_tmem, da + 6, db + 6, idesc, 1u);
+                                }
+                            }
+                            if (++in_st == tps) {
+                                in_st = 0;
+                                if (sb % US_BB == US_BB - 1) umma_commit_w(&b_empty[sb / US_BB]);
+                                if (++sb == US_SB) { sb = 0; pb ^= 1u; }
+                            }
+                        }
+                        if (sa % US_AB == US_AB - 1) umma_commit_w(&a_empty[sa / US_AB]);
+                        if (++sa == US_SA) { sa = 0; pa ^= 1u; }
+                    }
+                    if (in_st != 0) {   // the unit's last stage was partly filled: the next unit starts a new one
+                        if (sb % US_BB == US_BB - 1) umma_commit_w(&b_empty[sb / US_BB]);
+                        if (++sb == US_SB) { sb = 0; pb ^= 1u; }
+                    }
+                    umma_commit_w(&tfull[buf]);
+                    if (lane == 0) us_stamp(a, j, 11);
+                }
+            }
+        __syncwarp();
+    } else if (warp >= 4) {
+        // ---- epilogue warpgroup: thread r owns tile row r (TMEM lane r)
+        const int ew = warp - 4;
+        const int r = ew * 32 + lane;
+        int j = 0;
+        for (int s = 0; s < a.n_steps; ++s)
+            for (int l = 0; l < a.n_layers; ++l) {
+                const UsHdr& H = s_hdr[l];
+                const int units = H.units, n_sl = H.n_slices, ns = H.ns, N = H.N, epi = H.epi;
+                for (int u = c0; u < units; u += G, ++j) {
+                    const int buf = j & 1;
+                    const int tile = u / n_sl, slice = u % n_sl;
+                    us_wait(&tfull[buf], ((uint32_t)j >> 1) & 1u, spin);
+                    tc_fence_after();
+                    if (r == 0) us_stamp(a, j, 8);
+                    us_wait(&vfull[buf], ((uint32_t)j >> 1) & 1u, spin);
+                    if (r == 0) us_stamp(a, j, 2);
+                    const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(buf * 64);
+                    float* red = s_red + (j & 1) * (US_RED / 2);
+                    const float* vec = s_vec + buf * US_VEC;
+                    if (a.dbg & 1) {   // knob: no epilogue work
+                    } else if (epi == EPI_FINAL)
+                        us_final(a, H, tile, taddr, red, vec, s_wout, s_bout, r, lane, ew);
+                    else if (ns == 32)
+                        us_epilogue<32, 1>(a, H, tile, slice, taddr, red, vec, r, lane, ew);
+                    else if (N == 64)
+                        us_epilogue<16, 2>(a, H, tile, slice, taddr, red, vec, r, lane, ew);
+                    else
+                        us_epilogue<16, 1>(a, H, tile, slice, taddr, red, vec, r, lane, ew);
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&tempty[buf]);
+                        mbar_arrive(&vempty[buf]);
+                    }
+                    // publish the unit: every epilogue thread's stores precede the release
+                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                    if (r == 0) {
+                        us_stamp(a, j, 3);
+                        red_release_gpu(a.done, 1u);
+                    }
+                }
+            }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(128));
+    }
+}
+
+// ===========================================================================
+// host side
+// ===========================================================================
+static size_t kpad64(int K) { return (size_t)((K + 63) / 64) * 64; }
+
+static int us_build_layer(const Layout& L, const char* packed, const TcLayer& ly, int B, UsMaps& m, UsHdr& o,
+                          std::vector<UsGroup>& grp_all, std::vector<UsTap>& tap_all) {
+    memset(&m, 0, sizeof(m));
+    memset(&o, 0, sizeof(o));
+    const PConv& c = *ly.c;
+    const int N = c.N;
+    const __nv_bfloat16* W = reinterpret_cast<const __nv_bfloat16*>(packed);
+    const bool fin = ly.epi == EPI_FINAL;
+    o.ns = fin ? 64 : (N == 256 ? 32 : 16);   // whole GroupNorm groups (N / 8 channels)
+    if (N % o.ns) return PS_FAIL(PS_ERR_SHAPE);
+    o.N = N;
+    o.n_slices = N / o.ns;
+    o.Tv = ly.Tv;
+    o.nb = 128 / ly.Tv;
+    o.units = ((B + o.nb - 1) / o.nb) * o.n_slices;
+    o.epi = ly.epi;
+    o.res = ly.res ? 1 : 0;
+    o.film_col = c.film_col;
+    if ((ly.Tv + 4) * o.nb * 128 > US_A_BYTES || o.nb > US_FILM_P) return PS_FAIL(PS_ERR_SHAPE);
+    const int Bm = std::max(B, o.nb);
+    for (int s = 0; s < 3; ++s)
+        if (ly.src[s] && !(s == ly.xb_src ? make_xb_map(&m.tmA[s], ly.src[s], Bm, ly.Tv, o.nb)
+                                          : make_ts_map(&m.tmA[s], ly.src[s], Bm, ly.Tv, ly.ld[s], o.nb)))
+            return PS_FAIL(PS_ERR_CUDA);
+    if (!make_w_map(&m.tmW, W + c.w_off, N, (int)kpad64(c.K), o.ns)) return PS_FAIL(PS_ERR_CUDA);
+    if (ly.res && !make_w_map(&m.tmR, W + ly.res->w_off, N, (int)kpad64(ly.res->K), o.ns)) return PS_FAIL(PS_ERR_CUDA);
+    // taps grouped by the activation chunk they read (src, channel offset), as conv_tc.cu
+    struct Tmp { int src, c; std::vector<UsTap> taps; };
+    std::vector<Tmp> groups;
+    auto add = [&](const PConv& cc, int res, int shift) {
+        for (int i = 0; i < cc.n_seg; ++i) {
+            const PSeg& sg = cc.seg[i];
+            for (int j = 0; j < sg.nc; j += 64) {
+                const int src = sg.src + shift, ch = sg.c0 + j;
+                Tmp* gp = nullptr;
+                for (auto& g : groups)
+                    if (g.src == src && g.c == ch) gp = &g;
+                if (!gp) {
+                    groups.push_back(Tmp{src, ch, {}});
+                    gp = &groups.back();
+                }
+                UsTap tp{};
+                tp.kcol = (int16_t)(sg.k0 + j);
+                tp.dt = (int8_t)sg.dt;
+                tp.aoff = (int16_t)((2 + sg.dt) * o.nb * 8);
+                tp.res = (int8_t)res;
+                gp->taps.push_back(tp);
+            }
+        }
+    };
+    add(c, 0, 0);
+    if (ly.res) add(*ly.res, 1, ly.res_shift);
+    if ((int)groups.size() > US_MAXG) return PS_FAIL(PS_ERR_SHAPE);
+    bool first_main = true, first_res = true;
+    o.grp0 = (int)grp_all.size();
+    o.tap0 = (int)tap_all.size();
+    int nt = 0;
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        UsGroup g{};
+        g.c = (int16_t)groups[gi].c;
+        g.src = (int8_t)groups[gi].src;
+        g.ntap = (int8_t)groups[gi].taps.size();
+        g.tap0 = (int16_t)nt;   // relative to the layer's first tap
+        g.xb = (int8_t)(groups[gi].src == ly.xb_src ? 1 : 0);
+        grp_all.push_back(g);
+        for (auto tp : groups[gi].taps) {
+            if (nt >= US_MAXT) return PS_FAIL(PS_ERR_SHAPE);
+            bool& f = tp.res ? first_res : first_main;
+            tp.first = f ? 1 : 0;
+            f = false;
+            tap_all.push_back(tp);
+            ++nt;
+        }
+    }
+    o.n_grp = (int)groups.size();
+    o.n_tap = nt;
+    const float* side = L.side(packed);
+    o.bias = side + c.b_off;
+    if (c.g_off >= 0) {
+        o.gamma = side + c.g_off;
+        o.beta = side + c.be_off;
+    }
+    if (ly.res) o.rbias = side + ly.res->b_off;
+    o.res_src = ly.res_src;
+    o.out = ly.out;
+    return PS_OK;
+}
+
+struct UsPlan {
+    const void* packed = nullptr;
+    void* ws = nullptr;
+    int B = 0, T = 0;
+    char* d_tab = nullptr;   // [maps][hdr][groups][taps]
+    size_t tab_cap = 0;
+    UsMaps* d_maps = nullptr;
+    UsHdr* d_hdr = nullptr;
+    UsGroup* d_grp = nullptr;
+    UsTap* d_tap = nullptr;
+    int n_layers = 0, n_grp = 0, n_tap = 0;
+    int max_units = 0;
+    std::vector<int> units;
+    StepCoef* d_sc = nullptr;
+    int sc_cap = 0;
+    std::vector<StepCoef> sc_h;
+    unsigned* d_done = nullptr;
+};
+static UsPlan& us_plan() {
+    static UsPlan p;
+    return p;
+}
+
+static size_t us_smem_bytes(int n_layers, int n_grp, int n_tap) {
+    return 1024 + (size_t)US_SA * US_A_BYTES + (size_t)US_SB * US_B_BYTES +
+           (size_t)(US_RED + U_DOF * 64 + 8 + 2 * US_VEC) * 4 + (size_t)(2 * US_SA + 2 * US_SB + 8) * 8 +
+           n_layers * sizeof(UsHdr) + n_grp * sizeof(UsGroup) + n_tap * sizeof(UsTap) + 32;
+}
+
+static int us_n_sm() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
+bool unet_persist_eligible(int B, int T) {
+    if (T != 32 && T != 64) return false;
+    const char* env = std::getenv("PS_PERSIST");   // read per call: tests and A/B runs toggle it
+    if (env && env[0] == '0') return false;
+    if (env && env[0] == '1') return true;
+    return (long long)B * T <= 8192;   // measured crossover vs the layered kernels (tools/check_persist.py)
+}
+
+// host-side plan: layer table (tensor maps, tap lists) and step coefficients in device
+// memory.  Synchronous uploads -- call outside stream capture; rebuilt only when the
+// weights, workspace, batch or step table change.
+int unet_persist_prepare(const Layout& L, const char* packed, void* ws, int B, int T, const StepCoef* sc_h,
+                         int n_steps) {
+    if (!get_encoder()) return PS_FAIL(PS_ERR_CUDA);
+    UsPlan& P = us_plan();
+    const bool same_layers = P.d_tab && P.packed == packed && P.ws == ws && P.B == B && P.T == T;
+    const bool same_sc = P.d_sc && (int)P.sc_h.size() == n_steps &&
+                         memcmp(P.sc_h.data(), sc_h, (size_t)n_steps * sizeof(StepCoef)) == 0;
+    if (same_layers && same_sc) return PS_OK;
+    // a graph launched with the previous plan may still be reading it
+    if (cudaDeviceSynchronize() != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+    if (!same_layers) {
+        std::vector<TcLayer> list;
+        unet_layer_list(L, T, unet_slots(ws, B, T), false, list);
+        if ((int)list.size() > US_MAXL) return PS_FAIL(PS_ERR_SHAPE);
+        const int nl = (int)list.size();
+        std::vector<UsMaps> maps(nl);
+        std::vector<UsHdr> hdr(nl);
+        std::vector<UsGroup> grp;
+        std::vector<UsTap> tap;
+        int mx = 0;
+        P.units.assign(nl, 0);
+        for (int i = 0; i < nl; ++i) {
+            const int e = us_build_layer(L, packed, list[i], B, maps[i], hdr[i], grp, tap);
+            if (e) return e;
+            mx = std::max(mx, hdr[i].units);
+            P.units[i] = hdr[i].units;
+        }
+        const size_t o_hdr = nl * sizeof(UsMaps), o_grp = o_hdr + nl * sizeof(UsHdr),
+                     o_tap = o_grp + grp.size() * sizeof(UsGroup), total = o_tap + tap.size() * sizeof(UsTap);
+        if (us_smem_bytes(nl, (int)grp.size(), (int)tap.size()) > 227 * 1024) return PS_FAIL(PS_ERR_SHAPE);
+        if (total > P.tab_cap) {
+            if (P.d_tab) cudaFree(P.d_tab);
+            P.d_tab = nullptr;
+            if (cudaMalloc(&P.d_tab, total) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+            P.tab_cap = total;
+        }
+        std::vector<char> h(total);
+        memcpy(h.data(), maps.data(), o_hdr);
+        memcpy(h.data() + o_hdr, hdr.data(), nl * sizeof(UsHdr));
+        memcpy(h.data() + o_grp, grp.data(), grp.size() * sizeof(UsGroup));
+        memcpy(h.data() + o_tap, tap.data(), tap.size() * sizeof(UsTap));
+        if (cudaMemcpy(P.d_tab, h.data(), total, cudaMemcpyHostToDevice) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+        if (!P.d_done && cudaMalloc(&P.d_done, 256) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+        P.d_maps = reinterpret_cast<UsMaps*>(P.d_tab);
+        P.d_hdr = reinterpret_cast<UsHdr*>(P.d_tab + o_hdr);
+        P.d_grp = reinterpret_cast<UsGroup*>(P.d_tab + o_grp);
+        P.d_tap = reinterpret_cast<UsTap*>(P.d_tab + o_tap);
+        P.packed = packed;
+        P.ws = ws;
+        P.B = B;
+        P.T = T;
+        P.n_layers = nl;
+        P.n_grp = (int)grp.size();
+        P.n_tap = (int)tap.size();
+        P.max_units = mx;
+    }
+    if (!same_sc) {
+        if (n_steps > P.sc_cap) {
+            if (P.d_sc) cudaFree(P.d_sc);
+            P.d_sc = nullptr;
+            if (cudaMalloc(&P.d_sc, (size_t)n_steps * sizeof(StepCoef)) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+            P.sc_cap = n_steps;
+        }
+        if (cudaMemcpy(P.d_sc, sc_h, (size_t)n_steps * sizeof(StepCoef), cudaMemcpyHostToDevice) != cudaSuccess)
+            return PS_FAIL(PS_ERR_CUDA);
+        P.sc_h.assign(sc_h, sc_h + n_steps);
+    }
+    return PS_OK;
+}
+
+// the whole denoising loop (or one forward when eps_out is set) as one launch; capturable
+int unet_persist_launch(const Layout& L, const char* packed, void* ws, float* x, int B, int T, int S, int p0,
+                        unsigned key, const float* film_a, const float* film_b, int n_steps, const float* q_start,
+                        float* traj, float lo, float hi, float* eps_out, cudaStream_t st) {
+    UsPlan& P = us_plan();
+    if (!P.d_tab || P.packed != packed || P.ws != ws || P.B != B || P.T != T || (int)P.sc_h.size() != n_steps)
+        return PS_FAIL(PS_ERR_SHAPE);   // unet_persist_prepare first
+    const UnetSlots u = unet_slots(ws, B, T);
+    if (cudaMemsetAsync(P.d_done, 0, sizeof(unsigned), st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+    if (const int e = tc_xb(x, (size_t)B * T, u.a0, st)) return e;
+    UsArgs a;
+    memset(&a, 0, sizeof(a));
+    a.maps = P.d_maps;
+    a.hdr = P.d_hdr;
+    a.grp = P.d_grp;
+    a.tap = P.d_tap;
+    a.n_layers = P.n_layers;
+    a.n_grp_all = P.n_grp;
+    a.n_tap_all = P.n_tap;
+    a.B = B;
+    a.T = T;
+    a.S = S;
+    a.p0 = p0;
+    a.key = key;
+    a.n_steps = n_steps;
+    a.sc = P.d_sc;
+    a.film_a = film_a;
+    a.film_b = film_b;
+    a.x = x;
+    a.xb = u.a0;
+    const float* side = L.side(packed);
+    a.wout = side + L.outw_f32;
+    a.bout = side + L.out.b_off;
+    a.q_start = q_start;
+    a.traj = traj;
+    a.lo = lo;
+    a.hi = hi;
+    a.eps_out = eps_out;
+    a.done = P.d_done;
+    static const int dbg = std::getenv("PS_TC_DBG") ? std::atoi(std::getenv("PS_TC_DBG")) : 0;
+    a.dbg = dbg;
+    const size_t smem = us_smem_bytes(P.n_layers, P.n_grp, P.n_tap);
+    static size_t attr_set = 0;
+    if (smem > attr_set) {
+        if (cudaFuncSetAttribute(unet_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+            return PS_FAIL(PS_ERR_CUDA);
+        attr_set = smem;
+    }
+    // debug trace: PS_PERSIST_TRACE=<file> (uncaptured calls only, PS_NO_GRAPH=1)
+    static const char* trace_path = std::getenv("PS_PERSIST_TRACE");
+    static unsigned long long* d_trace = nullptr;
+    static size_t trace_bytes = 0;
+    const int grid_ = std::min(us_n_sm(), P.max_units);
+    if (trace_path) {
+        int per_step = 0;
+        for (int un : P.units) per_step += (un + grid_ - 1) / grid_;
+        a.trace_cap = per_step * n_steps;
+        const size_t need = (size_t)grid_ * a.trace_cap * 20 * 8;
+        if (need > trace_bytes) {
+            if (d_trace) cudaFree(d_trace);
+            cudaMalloc(&d_trace, need);
+            trace_bytes = need;
+        }
+        cudaMemset(d_trace, 0, need);
+        a.trace = d_trace;
+    }
+    // every CTA must be resident at once (units wait on other CTAs' units): cooperative launch,
+    // at most one CTA per SM
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid_);
+    cfg.blockDim = dim3(US_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ps_launch_counter().fetch_add(1, std::memory_order_relaxed);
+    if (cudaLaunchKernelEx(&cfg, unet_persist_kernel, a) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+    if (trace_path) {
+        std::vector<unsigned long long> h((size_t)grid_ * a.trace_cap * 20);
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h.data(), d_trace, h.size() * 8, cudaMemcpyDeviceToHost);
+        if (FILE* f = std::fopen(trace_path, "wb")) {
+            const int hdr[4] = {grid_, a.trace_cap, P.n_layers, n_steps};
+            std::fwrite(hdr, sizeof(hdr), 1, f);
+            std::fwrite(P.units.data(), sizeof(int), P.units.size(), f);
+            std::fwrite(h.data(), 8, h.size(), f);
+            std::fclose(f);
+        }
+    }
+    return PS_OK;
+}
+
+}  // namespace ps
