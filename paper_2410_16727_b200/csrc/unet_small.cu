@@ -10,7 +10,10 @@
 //   warp 0  weight producer: streams the unit's weight slice ([ns x 64] TMA boxes, packed
 //           8 KB per ring stage) and runs ahead across units and layers -- weights do not
 //           depend on activations, so the next layer's slice arrives while this layer computes;
-//   warp 1  MMA issuer (tcgen05, M = 128, N = ns, TMEM accumulators double-buffered);
+//   warps 1, 3  MMA issuers (tcgen05, M = 128, N = ns): the unit's 64-channel chunks alternate
+//           between the two warps, each with its own activation / weight rings and TMEM
+//           accumulators (summed by the epilogue) -- at these sizes a unit's MMA phase is the
+//           issuing warp's dependent instruction chain, which two warps halve;
 //   warp 2  activation producer: waits until every unit of the previous layer has published
 //           (a monotone completion counter in global memory, acquire), then TMA-loads the
 //           tile's 64-channel chunks with the conv halo (tap shifts are descriptor row shifts,
@@ -41,15 +44,19 @@ namespace ps {
 constexpr int US_MAXG = 24;
 constexpr int US_MAXT = 64;
 constexpr int US_MAXL = 32;
-constexpr int US_THREADS = 256;
-constexpr int US_SA = 4;             // activation stages (a multiple of US_AB)
+constexpr int US_THREADS = 256;      // 8 warps: see the role list above (a 9th warp would cap registers at 168)
+constexpr int US_PIPES = 2;          // MMA pipelines (issuing warps), each with its own rings and accumulators
+constexpr int US_SA = 4;             // activation stages (US_SA / US_PIPES per pipeline)
 constexpr int US_A_BYTES = 24576;    // >= (Tv + 4) * nb * 128 for every layer (T = 32, 64)
-constexpr int US_SB = 12;            // weight stages (a multiple of US_BB)
+constexpr int US_SB = 12;            // weight stages (US_SB / US_PIPES per pipeline, a multiple of US_BB)
 constexpr int US_B_BYTES = 8192;     // 64 / ns tap boxes of [ns x 64] bf16 per stage
-// stages are released in batches (one tcgen05.commit per batch): the tensor pipe processes
-// commits one after another at ~0.25 us each, which dominated small units' MMA phase
-constexpr int US_AB = 2;             // activation stages per release batch
-constexpr int US_BB = 4;             // weight stages per release batch
+constexpr int US_SAP = US_SA / US_PIPES, US_SBP = US_SB / US_PIPES;
+// weight stages per full / empty barrier.  1: a batch spanning units would make a pipeline's
+// MMAs wait for weights of a later unit that only arrive once the other pipeline's ring drains
+constexpr int US_BB = 1;
+constexpr int US_NBB = US_SBP / US_BB;   // weight batches per pipeline
+static_assert(US_BB == 1, "the producers index full / empty barriers by stage");
+constexpr int US_ACC = 64;           // TMEM columns per pipeline per buffer (main ns + residual ns)
 constexpr int US_RED = 2 * 4 * 16 * 16;   // GN partials [unit parity][warp][sample][2 * groups]
 
 struct UsGroup {
@@ -58,7 +65,7 @@ struct UsGroup {
     int8_t ntap;    // taps reading this chunk
     int16_t tap0;   // first tap
     int8_t xb;      // 8-channel bf16 state view (no swizzle)
-    int8_t pad;
+    int8_t pipe;    // MMA pipeline (groups alternate between the two issuing warps)
 };
 struct UsTap {
     int16_t kcol;   // weight K column
@@ -80,7 +87,8 @@ struct __align__(64) UsMaps {
 // would cost ~0.5 us on the critical path)
 struct UsHdr {
     int n_grp, n_tap, grp0, tap0;   // tables: entries [grp0, grp0 + n_grp) / [tap0, tap0 + n_tap)
-    int epi, res, N, ns, n_slices, Tv, nb, units, film_col, pad_;
+    int epi, res, N, ns, n_slices, Tv, nb, units, film_col;
+    int accs;   // accumulators written: bit 2p main, bit 2p+1 residual of pipeline p
     const float* bias;
     const float* gamma;
     const float* beta;
@@ -92,8 +100,9 @@ struct UsHdr {
 // tile's FiLM rows as (1 + scale, shift), and the step's coefficients
 constexpr int US_FILM_P = 16;                         // problems per tile (nb <= 16)
 constexpr int US_VEC_FILM = 256;
-constexpr int US_VEC_SC = US_VEC_FILM + US_FILM_P * 64;
+constexpr int US_VEC_SC = US_VEC_FILM + US_FILM_P * 64;   // FiLM rows, or the final layer's noise (128 x 7)
 constexpr int US_VEC = US_VEC_SC + 16;
+static_assert(128 * U_DOF <= US_FILM_P * 64, "final-layer noise fits the FiLM staging area");
 
 struct UsArgs {
     const UsMaps* maps;
@@ -166,6 +175,11 @@ __device__ __forceinline__ void us_wait(uint64_t* b, uint32_t parity, bool spin)
     else mbar_wait(b, parity);
 }
 
+// transaction bytes without an arrival (the producer arrives once per closed stage)
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void store_bf16_row(__nv_bfloat16* dst, const float* y, int n) {
     for (int c = 0; c < n; c += 8) {
         __align__(16) __nv_bfloat162 pk[4];
@@ -185,6 +199,23 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[NS]) {
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[cc + j] = __uint_as_float(rr[j]);
+    }
+}
+
+// sum of the accumulators a layer writes (bits of `accs` for one kind: 1 = pipeline 0, 2 =
+// pipeline 1; `off` selects main (0) or residual (NS) columns)
+template <int NS>
+__device__ __forceinline__ void acc_sum(uint32_t taddr, int bits, int off, float (&v)[NS]) {
+    if (bits & 1) {
+        tmem_ld_cols<NS>(taddr + (uint32_t)off, v);
+        if (bits & 2) {
+            float w[NS];
+            tmem_ld_cols<NS>(taddr + (uint32_t)(US_ACC + off), w);
+#pragma unroll
+            for (int c = 0; c < NS; ++c) v[c] += w[c];
+        }
+    } else {
+        tmem_ld_cols<NS>(taddr + (uint32_t)(US_ACC + off), v);
     }
 }
 
@@ -254,7 +285,7 @@ __device__ __forceinline__ void us_epilogue(const UsArgs& a, const UsHdr& H, int
         for (int i = 0; i < NS / 8; ++i) rq[i] = __ldcg(rs + i);
     }
     float v[NS];
-    tmem_ld_cols<NS>(taddr, v);
+    acc_sum<NS>(taddr, (H.accs & 1) | ((H.accs >> 1) & 2), 0, v);
 #pragma unroll
     for (int c = 0; c < NS; ++c) v[c] += vec[c];
     if (epi == EPI_PLAIN) {
@@ -277,7 +308,7 @@ __device__ __forceinline__ void us_epilogue(const UsArgs& a, const UsHdr& H, int
         for (int c = 0; c < NS; ++c) v[c] = fmaf(v[c], f[c], f[NS + c]);
     } else if (H.res) {
         float q[NS];
-        tmem_ld_cols<NS>(taddr + (uint32_t)NS, q);
+        acc_sum<NS>(taddr, ((H.accs >> 1) & 1) | ((H.accs >> 2) & 2), NS, q);
 #pragma unroll
         for (int c = 0; c < NS; ++c) v[c] += q[c] + vec[192 + c];
     } else if (valid) {
@@ -310,7 +341,7 @@ __device__ __forceinline__ void us_final(const UsArgs& a, const UsHdr& H, int ti
 #pragma unroll
         for (int d = 0; d < U_DOF; ++d) xv[d] = __ldcg(a.x + grow * U_DOF + d);
     float v[64];
-    tmem_ld_cols<64>(taddr, v);
+    acc_sum<64>(taddr, (H.accs & 1) | ((H.accs >> 1) & 2), 0, v);
 #pragma unroll
     for (int c = 0; c < 64; ++c) v[c] += vec[c];
     float mean[8], rstd[8];
@@ -335,19 +366,7 @@ __device__ __forceinline__ void us_final(const UsArgs& a, const UsHdr& H, int ti
         return;
     }
     const StepCoef sc = *reinterpret_cast<const StepCoef*>(vec + US_VEC_SC);
-    // this row's 7 noise elements e = 7 t + d of sample b: Philox blocks e / 4 (2 or 3 of them)
-    float z[12];
-    const int e0 = t * U_DOF, blk0 = e0 >> 2, off = e0 & 3;
-    if (sc.ddpm && !sc.last) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            float n4[4] = {0.f, 0.f, 0.f, 0.f};
-            if (k < 2 || off > 1)
-                normal4_tc((uint32_t)sc.k, (uint32_t)(a.p0 + b / a.S), (uint32_t)(b % a.S), (uint32_t)(blk0 + k), a.key, n4);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) z[4 * k + i] = n4[i];
-        }
-    }
+    const float* z = vec + US_VEC_FILM + r * U_DOF;   // this row's noise, staged by the prefetch warp
     float* xr = a.x + grow * U_DOF;
     __align__(16) __nv_bfloat16 xv8[8];
 #pragma unroll
@@ -360,8 +379,7 @@ __device__ __forceinline__ void us_final(const UsArgs& a, const UsHdr& H, int ti
             a.traj[grow * U_DOF + d] = (t == 0) ? a.q_start[(size_t)p * U_DOF + d] : a.lo + x0 * (a.hi - a.lo);
             continue;
         } else if (sc.ddpm) {
-            const float zd = off == 0 ? z[d] : off == 1 ? z[d + 1] : off == 2 ? z[d + 2] : z[d + 3];
-            xn = sc.c0 * x0 + sc.c1 * xv[d] + sc.sig * zd;
+            xn = sc.c0 * x0 + sc.c1 * xv[d] + sc.sig * z[d];
         } else {
             xn = sc.sqn * x0 + sc.sq1mn * eps[d];
         }
@@ -374,20 +392,68 @@ __device__ __forceinline__ void us_final(const UsArgs& a, const UsHdr& H, int ti
     }
 }
 
+// a unit's epilogue parameters -> shared memory, by the 128 epilogue threads while the unit's
+// MMAs run: bias / gamma / beta / rbias slices, the tile's FiLM rows as (1 + scale, shift),
+// and for the final layer the step coefficients and the tile's DDPM noise (data-independent
+// Philox blocks, stored as z[row * 7 + d] in the FiLM area)
+__device__ __forceinline__ void us_stage_params(const UsArgs& a, const UsHdr& H, int s, int tile, int n0, float* vec,
+                                                int tid) {
+    const int ns = H.ns, nb = H.nb, N = H.N, epi = H.epi;
+    for (int c = tid; c < ns; c += 128) {
+        vec[c] = __ldg(H.bias + n0 + c);
+        if (epi != EPI_PLAIN) {
+            vec[64 + c] = __ldg(H.gamma + n0 + c);
+            vec[128 + c] = __ldg(H.beta + n0 + c);
+        }
+        if (H.res) vec[192 + c] = __ldg(H.rbias + n0 + c);
+    }
+    if (epi == EPI_GN_FILM) {
+        const int b_lo = tile * nb, b_hi = min(b_lo + nb, a.B) - 1;
+        const int p_lo = b_lo / a.S, np = b_hi / a.S - p_lo + 1;
+        const float* fb = a.film_b + (size_t)s * 3584 + H.film_col + n0;
+        for (int i = tid; i < np * ns; i += 128) {
+            const int pp = i / ns, c = i - pp * ns;
+            const float* fa = a.film_a + (size_t)(p_lo + pp) * 3584 + H.film_col + n0;
+            vec[US_VEC_FILM + pp * 2 * ns + c] = 1.f + (__ldg(fa + c) + __ldg(fb + c));
+            vec[US_VEC_FILM + pp * 2 * ns + ns + c] = __ldg(fa + N + c) + __ldg(fb + N + c);
+        }
+    }
+    if (epi == EPI_FINAL && !a.eps_out) {
+        if (tid < (int)(sizeof(StepCoef) / 4))
+            vec[US_VEC_SC + tid] = __ldg(reinterpret_cast<const float*>(a.sc + s) + tid);
+        const StepCoef* scp = a.sc + s;
+        if (__ldg(&scp->ddpm) && !__ldg(&scp->last)) {
+            const int per = H.Tv * U_DOF / 4, k = __ldg(&scp->k);
+            for (int i = tid; i < nb * per; i += 128) {
+                const int sl = i / per, blk = i - sl * per;
+                const int b = tile * nb + sl;
+                float n4[4] = {0.f, 0.f, 0.f, 0.f};
+                if (b < a.B)
+                    normal4_tc((uint32_t)k, (uint32_t)(a.p0 + b / a.S), (uint32_t)(b % a.S), (uint32_t)blk, a.key, n4);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int e = 4 * blk + q, t = e / U_DOF, d = e - t * U_DOF;
+                    vec[US_VEC_FILM + (t * nb + sl) * U_DOF + d] = n4[q];
+                }
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __grid_constant__ UsArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_dyn[];
     uint8_t* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
-    uint8_t* sA = smem;
-    uint8_t* sB = sA + US_SA * US_A_BYTES;
+    uint8_t* sA = smem;                              // [pipe][US_SAP] activation stages
+    uint8_t* sB = sA + US_SA * US_A_BYTES;           // [pipe][US_SBP] weight stages
     float* s_red = reinterpret_cast<float*>(sB + US_SB * US_B_BYTES);
     float* s_wout = s_red + US_RED;
     float* s_bout = s_wout + U_DOF * 64;
     float* s_vec = s_bout + 8;                     // [2][US_VEC]
-    uint64_t* a_full = reinterpret_cast<uint64_t*>(s_vec + 2 * US_VEC);
+    uint64_t* a_full = reinterpret_cast<uint64_t*>(s_vec + 2 * US_VEC);   // [pipe][US_SAP]
     uint64_t* a_empty = a_full + US_SA;
-    uint64_t* b_full = a_empty + US_SA;
-    uint64_t* b_empty = b_full + US_SB;
-    uint64_t* tfull = b_empty + US_SB;
+    uint64_t* b_full = a_empty + US_SA;            // [pipe][US_NBB]: one per batch of US_BB stages
+    uint64_t* b_empty = b_full + US_PIPES * US_NBB;
+    uint64_t* tfull = b_empty + US_PIPES * US_NBB;
     uint64_t* tempty = tfull + 2;
     uint64_t* vfull = tempty + 2;
     uint64_t* vempty = vfull + 2;
@@ -404,12 +470,12 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
             mbar_init(&a_full[i], 1);
             mbar_init(&a_empty[i], 1);
         }
-        for (int i = 0; i < US_SB / US_BB; ++i) {
-            mbar_init(&b_full[i], US_BB);
+        for (int i = 0; i < US_PIPES * US_NBB; ++i) {
+            mbar_init(&b_full[i], US_BB);   // one arrival per stage closed by the producer
             mbar_init(&b_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&tfull[i], 1);
+            mbar_init(&tfull[i], US_PIPES);   // one commit per MMA pipeline
             mbar_init(&tempty[i], 4);
             mbar_init(&vfull[i], 1);
             mbar_init(&vempty[i], 4);
@@ -418,7 +484,7 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                     "r"(128));
+                     "r"(2 * US_PIPES * US_ACC));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     {   // layer tables -> shared memory
@@ -444,46 +510,59 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
     const int G = (int)gridDim.x, c0 = (int)blockIdx.x;
 
     if (warp == 0) {
-        // ---- weight producer: runs ahead over units and layers (bounded by the ring)
+        // ---- weight producer: runs ahead over units and layers (bounded by the rings).  A
+        // group's taps go to its pipeline's ring, packed 64 / ns tap boxes per stage; a stage
+        // closes when full or at the end of the unit
         if (lane == 0) {
-            int sb = 0;
-            uint32_t pb = 0;
+            // per-pipeline ring state in registers (indices are compile-time after unrolling)
+            int sb[US_PIPES] = {0, 0}, fill[US_PIPES] = {0, 0};
+            uint32_t pb[US_PIPES] = {0u, 0u};
             for (int s = 0; s < a.n_steps; ++s)
                 for (int l = 0; l < a.n_layers; ++l) {
                     const UsHdr& H = s_hdr[l];
+                    const UsGroup* grp = s_grp + H.grp0;
                     const UsTap* tap = s_tap + H.tap0;
                     const UsMaps* M = a.maps + l;
-                    const int units = H.units, ns = H.ns, n_sl = H.n_slices, n_tap = H.n_tap;
+                    const int units = H.units, ns = H.ns, n_sl = H.n_slices, n_grp = H.n_grp;
                     const int tps = 64 / ns;
+                    const uint32_t box = (uint32_t)(ns * 128);
                     for (int u = c0; u < units; u += G) {
-                        const int slice = u % n_sl;
-                        for (int t = 0; t < n_tap; t += tps) {
-                            if (sb % US_BB == 0) us_wait(&b_empty[sb / US_BB], pb ^ 1u, spin);
-                            const int n_in = min(tps, n_tap - t);
-                            if (a.dbg & 16) {   // knob: no weight traffic
-                                mbar_arrive(&b_full[sb / US_BB]);
-                                if (++sb == US_SB) { sb = 0; pb ^= 1u; }
-                                continue;
+                        const int nrow = (u % n_sl) * ns;
+                        for (int g0 = 0; g0 < n_grp; g0 += US_PIPES)
+#pragma unroll
+                            for (int p = 0; p < US_PIPES; ++p) {
+                                if (g0 + p >= n_grp) break;
+                                const UsGroup gr = grp[g0 + p];   // gr.pipe == p
+                                for (int k = 0; k < gr.ntap; ++k) {
+                                    if (fill[p] == 0) us_wait(&b_empty[p * US_NBB + sb[p]], pb[p] ^ 1u, spin);
+                                    uint64_t* bf = &b_full[p * US_NBB + sb[p]];
+                                    const UsTap tp = tap[gr.tap0 + k];
+                                    mbar_expect_tx_only(bf, box);
+                                    tma_load_2d(sB + (size_t)(p * US_SBP + sb[p]) * US_B_BYTES + fill[p] * box,
+                                                tp.res ? &M->tmR : &M->tmW, bf, tp.kcol, nrow);
+                                    if (++fill[p] == tps) {   // stage closed
+                                        mbar_arrive(bf);
+                                        fill[p] = 0;
+                                        if (++sb[p] == US_SBP) { sb[p] = 0; pb[p] ^= 1u; }
+                                    }
+                                }
                             }
-                            uint64_t* bf = &b_full[sb / US_BB];   // one full barrier per batch (US_BB arrivals)
-                            mbar_expect_tx(bf, (uint32_t)(n_in * ns * 128));
-                            for (int i = 0; i < n_in; ++i) {
-                                const UsTap tp = tap[t + i];
-                                tma_load_2d(sB + (size_t)sb * US_B_BYTES + i * ns * 128, tp.res ? &M->tmR : &M->tmW,
-                                            bf, tp.kcol, slice * ns);
+#pragma unroll
+                        for (int p = 0; p < US_PIPES; ++p)
+                            if (fill[p]) {   // the next unit starts a new stage
+                                mbar_arrive(&b_full[p * US_NBB + sb[p]]);
+                                fill[p] = 0;
+                                if (++sb[p] == US_SBP) { sb[p] = 0; pb[p] ^= 1u; }
                             }
-                            if (++sb == US_SB) { sb = 0; pb ^= 1u; }
-                        }
                     }
                 }
-            // complete the last batch (its full barrier counts US_BB stage arrivals)
-            for (; sb % US_BB != 0; ++sb) mbar_arrive(&b_full[sb / US_BB]);
         }
     } else if (warp == 2) {
         // ---- activation producer: waits for the previous layer, then loads the tile's chunks
+        // into their pipelines' rings
         if (lane == 0) {
-            int sa = 0, ja = 0;
-            uint32_t pa = 0;
+            int sa[US_PIPES] = {0, 0}, ja = 0;
+            uint32_t pa[US_PIPES] = {0u, 0u};
             unsigned base = 0;   // units of all earlier (step, layer)s
             for (int s = 0; s < a.n_steps; ++s)
                 for (int l = 0; l < a.n_layers; ++l) {
@@ -501,72 +580,31 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
                     for (int u = c0; u < units; u += G, ++ja) {
                         us_stamp(a, ja, 0);
                         const int b0 = (u / n_sl) * nb;
-                        for (int g = 0; g < n_grp; ++g) {
-                            const UsGroup gr = grp[g];
-                            if (sa % US_AB == 0) us_wait(&a_empty[sa / US_AB], pa ^ 1u, spin);
-                            if (a.dbg & 8) {   // knob: no activation traffic
-                                mbar_arrive(&a_full[sa]);
-                                if (++sa == US_SA) { sa = 0; pa ^= 1u; }
-                                continue;
+                        for (int g0 = 0; g0 < n_grp; g0 += US_PIPES)
+#pragma unroll
+                            for (int p = 0; p < US_PIPES; ++p) {
+                                if (g0 + p >= n_grp) break;
+                                const UsGroup gr = grp[g0 + p];   // gr.pipe == p
+                                const int st = p * US_SAP + sa[p];
+                                us_wait(&a_empty[st], pa[p] ^ 1u, spin);
+                                mbar_expect_tx(&a_full[st], (uint32_t)(gr.xb ? (Tv + 5) * nb * 16 : (Tv + 4) * nb * 128));
+                                tma_load_3d(sA + (size_t)st * US_A_BYTES, &M->tmA[gr.src], &a_full[st], gr.c, b0, -2);
+                                if (++sa[p] == US_SAP) { sa[p] = 0; pa[p] ^= 1u; }
                             }
-                            mbar_expect_tx(&a_full[sa], (uint32_t)(gr.xb ? (Tv + 5) * nb * 16 : (Tv + 4) * nb * 128));
-                            tma_load_3d(sA + (size_t)sa * US_A_BYTES, &M->tmA[gr.src], &a_full[sa], gr.c, b0, -2);
-                            if (++sa == US_SA) { sa = 0; pa ^= 1u; }
-                        }
                     }
                     base += (unsigned)units;
                 }
         }
-    } else if (warp == 3) {
-        // ---- parameter prefetch: each unit's per-channel vectors, FiLM rows and step
-        // coefficients into a double-buffered staging area, ahead of the epilogue
-        int j = 0;
-        for (int s = 0; s < a.n_steps; ++s)
-            for (int l = 0; l < a.n_layers; ++l) {
-                const UsHdr& H = s_hdr[l];
-                const int units = H.units, n_sl = H.n_slices, ns = H.ns, nb = H.nb, N = H.N, epi = H.epi;
-                for (int u = c0; u < units; u += G, ++j) {
-                    const int vb = j & 1;
-                    us_wait(&vempty[vb], (((uint32_t)j >> 1) & 1u) ^ 1u, spin);
-                    if (lane == 0) us_stamp(a, j, 9);
-                    float* vec = s_vec + vb * US_VEC;
-                    const int tile = u / n_sl, n0 = (u % n_sl) * ns;
-                    for (int c = lane; c < ns; c += 32) {
-                        vec[c] = __ldg(H.bias + n0 + c);
-                        if (epi != EPI_PLAIN) {
-                            vec[64 + c] = __ldg(H.gamma + n0 + c);
-                            vec[128 + c] = __ldg(H.beta + n0 + c);
-                        }
-                        if (H.res) vec[192 + c] = __ldg(H.rbias + n0 + c);
-                    }
-                    if (epi == EPI_GN_FILM) {
-                        const int b_lo = tile * nb, b_hi = min(b_lo + nb, a.B) - 1;
-                        const int p_lo = b_lo / a.S, np = b_hi / a.S - p_lo + 1;
-                        const float* fb = a.film_b + (size_t)s * 3584 + H.film_col + n0;
-                        for (int i = lane; i < np * ns; i += 32) {
-                            const int pp = i / ns, c = i - pp * ns;
-                            const float* fa = a.film_a + (size_t)(p_lo + pp) * 3584 + H.film_col + n0;
-                            vec[US_VEC_FILM + pp * 2 * ns + c] = 1.f + (__ldg(fa + c) + __ldg(fb + c));
-                            vec[US_VEC_FILM + pp * 2 * ns + ns + c] = __ldg(fa + N + c) + __ldg(fb + N + c);
-                        }
-                    }
-                    if (epi == EPI_FINAL && !a.eps_out && lane < (int)(sizeof(StepCoef) / 4))
-                        vec[US_VEC_SC + lane] = __ldg(reinterpret_cast<const float*>(a.sc + s) + lane);
-                    __syncwarp();
-                    if (lane == 0) {
-                        us_stamp(a, j, 10);
-                        mbar_arrive(&vfull[vb]);
-                    }
-                }
-            }
-    } else if (warp == 1) {
-        // ---- MMA issuer (whole warp; elect.sync inside the issue wrappers -- measured faster
-        // than a lane-0 loop here too).  A single warp's dependent instruction chain: keep the
-        // per-tap path short (no divisions, descriptors as 32-bit address words + constant high
-        // words, one 8-B table load per tap, one full-barrier wait per weight batch)
+    } else if (warp == 1 || warp == 3) {
+        // ---- MMA issuers, one per pipeline (whole warp; elect.sync inside the issue wrappers).
+        // A warp's dependent instruction chain: keep the per-tap path short (no divisions,
+        // descriptors as 32-bit address words + constant high words, one 8-B table load per tap,
+        // one full-barrier wait per weight batch)
+        const int p = warp == 1 ? 0 : 1;
         int sa = 0, sb = 0, j = 0;
         uint32_t pa = 0, pb = 0;
-        const uint32_t a_lo0 = smem_u32(sA) >> 4, b_lo0 = smem_u32(sB) >> 4;
+        const uint32_t a_lo0 = smem_u32(sA + (size_t)p * US_SAP * US_A_BYTES) >> 4;
+        const uint32_t b_lo0 = smem_u32(sB + (size_t)p * US_SBP * US_B_BYTES) >> 4;
         const uint64_t hi_sw = umma_desc_sw128(sA) & ~(uint64_t)0x3FFF;   // SBO 1024, version, SWIZZLE_128B
         const uint64_t hi_xb = ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);   // SBO 128, no swizzle
         for (int s = 0; s < a.n_steps; ++s)
@@ -582,18 +620,18 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
                     const int buf = j & 1;
                     us_wait(&tempty[buf], (((uint32_t)j >> 1) & 1u) ^ 1u, spin);
                     tc_fence_after();
-                    const uint32_t acc0 = tmem_base + (uint32_t)(buf * 64);
+                    const uint32_t acc0 = tmem_base + (uint32_t)(buf * US_PIPES * US_ACC + p * US_ACC);
                     int in_st = 0;   // tap position inside the current weight stage
-                    for (int g = 0; g < n_grp; ++g) {
+                    for (int g = p; g < n_grp; g += US_PIPES) {
                         const UsGroup gr = grp[g];
-                        us_wait(&a_full[sa], pa, spin);
+                        us_wait(&a_full[p * US_SAP + sa], pa, spin);
                         tc_fence_after();
                         if (g == 0 && lane == 0) us_stamp(a, j, 1);
                         const uint32_t a_lo = a_lo0 + (uint32_t)sa * (uint32_t)(US_A_BYTES >> 4);
                         for (int k = 0; k < gr.ntap; ++k) {
                             const UsTap tp = tap[gr.tap0 + k];
-                            if (in_st == 0 && sb % US_BB == 0) {   // a whole batch of stages lands together
-                                us_wait(&b_full[sb / US_BB], pb, spin);
+                            if (in_st == 0 && sb % US_BB == 0) {   // a batch of stages lands together
+                                us_wait(&b_full[p * US_NBB + sb / US_BB], pb, spin);
                                 tc_fence_after();
                             }
                             const uint32_t b_lo = b_lo0 + (uint32_t)sb * (uint32_t)(US_B_BYTES >> 4) + (uint32_t)in_st * bstep;
@@ -620,19 +658,19 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
                             }
                             if (++in_st == tps) {
                                 in_st = 0;
-                                if (sb % US_BB == US_BB - 1) umma_commit_w(&b_empty[sb / US_BB]);
-                                if (++sb == US_SB) { sb = 0; pb ^= 1u; }
+                                if (sb % US_BB == US_BB - 1) umma_commit_w(&b_empty[p * US_NBB + sb / US_BB]);
+                                if (++sb == US_SBP) { sb = 0; pb ^= 1u; }
                             }
                         }
-                        if (sa % US_AB == US_AB - 1) umma_commit_w(&a_empty[sa / US_AB]);
-                        if (++sa == US_SA) { sa = 0; pa ^= 1u; }
+                        umma_commit_w(&a_empty[p * US_SAP + sa]);
+                        if (++sa == US_SAP) { sa = 0; pa ^= 1u; }
                     }
                     if (in_st != 0) {   // the unit's last stage was partly filled: the next unit starts a new one
-                        if (sb % US_BB == US_BB - 1) umma_commit_w(&b_empty[sb / US_BB]);
-                        if (++sb == US_SB) { sb = 0; pb ^= 1u; }
+                        if (sb % US_BB == US_BB - 1) umma_commit_w(&b_empty[p * US_NBB + sb / US_BB]);
+                        if (++sb == US_SBP) { sb = 0; pb ^= 1u; }
                     }
-                    umma_commit_w(&tfull[buf]);
-                    if (lane == 0) us_stamp(a, j, 11);
+                    umma_commit_w(&tfull[buf]);   // also when this pipeline had no chunk in the unit
+                    if (lane == 0 && p == 0) us_stamp(a, j, 11);
                 }
             }
         __syncwarp();
@@ -648,12 +686,14 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
                 for (int u = c0; u < units; u += G, ++j) {
                     const int buf = j & 1;
                     const int tile = u / n_sl, slice = u % n_sl;
+                    // stage this unit's parameters while its MMAs run (the previous unit's
+                    // readers of this buffer all passed its publish barrier)
+                    us_stage_params(a, H, s, tile, slice * ns, s_vec + buf * US_VEC, r);
+                    asm volatile("bar.sync 3, 128;" ::: "memory");
                     us_wait(&tfull[buf], ((uint32_t)j >> 1) & 1u, spin);
                     tc_fence_after();
-                    if (r == 0) us_stamp(a, j, 8);
-                    us_wait(&vfull[buf], ((uint32_t)j >> 1) & 1u, spin);
                     if (r == 0) us_stamp(a, j, 2);
-                    const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(buf * 64);
+                    const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(buf * US_PIPES * US_ACC);
                     float* red = s_red + (j & 1) * (US_RED / 2);
                     const float* vec = s_vec + buf * US_VEC;
                     if (a.dbg & 1) {   // knob: no epilogue work
@@ -667,10 +707,7 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
                         us_epilogue<16, 1>(a, H, tile, slice, taddr, red, vec, r, lane, ew);
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) {
-                        mbar_arrive(&tempty[buf]);
-                        mbar_arrive(&vempty[buf]);
-                    }
+                    if (lane == 0) mbar_arrive(&tempty[buf]);
                     // publish the unit: every epilogue thread's stores precede the release
                     asm volatile("bar.sync 2, 128;" ::: "memory");
                     if (r == 0) {
@@ -683,7 +720,7 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(128));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * US_PIPES * US_ACC));
     }
 }
 
@@ -745,7 +782,7 @@ static int us_build_layer(const Layout& L, const char* packed, const TcLayer& ly
     add(c, 0, 0);
     if (ly.res) add(*ly.res, 1, ly.res_shift);
     if ((int)groups.size() > US_MAXG) return PS_FAIL(PS_ERR_SHAPE);
-    bool first_main = true, first_res = true;
+    bool first[US_PIPES][2] = {{true, true}, {true, true}};   // [pipeline][residual]
     o.grp0 = (int)grp_all.size();
     o.tap0 = (int)tap_all.size();
     int nt = 0;
@@ -756,12 +793,14 @@ static int us_build_layer(const Layout& L, const char* packed, const TcLayer& ly
         g.ntap = (int8_t)groups[gi].taps.size();
         g.tap0 = (int16_t)nt;   // relative to the layer's first tap
         g.xb = (int8_t)(groups[gi].src == ly.xb_src ? 1 : 0);
+        g.pipe = (int8_t)(gi % US_PIPES);
         grp_all.push_back(g);
         for (auto tp : groups[gi].taps) {
             if (nt >= US_MAXT) return PS_FAIL(PS_ERR_SHAPE);
-            bool& f = tp.res ? first_res : first_main;
+            bool& f = first[g.pipe][tp.res ? 1 : 0];
             tp.first = f ? 1 : 0;
             f = false;
+            o.accs |= 1 << (2 * g.pipe + (tp.res ? 1 : 0));
             tap_all.push_back(tp);
             ++nt;
         }
@@ -805,7 +844,7 @@ static UsPlan& us_plan() {
 
 static size_t us_smem_bytes(int n_layers, int n_grp, int n_tap) {
     return 1024 + (size_t)US_SA * US_A_BYTES + (size_t)US_SB * US_B_BYTES +
-           (size_t)(US_RED + U_DOF * 64 + 8 + 2 * US_VEC) * 4 + (size_t)(2 * US_SA + 2 * US_SB + 8) * 8 +
+           (size_t)(US_RED + U_DOF * 64 + 8 + 2 * US_VEC) * 4 + (size_t)(2 * US_SA + 2 * US_PIPES * US_NBB + 8) * 8 +
            n_layers * sizeof(UsHdr) + n_grp * sizeof(UsGroup) + n_tap * sizeof(UsTap) + 32;
 }
 
