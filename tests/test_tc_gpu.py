@@ -163,3 +163,23 @@ def test_persistent_small_batch_ddpm100(samplers, params, P, S, T):
     # (layered kernels: 0.093 rad at 1 x 32, 0.155 rad at T=64); RMS is the tight check
     assert np.abs(d).max() < (0.15 if T == 32 else 0.2)
     assert np.sqrt((d ** 2).mean()) < 2e-2
+
+
+def test_persistent_small_batch_ddim(samplers, params):
+    # deterministic DDIM through the persistent kernel's DDIM update, against the oracle and the
+    # layered kernels.  The strided schedule starts at k = 50: from k = 100 the squared-cosine
+    # schedule's x0 reconstruction multiplies the noise prediction by 1/sqrt(abar_100) (~2000),
+    # so any bf16 difference saturates the x0 clip (both bf16 paths sit ~0.4 rad RMS from the
+    # fp64 oracle there, the fp32 path 6e-5; tools/ddim_check.py)
+    _, s1 = samplers
+    P, S = 2, 16
+    cond = _cond(P, 23)
+    q0 = synth.make_problems(P, seed=29).q_start
+    steps = np.array([50, 40, 30, 20, 10, 1])
+    fa = s1.film(cond)
+    tp = _with_persist("1", lambda: s1.sample(fa, q0, S, steps=steps).cpu().numpy())
+    tl = _with_persist("0", lambda: s1.sample(fa, q0, S, steps=steps).cpu().numpy())
+    want = un.sample(params, ARCH, cond, q0, S, steps=steps)
+    assert np.array_equal(tp[:, 0], np.repeat(q0, S, axis=0))
+    assert np.sqrt(((tp - want) ** 2).mean()) < 2e-2
+    assert np.sqrt(((tp - tl) ** 2).mean()) < 2e-2
