@@ -11,6 +11,8 @@
 // through the read-only path with 8 scalar gathers per sphere lookup.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ps {
@@ -182,7 +184,7 @@ __device__ __forceinline__ float warp_min(float v) {
 
 // MODE 0: refine (n_iters steps + final cost/flags).  MODE 1: cost + gradient only.
 template <int WPL, int MODE>
-__global__ void __launch_bounds__(128) bl_refine_kernel(const __grid_constant__ BLParams P) {
+__global__ void __launch_bounds__(512) bl_refine_kernel(const __grid_constant__ BLParams P) {
     const int lane = threadIdx.x & 31;
     const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (b >= P.B) return;  // whole warp exits together
@@ -544,7 +546,9 @@ static int fill_params(BLParams& P, int B, int T, int S, const float* esdf, long
 template <int MODE>
 static int launch_bl(const BLParams& P, cudaStream_t st) {
     if (P.B == 0) return PS_OK;
-    const int threads = 128;
+    // a block holds 512 / 32 = 16 trajectories of one problem: seeds of a problem move through
+    // the same part of its ESDF, so their gathers share the SM's L1 (PS_REFINE_THREADS: A/B)
+    static const int threads = std::getenv("PS_REFINE_THREADS") ? std::atoi(std::getenv("PS_REFINE_THREADS")) : 512;
     const long long blocks = ((long long)P.B * 32 + threads - 1) / threads;
     if (P.T == 32)
         bl_refine_kernel<1, MODE><<<(unsigned)blocks, threads, 0, st>>>(P);

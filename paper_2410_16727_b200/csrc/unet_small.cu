@@ -44,7 +44,8 @@ namespace ps {
 constexpr int US_MAXG = 24;
 constexpr int US_MAXT = 64;
 constexpr int US_MAXL = 32;
-constexpr int US_THREADS = 256;      // 8 warps: see the role list above (a 9th warp would cap registers at 168)
+constexpr int US_EPI_THREADS = 256;  // 8 epilogue warps: lane quadrant x column half
+constexpr int US_THREADS = 128 + US_EPI_THREADS;   // 12 warps: see the role list above
 constexpr int US_PIPES = 2;          // MMA pipelines (issuing warps), each with its own rings and accumulators
 constexpr int US_SA = 4;             // activation stages (US_SA / US_PIPES per pipeline)
 constexpr int US_A_BYTES = 24576;    // >= (Tv + 4) * nb * 128 for every layer (T = 32, 64)
@@ -57,7 +58,7 @@ constexpr int US_BB = 1;
 constexpr int US_NBB = US_SBP / US_BB;   // weight batches per pipeline
 static_assert(US_BB == 1, "the producers index full / empty barriers by stage");
 constexpr int US_ACC = 64;           // TMEM columns per pipeline per buffer (main ns + residual ns)
-constexpr int US_RED = 2 * 4 * 16 * 16;   // GN partials [unit parity][warp][sample][2 * groups]
+constexpr int US_RED = 2 * 8 * 16 * 8;   // GN partials [unit parity][half][quadrant][sample][2 x 4 groups]
 
 struct UsGroup {
     int16_t c;      // channel offset in the source view
@@ -219,16 +220,20 @@ __device__ __forceinline__ void acc_sum(uint32_t taddr, int bits, int off, float
     }
 }
 
-// GroupNorm statistics of NGS groups (CG channels each) of this thread's row, reduced over the
-// rows of its sample: lanes sharing `sl` in the warp (xor offsets >= nb), then the 4 warps
-// through shared memory (one named barrier; `red` is double-buffered by unit parity)
-template <int NS, int NGS>
-__device__ __forceinline__ void gn_stats(const float (&v)[NS], int nb, int sl, int lane, int ew, float* red,
-                                         float inv_n, float (&mean)[NGS], float (&rstd)[NGS]) {
-    constexpr int CG = NS / NGS;
-    float s1[NGS], s2[NGS];
+// Epilogue thread layout: 8 warps; warp w owns TMEM lane quadrant q = w % 4 (tile rows
+// 32q .. 32q+31) and column half h of the unit's NS channels (NH = NS / 2 each).
+//
+// GroupNorm statistics of this thread's groups (NGL of them, CG channels each) over the rows
+// of its sample: lanes sharing `sl` (xor offsets >= nb), then the 4 quadrant warps -- and the
+// other column half when a group spans both halves (SPAN) -- through shared memory (one named
+// barrier; `red` is double-buffered by unit parity: [half][quadrant][sample][s1 x 4, s2 x 4])
+template <int NH, int NGL, bool SPAN>
+__device__ __forceinline__ void gn_stats(const float (&v)[NH], int nb, int sl, int lane, int q, int h, float* red,
+                                         float inv_n, float (&mean)[NGL], float (&rstd)[NGL]) {
+    constexpr int CG = SPAN ? NH : NH / NGL;   // channels of a group inside this half
+    float s1[NGL], s2[NGL];
 #pragma unroll
-    for (int g = 0; g < NGS; ++g) {
+    for (int g = 0; g < NGL; ++g) {
         s1[g] = s2[g] = 0.f;
 #pragma unroll
         for (int c = 0; c < CG; ++c) {
@@ -240,133 +245,146 @@ __device__ __forceinline__ void gn_stats(const float (&v)[NS], int nb, int sl, i
     for (int off = 16; off >= 1; off >>= 1)
         if (off >= nb)
 #pragma unroll
-            for (int g = 0; g < NGS; ++g) {
+            for (int g = 0; g < NGL; ++g) {
                 s1[g] += __shfl_xor_sync(PS_FULL, s1[g], off);
                 s2[g] += __shfl_xor_sync(PS_FULL, s2[g], off);
             }
     if (lane < nb)
 #pragma unroll
-        for (int g = 0; g < NGS; ++g) {
-            red[(ew * 16 + sl) * 16 + g] = s1[g];
-            red[(ew * 16 + sl) * 16 + 8 + g] = s2[g];
+        for (int g = 0; g < NGL; ++g) {
+            red[((h * 4 + q) * 16 + sl) * 8 + g] = s1[g];
+            red[((h * 4 + q) * 16 + sl) * 8 + 4 + g] = s2[g];
         }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
+    asm volatile("bar.sync 1, 256;" ::: "memory");
 #pragma unroll
-    for (int g = 0; g < NGS; ++g) {
+    for (int g = 0; g < NGL; ++g) {
         float a1 = 0.f, a2 = 0.f;
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            a1 += red[(w * 16 + sl) * 16 + g];
-            a2 += red[(w * 16 + sl) * 16 + 8 + g];
+        for (int hh = 0; hh < (SPAN ? 2 : 1); ++hh) {
+            const int hs = SPAN ? hh : h;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                a1 += red[((hs * 4 + w) * 16 + sl) * 8 + g];
+                a2 += red[((hs * 4 + w) * 16 + sl) * 8 + 4 + g];
+            }
         }
         mean[g] = a1 * inv_n;
         rstd[g] = rsqrtf(fmaxf(fmaf(a2, inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
     }
 }
 
-// epilogue of one unit of a non-final layer (NS channels, NGS GroupNorm groups in the slice);
-// vec: this unit's staged parameters
+// epilogue of one unit of a non-final layer (NS channels, NGS GroupNorm groups in the slice)
+// for this thread's column half; vec: this unit's staged parameters
 template <int NS, int NGS>
 __device__ __forceinline__ void us_epilogue(const UsArgs& a, const UsHdr& H, int tile, int slice, uint32_t taddr,
-                                            float* red, const float* vec, int r, int lane, int ew) {
+                                            float* red, const float* vec, int r, int lane, int q, int h) {
+    constexpr int NH = NS / 2, CG = NS / NGS;
+    constexpr bool SPAN = CG > NH;
+    constexpr int NGL = SPAN ? 1 : NH / CG;
     const int Tv = H.Tv, nb = H.nb, N = H.N, epi = H.epi;
-    const int n0 = slice * NS;
+    const int n0 = slice * NS, ch = h * NH;   // this half's first channel in the slice
     const int t0 = r / nb, sl = r % nb;
     const int b = tile * nb + sl;
     const bool valid = b < a.B;
     const size_t grow = (size_t)(valid ? b : 0) * Tv + t0;
     // identity residual (written by an earlier layer on another SM): issued first, read
     // through L2, so its latency overlaps the statistics
-    uint4 rq[NS / 8];
+    uint4 rq[NH / 8];
     const bool idres = epi == EPI_GN_RES && !H.res;
     if (idres && valid) {
-        const uint4* rs = reinterpret_cast<const uint4*>(H.res_src + grow * N + n0);
+        const uint4* rs = reinterpret_cast<const uint4*>(H.res_src + grow * N + n0 + ch);
 #pragma unroll
-        for (int i = 0; i < NS / 8; ++i) rq[i] = __ldcg(rs + i);
+        for (int i = 0; i < NH / 8; ++i) rq[i] = __ldcg(rs + i);
     }
-    float v[NS];
-    acc_sum<NS>(taddr, (H.accs & 1) | ((H.accs >> 1) & 2), 0, v);
+    float v[NH];
+    acc_sum<NH>(taddr + (uint32_t)ch, (H.accs & 1) | ((H.accs >> 1) & 2), 0, v);
 #pragma unroll
-    for (int c = 0; c < NS; ++c) v[c] += vec[c];
+    for (int c = 0; c < NH; ++c) v[c] += vec[ch + c];
     if (epi == EPI_PLAIN) {
-        if (valid) store_bf16_row(H.out + grow * N + n0, v, NS);
+        if (valid) store_bf16_row(H.out + grow * N + n0 + ch, v, NH);
         return;
     }
-    constexpr int CG = NS / NGS;
-    float mean[NGS], rstd[NGS];
-    gn_stats<NS, NGS>(v, nb, sl, lane, ew, red, 1.0f / (float)(Tv * CG), mean, rstd);
+    float mean[NGL], rstd[NGL];
+    gn_stats<NH, NGL, SPAN>(v, nb, sl, lane, q, h, red, 1.0f / (float)(Tv * CG), mean, rstd);
 #pragma unroll
-    for (int c = 0; c < NS; ++c) {
-        const int g = c / CG;
+    for (int c = 0; c < NH; ++c) {
+        const int g = SPAN ? 0 : c / CG;
         const float tt = fmaf(v[c], rstd[g], -mean[g] * rstd[g]);
-        v[c] = mish8(fmaf(tt, vec[64 + c], vec[128 + c]));
+        v[c] = mish8(fmaf(tt, vec[64 + ch + c], vec[128 + ch + c]));
     }
     if (epi == EPI_GN_FILM) {
         const int pp = (valid ? b : tile * nb) / a.S - (tile * nb) / a.S;
-        const float* f = vec + US_VEC_FILM + pp * 2 * NS;
+        const float* f = vec + US_VEC_FILM + pp * 2 * NS + ch;
 #pragma unroll
-        for (int c = 0; c < NS; ++c) v[c] = fmaf(v[c], f[c], f[NS + c]);
+        for (int c = 0; c < NH; ++c) v[c] = fmaf(v[c], f[c], f[NS + c]);
     } else if (H.res) {
-        float q[NS];
-        acc_sum<NS>(taddr, ((H.accs >> 1) & 1) | ((H.accs >> 2) & 2), NS, q);
+        float qv[NH];
+        acc_sum<NH>(taddr + (uint32_t)ch, ((H.accs >> 1) & 1) | ((H.accs >> 2) & 2), NS, qv);
 #pragma unroll
-        for (int c = 0; c < NS; ++c) v[c] += q[c] + vec[192 + c];
+        for (int c = 0; c < NH; ++c) v[c] += qv[c] + vec[192 + ch + c];
     } else if (valid) {
 #pragma unroll
-        for (int i = 0; i < NS / 8; ++i) {
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&rq[i]);
+        for (int i = 0; i < NH / 8; ++i) {
+            const __nv_bfloat162* hp = reinterpret_cast<const __nv_bfloat162*>(&rq[i]);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const float2 f = __bfloat1622float2(h[u]);
+                const float2 f = __bfloat1622float2(hp[u]);
                 v[8 * i + 2 * u] += f.x;
                 v[8 * i + 2 * u + 1] += f.y;
             }
         }
     }
-    if (valid) store_bf16_row(H.out + grow * N + n0, v, NS);
+    if (valid) store_bf16_row(H.out + grow * N + n0 + ch, v, NH);
 }
 
-// final layer: conv + GN + Mish over all 64 channels, 64 -> 7 projection (bf16 operands, fp32
-// sums, as the layered kernel's tensor-core projection), then the sampler update of the row
+// final layer: conv + GN + Mish over this half's 32 of the 64 channels and their share of the
+// 64 -> 7 projection (bf16 operands, fp32 sums, as the layered kernel's tensor-core
+// projection); half 1 hands its partial sums to half 0 through `xch`, which then runs the
+// sampler update of the row
 __device__ __forceinline__ void us_final(const UsArgs& a, const UsHdr& H, int tile, uint32_t taddr, float* red,
-                                         const float* vec, const float* s_wout, const float* s_bout, int r, int lane,
-                                         int ew) {
+                                         float* xch, const float* vec, const float* s_wout, const float* s_bout, int r,
+                                         int lane, int q, int h) {
     const int Tv = H.Tv, nb = H.nb;
     const int t = r / nb, sl = r % nb;
     const int b = tile * nb + sl;
     const bool valid = b < a.B;
     const size_t grow = (size_t)(valid ? b : 0) * Tv + t;
+    const int ch = h * 32;
     float xv[U_DOF];   // the row's state, loaded early (L2) to overlap the statistics
-    if (!a.eps_out)
+    if (!a.eps_out && h == 0)
 #pragma unroll
         for (int d = 0; d < U_DOF; ++d) xv[d] = __ldcg(a.x + grow * U_DOF + d);
-    float v[64];
-    acc_sum<64>(taddr, (H.accs & 1) | ((H.accs >> 1) & 2), 0, v);
+    float v[32];
+    acc_sum<32>(taddr + (uint32_t)ch, (H.accs & 1) | ((H.accs >> 1) & 2), 0, v);
 #pragma unroll
-    for (int c = 0; c < 64; ++c) v[c] += vec[c];
-    float mean[8], rstd[8];
-    gn_stats<64, 8>(v, nb, sl, lane, ew, red, 1.0f / (float)(Tv * 8), mean, rstd);
+    for (int c = 0; c < 32; ++c) v[c] += vec[ch + c];
+    float mean[4], rstd[4];
+    gn_stats<32, 4, false>(v, nb, sl, lane, q, h, red, 1.0f / (float)(Tv * 8), mean, rstd);
     float eps[U_DOF];
 #pragma unroll
     for (int d = 0; d < U_DOF; ++d) eps[d] = 0.f;
 #pragma unroll
-    for (int c = 0; c < 64; ++c) {
+    for (int c = 0; c < 32; ++c) {
         const int g = c / 8;
         const float tt = fmaf(v[c], rstd[g], -mean[g] * rstd[g]);
-        const float y = __bfloat162float(__float2bfloat16_rn(mish8(fmaf(tt, vec[64 + c], vec[128 + c]))));
+        const float y = __bfloat162float(__float2bfloat16_rn(mish8(fmaf(tt, vec[64 + ch + c], vec[128 + ch + c]))));
 #pragma unroll
-        for (int d = 0; d < U_DOF; ++d) eps[d] = fmaf(y, s_wout[d * 64 + c], eps[d]);
+        for (int d = 0; d < U_DOF; ++d) eps[d] = fmaf(y, s_wout[d * 64 + ch + c], eps[d]);
     }
+    if (h == 1)
 #pragma unroll
-    for (int d = 0; d < U_DOF; ++d) eps[d] += s_bout[d];
-    if (!valid) return;
+        for (int d = 0; d < U_DOF; ++d) xch[r * 8 + d] = eps[d];
+    asm volatile("bar.sync 4, 256;" ::: "memory");
+    if (h == 1 || !valid) return;
+#pragma unroll
+    for (int d = 0; d < U_DOF; ++d) eps[d] += xch[r * 8 + d] + s_bout[d];
     if (a.eps_out) {
 #pragma unroll
         for (int d = 0; d < U_DOF; ++d) a.eps_out[grow * U_DOF + d] = eps[d];
         return;
     }
     const StepCoef sc = *reinterpret_cast<const StepCoef*>(vec + US_VEC_SC);
-    const float* z = vec + US_VEC_FILM + r * U_DOF;   // this row's noise, staged by the prefetch warp
+    const float* z = vec + US_VEC_FILM + r * U_DOF;   // this row's noise, staged by the epilogue threads
     float* xr = a.x + grow * U_DOF;
     __align__(16) __nv_bfloat16 xv8[8];
 #pragma unroll
@@ -392,14 +410,14 @@ __device__ __forceinline__ void us_final(const UsArgs& a, const UsHdr& H, int ti
     }
 }
 
-// a unit's epilogue parameters -> shared memory, by the 128 epilogue threads while the unit's
+// a unit's epilogue parameters -> shared memory, by the 256 epilogue threads while the unit's
 // MMAs run: bias / gamma / beta / rbias slices, the tile's FiLM rows as (1 + scale, shift),
 // and for the final layer the step coefficients and the tile's DDPM noise (data-independent
 // Philox blocks, stored as z[row * 7 + d] in the FiLM area)
 __device__ __forceinline__ void us_stage_params(const UsArgs& a, const UsHdr& H, int s, int tile, int n0, float* vec,
                                                 int tid) {
     const int ns = H.ns, nb = H.nb, N = H.N, epi = H.epi;
-    for (int c = tid; c < ns; c += 128) {
+    for (int c = tid; c < ns; c += US_EPI_THREADS) {
         vec[c] = __ldg(H.bias + n0 + c);
         if (epi != EPI_PLAIN) {
             vec[64 + c] = __ldg(H.gamma + n0 + c);
@@ -411,7 +429,7 @@ __device__ __forceinline__ void us_stage_params(const UsArgs& a, const UsHdr& H,
         const int b_lo = tile * nb, b_hi = min(b_lo + nb, a.B) - 1;
         const int p_lo = b_lo / a.S, np = b_hi / a.S - p_lo + 1;
         const float* fb = a.film_b + (size_t)s * 3584 + H.film_col + n0;
-        for (int i = tid; i < np * ns; i += 128) {
+        for (int i = tid; i < np * ns; i += US_EPI_THREADS) {
             const int pp = i / ns, c = i - pp * ns;
             const float* fa = a.film_a + (size_t)(p_lo + pp) * 3584 + H.film_col + n0;
             vec[US_VEC_FILM + pp * 2 * ns + c] = 1.f + (__ldg(fa + c) + __ldg(fb + c));
@@ -424,7 +442,7 @@ __device__ __forceinline__ void us_stage_params(const UsArgs& a, const UsHdr& H,
         const StepCoef* scp = a.sc + s;
         if (__ldg(&scp->ddpm) && !__ldg(&scp->last)) {
             const int per = H.Tv * U_DOF / 4, k = __ldg(&scp->k);
-            for (int i = tid; i < nb * per; i += 128) {
+            for (int i = tid; i < nb * per; i += US_EPI_THREADS) {
                 const int sl = i / per, blk = i - sl * per;
                 const int b = tile * nb + sl;
                 float n4[4] = {0.f, 0.f, 0.f, 0.f};
@@ -476,7 +494,7 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], US_PIPES);   // one commit per MMA pipeline
-            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty[i], US_EPI_THREADS / 32);   // one arrival per epilogue warp
             mbar_init(&vfull[i], 1);
             mbar_init(&vempty[i], 4);
         }
@@ -499,7 +517,7 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
     }
     if (warp >= 4) {
         // the projection's operands as the layered kernel sees them: bf16 weights
-        for (int i = threadIdx.x - 128; i < U_DOF * 64; i += 128)
+        for (int i = threadIdx.x - 128; i < U_DOF * 64; i += US_EPI_THREADS)
             s_wout[i] = __bfloat162float(__float2bfloat16_rn(a.wout[i]));
         if (threadIdx.x - 128 < U_DOF) s_bout[threadIdx.x - 128] = a.bout[threadIdx.x - 128];
     }
@@ -675,9 +693,10 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
             }
         __syncwarp();
     } else if (warp >= 4) {
-        // ---- epilogue warpgroup: thread r owns tile row r (TMEM lane r)
-        const int ew = warp - 4;
-        const int r = ew * 32 + lane;
+        // ---- epilogue warps: thread (q, h) owns tile row r = 32 q + lane (TMEM lane r) and
+        // column half h of the unit's channels
+        const int q = warp & 3, h = (warp - 4) >> 2;
+        const int r = q * 32 + lane, et = threadIdx.x - 128;
         int j = 0;
         for (int s = 0; s < a.n_steps; ++s)
             for (int l = 0; l < a.n_layers; ++l) {
@@ -688,29 +707,30 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
                     const int tile = u / n_sl, slice = u % n_sl;
                     // stage this unit's parameters while its MMAs run (the previous unit's
                     // readers of this buffer all passed its publish barrier)
-                    us_stage_params(a, H, s, tile, slice * ns, s_vec + buf * US_VEC, r);
-                    asm volatile("bar.sync 3, 128;" ::: "memory");
+                    us_stage_params(a, H, s, tile, slice * ns, s_vec + buf * US_VEC, et);
+                    asm volatile("bar.sync 3, 256;" ::: "memory");
                     us_wait(&tfull[buf], ((uint32_t)j >> 1) & 1u, spin);
                     tc_fence_after();
-                    if (r == 0) us_stamp(a, j, 2);
-                    const uint32_t taddr = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(buf * US_PIPES * US_ACC);
+                    if (et == 0) us_stamp(a, j, 2);
+                    const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * US_PIPES * US_ACC);
                     float* red = s_red + (j & 1) * (US_RED / 2);
+                    float* xch = s_red + ((j + 1) & 1) * (US_RED / 2);   // the other parity: free during this unit
                     const float* vec = s_vec + buf * US_VEC;
                     if (a.dbg & 1) {   // knob: no epilogue work
                     } else if (epi == EPI_FINAL)
-                        us_final(a, H, tile, taddr, red, vec, s_wout, s_bout, r, lane, ew);
+                        us_final(a, H, tile, taddr, red, xch, vec, s_wout, s_bout, r, lane, q, h);
                     else if (ns == 32)
-                        us_epilogue<32, 1>(a, H, tile, slice, taddr, red, vec, r, lane, ew);
+                        us_epilogue<32, 1>(a, H, tile, slice, taddr, red, vec, r, lane, q, h);
                     else if (N == 64)
-                        us_epilogue<16, 2>(a, H, tile, slice, taddr, red, vec, r, lane, ew);
+                        us_epilogue<16, 2>(a, H, tile, slice, taddr, red, vec, r, lane, q, h);
                     else
-                        us_epilogue<16, 1>(a, H, tile, slice, taddr, red, vec, r, lane, ew);
+                        us_epilogue<16, 1>(a, H, tile, slice, taddr, red, vec, r, lane, q, h);
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[buf]);
                     // publish the unit: every epilogue thread's stores precede the release
-                    asm volatile("bar.sync 2, 128;" ::: "memory");
-                    if (r == 0) {
+                    asm volatile("bar.sync 2, 256;" ::: "memory");
+                    if (et == 0) {
                         us_stamp(a, j, 3);
                         red_release_gpu(a.done, 1u);
                     }

@@ -3,7 +3,8 @@ Run:  PS_NO_GRAPH=1 PS_PERSIST=1 PS_PERSIST_TRACE=gpurun_out/trace.bin python to
 Read: python tools/persist_trace.py gpurun_out/trace.bin [step]
 Per layer (one step): units, layer span (last publish - previous layer's last publish),
 and medians / maxima of: wait (counter seen - previous last publish), A load (first chunk
-landed - counter seen), MMA (accumulator ready - first chunk), epilogue (publish - ready)."""
+landed - counter seen), MMA (accumulator ready - first chunk), epilogue (publish - ready),
+and the pipeline-0 MMA warp's issue loop (last commit - first chunk)."""
 import sys
 import numpy as np
 
@@ -48,7 +49,7 @@ def main():
     prev_last = None
     tot = 0
     print(f"grid {grid}, {nl} layers, step {step}")
-    print("layer units  span_us  wait_med wait_max  A_med  A_max  mma_med mma_max  epi_med epi_max | MMA-warp kcyc: a_wait b_wait commit issue | tfull->vfull_us pf_start-t1 pf_dur | loop_us commit->ready_us | SM MHz")
+    print("layer units  span_us  wait_med wait_max  A_med  A_max  mma_med mma_max  epi_med epi_max  issue_loop_us")
     if step > 0:
         prev_last = max(r[3] for r in rec[(step - 1, nl - 1)])
     t_start = prev_last
@@ -61,8 +62,7 @@ def main():
         e = (r[:, 3] - r[:, 2]) / 1e3
         span = (last - prev_last) / 1e3 if prev_last is not None else float("nan")
         print(f"{l:5d} {units[l]:5d} {span:8.2f} {np.median(w):8.2f} {w.max():8.2f} {np.median(a_):6.2f} {a_.max():6.2f}"
-              f" {np.median(m):7.2f} {m.max():7.2f} {np.median(e):7.2f} {e.max():7.2f} | "
-              f"{np.median(r[:, 4]) / 1e3:6.2f} {np.median(r[:, 5]) / 1e3:6.2f} {np.median(r[:, 6]) / 1e3:6.2f} {np.median(r[:, 7]) / 1e3:6.2f} | {np.median(r[:, 2] - r[:, 8]) / 1e3:6.2f} {np.median(r[:, 9] - r[:, 1]) / 1e3:6.2f} {np.median(r[:, 10] - r[:, 9]) / 1e3:6.2f} | {np.median(r[:, 11] - r[:, 1]) / 1e3:6.2f} {np.median(r[:, 8] - r[:, 11]) / 1e3:6.2f} | {np.median(r[:, 6] / np.maximum(r[:, 11] - r[:, 1], 1)) * 1e3:6.0f}")
+              f" {np.median(m):7.2f} {m.max():7.2f} {np.median(e):7.2f} {e.max():7.2f}  {np.median(r[:, 11] - r[:, 1]) / 1e3:7.2f}")
         prev_last = last
     if t_start is not None:
         print(f"step total {(prev_last - t_start) / 1e3:.1f} us")

@@ -36,3 +36,7 @@ ms3 = timeit(lambda: bl.refine(q3, esdf3, 32, robot, grid, cost, out=outs3), rep
 res["cfg3_refine_ms"] = ms3
 res["cfg3_GBps_alg"] = P * 32 * 10 * 52992 / (ms3 * 1e-3) / 1e9
 print(json.dumps(res))
+# the planner's layout: 4^3 bricks
+esdf3b = bl.esdf_build(bx, grid, layout=bl.ESDF_BRICKED)
+ms3b = timeit(lambda: bl.refine(q3, esdf3b, 32, robot, grid, cost, out=outs3, esdf_layout=bl.ESDF_BRICKED), reps=5)
+print(json.dumps({"cfg3_refine_bricked_ms": ms3b, "cfg3_bricked_GBps_alg": P * 32 * 10 * 52992 / (ms3b * 1e-3) / 1e9}))
