@@ -129,7 +129,8 @@ def _with_persist(mode, f):
         os.environ.pop("PS_PERSIST", None)
 
 
-@pytest.mark.parametrize("P,S,T,k", [(1, 32, 32, 50), (1, 3, 32, 7), (3, 40, 64, 70), (4, 64, 32, 99)])
+@pytest.mark.parametrize("P,S,T,k", [(1, 32, 32, 50), (1, 3, 32, 7), (3, 40, 64, 70), (4, 64, 32, 99),
+                                     (5, 50, 32, 40)])
 def test_persistent_small_batch_forward(samplers, params, P, S, T, k):
     # the persistent all-layer kernel (csrc/unet_small.cu) against the oracle and against the
     # layered kernels on the same inputs (both bf16: agreement at the bf16 rounding level)
