@@ -473,9 +473,7 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
     uint64_t* b_empty = b_full + US_PIPES * US_NBB;
     uint64_t* tfull = b_empty + US_PIPES * US_NBB;
     uint64_t* tempty = tfull + 2;
-    uint64_t* vfull = tempty + 2;
-    uint64_t* vempty = vfull + 2;
-    UsHdr* s_hdr = reinterpret_cast<UsHdr*>(vempty + 2);
+    UsHdr* s_hdr = reinterpret_cast<UsHdr*>(tempty + 2);
     UsGroup* s_grp = reinterpret_cast<UsGroup*>(s_hdr + a.n_layers);
     UsTap* s_tap = reinterpret_cast<UsTap*>(s_grp + a.n_grp_all);
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(
@@ -495,8 +493,6 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], US_PIPES);   // one commit per MMA pipeline
             mbar_init(&tempty[i], US_EPI_THREADS / 32);   // one arrival per epilogue warp
-            mbar_init(&vfull[i], 1);
-            mbar_init(&vempty[i], 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
