@@ -808,8 +808,9 @@ extern "C" int ps_unet_forward(const void* packed, int mode, const float* x, int
     if (unet_persist_eligible(B, T)) {
         const StepCoef sc{};
         PS_TRY(unet_persist_prepare(L, reinterpret_cast<const char*>(packed), act, B, T, &sc, 1));
-        return unet_persist_launch(L, reinterpret_cast<const char*>(packed), act, const_cast<float*>(x), B, T, S, 0, 0u,
-                                   film_a, film_b, 1, nullptr, nullptr, 0.f, 0.f, eps, st);
+        const int e = unet_persist_launch(L, reinterpret_cast<const char*>(packed), act, const_cast<float*>(x), B, T, S,
+                                          0, 0u, film_a, film_b, 1, nullptr, nullptr, 0.f, 0.f, eps, st);
+        if (e != US_NOT_RESIDENT) return e;
     }
     return unet_eval_tc(L, reinterpret_cast<const char*>(packed), const_cast<float*>(x), B, T, S, film_a, film_b, act, eps, nullptr,
                         st);
@@ -994,9 +995,11 @@ static int sample_loop(const void* packed, int mode, const float* film_a, const 
     noise_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, B, T, S, p0, noise_key);
     PS_CHECK_LAUNCH();
     const char* pk = reinterpret_cast<const char*>(packed);
-    if (mode == 1 && unet_persist_eligible(B, T))   // one persistent launch for every step
-        return unet_persist_launch(L, pk, act, x, B, T, S, p0, noise_key, film_a, film_b, n_steps, q_start, traj, lo,
-                                   hi, nullptr, st);
+    if (mode == 1 && unet_persist_eligible(B, T)) {   // one persistent launch for every step
+        const int e = unet_persist_launch(L, pk, act, x, B, T, S, p0, noise_key, film_a, film_b, n_steps, q_start, traj,
+                                          lo, hi, nullptr, st);
+        if (e != US_NOT_RESIDENT) return e;
+    }
     std::vector<StepCoef> scs;
     step_coefs(coef_h, K, steps_h, n_steps, ddpm, scs);
     for (int i = 0; i < n_steps; ++i) {

@@ -79,7 +79,10 @@ bool make_ts_map(CUtensorMap* tm, const void* base, int B, int Tv, int C, int nb
 bool make_xb_map(CUtensorMap* tm, const void* base, int B, int Tv, int nb);
 bool make_w_map(CUtensorMap* tm, const void* base, int N, int Kp, int box_rows = 0);
 
-// persistent small-batch sampler (unet_small.cu)
+// persistent small-batch sampler (unet_small.cu); unet_persist_launch returns US_NOT_RESIDENT
+// (nothing launched) when its cooperative grid cannot be resident, e.g. while other work holds
+// SMs: callers then run the layered kernels instead
+constexpr int US_NOT_RESIDENT = 100;
 bool unet_persist_eligible(int B, int T);
 int unet_persist_prepare(const Layout& L, const char* packed, void* ws, int B, int T, const StepCoef* sc_h,
                          int n_steps);

@@ -1035,7 +1035,13 @@ int unet_persist_launch(const Layout& L, const char* packed, void* ws, float* x,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     ps_launch_counter().fetch_add(1, std::memory_order_relaxed);
-    if (cudaLaunchKernelEx(&cfg, unet_persist_kernel, a) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+    const cudaError_t le = cudaLaunchKernelEx(&cfg, unet_persist_kernel, a);
+    if (le == cudaErrorCooperativeLaunchTooLarge) {   // the SMs are not all available: caller falls back
+        cudaGetLastError();
+        ps_launch_counter().fetch_sub(1, std::memory_order_relaxed);
+        return US_NOT_RESIDENT;
+    }
+    if (le != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
     if (trace_path) {
         std::vector<unsigned long long> h((size_t)grid_ * a.trace_cap * 20);
         cudaStreamSynchronize(st);
