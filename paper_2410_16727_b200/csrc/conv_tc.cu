@@ -1518,7 +1518,9 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
     // every weight box and the leader issues M = 256 MMAs over both CTAs
     static const bool no_pair = std::getenv("PS_NO_PAIR") != nullptr;
     const int k_total = c.K + (ly.res ? ly.res->K : 0);
-    const bool pair = !no_pair && k_total >= 1024 && ly.epi != EPI_FINAL;   // weight-heavy layers
+    // (never for the 8-channel state view: its 16-B-row boxes have no CTA-pair load path)
+    static const int pair_k = std::getenv("PS_PAIR_K") ? std::atoi(std::getenv("PS_PAIR_K")) : 1024;   // A/B knob
+    const bool pair = !no_pair && k_total >= pair_k && ly.epi != EPI_FINAL && ly.xb_src < 0;   // weight-heavy layers
     // small batches: N-split the N >= 128 layers into two channel slices (whole GroupNorm
     // groups), doubling the CTAs per tile and halving each CTA's weight stream and MMA chain
     static const bool no_split = std::getenv("PS_NO_SPLIT") != nullptr;
