@@ -94,6 +94,9 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--budget", type=float, default=4.0, help="seconds of timed calls per combination")
     ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "sweep.json"))
+    ap.add_argument("--ddpm-cap", type=int, default=1024 * 128,
+                    help="skip ddpm100 combinations above this many trajectory-equivalents (0: no cap)")
+    ap.add_argument("--scheds", default="ddim10,ddpm100")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     params = spec.random_model(spec.ENCODER_CFG3)
@@ -101,11 +104,11 @@ def main():
     Ps = [1, 16, 256, 4096, 16384] if not args.quick else [1, 256]
     Ss = [8, 32, 128] if not args.quick else [32]
     Ts = [32, 64]
-    scheds = ["ddim10", "ddpm100"]
+    scheds = args.scheds.split(",")
     rows = []
     for sched, T, S, P in itertools.product(scheds, Ts, Ss, Ps):
         # the largest ddpm100 combinations take minutes per call: cap trajectories for ddpm100
-        if sched == "ddpm100" and P * S * (T // 32) > 1024 * 128:
+        if sched == "ddpm100" and args.ddpm_cap and P * S * (T // 32) > args.ddpm_cap:
             continue
         cap = 65536 if T == 32 else 32768
         r = run_combo(params, P, S, T, sched, args.budget, base, cap)
