@@ -41,7 +41,7 @@ struct BLParams {
 };
 
 // World term of one configuration (canonical order, see bl_oracle.c:config_world).
-template <bool WANT_GRAD>
+template <bool WANT_GRAD, bool PIPE2 = false>
 __device__ __forceinline__ void config_world(const BLParams& P, const Grid& g, const float (&q)[NJ],
                                              float& wc, float (&gq)[NJ], float& mc, bool& cl_any) {
     f3 X{1.f, 0.f, 0.f}, Y{0.f, 1.f, 0.f}, Z{0.f, 0.f, 1.f};
@@ -73,15 +73,17 @@ __device__ __forceinline__ void config_world(const BLParams& P, const Grid& g, c
         Z = Z2;
         f3 S1{0.f, 0.f, 0.f}, S2{0.f, 0.f, 0.f};
         const int s_end = P.link_start[k + 1];
-        for (int s = P.link_start[k]; s < s_end; ++s) {
-            const float lx = P.sph[s][0], ly = P.sph[s][1], lz = P.sph[s][2], r = P.sph[s][3];
-            f3 p{fmaf(X.x, lx, fmaf(Y.x, ly, fmaf(Z.x, lz, o.x))),
-                 fmaf(X.y, lx, fmaf(Y.y, ly, fmaf(Z.y, lz, o.y))),
-                 fmaf(X.z, lx, fmaf(Y.z, ly, fmaf(Z.z, lz, o.z)))};
+        auto sphere_pos = [&](int s) {
+            const float lx = P.sph[s][0], ly = P.sph[s][1], lz = P.sph[s][2];
+            return f3{fmaf(X.x, lx, fmaf(Y.x, ly, fmaf(Z.x, lz, o.x))),
+                      fmaf(X.y, lx, fmaf(Y.y, ly, fmaf(Z.y, lz, o.y))),
+                      fmaf(X.z, lx, fmaf(Y.z, ly, fmaf(Z.z, lz, o.z)))};
+        };
+        auto accumulate = [&](int s, const f3& p, const TriCell& cell) {
+            const float r = P.sph[s][3];
             f3 gr;
-            bool cl;
-            const float dv = c_trilinear(g, p, gr, cl);
-            cl_any |= cl;
+            const float dv = tri_eval(g, cell, gr);
+            cl_any |= cell.clamped;
             mc = fminf(mc, dv - r);
             const float hinge = (r + P.margin) - dv;
             if (hinge > 0.f) {
@@ -94,6 +96,24 @@ __device__ __forceinline__ void config_world(const BLParams& P, const Grid& g, c
                     S2.x = S2.x + gp.x; S2.y = S2.y + gp.y; S2.z = S2.z + gp.z;
                 }
             }
+        };
+        // two spheres per step: both cells' corner loads issued before either is evaluated;
+        // the accumulation order stays sequential (bit-identical to the oracle)
+        int s = P.link_start[k];
+        if (PIPE2)
+        for (; s + 1 < s_end; s += 2) {
+            const f3 pa = sphere_pos(s), pb = sphere_pos(s + 1);
+            TriCell ca, cb;
+            tri_gather(g, pa, ca);
+            tri_gather(g, pb, cb);
+            accumulate(s, pa, ca);
+            accumulate(s + 1, pb, cb);
+        }
+        for (; s < s_end; ++s) {
+            const f3 pa = sphere_pos(s);
+            TriCell ca;
+            tri_gather(g, pa, ca);
+            accumulate(s, pa, ca);
         }
         if (WANT_GRAD) {
 #pragma unroll
@@ -183,8 +203,10 @@ __device__ __forceinline__ float warp_min(float v) {
 }
 
 // MODE 0: refine (n_iters steps + final cost/flags).  MODE 1: cost + gradient only.
-template <int WPL, int MODE>
-__global__ void __launch_bounds__(512) bl_refine_kernel(const __grid_constant__ BLParams P) {
+// LB: block-size bound -- 512 for throughput (one problem's 16 trajectories per block share
+// the L1), 64 for small batches (up to 255 registers: the two-sphere gathers stay in flight)
+template <int WPL, int MODE, int LB = 512, bool PIPE2 = false>
+__global__ void __launch_bounds__(LB) bl_refine_kernel(const __grid_constant__ BLParams P) {
     const int lane = threadIdx.x & 31;
     const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (b >= P.B) return;  // whole warp exits together
@@ -210,7 +232,7 @@ __global__ void __launch_bounds__(512) bl_refine_kernel(const __grid_constant__ 
         for (int w = 0; w < WPL; ++w) {
             float wc, mc, gq[NJ];
             bool cl;
-            config_world<true>(P, g, q[w], wc, gq, mc, cl);
+            config_world<true, PIPE2>(P, g, q[w], wc, gq, mc, cl);
             cl_lane |= cl;
             ct[w] = wc + sm[w];
             const int t = lane * WPL + w;
@@ -236,7 +258,7 @@ __global__ void __launch_bounds__(512) bl_refine_kernel(const __grid_constant__ 
         for (int w = 0; w < WPL; ++w) {
             float wc, mc;
             bool cl;
-            config_world<true>(P, g, q[w], wc, gw[w], mc, cl);
+            config_world<true, PIPE2>(P, g, q[w], wc, gw[w], mc, cl);
         }
         smooth_terms<WPL, true>(P, q, lane, sm, gs);
 #pragma unroll
@@ -258,7 +280,7 @@ __global__ void __launch_bounds__(512) bl_refine_kernel(const __grid_constant__ 
     for (int w = 0; w < WPL; ++w) {
         float wc, mc, gq[NJ];
         bool cl;
-        config_world<false>(P, g, q[w], wc, gq, mc, cl);
+        config_world<false, PIPE2>(P, g, q[w], wc, gq, mc, cl);
         ct[w] = wc + sm[w];
         mc_lane = fminf(mc_lane, mc);
         cl_lane |= cl;
@@ -281,7 +303,7 @@ __global__ void __launch_bounds__(512) bl_refine_kernel(const __grid_constant__ 
                     const float q1 = (w + 1 < WPL) ? q[w + 1 < WPL ? w + 1 : w][k] : qn[k];
                     qi[k] = fmaf(f, q1 - q[w][k], q[w][k]);
                 }
-                config_world<false>(P, g, qi, wc, gq, mc, cl);
+                config_world<false, PIPE2>(P, g, qi, wc, gq, mc, cl);
                 mc_lane = fminf(mc_lane, mc);
                 cl_lane |= cl;
             }
@@ -549,6 +571,20 @@ static int launch_bl(const BLParams& P, cudaStream_t st) {
     // a block holds 512 / 32 = 16 trajectories of one problem: seeds of a problem move through
     // the same part of its ESDF, so their gathers share the SM's L1 (PS_REFINE_THREADS: A/B)
     static const int threads = std::getenv("PS_REFINE_THREADS") ? std::atoi(std::getenv("PS_REFINE_THREADS")) : 512;
+    static const int small_b = std::getenv("PS_REFINE_SMALL_B") ? std::atoi(std::getenv("PS_REFINE_SMALL_B")) : 512;
+    if (P.B <= small_b) {   // latency-bound: few warps, each with as many registers as it wants
+        const long long blocks = ((long long)P.B * 32 + 63) / 64;
+        static const bool pipe2 = std::getenv("PS_REFINE_NO_PIPE2") == nullptr;   // A/B knob
+        if (P.T == 32) {
+            if (pipe2) bl_refine_kernel<1, MODE, 64, true><<<(unsigned)blocks, 64, 0, st>>>(P);
+            else bl_refine_kernel<1, MODE, 64, false><<<(unsigned)blocks, 64, 0, st>>>(P);
+        } else {
+            if (pipe2) bl_refine_kernel<2, MODE, 64, true><<<(unsigned)blocks, 64, 0, st>>>(P);
+            else bl_refine_kernel<2, MODE, 64, false><<<(unsigned)blocks, 64, 0, st>>>(P);
+        }
+        PS_CHECK_LAUNCH();
+        return PS_OK;
+    }
     const long long blocks = ((long long)P.B * 32 + threads - 1) / threads;
     if (P.T == 32)
         bl_refine_kernel<1, MODE><<<(unsigned)blocks, threads, 0, st>>>(P);

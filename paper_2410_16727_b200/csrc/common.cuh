@@ -91,18 +91,26 @@ __host__ __device__ __forceinline__ size_t esdf_brick_index(int i, int j, int k,
 // Trilinear value + in-cell analytic gradient + clamp flag; generalises
 // planseed/_kernels.py:_bilinear (:23-57) to 3-D.  Manual fp32 weights, never
 // texture filtering (8-bit fractional weights would break parity).
-__device__ __forceinline__ float c_trilinear(const Grid& g, const f3& p, f3& grad, bool& clamped) {
+// Split in two stages so a caller can have several lookups' gathers in flight: tri_gather
+// (cell, fractions, the 8 corner loads) and tri_eval (the interpolation arithmetic).
+struct TriCell {
+    float v000, v001, v010, v011, v100, v101, v110, v111;
+    float tx, ty, tz;
+    bool clamped;
+};
+
+__device__ __forceinline__ void tri_gather(const Grid& g, const f3& p, TriCell& c) {
     float ux = (p.x - g.ox) * g.inv_h;
     float uy = (p.y - g.oy) * g.inv_h;
     float uz = (p.z - g.oz) * g.inv_h;
-    clamped = (ux < 0.f) | (ux > (float)(g.nx - 1)) | (uy < 0.f) | (uy > (float)(g.ny - 1)) |
-              (uz < 0.f) | (uz > (float)(g.nz - 1));
+    c.clamped = (ux < 0.f) | (ux > (float)(g.nx - 1)) | (uy < 0.f) | (uy > (float)(g.ny - 1)) |
+                (uz < 0.f) | (uz > (float)(g.nz - 1));
     float fi = fminf(fmaxf(floorf(ux), 0.f), (float)(g.nx - 2));
     float fj = fminf(fmaxf(floorf(uy), 0.f), (float)(g.ny - 2));
     float fk = fminf(fmaxf(floorf(uz), 0.f), (float)(g.nz - 2));
-    float tx = fminf(fmaxf(ux - fi, 0.f), 1.f);
-    float ty = fminf(fmaxf(uy - fj, 0.f), 1.f);
-    float tz = fminf(fmaxf(uz - fk, 0.f), 1.f);
+    c.tx = fminf(fmaxf(ux - fi, 0.f), 1.f);
+    c.ty = fminf(fmaxf(uy - fj, 0.f), 1.f);
+    c.tz = fminf(fmaxf(uz - fk, 0.f), 1.f);
     const float* v;
     size_t sx, sy, sz;
     if (g.brick) {   // neighbour steps stay inside a brick unless the cell sits on its edge
@@ -117,12 +125,15 @@ __device__ __forceinline__ float c_trilinear(const Grid& g, const f3& p, f3& gra
         sx = (size_t)g.ny * (size_t)g.nz;
         v = g.v + ((size_t)(int)fi * sx + (size_t)(int)fj * sy + (size_t)(int)fk);
     }
-    float v000 = __ldg(v), v001 = __ldg(v + sz), v010 = __ldg(v + sy), v011 = __ldg(v + sy + sz);
-    float v100 = __ldg(v + sx), v101 = __ldg(v + sx + sz), v110 = __ldg(v + sx + sy),
-          v111 = __ldg(v + sx + sy + sz);
-    float z00 = v001 - v000, z01 = v011 - v010, z10 = v101 - v100, z11 = v111 - v110;
-    float c00 = fmaf(tz, z00, v000), c01 = fmaf(tz, z01, v010);
-    float c10 = fmaf(tz, z10, v100), c11 = fmaf(tz, z11, v110);
+    c.v000 = __ldg(v); c.v001 = __ldg(v + sz); c.v010 = __ldg(v + sy); c.v011 = __ldg(v + sy + sz);
+    c.v100 = __ldg(v + sx); c.v101 = __ldg(v + sx + sz); c.v110 = __ldg(v + sx + sy); c.v111 = __ldg(v + sx + sy + sz);
+}
+
+__device__ __forceinline__ float tri_eval(const Grid& g, const TriCell& c, f3& grad) {
+    const float tx = c.tx, ty = c.ty, tz = c.tz;
+    float z00 = c.v001 - c.v000, z01 = c.v011 - c.v010, z10 = c.v101 - c.v100, z11 = c.v111 - c.v110;
+    float c00 = fmaf(tz, z00, c.v000), c01 = fmaf(tz, z01, c.v010);
+    float c10 = fmaf(tz, z10, c.v100), c11 = fmaf(tz, z11, c.v110);
     float e0 = c01 - c00, e1 = c11 - c10;
     float c0 = fmaf(ty, e0, c00), c1 = fmaf(ty, e1, c10);
     float dxv = c1 - c0;
@@ -132,6 +143,13 @@ __device__ __forceinline__ float c_trilinear(const Grid& g, const f3& p, f3& gra
     float dzv = fmaf(tx, zy1 - zy0, zy0);
     grad = f3{dxv * g.inv_h, dyv * g.inv_h, dzv * g.inv_h};
     return d;
+}
+
+__device__ __forceinline__ float c_trilinear(const Grid& g, const f3& p, f3& grad, bool& clamped) {
+    TriCell c;
+    tri_gather(g, p, c);
+    clamped = c.clamped;
+    return tri_eval(g, c, grad);
 }
 
 __device__ __forceinline__ float warp_sum_butterfly(float v) {
