@@ -571,8 +571,8 @@ static int launch_bl(const BLParams& P, cudaStream_t st) {
     // a block holds 512 / 32 = 16 trajectories of one problem: seeds of a problem move through
     // the same part of its ESDF, so their gathers share the SM's L1 (PS_REFINE_THREADS: A/B)
     static const int threads = std::getenv("PS_REFINE_THREADS") ? std::atoi(std::getenv("PS_REFINE_THREADS")) : 512;
-    static const int small_b = std::getenv("PS_REFINE_SMALL_B") ? std::atoi(std::getenv("PS_REFINE_SMALL_B")) : 512;
-    if (P.B <= small_b) {   // latency-bound: few warps, each with as many registers as it wants
+    static const int small_b = std::getenv("PS_REFINE_SMALL_B") ? std::atoi(std::getenv("PS_REFINE_SMALL_B")) : 1024;
+    if (P.B <= small_b) {   // latency-bound (B <= 1024; config 2 at 2048 is faster with 16-warp blocks): few warps, each with up to 255 registers
         const long long blocks = ((long long)P.B * 32 + 63) / 64;
         static const bool pipe2 = std::getenv("PS_REFINE_NO_PIPE2") == nullptr;   // A/B knob
         if (P.T == 32) {
