@@ -715,8 +715,12 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
                     if (a.dbg & 1) {   // knob: no epilogue work
                     } else if (epi == EPI_FINAL)
                         us_final(a, H, tile, taddr, red, xch, vec, s_wout, s_bout, r, lane, q, h);
-                    else if (ns == 32)
+                    else if (ns == 32 && N == 256)
                         us_epilogue<32, 1>(a, H, tile, slice, taddr, red, vec, r, lane, q, h);
+                    else if (ns == 32 && N == 128)
+                        us_epilogue<32, 2>(a, H, tile, slice, taddr, red, vec, r, lane, q, h);
+                    else if (ns == 32)
+                        us_epilogue<32, 4>(a, H, tile, slice, taddr, red, vec, r, lane, q, h);
                     else if (N == 64)
                         us_epilogue<16, 2>(a, H, tile, slice, taddr, red, vec, r, lane, q, h);
                     else
@@ -743,6 +747,16 @@ __global__ void __launch_bounds__(US_THREADS, 1) unet_persist_kernel(const __gri
 // ===========================================================================
 // host side
 // ===========================================================================
+static int us_n_sm() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
 static size_t kpad64(int K) { return (size_t)((K + 63) / 64) * 64; }
 
 static int us_build_layer(const Layout& L, const char* packed, const TcLayer& ly, int B, UsMaps& m, UsHdr& o,
@@ -753,7 +767,12 @@ static int us_build_layer(const Layout& L, const char* packed, const TcLayer& ly
     const int N = c.N;
     const __nv_bfloat16* W = reinterpret_cast<const __nv_bfloat16*>(packed);
     const bool fin = ly.epi == EPI_FINAL;
-    o.ns = fin ? 64 : (N == 256 ? 32 : 16);   // whole GroupNorm groups (N / 8 channels)
+    // whole GroupNorm groups (N / 8 channels); 32-channel slices for the 64/128-wide layers when
+    // 16-channel slices would give more units than a few per SM (larger batches)
+    static const int wide_units = std::getenv("PS_PERSIST_WIDE_UNITS") ? std::atoi(std::getenv("PS_PERSIST_WIDE_UNITS"))
+                                                                        : us_n_sm();   // measured: B=256 19.5 -> 17.3 ms
+    const int tiles_ = (B + 128 / ly.Tv - 1) / (128 / ly.Tv);
+    o.ns = fin ? 64 : (N == 256 ? 32 : (tiles_ * (N / 16) > wide_units ? 32 : 16));
     if (N % o.ns) return PS_FAIL(PS_ERR_SHAPE);
     o.N = N;
     o.n_slices = N / o.ns;
@@ -864,15 +883,6 @@ static size_t us_smem_bytes(int n_layers, int n_grp, int n_tap) {
            n_layers * sizeof(UsHdr) + n_grp * sizeof(UsGroup) + n_tap * sizeof(UsTap) + 32;
 }
 
-static int us_n_sm() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return n;
-}
 
 bool unet_persist_eligible(int B, int T) {
     if (T != 32 && T != 64) return false;
