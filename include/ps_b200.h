@@ -132,6 +132,19 @@ int ps_sample(const void* packed, int mode, const float* film_a, int P, int S, i
 /* n standard normals of the sampler's noise stream (test hook). */
 int ps_noise_probe(float* out, int n, int step, int prob, int seed, unsigned key, void* stream);
 
+/* Test hooks for the fused-epilogue transform (normal4_tc, csrc/tc_ptx.cuh) -- the noise the
+ * DDPM epilogues inject (the x_{k-1} draw of planseed's sampler, diffusion.py:535-556, with the
+ * reference's PCG64 stream replaced by the keyed Philox stream).  Device pointers:
+ *   ps_box_muller_probe: z[2i], z[2i+1] = transform of raw words (a[i], b[i]);
+ *   ps_normal4_probe:    out[4*blk .. 4*blk+3] for blocks 0..n_blocks-1 of (step, prob, seed);
+ *   ps_noise_scan:       every block of n_prob x n_seed x n_blk at `step`: adds the count of
+ *                        non-finite draws to *nonfinite, max |z| (float bits) to *maxabs_bits,
+ *                        sum z and sum z^2 to moments[0..1] (all zero-initialised by the caller). */
+int ps_box_muller_probe(const unsigned* a, const unsigned* b, int n, float* z, void* stream);
+int ps_normal4_probe(float* out, int n_blocks, int step, int prob, int seed, unsigned key, void* stream);
+int ps_noise_scan(int step, int n_prob, int n_seed, int n_blk, unsigned key, unsigned long long* nonfinite,
+                  unsigned* maxabs_bits, double* moments, void* stream);
+
 /* ============ Reference profile: planseed's own planar / FC / DDIM path ============
  * dtype 0 = float64 (parity with planseed), 1 = float32.  Argument lists follow the
  * numba kernels' 18 positional args (src/_kernels.py:165-176, built by _kernel_args,

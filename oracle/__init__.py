@@ -8,12 +8,14 @@ __graft_entry__.smoke() and by bench.py's CPU legs (cpu_baseline and
   oracle/c/bl_oracle.c   canonical-fp32 C restatement of the BASELINE-profile
                          refinement (bit-exact target for the CUDA kernels)
   oracle/bl_numpy.py     independent float64 numpy restatement of the same
-  oracle/ref_numpy.py    numpy restatement of planseed's own kernels (ref profile)
   oracle/unet_numpy.py   encoder / U-Net / DDPM restatement (BASELINE profile)
+  oracle/pipeline_cpu.py the BASELINE planning pipeline on host cores (CPU baseline)
 
-Parity pins: the ref-profile restatement is checked against planseed itself
-(imported from /root/reference when present) and against golden fixtures in
-tests/golden/ generated from planseed by tools/make_golden.py.
+The ref profile (planseed's own planar / FC / DDIM / Armijo path) needs no
+restatement: its oracle is planseed itself (imported from /root/reference when
+present) and the golden fixtures in tests/golden/ generated from planseed by
+tools/make_golden.py.  The BASELINE restatements are pinned to torch.nn.functional
+and to planseed by tests/test_unet_oracle_cpu.py and tests/test_bl_oracle.py.
 """
 
 from __future__ import annotations

@@ -241,18 +241,24 @@ def noise(step: int, problems: np.ndarray, seeds: np.ndarray, T: int, D: int = s
 # ----------------------------------------------------------------------------
 
 def sample(params, arch, cond, q_start, S, p0=0, T=spec.T_DEFAULT, betas=None, steps=None,
-           dtype=np.float64, x_init=None, return_eps=False):
+           dtype=np.float64, x_init=None, return_eps=False, problems=None, table_dtype=np.float32):
     """Seed generation for P problems x S seeds.
 
     steps=None: full K-step stochastic DDPM (posterior mean + sigma z).
     steps=[...]: deterministic DDIM (eta=0) over the given 1-based indices, as
     planseed's _ddim_core (diffusion.py:535-556).
+    problems: explicit global problem indices of the rows of cond (default p0 .. p0+P-1), so a
+    subset of a large batch can be checked (problems are independent: per-sample GroupNorm,
+    per-problem FiLM, noise keyed by the global index).
+    table_dtype: float32 = the device's coefficient tables; float64 = exact (planseed bridge).
     Returns physical trajectories (P*S, T, 7) with row 0 := q_start."""
     betas = spec.cosine_betas() if betas is None else betas
     K = betas.shape[0]
-    tab = spec.sampler_tables(betas)
+    tab = spec.sampler_tables(betas, dtype=table_dtype)
     P = cond.shape[0]
-    prob = np.repeat(np.arange(p0, p0 + P), S)
+    gp = np.arange(p0, p0 + P) if problems is None else np.asarray(problems)
+    assert gp.shape == (P,)
+    prob = np.repeat(gp, S)
     sidx = np.tile(np.arange(S), P)
     x = noise(0, prob, sidx, T) if x_init is None else np.asarray(x_init)
     x = x.astype(dtype)

@@ -50,6 +50,9 @@ _SIGS = {
     "ps_sample": [_vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int,
                   ctypes.c_uint, _vp, _c_f, _c_f, _vp, _vp, _vp],
     "ps_noise_probe": [_vp, _c_int, _c_int, _c_int, _c_int, ctypes.c_uint, _vp],
+    "ps_box_muller_probe": [_vp, _vp, _c_int, _vp, _vp],
+    "ps_normal4_probe": [_vp, _c_int, _c_int, _c_int, _c_int, ctypes.c_uint, _vp],
+    "ps_noise_scan": [_c_int, _c_int, _c_int, _c_int, ctypes.c_uint, _vp, _vp, _vp, _vp],
     "ps_ref_cost_terms": [_c_int, _vp, _c_int, _c_int, _c_int] + _REF_ARM + [_c_int, _vp, _vp, _vp, _vp,
                                                                           _vp],
     "ps_ref_optimize": [_c_int, _vp, _c_int, _c_int, _c_int, _c_int, _c_d, _c_d, _c_d, _c_int, _c_d, _c_d]

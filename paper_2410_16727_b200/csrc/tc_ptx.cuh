@@ -299,23 +299,30 @@ __device__ __forceinline__ float normal_tc(uint32_t step, uint32_t prob, uint32_
     return (comp & 1u) ? rad * sinf(ang) : rad * cosf(ang);
 }
 
-// the 4 normals of Philox block `blk` (elements 4*blk .. 4*blk+3), as normal_tc but with the
-// SFU forms of log / sin / cos (abs. error < 1e-5 against the exact transform, see
-// tests/test_sampler_gpu.py); used by the fused DDPM epilogue
+// Box-Muller pair of two raw Philox words (spec.py "Counter-based noise"), the fused-epilogue form.
+// The radius uses the full-precision logf: near u1 = 1 the true -2 ln u1 is ~1.2e-7, below the
+// absolute error of the SFU lg2.approx, whose sign could then flip (sqrtf of a negative -> NaN)
+// or inflate the radius by ~4e-4.  logf is within 1 ulp, so the radius is within ~1e-6 of the exact
+// transform for every one of the 2^24 values of a >> 8; the fmaxf guards u1 = 1 exactly.  The angle
+// is taken centred, 2 pi (u2 - 1/2) in [-pi, pi) (u2 - 1/2 is exact), where the SFU sincos holds its
+// documented 2^-21.4 absolute error; cos / sin of the centred angle are the negated uncentred ones.
+// tests/test_noise_gpu.py checks both words exhaustively against the float64 transform.
+__device__ __forceinline__ void box_muller_tc(uint32_t a, uint32_t b, float& z0, float& z1) {
+    const float u1 = ((float)(a >> 8) + 1.0f) * (1.0f / 16777216.0f);
+    const float u2 = (float)(b >> 8) * (1.0f / 16777216.0f);
+    const float rad = sqrtf(fmaxf(-2.0f * logf(u1), 0.0f));
+    float sn, cs;
+    __sincosf(6.28318530717958648f * (u2 - 0.5f), &sn, &cs);
+    z0 = -rad * cs;
+    z1 = -rad * sn;
+}
+
+// the 4 normals of Philox block `blk` (elements 4*blk .. 4*blk+3); used by the fused DDPM epilogues
 __device__ __forceinline__ void normal4_tc(uint32_t step, uint32_t prob, uint32_t seed, uint32_t blk, uint32_t key,
                                            float (&n)[4]) {
     const uint4 r = philox_tc(make_uint4(blk, step, prob, seed), key, 0x5EED5EEDu);
-    const uint32_t ab[4] = {r.x, r.y, r.z, r.w};
-#pragma unroll
-    for (int pr = 0; pr < 2; ++pr) {
-        const float u1 = ((float)(ab[2 * pr] >> 8) + 1.0f) * (1.0f / 16777216.0f);
-        const float u2 = (float)(ab[2 * pr + 1] >> 8) * (1.0f / 16777216.0f);
-        const float rad = sqrtf(-2.0f * __logf(u1));
-        float sn, cs;
-        __sincosf(6.28318530717958648f * u2, &sn, &cs);
-        n[2 * pr] = rad * cs;
-        n[2 * pr + 1] = rad * sn;
-    }
+    box_muller_tc(r.x, r.y, n[0], n[1]);
+    box_muller_tc(r.z, r.w, n[2], n[3]);
 }
 
 template <int NV>

@@ -380,7 +380,9 @@ class SamplerTables:
     sig: np.ndarray
 
 
-def sampler_tables(betas: np.ndarray) -> SamplerTables:
+def sampler_tables(betas: np.ndarray, dtype=np.float32) -> SamplerTables:
+    """float32 by default (the device tables); dtype=np.float64 keeps the exact coefficients
+    (used by the oracle's bridge to planseed's float64 sampler)."""
     K = betas.shape[0]
     ab = np.cumprod(1.0 - betas)
     ab_prev = np.concatenate([[1.0], ab[:-1]])
@@ -389,7 +391,7 @@ def sampler_tables(betas: np.ndarray) -> SamplerTables:
     c0 = np.sqrt(ab_prev) * betas / (1.0 - ab)
     c1 = np.sqrt(al) * (1.0 - ab_prev) / (1.0 - ab)
     var = betas * (1.0 - ab_prev) / (1.0 - ab)
-    f = lambda a: np.concatenate([z, a]).astype(np.float32)
+    f = lambda a: np.concatenate([z, a]).astype(dtype)
     return SamplerTables(sq=f(np.sqrt(ab)), sq1m=f(np.sqrt(1.0 - ab)), rsq=f(1.0 / np.sqrt(ab)),
                          c0=f(c0), c1=f(c1), sig=f(np.sqrt(var)))
 
