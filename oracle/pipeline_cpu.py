@@ -33,8 +33,9 @@ def _init_worker(enc_layers: int):
 
 
 def plan_problem(p: int, seed: int = 0, S: int = 32, T: int = 32, steps=None, n_iters: int = 10,
-                 enc_layers: int = 5):
-    """Plan one synthetic config-3 problem on one core; returns (best, traj_best, seconds)."""
+                 enc_layers: int = 5, full: bool = False, dtype=np.float32):
+    """Plan one synthetic config-3 problem on one core; returns (best, traj_best, seconds), or with
+    full=True (best, refined (S,T,7), cost (S,), feasible (S,), seconds)."""
     import oracle
     from oracle import unet_numpy as un
     from paper_2410_16727_b200 import spec, synth
@@ -46,12 +47,14 @@ def plan_problem(p: int, seed: int = 0, S: int = 32, T: int = 32, steps=None, n_
     pb = synth.config3_problems(1, p0=p, seed=seed) if enc_layers == 5 else synth.config0_problems(1, p0=p, seed=seed)
     esdf = oracle.esdf_build(pb.boxes[0], grid)
     cond = un.encode_problems(_STATE["params"], _STATE["enc"], pb.images, pb.q_start, pb.goal,
-                              dtype=np.float32)
+                              dtype=dtype)
     seeds = un.sample(_STATE["params"], spec.UNetArch(), cond, pb.q_start, S, p0=p, T=T, steps=steps,
-                      dtype=np.float32)
+                      dtype=dtype)
     ps = oracle.BLProblemSet(robot, grid, cost, esdf[None], grid.n_nodes)
     q, c, f, _ = oracle.bl_refine(ps, seeds.astype(np.float32), S, n_iters)
     best = int(oracle.select(c, f, S)[0])
+    if full:
+        return best, q, c, f, time.perf_counter() - t0
     return best, q[best], time.perf_counter() - t0
 
 

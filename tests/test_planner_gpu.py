@@ -1,0 +1,219 @@
+"""End-to-end parity of the benchmarked path: BLPlanner.plan_batch (ESDF build -> encoder -> DDPM
+sampler -> refinement -> flags -> best seed), config-3 shapes (2 x 240x320 depth images, 5-layer
+encoder, 128^3 ESDF from 20 boxes per problem, T=32, 100 DDPM steps, 10 refinement iterations),
+against the oracle pipeline -- the batched counterpart of planseed's plan_diffusion
+(pipeline.py:172-209; its determinism / row-0 tests, tests/test_pipeline.py:109-157).
+
+Bounds (written here):
+  * ESDF: bit-exact (canonical fp32 C oracle).
+  * fp32 mode (mode 0): seeds within 1e-4 rad max-abs of the float64 oracle sampler (north
+    star); refinement of the GPU's own seeds by the C oracle bit-exact (trajectories, costs,
+    flags, best index); the full oracle pipeline (float64 seeds -> C refinement) gives the same
+    flags and best indices, and refined trajectories within 1e-4 rad wherever a trajectory's
+    seed agreed (the trilinear ESDF is only C0 across cell faces: DESIGN.md §5.3).
+  * bf16 mode (mode 1, tcgen05): seeds within the bf16 bound of test_tc_gpu.py (RMS 2e-2 rad,
+    max 0.15 rad) on a problem subset checked against the float64 oracle; refinement of the
+    GPU's own seeds bit-exact against the C oracle for the whole batch; flag / best-index
+    agreement with the float64 oracle pipeline reported as a rate with a floor.
+P = 64 problems x 32 seeds = 2048 trajectories puts B*T = 65,536 above the persistent kernel's
+8,192 limit, so the layered tcgen05 kernels with the fused DDPM posterior + Philox epilogue
+(conv_tc.cu EPI_FINAL) run -- the path bench.py times.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import unet_numpy as un
+from paper_2410_16727_b200 import spec, synth
+
+pytestmark = pytest.mark.gpu
+
+S = 32
+ENC = spec.ENCODER_CFG3
+ARCH = spec.UNetArch()
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test without a CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def params():
+    return spec.random_model(ENC)
+
+
+def _planner(params, mode, P):
+    from paper_2410_16727_b200.planner import BLPlanner
+    return BLPlanner(params, ENC, mode=mode, S=S, max_problems=P)
+
+
+def _unbrick(planner, P):
+    from paper_2410_16727_b200 import bl
+    e = planner.esdf[:P]
+    if planner.esdf_layout == bl.ESDF_BRICKED:
+        e = bl.unbrick(e, planner.grid)
+    return e.cpu().numpy()
+
+
+_SEEDS = {}
+
+
+def _oracle_seeds(params, pb, idx):
+    """float64 oracle encoder + DDPM-100 sampler for the problems at batch positions idx
+    (~40 s per 128 trajectories on 8 host cores; cached per batch)."""
+    key = (pb.p0, pb.P, tuple(int(i) for i in idx))
+    if key not in _SEEDS:
+        cond = un.encode_problems(params, ENC, pb.images[idx], pb.q_start[idx], pb.goal[idx])
+        _SEEDS[key] = un.sample(params, ARCH, cond, pb.q_start[idx], S, problems=pb.p0 + np.asarray(idx))
+    return _SEEDS[key]
+
+
+def _oracle_refine(oracle_lib, planner, esdf, seeds):
+    ps = oracle_lib.BLProblemSet(planner.robot, planner.grid, planner.cost, esdf, planner.grid.n_nodes)
+    q, c, f, cl = oracle_lib.bl_refine(ps, seeds.astype(np.float32), S, planner.cost.n_iters)
+    return q, c, f, cl, oracle_lib.select(c, f, S)
+
+
+def _rows(idx):
+    return np.concatenate([np.arange(i * S, (i + 1) * S) for i in idx])
+
+
+def _check_finite(r):
+    for name in ("trajectories", "cost"):
+        assert np.isfinite(getattr(r, name)).all(), name
+
+
+class TestFp32Pipeline:
+    P = 4
+
+    @pytest.fixture(scope="class")
+    def run(self, torch_cuda, params):
+        pl = _planner(params, 0, self.P)
+        pb = synth.config3_problems(self.P, p0=5, seed=0)
+        host = pl.plan_batch(pb.images, pb.q_start, pb.goal, pb.boxes, p0=pb.p0)
+        dev = pl.plan_batch_device(*(torch_cuda.as_tensor(a).cuda() for a in
+                                     (pb.images, pb.q_start, pb.goal, pb.boxes)), p0=pb.p0)
+        return pl, pb, host, dev
+
+    def test_host_api_equals_device_api_and_finite(self, run):
+        pl, pb, host, dev = run
+        _check_finite(host)
+        for f in ("trajectories", "cost", "feasible", "best_index"):
+            assert np.array_equal(np.asarray(getattr(host, f)), getattr(dev, f).cpu().numpy()), f
+
+    def test_esdf_bitwise(self, run, oracle_lib):
+        pl, pb, _, _ = run
+        esdf = _unbrick(pl, self.P)
+        for p in range(self.P):
+            assert np.array_equal(esdf[p], oracle_lib.esdf_build(pb.boxes[p], pl.grid))
+
+    def test_seeds_within_1e4_rad(self, run, params):
+        pl, pb, _, dev = run
+        want = _oracle_seeds(params, pb, np.arange(self.P))
+        got = dev.seeds.cpu().numpy()
+        assert np.array_equal(got[:, 0], np.repeat(pb.q_start, S, axis=0))
+        assert np.abs(got - want).max() < 1e-4
+
+    def test_refine_of_gpu_seeds_bitwise(self, run, oracle_lib):
+        pl, pb, host, dev = run
+        q, c, f, cl, best = _oracle_refine(oracle_lib, pl, _unbrick(pl, self.P), dev.seeds.cpu().numpy())
+        assert np.array_equal(np.asarray(host.trajectories), q)
+        assert np.array_equal(np.asarray(host.cost), c)
+        assert np.array_equal(np.asarray(host.feasible).astype(bool), f)
+        assert np.array_equal(np.asarray(host.best_index), best)
+
+    def test_full_oracle_pipeline(self, run, params, oracle_lib):
+        pl, pb, host, dev = run
+        esdf = np.stack([oracle_lib.esdf_build(pb.boxes[p], pl.grid) for p in range(self.P)])
+        seeds = _oracle_seeds(params, pb, np.arange(self.P))
+        q, c, f, cl, best = _oracle_refine(oracle_lib, pl, esdf, seeds)
+        assert np.array_equal(np.asarray(host.feasible).astype(bool), f)
+        assert np.array_equal(np.asarray(host.best_index), best)
+        d = np.abs(np.asarray(host.trajectories) - q).reshape(len(q), -1).max(1)
+        # the refinement maps seeds 1e-5 apart to trajectories 1e-5 apart unless a sphere sits on
+        # an ESDF cell face; require the north-star bound for (nearly) all of them
+        assert np.mean(d < 1e-4) >= 0.95, np.sort(d)[-8:]
+
+
+class TestBf16LayeredPipeline:
+    P = 64
+    CHECK = np.array([0, 21, 42, 63])        # problems re-planned by the float64 oracle
+
+    @pytest.fixture(scope="class")
+    def run(self, torch_cuda, params):
+        assert self.P * S * 32 > 8192          # above the persistent kernel: layered tcgen05 DDPM
+        pl = _planner(params, 1, self.P)
+        pb = synth.config3_problems(self.P, p0=100, seed=0)
+        host = pl.plan_batch(pb.images, pb.q_start, pb.goal, pb.boxes, p0=pb.p0)
+        seeds = pl.seeds[:self.P * S].cpu().numpy()
+        again = pl.plan_batch(pb.images, pb.q_start, pb.goal, pb.boxes, p0=pb.p0)
+        return pl, pb, host, seeds, again
+
+    def test_finite_deterministic_row0(self, run):
+        pl, pb, host, seeds, again = run
+        _check_finite(host)
+        assert np.isfinite(seeds).all()
+        for f in ("trajectories", "cost", "feasible", "best_index"):
+            assert np.array_equal(np.asarray(getattr(host, f)), np.asarray(getattr(again, f))), f
+        assert np.array_equal(seeds[:, 0], np.repeat(pb.q_start, S, axis=0))
+        assert np.array_equal(np.asarray(host.trajectories)[:, 0], seeds[:, 0])
+
+    def test_esdf_bitwise_subset(self, run, oracle_lib):
+        pl, pb, _, _, _ = run
+        esdf = _unbrick(pl, self.P)
+        for p in self.CHECK:
+            assert np.array_equal(esdf[p], oracle_lib.esdf_build(pb.boxes[p], pl.grid))
+
+    def test_refine_of_gpu_seeds_bitwise_whole_batch(self, run, oracle_lib):
+        pl, pb, host, seeds, _ = run
+        q, c, f, cl, best = _oracle_refine(oracle_lib, pl, _unbrick(pl, self.P), seeds)
+        assert np.array_equal(np.asarray(host.trajectories), q)
+        assert np.array_equal(np.asarray(host.cost), c)
+        assert np.array_equal(np.asarray(host.feasible).astype(bool), f)
+        assert np.array_equal(np.asarray(host.clamped).astype(bool), cl)
+        assert np.array_equal(np.asarray(host.best_index), best)
+
+    def test_seeds_within_bf16_bound(self, run, params):
+        pl, pb, _, seeds, _ = run
+        want = _oracle_seeds(params, pb, self.CHECK)
+        d = seeds[_rows(self.CHECK)] - want
+        assert np.sqrt((d ** 2).mean()) < 2e-2
+        assert np.abs(d).max() < 0.15
+
+    def test_flag_and_argmin_agreement_with_oracle_pipeline(self, run, params, oracle_lib):
+        pl, pb, host, _, _ = run
+        esdf = np.stack([oracle_lib.esdf_build(pb.boxes[p], pl.grid) for p in self.CHECK])
+        q, c, f, cl, best = _oracle_refine(oracle_lib, pl, esdf, _oracle_seeds(params, pb, self.CHECK))
+        gf = np.asarray(host.feasible).astype(bool)[_rows(self.CHECK)]
+        gb = np.asarray(host.best_index)[self.CHECK]
+        flag_rate = float(np.mean(gf == f))
+        print(f"bf16 vs float64 oracle pipeline: flag agreement {flag_rate:.4f}, "
+              f"best-index agreement {np.mean(gb == best):.3f} over {len(self.CHECK)} problems")
+        # bf16 seeds differ by ~1e-2 rad, so a seed near the collision threshold can flip; the
+        # measured rates are reported in DESIGN.md §6 (tools/agreement.py at larger scale)
+        assert flag_rate >= 0.9
+
+
+@pytest.mark.parametrize("persist", ["0", "1"])
+def test_small_batch_ddpm100_both_sampler_paths(torch_cuda, params, persist):
+    """2 problems x 8 seeds through the persistent kernel and (PS_PERSIST=0) the layered tcgen05
+    kernels with the fused DDPM epilogue, against the float64 oracle sampler."""
+    from paper_2410_16727_b200.sampler import SeedSampler
+    smp = SeedSampler(params, ENC, mode=1)
+    pb = synth.config3_problems(2, p0=7, seed=0)
+    cond = un.encode_problems(params, ENC, pb.images, pb.q_start, pb.goal)
+    os.environ["PS_PERSIST"] = persist
+    try:
+        traj = smp.sample(smp.film(cond), pb.q_start, 8, p0=pb.p0).cpu().numpy()
+    finally:
+        os.environ.pop("PS_PERSIST", None)
+    want = un.sample(params, ARCH, cond, pb.q_start, 8, p0=pb.p0)
+    d = traj - want
+    assert np.isfinite(traj).all()
+    assert np.sqrt((d ** 2).mean()) < 2e-2 and np.abs(d).max() < 0.1
