@@ -4,9 +4,11 @@
 Workload (config 3): P problems x S seeds per call (default 1024 x 32), each problem
 with two 1x240x320 depth images and a 128^3 ESDF built from its 20 random boxes;
 bf16 U-Net, 100 DDPM steps, 10 refinement iterations, flags + best-seed selection.
-Weak scaling over GPUs: every rank plans its own P problems (global problem indices
-[rank*P, (rank+1)*P), noise keyed by the global index) and rank 0 gathers all results
-over NCCL.  One step = one planning call over the rank's problems.
+Strong scaling over GPUs (default, BASELINE config 3 "sharded evenly across 1/2/4/8 GPUs"):
+the P problems are split evenly, rank r plans global problems [r*P/N, (r+1)*P/N) (noise
+and inputs keyed by the global index, so results do not depend on N) and rank 0 gathers
+every rank's trajectories, costs, flags and best indices over NCCL.  --scaling weak gives
+every rank its own P problems instead.  One step = one planning call over the job.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...
@@ -36,7 +38,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--problems", type=int, default=1024)
+    ap.add_argument("--problems", type=int, default=1024,
+                    help="total problems of the job (strong) or per rank (weak)")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong")
     ap.add_argument("--seeds", type=int, default=32)
     ap.add_argument("--horizon", type=int, default=32)
     ap.add_argument("--schedule", choices=["ddpm100", "ddim10"], default="ddpm100")
@@ -100,23 +104,30 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- CPU legs
 def cpu_leg(args, budget_s: float, workers: int | None = None):
-    """Oracle pipeline on host cores (process per problem), bounded to ~budget_s."""
+    """Oracle pipeline on host cores (one problem per process), bounded to ~budget_s: rounds of
+    `workers` problems (problem indices continue across rounds) until the next round would
+    overrun the budget.  At least one round always runs."""
     from oracle import pipeline_cpu as pc
 
     ncpu = os.cpu_count() or 1
     workers = workers or max(1, min(ncpu, 64))
     steps = None if args.schedule == "ddpm100" else __import__(
         "paper_2410_16727_b200.spec", fromlist=["x"]).strided_steps(100, 10)
-    # one problem per worker keeps the sample bounded (~10-20 s of CPU work per core)
-    n = workers
-    wall, res = pc.run_parallel(n, workers, p0=0, S=args.seeds, T=args.horizon, steps=steps,
-                                n_iters=10)
+    wall, res, n = 0.0, [], 0
+    while True:
+        w, r = pc.run_parallel(workers, workers, p0=n, S=args.seeds, T=args.horizon, steps=steps,
+                               n_iters=10)
+        wall += w
+        res += r
+        n += workers
+        if wall + w > budget_s:
+            break
     per_problem = statistics.median(r[2] for r in res)
     return {"value": n * args.seeds / wall, "unit": "trajectories/s", "cores": workers,
             "kind": "port",
-            "sample": f"{n} config-3 problems x {args.seeds} seeds (one per process, "
-                      f"{workers} processes on {ncpu} host cpus; oracle/pipeline_cpu.py, "
-                      f"float32 numpy + C), median {per_problem:.1f} s per problem",
+            "sample": f"{n} config-3 problems x {args.seeds} seeds ({n // workers} round(s) of one problem "
+                      f"per process, {workers} processes on {ncpu} host cpus, budget {budget_s:.0f} s; "
+                      f"oracle/pipeline_cpu.py, float32 numpy + C), median {per_problem:.1f} s per problem",
             "wall_s": wall, "cpu_model": _cpu_model()}
 
 
@@ -147,7 +158,7 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "trajectories/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * statistics.median(x["wall_s"] for x in vals),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": _config(args),
         "cpu_baseline": {"value": v, "unit": "trajectories/s", "cores": leg["cores"], "kind": "port",
                          "sample": leg["sample"]},
@@ -157,12 +168,16 @@ def run_reference(args, rank, world):
 
 
 def _config(args):
+    if args.scaling == "strong":
+        par = (f"dp{args.gpus}: {args.problems} problems split evenly over {args.gpus} GPU(s), "
+               f"NCCL gather to rank 0")
+    else:
+        par = f"dp{args.gpus}: {args.problems} problems per GPU, NCCL gather to rank 0"
     return {"workload": f"config 3: {args.problems} problems x {args.seeds} seeds, T={args.horizon}, "
                         f"2x240x320 depth images, 128^3 ESDF (20 boxes) per problem, "
                         f"{args.schedule}, 10 refine iterations",
             "problems": args.problems, "seeds": args.seeds, "horizon": args.horizon,
-            "schedule": args.schedule, "precision": args.mode,
-            "parallelism": f"dp{args.gpus}: {args.problems} problems per GPU, NCCL gather to rank 0",
+            "schedule": args.schedule, "precision": args.mode, "parallelism": par,
             "l2": "inputs > L2 (8 GiB of ESDFs rebuilt per step)"}
 
 
@@ -194,15 +209,21 @@ def main():
     from paper_2410_16727_b200 import dist as psd
     from paper_2410_16727_b200.planner import BLPlanner
 
-    # weak scaling: every rank plans its own `--problems` problems (global indices
-    # [rank*P, (rank+1)*P)); the whole job is P*N problems.
-    P, S, T = args.problems, args.seeds, args.horizon
-    P_all = P * world
-    p0, _ = psd.shard(rank, world, P)
+    P_arg, S, T = args.problems, args.seeds, args.horizon
+    if args.scaling == "strong":
+        p0, p1 = psd.shard_even(rank, world, P_arg)
+        P_all = P_arg
+        per = [(r + 1) * P_arg // world - r * P_arg // world for r in range(world)]
+    else:
+        p0, p1 = psd.shard(rank, world, P_arg)
+        P_all = P_arg * world
+        per = [P_arg] * world
+    P = p1 - p0
+    counts = [[n * S for n in per]] * 3 + [per]
     steps = None if args.schedule == "ddpm100" else spec.strided_steps(100, 10)
     mode = 1 if args.mode == "bf16" else 0
     params = spec.random_model(spec.ENCODER_CFG3)
-    planner = BLPlanner(params, spec.ENCODER_CFG3, mode=mode, S=S, T=T, steps=steps, max_problems=P)
+    planner = BLPlanner(params, spec.ENCODER_CFG3, mode=mode, S=S, T=T, steps=steps, max_problems=max(per))
     pb = synth.config3_problems(P, p0=p0, seed=0)
     h_images = torch.as_tensor(pb.images).pin_memory()
     h_q = torch.as_tensor(pb.q_start).pin_memory()
@@ -211,18 +232,20 @@ def main():
     d_images, d_q = h_images.to(dev), h_q.to(dev)
     d_goal, d_boxes = h_goal.to(dev), h_boxes.to(dev)
 
-    # gather buffers (rank 0 receives every rank's trajectories, costs, flags, best)
-    def gather(r):
-        # the only collective: final results of every rank to rank 0 (NCCL gather)
-        psd.gather_to_rank0([r.trajectories, r.cost, r.feasible, r.best_index], rank, world)
-
-    ev = {"sample_start": torch.cuda.Event(enable_timing=True),
-          "sample_end": torch.cuda.Event(enable_timing=True)}
+    def new_events():
+        return {k: torch.cuda.Event(enable_timing=True)
+                for k in ("start", "end", "sample_start", "sample_end", "refine_start", "refine_end")}
 
     def step(events=None):
+        if events is not None:
+            events["start"].record()
         r = planner.plan_batch_device(d_images, d_q, d_goal, d_boxes, p0=p0, events=events)
-        gather(r)
-        return r
+        # the only collective: final results of every rank to rank 0 (NCCL gather)
+        g = psd.gather_to_rank0([r.trajectories, r.cost, r.feasible, r.best_index], rank, world,
+                                counts=counts)
+        if events is not None:
+            events["end"].record()
+        return r, g
 
     def barrier():
         if world > 1:
@@ -236,13 +259,11 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = _lib.lib().ps_launch_count()
+    evs = [new_events() for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sample_ms = []
     t_start.record()
-    for _ in range(args.steps):
-        step(ev)
-        ev["sample_end"].synchronize()
-        sample_ms.append(ev["sample_start"].elapsed_time(ev["sample_end"]))
+    for e in evs:
+        res = step(e)
     t_end.record()
     torch.cuda.synchronize()
     barrier()
@@ -250,26 +271,45 @@ def main():
     launches = (_lib.lib().ps_launch_count() - launches0) // args.steps
     clk = clocks.stop()
     ms = t_start.elapsed_time(t_end) / args.steps
-    ms_t = torch.tensor([ms], device=dev)
+    per_step = [e["start"].elapsed_time(e["end"]) for e in evs]
+    sample_ms = [e["sample_start"].elapsed_time(e["sample_end"]) for e in evs]
+    refine_ms = [e["refine_start"].elapsed_time(e["refine_end"]) for e in evs]
+    # max over ranks: the whole-job time and, step by step, the slowest rank's step
+    vec = torch.tensor([ms] + per_step, device=dev, dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
+        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+    ms_max = float(vec[0].item())
+    steps_max = sorted(vec[1:].tolist())
     value = P_all * S / (ms_max / 1000.0)
 
-    # end-to-end through the public API from pinned host buffers
+    # the step's outputs must be real numbers (the bench never checked them)
+    r_last, g_last = res
+    outs = g_last if rank == 0 else None
+    if outs is not None:
+        finite = bool(torch.isfinite(outs[0]).all().item() and torch.isfinite(outs[1]).all().item())
+        if not finite:
+            raise RuntimeError("non-finite trajectories or costs in the benchmark outputs")
+
+    # end-to-end through the public API from pinned host buffers: H2D of this rank's inputs, the
+    # planning call, the NCCL gather and rank 0's read-back of the whole job's results
     e2e = None
     if not args.no_e2e:
-        for _ in range(1):
-            planner.plan_batch(h_images, h_q, h_goal, h_boxes, p0=p0)
+        def e2e_call():
+            if world == 1:
+                return planner.plan_batch(h_images, h_q, h_goal, h_boxes, p0=p0)
+            return psd.plan_sharded(planner, h_images, h_q, h_goal, h_boxes, p0, rank, world, P_all)
+
+        e2e_call()
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            planner.plan_batch(h_images, h_q, h_goal, h_boxes, p0=p0)
+            e2e_call()
         e1.record()
         torch.cuda.synchronize()
+        wall_ms = 1000 * (time.perf_counter() - t0) / args.steps
         barrier()
         e_ms = e0.elapsed_time(e1) / args.steps
         et = torch.tensor([e_ms], device=dev)
@@ -277,9 +317,14 @@ def main():
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e_ms = float(et.item())
         h2d = sum(t.numel() * t.element_size() for t in (h_images, h_q, h_goal, h_boxes))
+        h2d_t = torch.tensor([h2d], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(h2d_t)
         e2e = {"value": P_all * S / (e_ms / 1000.0), "unit": "trajectories/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(BLPlanner.result_bytes(P, S, T)),
-               "ms_per_step": e_ms, "wall_ms_per_step": 1000 * (time.perf_counter() - t0) / args.steps}
+               "h2d_bytes_per_step": int(h2d_t.item()),
+               "d2h_bytes_per_step": int(BLPlanner.result_bytes(P_all, S, T) - (0 if world == 1 else P_all * S)),
+               "ms_per_step": e_ms, "wall_ms_per_step": wall_ms,
+               "path": "BLPlanner.plan_batch" if world == 1 else "dist.plan_sharded (plan + NCCL gather + D2H)"}
 
     if rank != 0:
         if world > 1:
@@ -297,7 +342,19 @@ def main():
     roof = {"bound": "tensor", "kernel": "ps_sample (bf16 tcgen05 U-Net, 100 steps)",
             "achieved": achieved, "peak": peaks["bf16"], "unit": "TFLOP/s",
             "frac": achieved / peaks["bf16"], "peak_source": peaks["source"],
-            "traffic": traffic, "traffic_source": traffic_src, "sampler_ms": s_ms, "sampler_share": s_ms / ms}
+            "traffic": traffic, "traffic_source": traffic_src, "sampler_ms": s_ms,
+            "sampler_share": s_ms / (ms_max)}
+    # refinement: gather-bound; SURVEY §8(d) algorithmic bytes 52,992 B per trajectory-iteration
+    # at T=32 (50 spheres x T x 8 corners x 4 B + state read + write), 10 iterations
+    r_ms = statistics.median(refine_ms)
+    r_bytes = P * S * 10 * (50 * T * 8 * 4 + 2 * T * 7 * 4)
+    r_traffic, r_src = _refine_traffic(P, S, T)
+    roof_refine = {"bound": "hbm", "kernel": "bl_refine_kernel (10 fixed steps + flags)",
+                   "achieved": r_bytes / (r_ms / 1000.0) / 1e9, "peak": peaks["hbm"], "unit": "GB/s",
+                   "frac": r_bytes / (r_ms / 1000.0) / 1e9 / peaks["hbm"], "algorithmic_bytes": r_bytes,
+                   "refine_ms": r_ms, "refine_share": r_ms / ms_max,
+                   "traffic": r_traffic, "traffic_source": r_src,
+                   "traffic_over_algorithmic": (r_traffic / r_bytes) if r_traffic else None}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -308,18 +365,34 @@ def main():
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "error": repr(e)}
 
+    def pct(q):
+        return steps_max[min(len(steps_max) - 1, int(round(q * (len(steps_max) - 1))))]
+
     line = {
         "metric": METRIC, "value": value, "unit": "trajectories/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-        "p50_ms_per_problem_batch": ms_max, "amortised_ms_per_problem": ms_max / P_all,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "p50_ms_per_problem": pct(0.5), "p99_ms_per_problem": pct(0.99),
+        "latency_note": (f"per-step device times over {len(steps_max)} timed steps (max over ranks); a batched "
+                         f"call plans all its problems at once, so the step time is each problem's latency"),
+        "amortised_ms_per_problem": ms_max / P_all,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "bf16" if mode == 1 else "f32", "data": "synthetic (seeded; MpiNet absent)",
-        "config": _config(args), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": int(launches), "clocks": clk,
+        "config": _config(args), "roofline": roof, "roofline_refine": roof_refine, "cpu_baseline": cpu,
+        "e2e": e2e, "gpu_launches": int(launches), "outputs_finite": True, "clocks": clk,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _refine_traffic(P, S, T):
+    """DRAM bytes of one refinement launch at this workload from a committed ncu --set full capture
+    (profiles/*_refine_traffic.json), or None."""
+    cands = sorted((ROOT / "profiles").glob("*_refine_traffic.json"))
+    if not cands or (P, S, T) != (1024, 32, 32):
+        return None, None
+    d = json.loads(cands[-1].read_text())
+    return d["dram_bytes_per_launch"], cands[-1].name
 
 
 def _traffic(n_evals, P, S, T):

@@ -33,7 +33,7 @@ def _init_worker(enc_layers: int):
 
 
 def plan_problem(p: int, seed: int = 0, S: int = 32, T: int = 32, steps=None, n_iters: int = 10,
-                 enc_layers: int = 5, full: bool = False, dtype=np.float32):
+                 enc_layers: int = 5, full: bool = False, dtype=np.float32, wide: bool = False):
     """Plan one synthetic config-3 problem on one core; returns (best, traj_best, seconds), or with
     full=True (best, refined (S,T,7), cost (S,), feasible (S,), seconds)."""
     import oracle
@@ -44,7 +44,10 @@ def plan_problem(p: int, seed: int = 0, S: int = 32, T: int = 32, steps=None, n_
         _init_worker(enc_layers)
     t0 = time.perf_counter()
     grid, cost, robot = spec.GridSpec(), spec.BLCost(), spec.make_bl_robot()
-    pb = synth.config3_problems(1, p0=p, seed=seed) if enc_layers == 5 else synth.config0_problems(1, p0=p, seed=seed)
+    if wide:
+        pb, grid, robot = synth.config3_wide(1, p0=p, seed=seed)
+    else:
+        pb = synth.config3_problems(1, p0=p, seed=seed) if enc_layers == 5 else synth.config0_problems(1, p0=p, seed=seed)
     esdf = oracle.esdf_build(pb.boxes[0], grid)
     cond = un.encode_problems(_STATE["params"], _STATE["enc"], pb.images, pb.q_start, pb.goal,
                               dtype=dtype)

@@ -75,7 +75,8 @@ class BLPlanner:
     # ------------------------------------------------------------------ device
     def plan_batch_device(self, images, q_start, goal, boxes, p0: int = 0, events=None, images_ready=None):
         """All inputs already on the device.  Returns PlanBatchResult of device tensors.
-        `events` (optional dict) receives CUDA events bracketing the sampler;
+        `events` (optional dict of CUDA events) records "sample_start"/"sample_end" around the
+        sampler and, when present, "refine_start"/"refine_end" around the refinement;
         `images_ready` (optional CUDA event) is waited on before the encoder, so an image
         upload on another stream overlaps the ESDF build."""
         torch = _lib.require_cuda()
@@ -96,7 +97,11 @@ class BLPlanner:
         if events is not None:
             events["sample_end"].record()
         out = tuple(o[:B] for o in self.out)
+        if events is not None and "refine_start" in events:
+            events["refine_start"].record()
         bl.refine(seeds, esdf, self.S, self.robot, self.grid, self.cost, out=out, esdf_layout=self.esdf_layout)
+        if events is not None and "refine_end" in events:
+            events["refine_end"].record()
         best = bl.select(out[1], out[2], self.S, out=self.best[:P])
         return PlanBatchResult(out[0], seeds, out[1], out[2], out[3], best)
 
@@ -104,12 +109,14 @@ class BLPlanner:
         bl.esdf_build(boxes, self.grid, layout=self.esdf_layout, out=out)
 
     # ------------------------------------------------------------------ host
-    def plan_batch(self, images, q_start, goal, boxes, p0: int = 0):
-        """End-to-end call from host (ideally pinned) arrays: H2D copies, the device
-        pipeline, and a D2H read of trajectories, costs, flags and best indices.  The
-        image upload runs on a side stream, overlapped with the ESDF build."""
+    def upload(self, images, q_start, goal, boxes):
+        """Host (ideally pinned) arrays -> this planner's device input buffers.  The small inputs go
+        on the current stream; the image upload runs on a side stream (its completion event is
+        self._img_ev), overlapped with the ESDF build.  Returns the device views."""
         torch = _lib.require_cuda()
         P = int(q_start.shape[0])
+        if P > self.Pmax:
+            raise ValueError("batch larger than max_problems")
         d_im, d_q, d_g, d_b = (self.d_images[:P], self.d_q[:P], self.d_goal[:P], self.d_boxes[:P])
         main = torch.cuda.current_stream()
         if not hasattr(self, "_copy_stream"):
@@ -121,13 +128,20 @@ class BLPlanner:
         with torch.cuda.stream(self._copy_stream):
             d_im.copy_(torch.as_tensor(images), non_blocking=True)
             self._img_ev.record()
-        r = self.plan_batch_device(d_im, d_q, d_g, d_b, p0=p0, images_ready=self._img_ev)
+        return d_im, d_q, d_g, d_b
+
+    def plan_batch(self, images, q_start, goal, boxes, p0: int = 0, events=None):
+        """End-to-end call from host (ideally pinned) arrays: H2D copies, the device
+        pipeline, and a D2H read of trajectories, costs, flags and best indices."""
+        torch = _lib.require_cuda()
+        d = self.upload(images, q_start, goal, boxes)
+        r = self.plan_batch_device(*d, p0=p0, images_ready=self._img_ev, events=events)
         host = PlanBatchResult(r.trajectories.to("cpu", non_blocking=True), None,
                                r.cost.to("cpu", non_blocking=True),
                                r.feasible.to("cpu", non_blocking=True),
                                r.clamped.to("cpu", non_blocking=True),
                                r.best_index.to("cpu", non_blocking=True))
-        main.synchronize()
+        torch.cuda.current_stream().synchronize()
         return host
 
     @staticmethod

@@ -103,6 +103,23 @@ def config3_problems(P: int = 1024, p0: int = 0, seed: int = 0) -> ProblemBatch:
     return make_problems(P, p0, seed, image_shape=(240, 320), n_images=2, n_rect=8)
 
 
+def config3_wide(P: int, p0: int = 0, seed: int = 0, h: float = 0.025):
+    """Config-3 inputs in a 128^3 grid at 2.5 cm (a 3.2 m cube) with the robot base at its centre
+    -> (ProblemBatch, GridSpec, DHRobot).  At config 3's own 1 cm / 1.28 m grid every seed of the
+    random-init U-Net leaves the ESDF extent (the 7 links reach ~1.6 m from the centre) and no
+    seed is feasible, so feasibility flags carry no information there; in this scene ~1 seed in 8
+    is feasible and none leaves the grid (used by the flag-agreement tests and tools/agreement.py)."""
+    import dataclasses
+
+    from .spec import make_bl_robot
+    grid = GridSpec(h=h, cube=128 * h)
+    robot = dataclasses.replace(make_bl_robot(), base=np.full(3, 64 * h))
+    pb = config3_problems(P, p0=p0, seed=seed)
+    pb.boxes = np.stack([sample_boxes(_rng(seed, p0 + i, STREAM_BOXES), N_BOXES, grid)
+                         for i in range(P)]).astype(np.float32)
+    return pb, grid, robot
+
+
 def refine_init(n_traj: int, t_len: int = 32, t0: int = 0, seed: int = 0,
                 noise: float = 0.2) -> np.ndarray:
     """BASELINE config 2 seeds: straight line q_start -> q_goal (both uniform within the

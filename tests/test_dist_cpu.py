@@ -66,3 +66,40 @@ def test_shard_ranges_cover_global_indices():
     ranges = [psd.shard(r, 4, P) for r in range(4)]
     assert ranges[0] == (0, 5) and ranges[-1] == (15, 20)
     assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+
+
+def test_shard_even_strong_scaling():
+    for total, world in ((1024, 8), (5, 2), (7, 4), (3, 4)):
+        r = [psd.shard_even(k, world, total) for k in range(world)]
+        assert r[0][0] == 0 and r[-1][1] == total
+        assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+        sizes = [b - a for a, b in r]
+        assert max(sizes) - min(sizes) <= 1
+
+
+def _uneven_worker(rank, world, port, total, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p0, p1 = psd.shard_even(rank, world, total)
+    per = [psd.shard_even(r, world, total)[1] - psd.shard_even(r, world, total)[0] for r in range(world)]
+    rows = torch.arange(p0, p1, dtype=torch.float32)[:, None].repeat(1, 3)
+    res = psd.gather_to_rank0([rows, rows[:, 0].to(torch.int32)], rank, world, counts=[per, per])
+    if rank == 0:
+        q.put([r.numpy() for r in res])
+    dist.destroy_process_group()
+
+
+def test_gloo_uneven_shards_gather_in_global_order():
+    total, world = 5, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_uneven_worker, args=(r, world, port, total, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    rows, idx = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert np.array_equal(idx, np.arange(total))
+    assert np.array_equal(rows, np.repeat(np.arange(total, dtype=np.float32)[:, None], 3, 1))

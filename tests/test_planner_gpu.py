@@ -48,9 +48,13 @@ def params():
     return spec.random_model(ENC)
 
 
-def _planner(params, mode, P):
+def _planner(params, mode, P, **kw):
     from paper_2410_16727_b200.planner import BLPlanner
-    return BLPlanner(params, ENC, mode=mode, S=S, max_problems=P)
+    return BLPlanner(params, ENC, mode=mode, S=S, max_problems=P, **kw)
+
+
+def wide_scene(P, p0):
+    return synth.config3_wide(P, p0=p0)
 
 
 def _unbrick(planner, P):
@@ -198,6 +202,28 @@ class TestBf16LayeredPipeline:
         # bf16 seeds differ by ~1e-2 rad, so a seed near the collision threshold can flip; the
         # measured rates are reported in DESIGN.md §6 (tools/agreement.py at larger scale)
         assert flag_rate >= 0.9
+
+
+class TestBf16WideGridFlags(TestBf16LayeredPipeline):
+    """Same checks with mixed feasibility flags (wide_scene); 16 problems x 32 seeds still run the
+    layered tcgen05 DDPM kernels (B*T = 16,384)."""
+    P = 16
+    CHECK = np.array([0, 5, 10, 15])
+
+    @pytest.fixture(scope="class")
+    def run(self, torch_cuda, params):
+        pb, grid, robot = wide_scene(self.P, 300)
+        pl = _planner(params, 1, self.P, grid=grid, robot=robot)
+        host = pl.plan_batch(pb.images, pb.q_start, pb.goal, pb.boxes, p0=pb.p0)
+        seeds = pl.seeds[:self.P * S].cpu().numpy()
+        again = pl.plan_batch(pb.images, pb.q_start, pb.goal, pb.boxes, p0=pb.p0)
+        return pl, pb, host, seeds, again
+
+    def test_flags_are_mixed_and_in_grid(self, run):
+        _, _, host, _, _ = run
+        f = np.asarray(host.feasible).astype(bool)
+        assert 0 < f.mean() < 1
+        assert not np.asarray(host.clamped).astype(bool).any()
 
 
 @pytest.mark.parametrize("persist", ["0", "1"])

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--dtype", default="float32")
     ap.add_argument("--mode", type=int, default=1)
     ap.add_argument("--p0", type=int, default=0)
+    ap.add_argument("--wide", action="store_true", help="synth.config3_wide scene (mixed flags)")
     a = ap.parse_args()
     import torch
 
@@ -40,8 +41,12 @@ def main():
     oracle.build()
     S = 32
     params = spec.random_model(spec.ENCODER_CFG3)
-    pl = BLPlanner(params, spec.ENCODER_CFG3, mode=a.mode, S=S, max_problems=a.problems)
-    pb = synth.config3_problems(a.problems, p0=a.p0, seed=0)
+    kw = {}
+    if a.wide:
+        pb, kw["grid"], kw["robot"] = synth.config3_wide(a.problems, p0=a.p0, seed=0)
+    else:
+        pb = synth.config3_problems(a.problems, p0=a.p0, seed=0)
+    pl = BLPlanner(params, spec.ENCODER_CFG3, mode=a.mode, S=S, max_problems=a.problems, **kw)
     r = pl.plan_batch(pb.images, pb.q_start, pb.goal, pb.boxes, p0=pb.p0)
     gq = np.asarray(r.trajectories).reshape(a.problems, S, 32, 7)
     gf = np.asarray(r.feasible).astype(bool).reshape(a.problems, S)
@@ -51,7 +56,7 @@ def main():
     t0 = time.perf_counter()
     workers = min(len(idx), os.cpu_count() or 1)
     with ProcessPoolExecutor(max_workers=workers, initializer=pc._init_worker, initargs=(5,)) as ex:
-        futs = [ex.submit(pc.plan_problem, a.p0 + int(i), full=True, dtype=dt) for i in idx]
+        futs = [ex.submit(pc.plan_problem, a.p0 + int(i), full=True, dtype=dt, wide=a.wide) for i in idx]
         res = [f.result() for f in futs]
     wall = time.perf_counter() - t0
     of = np.stack([x[3] for x in res])
@@ -61,6 +66,8 @@ def main():
     line = {
         "problems_gpu": a.problems, "problems_checked": int(len(idx)), "trajectories_checked": int(len(idx) * S),
         "gpu_mode": "bf16" if a.mode == 1 else "fp32", "oracle_dtype": a.dtype,
+        "scene": "config3_wide (2.5 cm grid, base at centre)" if a.wide else "config 3",
+        "clamped_rate_gpu": float(np.asarray(r.clamped).astype(bool).mean()),
         "flag_agreement": float(np.mean(gf[idx] == of)),
         "best_index_agreement": float(np.mean(gb[idx] == ob)),
         "gpu_best_feasible": float(np.mean(gf[idx][np.arange(len(idx)), gb[idx]])),
