@@ -231,27 +231,33 @@ template <int NH, int NGL, bool SPAN>
 __device__ __forceinline__ void gn_stats(const float (&v)[NH], int nb, int sl, int lane, int q, int h, float* red,
                                          float inv_n, float (&mean)[NGL], float (&rstd)[NGL]) {
     constexpr int CG = SPAN ? NH : NH / NGL;   // channels of a group inside this half
-    float s1[NGL], s2[NGL];
+    // A 16-channel group held whole by one half (32-channel slices of the 128-wide layers) is
+    // reduced as two 8-channel pieces, each over lanes and quadrant warps, summed piece after
+    // piece -- the order the 16-channel slices give (the group then spans both halves), so the
+    // statistics do not depend on the slice width the batch size selects (shard invariance).
+    constexpr int NSUB = (!SPAN && CG == 16) ? 2 : 1, CS = CG / NSUB, NP = NGL * NSUB;
+    static_assert(NP <= 4, "red holds 4 partial sums per thread");
+    float s1[NP], s2[NP];
 #pragma unroll
-    for (int g = 0; g < NGL; ++g) {
+    for (int g = 0; g < NP; ++g) {
         s1[g] = s2[g] = 0.f;
 #pragma unroll
-        for (int c = 0; c < CG; ++c) {
-            s1[g] += v[g * CG + c];
-            s2[g] = fmaf(v[g * CG + c], v[g * CG + c], s2[g]);
+        for (int c = 0; c < CS; ++c) {
+            s1[g] += v[g * CS + c];
+            s2[g] = fmaf(v[g * CS + c], v[g * CS + c], s2[g]);
         }
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1)
         if (off >= nb)
 #pragma unroll
-            for (int g = 0; g < NGL; ++g) {
+            for (int g = 0; g < NP; ++g) {
                 s1[g] += __shfl_xor_sync(PS_FULL, s1[g], off);
                 s2[g] += __shfl_xor_sync(PS_FULL, s2[g], off);
             }
     if (lane < nb)
 #pragma unroll
-        for (int g = 0; g < NGL; ++g) {
+        for (int g = 0; g < NP; ++g) {
             red[((h * 4 + q) * 16 + sl) * 8 + g] = s1[g];
             red[((h * 4 + q) * 16 + sl) * 8 + 4 + g] = s2[g];
         }
@@ -260,12 +266,12 @@ __device__ __forceinline__ void gn_stats(const float (&v)[NH], int nb, int sl, i
     for (int g = 0; g < NGL; ++g) {
         float a1 = 0.f, a2 = 0.f;
 #pragma unroll
-        for (int hh = 0; hh < (SPAN ? 2 : 1); ++hh) {
-            const int hs = SPAN ? hh : h;
+        for (int hh = 0; hh < (SPAN ? 2 : NSUB); ++hh) {
+            const int hs = SPAN ? hh : h, gp = SPAN ? g : g * NSUB + hh;
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
-                a1 += red[((hs * 4 + w) * 16 + sl) * 8 + g];
-                a2 += red[((hs * 4 + w) * 16 + sl) * 8 + 4 + g];
+                a1 += red[((hs * 4 + w) * 16 + sl) * 8 + gp];
+                a2 += red[((hs * 4 + w) * 16 + sl) * 8 + 4 + gp];
             }
         }
         mean[g] = a1 * inv_n;
