@@ -129,6 +129,15 @@ int ps_sample(const void* packed, int mode, const float* film_a, int P, int S, i
               unsigned noise_key, const float* q_start, float lo, float hi, void* ws, float* traj,
               void* stream);
 
+/* ps_sample with the first n_hp steps on the fp32 SIMT network (packed_hp: ps_unet_pack of the
+ * same weights in mode 0) and the rest on `mode` (1: bf16 tcgen05).  A strided DDIM schedule from
+ * the top of the squared-cosine schedule reconstructs x0 with 1/sqrt(abar_100) ~ 2e3 times the
+ * noise prediction (_ddim_core, diffusion.py:548-550), which bf16 cannot carry; the high-precision
+ * prefix keeps those steps in fp32.  n_hp = 0 is ps_sample. */
+int ps_sample_hp(const void* packed, int mode, const void* packed_hp, int n_hp, const float* film_a, int P, int S,
+                 int T, int p0, const int* steps_h, int n_steps, int ddpm, const float* coef_h, int K,
+                 unsigned noise_key, const float* q_start, float lo, float hi, void* ws, float* traj, void* stream);
+
 /* n standard normals of the sampler's noise stream (test hook). */
 int ps_noise_probe(float* out, int n, int step, int prob, int seed, unsigned key, void* stream);
 

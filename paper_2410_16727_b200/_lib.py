@@ -49,6 +49,8 @@ _SIGS = {
     "ps_sample_workspace_bytes": [_c_int, _c_int, _c_int, _c_int, _c_int],
     "ps_sample": [_vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int,
                   ctypes.c_uint, _vp, _c_f, _c_f, _vp, _vp, _vp],
+    "ps_sample_hp": [_vp, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _vp,
+                     _c_int, ctypes.c_uint, _vp, _c_f, _c_f, _vp, _vp, _vp],
     "ps_noise_probe": [_vp, _c_int, _c_int, _c_int, _c_int, ctypes.c_uint, _vp],
     "ps_box_muller_probe": [_vp, _vp, _c_int, _vp, _vp],
     "ps_normal4_probe": [_vp, _c_int, _c_int, _c_int, _c_int, ctypes.c_uint, _vp],

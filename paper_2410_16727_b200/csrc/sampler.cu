@@ -863,14 +863,15 @@ static uint64_t hash_bytes(const void* p, size_t n) {
     return h;
 }
 struct SampleKey {
-    const void* packed; const float* film_a; const float* q_start; void* ws; float* traj;
-    int mode, P, S, T, p0, n_steps, ddpm, K, persist;
+    const void* packed; const void* packed_hp; const float* film_a; const float* q_start; void* ws; float* traj;
+    int mode, P, S, T, p0, n_steps, ddpm, K, persist, n_hp;
     unsigned noise_key;
     float lo, hi;
     cudaStream_t stream;
     uint64_t steps_hash, coef_hash;
     bool operator==(const SampleKey& o) const {
-        return packed == o.packed && film_a == o.film_a && q_start == o.q_start && ws == o.ws && traj == o.traj &&
+        return packed == o.packed && packed_hp == o.packed_hp && n_hp == o.n_hp && film_a == o.film_a &&
+               q_start == o.q_start && ws == o.ws && traj == o.traj &&
                mode == o.mode && P == o.P && S == o.S && T == o.T && p0 == o.p0 && n_steps == o.n_steps &&
                ddpm == o.ddpm && K == o.K && persist == o.persist && noise_key == o.noise_key && lo == o.lo && hi == o.hi &&
                stream == o.stream && steps_hash == o.steps_hash && coef_hash == o.coef_hash;
@@ -896,15 +897,28 @@ static SampleGraph& sample_graph() {
     static SampleGraph g;
     return g;
 }
-static int sample_loop(const void* packed, int mode, const float* film_a, const float* film_b, const float* coef_h,
-                       int K, const int* steps_h, int n_steps, int ddpm, int B, int T, int S, int p0,
-                       unsigned noise_key, const float* q_start, float lo, float hi, float* x, float* eps,
-                       float* act, float* traj, size_t n, cudaStream_t st);
+static int sample_loop(const void* packed, int mode, const void* packed_hp, int n_hp, const float* film_a,
+                       const float* film_b, const float* coef_h, int K, const int* steps_h, int n_steps, int ddpm, int B,
+                       int T, int S, int p0, unsigned noise_key, const float* q_start, float lo, float hi, float* x,
+                       float* eps, float* act, float* traj, size_t n, cudaStream_t st);
 
 extern "C" int ps_sample(const void* packed, int mode, const float* film_a, int P, int S, int T, int p0,
                          const int* steps_h, int n_steps, int ddpm, const float* coef_h, int K, unsigned noise_key,
                          const float* q_start, float lo, float hi, void* ws, float* traj, void* stream) {
+    return ps_sample_hp(packed, mode, nullptr, 0, film_a, P, S, T, p0, steps_h, n_steps, ddpm, coef_h, K, noise_key,
+                        q_start, lo, hi, ws, traj, stream);
+}
+
+extern "C" int ps_sample_hp(const void* packed, int mode, const void* packed_hp, int n_hp, const float* film_a, int P,
+                            int S, int T, int p0, const int* steps_h, int n_steps, int ddpm, const float* coef_h, int K,
+                            unsigned noise_key, const float* q_start, float lo, float hi, void* ws, float* traj,
+                            void* stream) {
     if (P <= 0 || S <= 0 || (T != 32 && T != 64) || n_steps <= 0 || K <= 0) return PS_FAIL(PS_ERR_SHAPE);
+    if (n_hp < 0 || n_hp > n_steps || (n_hp > 0 && (!packed_hp || mode != 1))) return PS_FAIL(PS_ERR_SHAPE);
+    if (n_hp == n_steps) {   // every step in fp32: the plain fp32 sampler
+        return ps_sample_hp(packed_hp, 0, nullptr, 0, film_a, P, S, T, p0, steps_h, n_steps, ddpm, coef_h, K,
+                            noise_key, q_start, lo, hi, ws, traj, stream);
+    }
     for (int i = 0; i < n_steps; ++i)
         if (steps_h[i] < 1 || steps_h[i] > K) return PS_FAIL(PS_ERR_SHAPE);
     const int B = P * S;
@@ -929,21 +943,22 @@ extern "C" int ps_sample(const void* packed, int mode, const float* film_a, int 
     if (mode == 1 && unet_persist_eligible(B, T)) {
         std::vector<StepCoef> scs;
         step_coefs(coef_h, K, steps_h, n_steps, ddpm, scs);
-        PS_TRY(unet_persist_prepare(L, reinterpret_cast<const char*>(packed), act, B, T, scs.data(), n_steps));
+        PS_TRY(unet_persist_prepare(L, reinterpret_cast<const char*>(packed), act, B, T, scs.data() + n_hp,
+                                    n_steps - n_hp));
     }
     // The denoising loop (noise init + n_steps x ~31 launches) is captured once into a CUDA
     // graph and replayed while every argument that shapes it is unchanged: at small batch the
     // host cost of building ~31 launches per step (tensor maps, argument blocks) dominates.
     SampleKey key{};
-    key.packed = packed; key.film_a = film_a; key.q_start = q_start; key.ws = ws; key.traj = traj;
+    key.packed = packed; key.packed_hp = packed_hp; key.n_hp = n_hp; key.film_a = film_a; key.q_start = q_start; key.ws = ws; key.traj = traj;
     key.mode = mode; key.P = P; key.S = S; key.T = T; key.p0 = p0; key.n_steps = n_steps; key.ddpm = ddpm;
     key.K = K; key.persist = mode == 1 && unet_persist_eligible(B, T); key.noise_key = noise_key; key.lo = lo; key.hi = hi; key.stream = st;
     key.steps_hash = hash_bytes(steps_h, (size_t)n_steps * sizeof(int));
     key.coef_hash = hash_bytes(coef_h, (size_t)6 * (K + 1) * sizeof(float));
     static const bool use_graph = std::getenv("PS_NO_GRAPH") == nullptr;
     auto run_direct = [&]() {
-        return sample_loop(packed, mode, film_a, film_b, coef_h, K, steps_h, n_steps, ddpm, B, T, S, p0, noise_key,
-                           q_start, lo, hi, x, eps, act, traj, n, st);
+        return sample_loop(packed, mode, packed_hp, n_hp, film_a, film_b, coef_h, K, steps_h, n_steps, ddpm, B, T, S,
+                           p0, noise_key, q_start, lo, hi, x, eps, act, traj, n, st);
     };
     if (!use_graph) return run_direct();
     SampleGraph& G = sample_graph();
@@ -968,8 +983,8 @@ extern "C" int ps_sample(const void* packed, int mode, const float* film_a, int 
     G.reset();
     const long long launches0 = ps_launch_counter().load();
     if (cudaStreamBeginCapture(G.side, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return run_direct();
-    const int body = sample_loop(packed, mode, film_a, film_b, coef_h, K, steps_h, n_steps, ddpm, B, T, S, p0,
-                                 noise_key, q_start, lo, hi, x, eps, act, traj, n, G.side);
+    const int body = sample_loop(packed, mode, packed_hp, n_hp, film_a, film_b, coef_h, K, steps_h, n_steps, ddpm, B,
+                                 T, S, p0, noise_key, q_start, lo, hi, x, eps, act, traj, n, G.side);
     cudaGraph_t g = nullptr;
     const cudaError_t e = cudaStreamEndCapture(G.side, &g);
     if (body != PS_OK || e != cudaSuccess || cudaGraphInstantiate(&G.exec, g, 0) != cudaSuccess) {
@@ -986,23 +1001,36 @@ extern "C" int ps_sample(const void* packed, int mode, const float* film_a, int 
     return launch_graph();
 }
 
-// the denoising loop of ps_sample (captured into a graph by the caller)
-static int sample_loop(const void* packed, int mode, const float* film_a, const float* film_b, const float* coef_h,
-                       int K, const int* steps_h, int n_steps, int ddpm, int B, int T, int S, int p0,
-                       unsigned noise_key, const float* q_start, float lo, float hi, float* x, float* eps,
-                       float* act, float* traj, size_t n, cudaStream_t st) {
+// the denoising loop of ps_sample (captured into a graph by the caller).  The first n_hp steps
+// run the fp32 SIMT network from packed_hp (the mode-0 packing of the same weights; FiLM tables are
+// fp32 in both packings, so film_a / film_b serve both), the rest the `mode` network.
+static int sample_loop(const void* packed, int mode, const void* packed_hp, int n_hp, const float* film_a,
+                       const float* film_b, const float* coef_h, int K, const int* steps_h, int n_steps, int ddpm, int B,
+                       int T, int S, int p0, unsigned noise_key, const float* q_start, float lo, float hi, float* x,
+                       float* eps, float* act, float* traj, size_t n, cudaStream_t st) {
     Layout L = make_layout(mode, nullptr);
     noise_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, B, T, S, p0, noise_key);
     PS_CHECK_LAUNCH();
     const char* pk = reinterpret_cast<const char*>(packed);
-    if (mode == 1 && unet_persist_eligible(B, T)) {   // one persistent launch for every step
-        const int e = unet_persist_launch(L, pk, act, x, B, T, S, p0, noise_key, film_a, film_b, n_steps, q_start, traj,
-                                          lo, hi, nullptr, st);
-        if (e != US_NOT_RESIDENT) return e;
-    }
     std::vector<StepCoef> scs;
     step_coefs(coef_h, K, steps_h, n_steps, ddpm, scs);
-    for (int i = 0; i < n_steps; ++i) {
+    if (n_hp > 0) {
+        Layout L0 = make_layout(0, nullptr);
+        for (int i = 0; i < n_hp; ++i) {
+            PS_TRY(unet_eval_f32(L0, reinterpret_cast<const char*>(packed_hp), x, B, T, S, film_a,
+                                 film_b + (size_t)i * U_FILM_COLS, act, eps, st));
+            step_update_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, eps, scs[i], B, T, S, p0, noise_key,
+                                                                             q_start, traj, lo, hi);
+            PS_CHECK_LAUNCH();
+        }
+    }
+    if (mode == 1 && unet_persist_eligible(B, T)) {   // one persistent launch for every (remaining) step
+        const int e = unet_persist_launch(L, pk, act, x, B, T, S, p0, noise_key, film_a,
+                                          film_b + (size_t)n_hp * U_FILM_COLS, n_steps - n_hp, q_start, traj, lo, hi,
+                                          nullptr, st);
+        if (e != US_NOT_RESIDENT) return e;
+    }
+    for (int i = n_hp; i < n_steps; ++i) {
         const StepCoef& sc = scs[i];
         const float* fb = film_b + (size_t)i * U_FILM_COLS;
         if (mode == 0) {

@@ -27,8 +27,9 @@ class SeedSampler:
 
     def __init__(self, params: dict, enc: spec.EncoderArch = spec.ENCODER_CFG0,
                  arch: spec.UNetArch = spec.UNetArch(), mode: int = 0, betas=None,
-                 noise_seed: int = spec.NOISE_SEED):
+                 noise_seed: int = spec.NOISE_SEED, hp_rsq: float | None = spec.HP_RSQ):
         torch = _lib.require_cuda()
+        self.hp_rsq = hp_rsq
         L = _lib.lib()
         self.enc, self.arch, self.mode = enc, arch, int(mode)
         shapes = arch.param_shapes()
@@ -129,11 +130,34 @@ class SeedSampler:
         _lib.check(st, "unet_forward")
         return eps
 
+    def _packed_hp(self):
+        """mode-0 (fp32) packing of the same weights, for the high-precision DDIM prefix."""
+        if getattr(self, "_pk_hp", None) is None:
+            torch = _lib.require_cuda()
+            L = _lib.lib()
+            self._pk_hp = torch.empty(int(L.ps_unet_packed_bytes(0)), dtype=torch.uint8, device="cuda")
+            _lib.check(L.ps_unet_pack(_lib.ptr(self._blob), 0, _lib.ptr(self._pk_hp), _lib.stream_handle()),
+                       "unet_pack")
+        return self._pk_hp
+
+    def hp_steps(self, steps) -> int:
+        """How many leading DDIM steps run the fp32 network in mode 1: those whose x0 reconstruction
+        factor 1/sqrt(abar_k) exceeds spec.HP_RSQ (DDPM and mode 0: none)."""
+        if steps is None or self.mode == 0 or self.hp_rsq is None:
+            return 0
+        n = 0
+        for k in steps:
+            if self.coef[2][int(k)] <= self.hp_rsq:
+                break
+            n += 1
+        return n
+
     def sample(self, film_a, q_start, S: int, T: int = spec.T_DEFAULT, p0: int = 0, steps=None,
                stream=None, out=None):
         """Seeds for P problems x S seeds -> physical trajectories (P*S, T, 7), row 0 = q_start.
 
-        steps=None: K-step DDPM; otherwise deterministic DDIM over the given indices."""
+        steps=None: K-step DDPM; otherwise deterministic DDIM over the given indices (in mode 1 the
+        leading steps with 1/sqrt(abar_k) > hp_rsq run the fp32 network, see hp_steps)."""
         torch = _lib.require_cuda()
         from .bl import _dev
         q = _dev(q_start)
@@ -146,12 +170,17 @@ class SeedSampler:
             ddpm = 0
         L = _lib.lib()
         B = P * S
-        ws = self._workspace(L.ps_sample_workspace_bytes(B, T, P, len(ks), self.mode))
+        n_hp = self.hp_steps(None if ddpm else ks)
+        nbytes = L.ps_sample_workspace_bytes(B, T, P, len(ks), self.mode)
+        if n_hp:
+            nbytes = max(nbytes, L.ps_sample_workspace_bytes(B, T, P, len(ks), 0))
+        ws = self._workspace(nbytes)
         traj = out if out is not None else torch.empty((B, T, 7), dtype=torch.float32, device="cuda")
-        st = L.ps_sample(_lib.ptr(self.packed), self.mode, _lib.ptr(film_a), P, S, T, int(p0),
-                         _lib.hptr(ks), len(ks), ddpm, _lib.hptr(self.coef), self.K, self.noise_key,
-                         _lib.ptr(q), -spec.JOINT_LIMIT, spec.JOINT_LIMIT, _lib.ptr(ws),
-                         _lib.ptr(traj), _lib.stream_handle(stream))
+        hp = self._packed_hp() if n_hp else None
+        st = L.ps_sample_hp(_lib.ptr(self.packed), self.mode, _lib.ptr(hp) if n_hp else None, n_hp,
+                            _lib.ptr(film_a), P, S, T, int(p0), _lib.hptr(ks), len(ks), ddpm,
+                            _lib.hptr(self.coef), self.K, self.noise_key, _lib.ptr(q), -spec.JOINT_LIMIT,
+                            spec.JOINT_LIMIT, _lib.ptr(ws), _lib.ptr(traj), _lib.stream_handle(stream))
         _lib.check(st, "sample")
         return traj
 

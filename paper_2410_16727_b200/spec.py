@@ -354,6 +354,11 @@ def cosine_betas(K: int = K_STEPS, s: float = COSINE_S, max_beta: float = 0.999)
     return np.array(betas, dtype=np.float64)
 
 
+# Strided DDIM in bf16: steps whose x0 reconstruction factor 1/sqrt(abar_k) exceeds HP_RSQ run the
+# noise prediction in fp32 (k = 100: 2029, k = 89: 5.9 in the 10-step schedule; k = 78: 3.0 does not)
+HP_RSQ = 4.0
+
+
 def strided_steps(K: int, n_steps: int) -> np.ndarray:
     """round-half-even(linspace(K, 1, n)) -- planseed/diffusion.py:520-526."""
     if n_steps > K:
