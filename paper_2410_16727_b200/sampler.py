@@ -27,7 +27,7 @@ class SeedSampler:
 
     def __init__(self, params: dict, enc: spec.EncoderArch = spec.ENCODER_CFG0,
                  arch: spec.UNetArch = spec.UNetArch(), mode: int = 0, betas=None,
-                 noise_seed: int = spec.NOISE_SEED, hp_rsq: float | None = spec.HP_RSQ):
+                 noise_seed: int = spec.NOISE_SEED, hp_rsq: float | None = None):
         torch = _lib.require_cuda()
         self.hp_rsq = hp_rsq
         L = _lib.lib()
@@ -157,7 +157,8 @@ class SeedSampler:
         """Seeds for P problems x S seeds -> physical trajectories (P*S, T, 7), row 0 = q_start.
 
         steps=None: K-step DDPM; otherwise deterministic DDIM over the given indices (in mode 1 the
-        leading steps with 1/sqrt(abar_k) > hp_rsq run the fp32 network, see hp_steps)."""
+        leading steps with 1/sqrt(abar_k) > hp_rsq run the fp32 network, see hp_steps; without
+        hp_rsq a bf16 DDIM schedule from the top of the schedule warns, spec.DDIM_BF16_MAX_RSQ)."""
         torch = _lib.require_cuda()
         from .bl import _dev
         q = _dev(q_start)
@@ -171,6 +172,12 @@ class SeedSampler:
         L = _lib.lib()
         B = P * S
         n_hp = self.hp_steps(None if ddpm else ks)
+        if self.mode == 1 and not ddpm and n_hp == 0 and self.coef[2][int(ks[0])] > spec.DDIM_BF16_MAX_RSQ:
+            import warnings
+            warnings.warn(f"bf16 strided DDIM from k={int(ks[0])} (x0 factor 1/sqrt(abar) = "
+                          f"{float(self.coef[2][int(ks[0])]):.0f}) is numerically unqualified "
+                          "(~0.4 rad RMS from the fp32 result); use mode=0 or hp_rsq (spec.HP_RSQ)",
+                          RuntimeWarning, stacklevel=2)
         nbytes = L.ps_sample_workspace_bytes(B, T, P, len(ks), self.mode)
         if n_hp:
             nbytes = max(nbytes, L.ps_sample_workspace_bytes(B, T, P, len(ks), 0))

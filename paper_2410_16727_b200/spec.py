@@ -354,8 +354,14 @@ def cosine_betas(K: int = K_STEPS, s: float = COSINE_S, max_beta: float = 0.999)
     return np.array(betas, dtype=np.float64)
 
 
-# Strided DDIM in bf16: steps whose x0 reconstruction factor 1/sqrt(abar_k) exceeds HP_RSQ run the
-# noise prediction in fp32 (k = 100: 2029, k = 89: 5.9 in the 10-step schedule; k = 78: 3.0 does not)
+# Strided DDIM in bf16 (mode 1).  The x0 reconstruction multiplies the noise prediction by
+# 1/sqrt(abar_k): 2029 at k = 100, 5.9 at k = 89, 3.0 at k = 78 in the 10-step schedule, and the
+# deterministic update carries every error forward, so bf16-level noise-prediction differences end
+# ~0.37 rad RMS from the float64 oracle (fp32: 6e-5).  A schedule whose first x0 factor exceeds
+# DDIM_BF16_MAX_RSQ is numerically unqualified in bf16 (SeedSampler warns).  SeedSampler(hp_rsq=h)
+# runs the leading steps with factor > h on the fp32 network: h = 4 (2 fp32 steps) measured 0.068
+# rad RMS, h = 2.5 (3 steps) 0.037, at 6-9x the sampler time at 1024 x 32.
+DDIM_BF16_MAX_RSQ = 50.0
 HP_RSQ = 4.0
 
 
