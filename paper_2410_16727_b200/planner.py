@@ -42,9 +42,9 @@ class BLPlanner:
                  T: int = spec.T_DEFAULT, robot: spec.DHRobot | None = None,
                  grid: spec.GridSpec = spec.GridSpec(), cost: spec.BLCost = spec.BLCost(),
                  steps=None, max_problems: int = 1024, n_images: int = 2,
-                 image_shape=(240, 320), n_boxes: int = spec.N_BOXES):
+                 image_shape=(240, 320), n_boxes: int = spec.N_BOXES, hp_rsq: float | None = None, betas=None):
         torch = _lib.require_cuda()
-        self.sampler = SeedSampler(params, enc, arch, mode=mode)
+        self.sampler = SeedSampler(params, enc, arch, mode=mode, hp_rsq=hp_rsq, betas=betas)
         self.S, self.T = int(S), int(T)
         self.robot = robot or spec.make_bl_robot()
         self.grid, self.cost = grid, cost
@@ -71,6 +71,14 @@ class BLPlanner:
         self.d_goal = torch.empty((self.Pmax, 7), dtype=torch.float32, device=dev)
         self.d_boxes = torch.empty((self.Pmax, n_boxes, 6), dtype=torch.float32, device=dev)
         self.timing = {}
+
+    @classmethod
+    def from_checkpoint(cls, path, **kw) -> "BLPlanner":
+        """A planner over a unet1d PSCK checkpoint (checkpoint.py): weights, encoder depth and the
+        noise schedule come from the file."""
+        from .checkpoint import load_checkpoint
+        params, enc, arch, betas, _ = load_checkpoint(path)
+        return cls(params, enc, arch, betas=betas, **kw)
 
     # ------------------------------------------------------------------ device
     def plan_batch_device(self, images, q_start, goal, boxes, p0: int = 0, events=None, images_ready=None):

@@ -50,6 +50,14 @@ class SeedSampler:
         self.noise_key = int(noise_seed) & 0xFFFFFFFF
         self._ws = None
 
+    @classmethod
+    def from_checkpoint(cls, path, mode: int = 1, **kw) -> "SeedSampler":
+        """A sampler over the weights and noise schedule of a unet1d PSCK file (checkpoint.py;
+        the container of planseed's load_checkpoint, diffusion.py:657-687)."""
+        from .checkpoint import load_checkpoint
+        params, enc, arch, betas, _ = load_checkpoint(path)
+        return cls(params, enc, arch, mode=mode, betas=betas, **kw)
+
     # ------------------------------------------------------------------ helpers
     def _workspace(self, nbytes: int):
         torch = _lib.require_cuda()

@@ -243,3 +243,18 @@ def test_small_batch_ddpm100_both_sampler_paths(torch_cuda, params, persist):
     d = traj - want
     assert np.isfinite(traj).all()
     assert np.sqrt((d ** 2).mean()) < 2e-2 and np.abs(d).max() < 0.1
+
+
+def test_checkpoint_loaded_planner_is_bitwise_identical(torch_cuda, params, tmp_path):
+    """A unet1d PSCK file (checkpoint.py, planseed's container) drives the GPU planner to the same
+    bits as the in-memory weights."""
+    from paper_2410_16727_b200 import checkpoint as ck
+    from paper_2410_16727_b200.planner import BLPlanner
+    path = tmp_path / "bl.psck"
+    ck.save_checkpoint(path, params, ENC, ARCH, spec.cosine_betas())
+    pb = synth.config3_problems(2, p0=11, seed=0)
+    a = _planner(params, 1, 2).plan_batch(pb.images, pb.q_start, pb.goal, pb.boxes, p0=pb.p0)
+    b = BLPlanner.from_checkpoint(path, mode=1, S=S, max_problems=2).plan_batch(
+        pb.images, pb.q_start, pb.goal, pb.boxes, p0=pb.p0)
+    for f in ("trajectories", "cost", "feasible", "best_index"):
+        assert np.array_equal(np.asarray(getattr(a, f)), np.asarray(getattr(b, f))), f
