@@ -74,6 +74,21 @@ int ps_bl_refine_layout(const float* q_in, int B, int T, int S, const float* esd
                         const float* weights_h, int n_iters, float* q_out, float* cost, uint8_t* feasible,
                         uint8_t* clamped, void* stream);
 
+/* ps_bl_cost over an ESDF in `layout` (see ps_esdf_build_boxes_layout); identical results. */
+int ps_bl_cost_layout(const float* q, int B, int T, int S, const float* esdf, long long esdf_stride, int layout,
+                      const int* n_h, const float* origin_h, float h, const float* dh_h, const float* base_h,
+                      const float* sph_h, const int* sph_link_h, int n_sph, const float* weights_h, float* cost,
+                      float* grad, uint8_t* clamped, void* stream);
+
+/* trajopt.optimize semantics (trajopt.py:140-177) over ps_bl_refine_layout: PS_ERR_SHAPE for an
+ * empty batch or n_iters < 1; the initial seeds are evaluated first and PS_ERR_OUT_OF_GRID is
+ * returned, without refining, if any leaves the ESDF extent (evaluate_cost_batch's ValueError,
+ * trajopt.py:116-118) -- clamped0 (B,) then names them.  Synchronises `stream` once. */
+int ps_bl_optimize(const float* q_in, int B, int T, int S, const float* esdf, long long esdf_stride, int layout,
+                   const int* n_h, const float* origin_h, float h, const float* dh_h, const float* base_h,
+                   const float* sph_h, const int* sph_link_h, int n_sph, const float* weights_h, int n_iters,
+                   float* q_out, float* cost, uint8_t* feasible, uint8_t* clamped, uint8_t* clamped0, void* stream);
+
 /* Best seed per problem: lowest-cost feasible seed, else lowest cost; ties to the
  * lower index.  pipeline.select_best (pipeline.py:160-165).  best: (P,) int32. */
 int ps_select(const float* cost, const uint8_t* feasible, int P, int S, int32_t* best,

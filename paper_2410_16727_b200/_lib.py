@@ -35,6 +35,10 @@ _SIGS = {
                    _c_int, _vp, _vp, _vp, _vp, _vp],
     "ps_bl_refine": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,
                      _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp],
+    "ps_bl_cost_layout": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _c_int, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,
+                          _c_int, _vp, _vp, _vp, _vp, _vp],
+    "ps_bl_optimize": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _c_int, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,
+                       _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp],
     "ps_select": [_vp, _vp, _c_int, _c_int, _vp, _vp],
     "ps_unet_param_count": [],
     "ps_unet_param_offset": [ctypes.c_char_p],

@@ -7,6 +7,9 @@ Batched counterparts of the reference refiner / planner helpers:
                                                                         pipeline.py:139-157)
   select          ~ pipeline.select_best                               (pipeline.py:160-165)
 
+  evaluate_cost_batch / optimize  the reference-semantics forms: raise ValueError naming the
+                  seeds that leave the ESDF extent (trajopt.py:116-118, :157-163)
+
 Inputs may be numpy arrays or torch CUDA tensors; outputs are torch CUDA tensors.
 """
 
@@ -92,9 +95,18 @@ def _esdf_stride(esdf, grid: GridSpec, n_problems: int) -> int:
     return grid.n_nodes
 
 
+OUT_OF_GRID_MSG = "trajectory collision points leave the ESDF extent"
+
+
+def _raise_out_of_grid(clamped):
+    seeds = clamped.nonzero().flatten().cpu().tolist()
+    raise ValueError(f"{OUT_OF_GRID_MSG} (seeds {seeds})")
+
+
 def cost(q, esdf, S: int, robot: DHRobot, grid: GridSpec = GridSpec(), w: BLCost = BLCost(),
-         stream=None):
-    """Batched cost (B,), gradient (B,T,7) (row 0 zero) and clamped flags (B,)."""
+         stream=None, esdf_layout: int = ESDF_C_ORDER):
+    """Batched cost (B,), gradient (B,T,7) (row 0 zero) and clamped flags (B,) -- the kernel-level
+    form (cost_terms_batch, _kernels.py:165-312): never raises for out-of-grid points."""
     torch = _lib.require_cuda()
     qd = _dev(q)
     B, T, D = qd.shape
@@ -107,13 +119,59 @@ def cost(q, esdf, S: int, robot: DHRobot, grid: GridSpec = GridSpec(), w: BLCost
     c = torch.empty(B, dtype=torch.float32, device="cuda")
     g = torch.empty_like(qd)
     cl = torch.empty(B, dtype=torch.uint8, device="cuda")
-    st = _lib.lib().ps_bl_cost(_lib.ptr(qd), B, T, S, _lib.ptr(e), _esdf_stride(e, grid, -(-B // S)),
-                               _lib.hptr(n), _lib.hptr(o), grid.h, _lib.hptr(rt.dh),
-                               _lib.hptr(rt.base), _lib.hptr(rt.sph), _lib.hptr(rt.link),
-                               len(rt.link), _lib.hptr(wts), _lib.ptr(c), _lib.ptr(g), _lib.ptr(cl),
-                               _lib.stream_handle(stream))
+    st = _lib.lib().ps_bl_cost_layout(_lib.ptr(qd), B, T, S, _lib.ptr(e), _esdf_stride(e, grid, -(-B // S)),
+                                      int(esdf_layout), _lib.hptr(n), _lib.hptr(o), grid.h, _lib.hptr(rt.dh),
+                                      _lib.hptr(rt.base), _lib.hptr(rt.sph), _lib.hptr(rt.link),
+                                      len(rt.link), _lib.hptr(wts), _lib.ptr(c), _lib.ptr(g), _lib.ptr(cl),
+                                      _lib.stream_handle(stream))
     _lib.check(st, "bl_cost")
     return c, g, cl.bool()
+
+
+def evaluate_cost_batch(q, esdf, S: int, robot: DHRobot, grid: GridSpec = GridSpec(), w: BLCost = BLCost(),
+                        stream=None, esdf_layout: int = ESDF_C_ORDER):
+    """trajopt.evaluate_cost_batch semantics (trajopt.py:104-119): (totals, grads); raises
+    ValueError naming the seeds whose collision spheres leave the ESDF extent."""
+    c, g, cl = cost(q, esdf, S, robot, grid, w, stream, esdf_layout)
+    if bool(cl.any()):
+        _raise_out_of_grid(cl)
+    return c, g
+
+
+def optimize(q, esdf, S: int, robot: DHRobot, grid: GridSpec = GridSpec(), w: BLCost = BLCost(),
+             n_iters: int | None = None, stream=None, out=None, esdf_layout: int = ESDF_C_ORDER):
+    """trajopt.optimize semantics (trajopt.py:140-177) for the fixed-step BL refinement: ValueError
+    for n_iters < 1 or no seeds, and -- before any refinement -- for seeds that leave the ESDF
+    extent (ps_bl_optimize).  Returns refine()'s (q_out, cost, feasible, clamped)."""
+    torch = _lib.require_cuda()
+    n_iters = w.n_iters if n_iters is None else int(n_iters)
+    if n_iters < 1:
+        raise ValueError("n_iters must be >= 1")
+    qd = _dev(q)
+    if qd.dim() != 3 or qd.shape[0] == 0:
+        raise ValueError("need at least one seed")
+    B, T, D = qd.shape
+    if D != 7 or T not in (32, 64):
+        raise ValueError("q must be (B, 32|64, 7)")
+    e = _dev(esdf)
+    rt = RobotTables.of(robot)
+    n, o = _grid_args(grid)
+    wts = w.as_f32()
+    if out is None:
+        out = (torch.empty_like(qd), torch.empty(B, dtype=torch.float32, device="cuda"),
+               torch.empty(B, dtype=torch.uint8, device="cuda"),
+               torch.empty(B, dtype=torch.uint8, device="cuda"))
+    qo, c, f, cl = out
+    cl0 = torch.empty(B, dtype=torch.uint8, device="cuda")
+    st = _lib.lib().ps_bl_optimize(_lib.ptr(qd), B, T, S, _lib.ptr(e), _esdf_stride(e, grid, -(-B // S)),
+                                   int(esdf_layout), _lib.hptr(n), _lib.hptr(o), grid.h, _lib.hptr(rt.dh),
+                                   _lib.hptr(rt.base), _lib.hptr(rt.sph), _lib.hptr(rt.link), len(rt.link),
+                                   _lib.hptr(wts), n_iters, _lib.ptr(qo), _lib.ptr(c), _lib.ptr(f), _lib.ptr(cl),
+                                   _lib.ptr(cl0), _lib.stream_handle(stream))
+    if st == _lib.PS_ERR_OUT_OF_GRID:
+        _raise_out_of_grid(cl0.bool())
+    _lib.check(st, "bl_optimize")
+    return qo, c, f, cl
 
 
 def refine(q, esdf, S: int, robot: DHRobot, grid: GridSpec = GridSpec(), w: BLCost = BLCost(),

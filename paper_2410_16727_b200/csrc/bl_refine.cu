@@ -13,6 +13,8 @@
 
 #include <cstdlib>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace ps {
@@ -609,6 +611,44 @@ extern "C" int ps_bl_cost(const float* q, int B, int T, int S, const float* esdf
     if (st) return st;
     P.q_in = q; P.cost = cost; P.grad = grad; P.clamped = clamped; P.n_iters = 0;
     return launch_bl<1>(P, (cudaStream_t)stream);
+}
+
+extern "C" int ps_bl_cost_layout(const float* q, int B, int T, int S, const float* esdf, long long esdf_stride,
+                                 int layout, const int* n_h, const float* origin_h, float h, const float* dh_h,
+                                 const float* base_h, const float* sph_h, const int* sph_link_h, int n_sph,
+                                 const float* weights_h, float* cost, float* grad, uint8_t* clamped, void* stream) {
+    BLParams P{};
+    int st = fill_params(P, B, T, S, esdf, esdf_stride, n_h, origin_h, h, dh_h, base_h, sph_h, sph_link_h,
+                         n_sph, weights_h);
+    if (st) return st;
+    if (layout < 0 || layout > 1 || (layout == 1 && ((n_h[0] & 3) || (n_h[1] & 3) || (n_h[2] & 3))))
+        return PS_ERR_SHAPE;
+    P.esdf_brick = layout;
+    P.q_in = q; P.cost = cost; P.grad = grad; P.clamped = clamped; P.n_iters = 0;
+    return launch_bl<1>(P, (cudaStream_t)stream);
+}
+
+// optimize() semantics (trajopt.py:140-177): reject an empty batch / n_iters < 1, evaluate the
+// initial seeds first and return PS_ERR_OUT_OF_GRID -- without refining -- if any of them leaves
+// the ESDF extent (evaluate_cost_batch's ValueError, trajopt.py:116-118); clamped0 then names
+// them.  The pre-check uses `cost` and `q_out` as scratch and synchronises `stream` once.
+extern "C" int ps_bl_optimize(const float* q_in, int B, int T, int S, const float* esdf, long long esdf_stride,
+                              int layout, const int* n_h, const float* origin_h, float h, const float* dh_h,
+                              const float* base_h, const float* sph_h, const int* sph_link_h, int n_sph,
+                              const float* weights_h, int n_iters, float* q_out, float* cost, uint8_t* feasible,
+                              uint8_t* clamped, uint8_t* clamped0, void* stream) {
+    if (B <= 0 || n_iters < 1) return PS_ERR_SHAPE;
+    int st = ps_bl_cost_layout(q_in, B, T, S, esdf, esdf_stride, layout, n_h, origin_h, h, dh_h, base_h, sph_h,
+                               sph_link_h, n_sph, weights_h, cost, q_out, clamped0, stream);
+    if (st) return st;
+    std::vector<uint8_t> c0((size_t)B);
+    if (cudaMemcpyAsync(c0.data(), clamped0, (size_t)B, cudaMemcpyDeviceToHost, (cudaStream_t)stream) != cudaSuccess ||
+        cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess)
+        return PS_FAIL(PS_ERR_CUDA);
+    for (int b = 0; b < B; ++b)
+        if (c0[(size_t)b]) return PS_ERR_OUT_OF_GRID;
+    return ps_bl_refine_layout(q_in, B, T, S, esdf, esdf_stride, layout, n_h, origin_h, h, dh_h, base_h, sph_h,
+                               sph_link_h, n_sph, weights_h, n_iters, q_out, cost, feasible, clamped, stream);
 }
 
 extern "C" int ps_bl_refine(const float* q_in, int B, int T, int S, const float* esdf,

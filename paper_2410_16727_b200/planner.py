@@ -42,13 +42,20 @@ class BLPlanner:
                  T: int = spec.T_DEFAULT, robot: spec.DHRobot | None = None,
                  grid: spec.GridSpec = spec.GridSpec(), cost: spec.BLCost = spec.BLCost(),
                  steps=None, max_problems: int = 1024, n_images: int = 2,
-                 image_shape=(240, 320), n_boxes: int = spec.N_BOXES, hp_rsq: float | None = None, betas=None):
+                 image_shape=(240, 320), n_boxes: int = spec.N_BOXES, hp_rsq: float | None = None, betas=None,
+                 strict: bool = False):
         torch = _lib.require_cuda()
         self.sampler = SeedSampler(params, enc, arch, mode=mode, hp_rsq=hp_rsq, betas=betas)
         self.S, self.T = int(S), int(T)
         self.robot = robot or spec.make_bl_robot()
         self.grid, self.cost = grid, cost
         self.steps = steps
+        # strict=True: planseed's contract -- seeds leaving the ESDF extent raise ValueError before
+        # refinement (trajopt.optimize, trajopt.py:157-163).  Default False: at BASELINE config 3 every
+        # seed of a random-init U-Net leaves the 1.28 m grid (the arm reaches ~1.6 m from its centre),
+        # so the planner reports them per seed in `clamped` instead of raising (their lookups clamp to the
+        # grid boundary, as planseed's sample_esdf_many does, geometry.py:223-240).
+        self.strict = bool(strict)
         self.Pmax = int(max_problems)
         B = self.Pmax * self.S
         dev = "cuda"
@@ -107,7 +114,11 @@ class BLPlanner:
         out = tuple(o[:B] for o in self.out)
         if events is not None and "refine_start" in events:
             events["refine_start"].record()
-        bl.refine(seeds, esdf, self.S, self.robot, self.grid, self.cost, out=out, esdf_layout=self.esdf_layout)
+        if self.strict:
+            bl.optimize(seeds, esdf, self.S, self.robot, self.grid, self.cost, out=out, esdf_layout=self.esdf_layout)
+        else:
+            bl.refine(seeds, esdf, self.S, self.robot, self.grid, self.cost, out=out,
+                      esdf_layout=self.esdf_layout)
         if events is not None and "refine_end" in events:
             events["refine_end"].record()
         best = bl.select(out[1], out[2], self.S, out=self.best[:P])

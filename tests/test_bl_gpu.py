@@ -139,6 +139,58 @@ class TestRefine:
             bl.refine(np.zeros((4, 48, 7), np.float32), dev, 4, RB, grid, COST)
 
 
+class TestReferenceSemantics:
+    """evaluate_cost_batch / optimize raise planseed's ValueError naming the out-of-grid seeds
+    (trajopt.py:116-118, :157-163); in-grid batches give refine()'s exact results."""
+
+    def _setup(self, bl, n_grid=128, h=0.025):
+        grid = spec.GridSpec(n=(n_grid,) * 3, h=h, cube=n_grid * h)
+        import dataclasses
+        robot = dataclasses.replace(RB, base=np.full(3, n_grid * h / 2))
+        boxes = np.stack([synth.sample_boxes(np.random.default_rng(3), 6, grid)]).astype(np.float32)
+        return grid, robot, bl.esdf_build(boxes, grid)
+
+    def test_in_grid_optimize_equals_refine(self, bl):
+        grid, robot, esdf = self._setup(bl)
+        q = synth.refine_init(16, seed=4) * 0.3
+        a = [o.cpu().numpy() for o in bl.refine(q, esdf, 16, robot, grid, COST)]
+        b = [o.cpu().numpy() for o in bl.optimize(q, esdf, 16, robot, grid, COST)]
+        assert not a[3].any()
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+        c, g = bl.evaluate_cost_batch(q, esdf, 16, robot, grid, COST)
+        c2, g2, _ = bl.cost(q, esdf, 16, robot, grid, COST)
+        assert np.array_equal(c.cpu().numpy(), c2.cpu().numpy())
+
+    def test_out_of_grid_raises_naming_seeds(self, bl):
+        grid, robot, esdf = self._setup(bl)
+        q = synth.refine_init(8, seed=4) * 0.3
+        far = robot.__class__(**{**robot.__dict__, "base": np.full(3, 0.05)})   # arm leaves the grid
+        _, _, cl = bl.cost(q, esdf, 8, far, grid, COST)
+        want = np.nonzero(cl.cpu().numpy())[0].tolist()
+        assert want
+        with pytest.raises(ValueError, match=r"leave the ESDF extent \(seeds " + str(want).replace("[", r"\[").replace("]", r"\]")):
+            bl.optimize(q, esdf, 8, far, grid, COST)
+        with pytest.raises(ValueError, match="leave the ESDF extent"):
+            bl.evaluate_cost_batch(q, esdf, 8, far, grid, COST)
+        with pytest.raises(ValueError, match="n_iters"):
+            bl.optimize(q, esdf, 8, robot, grid, COST, n_iters=0)
+        with pytest.raises(ValueError, match="at least one seed"):
+            bl.optimize(q[:0], esdf, 8, robot, grid, COST)
+
+    def test_strict_planner_raises_at_config3(self, torch_cuda):
+        from paper_2410_16727_b200.planner import BLPlanner
+        params = spec.random_model(spec.ENCODER_CFG3)
+        pb = synth.config3_problems(1, p0=0, seed=0)
+        pl = BLPlanner(params, spec.ENCODER_CFG3, mode=1, S=8, max_problems=1, strict=True)
+        with pytest.raises(ValueError, match="leave the ESDF extent"):
+            pl.plan_batch(pb.images, pb.q_start, pb.goal, pb.boxes)
+        pbw, grid, robot = synth.config3_wide(1, p0=0)
+        pw = BLPlanner(params, spec.ENCODER_CFG3, mode=1, S=8, max_problems=1, strict=True, grid=grid, robot=robot)
+        r = pw.plan_batch(pbw.images, pbw.q_start, pbw.goal, pbw.boxes)
+        assert not np.asarray(r.clamped).any()
+
+
 class TestSelect:
     def test_matches_oracle_with_ties(self, bl, oracle_lib):
         rng = np.random.default_rng(7)
