@@ -4,6 +4,9 @@
 // shares the layout built here.
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -893,9 +896,16 @@ struct SampleGraph {
         n_kernels = 0;
     }
 };
-static SampleGraph& sample_graph() {
-    static SampleGraph g;
-    return g;
+// One captured loop per (device, caller stream, workspace): concurrent callers on different
+// streams replay their own graphs on their own side streams.  Entries are created under the
+// mutex and never erased (std::map references stay valid).
+static SampleGraph& sample_graph(cudaStream_t caller, const void* ws) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, cudaStream_t, const void*>, SampleGraph> graphs;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    return graphs[std::make_tuple(dev, caller, ws)];
 }
 static int sample_loop(const void* packed, int mode, const void* packed_hp, int n_hp, const float* film_a,
                        const float* film_b, const float* coef_h, int K, const int* steps_h, int n_steps, int ddpm, int B,
@@ -961,7 +971,7 @@ extern "C" int ps_sample_hp(const void* packed, int mode, const void* packed_hp,
                            p0, noise_key, q_start, lo, hi, x, eps, act, traj, n, st);
     };
     if (!use_graph) return run_direct();
-    SampleGraph& G = sample_graph();
+    SampleGraph& G = sample_graph(st, ws);
     // graphs run on a private stream ordered after / before the caller's stream by events
     // (the caller may be on the legacy default stream, which cannot be captured)
     if (!G.side) {

@@ -33,6 +33,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -877,10 +880,19 @@ struct UsPlan {
     int sc_cap = 0;
     std::vector<StepCoef> sc_h;
     unsigned* d_done = nullptr;
+    cudaStream_t up = nullptr;      // private upload stream (never the caller's, which may be capturing)
+    cudaEvent_t used = nullptr;     // recorded after every launch that reads this plan's tables
 };
-static UsPlan& us_plan() {
-    static UsPlan p;
-    return p;
+// One plan per (device, workspace): concurrent samplers on different streams own different
+// workspaces (activations live there), so their plans, completion counters and tables never
+// alias.  Entries are created under the mutex and never erased (std::map references stay valid).
+static UsPlan& us_plan(const void* ws) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, UsPlan> plans;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    return plans[{dev, ws}];
 }
 
 static size_t us_smem_bytes(int n_layers, int n_grp, int n_tap) {
@@ -899,18 +911,23 @@ bool unet_persist_eligible(int B, int T) {
 }
 
 // host-side plan: layer table (tensor maps, tap lists) and step coefficients in device
-// memory.  Synchronous uploads -- call outside stream capture; rebuilt only when the
-// weights, workspace, batch or step table change.
+// memory, one per (device, workspace); rebuilt only when the weights, batch or step table change.
+// Uploads run on the plan's private stream and complete before this returns, after waiting for
+// the last launch that read the old tables (its event) -- no device-wide synchronisation, and the
+// caller's stream is never touched, so it may be capturing.
 int unet_persist_prepare(const Layout& L, const char* packed, void* ws, int B, int T, const StepCoef* sc_h,
                          int n_steps) {
     if (!get_encoder()) return PS_FAIL(PS_ERR_CUDA);
-    UsPlan& P = us_plan();
+    UsPlan& P = us_plan(ws);
     const bool same_layers = P.d_tab && P.packed == packed && P.ws == ws && P.B == B && P.T == T;
     const bool same_sc = P.d_sc && (int)P.sc_h.size() == n_steps &&
                          memcmp(P.sc_h.data(), sc_h, (size_t)n_steps * sizeof(StepCoef)) == 0;
     if (same_layers && same_sc) return PS_OK;
-    // a graph launched with the previous plan may still be reading it
-    if (cudaDeviceSynchronize() != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+    if (!P.up && (cudaStreamCreateWithFlags(&P.up, cudaStreamNonBlocking) != cudaSuccess ||
+                  cudaEventCreateWithFlags(&P.used, cudaEventDisableTiming) != cudaSuccess))
+        return PS_FAIL(PS_ERR_CUDA);
+    // a launch (or graph replay) with the previous tables may still be reading them
+    if (cudaEventSynchronize(P.used) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
     if (!same_layers) {
         std::vector<TcLayer> list;
         unet_layer_list(L, T, unet_slots(ws, B, T), false, list);
@@ -942,7 +959,9 @@ int unet_persist_prepare(const Layout& L, const char* packed, void* ws, int B, i
         memcpy(h.data() + o_hdr, hdr.data(), nl * sizeof(UsHdr));
         memcpy(h.data() + o_grp, grp.data(), grp.size() * sizeof(UsGroup));
         memcpy(h.data() + o_tap, tap.data(), tap.size() * sizeof(UsTap));
-        if (cudaMemcpy(P.d_tab, h.data(), total, cudaMemcpyHostToDevice) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+        if (cudaMemcpyAsync(P.d_tab, h.data(), total, cudaMemcpyHostToDevice, P.up) != cudaSuccess ||
+            cudaStreamSynchronize(P.up) != cudaSuccess)
+            return PS_FAIL(PS_ERR_CUDA);
         if (!P.d_done && cudaMalloc(&P.d_done, 256) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
         P.d_maps = reinterpret_cast<UsMaps*>(P.d_tab);
         P.d_hdr = reinterpret_cast<UsHdr*>(P.d_tab + o_hdr);
@@ -964,7 +983,9 @@ int unet_persist_prepare(const Layout& L, const char* packed, void* ws, int B, i
             if (cudaMalloc(&P.d_sc, (size_t)n_steps * sizeof(StepCoef)) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
             P.sc_cap = n_steps;
         }
-        if (cudaMemcpy(P.d_sc, sc_h, (size_t)n_steps * sizeof(StepCoef), cudaMemcpyHostToDevice) != cudaSuccess)
+        if (cudaMemcpyAsync(P.d_sc, sc_h, (size_t)n_steps * sizeof(StepCoef), cudaMemcpyHostToDevice, P.up) !=
+                cudaSuccess ||
+            cudaStreamSynchronize(P.up) != cudaSuccess)
             return PS_FAIL(PS_ERR_CUDA);
         P.sc_h.assign(sc_h, sc_h + n_steps);
     }
@@ -975,7 +996,7 @@ int unet_persist_prepare(const Layout& L, const char* packed, void* ws, int B, i
 int unet_persist_launch(const Layout& L, const char* packed, void* ws, float* x, int B, int T, int S, int p0,
                         unsigned key, const float* film_a, const float* film_b, int n_steps, const float* q_start,
                         float* traj, float lo, float hi, float* eps_out, cudaStream_t st) {
-    UsPlan& P = us_plan();
+    UsPlan& P = us_plan(ws);
     if (!P.d_tab || P.packed != packed || P.ws != ws || P.B != B || P.T != T || (int)P.sc_h.size() != n_steps)
         return PS_FAIL(PS_ERR_SHAPE);   // unet_persist_prepare first
     const UnetSlots u = unet_slots(ws, B, T);
@@ -1013,12 +1034,18 @@ int unet_persist_launch(const Layout& L, const char* packed, void* ws, float* x,
     static const int dbg = std::getenv("PS_TC_DBG") ? std::atoi(std::getenv("PS_TC_DBG")) : 0;
     a.dbg = dbg;
     const size_t smem = us_smem_bytes(P.n_layers, P.n_grp, P.n_tap);
-    static size_t attr_set = 0;
-    if (smem > attr_set) {
-        if (cudaFuncSetAttribute(unet_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
-            return PS_FAIL(PS_ERR_CUDA);
-        attr_set = smem;
+    {
+        static std::mutex mu;
+        static std::map<int, size_t> attr_set;   // per device
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(mu);
+        if (smem > attr_set[dev]) {
+            if (cudaFuncSetAttribute(unet_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+                cudaSuccess)
+                return PS_FAIL(PS_ERR_CUDA);
+            attr_set[dev] = smem;
+        }
     }
     // debug trace: PS_PERSIST_TRACE=<file> (uncaptured calls only, PS_NO_GRAPH=1)
     static const char* trace_path = std::getenv("PS_PERSIST_TRACE");
@@ -1058,6 +1085,7 @@ int unet_persist_launch(const Layout& L, const char* packed, void* ws, float* x,
         return US_NOT_RESIDENT;
     }
     if (le != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+    if (cudaEventRecord(P.used, st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
     if (trace_path) {
         std::vector<unsigned long long> h((size_t)grid_ * a.trace_cap * 20);
         cudaStreamSynchronize(st);

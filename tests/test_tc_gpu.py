@@ -211,3 +211,39 @@ def test_ddim10_bf16_from_k100_fp32_prefix(params, persist):
         rms[hp] = np.sqrt(((traj - want) ** 2).mean())
     assert rms[spec.HP_RSQ] < 0.1
     assert rms[spec.HP_RSQ] < 0.5 * rms[None]
+
+
+@pytest.mark.parametrize("P", [2, 24])
+def test_concurrent_streams_own_workspaces(params, P):
+    # two samplers (own workspaces -> own persistent plans, completion counters and captured
+    # graphs) driven from two host threads on two streams at once give the bits of a sequential run
+    # (P = 2: persistent kernel; P = 24: layered kernels)
+    import threading
+
+    import torch
+    from paper_2410_16727_b200.sampler import SeedSampler
+    sa, sb = SeedSampler(params, mode=1), SeedSampler(params, mode=1)
+    ca, cb = _cond(P, 31), _cond(P, 32)
+    qa, qb = synth.make_problems(P, seed=33).q_start, synth.make_problems(P, seed=34).q_start
+    want_a = sa.sample(sa.film(ca), qa, 32, p0=0).cpu().numpy()
+    want_b = sb.sample(sb.film(cb), qb, 32, p0=P).cpu().numpy()
+    got = {}
+
+    def run(name, smp, c, q, p0):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            fa = smp.film(c)
+            outs = [smp.sample(fa, q, 32, p0=p0) for _ in range(3)]
+        st.synchronize()
+        got[name] = [o.cpu().numpy() for o in outs]
+
+    th = [threading.Thread(target=run, args=("a", sa, ca, qa, 0)),
+          threading.Thread(target=run, args=("b", sb, cb, qb, P))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    for o in got["a"]:
+        assert np.array_equal(o, want_a)
+    for o in got["b"]:
+        assert np.array_equal(o, want_b)
