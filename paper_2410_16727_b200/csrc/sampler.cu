@@ -983,7 +983,9 @@ extern "C" int ps_sample_hp(const void* packed, int mode, const void* packed_hp,
     key.stream = G.side;
     auto launch_graph = [&]() -> int {
         if (cudaEventRecord(G.ev_in, st) != cudaSuccess || cudaStreamWaitEvent(G.side, G.ev_in, 0) != cudaSuccess ||
-            cudaGraphLaunch(G.exec, G.side) != cudaSuccess || cudaEventRecord(G.ev_out, G.side) != cudaSuccess ||
+            cudaGraphLaunch(G.exec, G.side) != cudaSuccess ||
+            (G.key.persist && unet_persist_mark_used(act, G.side) != PS_OK) ||
+            cudaEventRecord(G.ev_out, G.side) != cudaSuccess ||
             cudaStreamWaitEvent(st, G.ev_out, 0) != cudaSuccess)
             return PS_FAIL(PS_ERR_CUDA);
         ps_launch_counter().fetch_add(G.n_kernels, std::memory_order_relaxed);

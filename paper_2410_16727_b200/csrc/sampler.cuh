@@ -86,6 +86,7 @@ constexpr int US_NOT_RESIDENT = 100;
 bool unet_persist_eligible(int B, int T);
 int unet_persist_prepare(const Layout& L, const char* packed, void* ws, int B, int T, const StepCoef* sc_h,
                          int n_steps);
+int unet_persist_mark_used(void* ws, cudaStream_t st);
 int unet_persist_launch(const Layout& L, const char* packed, void* ws, float* x, int B, int T, int S, int p0,
                         unsigned key, const float* film_a, const float* film_b, int n_steps, const float* q_start,
                         float* traj, float lo, float hi, float* eps_out, cudaStream_t st);

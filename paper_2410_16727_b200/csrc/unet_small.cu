@@ -992,6 +992,13 @@ int unet_persist_prepare(const Layout& L, const char* packed, void* ws, int B, i
     return PS_OK;
 }
 
+// after a replay of a graph that captured unet_persist_launch on `ws`: mark the plan in use
+int unet_persist_mark_used(void* ws, cudaStream_t st) {
+    UsPlan& P = us_plan(ws);
+    if (P.used && cudaEventRecord(P.used, st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+    return PS_OK;
+}
+
 // the whole denoising loop (or one forward when eps_out is set) as one launch; capturable
 int unet_persist_launch(const Layout& L, const char* packed, void* ws, float* x, int B, int T, int S, int p0,
                         unsigned key, const float* film_a, const float* film_b, int n_steps, const float* q_start,
@@ -1085,7 +1092,11 @@ int unet_persist_launch(const Layout& L, const char* packed, void* ws, float* x,
         return US_NOT_RESIDENT;
     }
     if (le != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
-    if (cudaEventRecord(P.used, st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+    // an event recorded inside a capture cannot be waited on from the host (cudaErrorCapturedEvent):
+    // captured launches are marked by the graph's launcher (unet_persist_mark_used) instead
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
+    if (cs == cudaStreamCaptureStatusNone && cudaEventRecord(P.used, st) != cudaSuccess) return PS_FAIL(PS_ERR_CUDA);
     if (trace_path) {
         std::vector<unsigned long long> h((size_t)grid_ * a.trace_cap * 20);
         cudaStreamSynchronize(st);
