@@ -509,6 +509,131 @@ __global__ void __launch_bounds__(256) esdf_cull_kernel(const float* __restrict_
 }
 
 // ---------------------------------------------------------------------------
+// ESDF build with 3-D tile culling: one warp per 8x8x8-node tile (2x2x2 bricks of 4^3).
+// Lane b < n_boxes bounds box b's signed distance over the tile: L_b <= d_b(n) <= U_b for every
+// node n (L_b: the box-to-tile-AABB distance, -inf when they overlap; U_b: the largest corner
+// value -- a box's signed distance is convex, so its maximum over the tile is at a corner), both
+// padded by a margin far above the fp32 rounding of the node expression.  With U* = min(cap,
+// min_b U_b) >= every node's result, a box with L_b > U* cannot be any node's minimum and is
+// skipped for the whole tile; typically 1-4 of 20 boxes survive.  The survivors are evaluated
+// per node with the canonical expression, and min over a superset of the argmin boxes equals the
+// min over all boxes, so results stay bit-identical to orc_esdf_build (see esdf_cull_kernel for
+// the sqrtf / inside-term identity).  Lane l writes 4 rows of 4 k-adjacent nodes (float4, one
+// brick row in either layout).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) esdf_tile_kernel(const float* __restrict__ boxes, int n_boxes, int P, int nx,
+                                                        int ny, int nz, float ox, float oy, float oz, float h,
+                                                        float cap, float* __restrict__ out, int brick) {
+    const int lane = threadIdx.x & 31;
+    const int tx = (nx + 7) >> 3, ty = (ny + 7) >> 3, tz = (nz + 7) >> 3;
+    const long long tiles_per = (long long)tx * ty * tz, n_tiles = tiles_per * P;
+    const long long n_nodes = (long long)nx * ny * nz;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    int cur_p = -1;
+    float cx = 0.f, cy = 0.f, cz = 0.f, hx = 0.f, hy = 0.f, hz = 0.f;
+    for (long long t = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < n_tiles; t += warps) {
+        const int p = (int)(t / tiles_per);
+        long long r = t - (long long)p * tiles_per;
+        const int ti = (int)(r / ((long long)ty * tz));
+        r -= (long long)ti * ty * tz;
+        const int tj = (int)(r / tz), tk = (int)(r - (long long)tj * tz);
+        if (p != cur_p) {   // box b (centre, half extent) in lane b, as the oracle computes them
+            cur_p = p;
+            if (lane < n_boxes) {
+                const float* bx = boxes + ((size_t)p * n_boxes + lane) * 6;
+                cx = 0.5f * (bx[0] + bx[3]); hx = 0.5f * (bx[3] - bx[0]);
+                cy = 0.5f * (bx[1] + bx[4]); hy = 0.5f * (bx[4] - bx[1]);
+                cz = 0.5f * (bx[2] + bx[5]); hz = 0.5f * (bx[5] - bx[2]);
+            }
+        }
+        const int i0 = ti * 8, j0 = tj * 8, k0 = tk * 8;
+        const int i1 = min(i0 + 8, nx) - 1, j1 = min(j0 + 8, ny) - 1, k1 = min(k0 + 8, nz) - 1;
+        // tile AABB of the node positions
+        const float xa = fmaf((float)i0, h, ox), xb = fmaf((float)i1, h, ox);
+        const float ya = fmaf((float)j0, h, oy), yb = fmaf((float)j1, h, oy);
+        const float za = fmaf((float)k0, h, oz), zb = fmaf((float)k1, h, oz);
+        float L = __int_as_float(0x7f800000), U = __int_as_float(0x7f800000);
+        if (lane < n_boxes) {
+            const float gx = fmaxf(fmaxf((cx - hx) - xb, xa - (cx + hx)), 0.f);
+            const float gy = fmaxf(fmaxf((cy - hy) - yb, ya - (cy + hy)), 0.f);
+            const float gz = fmaxf(fmaxf((cz - hz) - zb, za - (cz + hz)), 0.f);
+            const float gg = gx * gx + gy * gy + gz * gz;
+            L = gg > 0.f ? sqrtf(gg) * (1.f - 1e-5f) - 1e-5f : -__int_as_float(0x7f800000);
+            float u = -__int_as_float(0x7f800000);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const float qx = fabsf(((c & 1) ? xb : xa) - cx) - hx;
+                const float qy = fabsf(((c & 2) ? yb : ya) - cy) - hy;
+                const float qz = fabsf(((c & 4) ? zb : za) - cz) - hz;
+                const float ax = fmaxf(qx, 0.f), ay = fmaxf(qy, 0.f), az = fmaxf(qz, 0.f);
+                u = fmaxf(u, sqrtf(ax * ax + ay * ay + az * az) + fminf(fmaxf(qx, fmaxf(qy, qz)), 0.f));
+            }
+            U = u + 1e-5f * (1.f + fabsf(u));
+        }
+        float ustar = fminf(U, cap);
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) ustar = fminf(ustar, __shfl_xor_sync(PS_FULL, ustar, off));
+        unsigned live = __ballot_sync(PS_FULL, lane < n_boxes && !(L > ustar));
+        // this lane's 4 rows: (i0 + (lane >> 4) + 2m, j0 + ((lane >> 1) & 7), k0 + 4 (lane & 1))
+        const int jj = j0 + ((lane >> 1) & 7), kk = k0 + 4 * (lane & 1);
+        const float py = fmaf((float)jj, h, oy);
+        float pz[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pz[e] = fmaf((float)(kk + e), h, oz);
+        float mx[4][4], mi[4][4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                mx[m][e] = __int_as_float(0x7f800000);
+                mi[m][e] = __int_as_float(0x7f800000);
+            }
+        while (live) {
+            const int b = __ffs(live) - 1;
+            live &= live - 1;
+            const float bcx = __shfl_sync(PS_FULL, cx, b), bhx = __shfl_sync(PS_FULL, hx, b);
+            const float bcy = __shfl_sync(PS_FULL, cy, b), bhy = __shfl_sync(PS_FULL, hy, b);
+            const float bcz = __shfl_sync(PS_FULL, cz, b), bhz = __shfl_sync(PS_FULL, hz, b);
+            const float qy = fabsf(py - bcy) - bhy;
+            const float ay = fmaxf(qy, 0.f);
+            float qz[4], az2[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                qz[e] = fabsf(pz[e] - bcz) - bhz;
+                const float az = fmaxf(qz[e], 0.f);
+                az2[e] = fmaf(ay, ay, az * az);   // the oracle's inner fmaf(ay, ay, az * az)
+            }
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const float px = fmaf((float)(i0 + (lane >> 4) + 2 * m), h, ox);
+                const float qx = fabsf(px - bcx) - bhx;
+                const float ax = fmaxf(qx, 0.f);
+                const float mqxy = fmaxf(qx, qy);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    mx[m][e] = fminf(mx[m][e], fmaf(ax, ax, az2[e]));
+                    mi[m][e] = fminf(mi[m][e], fmaxf(mqxy, qz[e]));
+                }
+            }
+        }
+        float* o = out + (size_t)p * (size_t)n_nodes;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int ii = i0 + (lane >> 4) + 2 * m;
+            if (ii > i1 || jj > j1 || kk > k1) continue;
+            float res[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                res[e] = fminf(cap, sqrtf(mx[m][e]));
+                if (mi[m][e] < 0.f) res[e] = fminf(res[e], mi[m][e]);
+            }
+            const size_t idx = brick ? esdf_brick_index(ii, jj, kk, ny, nz) : ((size_t)ii * ny + jj) * nz + kk;
+            *reinterpret_cast<float4*>(o + idx) = make_float4(res[0], res[1], res[2], res[3]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // select_best: one warp per problem; lexicographic (infeasible, cost, index) min.
 // ---------------------------------------------------------------------------
 __global__ void select_kernel(const float* __restrict__ cost, const uint8_t* __restrict__ feas, int P,
@@ -689,7 +814,16 @@ extern "C" int ps_esdf_build_boxes_layout(const float* boxes, int P, int n_boxes
     const long long n_nodes = (long long)n_h[0] * n_h[1] * n_h[2];
     const int threads = 256;
     cudaStream_t st = (cudaStream_t)stream;
-    if (n_boxes <= 32) {
+    static const bool no_tile = std::getenv("PS_ESDF_NO_TILE") != nullptr;   // A/B knob
+    if (n_boxes <= 32 && !no_tile && (n_h[0] & 3) == 0 && (n_h[1] & 3) == 0 && (n_h[2] & 3) == 0) {
+        const long long n_tiles = (long long)((n_h[0] + 7) / 8) * ((n_h[1] + 7) / 8) * ((n_h[2] + 7) / 8) * P;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const long long blocks = std::min<long long>((n_tiles + 7) / 8, (long long)sms * 8);
+        esdf_tile_kernel<<<(unsigned)blocks, 256, 0, st>>>(boxes, n_boxes, P, n_h[0], n_h[1], n_h[2], origin_h[0],
+                                                          origin_h[1], origin_h[2], h, cap, out, layout);
+    } else if (n_boxes <= 32) {
         const int n_col = n_h[0] * n_h[1];
         // a few blocks per problem, each looping over many columns: the per-block box setup
         // and launch cost are amortised (one column per warp made them dominate)
