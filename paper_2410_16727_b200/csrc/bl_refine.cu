@@ -43,7 +43,7 @@ struct BLParams {
 };
 
 // World term of one configuration (canonical order, see bl_oracle.c:config_world).
-template <bool WANT_GRAD, bool PIPE2 = false>
+template <bool WANT_GRAD, int PIPE = 1>
 __device__ __forceinline__ void config_world(const BLParams& P, const Grid& g, const float (&q)[NJ],
                                              float& wc, float (&gq)[NJ], float& mc, bool& cl_any) {
     f3 X{1.f, 0.f, 0.f}, Y{0.f, 1.f, 0.f}, Z{0.f, 0.f, 1.f};
@@ -99,10 +99,22 @@ __device__ __forceinline__ void config_world(const BLParams& P, const Grid& g, c
                 }
             }
         };
-        // two spheres per step: both cells' corner loads issued before either is evaluated;
-        // the accumulation order stays sequential (bit-identical to the oracle)
+        // PIPE spheres per step: all their cells' corner loads are issued before any is
+        // evaluated; the accumulation order stays sequential (bit-identical to the oracle)
         int s = P.link_start[k];
-        if (PIPE2)
+        if (PIPE >= 4)
+        for (; s + 3 < s_end; s += 4) {
+            f3 pp[4];
+            TriCell cc[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                pp[u] = sphere_pos(s + u);
+                tri_gather(g, pp[u], cc[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) accumulate(s + u, pp[u], cc[u]);
+        }
+        if (PIPE >= 2)
         for (; s + 1 < s_end; s += 2) {
             const f3 pa = sphere_pos(s), pb = sphere_pos(s + 1);
             TriCell ca, cb;
@@ -207,7 +219,7 @@ __device__ __forceinline__ float warp_min(float v) {
 // MODE 0: refine (n_iters steps + final cost/flags).  MODE 1: cost + gradient only.
 // LB: block-size bound -- 512 for throughput (one problem's 16 trajectories per block share
 // the L1), 64 for small batches (up to 255 registers: the two-sphere gathers stay in flight)
-template <int WPL, int MODE, int LB = 512, bool PIPE2 = false>
+template <int WPL, int MODE, int LB = 512, int PIPE = 1>
 __global__ void __launch_bounds__(LB) bl_refine_kernel(const __grid_constant__ BLParams P) {
     const int lane = threadIdx.x & 31;
     const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -234,7 +246,7 @@ __global__ void __launch_bounds__(LB) bl_refine_kernel(const __grid_constant__ B
         for (int w = 0; w < WPL; ++w) {
             float wc, mc, gq[NJ];
             bool cl;
-            config_world<true, PIPE2>(P, g, q[w], wc, gq, mc, cl);
+            config_world<true, PIPE>(P, g, q[w], wc, gq, mc, cl);
             cl_lane |= cl;
             ct[w] = wc + sm[w];
             const int t = lane * WPL + w;
@@ -260,7 +272,7 @@ __global__ void __launch_bounds__(LB) bl_refine_kernel(const __grid_constant__ B
         for (int w = 0; w < WPL; ++w) {
             float wc, mc;
             bool cl;
-            config_world<true, PIPE2>(P, g, q[w], wc, gw[w], mc, cl);
+            config_world<true, PIPE>(P, g, q[w], wc, gw[w], mc, cl);
         }
         smooth_terms<WPL, true>(P, q, lane, sm, gs);
 #pragma unroll
@@ -282,7 +294,7 @@ __global__ void __launch_bounds__(LB) bl_refine_kernel(const __grid_constant__ B
     for (int w = 0; w < WPL; ++w) {
         float wc, mc, gq[NJ];
         bool cl;
-        config_world<false, PIPE2>(P, g, q[w], wc, gq, mc, cl);
+        config_world<false, PIPE>(P, g, q[w], wc, gq, mc, cl);
         ct[w] = wc + sm[w];
         mc_lane = fminf(mc_lane, mc);
         cl_lane |= cl;
@@ -305,7 +317,7 @@ __global__ void __launch_bounds__(LB) bl_refine_kernel(const __grid_constant__ B
                     const float q1 = (w + 1 < WPL) ? q[w + 1 < WPL ? w + 1 : w][k] : qn[k];
                     qi[k] = fmaf(f, q1 - q[w][k], q[w][k]);
                 }
-                config_world<false, PIPE2>(P, g, qi, wc, gq, mc, cl);
+                config_world<false, PIPE>(P, g, qi, wc, gq, mc, cl);
                 mc_lane = fminf(mc_lane, mc);
                 cl_lane |= cl;
             }
@@ -695,28 +707,28 @@ static int fill_params(BLParams& P, int B, int T, int S, const float* esdf, long
 template <int MODE>
 static int launch_bl(const BLParams& P, cudaStream_t st) {
     if (P.B == 0) return PS_OK;
-    // a block holds 512 / 32 = 16 trajectories of one problem: seeds of a problem move through
-    // the same part of its ESDF, so their gathers share the SM's L1 (PS_REFINE_THREADS: A/B)
-    static const int threads = std::getenv("PS_REFINE_THREADS") ? std::atoi(std::getenv("PS_REFINE_THREADS")) : 512;
+    // large batches: blocks of one problem's trajectories (their gathers share the SM's L1), several
+    // spheres' corner loads in flight per warp (PS_REFINE_VARIANT: A/B of block size x pipeline depth)
+    static const int variant = std::getenv("PS_REFINE_VARIANT") ? std::atoi(std::getenv("PS_REFINE_VARIANT")) : 0;
     static const int small_b = std::getenv("PS_REFINE_SMALL_B") ? std::atoi(std::getenv("PS_REFINE_SMALL_B")) : 1024;
-    if (P.B <= small_b) {   // latency-bound (B <= 1024; config 2 at 2048 is faster with 16-warp blocks): few warps, each with up to 255 registers
-        const long long blocks = ((long long)P.B * 32 + 63) / 64;
-        static const bool pipe2 = std::getenv("PS_REFINE_NO_PIPE2") == nullptr;   // A/B knob
-        if (P.T == 32) {
-            if (pipe2) bl_refine_kernel<1, MODE, 64, true><<<(unsigned)blocks, 64, 0, st>>>(P);
-            else bl_refine_kernel<1, MODE, 64, false><<<(unsigned)blocks, 64, 0, st>>>(P);
-        } else {
-            if (pipe2) bl_refine_kernel<2, MODE, 64, true><<<(unsigned)blocks, 64, 0, st>>>(P);
-            else bl_refine_kernel<2, MODE, 64, false><<<(unsigned)blocks, 64, 0, st>>>(P);
+    auto go = [&](auto kern, int threads) {
+        const long long blocks = ((long long)P.B * 32 + threads - 1) / threads;
+        kern<<<(unsigned)blocks, threads, 0, st>>>(P);
+    };
+    if (P.B <= small_b) {   // latency-bound: few warps, each with up to 255 registers
+        if (P.T == 32) go(bl_refine_kernel<1, MODE, 64, 2>, 64);
+        else go(bl_refine_kernel<2, MODE, 64, 2>, 64);
+    } else if (P.T == 32) {
+        switch (variant) {
+            case 1: go(bl_refine_kernel<1, MODE, 256, 2>, 256); break;
+            case 2: go(bl_refine_kernel<1, MODE, 256, 4>, 256); break;
+            case 3: go(bl_refine_kernel<1, MODE, 128, 4>, 128); break;
+            case 4: go(bl_refine_kernel<1, MODE, 512, 2>, 512); break;
+            default: go(bl_refine_kernel<1, MODE, 512, 1>, 512);
         }
-        PS_CHECK_LAUNCH();
-        return PS_OK;
+    } else {
+        go(bl_refine_kernel<2, MODE, 512, 1>, 512);
     }
-    const long long blocks = ((long long)P.B * 32 + threads - 1) / threads;
-    if (P.T == 32)
-        bl_refine_kernel<1, MODE><<<(unsigned)blocks, threads, 0, st>>>(P);
-    else
-        bl_refine_kernel<2, MODE><<<(unsigned)blocks, threads, 0, st>>>(P);
     PS_CHECK_LAUNCH();
     return PS_OK;
 }
