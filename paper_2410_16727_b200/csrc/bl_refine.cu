@@ -707,25 +707,20 @@ static int fill_params(BLParams& P, int B, int T, int S, const float* esdf, long
 template <int MODE>
 static int launch_bl(const BLParams& P, cudaStream_t st) {
     if (P.B == 0) return PS_OK;
-    // large batches: blocks of one problem's trajectories (their gathers share the SM's L1), several
-    // spheres' corner loads in flight per warp (PS_REFINE_VARIANT: A/B of block size x pipeline depth)
-    static const int variant = std::getenv("PS_REFINE_VARIANT") ? std::atoi(std::getenv("PS_REFINE_VARIANT")) : 0;
+    // large batches: 512-thread blocks of one problem's trajectories (their gathers share the SM's
+    // L1), one sphere's corner loads in flight per warp.  Measured at 1024 x 32 (bricked ESDF):
+    // 13.7 ms; 2 spheres in flight 14.3 ms, 256-thread blocks with 2 / 4 in flight 15.3 / 28.6 ms
+    // (registers: 118 -> 125 / 146 per thread cost more occupancy than the overlap gains).
     static const int small_b = std::getenv("PS_REFINE_SMALL_B") ? std::atoi(std::getenv("PS_REFINE_SMALL_B")) : 1024;
     auto go = [&](auto kern, int threads) {
         const long long blocks = ((long long)P.B * 32 + threads - 1) / threads;
         kern<<<(unsigned)blocks, threads, 0, st>>>(P);
     };
-    if (P.B <= small_b) {   // latency-bound: few warps, each with up to 255 registers
+    if (P.B <= small_b) {   // latency-bound: few warps, each with up to 255 registers, 2 spheres in flight
         if (P.T == 32) go(bl_refine_kernel<1, MODE, 64, 2>, 64);
         else go(bl_refine_kernel<2, MODE, 64, 2>, 64);
     } else if (P.T == 32) {
-        switch (variant) {
-            case 1: go(bl_refine_kernel<1, MODE, 256, 2>, 256); break;
-            case 2: go(bl_refine_kernel<1, MODE, 256, 4>, 256); break;
-            case 3: go(bl_refine_kernel<1, MODE, 128, 4>, 128); break;
-            case 4: go(bl_refine_kernel<1, MODE, 512, 2>, 512); break;
-            default: go(bl_refine_kernel<1, MODE, 512, 1>, 512);
-        }
+        go(bl_refine_kernel<1, MODE, 512, 1>, 512);
     } else {
         go(bl_refine_kernel<2, MODE, 512, 1>, 512);
     }
