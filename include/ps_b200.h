@@ -89,6 +89,19 @@ int ps_bl_optimize(const float* q_in, int B, int T, int S, const float* esdf, lo
                    const float* sph_h, const int* sph_link_h, int n_sph, const float* weights_h, int n_iters,
                    float* q_out, float* cost, uint8_t* feasible, uint8_t* clamped, uint8_t* clamped0, void* stream);
 
+/* Ground-truth evaluation of B trajectories (trajopt.metrics / retime / traj_min_clearance,
+ * trajopt.py:209-272, _kernels.py:144-162) against each problem's analytic boxes (P, n_boxes, 6)
+ * and goal (P, 7: xyz relative to the base, quaternion w x y z): per trajectory the min clearance
+ * over waypoints + `interp` interpolants per segment (sphere surface to box SDF, capped at cap),
+ * the end pose's translation / rotation error (frame after joint 7), the retimed motion time and
+ * max jerk for limits_h = (vel, acc, jerk), collision_free = clearance > 0 and success =
+ * collision_free && terr <= delta_t && aerr <= delta_r_deg.  T in {32, 64}. */
+int ps_bl_metrics(const float* traj, int B, int T, int S, const float* boxes, int n_boxes, const float* goal,
+                  const float* dh_h, const float* base_h, const float* sph_h, const int* sph_link_h, int n_sph,
+                  const float* limits_h, float cap, float delta_t, float delta_r_deg, int interp, float* clearance,
+                  float* terr, float* aerr_deg, float* motion_time, float* max_jerk, uint8_t* success,
+                  uint8_t* collision_free, void* stream);
+
 /* Best seed per problem: lowest-cost feasible seed, else lowest cost; ties to the
  * lower index.  pipeline.select_best (pipeline.py:160-165).  best: (P,) int32. */
 int ps_select(const float* cost, const uint8_t* feasible, int P, int S, int32_t* best,

@@ -193,3 +193,79 @@ def select_best(cost: np.ndarray, feasible: np.ndarray, S: int) -> np.ndarray:
         pool = [i for i in range(S) if f[i]] or list(range(S))
         out[p] = min(pool, key=lambda i: (c[i], i))
     return out
+
+
+# ----------------------------------------------------------------------------
+# Ground-truth evaluation (trajopt.metrics / retime / traj_min_clearance,
+# planseed/trajopt.py:209-272, planseed/_kernels.py:144-162), 3-D BL form
+# ----------------------------------------------------------------------------
+
+def box_sdf(boxes: np.ndarray, pts: np.ndarray, cap: float) -> np.ndarray:
+    """Analytic signed distance (..., 3) -> (...,) to the union of axis-aligned boxes (nb, 6),
+    capped at `cap` (planseed/_kernels.py:60-83 in 3-D)."""
+    b = np.asarray(boxes, dtype=np.float64)
+    d = np.full(pts.shape[:-1], cap, dtype=np.float64)
+    if b.shape[0] == 0:
+        return d
+    c = 0.5 * (b[:, :3] + b[:, 3:])
+    hw = 0.5 * (b[:, 3:] - b[:, :3])
+    q = np.abs(pts[..., None, :] - c) - hw                     # (..., nb, 3)
+    out = np.linalg.norm(np.maximum(q, 0.0), axis=-1)
+    ins = np.minimum(q.max(axis=-1), 0.0)
+    return np.minimum(d, (out + ins).min(axis=-1))
+
+
+def traj_min_clearance(robot, boxes, traj: np.ndarray, cap: float, interp_per_seg: int = 4) -> float:
+    """Min over waypoints and interp_per_seg interpolants per segment of min over spheres of
+    (box SDF at the centre - radius)."""
+    traj = np.asarray(traj, dtype=np.float64)
+    f = (np.arange(interp_per_seg) + 1.0) / (interp_per_seg + 1.0)
+    qi = traj[:-1, None, :] + f[None, :, None] * (traj[1:, None, :] - traj[:-1, None, :])
+    qs = np.concatenate([traj, qi.reshape(-1, traj.shape[1])], axis=0)
+    p, _ = sphere_centers(robot, qs)
+    return float((box_sdf(boxes, p, cap) - robot.sphere_radius).min())
+
+
+def retime(traj: np.ndarray, vel=2.1, acc=15.0, jerk=7500.0):
+    """(motion_time, max_jerk) -- planseed/trajopt.py:209-228 and metrics' max-jerk line."""
+    traj = np.asarray(traj, dtype=np.float64)
+    n = traj.shape[0]
+    D = diff_matrix(n)
+    v = D @ traj
+    a = D @ v
+    j = D @ a
+    dt = max(float(np.max(np.abs(v).max(0) / vel)), float(np.sqrt(np.max(np.abs(a).max(0) / acc))),
+             float(np.cbrt(np.max(np.abs(j).max(0) / jerk))))
+    mt = dt * (n - 1)
+    return mt, (float(np.abs(j).max()) / dt ** 3 if mt > 0.0 else 0.0)
+
+
+def quat_matrix(qw, qx, qy, qz) -> np.ndarray:
+    return np.array([[1 - 2 * (qy * qy + qz * qz), 2 * (qx * qy - qz * qw), 2 * (qx * qz + qy * qw)],
+                     [2 * (qx * qy + qz * qw), 1 - 2 * (qx * qx + qz * qz), 2 * (qy * qz - qx * qw)],
+                     [2 * (qx * qz - qy * qw), 2 * (qy * qz + qx * qw), 1 - 2 * (qx * qx + qy * qy)]])
+
+
+def end_pose_errors(robot, q_last: np.ndarray, goal: np.ndarray):
+    """(translation error m, rotation error deg) of the frame after joint 7 against the goal
+    (xyz relative to the base, unit quaternion w, x, y, z)."""
+    F = dh_frames(robot, np.asarray(q_last, dtype=np.float64))[-1]
+    terr = float(np.linalg.norm(F[:3, 3] - robot.base - goal[:3]))
+    G = quat_matrix(*goal[3:7])
+    R = G.T @ F[:3, :3]
+    v = np.array([R[2, 1] - R[1, 2], R[0, 2] - R[2, 0], R[1, 0] - R[0, 1]])
+    ang = np.arctan2(np.linalg.norm(v), np.trace(R) - 1.0)
+    return terr, float(np.degrees(ang))
+
+
+def bl_metrics(robot, boxes, goal, traj, cap, delta_t=0.005, delta_r_deg=2.86, interp_per_seg=4,
+               limits=(2.1, 15.0, 7500.0)):
+    """trajopt.metrics for one BL trajectory: dict of success, collision_free, clearance,
+    translation_error, angle_error_deg, motion_time, max_jerk."""
+    clr = traj_min_clearance(robot, boxes, traj, cap, interp_per_seg)
+    terr, aerr = end_pose_errors(robot, traj[-1], np.asarray(goal, dtype=np.float64))
+    mt, mj = retime(traj, *limits)
+    free = clr > 0.0
+    return {"success": bool(free and terr <= delta_t and aerr <= delta_r_deg), "collision_free": free,
+            "clearance": clr, "translation_error": terr, "angle_error_deg": aerr, "motion_time": mt,
+            "max_jerk": mj}

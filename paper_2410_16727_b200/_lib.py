@@ -39,6 +39,8 @@ _SIGS = {
                           _c_int, _vp, _vp, _vp, _vp, _vp],
     "ps_bl_optimize": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _c_int, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,
                        _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp],
+    "ps_bl_metrics": [_vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _c_int, _vp, _c_f, _c_f,
+                      _c_f, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "ps_select": [_vp, _vp, _c_int, _c_int, _vp, _vp],
     "ps_unet_param_count": [],
     "ps_unet_param_offset": [ctypes.c_char_p],

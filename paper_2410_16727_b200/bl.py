@@ -203,6 +203,53 @@ def refine(q, esdf, S: int, robot: DHRobot, grid: GridSpec = GridSpec(), w: BLCo
     return qo, c, f, cl
 
 
+@dataclass
+class BLMetrics:
+    """trajopt.TrajectoryMetrics for a batch (device tensors, one entry per trajectory)."""
+
+    success: object
+    collision_free: object
+    clearance: object
+    translation_error: object
+    angle_error_deg: object
+    motion_time: object
+    max_jerk: object
+
+
+def metrics(traj, boxes, goal, S: int, robot: DHRobot, cap: float = GridSpec().cap,
+            delta_t: float | None = None, delta_r_deg: float | None = None,
+            interp_per_seg: int | None = None, limits=None, stream=None) -> BLMetrics:
+    """Ground-truth evaluation of (B, T, 7) trajectories against each problem's analytic boxes
+    (P, n_boxes, 6) and goal (P, 7) -- trajopt.metrics / retime / traj_min_clearance
+    (trajopt.py:209-272, _kernels.py:144-162) in 3-D, one launch for the whole batch."""
+    from . import spec
+    torch = _lib.require_cuda()
+    q = _dev(traj)
+    B, T, D = q.shape
+    if D != 7 or T not in (32, 64):
+        raise ValueError("traj must be (B, 32|64, 7)")
+    bx, g = _dev(boxes), _dev(goal)
+    if bx.dim() != 3 or bx.shape[2] != 6 or g.shape != (bx.shape[0], 7) or bx.shape[0] * S < B:
+        raise ValueError("boxes (P, n_boxes, 6) and goal (P, 7) for P = B / S problems")
+    rt = RobotTables.of(robot)
+    lim = np.asarray(limits if limits is not None else (spec.VEL_LIMIT, spec.ACC_LIMIT, spec.JERK_LIMIT),
+                     dtype=np.float32)
+    f = lambda: torch.empty(B, dtype=torch.float32, device="cuda")
+    u = lambda: torch.empty(B, dtype=torch.uint8, device="cuda")
+    out = BLMetrics(u(), u(), f(), f(), f(), f(), f())
+    st = _lib.lib().ps_bl_metrics(
+        _lib.ptr(q), B, T, S, _lib.ptr(bx), bx.shape[1], _lib.ptr(g), _lib.hptr(rt.dh), _lib.hptr(rt.base),
+        _lib.hptr(rt.sph), _lib.hptr(rt.link), len(rt.link), _lib.hptr(lim), float(cap),
+        spec.DELTA_T if delta_t is None else float(delta_t),
+        spec.DELTA_R_DEG if delta_r_deg is None else float(delta_r_deg),
+        spec.INTERP_PER_SEG if interp_per_seg is None else int(interp_per_seg),
+        _lib.ptr(out.clearance), _lib.ptr(out.translation_error), _lib.ptr(out.angle_error_deg),
+        _lib.ptr(out.motion_time), _lib.ptr(out.max_jerk), _lib.ptr(out.success), _lib.ptr(out.collision_free),
+        _lib.stream_handle(stream))
+    _lib.check(st, "bl_metrics")
+    return out
+
+
 def select(cost_, feasible, S: int, stream=None, out=None):
     """Best seed per problem (P,) int32: lowest-cost feasible, else lowest cost, ties low."""
     torch = _lib.require_cuda()

@@ -342,6 +342,187 @@ __global__ void __launch_bounds__(LB) bl_refine_kernel(const __grid_constant__ B
 }
 
 // ---------------------------------------------------------------------------
+// Ground-truth evaluation (trajopt.metrics / retime / traj_min_clearance, planseed/trajopt.py:
+// 209-272, _kernels.py:144-162) against the problem's analytic boxes: one warp per trajectory,
+// lane = waypoint(s).  Clearance = min over waypoints + interp interpolants per segment of
+// min over spheres of (box SDF at the centre - radius), capped; end-pose errors of the frame after
+// joint 7; uniform retiming from the D / D^2 / D^3 stencils and the per-joint limits.
+// ---------------------------------------------------------------------------
+struct BLMetricArgs {
+    const float* traj;        // (B, T, 7)
+    const float* boxes;       // (P, n_boxes, 6)
+    const float* goal;        // (P, 7): xyz relative to the base, quaternion (w, x, y, z)
+    int n_boxes, interp;
+    float cap, vel, acc, jerk, delta_t, delta_r_deg;
+    float* clearance;         // (B,)
+    float* terr;
+    float* aerr_deg;
+    float* motion_time;
+    float* max_jerk;
+    uint8_t* success;
+    uint8_t* collision_free;
+};
+
+// FK of one configuration; calls f(link k, X, Y, Z, o) after each joint (frame k+1)
+template <typename F>
+__device__ __forceinline__ void fk_frames(const BLParams& P, const float (&q)[NJ], F&& f) {
+    f3 X{1.f, 0.f, 0.f}, Y{0.f, 1.f, 0.f}, Z{0.f, 0.f, 1.f};
+    f3 o{P.base[0], P.base[1], P.base[2]};
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) {
+        float sn, cs;
+        c_sincos(q[k], sn, cs);
+        const float a = P.dh[k][0], dd = P.dh[k][1], ca = P.dh[k][2], sa = P.dh[k][3];
+        const float ac = a * cs, as = a * sn;
+        o.x = fmaf(ac, X.x, fmaf(as, Y.x, fmaf(dd, Z.x, o.x)));
+        o.y = fmaf(ac, X.y, fmaf(as, Y.y, fmaf(dd, Z.y, o.y)));
+        o.z = fmaf(ac, X.z, fmaf(as, Y.z, fmaf(dd, Z.z, o.z)));
+        f3 X1{fmaf(cs, X.x, sn * Y.x), fmaf(cs, X.y, sn * Y.y), fmaf(cs, X.z, sn * Y.z)};
+        f3 Y1{fmaf(cs, Y.x, -(sn * X.x)), fmaf(cs, Y.y, -(sn * X.y)), fmaf(cs, Y.z, -(sn * X.z))};
+        f3 Y2{fmaf(ca, Y1.x, sa * Z.x), fmaf(ca, Y1.y, sa * Z.y), fmaf(ca, Y1.z, sa * Z.z)};
+        f3 Z2{fmaf(ca, Z.x, -(sa * Y1.x)), fmaf(ca, Z.y, -(sa * Y1.y)), fmaf(ca, Z.z, -(sa * Y1.z))};
+        X = X1;
+        Y = Y2;
+        Z = Z2;
+        f(k, X, Y, Z, o);
+    }
+}
+
+__device__ __forceinline__ float config_clearance3(const BLParams& P, const float (&q)[NJ], const float* bx, int nb,
+                                                   float cap) {
+    float best = cap;
+    fk_frames(P, q, [&](int k, const f3& X, const f3& Y, const f3& Z, const f3& o) {
+        for (int s = P.link_start[k]; s < P.link_start[k + 1]; ++s) {
+            const float lx = P.sph[s][0], ly = P.sph[s][1], lz = P.sph[s][2];
+            const float px = fmaf(X.x, lx, fmaf(Y.x, ly, fmaf(Z.x, lz, o.x)));
+            const float py = fmaf(X.y, lx, fmaf(Y.y, ly, fmaf(Z.y, lz, o.y)));
+            const float pz = fmaf(X.z, lx, fmaf(Y.z, ly, fmaf(Z.z, lz, o.z)));
+            float d = cap;
+            for (int b = 0; b < nb; ++b) {
+                const float* c = bx + 6 * b;   // centre, half extent
+                const float qx = fabsf(px - c[0]) - c[3], qy = fabsf(py - c[1]) - c[4], qz = fabsf(pz - c[2]) - c[5];
+                const float ax = fmaxf(qx, 0.f), ay = fmaxf(qy, 0.f), az = fmaxf(qz, 0.f);
+                d = fminf(d, sqrtf(fmaf(ax, ax, fmaf(ay, ay, az * az))) + fminf(fmaxf(qx, fmaxf(qy, qz)), 0.f));
+            }
+            best = fminf(best, d - P.sph[s][3]);
+        }
+    });
+    return best;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) v = fmaxf(v, __shfl_xor_sync(PS_FULL, v, off));
+    return v;
+}
+
+template <int WPL>
+__global__ void __launch_bounds__(256) bl_metrics_kernel(const __grid_constant__ BLParams P,
+                                                          const __grid_constant__ BLMetricArgs M) {
+    __shared__ float s_box[8][64 * 6];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (b >= P.B) return;   // whole warp
+    const int p = b / P.S;
+    float* bx = s_box[wib];
+    for (int i = lane; i < M.n_boxes * 3; i += 32) {
+        const int k = i / 3, a = i % 3;
+        const float lo = M.boxes[((size_t)p * M.n_boxes + k) * 6 + a], hi = M.boxes[((size_t)p * M.n_boxes + k) * 6 + 3 + a];
+        bx[6 * k + a] = 0.5f * (lo + hi);
+        bx[6 * k + 3 + a] = 0.5f * (hi - lo);
+    }
+    __syncwarp();
+    float q[WPL][NJ];
+    const float* qb = M.traj + (size_t)b * P.T * NJ;
+#pragma unroll
+    for (int w = 0; w < WPL; ++w)
+#pragma unroll
+        for (int k = 0; k < NJ; ++k) q[w][k] = qb[(lane * WPL + w) * NJ + k];
+    // clearance at the waypoints and the interpolants toward the next waypoint
+    float qn[NJ];
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) qn[k] = __shfl_down_sync(PS_FULL, q[0][k], 1);
+    float clr = M.cap;
+#pragma unroll
+    for (int w = 0; w < WPL; ++w) {
+        clr = fminf(clr, config_clearance3(P, q[w], bx, M.n_boxes, M.cap));
+        const int t = lane * WPL + w;
+        if (t + 1 < P.T) {
+            for (int i = 0; i < M.interp; ++i) {
+                const float f = (float)(i + 1) / (float)(M.interp + 1);
+                float qi[NJ];
+#pragma unroll
+                for (int k = 0; k < NJ; ++k) {
+                    const float q1 = (w + 1 < WPL) ? q[w + 1 < WPL ? w + 1 : w][k] : qn[k];
+                    qi[k] = fmaf(f, q1 - q[w][k], q[w][k]);
+                }
+                clr = fminf(clr, config_clearance3(P, qi, bx, M.n_boxes, M.cap));
+            }
+        }
+    }
+    clr = warp_min(clr);
+    // retiming: per-joint max |D q|, |D^2 q|, |D^3 q| over the trajectory
+    float rv = 0.f, ra = 0.f, rj = 0.f, jmax = 0.f;
+#pragma unroll
+    for (int k = 0; k < NJ; ++k) {
+        float y[WPL], v[WPL], a[WPL], jk[WPL];
+#pragma unroll
+        for (int w = 0; w < WPL; ++w) y[w] = q[w][k];
+        stencil<WPL, false>(y, v, lane, P.T);
+        stencil<WPL, false>(v, a, lane, P.T);
+        stencil<WPL, false>(a, jk, lane, P.T);
+        float mv = 0.f, ma = 0.f, mj = 0.f;
+#pragma unroll
+        for (int w = 0; w < WPL; ++w) {
+            mv = fmaxf(mv, fabsf(v[w]));
+            ma = fmaxf(ma, fabsf(a[w]));
+            mj = fmaxf(mj, fabsf(jk[w]));
+        }
+        mv = warp_max(mv);
+        ma = warp_max(ma);
+        mj = warp_max(mj);
+        rv = fmaxf(rv, mv / M.vel);
+        ra = fmaxf(ra, ma / M.acc);
+        rj = fmaxf(rj, mj / M.jerk);
+        jmax = fmaxf(jmax, mj);
+    }
+    const float dt = fmaxf(rv, fmaxf(sqrtf(ra), cbrtf(rj)));
+    const float mt = dt * (float)(P.T - 1);
+    // end pose: the lane holding the last waypoint
+    if (lane == (P.T - 1) / WPL) {
+        float ql[NJ];
+#pragma unroll
+        for (int k = 0; k < NJ; ++k) ql[k] = q[WPL - 1][k];
+        f3 E[3], oe{0.f, 0.f, 0.f};
+        fk_frames(P, ql, [&](int k, const f3& X, const f3& Y, const f3& Z, const f3& o) {
+            if (k == NJ - 1) {
+                E[0] = X; E[1] = Y; E[2] = Z; oe = o;
+            }
+        });
+        const float* g = M.goal + (size_t)p * 7;
+        const float dx = (oe.x - P.base[0]) - g[0], dy = (oe.y - P.base[1]) - g[1], dz = (oe.z - P.base[2]) - g[2];
+        const float terr = sqrtf(dx * dx + dy * dy + dz * dz);
+        const float w = g[3], x = g[4], y = g[5], z = g[6];
+        const f3 G[3] = {{1.f - 2.f * (y * y + z * z), 2.f * (x * y + z * w), 2.f * (x * z - y * w)},
+                         {2.f * (x * y - z * w), 1.f - 2.f * (x * x + z * z), 2.f * (y * z + x * w)},
+                         {2.f * (x * z + y * w), 2.f * (y * z - x * w), 1.f - 2.f * (x * x + y * y)}};
+        auto dot = [](const f3& u, const f3& v) { return u.x * v.x + u.y * v.y + u.z * v.z; };
+        const float tr = dot(G[0], E[0]) + dot(G[1], E[1]) + dot(G[2], E[2]);
+        const float v0 = dot(G[2], E[1]) - dot(G[1], E[2]), v1 = dot(G[0], E[2]) - dot(G[2], E[0]),
+                    v2 = dot(G[1], E[0]) - dot(G[0], E[1]);
+        const float aerr = atan2f(sqrtf(v0 * v0 + v1 * v1 + v2 * v2), tr - 1.f) * 57.29577951308232f;
+        const bool free_ = clr > 0.f;
+        M.clearance[b] = clr;
+        M.terr[b] = terr;
+        M.aerr_deg[b] = aerr;
+        M.motion_time[b] = mt;
+        M.max_jerk[b] = mt > 0.f ? jmax / (dt * dt * dt) : 0.f;
+        M.collision_free[b] = free_ ? 1 : 0;
+        M.success[b] = (free_ && terr <= M.delta_t && aerr <= M.delta_r_deg) ? 1 : 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // ESDF build: 4 consecutive z nodes per thread, float4 store (nz % 4 == 0).
 // ---------------------------------------------------------------------------
 constexpr int MAX_BOXES = 64;
@@ -781,6 +962,31 @@ extern "C" int ps_bl_optimize(const float* q_in, int B, int T, int S, const floa
         if (c0[(size_t)b]) return PS_ERR_OUT_OF_GRID;
     return ps_bl_refine_layout(q_in, B, T, S, esdf, esdf_stride, layout, n_h, origin_h, h, dh_h, base_h, sph_h,
                                sph_link_h, n_sph, weights_h, n_iters, q_out, cost, feasible, clamped, stream);
+}
+
+extern "C" int ps_bl_metrics(const float* traj, int B, int T, int S, const float* boxes, int n_boxes,
+                             const float* goal, const float* dh_h, const float* base_h, const float* sph_h,
+                             const int* sph_link_h, int n_sph, const float* limits_h, float cap, float delta_t,
+                             float delta_r_deg, int interp, float* clearance, float* terr, float* aerr_deg,
+                             float* motion_time, float* max_jerk, uint8_t* success, uint8_t* collision_free,
+                             void* stream) {
+    if (n_boxes < 0 || n_boxes > 64 || interp < 0) return PS_FAIL(PS_ERR_SHAPE);
+    BLParams P{};
+    const int n_dummy[3] = {2, 2, 2};
+    const float o_dummy[3] = {0.f, 0.f, 0.f}, w_dummy[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int st = fill_params(P, B, T, S, nullptr, 0, n_dummy, o_dummy, 1.f, dh_h, base_h, sph_h, sph_link_h, n_sph,
+                         w_dummy);
+    if (st) return st;
+    if (B == 0) return PS_OK;
+    BLMetricArgs M{traj, boxes, goal, n_boxes, interp, cap, limits_h[0], limits_h[1], limits_h[2], delta_t,
+                   delta_r_deg, clearance, terr, aerr_deg, motion_time, max_jerk, success, collision_free};
+    const unsigned blocks = (unsigned)(((long long)B * 32 + 255) / 256);
+    if (T == 32)
+        bl_metrics_kernel<1><<<blocks, 256, 0, (cudaStream_t)stream>>>(P, M);
+    else
+        bl_metrics_kernel<2><<<blocks, 256, 0, (cudaStream_t)stream>>>(P, M);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
 }
 
 extern "C" int ps_bl_refine(const float* q_in, int B, int T, int S, const float* esdf,

@@ -154,6 +154,13 @@ class BLCost:
 
 INTERP_PER_SEG = 4  # planseed/pipeline.py:139-157 dense check
 
+# Ground-truth evaluation (trajopt.metrics / retime, planseed/trajopt.py:209-272): planseed's
+# per-joint limits (arm.py:48-53) and the PlanRequest success thresholds (pipeline.py:37-60).
+# BL end pose: the frame after joint 7; goal xyz is relative to the robot base, the goal
+# quaternion (w, x, y, z) is the end-effector orientation in the base (= world) axes.
+VEL_LIMIT, ACC_LIMIT, JERK_LIMIT = 2.1, 15.0, 7500.0
+DELTA_T, DELTA_R_DEG = 0.005, 2.86
+
 # ----------------------------------------------------------------------------
 # Observation encoder (depth CNN) and condition vector
 # ----------------------------------------------------------------------------

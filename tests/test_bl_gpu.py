@@ -193,6 +193,56 @@ class TestReferenceSemantics:
         assert not np.asarray(r.clamped).any()
 
 
+class TestMetrics:
+    """bl.metrics (ps_bl_metrics, fp32) against the float64 oracle's trajopt.metrics restatement
+    (oracle/bl_numpy.bl_metrics, pinned to planseed in test_bl_oracle.TestMetricsOracle).
+    Bounds: clearance / translation error within 2e-5 m, angle within 1e-2 deg, motion time and
+    max jerk within 1e-4 relative; flags equal wherever the value is not within that bound of
+    its threshold."""
+
+    def _case(self, P=6, S=8, seed=0):
+        from oracle import bl_numpy as bn
+        pb, grid, robot = synth.config3_wide(P, p0=seed)
+        q = synth.refine_init(P * S, seed=seed + 1) * 0.35
+        # half the problems get their goal at the last waypoint's own end pose (success decided by
+        # clearance alone), the rest a random goal
+        goal = pb.goal.astype(np.float64).copy()
+        for p in range(0, P, 2):
+            F = bn.dh_frames(robot, q[p * S + 1, -1].astype(np.float64))[-1]
+            R = F[:3, :3]
+            w = np.sqrt(max(1e-12, 1 + np.trace(R))) / 2
+            goal[p] = np.concatenate([F[:3, 3] - robot.base, [w, (R[2, 1] - R[1, 2]) / (4 * w),
+                                      (R[0, 2] - R[2, 0]) / (4 * w), (R[1, 0] - R[0, 1]) / (4 * w)]])
+        return pb.boxes, goal.astype(np.float32), q, robot, grid
+
+    @pytest.mark.parametrize("T", [32, 64])
+    def test_vs_oracle(self, bl, T):
+        from oracle import bl_numpy as bn
+        S = 8
+        boxes, goal, q, robot, grid = self._case(S=S)
+        if T == 64:
+            q = np.repeat(q, 2, axis=1)
+        m = bl.metrics(q, boxes, goal, S, robot, cap=grid.cap)
+        got = {k: getattr(m, k).cpu().numpy() for k in ("clearance", "translation_error", "angle_error_deg",
+                                                         "motion_time", "max_jerk", "success", "collision_free")}
+        n_succ = 0
+        for b in range(len(q)):
+            r = bn.bl_metrics(robot, boxes[b // S], goal[b // S].astype(np.float64), q[b].astype(np.float64),
+                              grid.cap)
+            assert abs(got["clearance"][b] - r["clearance"]) < 2e-5
+            assert abs(got["translation_error"][b] - r["translation_error"]) < 2e-5
+            assert abs(got["angle_error_deg"][b] - r["angle_error_deg"]) < 1e-2
+            assert got["motion_time"][b] == pytest.approx(r["motion_time"], rel=1e-4)
+            assert got["max_jerk"][b] == pytest.approx(r["max_jerk"], rel=1e-4)
+            if abs(r["clearance"]) > 2e-5:
+                assert bool(got["collision_free"][b]) == r["collision_free"]
+                if (abs(r["translation_error"] - spec.DELTA_T) > 2e-5 and abs(r["angle_error_deg"] - spec.DELTA_R_DEG) > 1e-2):
+                    assert bool(got["success"][b]) == r["success"]
+            n_succ += r["success"]
+        assert 0 < n_succ < len(q)                     # both outcomes exercised
+        assert 0 < got["collision_free"].mean() < 1
+
+
 class TestSelect:
     def test_matches_oracle_with_ties(self, bl, oracle_lib):
         rng = np.random.default_rng(7)

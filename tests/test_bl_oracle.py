@@ -245,3 +245,67 @@ class TestBridgeToPlanseed:
         assert not cl.any()
         np.testing.assert_allclose(c64, tot, rtol=1e-10, atol=1e-12)
         np.testing.assert_allclose(g64, grad, rtol=1e-9, atol=1e-9)
+
+
+class TestMetricsOracle:
+    """oracle.bl_numpy ground-truth evaluation pinned to planseed's own retime / metrics /
+    traj_min_clearance (trajopt.py:209-272, _kernels.py:144-162)."""
+
+    def test_retime_matches_planseed(self, planseed):
+        from planseed.arm import default_arm
+        from planseed.trajopt import jerk_matrix, retime
+        arm = default_arm()
+        rng = np.random.default_rng(5)
+        for T in (32, 64):
+            traj = np.cumsum(rng.standard_normal((T, 7)) * 0.05, axis=0)
+            mt_ref, _ = retime(arm, traj)
+            dt = mt_ref / (T - 1)
+            mj_ref = float(np.max(np.abs(jerk_matrix(T) @ traj)) / dt ** 3)
+            mt, mj = bn.retime(traj, arm.vel_limit[0], arm.acc_limit[0], arm.jerk_limit[0])
+            assert mt == pytest.approx(mt_ref, rel=1e-12) and mj == pytest.approx(mj_ref, rel=1e-9)
+        assert bn.retime(np.zeros((32, 7)))[0] == 0.0
+        assert (spec.VEL_LIMIT, spec.ACC_LIMIT, spec.JERK_LIMIT) == (arm.vel_limit[0], arm.acc_limit[0],
+                                                                     arm.jerk_limit[0])
+
+    def test_clearance_matches_planseed_in_the_planar_degenerate_case(self, planseed):
+        # zero-radius spheres at planseed's collision points, boxes extruded along z: the 3-D
+        # clearance equals planseed's traj_min_clearance over the same boxes
+        from planseed import _kernels as K
+        from planseed.arm import default_arm
+        from planseed.geometry import Box, World
+        arm = default_arm()
+        world = World([Box(lo=(-0.5, 0.3), hi=(-0.1, 0.6)), Box(lo=(0.2, -0.7), hi=(0.6, -0.3))])
+        m = arm.points_per_link
+        fr = arm.point_fractions()
+        link = np.repeat(np.arange(7), m)
+        off = np.zeros((7 * m, 3))
+        off[:, 0] = -(1.0 - np.tile(fr, 7)) * arm.lengths[link]
+        robot = spec.DHRobot(a=arm.lengths.copy(), d=np.zeros(7), alpha=np.zeros(7),
+                             base=np.array([arm.base[0], arm.base[1], 0.0]), lo=arm.lo, hi=arm.hi,
+                             sphere_link=link.astype(np.int32), sphere_offset=off, sphere_radius=np.zeros(7 * m))
+        boxes3 = np.array([[b[0], b[1], -50.0, b[2], b[3], 50.0] for b in world.box_arr])
+        rng = np.random.default_rng(8)
+        for _ in range(5):
+            traj = np.cumsum(rng.standard_normal((32, 7)) * 0.1, axis=0)
+            want = K.traj_min_clearance(traj, 4, arm.lengths, float(arm.base[0]), float(arm.base[1]),
+                                        arm.point_fractions(), np.zeros((0, 3)), world.box_arr, world.sdf_cap)
+            got = bn.traj_min_clearance(robot, boxes3, traj, world.sdf_cap, 4)
+            assert got == pytest.approx(want, rel=1e-12, abs=1e-12)
+
+    def test_end_pose_errors_zero_at_own_pose(self):
+        rng = np.random.default_rng(3)
+        q = rng.uniform(-2, 2, 7)
+        F = bn.dh_frames(RB, q)[-1]
+        R = F[:3, :3]
+        w = np.sqrt(max(1e-12, 1 + np.trace(R))) / 2
+        quat = np.array([w, (R[2, 1] - R[1, 2]) / (4 * w), (R[0, 2] - R[2, 0]) / (4 * w), (R[1, 0] - R[0, 1]) / (4 * w)])
+        goal = np.concatenate([F[:3, 3] - RB.base, quat])
+        terr, aerr = bn.end_pose_errors(RB, q, goal)
+        assert terr < 1e-12 and aerr < 1e-6
+        # a 10 degree turn about the goal z axis reads as 10 degrees
+        c, s = np.cos(np.radians(5)), np.sin(np.radians(5))
+        qz = np.array([c, 0, 0, s])
+        def qmul(a, b):
+            return np.array([a[0] * b[0] - a[1:] @ b[1:], *(a[0] * b[1:] + b[0] * a[1:] + np.cross(a[1:], b[1:]))])
+        g2 = np.concatenate([goal[:3], qmul(quat, qz)])
+        assert bn.end_pose_errors(RB, q, g2)[1] == pytest.approx(10.0, abs=1e-6)
