@@ -204,11 +204,14 @@ class TestMetrics:
         from oracle import bl_numpy as bn
         pb, grid, robot = synth.config3_wide(P, p0=seed)
         q = synth.refine_init(P * S, seed=seed + 1) * 0.35
-        # half the problems get their goal at the last waypoint's own end pose (success decided by
-        # clearance alone), the rest a random goal
+        # half the problems get their goal at the end pose of a collision-free seed (success then
+        # decided by the thresholds), the rest a random goal
         goal = pb.goal.astype(np.float64).copy()
         for p in range(0, P, 2):
-            F = bn.dh_frames(robot, q[p * S + 1, -1].astype(np.float64))[-1]
+            clr = [bn.traj_min_clearance(robot, pb.boxes[p], q[p * S + s].astype(np.float64), grid.cap)
+                   for s in range(S)]
+            s_free = int(np.argmax(clr))
+            F = bn.dh_frames(robot, q[p * S + s_free, -1].astype(np.float64))[-1]
             R = F[:3, :3]
             w = np.sqrt(max(1e-12, 1 + np.trace(R))) / 2
             goal[p] = np.concatenate([F[:3, 3] - robot.base, [w, (R[2, 1] - R[1, 2]) / (4 * w),
