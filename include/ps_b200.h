@@ -102,6 +102,16 @@ int ps_bl_metrics(const float* traj, int B, int T, int S, const float* boxes, in
                   float* terr, float* aerr_deg, float* motion_time, float* max_jerk, uint8_t* success,
                   uint8_t* collision_free, void* stream);
 
+/* guided_ddim_sample's guide() (diffusion.py:598-617) for the BL cost on normalised x0_hat
+ * (B,T,7), in place: n_grad descent steps from step alpha with <= max_halvings halvings until the
+ * cost of the denormalised candidate (lo_h + x * span_h, per joint) decreases; one warp per seed,
+ * one launch.  clamped (B,): some evaluation left the ESDF extent (planseed raises ValueError
+ * there; the host shim does in strict mode). */
+int ps_bl_guide(float* x0, int B, int T, int S, const float* esdf, long long esdf_stride, int layout, const int* n_h,
+                const float* origin_h, float h, const float* dh_h, const float* base_h, const float* sph_h,
+                const int* sph_link_h, int n_sph, const float* weights_h, const float* lo_h, const float* span_h,
+                int n_grad, float alpha, int max_halvings, uint8_t* clamped, void* stream);
+
 /* Best seed per problem: lowest-cost feasible seed, else lowest cost; ties to the
  * lower index.  pipeline.select_best (pipeline.py:160-165).  best: (P,) int32. */
 int ps_select(const float* cost, const uint8_t* feasible, int P, int S, int32_t* best,
@@ -165,6 +175,18 @@ int ps_sample(const void* packed, int mode, const float* film_a, int P, int S, i
 int ps_sample_hp(const void* packed, int mode, const void* packed_hp, int n_hp, const float* film_a, int P, int S,
                  int T, int p0, const int* steps_h, int n_steps, int ddpm, const float* coef_h, int K,
                  unsigned noise_key, const float* q_start, float lo, float hi, void* ws, float* traj, void* stream);
+
+/* Elementwise pieces of a host-orchestrated DDIM loop (cost-guided sampling), fp32:
+ *   ps_noise_init: x_K (B,T,7) from the sampler's Philox stream (step 0), as ps_sample draws it;
+ *   ps_ddim_x0:    x0 = clip((x - sq1m eps) rsq, clip_lo, clip_hi)      (_ddim_core, diffusion.py:548-550);
+ *   ps_ddim_next:  x = sqn x0 + sq1mn eps                                (diffusion.py:553-555);
+ *   ps_denorm_pin: traj = lo + x0 (hi - lo), row 0 := q_start[b / S]   (ddim_sample, diffusion.py:559-569). */
+int ps_noise_init(float* x, int B, int T, int S, int p0, unsigned key, void* stream);
+int ps_ddim_x0(const float* x, const float* eps, long long n, float sq1m, float rsq, float clip_lo, float clip_hi,
+               float* x0, void* stream);
+int ps_ddim_next(float* x, const float* x0, const float* eps, long long n, float sqn, float sq1mn, void* stream);
+int ps_denorm_pin(const float* x0, int B, int T, int S, const float* q_start, float lo, float hi, float* traj,
+                  void* stream);
 
 /* n standard normals of the sampler's noise stream (test hook). */
 int ps_noise_probe(float* out, int n, int step, int prob, int seed, unsigned key, void* stream);

@@ -115,6 +115,19 @@ def bl_refine(ps: BLProblemSet, q: np.ndarray, S: int, n_iters: int):
     return out, cost, feas.astype(bool), cl.astype(bool)
 
 
+def bl_guide(ps: BLProblemSet, x0: np.ndarray, S: int, lo, span, n_grad: int, alpha: float,
+             max_halvings: int):
+    """guided_ddim_sample's guide() on normalised x0 (B,T,7) -> (guided x0, clamped flags)."""
+    x = _f(x0).copy()
+    B, T, _ = x.shape
+    cl = np.empty(B, np.int32)
+    lib().orc_bl_guide(_p(x), B, T, S, _p(ps.esdf), ctypes.c_longlong(ps.esdf_stride), _p(ps.n), _p(ps.origin),
+                       ctypes.c_float(ps.grid.h), _p(ps.dh), _p(ps.base), _p(ps.sph), _p(ps.link),
+                       ctypes.c_int(len(ps.link)), _p(ps.w), _p(_f(lo)), _p(_f(span)), ctypes.c_int(n_grad),
+                       ctypes.c_float(alpha), ctypes.c_int(max_halvings), _p(cl))
+    return x, cl.astype(bool)
+
+
 def select(cost: np.ndarray, feasible: np.ndarray, S: int) -> np.ndarray:
     cost = _f(cost)
     feas = np.ascontiguousarray(feasible, dtype=np.int32)

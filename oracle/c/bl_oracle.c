@@ -361,6 +361,67 @@ void orc_bl_refine(const float *q_in, int B, int T, int S, const float *esdf, lo
     free(sm); free(gs); free(ct); free(x);
 }
 
+/* one trajectory's cost (and gradient, row 0 zero, when grad != NULL); as orc_bl_cost */
+static float traj_cost(const robot_t *rb, const grid_t *g, const cost_t *w, const float *q, int T, float *grad,
+                       int *clamped, float *sm, float *gs, float *ct) {
+    smooth_terms(q, T, w, sm, grad ? gs : NULL);
+    int cl_any = 0;
+    for (int t = 0; t < T; ++t) {
+        float wc, mc, gq[NJ];
+        int cl;
+        config_world(rb, g, w, q + t * NJ, grad ? 1 : 0, &wc, gq, &mc, &cl);
+        cl_any |= cl;
+        ct[t] = wc + sm[t];
+        if (grad)
+            for (int k = 0; k < NJ; ++k) grad[t * NJ + k] = (t == 0) ? 0.f : fmaf(2.0f, gs[t * NJ + k], gq[k]);
+    }
+    *clamped = cl_any;
+    return lane_sum(ct, T);
+}
+
+/* guided_ddim_sample's guide() (planseed/diffusion.py:598-617) for the BL cost on normalised
+ * x0_hat (B,T,7), in place: n_grad descent steps, each from step alpha with <= max_halvings
+ * halvings until the cost of the denormalised candidate (lo + x * span) decreases.
+ * clamped[b] = some evaluation of trajectory b left the ESDF extent. */
+void orc_bl_guide(float *x, int B, int T, int S, const float *esdf, long long esdf_stride, const int *n,
+                  const float *origin, float h, const float *dh, const float *base, const float *sph,
+                  const int *sph_link, int n_sph, const float *wts, const float *lo, const float *span,
+                  int n_grad, float alpha, int max_halvings, int *clamped) {
+    robot_t rb = {dh, base, sph, sph_link, n_sph};
+    cost_t w = {wts[0], wts[1], wts[2], wts[3], wts[4], wts[5]};
+    float *sm = (float *)malloc(sizeof(float) * T), *gs = (float *)malloc(sizeof(float) * T * NJ);
+    float *ct = (float *)malloc(sizeof(float) * T), *q = (float *)malloc(sizeof(float) * T * NJ);
+    float *gr = (float *)malloc(sizeof(float) * T * NJ), *cand = (float *)malloc(sizeof(float) * T * NJ);
+    for (int b = 0; b < B; ++b) {
+        grid_t g;
+        setup(&g, esdf + (size_t)(b / S) * (size_t)esdf_stride, n, origin, h);
+        float *xb = x + (size_t)b * T * NJ;
+        int cl_any = 0, cl;
+        for (int it = 0; it < n_grad; ++it) {
+            for (int i = 0; i < T * NJ; ++i) q[i] = lo[i % NJ] + xb[i] * span[i % NJ];
+            const float c = traj_cost(&rb, &g, &w, q, T, gr, &cl, sm, gs, ct);
+            cl_any |= cl;
+            for (int i = 0; i < T * NJ; ++i) gr[i] = gr[i] * span[i % NJ];
+            float step = alpha;
+            for (int hv = 0; hv < max_halvings; ++hv) {
+                for (int i = 0; i < T * NJ; ++i) {
+                    cand[i] = xb[i] - step * gr[i];
+                    q[i] = lo[i % NJ] + cand[i] * span[i % NJ];
+                }
+                const float cn = traj_cost(&rb, &g, &w, q, T, NULL, &cl, sm, gs, ct);
+                cl_any |= cl;
+                if (cn < c) {
+                    memcpy(xb, cand, sizeof(float) * T * NJ);
+                    break;
+                }
+                step = step * 0.5f;
+            }
+        }
+        clamped[b] = cl_any;
+    }
+    free(sm); free(gs); free(ct); free(q); free(gr); free(cand);
+}
+
 /* lowest-cost feasible seed, else lowest cost; ties to the lower index */
 void orc_select(const float *cost, const int *feasible, int P, int S, int *best) {
     for (int p = 0; p < P; ++p) {

@@ -241,7 +241,8 @@ def noise(step: int, problems: np.ndarray, seeds: np.ndarray, T: int, D: int = s
 # ----------------------------------------------------------------------------
 
 def sample(params, arch, cond, q_start, S, p0=0, T=spec.T_DEFAULT, betas=None, steps=None,
-           dtype=np.float64, x_init=None, return_eps=False, problems=None, table_dtype=np.float32):
+           dtype=np.float64, x_init=None, return_eps=False, problems=None, table_dtype=np.float32,
+           guide_fn=None):
     """Seed generation for P problems x S seeds.
 
     steps=None: full K-step stochastic DDPM (posterior mean + sigma z).
@@ -251,6 +252,8 @@ def sample(params, arch, cond, q_start, S, p0=0, T=spec.T_DEFAULT, betas=None, s
     subset of a large batch can be checked (problems are independent: per-sample GroupNorm,
     per-problem FiLM, noise keyed by the global index).
     table_dtype: float32 = the device's coefficient tables; float64 = exact (planseed bridge).
+    guide_fn(i, k, x0_hat) -> x0_hat: guided_ddim_sample's hook (diffusion.py:540-552), DDIM only,
+    never on the last step.
     Returns physical trajectories (P*S, T, 7) with row 0 := q_start."""
     betas = spec.cosine_betas() if betas is None else betas
     K = betas.shape[0]
@@ -273,6 +276,8 @@ def sample(params, arch, cond, q_start, S, p0=0, T=spec.T_DEFAULT, betas=None, s
                 z = noise(k, prob, sidx, T).astype(dtype)
                 x = tab.c0[k] * x0 + tab.c1[k] * x + tab.sig[k] * z
         elif i + 1 < len(ks):
+            if guide_fn is not None:
+                x0 = guide_fn(i, k, x0)
             kn = ks[i + 1]
             x = tab.sq[kn] * x0 + tab.sq1m[kn] * eps
     traj = lo + x0 * (hi - lo)

@@ -41,6 +41,12 @@ _SIGS = {
                        _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp],
     "ps_bl_metrics": [_vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp, _c_int, _vp, _c_f, _c_f,
                       _c_f, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "ps_bl_guide": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _c_int, _vp, _vp, _c_f, _vp, _vp, _vp, _vp, _c_int,
+                    _vp, _vp, _vp, _c_int, _c_f, _c_int, _vp, _vp],
+    "ps_noise_init": [_vp, _c_int, _c_int, _c_int, _c_int, ctypes.c_uint, _vp],
+    "ps_ddim_x0": [_vp, _vp, _c_ll, _c_f, _c_f, _c_f, _c_f, _vp, _vp],
+    "ps_ddim_next": [_vp, _vp, _vp, _c_ll, _c_f, _c_f, _vp],
+    "ps_denorm_pin": [_vp, _c_int, _c_int, _c_int, _vp, _c_f, _c_f, _vp, _vp],
     "ps_select": [_vp, _vp, _c_int, _c_int, _vp, _vp],
     "ps_unet_param_count": [],
     "ps_unet_param_offset": [ctypes.c_char_p],

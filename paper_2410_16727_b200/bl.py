@@ -203,6 +203,31 @@ def refine(q, esdf, S: int, robot: DHRobot, grid: GridSpec = GridSpec(), w: BLCo
     return qo, c, f, cl
 
 
+def guide(x0, esdf, S: int, robot: DHRobot, grid: GridSpec = GridSpec(), w: BLCost = BLCost(),
+          lo=None, span=None, n_grad: int = 20, alpha: float = 1.0, max_halvings: int = 8, stream=None,
+          esdf_layout: int = ESDF_C_ORDER):
+    """guided_ddim_sample's guide() (planseed/diffusion.py:598-617) for the BL cost, in place on the
+    normalised x0_hat (B,T,7) device tensor; returns the per-seed clamped flags (B,) (some
+    evaluation left the ESDF extent)."""
+    torch = _lib.require_cuda()
+    B, T, D = x0.shape
+    if D != 7 or T not in (32, 64) or not x0.is_cuda or x0.dtype != torch.float32 or not x0.is_contiguous():
+        raise ValueError("x0 must be a contiguous float32 CUDA tensor (B, 32|64, 7)")
+    e = _dev(esdf)
+    rt = RobotTables.of(robot)
+    n, o = _grid_args(grid)
+    lo = np.ascontiguousarray(robot.lo if lo is None else lo, dtype=np.float32)
+    span = np.ascontiguousarray((robot.hi - robot.lo) if span is None else span, dtype=np.float32)
+    cl = torch.empty(B, dtype=torch.uint8, device="cuda")
+    st = _lib.lib().ps_bl_guide(_lib.ptr(x0), B, T, S, _lib.ptr(e), _esdf_stride(e, grid, -(-B // S)),
+                                int(esdf_layout), _lib.hptr(n), _lib.hptr(o), grid.h, _lib.hptr(rt.dh),
+                                _lib.hptr(rt.base), _lib.hptr(rt.sph), _lib.hptr(rt.link), len(rt.link),
+                                _lib.hptr(w.as_f32()), _lib.hptr(lo), _lib.hptr(span), int(n_grad), float(alpha),
+                                int(max_halvings), _lib.ptr(cl), _lib.stream_handle(stream))
+    _lib.check(st, "bl_guide")
+    return cl.bool()
+
+
 @dataclass
 class BLMetrics:
     """trajopt.TrajectoryMetrics for a batch (device tensors, one entry per trajectory)."""

@@ -342,6 +342,107 @@ __global__ void __launch_bounds__(LB) bl_refine_kernel(const __grid_constant__ B
 }
 
 // ---------------------------------------------------------------------------
+// Cost-guided sampling's guide step (guided_ddim_sample, planseed/diffusion.py:572-628) for the BL
+// cost: per trajectory (one warp), n_grad descent steps on the normalised x0_hat, each from step
+// alpha with <= max_halvings halvings until the cost of the denormalised candidate decreases.
+// Seeds are independent (their costs never mix), so the whole guide step is one launch.  The
+// evaluation order is orc_bl_guide's (oracle/c/bl_oracle.c): bit-identical results.
+// ---------------------------------------------------------------------------
+struct BLGuideArgs {
+    float* x;                 // (B, T, 7) normalised x0_hat, in place
+    float lo[NJ], span[NJ];   // denormalise: q = lo + x * span
+    int n_grad, max_halvings;
+    float alpha;
+    uint8_t* clamped;         // (B,) some evaluation left the ESDF extent
+};
+
+template <int WPL, bool GRAD>
+__device__ __forceinline__ float traj_cost_dev(const BLParams& P, const Grid& g, const float (&q)[WPL][NJ], int lane,
+                                               float (&grad)[WPL][NJ], bool& cl_any) {
+    float sm[WPL], gs[WPL][NJ], ct[WPL];
+    smooth_terms<WPL, GRAD>(P, q, lane, sm, gs);
+    bool cl_lane = false;
+#pragma unroll
+    for (int w = 0; w < WPL; ++w) {
+        float wc, mc, gq[NJ];
+        bool cl;
+        config_world<GRAD, 1>(P, g, q[w], wc, gq, mc, cl);
+        cl_lane |= cl;
+        ct[w] = wc + sm[w];
+        if (GRAD) {
+            const int t = lane * WPL + w;
+#pragma unroll
+            for (int k = 0; k < NJ; ++k) grad[w][k] = (t == 0) ? 0.f : fmaf(2.0f, gs[w][k], gq[k]);
+        }
+    }
+    float c = ct[0];
+#pragma unroll
+    for (int w = 1; w < WPL; ++w) c = c + ct[w];
+    cl_any = __any_sync(PS_FULL, cl_lane);
+    return warp_sum_butterfly(c);
+}
+
+template <int WPL>
+__global__ void __launch_bounds__(256) bl_guide_kernel(const __grid_constant__ BLParams P,
+                                                        const __grid_constant__ BLGuideArgs A) {
+    const int lane = threadIdx.x & 31;
+    const int b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (b >= P.B) return;   // whole warp
+    Grid g;
+    g.v = P.esdf + (size_t)(b / P.S) * (size_t)P.esdf_stride;
+    g.nx = P.nx; g.ny = P.ny; g.nz = P.nz;
+    g.ox = P.ox; g.oy = P.oy; g.oz = P.oz; g.inv_h = P.inv_h;
+    g.brick = P.esdf_brick;
+    float x[WPL][NJ], q[WPL][NJ], gr[WPL][NJ];
+    float* xb = A.x + (size_t)b * P.T * NJ;
+#pragma unroll
+    for (int w = 0; w < WPL; ++w)
+#pragma unroll
+        for (int k = 0; k < NJ; ++k) x[w][k] = xb[(lane * WPL + w) * NJ + k];
+    bool cl_any = false;
+    for (int it = 0; it < A.n_grad; ++it) {
+#pragma unroll
+        for (int w = 0; w < WPL; ++w)
+#pragma unroll
+            for (int k = 0; k < NJ; ++k) q[w][k] = A.lo[k] + x[w][k] * A.span[k];
+        bool cl;
+        const float c = traj_cost_dev<WPL, true>(P, g, q, lane, gr, cl);
+        cl_any |= cl;
+#pragma unroll
+        for (int w = 0; w < WPL; ++w)
+#pragma unroll
+            for (int k = 0; k < NJ; ++k) gr[w][k] = gr[w][k] * A.span[k];
+        float step = A.alpha;
+        for (int hv = 0; hv < A.max_halvings; ++hv) {
+            float cand[WPL][NJ];
+#pragma unroll
+            for (int w = 0; w < WPL; ++w)
+#pragma unroll
+                for (int k = 0; k < NJ; ++k) {
+                    cand[w][k] = x[w][k] - step * gr[w][k];
+                    q[w][k] = A.lo[k] + cand[w][k] * A.span[k];
+                }
+            float dummy[WPL][NJ];
+            const float cn = traj_cost_dev<WPL, false>(P, g, q, lane, dummy, cl);
+            cl_any |= cl;
+            if (cn < c) {   // warp-uniform: both costs are warp-reduced
+#pragma unroll
+                for (int w = 0; w < WPL; ++w)
+#pragma unroll
+                    for (int k = 0; k < NJ; ++k) x[w][k] = cand[w][k];
+                break;
+            }
+            step = step * 0.5f;
+        }
+    }
+#pragma unroll
+    for (int w = 0; w < WPL; ++w)
+#pragma unroll
+        for (int k = 0; k < NJ; ++k) xb[(lane * WPL + w) * NJ + k] = x[w][k];
+    if (lane == 0) A.clamped[b] = cl_any ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
 // Ground-truth evaluation (trajopt.metrics / retime / traj_min_clearance, planseed/trajopt.py:
 // 209-272, _kernels.py:144-162) against the problem's analytic boxes: one warp per trajectory,
 // lane = waypoint(s).  Clearance = min over waypoints + interp interpolants per segment of
@@ -985,6 +1086,39 @@ extern "C" int ps_bl_metrics(const float* traj, int B, int T, int S, const float
         bl_metrics_kernel<1><<<blocks, 256, 0, (cudaStream_t)stream>>>(P, M);
     else
         bl_metrics_kernel<2><<<blocks, 256, 0, (cudaStream_t)stream>>>(P, M);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+extern "C" int ps_bl_guide(float* x0, int B, int T, int S, const float* esdf, long long esdf_stride, int layout,
+                           const int* n_h, const float* origin_h, float h, const float* dh_h, const float* base_h,
+                           const float* sph_h, const int* sph_link_h, int n_sph, const float* weights_h,
+                           const float* lo_h, const float* span_h, int n_grad, float alpha, int max_halvings,
+                           uint8_t* clamped, void* stream) {
+    BLParams P{};
+    int st = fill_params(P, B, T, S, esdf, esdf_stride, n_h, origin_h, h, dh_h, base_h, sph_h, sph_link_h, n_sph,
+                         weights_h);
+    if (st) return st;
+    if (layout < 0 || layout > 1 || (layout == 1 && ((n_h[0] & 3) || (n_h[1] & 3) || (n_h[2] & 3))) || n_grad < 0 ||
+        max_halvings < 0)
+        return PS_FAIL(PS_ERR_SHAPE);
+    P.esdf_brick = layout;
+    if (B == 0 || n_grad == 0) return PS_OK;
+    BLGuideArgs A{};
+    A.x = x0;
+    for (int k = 0; k < NJ; ++k) {
+        A.lo[k] = lo_h[k];
+        A.span[k] = span_h[k];
+    }
+    A.n_grad = n_grad;
+    A.max_halvings = max_halvings;
+    A.alpha = alpha;
+    A.clamped = clamped;
+    const unsigned blocks = (unsigned)(((long long)B * 32 + 255) / 256);
+    if (T == 32)
+        bl_guide_kernel<1><<<blocks, 256, 0, (cudaStream_t)stream>>>(P, A);
+    else
+        bl_guide_kernel<2><<<blocks, 256, 0, (cudaStream_t)stream>>>(P, A);
     PS_CHECK_LAUNCH();
     return PS_OK;
 }

@@ -819,6 +819,68 @@ extern "C" int ps_unet_forward(const void* packed, int mode, const float* x, int
                         st);
 }
 
+// ---- elementwise DDIM pieces for host-orchestrated loops (cost-guided sampling)
+__global__ void ddim_x0_kernel(const float* __restrict__ x, const float* __restrict__ eps, size_t n, float sq1m,
+                               float rsq, float clo, float chi, float* __restrict__ x0) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) x0[i] = fminf(fmaxf((x[i] - sq1m * eps[i]) * rsq, clo), chi);
+}
+__global__ void ddim_next_kernel(float* __restrict__ x, const float* __restrict__ x0, const float* __restrict__ eps,
+                                 size_t n, float sqn, float sq1mn) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) x[i] = sqn * x0[i] + sq1mn * eps[i];
+}
+__global__ void denorm_pin_kernel(const float* __restrict__ x0, int B, int T, int S, const float* __restrict__ q_start,
+                                  float lo, float hi, float* __restrict__ traj) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t n = (size_t)B * T * U_DOF;
+    if (i >= n) return;
+    const int d = (int)(i % U_DOF);
+    const int t = (int)((i / U_DOF) % T);
+    const int b = (int)(i / ((size_t)T * U_DOF));
+    traj[i] = (t == 0) ? q_start[(size_t)(b / S) * U_DOF + d] : lo + x0[i] * (hi - lo);
+}
+
+extern "C" int ps_noise_init(float* x, int B, int T, int S, int p0, unsigned key, void* stream) {
+    if (B < 0 || T <= 0 || S <= 0) return PS_FAIL(PS_ERR_SHAPE);
+    const size_t n = (size_t)B * T * U_DOF;
+    if (n == 0) return PS_OK;
+    noise_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(x, B, T, S, p0, key);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+extern "C" int ps_ddim_x0(const float* x, const float* eps, long long n, float sq1m, float rsq, float clip_lo,
+                          float clip_hi, float* x0, void* stream) {
+    if (n < 0) return PS_FAIL(PS_ERR_SHAPE);
+    if (n == 0) return PS_OK;
+    ddim_x0_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(x, eps, (size_t)n, sq1m, rsq,
+                                                                                  clip_lo, clip_hi, x0);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+extern "C" int ps_ddim_next(float* x, const float* x0, const float* eps, long long n, float sqn, float sq1mn,
+                            void* stream) {
+    if (n < 0) return PS_FAIL(PS_ERR_SHAPE);
+    if (n == 0) return PS_OK;
+    ddim_next_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(x, x0, eps, (size_t)n, sqn,
+                                                                                    sq1mn);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
+extern "C" int ps_denorm_pin(const float* x0, int B, int T, int S, const float* q_start, float lo, float hi,
+                             float* traj, void* stream) {
+    if (B < 0 || T <= 0 || S <= 0) return PS_FAIL(PS_ERR_SHAPE);
+    const size_t n = (size_t)B * T * U_DOF;
+    if (n == 0) return PS_OK;
+    denorm_pin_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(x0, B, T, S, q_start, lo, hi,
+                                                                                     traj);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
 extern "C" int ps_noise_probe(float* out, int n, int step, int prob, int seed, unsigned key, void* stream) {
     noise_probe_kernel<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(out, n, (uint32_t)step, (uint32_t)prob,
                                                                            (uint32_t)seed, key);

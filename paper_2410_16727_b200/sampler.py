@@ -200,6 +200,56 @@ class SeedSampler:
         return traj
 
 
+    def guided_sample(self, film_a, q_start, S: int, esdf, robot: spec.DHRobot, grid: spec.GridSpec = spec.GridSpec(),
+                      cost: spec.BLCost = spec.BLCost(), T: int = spec.T_DEFAULT, p0: int = 0, n_steps: int = 5,
+                      k_guide_frac: float = 0.6, n_grad: int = 20, alpha_guide: float = 1.0, max_halvings: int = 8,
+                      esdf_layout: int = 0, strict: bool = False, stream=None):
+        """guided_ddim_sample (planseed/diffusion.py:572-628) for P problems x S seeds: strided DDIM over
+        round(linspace(K, 1, n_steps)) with, on every sub-step whose index k < k_guide_frac * K except the
+        last, the BL-cost guide step (bl.guide: n_grad descent steps, <= max_halvings halvings each) on
+        x0_hat against each problem's ESDF.  Returns (trajectories (P*S, T, 7), log [(k, guided)]).
+        strict=True raises planseed's ValueError when an evaluation leaves the ESDF extent."""
+        torch = _lib.require_cuda()
+        from . import bl
+        from .bl import _dev
+        q = _dev(q_start)
+        P = q.shape[0]
+        B = P * S
+        L = _lib.lib()
+        ks = spec.strided_steps(self.K, n_steps)
+        tab = spec.sampler_tables(self.betas)
+        x = torch.empty((B, T, 7), dtype=torch.float32, device="cuda")
+        x0 = torch.empty_like(x)
+        n = x.numel()
+        sh = _lib.stream_handle(stream)
+        _lib.check(L.ps_noise_init(_lib.ptr(x), B, T, S, int(p0), self.noise_key, sh), "noise_init")
+        k_guide = k_guide_frac * self.K
+        lo, hi = -spec.JOINT_LIMIT, spec.JOINT_LIMIT
+        log = []
+        for i, k in enumerate(ks):
+            k = int(k)
+            eps = self.predict_noise(x, k, film_a, S, stream=stream)
+            _lib.check(L.ps_ddim_x0(_lib.ptr(x), _lib.ptr(eps), n, float(tab.sq1m[k]), float(tab.rsq[k]),
+                                    spec.X0_CLIP[0], spec.X0_CLIP[1], _lib.ptr(x0), sh), "ddim_x0")
+            if i + 1 == len(ks):
+                log.append((k, False))
+                break
+            guided = bool(k < k_guide and alpha_guide != 0.0)
+            log.append((k, guided))
+            if guided:
+                cl = bl.guide(x0, esdf, S, robot, grid, cost, lo=np.full(7, lo), span=np.full(7, hi - lo),
+                              n_grad=n_grad, alpha=alpha_guide, max_halvings=max_halvings, stream=stream,
+                              esdf_layout=esdf_layout)
+                if strict and bool(cl.any()):
+                    bl._raise_out_of_grid(cl)
+            kn = int(ks[i + 1])
+            _lib.check(L.ps_ddim_next(_lib.ptr(x), _lib.ptr(x0), _lib.ptr(eps), n, float(tab.sq[kn]),
+                                      float(tab.sq1m[kn]), sh), "ddim_next")
+        traj = torch.empty_like(x)
+        _lib.check(L.ps_denorm_pin(_lib.ptr(x0), B, T, S, _lib.ptr(q), lo, hi, _lib.ptr(traj), sh), "denorm_pin")
+        return traj, log
+
+
 def noise_probe(n: int, step: int, prob: int, seed: int, key: int = spec.NOISE_SEED):
     torch = _lib.require_cuda()
     out = torch.empty(n, dtype=torch.float32, device="cuda")

@@ -309,3 +309,44 @@ class TestMetricsOracle:
             return np.array([a[0] * b[0] - a[1:] @ b[1:], *(a[0] * b[1:] + b[0] * a[1:] + np.cross(a[1:], b[1:]))])
         g2 = np.concatenate([goal[:3], qmul(quat, qz)])
         assert bn.end_pose_errors(RB, q, g2)[1] == pytest.approx(10.0, abs=1e-6)
+
+
+class TestGuideOracle:
+    def test_c_guide_is_planseeds_guide_loop(self, oracle_lib):
+        """orc_bl_guide == planseed's guide() (diffusion.py:598-617) written over the BL cost in
+        float32 numpy (cost_fn = the canonical C cost), bit for bit."""
+        grid = small_grid()
+        boxes = np.stack([synth.sample_boxes(np.random.default_rng(4), 8, grid)]).astype(np.float32)
+        esdf = oracle_lib.esdf_build(boxes[0], grid)
+        ps = oracle_lib.BLProblemSet(RB, grid, COST, esdf[None], grid.n_nodes)
+        import dataclasses
+        robot = dataclasses.replace(RB, base=np.full(3, grid.cube / 2))
+        ps = oracle_lib.BLProblemSet(robot, grid, COST, esdf[None], grid.n_nodes)
+        rng = np.random.default_rng(6)
+        x0 = rng.uniform(0.3, 0.7, (6, 32, 7)).astype(np.float32)
+        lo = np.full(7, -spec.JOINT_LIMIT, np.float32)
+        span = np.full(7, 2 * spec.JOINT_LIMIT, np.float32)
+        n_grad, alpha, max_halvings = 5, np.float32(1.0), 8
+
+        def cost_fn(trajs):
+            c, g, _ = oracle_lib.bl_cost(ps, trajs, len(trajs))
+            return c, g
+
+        x = x0.copy()
+        for _ in range(n_grad):                      # planseed's loop, float32 throughout
+            costs, grads = cost_fn(lo + x * span)
+            g_norm = grads * span
+            step = np.full(x.shape[0], alpha, np.float32)
+            remaining = np.ones(x.shape[0], dtype=bool)
+            for _ in range(max_halvings):
+                if not remaining.any():
+                    break
+                cand = x - step[:, None, None] * g_norm
+                new_costs, _ = cost_fn(lo + cand * span)
+                improved = remaining & (new_costs < costs)
+                x = np.where(improved[:, None, None], cand, x)
+                remaining = remaining & ~improved
+                step = np.where(remaining, step * np.float32(0.5), step)
+        got, cl = oracle_lib.bl_guide(ps, x0, 6, lo, span, n_grad, float(alpha), max_halvings)
+        assert np.array_equal(got, x)
+        assert not np.array_equal(got, x0)           # guidance moved the seeds
