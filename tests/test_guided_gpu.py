@@ -66,7 +66,7 @@ def test_guided_sampler_log_alpha0_and_oracle(torch_cuda, oracle_lib):
     t0, log0 = smp.guided_sample(fa, pb.q_start, S, esdf, robot, grid, n_steps=5, alpha_guide=0.0)
     plain = smp.sample(fa, pb.q_start, S, steps=spec.strided_steps(100, 5)).cpu().numpy()
     assert not any(g for _, g in log0)
-    assert np.abs(t0.cpu().numpy() - plain).max() < 1e-5
+    assert np.abs(t0.cpu().numpy() - plain).max() < 1e-4      # same math, separately rounded kernels
     # float64 oracle sampler with the C guide on its own x0_hat
     e = esdf.cpu().numpy()
     ps = oracle_lib.BLProblemSet(robot, grid, spec.BLCost(), e, grid.n_nodes)
