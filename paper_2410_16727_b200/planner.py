@@ -26,6 +26,15 @@ from . import _lib, bl, spec
 from .sampler import SeedSampler
 
 
+@dataclass(frozen=True)
+class GuidanceParams:
+    """planseed pipeline.GuidanceParams (pipeline.py:58-61): cost-guided DDIM seeding."""
+
+    k_guide_frac: float = 0.6
+    n_grad: int = 20
+    alpha_guide: float = 1.0
+
+
 @dataclass
 class PlanBatchResult:
     trajectories: object    # (P*S, T, 7) refined, physical radians
@@ -43,7 +52,7 @@ class BLPlanner:
                  grid: spec.GridSpec = spec.GridSpec(), cost: spec.BLCost = spec.BLCost(),
                  steps=None, max_problems: int = 1024, n_images: int = 2,
                  image_shape=(240, 320), n_boxes: int = spec.N_BOXES, hp_rsq: float | None = None, betas=None,
-                 strict: bool = False):
+                 strict: bool = False, guidance: GuidanceParams | None = None):
         torch = _lib.require_cuda()
         self.sampler = SeedSampler(params, enc, arch, mode=mode, hp_rsq=hp_rsq, betas=betas)
         self.S, self.T = int(S), int(T)
@@ -56,6 +65,12 @@ class BLPlanner:
         # so the planner reports them per seed in `clamped` instead of raising (their lookups clamp to the
         # grid boundary, as planseed's sample_esdf_many does, geometry.py:223-240).
         self.strict = bool(strict)
+        # guidance (plan_diffusion's guided branch, pipeline.py:189-197): strided DDIM over `steps`
+        # with the BL-cost guide step against each problem's ESDF (SeedSampler.guided_sample)
+        self.guidance = guidance
+        if guidance is not None and guidance.alpha_guide != 0.0:
+            if steps is None or list(steps) != list(spec.strided_steps(100, len(steps))):
+                raise ValueError("guidance needs a strided DDIM schedule: steps = spec.strided_steps(K, n)")
         self.Pmax = int(max_problems)
         B = self.Pmax * self.S
         dev = "cuda"
@@ -107,8 +122,17 @@ class BLPlanner:
         fa = self.sampler.film(cond, out=self.film_a[:P])
         if events is not None:
             events["sample_start"].record()
-        seeds = self.sampler.sample(fa, q_start, self.S, self.T, p0=p0, steps=self.steps,
-                                    out=self.seeds[:B])
+        if self.guidance is not None and self.guidance.alpha_guide != 0.0:
+            g = self.guidance
+            seeds, _ = self.sampler.guided_sample(fa, q_start, self.S, esdf, self.robot, self.grid, self.cost, T=self.T,
+                                                  p0=p0, n_steps=len(self.steps), k_guide_frac=g.k_guide_frac,
+                                                  n_grad=g.n_grad, alpha_guide=g.alpha_guide,
+                                                  esdf_layout=self.esdf_layout, strict=self.strict)
+            self.seeds[:B].copy_(seeds)
+            seeds = self.seeds[:B]
+        else:
+            seeds = self.sampler.sample(fa, q_start, self.S, self.T, p0=p0, steps=self.steps,
+                                        out=self.seeds[:B])
         if events is not None:
             events["sample_end"].record()
         out = tuple(o[:B] for o in self.out)

@@ -87,3 +87,20 @@ def test_guided_sampler_log_alpha0_and_oracle(torch_cuda, oracle_lib):
     c_g, _, _ = bl.cost(traj, esdf, S, robot, grid)
     c_0, _, _ = bl.cost(t0, esdf, S, robot, grid)
     assert c_g.sum().item() < c_0.sum().item()
+
+
+def test_planner_with_guidance(torch_cuda):
+    from paper_2410_16727_b200.planner import BLPlanner, GuidanceParams
+    params = spec.random_model(spec.ENCODER_CFG3)
+    P, S = 2, 8
+    pb, grid, robot = _scene(P)
+    steps = spec.strided_steps(100, 5)
+    kw = dict(mode=0, S=S, max_problems=P, grid=grid, robot=robot, steps=steps)
+    pg = BLPlanner(params, spec.ENCODER_CFG3, guidance=GuidanceParams(n_grad=4), **kw)
+    p0 = BLPlanner(params, spec.ENCODER_CFG3, **kw)
+    rg = pg.plan_batch(pb.images, pb.q_start, pb.goal, pb.boxes)
+    r0 = p0.plan_batch(pb.images, pb.q_start, pb.goal, pb.boxes)
+    assert np.isfinite(np.asarray(rg.trajectories)).all()
+    assert not np.array_equal(np.asarray(rg.trajectories), np.asarray(r0.trajectories))
+    with pytest.raises(ValueError, match="strided DDIM"):
+        BLPlanner(params, spec.ENCODER_CFG3, guidance=GuidanceParams(), mode=0, S=S, max_problems=P)
