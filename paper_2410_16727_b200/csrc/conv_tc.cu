@@ -981,16 +981,6 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         // the warp's [32 rows x 16 ch] box; lane 0 first waits until the store from the other
         // buffer has been read out, so the next slab can be written right after __syncwarp
         auto stage_store = [&](const __nv_bfloat162* pk, int c0, int mb) {
-            if (a.dbg & 64) {   // A/B: this row's 16 channels straight to global (two full 16-B halves
-                                // of one 32-B sector), no staging / fence / bulk wait
-                const int bb = cur_tile * nb + sl;
-                if (bb < a.B) {
-                    uint4* g = reinterpret_cast<uint4*>(a.out + ((size_t)bb * Tv + t0 + mb * tstep) * NF + c0 + cur_noff);
-                    g[0] = reinterpret_cast<const uint4*>(pk)[0];
-                    g[1] = reinterpret_cast<const uint4*>(pk)[1];
-                }
-                return;
-            }
             uint8_t* so = sOut + (size_t)(ew * 2 + (ob & 1u)) * 1024;
             *reinterpret_cast<uint4*>(so + lane * 32) = reinterpret_cast<const uint4*>(pk)[0];
             *reinterpret_cast<uint4*>(so + lane * 32 + 16) = reinterpret_cast<const uint4*>(pk)[1];
