@@ -188,6 +188,12 @@ int ps_ddim_next(float* x, const float* x0, const float* eps, long long n, float
 int ps_denorm_pin(const float* x0, int B, int T, int S, const float* q_start, float lo, float hi, float* traj,
                   void* stream);
 
+/* Observation synthesis for the BASELINE scenes (the render_depth_scan step of planseed's data
+ * path, geometry.py:279-329, in BASELINE.json's image form): n_img depth images (H, W) from
+ * params (n_img, 1 + 5 n_rect) = [background, (y0, y1, x0, x1, depth) x n_rect]; each pixel keeps
+ * the nearest depth of the rectangles covering it (synth.depth_image_params draws them). */
+int ps_render_depth_rects(const float* params, int n_img, int n_rect, int H, int W, float* out, void* stream);
+
 /* n standard normals of the sampler's noise stream (test hook). */
 int ps_noise_probe(float* out, int n, int step, int prob, int seed, unsigned key, void* stream);
 

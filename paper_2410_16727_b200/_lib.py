@@ -43,6 +43,7 @@ _SIGS = {
                       _c_f, _c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "ps_bl_guide": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _c_int, _vp, _vp, _c_f, _vp, _vp, _vp, _vp, _c_int,
                     _vp, _vp, _vp, _c_int, _c_f, _c_int, _vp, _vp],
+    "ps_render_depth_rects": [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp],
     "ps_noise_init": [_vp, _c_int, _c_int, _c_int, _c_int, ctypes.c_uint, _vp],
     "ps_ddim_x0": [_vp, _vp, _c_ll, _c_f, _c_f, _c_f, _c_f, _vp, _vp],
     "ps_ddim_next": [_vp, _vp, _vp, _c_ll, _c_f, _c_f, _vp],

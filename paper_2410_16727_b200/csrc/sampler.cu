@@ -841,6 +841,34 @@ __global__ void denorm_pin_kernel(const float* __restrict__ x0, int B, int T, in
     traj[i] = (t == 0) ? q_start[(size_t)(b / S) * U_DOF + d] : lo + x0[i] * (hi - lo);
 }
 
+// synthetic depth images: background + axis-aligned rectangles, each pixel keeps the nearest depth
+__global__ void render_rects_kernel(const float* __restrict__ prm, int n_img, int n_rect, int H, int W,
+                                    float* __restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t npx = (size_t)H * W;
+    if (i >= npx * n_img) return;
+    const int img = (int)(i / npx);
+    const int y = (int)((i % npx) / W), x = (int)(i % W);
+    const float* p = prm + (size_t)img * (1 + 5 * n_rect);
+    float v = p[0];
+    for (int r = 0; r < n_rect; ++r) {
+        const float* q = p + 1 + 5 * r;
+        if (y >= (int)q[0] && y < (int)q[1] && x >= (int)q[2] && x < (int)q[3]) v = fminf(v, q[4]);
+    }
+    out[i] = v;
+}
+
+extern "C" int ps_render_depth_rects(const float* params, int n_img, int n_rect, int H, int W, float* out,
+                                     void* stream) {
+    if (n_img < 0 || n_rect < 0 || H <= 0 || W <= 0) return PS_FAIL(PS_ERR_SHAPE);
+    const size_t n = (size_t)n_img * H * W;
+    if (n == 0) return PS_OK;
+    render_rects_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(params, n_img, n_rect, H, W,
+                                                                                       out);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
+
 extern "C" int ps_noise_init(float* x, int B, int T, int S, int p0, unsigned key, void* stream) {
     if (B < 0 || T <= 0 || S <= 0) return PS_FAIL(PS_ERR_SHAPE);
     const size_t n = (size_t)B * T * U_DOF;

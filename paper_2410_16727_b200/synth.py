@@ -60,17 +60,59 @@ def sample_boxes(rng, n_boxes: int = N_BOXES, grid: GridSpec = GridSpec()) -> np
     return np.concatenate([lo, lo + side], axis=1)
 
 
+def depth_image_params(rng, h: int, w: int, n_rect: int) -> np.ndarray:
+    """The draws of one synthetic depth image: [background, (y0, y1, x0, x1, depth) x n_rect]
+    (float64; the corners are integers).  Background b ~ U(0.3, 2.0) m; n_rect axis-aligned
+    pixel rectangles with random corners at depths ~ U(0.3, 2.0)."""
+    out = np.empty(1 + 5 * n_rect)
+    out[0] = rng.uniform(0.3, 2.0)
+    for r in range(n_rect):
+        ys = np.sort(rng.integers(0, h + 1, size=2))
+        xs = np.sort(rng.integers(0, w + 1, size=2))
+        out[1 + 5 * r:6 + 5 * r] = (ys[0], ys[1], xs[0], xs[1], rng.uniform(0.3, 2.0))
+    return out
+
+
+def render_depth_params(prm: np.ndarray, h: int, w: int) -> np.ndarray:
+    """Host rasteriser of depth_image_params: each pixel keeps the nearest depth."""
+    img = np.full((h, w), prm[0])
+    for r in range((len(prm) - 1) // 5):
+        y0, y1, x0, x1, depth = prm[1 + 5 * r:6 + 5 * r]
+        sub = img[int(y0):int(y1), int(x0):int(x1)]
+        np.minimum(sub, depth, out=sub)
+    return img
+
+
 def synth_depth_image(rng, h: int, w: int, n_rect: int) -> np.ndarray:
     """Uniform background b ~ U(0.3, 2.0) m; n_rect axis-aligned pixel rectangles
     with random corners at depths ~ U(0.3, 2.0); each pixel keeps the nearest depth."""
-    img = np.full((h, w), rng.uniform(0.3, 2.0))
-    for _ in range(n_rect):
-        ys = np.sort(rng.integers(0, h + 1, size=2))
-        xs = np.sort(rng.integers(0, w + 1, size=2))
-        depth = rng.uniform(0.3, 2.0)
-        sub = img[ys[0]:ys[1], xs[0]:xs[1]]
-        np.minimum(sub, depth, out=sub)
-    return img
+    return render_depth_params(depth_image_params(rng, h, w, n_rect), h, w)
+
+
+def image_params(P: int, p0: int = 0, seed: int = 0, image_shape=(240, 320), n_images: int = 2,
+                 n_rect: int = 8) -> np.ndarray:
+    """(P, n_images, 1 + 5 n_rect) draws of make_problems' images (same per-problem streams)."""
+    out = np.empty((P, n_images, 1 + 5 * n_rect))
+    for i in range(P):
+        ri = _rng(seed, p0 + i, STREAM_IMAGE)
+        for m in range(n_images):
+            out[i, m] = depth_image_params(ri, image_shape[0], image_shape[1], n_rect)
+    return out
+
+
+def render_images_device(params: np.ndarray, image_shape, stream=None):
+    """Rasterise image_params on the GPU (ps_render_depth_rects) -> (P, n_images, H, W) float32
+    CUDA tensor, bit-identical to the host rasteriser (min of float32-rounded depths)."""
+    from . import _lib
+    torch = _lib.require_cuda()
+    prm = np.ascontiguousarray(params, dtype=np.float32)
+    P, n_img, n_par = prm.shape
+    H, W = image_shape
+    d_prm = torch.as_tensor(prm, device="cuda")
+    out = torch.empty((P, n_img, H, W), dtype=torch.float32, device="cuda")
+    _lib.check(_lib.lib().ps_render_depth_rects(_lib.ptr(d_prm), P * n_img, (n_par - 1) // 5, H, W, _lib.ptr(out),
+                                                _lib.stream_handle(stream)), "render_depth_rects")
+    return out
 
 
 def make_problems(P: int, p0: int = 0, seed: int = 0, n_boxes: int = N_BOXES,

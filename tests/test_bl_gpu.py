@@ -282,3 +282,15 @@ class TestBrickedEsdf:
         for u, v in zip(r0, r1):
             assert np.array_equal(u, v)
         assert np.unique(r0[1]).size > P * S // 2   # non-trivial costs
+
+
+def test_depth_images_rendered_on_device_bitwise(torch_cuda):
+    """ps_render_depth_rects rasterises synth.image_params to the host generator's bits."""
+    pb = synth.config3_problems(5, p0=17)
+    prm = synth.image_params(5, p0=17)
+    got = synth.render_images_device(prm, (240, 320)).cpu().numpy()
+    assert np.array_equal(got, pb.images)
+    p0 = synth.config0_problems(2, p0=3)
+    got0 = synth.render_images_device(synth.image_params(2, p0=3, image_shape=(128, 128), n_images=1, n_rect=5),
+                                      (128, 128)).cpu().numpy()
+    assert np.array_equal(got0, p0.images)

@@ -350,3 +350,10 @@ class TestGuideOracle:
         got, cl = oracle_lib.bl_guide(ps, x0, 6, lo, span, n_grad, float(alpha), max_halvings)
         assert np.array_equal(got, x)
         assert not np.array_equal(got, x0)           # guidance moved the seeds
+
+
+def test_image_params_reproduce_the_generator():
+    pb = synth.config3_problems(2, p0=9)
+    prm = synth.image_params(2, p0=9)
+    img = np.stack([[synth.render_depth_params(prm[i, m], 240, 320) for m in range(2)] for i in range(2)])
+    assert np.array_equal(img.astype(np.float32), pb.images)
