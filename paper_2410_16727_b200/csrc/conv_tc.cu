@@ -735,8 +735,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     float* s_beta = s_gamma + NF;
     float* s_rbias = s_beta + NF;
     float* s_wout = s_rbias + NF;                // [7][64]
-    float* s_red = s_wout + 7 * 64;              // [2 tile parity][WG][4 quadrants][32 samples][2*NG]
-    float* s_film = s_red + 2 * UT_EPI_WG * 4 * 32 * 2 * NG;  // [2 tile parity][WG][TC_FILM_P][2*NC]
+    float* s_red = s_wout + 7 * 64;              // [2 tile parity][WG][MB][4 quadrants][32 samples][2*NG]
+    float* s_film = s_red + 2 * UT_EPI_WG * MB * 4 * 32 * 2 * NG;  // [2 tile parity][WG][TC_FILM_P][2*NC]
     UtGroup* s_grp = reinterpret_cast<UtGroup*>(s_film + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC);
     UtTap* s_tap = reinterpret_cast<UtTap*>(s_grp + UT_MAXG);
 
@@ -967,7 +967,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         const int t0 = r / nb, sl = r % nb;  // tile row = (time, sample); M-block mb adds 128/nb steps
         const int tstep = 128 / nb;
         const float inv_n = 1.0f / (float)(Tv * CG);
-        float* red = s_red + wg * (4 * 32 * 2 * NG);
+        float* red = s_red + wg * (MB * 4 * 32 * 2 * NG);
         const int cbase = NSPLIT > 1 ? wg * NC : 0;   // first column of this warpgroup
         const int ew = warp - 2;                       // epilogue warp 0..4*WG-1
         const float* s_bias_all = s_bias;
@@ -1088,10 +1088,16 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     }
                 }
             } else {
-                // ---- GroupNorm statistics: rows of one sample share `sl` across all 4 warps
-                float s1[NG], s2[NG], mean[NG], rstd[NG];
+                // ---- GroupNorm statistics in a canonical order that does not depend on MB (so not on
+                // the batch size): per row, the group's channels in chunk order; the rows of a sample
+                // combined as the complete binary tree over t -- xor shuffles over the lanes holding
+                // consecutive t (offsets nb, 2 nb, ...), then the blocks of consecutive t held by each
+                // (M-block, warp), in t order, through shared memory
+                float s1[MB][NG], s2[MB][NG], mean[NG], rstd[NG];
 #pragma unroll
-                for (int g = 0; g < NG; ++g) s1[g] = s2[g] = 0.f;
+                for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) s1[mb][g] = s2[mb][g] = 0.f;
                 constexpr int SC = NC < 32 ? NC : 32;   // stats chunk width
                 // KEEP: narrow warpgroup slices keep the biased accumulator values in registers
                 // between the statistics and the normalise pass (no second TMEM read / bias add)
@@ -1129,27 +1135,31 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                         }
 #pragma unroll
                         for (int g = 0; g < NG; ++g) {
-                            s1[g] += a1[g].x + a1[g].y;
-                            s2[g] += a2[g].x + a2[g].y;
+                            s1[mb][g] += a1[g].x + a1[g].y;
+                            s2[mb][g] += a2[g].x + a2[g].y;
                         }
                     }
 #pragma unroll
-                for (int off = 16; off >= 1; off >>= 1)
+                for (int off = 1; off <= 16; off <<= 1)
                     if (off >= nb)
 #pragma unroll
-                        for (int g = 0; g < NG; ++g) {
-                            s1[g] += __shfl_xor_sync(PS_FULL, s1[g], off);
-                            s2[g] += __shfl_xor_sync(PS_FULL, s2[g], off);
-                        }
-                // partials of the 4 warps -> smem (double-buffered by tile parity, so one barrier
-                // suffices); the tile's FiLM rows are staged before the same barrier
-                float* redj = red + (j & 1) * (UT_EPI_WG * 4 * 32 * 2 * NG);
+                        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+                            for (int g = 0; g < NG; ++g) {
+                                s1[mb][g] += __shfl_xor_sync(PS_FULL, s1[mb][g], off);
+                                s2[mb][g] += __shfl_xor_sync(PS_FULL, s2[mb][g], off);
+                            }
+                // block partials -> smem (double-buffered by tile parity, so one barrier suffices);
+                // the tile's FiLM rows are staged before the same barrier
+                float* redj = red + (j & 1) * (UT_EPI_WG * MB * 4 * 32 * 2 * NG);
                 if (lane < nb)
 #pragma unroll
-                    for (int g = 0; g < NG; ++g) {
-                        redj[(q * 32 + sl) * 2 * NG + g] = s1[g];
-                        redj[(q * 32 + sl) * 2 * NG + NG + g] = s2[g];
-                    }
+                    for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+                        for (int g = 0; g < NG; ++g) {
+                            redj[((mb * 4 + q) * 32 + sl) * 2 * NG + g] = s1[mb][g];
+                            redj[((mb * 4 + q) * 32 + sl) * 2 * NG + NG + g] = s2[mb][g];
+                        }
                 bool film_staged = false;
                 if constexpr (EPI == EPI_GN_FILM) {
                     const int b_last = min(tile * nb + nb - 1, a.B - 1);
@@ -1170,14 +1180,21 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
-                    float a1 = 0.f, a2 = 0.f;
+                    float b1[4 * MB], b2[4 * MB];   // blocks of consecutive t, in t order
 #pragma unroll
-                    for (int qq = 0; qq < 4; ++qq) {
-                        a1 += redj[(qq * 32 + sl) * 2 * NG + g];
-                        a2 += redj[(qq * 32 + sl) * 2 * NG + NG + g];
+                    for (int bi = 0; bi < 4 * MB; ++bi) {
+                        b1[bi] = redj[(bi * 32 + sl) * 2 * NG + g];
+                        b2[bi] = redj[(bi * 32 + sl) * 2 * NG + NG + g];
                     }
-                    mean[g] = a1 * inv_n;
-                    rstd[g] = rsqrtf(fmaxf(fmaf(a2, inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
+#pragma unroll
+                    for (int w = 1; w < 4 * MB; w <<= 1)
+#pragma unroll
+                        for (int bi = 0; bi < 4 * MB; bi += 2 * w) {
+                            b1[bi] = b1[bi] + b1[bi + w];
+                            b2[bi] = b2[bi] + b2[bi + w];
+                        }
+                    mean[g] = b1[0] * inv_n;
+                    rstd[g] = rsqrtf(fmaxf(fmaf(b2[0], inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
                 }
 
                 const int p = b / a.S;
@@ -1443,7 +1460,7 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     // staged FiLM, tap tables
     constexpr int NSPLIT_ = UT_EPI_WG;
     constexpr int NG_ = 8 / (SPLIT * NSPLIT_), NC_ = N / NSPLIT_;
-    const size_t vec = (size_t)(4 * N * SPLIT + 7 * 64 + 2 * UT_EPI_WG * 4 * 32 * 2 * NG_ + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
+    const size_t vec = (size_t)(4 * N * SPLIT + 7 * 64 + 2 * UT_EPI_WG * MB * 4 * 32 * 2 * NG_ + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
                        UT_MAXG * sizeof(UtGroup) + UT_MAXTAP * sizeof(UtTap) + 64;
     const size_t fin = EPI == EPI_FINAL ? 2 * 16384 + 2048 + 2 * 128 * U_DOF * 4 : (size_t)UT_EPI_WG * 2 * 4096;
     const size_t budget = 225 * 1024 - vec - 2048 - fin;

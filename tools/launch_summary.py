@@ -28,7 +28,7 @@ def short(name):
 
 def main():
     rows = load(sys.argv[1])
-    starts = [i for i, (_, n, _) in enumerate(rows) if n.startswith("esdf_cull_kernel")]
+    starts = [i for i, (_, n, _) in enumerate(rows) if short(n).startswith("esdf_")]
     step = rows[starts[-1]:]
     tot = sum(t for _, _, t in step)
     agg = OrderedDict()
