@@ -1529,8 +1529,19 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n_sm_rl, cudaDevAttrMultiProcessorCount, dev);
     }
-    const bool small = (long long)B * ly.Tv < 256LL * n_sm_rl;
-    const int MBv = (!small && ly.epi != EPI_FINAL && (N == 64 || (N == 128 && !ly.res))) ? 2 : 1;
+    // Tile shape from the wave count: two-M-block tiles (each weight stage feeds 8 MMAs) unless
+    // one-M-block tiles need fewer M-block rounds per SM (ceil(tiles / #SM) x MB), or tie while
+    // two-M-block tiles would leave SMs idle.  Results do not depend on the choice: the GroupNorm
+    // statistics use one summation tree for either shape.
+    static const bool no_mbq = std::getenv("PS_NO_MB_WAVES") != nullptr;   // A/B: the old small-batch rule
+    int MBv = 1;
+    if (ly.epi != EPI_FINAL && (N == 64 || (N == 128 && !ly.res))) {
+        const long long rows = (long long)B * ly.Tv;
+        const long long t1 = (rows + 127) / 128, t2 = (rows + 255) / 256;
+        const long long u1 = (t1 + n_sm_rl - 1) / n_sm_rl, u2 = 2 * ((t2 + n_sm_rl - 1) / n_sm_rl);
+        if (no_mbq) MBv = rows < 256LL * n_sm_rl ? 1 : 2;
+        else MBv = (u2 < u1 || (u2 == u1 && t2 >= n_sm_rl)) ? 2 : 1;
+    }
     const int nb = MBv * 128 / ly.Tv;
     for (int s = 0; s < 3; ++s)
         // maps span >= nb samples (the workspace is padded to TC_MIN_B): a TMA box larger than
