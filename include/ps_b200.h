@@ -47,6 +47,11 @@ int ps_esdf_build_boxes(const float* boxes, int P, int n_boxes, const int* n_h,
 int ps_esdf_build_boxes_layout(const float* boxes, int P, int n_boxes, const int* n_h,
                                const float* origin_h, float h, float cap, float* out, int layout, void* stream);
 
+/* Quad-brick ESDF (refinement layout 2, see csrc/common.cuh): from P bricked ESDFs (layout 1) write
+ * the (P, nodes) float4 entries (v(i,j,k), v(i,j,k+1), v(i,j+1,k), v(i,j+1,k+1)) in brick order, so
+ * a trilinear lookup is two 16-B loads.  4x the storage: for an ESDF shared by a large batch. */
+int ps_esdf_quad_expand(const float* bricks, int P, const int* n_h, float* quads, void* stream);
+
 /* Batched cost and gradient (no update): cost (B,), grad (B,T,7) with row 0 zero,
  * clamped (B,) uint8.  Trajectory b reads ESDF esdf + (b / S) * esdf_stride.
  * BL analogue of _kernels.cost_terms_batch (_kernels.py:165-312). */
@@ -67,7 +72,8 @@ int ps_bl_refine(const float* q_in, int B, int T, int S, const float* esdf,
                  const int* sph_link_h, int n_sph, const float* weights_h, int n_iters,
                  float* q_out, float* cost, uint8_t* feasible, uint8_t* clamped, void* stream);
 
-/* ps_bl_refine over an ESDF in `layout` (see ps_esdf_build_boxes_layout); identical results. */
+/* ps_bl_refine over an ESDF in `layout` (0 C order, 1 bricks, 2 quad bricks: ps_esdf_quad_expand;
+ * esdf_stride in floats, 4 per node for layout 2); identical results. */
 int ps_bl_refine_layout(const float* q_in, int B, int T, int S, const float* esdf, long long esdf_stride,
                         int layout, const int* n_h, const float* origin_h, float h, const float* dh_h,
                         const float* base_h, const float* sph_h, const int* sph_link_h, int n_sph,

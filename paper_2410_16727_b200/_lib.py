@@ -31,6 +31,7 @@ _SIGS = {
     "ps_esdf_build_boxes_layout": [_vp, _c_int, _c_int, _vp, _vp, _c_f, _c_f, _vp, _c_int, _vp],
     "ps_bl_refine_layout": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _c_int, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,
                             _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp],
+    "ps_esdf_quad_expand": [_vp, _c_int, _vp, _vp, _vp],
     "ps_bl_cost": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,
                    _c_int, _vp, _vp, _vp, _vp, _vp],
     "ps_bl_refine": [_vp, _c_int, _c_int, _c_int, _vp, _c_ll, _vp, _vp, _c_f, _vp, _vp, _vp, _vp,

@@ -55,7 +55,7 @@ def _grid_args(grid: GridSpec):
     return n, o
 
 
-ESDF_C_ORDER, ESDF_BRICKED = 0, 1
+ESDF_C_ORDER, ESDF_BRICKED, ESDF_QUAD = 0, 1, 2
 
 
 def esdf_build(boxes, grid: GridSpec = GridSpec(), stream=None, layout: int = ESDF_C_ORDER, out=None):
@@ -67,9 +67,17 @@ def esdf_build(boxes, grid: GridSpec = GridSpec(), stream=None, layout: int = ES
     if b.dim() != 3 or b.shape[2] != 6:
         raise ValueError("boxes must be (P, n_boxes, 6)")
     P = b.shape[0]
+    n, o = _grid_args(grid)
+    if layout == ESDF_QUAD:
+        # quad bricks (4 floats per node, see ps_esdf_quad_expand): built as bricks, then expanded
+        bricks = esdf_build(b, grid, stream, ESDF_BRICKED)
+        if out is None:
+            out = torch.empty((P,) + tuple(grid.n) + (4,), dtype=torch.float32, device="cuda")
+        _lib.check(_lib.lib().ps_esdf_quad_expand(_lib.ptr(bricks), P, _lib.hptr(n), _lib.ptr(out),
+                                                  _lib.stream_handle(stream)), "esdf_quad_expand")
+        return out
     if out is None:
         out = torch.empty((P,) + tuple(grid.n), dtype=torch.float32, device="cuda")
-    n, o = _grid_args(grid)
     st = _lib.lib().ps_esdf_build_boxes_layout(_lib.ptr(b), P, b.shape[1], _lib.hptr(n), _lib.hptr(o),
                                                grid.h, grid.cap, _lib.ptr(out), int(layout),
                                                _lib.stream_handle(stream))
@@ -86,13 +94,15 @@ def unbrick(esdf_bricked, grid: GridSpec = GridSpec()):
 
 
 def _esdf_stride(esdf, grid: GridSpec, n_problems: int) -> int:
-    if esdf.dim() == 3:
+    """Floats between consecutive problems' ESDFs (4 per node for quad bricks, (P, nx, ny, nz, 4))."""
+    quad = esdf.dim() in (4, 5) and esdf.shape[-1] == 4 and tuple(esdf.shape[-4:-1]) == tuple(grid.n)
+    if esdf.dim() == (4 if quad else 3):
         return 0                      # one ESDF shared by every problem
     if esdf.shape[0] == 1:
         return 0
     if esdf.shape[0] < n_problems:
         raise ValueError("need one ESDF per problem (or a single shared one)")
-    return grid.n_nodes
+    return grid.n_nodes * (4 if quad else 1)
 
 
 OUT_OF_GRID_MSG = "trajectory collision points leave the ESDF extent"

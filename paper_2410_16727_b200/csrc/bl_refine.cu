@@ -1035,7 +1035,7 @@ extern "C" int ps_bl_cost_layout(const float* q, int B, int T, int S, const floa
     int st = fill_params(P, B, T, S, esdf, esdf_stride, n_h, origin_h, h, dh_h, base_h, sph_h, sph_link_h,
                          n_sph, weights_h);
     if (st) return st;
-    if (layout < 0 || layout > 1 || (layout == 1 && ((n_h[0] & 3) || (n_h[1] & 3) || (n_h[2] & 3))))
+    if (layout < 0 || layout > 2 || (layout >= 1 && ((n_h[0] & 3) || (n_h[1] & 3) || (n_h[2] & 3))))
         return PS_ERR_SHAPE;
     P.esdf_brick = layout;
     P.q_in = q; P.cost = cost; P.grad = grad; P.clamped = clamped; P.n_iters = 0;
@@ -1099,7 +1099,7 @@ extern "C" int ps_bl_guide(float* x0, int B, int T, int S, const float* esdf, lo
     int st = fill_params(P, B, T, S, esdf, esdf_stride, n_h, origin_h, h, dh_h, base_h, sph_h, sph_link_h, n_sph,
                          weights_h);
     if (st) return st;
-    if (layout < 0 || layout > 1 || (layout == 1 && ((n_h[0] & 3) || (n_h[1] & 3) || (n_h[2] & 3))) || n_grad < 0 ||
+    if (layout < 0 || layout > 2 || (layout >= 1 && ((n_h[0] & 3) || (n_h[1] & 3) || (n_h[2] & 3))) || n_grad < 0 ||
         max_halvings < 0)
         return PS_FAIL(PS_ERR_SHAPE);
     P.esdf_brick = layout;
@@ -1143,13 +1143,45 @@ extern "C" int ps_bl_refine_layout(const float* q_in, int B, int T, int S, const
     int st = fill_params(P, B, T, S, esdf, esdf_stride, n_h, origin_h, h, dh_h, base_h, sph_h, sph_link_h,
                          n_sph, weights_h);
     if (st) return st;
-    if (layout < 0 || layout > 1 || (layout == 1 && ((n_h[0] & 3) || (n_h[1] & 3) || (n_h[2] & 3))))
+    if (layout < 0 || layout > 2 || (layout >= 1 && ((n_h[0] & 3) || (n_h[1] & 3) || (n_h[2] & 3))))
         return PS_ERR_SHAPE;
     P.esdf_brick = layout;
     if (n_iters < 0) return PS_ERR_SHAPE;
     P.q_in = q_in; P.q_out = q_out; P.cost = cost; P.feasible = feasible; P.clamped = clamped;
     P.n_iters = n_iters;
     return launch_bl<0>(P, (cudaStream_t)stream);
+}
+
+// bricked scalar ESDF -> quad bricks (see common.cuh): one thread per node
+__global__ void esdf_quad_kernel(const float* __restrict__ src, int nx, int ny, int nz, long long n_nodes, int P,
+                                 float4* __restrict__ dst) {
+    const long long i_all = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i_all >= n_nodes * P) return;
+    const int p = (int)(i_all / n_nodes);
+    const long long e = i_all - (long long)p * n_nodes;   // brick-order entry index
+    (void)P;
+    const int bz = nz >> 2, by = ny >> 2;
+    const long long brick = e >> 6;
+    const int w = (int)(e & 63);
+    const int ib = (int)(brick / ((long long)by * bz)), jb = (int)((brick / bz) % by), kb = (int)(brick % bz);
+    const int i = ib * 4 + (w >> 4), j = jb * 4 + ((w >> 2) & 3), k = kb * 4 + (w & 3);
+    const int j1 = min(j + 1, ny - 1), k1 = min(k + 1, nz - 1);
+    const float* v = src + (size_t)p * n_nodes;
+    dst[(size_t)p * n_nodes + e] = make_float4(v[esdf_brick_index(i, j, k, ny, nz)], v[esdf_brick_index(i, j, k1, ny, nz)],
+                                               v[esdf_brick_index(i, j1, k, ny, nz)],
+                                               v[esdf_brick_index(i, j1, k1, ny, nz)]);
+}
+
+extern "C" int ps_esdf_quad_expand(const float* bricks, int P, const int* n_h, float* quads, void* stream) {
+    if (P < 0 || (n_h[0] & 3) || (n_h[1] & 3) || (n_h[2] & 3) || n_h[0] < 4 || n_h[1] < 4 || n_h[2] < 4)
+        return PS_FAIL(PS_ERR_SHAPE);
+    if (P == 0) return PS_OK;
+    const long long n_nodes = (long long)n_h[0] * n_h[1] * n_h[2];
+    const long long n = n_nodes * P;
+    esdf_quad_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        bricks, n_h[0], n_h[1], n_h[2], n_nodes, P, reinterpret_cast<float4*>(quads));
+    PS_CHECK_LAUNCH();
+    return PS_OK;
 }
 
 extern "C" int ps_esdf_build_boxes_layout(const float* boxes, int P, int n_boxes, const int* n_h,

@@ -75,7 +75,7 @@ struct Grid {
     const float* __restrict__ v;
     int nx, ny, nz;
     float ox, oy, oz, inv_h;
-    int brick;   // 0: C order (z fastest); 1: 4x4x4 bricks (see esdf_brick_index)
+    int brick;   // 0: C order (z fastest); 1: 4x4x4 bricks (see esdf_brick_index); 2: quad bricks
 };
 
 // 4x4x4-brick layout of an (nx, ny, nz) grid with all extents multiples of 4: brick
@@ -87,6 +87,13 @@ __host__ __device__ __forceinline__ size_t esdf_brick_index(int i, int j, int k,
     return (((size_t)(i >> 2) * (size_t)(ny >> 2) + (size_t)(j >> 2)) * (size_t)(nz >> 2) + (size_t)(k >> 2)) * 64 +
            (size_t)((i & 3) * 16 + (j & 3) * 4 + (k & 3));
 }
+
+// Quad-brick layout (layout 2): node (i, j, k) holds the float4 (v(i,j,k), v(i,j,k+1), v(i,j+1,k),
+// v(i,j+1,k+1)) (neighbours clamped at the upper faces, never read as cell corners), entries in the
+// 4^3-brick order of esdf_brick_index.  A trilinear cell's 8 corners are the entries of (i, j, k)
+// and (i+1, j, k): two 16-B loads instead of eight scalar gathers (L1TEX wavefronts / 4), at 4x
+// the storage -- the layout for an ESDF shared by a large batch (BASELINE config 2: 33.6 MB,
+// L2-resident).
 
 // Trilinear value + in-cell analytic gradient + clamp flag; generalises
 // planseed/_kernels.py:_bilinear (:23-57) to 3-D.  Manual fp32 weights, never
@@ -113,6 +120,15 @@ __device__ __forceinline__ void tri_gather(const Grid& g, const f3& p, TriCell& 
     c.tz = fminf(fmaxf(uz - fk, 0.f), 1.f);
     const float* v;
     size_t sx, sy, sz;
+    if (g.brick == 2) {   // quad bricks: two 16-B loads hold the cell's 8 corners
+        const int ii = (int)fi, jj = (int)fj, kk = (int)fk;
+        const float4* q4 = reinterpret_cast<const float4*>(g.v) + esdf_brick_index(ii, jj, kk, g.ny, g.nz);
+        const size_t s4 = (ii & 3) == 3 ? (size_t)(g.ny >> 2) * (size_t)(g.nz >> 2) * 64 - 48 : 16;
+        const float4 a = __ldg(q4), b = __ldg(q4 + s4);
+        c.v000 = a.x; c.v001 = a.y; c.v010 = a.z; c.v011 = a.w;
+        c.v100 = b.x; c.v101 = b.y; c.v110 = b.z; c.v111 = b.w;
+        return;
+    }
     if (g.brick) {   // neighbour steps stay inside a brick unless the cell sits on its edge
         const int ii = (int)fi, jj = (int)fj, kk = (int)fk;
         v = g.v + esdf_brick_index(ii, jj, kk, g.ny, g.nz);

@@ -294,3 +294,25 @@ def test_depth_images_rendered_on_device_bitwise(torch_cuda):
     got0 = synth.render_images_device(synth.image_params(2, p0=3, image_shape=(128, 128), n_images=1, n_rect=5),
                                       (128, 128)).cpu().numpy()
     assert np.array_equal(got0, p0.images)
+
+
+@pytest.mark.parametrize("shared", [True, False])
+def test_quad_brick_layout_bitwise(bl, oracle_lib, shared):
+    """Layout 2 (quad bricks, two 16-B loads per lookup) gives the C-order results bit for bit:
+    refinement, cost/gradient and flags, for a shared ESDF (config 2) and per-problem ESDFs."""
+    grid = spec.GridSpec()
+    P, S = (1, 64) if shared else (3, 16)
+    boxes = np.stack([synth.sample_boxes(np.random.default_rng(9 + i), 20, grid) for i in range(P)]).astype(np.float32)
+    c_order = bl.esdf_build(boxes, grid)
+    quad = bl.esdf_build(boxes, grid, layout=bl.ESDF_QUAD)
+    assert quad.shape == (P, 128, 128, 128, 4)
+    e0, e2 = (c_order[0], quad[0]) if shared else (c_order, quad)
+    q = synth.refine_init(P * S if not shared else S, seed=12)
+    a = [o.cpu().numpy() for o in bl.refine(q, e0, S, RB, grid, COST)]
+    b = [o.cpu().numpy() for o in bl.refine(q, e2, S, RB, grid, COST, esdf_layout=bl.ESDF_QUAD)]
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    ca = [o.cpu().numpy() for o in bl.cost(q, e0, S, RB, grid, COST)]
+    cb = [o.cpu().numpy() for o in bl.cost(q, e2, S, RB, grid, COST, esdf_layout=bl.ESDF_QUAD)]
+    for x, y in zip(ca, cb):
+        assert np.array_equal(x, y)

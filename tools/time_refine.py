@@ -23,6 +23,10 @@ outs = (torch.empty_like(q), torch.empty(2048, device="cuda"), torch.empty(2048,
 ms = timeit(lambda: bl.refine(q, esdf[0], 2048, robot, grid, cost, out=outs))
 res["cfg2_refine_ms"] = ms
 res["cfg2_GBps_alg"] = 2048 * 10 * 52992 / (ms * 1e-3) / 1e9
+esdf_q = bl.esdf_build(boxes, grid, layout=bl.ESDF_QUAD)
+ms_q = timeit(lambda: bl.refine(q, esdf_q[0], 2048, robot, grid, cost, out=outs, esdf_layout=bl.ESDF_QUAD))
+res["cfg2_quad_refine_ms"] = ms_q
+res["cfg2_quad_GBps_alg"] = 2048 * 10 * 52992 / (ms_q * 1e-3) / 1e9
 # config 3-like: 1024 problems x 32 seeds, per-problem ESDF
 P = 1024
 pb = synth.make_problems(P, seed=0)
