@@ -1051,6 +1051,29 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             const int b = tile * nb + sl;
             const bool valid = b < a.B;
             const uint32_t t_lane0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC + cbase);
+            // FiLM rows of this tile's problems: loaded (L2) before waiting for the accumulator, so
+            // their latency overlaps the wait and the statistics instead of preceding the GN barrier
+            float fpre[2] = {0.f, 0.f};
+            int f_plo = 0, f_n = 0;
+            if constexpr (EPI == EPI_GN_FILM) {
+                static_assert(TC_FILM_P * 2 * NC <= 256, "two FiLM values per thread");
+                const int b_last = min(tile * nb + nb - 1, a.B - 1);
+                f_plo = (tile * nb) / a.S;
+                const int p_hi = b_last / a.S;
+                if (p_hi - f_plo < TC_FILM_P) {
+                    f_n = (p_hi - f_plo + 1) * 2 * NC;
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int i = r + 128 * u;
+                        if (i < f_n) {
+                            const int pp = i / (2 * NC), w = i % (2 * NC);
+                            const int c = cbase + (w < NC ? w : w - NC);
+                            fpre[u] = __ldg(a.film + (size_t)(f_plo + pp) * 3584 + a.film_col + cur_noff +
+                                            (w < NC ? c : NF + c));
+                        }
+                    }
+                }
+            }
             mbar_wait(&tfull[buf], (uint32_t)(j / NBUF) & 1u);
             tc_fence_after();
 
@@ -1162,17 +1185,15 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                         }
                 bool film_staged = false;
                 if constexpr (EPI == EPI_GN_FILM) {
-                    const int b_last = min(tile * nb + nb - 1, a.B - 1);
-                    const int p_lo = (tile * nb) / a.S, p_hi = b_last / a.S;
                     float* sf = s_film + ((j & 1) * UT_EPI_WG + wg) * (TC_FILM_P * 2 * NC);
-                    if (p_hi - p_lo < TC_FILM_P) {
-                        const int n = (p_hi - p_lo + 1) * 2 * NC;
-                        for (int i = r; i < n; i += 128) {
-                            const int pp = i / (2 * NC), w = i % (2 * NC);
-                            const int c = cbase + (w < NC ? w : w - NC);
-                            const float v = __ldg(a.film + (size_t)(p_lo + pp) * 3584 + a.film_col + cur_noff +
-                                                  (w < NC ? c : NF + c));
-                            sf[pp * 2 * NC + w] = w < NC ? 1.f + v : v;
+                    if (f_n > 0) {
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int i = r + 128 * u;
+                            if (i < f_n) {
+                                const int pp = i / (2 * NC), w = i % (2 * NC);
+                                sf[pp * 2 * NC + w] = w < NC ? 1.f + fpre[u] : fpre[u];
+                            }
                         }
                         film_staged = true;
                     }
