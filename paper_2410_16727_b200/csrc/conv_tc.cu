@@ -1126,6 +1126,13 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                 // between the statistics and the normalise pass (no second TMEM read / bias add)
                 constexpr bool KEEP = (EPI == EPI_GN_FILM || (EPI == EPI_GN_RES && !RES)) && SC == 16 && NC == 16;
                 float kv[KEEP ? MB : 1][16];
+                // 16-channel slices: every M-block's accumulator row is loaded before one wait
+                uint32_t rr_all[NC == 16 ? MB : 1][16];
+                if constexpr (NC == 16) {
+#pragma unroll
+                    for (int mb = 0; mb < MB; ++mb) tmem_ld16(t_lane0 + (uint32_t)(mb * ACC1), rr_all[mb]);
+                    tmem_wait_ld();
+                }
 #pragma unroll
                 for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
@@ -1133,6 +1140,9 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                         float v[SC];
                         if constexpr (SC == 32) {
                             tmem_ld32(t_lane0 + (uint32_t)(mb * ACC1) + cc, v);
+                        } else if constexpr (NC == 16) {
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj) v[jj] = __uint_as_float(rr_all[NC == 16 ? mb : 0][jj]);
                         } else {
                             uint32_t rr[16];
                             tmem_ld16(t_lane0 + (uint32_t)(mb * ACC1) + cc, rr);
