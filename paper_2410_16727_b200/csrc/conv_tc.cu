@@ -1124,7 +1124,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                 constexpr int SC = NC < 32 ? NC : 32;   // stats chunk width
                 // KEEP: narrow warpgroup slices keep the biased accumulator values in registers
                 // between the statistics and the normalise pass (no second TMEM read / bias add)
-                constexpr bool KEEP = (EPI == EPI_GN_FILM || (EPI == EPI_GN_RES && !RES)) && SC == 16 && NC == 16;
+                constexpr bool KEEP = (EPI == EPI_GN_FILM || EPI == EPI_GN_RES) && SC == 16 && NC == 16;
                 float kv[KEEP ? MB : 1][16];
                 // 16-channel slices: every M-block's accumulator row is loaded before one wait
                 uint32_t rr_all[NC == 16 ? MB : 1][16];
@@ -1346,6 +1346,14 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     // no early-out on `valid`: tcgen05.ld is .sync.aligned and lanes of one warp
                     // belong to different samples, so only global accesses are predicated
                     {
+                      // kept 16-channel slices with a projection residual: both M-blocks' residual
+                      // accumulators loaded before one wait
+                      uint32_t rq_all[KEEP && RES ? MB : 1][16];
+                      if constexpr (KEEP && RES) {
+#pragma unroll
+                          for (int mb = 0; mb < MB; ++mb) tmem_ld16(t_lane0 + (uint32_t)(mb * ACC1) + N, rq_all[mb]);
+                          tmem_wait_ld();
+                      }
 #pragma unroll
                       for (int mb = 0; mb < MB; ++mb) {
                         const int grow = b * Tv + t0 + mb * tstep;
@@ -1409,8 +1417,9 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                                         y[jj] = fmaf(y[jj], 1.f + __ldg(fr + c0 + jj), __ldg(fr + NF + c0 + jj));
                                 }
                             } else if constexpr (RES) {
+                                const uint32_t* rqp = KEEP ? rq_all[KEEP && RES ? mb : 0] : rq;
 #pragma unroll
-                                for (int jj = 0; jj < 16; ++jj) y[jj] += __uint_as_float(rq[jj]) + s_rbias[c0 + jj];
+                                for (int jj = 0; jj < 16; ++jj) y[jj] += __uint_as_float(rqp[jj]) + s_rbias[c0 + jj];
                             } else {
                                 stage_store_res(y, c0, mb, j, mb * (NC / 16) + cc / 16);
                                 continue;
