@@ -282,6 +282,35 @@ int ps_ref_metrics(const double* trajs, int S, int T, int D, const double* lengt
 int ps_ref_denorm_pin(const double* x0, int B, int T, int D, const double* lo, const double* hi,
                       const double* q0, double* traj, void* stream);
 
+/* ================= Reference profile: training (csrc/ref_train.cu, float64) ================
+ * The layer-level kernels of loss_eq2 / train (src/diffusion.py:415-508, src/autodiff.py): the host
+ * (ref/train.py) runs the forward pass, the backward pass in reverse layer order and Adam.
+ *   ps_train_gemm:      C (+)= op(A) op(B), row-major with leading dims, op = transpose when t* = 1;
+ *   ps_train_bias_act:  y += b (rows), act 1: y = silu(y) keeping the pre-activation;
+ *   ps_train_silu_bwd:  g *= silu'(pre);   ps_train_colsum: db (+)= column sums;
+ *   ps_train_film(_bwd): out = a (1 + sc) + sh;  da = g (1 + sc), dsc = g a;
+ *   ps_train_conv1d(_bwd): valid-mode strided conv1d + silu (autodiff.py:226-246) and its dw, db, gx;
+ *   ps_train_fk_loss:   per (b, t) row the FK point-set error of the planar chain and the plain noise
+ *                       error (fk_weighted_mse + mse_stabilizer plain_weighted_mse, diffusion.py:304-349)
+ *                       and d loss / d eps_pred;
+ *   ps_train_adam:      Adam.step for one parameter tensor (autodiff.py:272-284). */
+int ps_train_gemm(const double* A, int lda, int ta, const double* B, int ldb, int tb, double* C, int ldc, int M, int N,
+                  int K, int accumulate, void* stream);
+int ps_train_bias_act(double* y, int ldy, const double* b, int R, int N, int act, double* pre, void* stream);
+int ps_train_silu_bwd(double* g, int ldg, const double* pre, int R, int N, void* stream);
+int ps_train_colsum(const double* g, int ldg, int R, int N, double* db, int accumulate, void* stream);
+int ps_train_film(const double* a, const double* sc, const double* sh, int n, double* out, void* stream);
+int ps_train_film_bwd(const double* g, const double* a, const double* sc, int n, double* da, double* dsc, void* stream);
+int ps_train_conv1d(const double* x, int B, int C, int L, const double* w, const double* b, int O, int K, int S,
+                    double* pre, double* y, void* stream);
+int ps_train_conv1d_bwd(const double* gy, const double* x, const double* w, int B, int C, int L, int O, int K, int S,
+                        double* dw, double* db, double* gx, void* stream);
+int ps_train_fk_loss(const double* eps_true, const double* eps_pred, int B, int T, int D, int M, const double* w,
+                     const double* lo, const double* span, const double* len, const double* fr, double base_x,
+                     double base_y, double mse_w, double* row_fk, double* row_mse, double* grad, void* stream);
+int ps_train_adam(double* p, const double* g, double* m, double* v, long long n, double lr, double b1, double b2,
+                  double b1t, double b2t, double eps, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -90,6 +90,17 @@ _SIGS = {
     "ps_ref_metrics": [_vp, _c_int, _c_int, _c_int, _vp, _c_d, _c_d, _vp, _c_int, _vp, _c_int, _vp, _c_int, _c_d,
                        _c_d, _c_d, _c_d, _vp, _vp, _vp, _vp, _c_int, _vp, _vp],
     "ps_ref_denorm_pin": [_vp, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp],
+    "ps_train_gemm": [_vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
+    "ps_train_bias_act": [_vp, _c_int, _vp, _c_int, _c_int, _c_int, _vp, _vp],
+    "ps_train_silu_bwd": [_vp, _c_int, _vp, _c_int, _c_int, _vp],
+    "ps_train_colsum": [_vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
+    "ps_train_film": [_vp, _vp, _vp, _c_int, _vp, _vp],
+    "ps_train_film_bwd": [_vp, _vp, _vp, _c_int, _vp, _vp, _vp],
+    "ps_train_conv1d": [_vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp],
+    "ps_train_conv1d_bwd": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp],
+    "ps_train_fk_loss": [_vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp, _c_d, _c_d, _c_d, _vp, _vp,
+                         _vp, _vp],
+    "ps_train_adam": [_vp, _vp, _vp, _vp, _c_ll, _c_d, _c_d, _c_d, _c_d, _c_d, _c_d, _vp],
     "ps_encoder_packed_bytes": [_c_int, _c_int, _c_int],
     "ps_encoder_pack": [_vp, _c_int, _c_int, _c_int, _vp, _vp],
     "ps_encode_tc_workspace_bytes": [_c_int, _c_int, _c_int, _c_int],

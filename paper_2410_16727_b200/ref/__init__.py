@@ -7,4 +7,4 @@
 Objects from planseed itself (ArmModel, SdfGrid, DenoiserNet, DepthScan, Pose2,
 CostWeights) are accepted as well as this package's compatible types."""
 
-from . import diffusion, pipeline, trajopt, types  # noqa: F401
+from . import diffusion, pipeline, train, trajopt, types  # noqa: F401

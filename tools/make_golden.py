@@ -275,6 +275,70 @@ def gen_scans():
     return out
 
 
+def train_records(n=3):
+    """Small ProblemRecords (planseed/data.py:51-63) with smooth expert trajectories and scans."""
+    from planseed.data import PlanningProblem, ProblemRecord
+    rng = np.random.default_rng(50)
+    w = World([Circle(center=(0.35, 0.1), radius=0.12), Box(lo=(-0.5, 0.3), hi=(-0.1, 0.6))])
+    recs = []
+    for i in range(n):
+        q0 = rng.uniform(-1.5, 1.5, size=7)
+        q1 = rng.uniform(-1.5, 1.5, size=7)
+        expert = q0 + np.linspace(0, 1, T)[:, None] * (q1 - q0) + 0.02 * np.sin(np.linspace(0, 3, T))[:, None]
+        goal = fk_pose(ARM, expert[-1])
+        scans = [render_depth_scan(w, SensorPose(position=(rng.uniform(-0.8, 0.8), rng.uniform(-0.8, 0.8)),
+                                                 heading=rng.uniform(-3, 3))) for _ in range(2)]
+        recs.append(ProblemRecord(problem=PlanningProblem(world_id="g", q_start=q0, goal=goal), world=w,
+                                  expert=expert, graph_used=bool(i % 2), scans=scans))
+    return recs
+
+
+def record_dict(recs):
+    out = {}
+    for i, r in enumerate(recs):
+        out[f"r{i}_expert"] = r.expert
+        out[f"r{i}_q0"] = r.problem.q_start
+        out[f"r{i}_goal"] = np.array([*r.problem.goal.pos, r.problem.goal.theta])
+        out[f"r{i}_graph_used"] = np.array(r.graph_used)
+        for j, sc in enumerate(r.scans):
+            out[f"r{i}_s{j}_depths"] = sc.depths
+            out[f"r{i}_s{j}_pose"] = np.array([*sc.pose.position, sc.pose.heading])
+    return out
+
+
+def gen_train():
+    """diffusion.loss_eq2 (one record, k = 37) and a short diffusion.train run (3 records, batch 4,
+    2 epochs): loss, every parameter gradient, the loss curve and per-parameter sums of the trained
+    weights (src/diffusion.py:435-508)."""
+    from planseed.diffusion import ArchConfig, TrainConfig, loss_eq2, train
+    recs = train_records()
+    out = record_dict(recs)
+    net = create_net(ArchConfig(), seed=0)
+    eps = np.random.default_rng(51).standard_normal((T, 7))
+    loss, grads = loss_eq2(ARM, net, recs[0], 37, eps, alpha_loss=4.0, scan_index=1)
+    out["eq2_eps"] = eps
+    out["eq2_loss"] = np.float64(loss)
+    sel = np.random.default_rng(52)
+    for k, g in grads.items():
+        g = np.asarray(g)
+        if g.size <= 20000:
+            out[f"eq2_grad_{k}"] = g
+        else:   # large matrices: sums plus 256 sampled entries (keeps the fixture small)
+            idx = np.sort(sel.choice(g.size, 256, replace=False))
+            out[f"eq2_gsum_{k}"] = np.array([g.sum(), (g * g).sum()])
+            out[f"eq2_gidx_{k}"] = idx
+            out[f"eq2_gval_{k}"] = g.ravel()[idx]
+    net2 = create_net(ArchConfig(), seed=0)
+    curve = train(net2, recs, make_schedule(), ARM, TrainConfig(batch_size=4, epochs=2, lr=1e-3, seed=3))
+    out["train_curve"] = np.array(curve)
+    for k, p in net2.params.items():
+        d = np.asarray(p.data)
+        out[f"train_sum_{k}"] = np.array([d.sum(), (d * d).sum()])
+    out["train_full_trunk_out_b"] = np.asarray(net2.params["trunk_out_b"].data)
+    out["train_full_scan_conv0_w"] = np.asarray(net2.params["scan_conv0_w"].data)
+    return out
+
+
 def main(out_dir: Path = ROOT / "tests" / "golden"):
     out_dir.mkdir(parents=True, exist_ok=True)
     for name, c in gen_cost().items():
@@ -285,6 +349,7 @@ def main(out_dir: Path = ROOT / "tests" / "golden"):
     np.savez_compressed(out_dir / "ref_guided.npz", **gen_guided())
     np.savez_compressed(out_dir / "ref_metrics.npz", **gen_metrics())
     np.savez_compressed(out_dir / "ref_scans.npz", **gen_scans())
+    np.savez_compressed(out_dir / "ref_train.npz", **gen_train())
     return out_dir
 
 
