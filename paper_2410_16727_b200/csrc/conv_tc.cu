@@ -1187,12 +1187,18 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                 float* redj = red + (j & 1) * (UT_EPI_WG * MB * 4 * 32 * 2 * NG);
                 if (lane < nb)
 #pragma unroll
-                    for (int mb = 0; mb < MB; ++mb)
+                    for (int mb = 0; mb < MB; ++mb) {
+                        if constexpr (NG == 2) {   // (s1 g0, s1 g1, s2 g0, s2 g1): one 16-B store
+                            *reinterpret_cast<float4*>(redj + ((mb * 4 + q) * 32 + sl) * 4) =
+                                make_float4(s1[mb][0], s1[mb][NG - 1], s2[mb][0], s2[mb][NG - 1]);
+                        } else {
 #pragma unroll
-                        for (int g = 0; g < NG; ++g) {
-                            redj[((mb * 4 + q) * 32 + sl) * 2 * NG + g] = s1[mb][g];
-                            redj[((mb * 4 + q) * 32 + sl) * 2 * NG + NG + g] = s2[mb][g];
+                            for (int g = 0; g < NG; ++g) {
+                                redj[((mb * 4 + q) * 32 + sl) * 2 * NG + g] = s1[mb][g];
+                                redj[((mb * 4 + q) * 32 + sl) * 2 * NG + NG + g] = s2[mb][g];
+                            }
                         }
+                    }
                 bool film_staged = false;
                 if constexpr (EPI == EPI_GN_FILM) {
                     float* sf = s_film + ((j & 1) * UT_EPI_WG + wg) * (TC_FILM_P * 2 * NC);
@@ -1209,23 +1215,48 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     }
                 }
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
-#pragma unroll
-                for (int g = 0; g < NG; ++g) {
-                    float b1[4 * MB], b2[4 * MB];   // blocks of consecutive t, in t order
+                if constexpr (NG == 2) {
+                    // blocks of consecutive t, in t order, as (s1, s1, s2, s2) vectors; the tree adds
+                    // run on packed pairs (the same two-operand fp32 adds per lane)
+                    float2 b1[4 * MB], b2[4 * MB];
 #pragma unroll
                     for (int bi = 0; bi < 4 * MB; ++bi) {
-                        b1[bi] = redj[(bi * 32 + sl) * 2 * NG + g];
-                        b2[bi] = redj[(bi * 32 + sl) * 2 * NG + NG + g];
+                        const float4 v4 = *reinterpret_cast<const float4*>(redj + (bi * 32 + sl) * 4);
+                        b1[bi] = f2(v4.x, v4.y);
+                        b2[bi] = f2(v4.z, v4.w);
                     }
 #pragma unroll
                     for (int w = 1; w < 4 * MB; w <<= 1)
 #pragma unroll
                         for (int bi = 0; bi < 4 * MB; bi += 2 * w) {
-                            b1[bi] = b1[bi] + b1[bi + w];
-                            b2[bi] = b2[bi] + b2[bi + w];
+                            b1[bi] = fadd2(b1[bi], b1[bi + w]);
+                            b2[bi] = fadd2(b2[bi], b2[bi + w]);
                         }
-                    mean[g] = b1[0] * inv_n;
-                    rstd[g] = rsqrtf(fmaxf(fmaf(b2[0], inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
+                    const float t1[2] = {b1[0].x, b1[0].y}, t2[2] = {b2[0].x, b2[0].y};
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        mean[g] = t1[g] * inv_n;
+                        rstd[g] = rsqrtf(fmaxf(fmaf(t2[g], inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
+                    }
+                } else {
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) {
+                        float b1[4 * MB], b2[4 * MB];   // blocks of consecutive t, in t order
+#pragma unroll
+                        for (int bi = 0; bi < 4 * MB; ++bi) {
+                            b1[bi] = redj[(bi * 32 + sl) * 2 * NG + g];
+                            b2[bi] = redj[(bi * 32 + sl) * 2 * NG + NG + g];
+                        }
+#pragma unroll
+                        for (int w = 1; w < 4 * MB; w <<= 1)
+#pragma unroll
+                            for (int bi = 0; bi < 4 * MB; bi += 2 * w) {
+                                b1[bi] = b1[bi] + b1[bi + w];
+                                b2[bi] = b2[bi] + b2[bi + w];
+                            }
+                        mean[g] = b1[0] * inv_n;
+                        rstd[g] = rsqrtf(fmaxf(fmaf(b2[0], inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
+                    }
                 }
 
                 const int p = b / a.S;
