@@ -130,6 +130,8 @@ def lib():
         alt = os.environ.get("PS_LIB_OVERRIDE")   # A/B timing of an alternative build (tools only)
         L = ctypes.CDLL(alt if alt else str(path))
         for name, args in _SIGS.items():
+            if alt and not hasattr(L, name):   # an older build under A/B: bind what it has
+                continue
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = _RESTYPE.get(name, ctypes.c_int)
