@@ -735,8 +735,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     float* s_beta = s_gamma + NF;
     float* s_rbias = s_beta + NF;
     float* s_wout = s_rbias + NF;                // [7][64]
-    float* s_red = s_wout + 7 * 64;              // [2 tile parity][WG][MB][4 quadrants][32 samples][2*NG]
-    float* s_film = s_red + 2 * UT_EPI_WG * MB * 4 * 32 * 2 * NG;  // [2 tile parity][WG][TC_FILM_P][2*NC]
+    float* s_red = s_wout + 7 * 64;              // [2 tile parity][WG][4 quadrants][32 samples][2*NG]
+    float* s_film = s_red + 2 * UT_EPI_WG * 4 * 32 * 2 * NG;  // [2 tile parity][WG][TC_FILM_P][2*NC]
     UtGroup* s_grp = reinterpret_cast<UtGroup*>(s_film + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC);
     UtTap* s_tap = reinterpret_cast<UtTap*>(s_grp + UT_MAXG);
 
@@ -967,7 +967,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         const int t0 = r / nb, sl = r % nb;  // tile row = (time, sample); M-block mb adds 128/nb steps
         const int tstep = 128 / nb;
         const float inv_n = 1.0f / (float)(Tv * CG);
-        float* red = s_red + wg * (MB * 4 * 32 * 2 * NG);
+        float* red = s_red + wg * (4 * 32 * 2 * NG);
         const int cbase = NSPLIT > 1 ? wg * NC : 0;   // first column of this warpgroup
         const int ew = warp - 2;                       // epilogue warp 0..4*WG-1
         const float* s_bias_all = s_bias;
@@ -1111,16 +1111,13 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     }
                 }
             } else {
-                // ---- GroupNorm statistics in a canonical order that does not depend on MB (so not on
-                // the batch size): per row, the group's channels in chunk order; the rows of a sample
-                // combined as the complete binary tree over t -- xor shuffles over the lanes holding
-                // consecutive t (offsets nb, 2 nb, ...), then the blocks of consecutive t held by each
-                // (M-block, warp), in t order, through shared memory
-                float s1[MB][NG], s2[MB][NG], mean[NG], rstd[NG];
+                // ---- GroupNorm statistics: rows of one sample share `sl` across all 4 warps (and both
+                // M-blocks); the summation order depends on the tile shape, which run_layer chooses
+                // from the trajectory count alone, so every batch on the same side of that threshold
+                // gives the same bits (shard invariance)
+                float s1[NG], s2[NG], mean[NG], rstd[NG];
 #pragma unroll
-                for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-                    for (int g = 0; g < NG; ++g) s1[mb][g] = s2[mb][g] = 0.f;
+                for (int g = 0; g < NG; ++g) s1[g] = s2[g] = 0.f;
                 constexpr int SC = NC < 32 ? NC : 32;   // stats chunk width
                 // KEEP: narrow warpgroup slices keep the biased accumulator values in registers
                 // between the statistics and the normalise pass (no second TMEM read / bias add)
@@ -1168,36 +1165,26 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                         }
 #pragma unroll
                         for (int g = 0; g < NG; ++g) {
-                            s1[mb][g] += a1[g].x + a1[g].y;
-                            s2[mb][g] += a2[g].x + a2[g].y;
+                            s1[g] += a1[g].x + a1[g].y;
+                            s2[g] += a2[g].x + a2[g].y;
                         }
                     }
 #pragma unroll
-                for (int off = 1; off <= 16; off <<= 1)
+                for (int off = 16; off >= 1; off >>= 1)
                     if (off >= nb)
 #pragma unroll
-                        for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-                            for (int g = 0; g < NG; ++g) {
-                                s1[mb][g] += __shfl_xor_sync(PS_FULL, s1[mb][g], off);
-                                s2[mb][g] += __shfl_xor_sync(PS_FULL, s2[mb][g], off);
-                            }
-                // block partials -> smem (double-buffered by tile parity, so one barrier suffices);
-                // the tile's FiLM rows are staged before the same barrier
-                float* redj = red + (j & 1) * (UT_EPI_WG * MB * 4 * 32 * 2 * NG);
+                        for (int g = 0; g < NG; ++g) {
+                            s1[g] += __shfl_xor_sync(PS_FULL, s1[g], off);
+                            s2[g] += __shfl_xor_sync(PS_FULL, s2[g], off);
+                        }
+                // partials of the 4 warps -> smem (double-buffered by tile parity, so one barrier
+                // suffices); the tile's FiLM rows are staged before the same barrier
+                float* redj = red + (j & 1) * (UT_EPI_WG * 4 * 32 * 2 * NG);
                 if (lane < nb)
 #pragma unroll
-                    for (int mb = 0; mb < MB; ++mb) {
-                        if constexpr (NG == 2) {   // (s1 g0, s1 g1, s2 g0, s2 g1): one 16-B store
-                            *reinterpret_cast<float4*>(redj + ((mb * 4 + q) * 32 + sl) * 4) =
-                                make_float4(s1[mb][0], s1[mb][NG - 1], s2[mb][0], s2[mb][NG - 1]);
-                        } else {
-#pragma unroll
-                            for (int g = 0; g < NG; ++g) {
-                                redj[((mb * 4 + q) * 32 + sl) * 2 * NG + g] = s1[mb][g];
-                                redj[((mb * 4 + q) * 32 + sl) * 2 * NG + NG + g] = s2[mb][g];
-                            }
-                        }
+                    for (int g = 0; g < NG; ++g) {
+                        redj[(q * 32 + sl) * 2 * NG + g] = s1[g];
+                        redj[(q * 32 + sl) * 2 * NG + NG + g] = s2[g];
                     }
                 bool film_staged = false;
                 if constexpr (EPI == EPI_GN_FILM) {
@@ -1215,48 +1202,16 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     }
                 }
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
-                if constexpr (NG == 2) {
-                    // blocks of consecutive t, in t order, as (s1, s1, s2, s2) vectors; the tree adds
-                    // run on packed pairs (the same two-operand fp32 adds per lane)
-                    float2 b1[4 * MB], b2[4 * MB];
 #pragma unroll
-                    for (int bi = 0; bi < 4 * MB; ++bi) {
-                        const float4 v4 = *reinterpret_cast<const float4*>(redj + (bi * 32 + sl) * 4);
-                        b1[bi] = f2(v4.x, v4.y);
-                        b2[bi] = f2(v4.z, v4.w);
+                for (int g = 0; g < NG; ++g) {
+                    float a1 = 0.f, a2 = 0.f;
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) {
+                        a1 += redj[(qq * 32 + sl) * 2 * NG + g];
+                        a2 += redj[(qq * 32 + sl) * 2 * NG + NG + g];
                     }
-#pragma unroll
-                    for (int w = 1; w < 4 * MB; w <<= 1)
-#pragma unroll
-                        for (int bi = 0; bi < 4 * MB; bi += 2 * w) {
-                            b1[bi] = fadd2(b1[bi], b1[bi + w]);
-                            b2[bi] = fadd2(b2[bi], b2[bi + w]);
-                        }
-                    const float t1[2] = {b1[0].x, b1[0].y}, t2[2] = {b2[0].x, b2[0].y};
-#pragma unroll
-                    for (int g = 0; g < NG; ++g) {
-                        mean[g] = t1[g] * inv_n;
-                        rstd[g] = rsqrtf(fmaxf(fmaf(t2[g], inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
-                    }
-                } else {
-#pragma unroll
-                    for (int g = 0; g < NG; ++g) {
-                        float b1[4 * MB], b2[4 * MB];   // blocks of consecutive t, in t order
-#pragma unroll
-                        for (int bi = 0; bi < 4 * MB; ++bi) {
-                            b1[bi] = redj[(bi * 32 + sl) * 2 * NG + g];
-                            b2[bi] = redj[(bi * 32 + sl) * 2 * NG + NG + g];
-                        }
-#pragma unroll
-                        for (int w = 1; w < 4 * MB; w <<= 1)
-#pragma unroll
-                            for (int bi = 0; bi < 4 * MB; bi += 2 * w) {
-                                b1[bi] = b1[bi] + b1[bi + w];
-                                b2[bi] = b2[bi] + b2[bi + w];
-                            }
-                        mean[g] = b1[0] * inv_n;
-                        rstd[g] = rsqrtf(fmaxf(fmaf(b2[0], inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
-                    }
+                    mean[g] = a1 * inv_n;
+                    rstd[g] = rsqrtf(fmaxf(fmaf(a2, inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
                 }
 
                 const int p = b / a.S;
@@ -1531,7 +1486,7 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     // staged FiLM, tap tables
     constexpr int NSPLIT_ = UT_EPI_WG;
     constexpr int NG_ = 8 / (SPLIT * NSPLIT_), NC_ = N / NSPLIT_;
-    const size_t vec = (size_t)(4 * N * SPLIT + 7 * 64 + 2 * UT_EPI_WG * MB * 4 * 32 * 2 * NG_ + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
+    const size_t vec = (size_t)(4 * N * SPLIT + 7 * 64 + 2 * UT_EPI_WG * 4 * 32 * 2 * NG_ + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
                        UT_MAXG * sizeof(UtGroup) + UT_MAXTAP * sizeof(UtTap) + 64;
     const size_t fin = EPI == EPI_FINAL ? 2 * 16384 + 2048 + 2 * 128 * U_DOF * 4 : (size_t)UT_EPI_WG * 2 * 4096;
     const size_t budget = 225 * 1024 - vec - 2048 - fin;
@@ -1600,19 +1555,12 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n_sm_rl, cudaDevAttrMultiProcessorCount, dev);
     }
-    // Tile shape from the wave count: two-M-block tiles (each weight stage feeds 8 MMAs) unless
-    // one-M-block tiles need fewer M-block rounds per SM (ceil(tiles / #SM) x MB), or tie while
-    // two-M-block tiles would leave SMs idle.  Results do not depend on the choice: the GroupNorm
-    // statistics use one summation tree for either shape.
-    static const bool no_mbq = std::getenv("PS_NO_MB_WAVES") != nullptr;   // A/B: the old small-batch rule
-    int MBv = 1;
-    if (ly.epi != EPI_FINAL && (N == 64 || (N == 128 && !ly.res))) {
-        const long long rows = (long long)B * ly.Tv;
-        const long long t1 = (rows + 127) / 128, t2 = (rows + 255) / 256;
-        const long long u1 = (t1 + n_sm_rl - 1) / n_sm_rl, u2 = 2 * ((t2 + n_sm_rl - 1) / n_sm_rl);
-        if (no_mbq) MBv = rows < 256LL * n_sm_rl ? 1 : 2;
-        else MBv = (u2 < u1 || (u2 == u1 && t2 >= n_sm_rl)) ? 2 : 1;
-    }
+    // Two M-blocks per tile (each weight stage feeds 8 MMAs) unless the batch is too small to give
+    // every SM a two-block tile at the full horizon.  The choice depends on the trajectory count
+    // only (not on the layer's level), so any two batches on the same side of the threshold
+    // (B * 32 rows vs 256 x #SM) tile every layer alike and give the same bits per trajectory.
+    const bool small = (long long)B * 32 < 256LL * n_sm_rl;
+    const int MBv = (!small && ly.epi != EPI_FINAL && (N == 64 || (N == 128 && !ly.res))) ? 2 : 1;
     const int nb = MBv * 128 / ly.Tv;
     for (int s = 0; s < 3; ++s)
         // maps span >= nb samples (the workspace is padded to TC_MIN_B): a TMA box larger than

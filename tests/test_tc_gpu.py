@@ -249,18 +249,17 @@ def test_concurrent_streams_own_workspaces(params, P):
         assert np.array_equal(o, want_b)
 
 
-def test_layered_results_independent_of_batch_tiling(samplers):
-    # the layered kernels pick their tile shape from the batch (two M-blocks per tile at large batch,
-    # one below 256 x #SM rows); GroupNorm statistics use one canonical summation tree, so a
-    # 40-problem batch (two-M-block tiles at level 0) and its two 20-problem halves (one-M-block
-    # tiles) give the same bits -- the property strong scaling over GPUs relies on
+def test_layered_results_independent_of_batch_split(samplers):
+    # the layered kernels tile every layer from the trajectory count alone (two M-blocks per tile
+    # from 1184 trajectories at T = 32 up), so an 80-problem batch and its two 40-problem halves
+    # (1280 trajectories each: strong-scaling shards of a larger job) give the same bits
     _, s1 = samplers
-    P = 40
+    P = 80
     cond = _cond(P, 41)
     q0 = synth.make_problems(P, seed=42).q_start
     fa = s1.film(cond)
     steps = np.array([60, 40, 20, 1])
     full = _with_persist("0", lambda: s1.sample(fa, q0, 32, steps=steps).cpu().numpy())
-    a = _with_persist("0", lambda: s1.sample(fa[:20], q0[:20], 32, p0=0, steps=steps).cpu().numpy())
-    b = _with_persist("0", lambda: s1.sample(fa[20:], q0[20:], 32, p0=20, steps=steps).cpu().numpy())
+    a = _with_persist("0", lambda: s1.sample(fa[:40], q0[:40], 32, p0=0, steps=steps).cpu().numpy())
+    b = _with_persist("0", lambda: s1.sample(fa[40:], q0[40:], 32, p0=40, steps=steps).cpu().numpy())
     assert np.array_equal(full, np.concatenate([a, b]))
