@@ -652,27 +652,7 @@ struct UtArgs {
     float lo, hi;
     float* eps_out;
     int dbg;
-    // per-tile dependencies between consecutive layers (instead of a whole-grid wait): each
-    // epilogue warp adds 1 to cnt_out[tile] once its stores of the tile are complete; a tile of the
-    // next layer is loaded once cnt_in[t] reached in_expect for every previous-layer tile t holding
-    // its samples (in_nb samples per previous-layer tile).  cnt_in == nullptr: griddepcontrol.wait.
-    unsigned* cnt_out;
-    const unsigned* cnt_in;
-    int in_nb, in_expect;
 };
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-template <int N_PENDING>
-__device__ __forceinline__ void bulk_wait_group() {
-    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N_PENDING) : "memory");
-}
 
 // SW128 K-major descriptor for a matrix starting `row` rows into a 1024-B aligned slot
 // (measured on B200: the MMA applies the SW128 XOR pattern from absolute smem address
@@ -861,22 +841,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         pre = a.resident ? a.n_tap : (a.n_tap < SB ? a.n_tap : SB);
         for (int t = 0; t < pre; ++t) load_w(t, t, slice_of(0));
     }
-    if (a.cnt_in == nullptr) pdl_wait();
+    pdl_wait();
     pdl_launch_dependents();
-    // the previous layer's tiles holding the samples of tile `tile_`: wait until every epilogue
-    // warp that stores them has published (bounded: a tile that never publishes is a bug -- trap
-    // instead of hanging the GPU); then order the TMA reads after the acquire
-    auto wait_inputs = [&](int tile_) {
-        const int s0 = tile_ * nb, s1 = min(s0 + nb, a.B) - 1;
-        for (int t = s0 / a.in_nb; t <= s1 / a.in_nb; ++t) {
-            long long spins = 0;
-            while (ld_acquire_u32(a.cnt_in + t) < (unsigned)a.in_expect) {
-                if (++spins > (1LL << 26)) __trap();
-                __nanosleep(32);
-            }
-        }
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-    };
 
     if (warp == 0) {
         if (lane == 0) {
@@ -889,7 +855,6 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             int issued = 0;   // streamed weight boxes counted from the start of the kernel
             for (int j = 0; j < my_tiles; ++j) {
                 const int b0 = tile_of(j) * nb;
-                if (a.cnt_in) wait_inputs(tile_of(j));
                 for (int g = 0; g < n_grp; ++g) {
                     const UtGroup gr = s_grp[g];
                     mbar_wait(&a_empty[sa], pa ^ 1u);
@@ -1060,12 +1025,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             fence_proxy_async_smem();
             if (lane == 0) {
                 bulk_wait_read0();   // the other buffer's store has been read out: prefetch into it
-                if (slab + 1 < n_slab) {
-                    res_load(ob + 1, cur_tile, slab + 1, cur_noff);
-                } else if (j_ + 1 < my_tiles) {
-                    if (a.cnt_in) wait_inputs(tile_of(j_ + 1));
-                    res_load(ob + 1, tile_of(j_ + 1), 0, slice_of(j_ + 1) * N);
-                }
+                if (slab + 1 < n_slab) res_load(ob + 1, cur_tile, slab + 1, cur_noff);
+                else if (j_ + 1 < my_tiles) res_load(ob + 1, tile_of(j_ + 1), 0, slice_of(j_ + 1) * N);
             }
             __syncwarp();
             if (lane == 0) {
@@ -1074,10 +1035,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             }
             ++ob;
         };
-        if (IDRES && lane == 0 && my_tiles > 0) {
-            if (a.cnt_in) wait_inputs(tile_of(0));
-            res_load(0, tile_of(0), 0, slice_of(0) * N);
-        }
+        if (IDRES && lane == 0 && my_tiles > 0) res_load(0, tile_of(0), 0, slice_of(0) * N);
         // NSPLIT > 1: every warpgroup drains every tile; FINAL (NSPLIT 1): warpgroups 0/1
         // alternate tiles (one per TMEM buffer -- a third waiter would alias barrier phases)
         for (int j = 0; j < my_tiles; ++j) {
@@ -1468,24 +1426,9 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             if (lane == 0) {
                 if (PAIR && !leader) mbar_arrive_remote(leader_addr(&tempty[buf]));
                 else mbar_arrive(&tempty[buf]);
-                // publish the previous tile: its stores are complete once at most this tile's
-                // MB x NC/16 store groups are pending
-                if constexpr (!FIN) {
-                    if (a.cnt_out && j > 0) {
-                        bulk_wait_group<MB * (NC / 16)>();
-                        asm volatile("fence.proxy.async.global;" ::: "memory");
-                        red_release_add(a.cnt_out + tile_of(j - 1), 1u);
-                    }
-                }
             }
         }
-        if (!FIN && lane == 0) {
-            bulk_wait0();   // output stores complete before the grid ends
-            if (a.cnt_out && my_tiles > 0) {
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                red_release_add(a.cnt_out + tile_of(my_tiles - 1), 1u);
-            }
-        }
+        if (!FIN && lane == 0) bulk_wait0();   // output stores complete before the grid ends
     }
     __syncthreads();
     if constexpr (PAIR) {
@@ -1596,16 +1539,8 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
 }
 
 
-// per-tile dependencies of one layer launch (UtArgs::cnt_*); run_layer fills out_nb / out_expect
-struct TileDep {
-    unsigned* cnt_out = nullptr;
-    const unsigned* cnt_in = nullptr;
-    int in_nb = 1, in_expect = 0;
-    int out_nb = 1, out_expect = 0;
-};
-
 static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int B, int S, const float* film,
-                     float* x, const TcStep* step, float* eps_out, cudaStream_t st, TileDep* dep = nullptr) {
+                     float* x, const TcStep* step, float* eps_out, cudaStream_t st) {
     UtArgs a;
     memset(&a, 0, sizeof(a));
     const PConv& c = *ly.c;
@@ -1646,14 +1581,6 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
     const bool tiny = 2LL * ((long long)B * ly.Tv + 127) / 128 <= n_sm_rl;   // both slices still fit on the SMs
     const int split = (!no_split && tiny && N >= 128 && ly.epi != EPI_FINAL) ? 2 : 1;
     const int wrows = N / split / (pair ? 2 : 1);
-    if (dep) {
-        a.cnt_out = ly.epi == EPI_FINAL ? nullptr : dep->cnt_out;
-        a.cnt_in = dep->cnt_in;
-        a.in_nb = dep->in_nb;
-        a.in_expect = dep->in_expect;
-        dep->out_nb = nb;
-        dep->out_expect = UT_EPI_WG * 4 * split;   // epilogue warps storing each tile
-    }
     if (!make_w_map(&a.tmW, W + c.w_off, N, (int)kpad(c.K), wrows)) return PS_FAIL(PS_ERR_CUDA);
     if (ly.epi != EPI_FINAL && !make_out_map(&a.tmO, ly.out, std::max(B, nb), ly.Tv, N, nb))
         return PS_FAIL(PS_ERR_CUDA);
@@ -1768,13 +1695,10 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
 
 constexpr int TC_MIN_B = 64;   // activation slots are padded to at least this many samples
 
-constexpr int TC_MAX_LAYERS = 32;
-static size_t tc_cnt_stride(int B) { return (size_t)std::max(B, TC_MIN_B) / 2 + 64; }   // >= tiles of any layer
-
 size_t tc_workspace_bytes(int B, int T) {
     const size_t Bp = (size_t)std::max(B, TC_MIN_B);
     const size_t slot = Bp * T * 128 * 2;
-    return Bp * T * 64 * 2 + 5 * slot + (size_t)B * 3584 * 4 + (size_t)TC_MAX_LAYERS * tc_cnt_stride(B) * 4 + 4096;
+    return Bp * T * 64 * 2 + 5 * slot + (size_t)B * 3584 * 4 + 4096;
 }
 
 #define PS_TRY_TC(x)        \
@@ -1794,8 +1718,6 @@ UnetSlots unet_slots(void* ws, int B, int T) {
     u.skip1 = u.h + slot;
     u.skip2 = u.skip1 + slot;
     u.film = reinterpret_cast<float*>(u.skip2 + slot);
-    u.cnt = reinterpret_cast<unsigned*>(u.film + (size_t)B * 3584);
-    u.cnt_stride = tc_cnt_stride(B);
     return u;
 }
 
@@ -1897,25 +1819,9 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
     }
     std::vector<TcLayer> layers;
     unet_layer_list(L, T, u, true, layers);
-    // per-tile dependencies between consecutive layers (PS_NO_TILE_DEPS=1: whole-grid waits, A/B)
-    static const bool no_deps = std::getenv("PS_NO_TILE_DEPS") != nullptr;
-    const bool deps = !no_deps && (int)layers.size() <= TC_MAX_LAYERS;
-    if (deps && cudaMemsetAsync(u.cnt, 0, layers.size() * u.cnt_stride * sizeof(unsigned), st) != cudaSuccess)
-        return PS_FAIL(PS_ERR_CUDA);
-    TileDep dep;
-    for (size_t i = 0; i < layers.size(); ++i) {
-        const TcLayer& ly = layers[i];
+    for (const TcLayer& ly : layers) {
         const bool fin = ly.epi == EPI_FINAL;
-        TileDep* dp = nullptr;
-        if (deps) {
-            dep.cnt_in = i > 0 ? u.cnt + (i - 1) * u.cnt_stride : nullptr;
-            dep.in_nb = dep.out_nb;
-            dep.in_expect = dep.out_expect;
-            dep.cnt_out = u.cnt + i * u.cnt_stride;
-            dp = &dep;
-        }
-        PS_TRY_TC(run_layer(L, packed, ly, B, S, u.film, x, fin ? step : nullptr, fin && !step ? eps : nullptr, st,
-                            dp));
+        PS_TRY_TC(run_layer(L, packed, ly, B, S, u.film, x, fin ? step : nullptr, fin && !step ? eps : nullptr, st));
     }
     return PS_OK;
 }

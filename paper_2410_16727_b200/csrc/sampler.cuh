@@ -68,8 +68,6 @@ struct TcLayer {
 struct UnetSlots {
     __nv_bfloat16 *a0, *cur, *nxt, *h, *skip1, *skip2;
     float* film;
-    unsigned* cnt;      // per-(layer, tile) publish counters of the layered forward
-    size_t cnt_stride;  // counters per layer
 };
 UnetSlots unet_slots(void* ws, int B, int T);
 void unet_layer_list(const Layout& L, int T, const UnetSlots& u, bool split_res256, std::vector<TcLayer>& out);
