@@ -258,3 +258,26 @@ def test_checkpoint_loaded_planner_is_bitwise_identical(torch_cuda, params, tmp_
         pb.images, pb.q_start, pb.goal, pb.boxes, p0=pb.p0)
     for f in ("trajectories", "cost", "feasible", "best_index"):
         assert np.array_equal(np.asarray(getattr(a, f)), np.asarray(getattr(b, f))), f
+
+
+def test_bf16_layered_pipeline_horizon64(torch_cuda, params, oracle_lib):
+    """Config-4 horizon (T = 64, two waypoints per lane in the refinement): 16 problems x 32 seeds run
+    the layered kernels (B*T = 32768); refinement of the GPU's seeds bit-exact against the C
+    oracle, seeds of one problem within the T = 64 bf16 bound (0.2 rad max, 2e-2 RMS)."""
+    from paper_2410_16727_b200.planner import BLPlanner
+    P = 16
+    pl = BLPlanner(params, ENC, mode=1, S=S, T=64, max_problems=P)
+    pb = synth.config3_problems(P, p0=500, seed=0)
+    host = pl.plan_batch(pb.images, pb.q_start, pb.goal, pb.boxes, p0=pb.p0)
+    seeds = pl.seeds[:P * S].cpu().numpy()
+    assert seeds.shape == (P * S, 64, 7) and np.isfinite(seeds).all()
+    e = _unbrick(pl, P)
+    ps = oracle_lib.BLProblemSet(pl.robot, pl.grid, pl.cost, e, pl.grid.n_nodes)
+    q, c, f, cl = oracle_lib.bl_refine(ps, seeds, S, pl.cost.n_iters)
+    assert np.array_equal(np.asarray(host.trajectories), q)
+    assert np.array_equal(np.asarray(host.cost), c)
+    assert np.array_equal(np.asarray(host.best_index), oracle_lib.select(c, f, S))
+    cond = un.encode_problems(params, ENC, pb.images[:1], pb.q_start[:1], pb.goal[:1])
+    want = un.sample(params, ARCH, cond, pb.q_start[:1], S, T=64, problems=np.array([pb.p0]))
+    d = seeds[:S] - want
+    assert np.sqrt((d ** 2).mean()) < 2e-2 and np.abs(d).max() < 0.2
