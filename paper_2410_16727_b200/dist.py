@@ -65,7 +65,7 @@ def plan_sharded(planner, images, q_start, goal, boxes, p0: int, rank: int, worl
     from .planner import PlanBatchResult
 
     d = planner.upload(images, q_start, goal, boxes)
-    r = planner.plan_batch_device(*d, p0=p0, images_ready=planner._img_ev)
+    r = planner.plan_batch_device(*d, p0=p0, images_ready=planner._img_chunks)
     S = planner.S
     per = [(rr + 1) * total // world - rr * total // world for rr in range(world)]
     cnt = [[n * S for n in per]] * 3 + [per]

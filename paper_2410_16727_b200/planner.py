@@ -86,6 +86,7 @@ class BLPlanner:
                     torch.empty(B, dtype=torch.uint8, device=dev))
         self.best = torch.empty(self.Pmax, dtype=torch.int32, device=dev)
         self.film_a = torch.empty((self.Pmax, 3584), dtype=torch.float32, device=dev)
+        self.cond = torch.empty((self.Pmax, spec.COND_DIM), dtype=torch.float32, device=dev)
         # device copies of host inputs for the end-to-end path
         self.d_images = torch.empty((self.Pmax, n_images) + tuple(image_shape), dtype=torch.float32,
                                     device=dev)
@@ -107,8 +108,9 @@ class BLPlanner:
         """All inputs already on the device.  Returns PlanBatchResult of device tensors.
         `events` (optional dict of CUDA events) records "sample_start"/"sample_end" around the
         sampler and, when present, "refine_start"/"refine_end" around the refinement;
-        `images_ready` (optional CUDA event) is waited on before the encoder, so an image
-        upload on another stream overlaps the ESDF build."""
+        `images_ready` (optional CUDA event, or a list of (event, p_begin, p_end) chunks) is waited on
+        before the encoder -- chunk by chunk, so an image upload on another stream overlaps the ESDF
+        build and the encoding of the chunks that already arrived."""
         torch = _lib.require_cuda()
         P = int(q_start.shape[0])
         if P > self.Pmax:
@@ -116,9 +118,15 @@ class BLPlanner:
         B = P * self.S
         esdf = self.esdf[:P]
         self._esdf_build(boxes, esdf)
-        if images_ready is not None:
-            torch.cuda.current_stream().wait_event(images_ready)
-        cond = self.sampler.encode(images, q_start, goal)
+        if isinstance(images_ready, (list, tuple)):
+            cond = self.cond[:P]
+            for ev, c0, c1 in images_ready:
+                torch.cuda.current_stream().wait_event(ev)
+                self.sampler.encode(images[c0:c1], q_start[c0:c1], goal[c0:c1], out=cond[c0:c1])
+        else:
+            if images_ready is not None:
+                torch.cuda.current_stream().wait_event(images_ready)
+            cond = self.sampler.encode(images, q_start, goal, out=self.cond[:P])
         fa = self.sampler.film(cond, out=self.film_a[:P])
         if events is not None:
             events["sample_start"].record()
@@ -152,10 +160,11 @@ class BLPlanner:
         bl.esdf_build(boxes, self.grid, layout=self.esdf_layout, out=out)
 
     # ------------------------------------------------------------------ host
-    def upload(self, images, q_start, goal, boxes):
+    def upload(self, images, q_start, goal, boxes, n_chunks: int = 4):
         """Host (ideally pinned) arrays -> this planner's device input buffers.  The small inputs go
-        on the current stream; the image upload runs on a side stream (its completion event is
-        self._img_ev), overlapped with the ESDF build.  Returns the device views."""
+        on the current stream; the images go on a side stream in `n_chunks` problem chunks, each with
+        its completion event (self._img_chunks: [(event, p_begin, p_end)]), so the ESDF build and
+        the encoding of arrived chunks overlap the rest of the upload.  Returns the device views."""
         torch = _lib.require_cuda()
         P = int(q_start.shape[0])
         if P > self.Pmax:
@@ -164,13 +173,21 @@ class BLPlanner:
         main = torch.cuda.current_stream()
         if not hasattr(self, "_copy_stream"):
             self._copy_stream = torch.cuda.Stream()
-            self._img_ev = torch.cuda.Event()
+            self._img_evs = []
+        n_chunks = max(1, min(int(n_chunks), P))
+        while len(self._img_evs) < n_chunks:
+            self._img_evs.append(torch.cuda.Event())
         for dst, src in ((d_q, q_start), (d_g, goal), (d_b, boxes)):
             dst.copy_(torch.as_tensor(src), non_blocking=True)
         self._copy_stream.wait_stream(main)          # buffers free from the previous call
+        h_im = torch.as_tensor(images)
+        self._img_chunks = []
         with torch.cuda.stream(self._copy_stream):
-            d_im.copy_(torch.as_tensor(images), non_blocking=True)
-            self._img_ev.record()
+            for i in range(n_chunks):
+                c0, c1 = i * P // n_chunks, (i + 1) * P // n_chunks
+                d_im[c0:c1].copy_(h_im[c0:c1], non_blocking=True)
+                self._img_evs[i].record()
+                self._img_chunks.append((self._img_evs[i], c0, c1))
         return d_im, d_q, d_g, d_b
 
     def plan_batch(self, images, q_start, goal, boxes, p0: int = 0, events=None):
@@ -178,7 +195,7 @@ class BLPlanner:
         pipeline, and a D2H read of trajectories, costs, flags and best indices."""
         torch = _lib.require_cuda()
         d = self.upload(images, q_start, goal, boxes)
-        r = self.plan_batch_device(*d, p0=p0, images_ready=self._img_ev, events=events)
+        r = self.plan_batch_device(*d, p0=p0, images_ready=self._img_chunks, events=events)
         host = PlanBatchResult(r.trajectories.to("cpu", non_blocking=True), None,
                                r.cost.to("cpu", non_blocking=True),
                                r.feasible.to("cpu", non_blocking=True),

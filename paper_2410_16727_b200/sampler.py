@@ -80,8 +80,9 @@ class SeedSampler:
             self._encp[key] = buf
         return self._encp[key]
 
-    def encode(self, images, q_start, goal, stream=None):
-        """images (P, n_img, H, W) depth metres; q_start (P,7); goal (P,7) -> cond (P,270).
+    def encode(self, images, q_start, goal, stream=None, out=None):
+        """images (P, n_img, H, W) depth metres; q_start (P,7); goal (P,7) -> cond (P,270)
+        (written into `out` when given).
 
         mode 1 runs the tcgen05 encoder (bf16 activations), mode 0 the fp32 SIMT one."""
         torch = _lib.require_cuda()
@@ -96,7 +97,7 @@ class SeedSampler:
             nb = int(L.ps_encode_tc_workspace_bytes(P * n_img, H, W, nl))
             if getattr(self, "_encws", None) is None or self._encws.numel() < nb:
                 self._encws = torch.empty(nb, dtype=torch.uint8, device="cuda")
-            cond = torch.empty((P, spec.COND_DIM), dtype=torch.float32, device="cuda")
+            cond = out if out is not None else torch.empty((P, spec.COND_DIM), dtype=torch.float32, device="cuda")
             st = L.ps_encode_tc(_lib.ptr(im), P, n_img, H, W, _lib.ptr(packed), nl, _lib.ptr(q),
                                 _lib.ptr(g), -spec.JOINT_LIMIT, spec.JOINT_LIMIT, _lib.ptr(self._encws),
                                 _lib.ptr(cond), _lib.stream_handle(stream))
@@ -104,7 +105,7 @@ class SeedSampler:
             return cond
         ws = torch.empty(int(L.ps_encode_workspace_bytes(P * n_img, H, W, nl)), dtype=torch.uint8,
                          device="cuda")
-        cond = torch.empty((P, spec.COND_DIM), dtype=torch.float32, device="cuda")
+        cond = out if out is not None else torch.empty((P, spec.COND_DIM), dtype=torch.float32, device="cuda")
         st = L.ps_encode(_lib.ptr(im), P, n_img, H, W, _lib.ptr(self.enc_w), nl, _lib.ptr(q),
                          _lib.ptr(g), -spec.JOINT_LIMIT, spec.JOINT_LIMIT, _lib.ptr(ws),
                          _lib.ptr(cond), _lib.stream_handle(stream))
