@@ -8,7 +8,6 @@ pointers plus sizes; torch is only the allocator and stream provider.
 from __future__ import annotations
 
 import ctypes
-from pathlib import Path
 
 import numpy as np
 

@@ -12,7 +12,7 @@ the reference line for line, as the sampler drop-in does."""
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Callable, Dict, List, Optional, Sequence
+from typing import Callable, List, Optional, Sequence
 
 import numpy as np
 

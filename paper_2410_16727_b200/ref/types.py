@@ -6,7 +6,7 @@ kernels read).  These are data containers and input adapters, not compute."""
 from __future__ import annotations
 
 from dataclasses import dataclass, field
-from typing import Optional, Tuple
+from typing import Tuple
 
 import numpy as np
 
