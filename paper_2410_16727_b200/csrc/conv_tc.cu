@@ -620,6 +620,12 @@ struct UtTap {
 
 constexpr int UT_EPI_WG = 4;                       // U-Net epilogue warpgroups
 constexpr int UT_THREADS = 64 + 128 * UT_EPI_WG;
+// GroupNorm partials in shared memory: [2 tile parity][WG][4 quadrants][32 samples][2 * NG];
+// FINAL (one warpgroup per tile, all 8 groups): [WG][4 quadrants][32 samples][16]
+template <int EPI, int NG>
+__host__ __device__ constexpr int ut_red_floats() {
+    return EPI == EPI_FINAL ? UT_EPI_WG * 4 * 32 * 16 : 2 * UT_EPI_WG * 4 * 32 * 2 * NG;
+}
 
 struct UtArgs {
     CUtensorMap tmA[3];
@@ -713,22 +719,22 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     const int SA = a.sa_stages, SB = a.sb_stages;
     uint8_t* sA = smem;
     uint8_t* sB = smem + (size_t)SA * A_BYTES;
-    // FINAL only: projection A tiles [2][128 x 64] bf16 SW128, W_out^T [16 x 64] bf16 SW128,
-    // per-tile noise [2][128 x 7]
+    // FINAL only: per epilogue warpgroup a projection A tile [128 x 64] bf16 SW128 and the
+    // tile's noise [128 x 7]; W_out^T [16 x 64] bf16 SW128
     uint8_t* sP = sB + (size_t)SB * B_BYTES;
-    uint8_t* sWo = sP + (FIN ? 2 * 16384 : 0);
+    uint8_t* sWo = sP + (FIN ? UT_EPI_WG * 16384 : 0);
     float* sZ = reinterpret_cast<float*>(sWo + (FIN ? 2048 : 0));
     // output staging (non-FINAL): per warpgroup two [128 rows x 16 ch] bf16 buffers that
     // TMA-store 16-channel column slabs of the tile (coalesced writes off the LSU path)
-    uint8_t* sOut = reinterpret_cast<uint8_t*>(sZ) + (FIN ? 2 * 128 * U_DOF * 4 : 0);
+    uint8_t* sOut = reinterpret_cast<uint8_t*>(sZ) + (FIN ? UT_EPI_WG * 128 * U_DOF * 4 : 0);
     uint64_t* a_full = reinterpret_cast<uint64_t*>(sOut + (FIN ? 0 : UT_EPI_WG * 2 * 4096));
     uint64_t* a_empty = a_full + SA;
     uint64_t* b_full = a_empty + SA;
     uint64_t* b_empty = b_full + SB;
     uint64_t* tfull = b_empty + SB;
     uint64_t* tempty = tfull + 4;
-    uint64_t* pbar = tempty + 4;                 // FINAL: projection MMA done
-    uint64_t* rbar = pbar + 2;                   // identity residual slabs: [epilogue warp][2]
+    uint64_t* pbar = tempty + 4;                 // FINAL: projection MMA done, per warpgroup
+    uint64_t* rbar = pbar + 4;                   // identity residual slabs: [epilogue warp][2]
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(rbar + 8 * UT_EPI_WG);
     float* s_bias = reinterpret_cast<float*>(tmem_holder + 4);
     float* s_gamma = s_bias + NF;
@@ -736,7 +742,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     float* s_rbias = s_beta + NF;
     float* s_wout = s_rbias + NF;                // [7][64]
     float* s_red = s_wout + 7 * 64;              // [2 tile parity][WG][4 quadrants][32 samples][2*NG]
-    float* s_film = s_red + 2 * UT_EPI_WG * 4 * 32 * 2 * NG;  // [2 tile parity][WG][TC_FILM_P][2*NC]
+    float* s_film = s_red + ut_red_floats<EPI, NG>();  // [2 tile parity][WG][TC_FILM_P][2*NC]
     UtGroup* s_grp = reinterpret_cast<UtGroup*>(s_film + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC);
     UtTap* s_tap = reinterpret_cast<UtTap*>(s_grp + UT_MAXG);
 
@@ -769,9 +775,10 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         }
         for (int b = 0; b < 4; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], (PAIR ? 2 : 1) * 4 * NSPLIT);   // one arrival per epilogue warp (both CTAs)
+            // one arrival per epilogue warp (both CTAs); FINAL: the 4 warps of the tile's warpgroup
+            mbar_init(&tempty[b], FIN ? 4 : (PAIR ? 2 : 1) * 4 * NSPLIT);
         }
-        mbar_init(pbar, 1);
+        for (int i = 0; i < 4; ++i) mbar_init(&pbar[i], 1);
         for (int i = 0; i < 8 * UT_EPI_WG; ++i) mbar_init(&rbar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmA[0]) : "memory");
@@ -959,6 +966,177 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             }
         }
         __syncwarp();
+    } else if constexpr (FIN) {
+        // ======================= final-layer epilogue =======================
+        // Warpgroup w drains the CTA's tiles j = w, w + 4, ... alone: all 64 channels of its
+        // 128 rows (TMEM buffer w), Mish(GN(acc + bias)) as a bf16 SW128 tile in its own smem
+        // buffer, the 64->7 projection as one M128 x N16 tcgen05 MMA into its own 16 TMEM
+        // columns (its own barrier), then x0 clip + DDPM posterior / DDIM / denormalise for its
+        // rows.  No barrier spans warpgroups, so four tiles' epilogues overlap.  The statistics
+        // keep the summation order of the channel-split epilogue (per 8-channel group: packed
+        // pair sums, then the time shuffles, then the 4 quadrants in order).
+        static_assert(N == 64 && MB == 1 && NBUF == 4 && UT_EPI_WG == 4 && CG == 8, "final layer shape");
+        const int wg = (warp - 2) >> 2;
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        const int t = r / nb, sl = r % nb;
+        const float inv_n = 1.0f / (float)(Tv * CG);
+        float* red = s_red + wg * (4 * 32 * 16);
+        uint8_t* sPw = sP + wg * 16384;
+        float* sZw = sZ + wg * (128 * U_DOF);
+        const uint32_t t_lane0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(wg * ACC);
+        const uint32_t pcol = (uint32_t)(PROJ_COL + 16 * wg);
+        const StepCoef sc = a.sc;
+        const bool noisy = !a.eps_out && !sc.last && sc.ddpm;
+        const int per = Tv * U_DOF / 4;   // Philox blocks per sample
+        int it = 0;
+        for (int j = wg; j < my_tiles; j += 4, ++it) {
+            const int tile = tile_of(j);
+            const int b = tile * nb + sl;
+            const bool valid = b < a.B;
+            mbar_wait(&tfull[wg], (uint32_t)it & 1u);
+            tc_fence_after();
+            if (a.dbg & 1) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[wg]);
+                continue;
+            }
+            float s1[8], s2[8];
+#pragma unroll
+            for (int cc = 0; cc < 64; cc += 16) {
+                uint32_t rr[16];
+                tmem_ld16(t_lane0 + cc, rr);
+                tmem_wait_ld();
+                float2 a1[2], a2[2];
+#pragma unroll
+                for (int g = 0; g < 2; ++g) a1[g] = a2[g] = f2(0.f, 0.f);
+#pragma unroll
+                for (int jj = 0; jj < 16; jj += 2) {
+                    const int g = jj / 8;
+                    const float2 bb = *reinterpret_cast<const float2*>(s_bias + cc + jj);
+                    const float2 xv = fadd2(f2(__uint_as_float(rr[jj]), __uint_as_float(rr[jj + 1])), bb);
+                    a1[g] = fadd2(a1[g], xv);
+                    a2[g] = ffma2(xv, xv, a2[g]);
+                }
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {
+                    s1[cc / 8 + g] = 0.f + (a1[g].x + a1[g].y);
+                    s2[cc / 8 + g] = 0.f + (a2[g].x + a2[g].y);
+                }
+            }
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1)
+                if (off >= nb)
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) {
+                        s1[g] += __shfl_xor_sync(PS_FULL, s1[g], off);
+                        s2[g] += __shfl_xor_sync(PS_FULL, s2[g], off);
+                    }
+            if (lane < nb) {
+                float4* rp = reinterpret_cast<float4*>(red + (q * 32 + sl) * 16);
+                rp[0] = make_float4(s1[0], s1[1], s1[2], s1[3]);
+                rp[1] = make_float4(s1[4], s1[5], s1[6], s1[7]);
+                rp[2] = make_float4(s2[0], s2[1], s2[2], s2[3]);
+                rp[3] = make_float4(s2[4], s2[5], s2[6], s2[7]);
+            }
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+            float mean[8], rstd[8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                float a1 = 0.f, a2 = 0.f;
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                    a1 += red[(qq * 32 + sl) * 16 + g];
+                    a2 += red[(qq * 32 + sl) * 16 + 8 + g];
+                }
+                mean[g] = a1 * inv_n;
+                rstd[g] = rsqrtf(fmaxf(fmaf(a2, inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
+            }
+            // y = Mish(GN(acc + bias)) -> bf16 projection tile (row r: 128 B, SW128)
+#pragma unroll
+            for (int cc = 0; cc < 64; cc += 16) {
+                uint32_t rr[16];
+                tmem_ld16(t_lane0 + cc, rr);
+                tmem_wait_ld();
+                __align__(16) __nv_bfloat162 pk[8];
+#pragma unroll
+                for (int jj = 0; jj < 16; jj += 2) {
+                    float yv[2];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int c = cc + jj + u;
+                        const int g = c / 8;
+                        const float xv = __uint_as_float(rr[jj + u]) + s_bias[c];
+                        const float tt = fmaf(xv, rstd[g], -mean[g] * rstd[g]);
+                        yv[u] = mish8(fmaf(tt, s_gamma[c], s_beta[c]));
+                    }
+                    pk[jj / 2] = __floats2bfloat162_rn(yv[0], yv[1]);
+                }
+                const int jc = cc >> 3;
+                *reinterpret_cast<uint4*>(sPw + r * 128 + (((jc) ^ (r & 7)) << 4)) = *reinterpret_cast<const uint4*>(&pk[0]);
+                *reinterpret_cast<uint4*>(sPw + r * 128 + (((jc + 1) ^ (r & 7)) << 4)) = *reinterpret_cast<const uint4*>(&pk[4]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[wg]);   // accumulator drained: tile j + 4's MMAs may start
+            if (noisy) {
+                // the tile's Philox blocks (nb samples x Tv*7/4)
+                for (int i = r; i < nb * per; i += 128) {
+                    const int s2_ = i / per, blk = i - s2_ * per;
+                    const int b2 = tile * nb + s2_;
+                    float n4[4] = {0.f, 0.f, 0.f, 0.f};
+                    if (b2 < a.B)
+                        normal4_tc((uint32_t)sc.k, (uint32_t)(a.p0 + b2 / a.S), (uint32_t)(b2 % a.S), (uint32_t)blk, a.key, n4);
+                    *reinterpret_cast<float4*>(sZw + s2_ * Tv * U_DOF + blk * 4) = make_float4(n4[0], n4[1], n4[2], n4[3]);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+            if (threadIdx.x == 64 + 128 * wg) {
+                tc_fence_after();
+                constexpr uint32_t idp = idesc_bf16(128, 16);
+                const uint64_t dP = umma_desc_sw128(sPw), dW = umma_desc_sw128(sWo);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    umma_bf16(tmem_base + pcol, dP + (uint64_t)(kk * 2), dW + (uint64_t)(kk * 2), idp, kk > 0 ? 1u : 0u);
+                umma_commit(&pbar[wg]);
+            }
+            __syncwarp();
+            mbar_wait(&pbar[wg], (uint32_t)it & 1u);
+            tc_fence_after();
+            uint32_t pr[16];
+            tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + pcol, pr);
+            tmem_wait_ld();
+            float eps[U_DOF];
+#pragma unroll
+            for (int d = 0; d < U_DOF; ++d) eps[d] = __uint_as_float(pr[d]) + s_wout[d];
+            if (valid) {
+                const int grow = b * Tv + t;
+                const int p = b / a.S;
+                float* xr = a.x + (size_t)grow * U_DOF;
+                if (a.eps_out) {
+#pragma unroll
+                    for (int d = 0; d < U_DOF; ++d) a.eps_out[(size_t)grow * U_DOF + d] = eps[d];
+                } else {
+                    const float* zr = sZw + sl * Tv * U_DOF + t * U_DOF;
+#pragma unroll
+                    for (int d = 0; d < U_DOF; ++d) {
+                        const float xv = xr[d];
+                        float x0 = (xv - sc.sq1m * eps[d]) * sc.rsq;
+                        x0 = fminf(fmaxf(x0, -0.1f), 1.1f);
+                        if (sc.last) {
+                            a.traj[(size_t)grow * U_DOF + d] =
+                                (t == 0) ? a.q_start[(size_t)p * U_DOF + d] : a.lo + x0 * (a.hi - a.lo);
+                        } else if (sc.ddpm) {
+                            xr[d] = sc.c0 * x0 + sc.c1 * xv + sc.sig * zr[d];
+                        } else {
+                            xr[d] = sc.sqn * x0 + sc.sq1mn * eps[d];
+                        }
+                    }
+                }
+            }
+        }
     } else {
         // ============================ epilogue ============================
         const int wg = (warp - 2) >> 2;
@@ -1036,8 +1214,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             ++ob;
         };
         if (IDRES && lane == 0 && my_tiles > 0) res_load(0, tile_of(0), 0, slice_of(0) * N);
-        // NSPLIT > 1: every warpgroup drains every tile; FINAL (NSPLIT 1): warpgroups 0/1
-        // alternate tiles (one per TMEM buffer -- a third waiter would alias barrier phases)
+        // every warpgroup drains every tile (its N / 4 channels)
         for (int j = 0; j < my_tiles; ++j) {
             const int tile = tile_of(j);
             cur_tile = tile;
@@ -1215,107 +1392,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                 }
 
                 const int p = b / a.S;
-                if constexpr (EPI == EPI_FINAL) {
-                    static_assert(N == 64 && NC % 16 == 0 && MB == 1, "final layer has 64 channels");
-                    const int t = t0;
-                    const int grow = b * Tv + t;
-                    uint8_t* sPb = sP + (j & 1) * 16384;
-                    float* sZb = sZ + (j & 1) * (128 * U_DOF);
-                    // y = Mish(GN(acc + bias)) for this warpgroup's 32 channels -> bf16 projection tile
-#pragma unroll
-                    for (int cc = 0; cc < NC; cc += 16) {
-                        const int c0 = cbase + cc;
-                        uint32_t rr[16];
-                        tmem_ld16(t_lane0 + cc, rr);
-                        tmem_wait_ld();
-                        const int gi = cc / CG;
-                        __align__(16) __nv_bfloat162 pk[8];
-#pragma unroll
-                        for (int jj = 0; jj < 16; jj += 2) {
-                            float yv[2];
-#pragma unroll
-                            for (int u = 0; u < 2; ++u) {
-                                const int c = c0 + jj + u;
-                                const int g = gi + (jj + u) / CG;
-                                const float xv = __uint_as_float(rr[jj + u]) + s_bias[c];
-                                const float tt = fmaf(xv, sel(rstd, g), -sel(mean, g) * sel(rstd, g));
-                                yv[u] = mish8(fmaf(tt, s_gamma[c], s_beta[c]));
-                            }
-                            pk[jj / 2] = __floats2bfloat162_rn(yv[0], yv[1]);
-                        }
-                        const int jc = c0 >> 3;
-                        *reinterpret_cast<uint4*>(sPb + r * 128 + (((jc) ^ (r & 7)) << 4)) =
-                            *reinterpret_cast<const uint4*>(&pk[0]);
-                        *reinterpret_cast<uint4*>(sPb + r * 128 + (((jc + 1) ^ (r & 7)) << 4)) =
-                            *reinterpret_cast<const uint4*>(&pk[4]);
-                    }
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[buf]);   // accumulator drained: the next tile's MMAs may start
-                    const StepCoef sc = a.sc;
-                    const bool noisy = !a.eps_out && !sc.last && sc.ddpm;
-                    if (noisy) {
-                        // the tile's Philox blocks (nb samples x Tv*7/4), spread over both warpgroups
-                        const int per = Tv * U_DOF / 4;
-                        for (int i = threadIdx.x - 64; i < nb * per; i += 128 * UT_EPI_WG) {
-                            const int s2 = i / per, blk = i - s2 * per;
-                            const int b2 = tile * nb + s2;
-                            float n4[4] = {0.f, 0.f, 0.f, 0.f};
-                            if (b2 < a.B)
-                                normal4_tc((uint32_t)sc.k, (uint32_t)(a.p0 + b2 / a.S), (uint32_t)(b2 % a.S),
-                                           (uint32_t)blk, a.key, n4);
-                            *reinterpret_cast<float4*>(sZb + s2 * Tv * U_DOF + blk * 4) =
-                                make_float4(n4[0], n4[1], n4[2], n4[3]);
-                        }
-                    }
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    asm volatile("bar.sync 5, %0;" ::"r"(128 * UT_EPI_WG) : "memory");
-                    if (wg == 0) {
-                        if (threadIdx.x == 64) {
-                            tc_fence_after();
-                            constexpr uint32_t idp = idesc_bf16(128, 16);
-                            const uint64_t dP = umma_desc_sw128(sPb), dW = umma_desc_sw128(sWo);
-#pragma unroll
-                            for (int kk = 0; kk < 4; ++kk)
-                                umma_bf16(tmem_base + (uint32_t)PROJ_COL, dP + (uint64_t)(kk * 2),
-                                          dW + (uint64_t)(kk * 2), idp, kk > 0 ? 1u : 0u);
-                            umma_commit(pbar);
-                        }
-                        __syncwarp();
-                        mbar_wait(pbar, (uint32_t)j & 1u);
-                        tc_fence_after();
-                        uint32_t pr[16];
-                        tmem_ld16(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)PROJ_COL, pr);
-                        tmem_wait_ld();
-                        float eps[U_DOF];
-#pragma unroll
-                        for (int d = 0; d < U_DOF; ++d) eps[d] = __uint_as_float(pr[d]) + s_wout[d];
-                        if (valid) {
-                            float* xr = a.x + (size_t)grow * U_DOF;
-                            if (a.eps_out) {
-#pragma unroll
-                                for (int d = 0; d < U_DOF; ++d) a.eps_out[(size_t)grow * U_DOF + d] = eps[d];
-                            } else {
-                                const float* zr = sZb + sl * Tv * U_DOF + t * U_DOF;
-#pragma unroll
-                                for (int d = 0; d < U_DOF; ++d) {
-                                    const float xv = xr[d];
-                                    float x0 = (xv - sc.sq1m * eps[d]) * sc.rsq;
-                                    x0 = fminf(fmaxf(x0, -0.1f), 1.1f);
-                                    if (sc.last) {
-                                        a.traj[(size_t)grow * U_DOF + d] =
-                                            (t == 0) ? a.q_start[(size_t)p * U_DOF + d] : a.lo + x0 * (a.hi - a.lo);
-                                    } else if (sc.ddpm) {
-                                        xr[d] = sc.c0 * x0 + sc.c1 * xv + sc.sig * zr[d];
-                                    } else {
-                                        xr[d] = sc.sqn * x0 + sc.sq1mn * eps[d];
-                                    }
-                                }
-                            }
-                        }
-                    }
-                    continue;   // tempty already released
-                } else {
+                {
                     // per-tile FiLM rows staged as (1 + scale, shift) for this warpgroup's columns
                     const float* fs1 = nullptr;
                     const float* fsh = nullptr;
@@ -1486,9 +1563,9 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     // staged FiLM, tap tables
     constexpr int NSPLIT_ = UT_EPI_WG;
     constexpr int NG_ = 8 / (SPLIT * NSPLIT_), NC_ = N / NSPLIT_;
-    const size_t vec = (size_t)(4 * N * SPLIT + 7 * 64 + 2 * UT_EPI_WG * 4 * 32 * 2 * NG_ + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
+    const size_t vec = (size_t)(4 * N * SPLIT + 7 * 64 + ut_red_floats<EPI, NG_>() + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
                        UT_MAXG * sizeof(UtGroup) + UT_MAXTAP * sizeof(UtTap) + 64;
-    const size_t fin = EPI == EPI_FINAL ? 2 * 16384 + 2048 + 2 * 128 * U_DOF * 4 : (size_t)UT_EPI_WG * 2 * 4096;
+    const size_t fin = EPI == EPI_FINAL ? UT_EPI_WG * (16384 + 128 * U_DOF * 4) + 2048 : (size_t)UT_EPI_WG * 2 * 4096;
     const size_t budget = 225 * 1024 - vec - 2048 - fin;
     a.sa_stages = 3 * (size_t)A_BYTES <= 110 * 1024 ? 3 : 2;
     const int sb_fit = (int)((budget - (size_t)a.sa_stages * A_BYTES) / B_BYTES);
@@ -1506,7 +1583,7 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     }
     if (a.sb_stages < 2 && !a.resident) return PS_FAIL(PS_ERR_SHAPE);
     const size_t smem = 1024 + (size_t)a.sa_stages * A_BYTES + (size_t)a.sb_stages * B_BYTES + fin +
-                        (2 * (a.sa_stages + a.sb_stages) + 10 + 8 * UT_EPI_WG) * 8 + 16 + vec;
+                        (2 * (a.sa_stages + a.sb_stages) + 12 + 8 * UT_EPI_WG) * 8 + 16 + vec;
     auto kern = unet_tc_kernel<N, EPI, RES, MB, PAIR, SPLIT>;
     static int set_bytes = 0;
     if ((int)smem > set_bytes) {
