@@ -697,14 +697,16 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     constexpr int B_BYTES = PAIR ? N * 64 : N * 128;   // this CTA's share of a weight stage
     constexpr int ACC1 = acc_cols<N, RES>();          // columns of one M-block
     constexpr int ACC = MB * ACC1;                     // columns of one tile
-    // TMEM accumulator buffers: up to 4, so the commit -> epilogue -> release round trip of a
-    // tile hides behind the MMAs of the following tiles even when a tile's K loop is short
-    constexpr int NBUF = 4 * ACC <= 512 ? 4 : 2 * ACC <= 512 ? 2 : 1;
     constexpr bool FIN = EPI == EPI_FINAL;
+    // TMEM accumulator buffers: up to 4, so the commit -> epilogue -> release round trip of a
+    // tile hides behind the MMAs of the following tiles even when a tile's K loop is short.
+    // FINAL: 7 x 64 columns + the warpgroups' 4 x 16 projection columns = all 512, so the MMAs
+    // run up to three tiles ahead of the four warpgroup-owned tiles in flight
+    constexpr int NBUF = FIN ? 7 : 4 * ACC <= 512 ? 4 : 2 * ACC <= 512 ? 2 : 1;
     // FINAL: the 64->7 projection runs on the tensor core from a bf16 tile in smem into
-    // 16 extra TMEM columns after the accumulators
+    // 16 TMEM columns per epilogue warpgroup after the accumulators
     constexpr int PROJ_COL = NBUF * ACC;
-    constexpr int NUSED = NBUF * ACC + (FIN ? 16 : 0);
+    constexpr int NUSED = NBUF * ACC + (FIN ? 16 * UT_EPI_WG : 0);
     constexpr int NCOLS = NUSED <= 32 ? 32 : NUSED <= 64 ? 64 : NUSED <= 128 ? 128 : NUSED <= 256 ? 256 : 512;
     constexpr int CG = NF / 8;   // channels per GroupNorm group (of the full layer)
     // both warpgroups drain every tile, each half of the channels / GroupNorm groups
@@ -732,8 +734,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     uint64_t* b_full = a_empty + SA;
     uint64_t* b_empty = b_full + SB;
     uint64_t* tfull = b_empty + SB;
-    uint64_t* tempty = tfull + 4;
-    uint64_t* pbar = tempty + 4;                 // FINAL: projection MMA done, per warpgroup
+    uint64_t* tempty = tfull + 8;
+    uint64_t* pbar = tempty + 8;                 // FINAL: projection MMA done, per warpgroup
     uint64_t* rbar = pbar + 4;                   // identity residual slabs: [epilogue warp][2]
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(rbar + 8 * UT_EPI_WG);
     float* s_bias = reinterpret_cast<float*>(tmem_holder + 4);
@@ -773,7 +775,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             mbar_init(&b_full[i], 1);
             mbar_init(&b_empty[i], 1);
         }
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < NBUF; ++b) {
             mbar_init(&tfull[b], 1);
             // one arrival per epilogue warp (both CTAs); FINAL: the 4 warps of the tile's warpgroup
             mbar_init(&tempty[b], FIN ? 4 : (PAIR ? 2 : 1) * 4 * NSPLIT);
@@ -975,7 +977,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         // rows.  No barrier spans warpgroups, so four tiles' epilogues overlap.  The statistics
         // keep the summation order of the channel-split epilogue (per 8-channel group: packed
         // pair sums, then the time shuffles, then the 4 quadrants in order).
-        static_assert(N == 64 && MB == 1 && NBUF == 4 && UT_EPI_WG == 4 && CG == 8, "final layer shape");
+        static_assert(N == 64 && MB == 1 && UT_EPI_WG == 4 && CG == 8 && NCOLS == 512, "final layer shape");
         const int wg = (warp - 2) >> 2;
         const int q = warp & 3;
         const int r = q * 32 + lane;
@@ -984,7 +986,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         float* red = s_red + wg * (4 * 32 * 16);
         uint8_t* sPw = sP + wg * 16384;
         float* sZw = sZ + wg * (128 * U_DOF);
-        const uint32_t t_lane0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(wg * ACC);
+        const uint32_t t_lane = tmem_base + ((uint32_t)(q * 32) << 16);
         const uint32_t pcol = (uint32_t)(PROJ_COL + 16 * wg);
         const StepCoef sc = a.sc;
         const bool noisy = !a.eps_out && !sc.last && sc.ddpm;
@@ -994,12 +996,14 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             const int tile = tile_of(j);
             const int b = tile * nb + sl;
             const bool valid = b < a.B;
-            mbar_wait(&tfull[wg], (uint32_t)it & 1u);
+            const int buf = j % NBUF;
+            const uint32_t t_lane0 = t_lane + (uint32_t)(buf * ACC);
+            mbar_wait(&tfull[buf], (uint32_t)(j / NBUF) & 1u);
             tc_fence_after();
             if (a.dbg & 1) {
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[wg]);
+                if (lane == 0) mbar_arrive(&tempty[buf]);
                 continue;
             }
             float s1[8], s2[8];
@@ -1062,16 +1066,15 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                 __align__(16) __nv_bfloat162 pk[8];
 #pragma unroll
                 for (int jj = 0; jj < 16; jj += 2) {
-                    float yv[2];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int c = cc + jj + u;
-                        const int g = c / 8;
-                        const float xv = __uint_as_float(rr[jj + u]) + s_bias[c];
-                        const float tt = fmaf(xv, rstd[g], -mean[g] * rstd[g]);
-                        yv[u] = mish8(fmaf(tt, s_gamma[c], s_beta[c]));
-                    }
-                    pk[jj / 2] = __floats2bfloat162_rn(yv[0], yv[1]);
+                    const int c = cc + jj, g = c / 8;
+                    const float2 bb = *reinterpret_cast<const float2*>(s_bias + c);
+                    const float2 ga = *reinterpret_cast<const float2*>(s_gamma + c);
+                    const float2 be = *reinterpret_cast<const float2*>(s_beta + c);
+                    const float2 xv = fadd2(f2(__uint_as_float(rr[jj]), __uint_as_float(rr[jj + 1])), bb);
+                    const float nm = -mean[g] * rstd[g];
+                    const float2 tt = ffma2(xv, f2(rstd[g], rstd[g]), f2(nm, nm));
+                    const float2 yv = mish2(ffma2(tt, ga, be));
+                    pk[jj / 2] = __floats2bfloat162_rn(yv.x, yv.y);
                 }
                 const int jc = cc >> 3;
                 *reinterpret_cast<uint4*>(sPw + r * 128 + (((jc) ^ (r & 7)) << 4)) = *reinterpret_cast<const uint4*>(&pk[0]);
@@ -1079,7 +1082,15 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[wg]);   // accumulator drained: tile j + 4's MMAs may start
+            if (lane == 0) mbar_arrive(&tempty[buf]);   // accumulator drained: its next tile's MMAs may start
+            // the rows' state, loaded ahead of the projection (only the DDPM / DDIM update reads it)
+            const int grow = b * Tv + t;
+            float xs[U_DOF];
+#pragma unroll
+            for (int d = 0; d < U_DOF; ++d) xs[d] = 0.f;
+            if (valid && !a.eps_out)
+#pragma unroll
+                for (int d = 0; d < U_DOF; ++d) xs[d] = a.x[(size_t)grow * U_DOF + d];
             if (noisy) {
                 // the tile's Philox blocks (nb samples x Tv*7/4)
                 for (int i = r; i < nb * per; i += 128) {
@@ -1112,7 +1123,6 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
 #pragma unroll
             for (int d = 0; d < U_DOF; ++d) eps[d] = __uint_as_float(pr[d]) + s_wout[d];
             if (valid) {
-                const int grow = b * Tv + t;
                 const int p = b / a.S;
                 float* xr = a.x + (size_t)grow * U_DOF;
                 if (a.eps_out) {
@@ -1122,7 +1132,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     const float* zr = sZw + sl * Tv * U_DOF + t * U_DOF;
 #pragma unroll
                     for (int d = 0; d < U_DOF; ++d) {
-                        const float xv = xr[d];
+                        const float xv = xs[d];
                         float x0 = (xv - sc.sq1m * eps[d]) * sc.rsq;
                         x0 = fminf(fmaxf(x0, -0.1f), 1.1f);
                         if (sc.last) {
@@ -1583,7 +1593,7 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     }
     if (a.sb_stages < 2 && !a.resident) return PS_FAIL(PS_ERR_SHAPE);
     const size_t smem = 1024 + (size_t)a.sa_stages * A_BYTES + (size_t)a.sb_stages * B_BYTES + fin +
-                        (2 * (a.sa_stages + a.sb_stages) + 12 + 8 * UT_EPI_WG) * 8 + 16 + vec;
+                        (2 * (a.sa_stages + a.sb_stages) + 20 + 8 * UT_EPI_WG) * 8 + 16 + vec;
     auto kern = unet_tc_kernel<N, EPI, RES, MB, PAIR, SPLIT>;
     static int set_bytes = 0;
     if ((int)smem > set_bytes) {
