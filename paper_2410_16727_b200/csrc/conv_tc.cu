@@ -639,6 +639,7 @@ struct UtArgs {
     int sa_stages, sb_stages;
     int resident;   // 1: every tap's weight box stays in B stage <tap> for the whole kernel
     int B, Tv, nb, S;
+    unsigned long long s_magic;   // ceil(2^40 / S): x / S = (x * s_magic) >> 40 for x < 2^40 / S
     const float* bias;
     const float* gamma;
     const float* beta;
@@ -659,6 +660,11 @@ struct UtArgs {
     float* eps_out;
     int dbg;
 };
+
+// sample -> problem index without an integer division (exact for x < 2^40 / S)
+__device__ __forceinline__ int div_s(const UtArgs& a, int x) {
+    return (int)(((unsigned long long)(unsigned)x * a.s_magic) >> 40);
+}
 
 // SW128 K-major descriptor for a matrix starting `row` rows into a 1024-B aligned slot
 // (measured on B200: the MMA applies the SW128 XOR pattern from absolute smem address
@@ -737,15 +743,16 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
     uint64_t* tempty = tfull + 8;
     uint64_t* pbar = tempty + 8;                 // FINAL: projection MMA done, per warpgroup
     uint64_t* rbar = pbar + 4;                   // identity residual slabs: [epilogue warp][2]
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(rbar + 8 * UT_EPI_WG);
+    uint64_t* gnbar = rbar + 8 * UT_EPI_WG;      // GroupNorm partials posted: [epilogue warpgroup][2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gnbar + 2 * UT_EPI_WG);
     float* s_bias = reinterpret_cast<float*>(tmem_holder + 4);
     float* s_gamma = s_bias + NF;
     float* s_beta = s_gamma + NF;
     float* s_rbias = s_beta + NF;
     float* s_wout = s_rbias + NF;                // [7][64]
     float* s_red = s_wout + 7 * 64;              // [2 tile parity][WG][4 quadrants][32 samples][2*NG]
-    float* s_film = s_red + ut_red_floats<EPI, NG>();  // [2 tile parity][WG][TC_FILM_P][2*NC]
-    UtGroup* s_grp = reinterpret_cast<UtGroup*>(s_film + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC);
+    float* s_film = s_red + ut_red_floats<EPI, NG>();  // [3 tiles][WG][TC_FILM_P][2*NC]
+    UtGroup* s_grp = reinterpret_cast<UtGroup*>(s_film + 3 * UT_EPI_WG * TC_FILM_P * 2 * NC);
     UtTap* s_tap = reinterpret_cast<UtTap*>(s_grp + UT_MAXG);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -782,6 +789,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         }
         for (int i = 0; i < 4; ++i) mbar_init(&pbar[i], 1);
         for (int i = 0; i < 8 * UT_EPI_WG; ++i) mbar_init(&rbar[i], 1);
+        for (int i = 0; i < 2 * UT_EPI_WG; ++i) mbar_init(&gnbar[i], 128);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmA[0]) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tmW) : "memory");
@@ -1097,8 +1105,10 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     const int s2_ = i / per, blk = i - s2_ * per;
                     const int b2 = tile * nb + s2_;
                     float n4[4] = {0.f, 0.f, 0.f, 0.f};
-                    if (b2 < a.B)
-                        normal4_tc((uint32_t)sc.k, (uint32_t)(a.p0 + b2 / a.S), (uint32_t)(b2 % a.S), (uint32_t)blk, a.key, n4);
+                    if (b2 < a.B) {
+                        const int p2 = div_s(a, b2);
+                        normal4_tc((uint32_t)sc.k, (uint32_t)(a.p0 + p2), (uint32_t)(b2 - p2 * a.S), (uint32_t)blk, a.key, n4);
+                    }
                     *reinterpret_cast<float4*>(sZw + s2_ * Tv * U_DOF + blk * 4) = make_float4(n4[0], n4[1], n4[2], n4[3]);
                 }
             }
@@ -1123,7 +1133,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
 #pragma unroll
             for (int d = 0; d < U_DOF; ++d) eps[d] = __uint_as_float(pr[d]) + s_wout[d];
             if (valid) {
-                const int p = b / a.S;
+                const int p = div_s(a, b);
                 float* xr = a.x + (size_t)grow * U_DOF;
                 if (a.eps_out) {
 #pragma unroll
@@ -1176,7 +1186,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             if (lane == 0) bulk_wait_read0();
             __syncwarp();
             if (lane == 0) {
-                tma_store_3d(&a.tmO, so, c0 + cur_noff, cur_tile * nb, mb * (128 / nb) + t_w);
+                tma_store_3d(&a.tmO, so, c0 + cur_noff, cur_tile * nb, mb * tstep + t_w);
                 bulk_commit();
             }
             ++ob;
@@ -1191,7 +1201,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             uint64_t* bar = &rbar[ew * 2 + (o & 1u)];
             mbar_expect_tx(bar, 1024u);
             tma_load_3d(sOut + (size_t)(ew * 2 + (o & 1u)) * 1024, &a.tmRes, bar, c_, tile_ * nb,
-                        mb_ * (128 / nb) + t_w);
+                        mb_ * tstep + t_w);
         };
         auto stage_store_res = [&](float* y, int c0, int mb, int j_, int slab) {
             const uint32_t bi = ob & 1u;
@@ -1218,72 +1228,39 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             }
             __syncwarp();
             if (lane == 0) {
-                tma_store_3d(&a.tmO, so, c0 + cur_noff, cur_tile * nb, mb * (128 / nb) + t_w);
+                tma_store_3d(&a.tmO, so, c0 + cur_noff, cur_tile * nb, mb * tstep + t_w);
                 bulk_commit();
             }
             ++ob;
         };
         if (IDRES && lane == 0 && my_tiles > 0) res_load(0, tile_of(0), 0, slice_of(0) * N);
         // every warpgroup drains every tile (its N / 4 channels)
-        for (int j = 0; j < my_tiles; ++j) {
-            const int tile = tile_of(j);
-            cur_tile = tile;
-            cur_noff = slice_of(j) * N;
-            // this item's channel slice of the per-channel vectors
-            const float* s_bias = s_bias_all + cur_noff;
-            const float* s_gamma = s_gamma_all + cur_noff;
-            const float* s_beta = s_beta_all + cur_noff;
-            const float* s_rbias = s_rbias_all + cur_noff;
-            const int buf = j % NBUF;
-            const int b = tile * nb + sl;
-            const bool valid = b < a.B;
-            const uint32_t t_lane0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC + cbase);
-            // FiLM rows of this tile's problems: loaded (L2) before waiting for the accumulator, so
-            // their latency overlaps the wait and the statistics instead of preceding the GN barrier
-            float fpre[2] = {0.f, 0.f};
-            int f_plo = 0, f_n = 0;
-            if constexpr (EPI == EPI_GN_FILM) {
-                static_assert(TC_FILM_P * 2 * NC <= 256, "two FiLM values per thread");
-                const int b_last = min(tile * nb + nb - 1, a.B - 1);
-                f_plo = (tile * nb) / a.S;
-                const int p_hi = b_last / a.S;
-                if (p_hi - f_plo < TC_FILM_P) {
-                    f_n = (p_hi - f_plo + 1) * 2 * NC;
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int i = r + 128 * u;
-                        if (i < f_n) {
-                            const int pp = i / (2 * NC), w = i % (2 * NC);
-                            const int c = cbase + (w < NC ? w : w - NC);
-                            fpre[u] = __ldg(a.film + (size_t)(f_plo + pp) * 3584 + a.film_col + cur_noff +
-                                            (w < NC ? c : NF + c));
-                        }
-                    }
-                }
-            }
-            mbar_wait(&tfull[buf], (uint32_t)(j / NBUF) & 1u);
-            tc_fence_after();
-
-            if (a.dbg & 1) {
-            } else if constexpr (EPI == EPI_PLAIN) {
+        if constexpr (EPI == EPI_PLAIN) {
+            for (int j = 0; j < my_tiles; ++j) {
+                cur_tile = tile_of(j);
+                cur_noff = slice_of(j) * N;
+                const float* s_bias = s_bias_all + cur_noff;
+                const int buf = j % NBUF;
+                const uint32_t t_lane0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC + cbase);
+                mbar_wait(&tfull[buf], (uint32_t)(j / NBUF) & 1u);
+                tc_fence_after();
+                if (!(a.dbg & 1)) {
 #pragma unroll 1
-                for (int mb = 0; mb < MB; ++mb) {
-                    const int grow = b * Tv + t0 + mb * tstep;
-                    const uint32_t t_lane = t_lane0 + (uint32_t)(mb * ACC1);
-                    constexpr int PC = NC < 32 ? NC : 32;
+                    for (int mb = 0; mb < MB; ++mb) {
+                        const uint32_t t_lane = t_lane0 + (uint32_t)(mb * ACC1);
+                        constexpr int PC = NC < 32 ? NC : 32;
 #pragma unroll 1
-                    for (int cc = 0; cc < NC; cc += PC) {
-                        float v[PC];
-                        if constexpr (PC == 32) {
-                            tmem_ld32(t_lane + cc, v);
-                        } else {
-                            uint32_t rr[16];
-                            tmem_ld16(t_lane + cc, rr);
-                            tmem_wait_ld();
+                        for (int cc = 0; cc < NC; cc += PC) {
+                            float v[PC];
+                            if constexpr (PC == 32) {
+                                tmem_ld32(t_lane + cc, v);
+                            } else {
+                                uint32_t rr[16];
+                                tmem_ld16(t_lane + cc, rr);
+                                tmem_wait_ld();
 #pragma unroll
-                            for (int jj = 0; jj < 16; ++jj) v[jj] = __uint_as_float(rr[jj]);
-                        }
-                        {
+                                for (int jj = 0; jj < 16; ++jj) v[jj] = __uint_as_float(rr[jj]);
+                            }
                             const int c0 = cbase + cc;
 #pragma unroll
                             for (int h = 0; h < PC; h += 16) {
@@ -1297,24 +1274,66 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                         }
                     }
                 }
-            } else {
-                // ---- GroupNorm statistics: rows of one sample share `sl` across all 4 warps (and both
-                // M-blocks); the summation order depends on the tile shape, which run_layer chooses
-                // from the trajectory count alone, so every batch on the same side of that threshold
-                // gives the same bits (shard invariance)
-                float s1[NG], s2[NG], mean[NG], rstd[NG];
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (PAIR && !leader) mbar_arrive_remote(leader_addr(&tempty[buf]));
+                    else mbar_arrive(&tempty[buf]);
+                }
+            }
+        } else {
+            // GroupNorm layers, software-pipelined by one tile (PIPE): the statistics of tile j + 1 (wait
+            // for its accumulator, sums per (sample, group), time shuffles, the warp's partials and
+            // the tile's FiLM rows to smem, an arrival on the warpgroup's barrier) run before the
+            // normalise pass of tile j, so nobody waits on the slowest warp of a tile: by the time a
+            // warp needs tile j's partials, a whole normalise pass has passed since they were
+            // posted.  Partials are double-buffered (a warp writes tile j + 2's only after every warp
+            // arrived for j + 1, i.e. read tile j's); staged FiLM rows, read in the normalise pass
+            // after that arrival, are triple-buffered.  Same arithmetic and summation order as the
+            // unpipelined epilogue.  (PS_TC_DBG bit 1 is ignored here.)
+            uint64_t* gnb = gnbar + wg * 2;
+            auto film_rows = [&](int tile_, int& plo, int& phi) {
+                plo = div_s(a, tile_ * nb);
+                phi = div_s(a, min(tile_ * nb + nb - 1, a.B - 1));
+            };
+            auto stats = [&](int jn) {
+                const int tile_n = tile_of(jn);
+                const int noff_n = slice_of(jn) * N;
+                const int buf_n = jn % NBUF;
+                const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf_n * ACC + cbase);
+                const float* sb_n = s_bias_all + noff_n;
+                // FiLM rows of the tile's problems: loaded (L2) before waiting for the accumulator
+                float fpre[2] = {0.f, 0.f};
+                int f_plo = 0, f_n = 0;
+                if constexpr (EPI == EPI_GN_FILM) {
+                    static_assert(TC_FILM_P * 2 * NC <= 256, "two FiLM values per thread");
+                    int p_hi;
+                    film_rows(tile_n, f_plo, p_hi);
+                    if (p_hi - f_plo < TC_FILM_P) {
+                        f_n = (p_hi - f_plo + 1) * 2 * NC;
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int i = r + 128 * u;
+                            if (i < f_n) {
+                                const int pp = i / (2 * NC), w = i % (2 * NC);
+                                const int c = cbase + (w < NC ? w : w - NC);
+                                fpre[u] = __ldg(a.film + (size_t)(f_plo + pp) * 3584 + a.film_col + noff_n +
+                                                (w < NC ? c : NF + c));
+                            }
+                        }
+                    }
+                }
+                mbar_wait(&tfull[buf_n], (uint32_t)(jn / NBUF) & 1u);
+                tc_fence_after();
+                float s1[NG], s2[NG];
 #pragma unroll
                 for (int g = 0; g < NG; ++g) s1[g] = s2[g] = 0.f;
                 constexpr int SC = NC < 32 ? NC : 32;   // stats chunk width
-                // KEEP: narrow warpgroup slices keep the biased accumulator values in registers
-                // between the statistics and the normalise pass (no second TMEM read / bias add)
-                constexpr bool KEEP = (EPI == EPI_GN_FILM || EPI == EPI_GN_RES) && SC == 16 && NC == 16;
-                float kv[KEEP ? MB : 1][16];
                 // 16-channel slices: every M-block's accumulator row is loaded before one wait
                 uint32_t rr_all[NC == 16 ? MB : 1][16];
                 if constexpr (NC == 16) {
 #pragma unroll
-                    for (int mb = 0; mb < MB; ++mb) tmem_ld16(t_lane0 + (uint32_t)(mb * ACC1), rr_all[mb]);
+                    for (int mb = 0; mb < MB; ++mb) tmem_ld16(tl + (uint32_t)(mb * ACC1), rr_all[mb]);
                     tmem_wait_ld();
                 }
 #pragma unroll
@@ -1323,13 +1342,13 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     for (int cc = 0; cc < NC; cc += SC) {
                         float v[SC];
                         if constexpr (SC == 32) {
-                            tmem_ld32(t_lane0 + (uint32_t)(mb * ACC1) + cc, v);
+                            tmem_ld32(tl + (uint32_t)(mb * ACC1) + cc, v);
                         } else if constexpr (NC == 16) {
 #pragma unroll
                             for (int jj = 0; jj < 16; ++jj) v[jj] = __uint_as_float(rr_all[NC == 16 ? mb : 0][jj]);
                         } else {
                             uint32_t rr[16];
-                            tmem_ld16(t_lane0 + (uint32_t)(mb * ACC1) + cc, rr);
+                            tmem_ld16(tl + (uint32_t)(mb * ACC1) + cc, rr);
                             tmem_wait_ld();
 #pragma unroll
                             for (int jj = 0; jj < 16; ++jj) v[jj] = __uint_as_float(rr[jj]);
@@ -1341,12 +1360,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
 #pragma unroll
                         for (int jj = 0; jj < SC; jj += 2) {
                             const int g = (cc + jj) / CG;
-                            const float2 bb = *reinterpret_cast<const float2*>(s_bias + cbase + cc + jj);
+                            const float2 bb = *reinterpret_cast<const float2*>(sb_n + cbase + cc + jj);
                             const float2 xv = fadd2(f2(v[jj], v[jj + 1]), bb);
-                            if constexpr (KEEP) {
-                                kv[KEEP ? mb : 0][(jj) & 15] = xv.x;
-                                kv[KEEP ? mb : 0][(jj + 1) & 15] = xv.y;
-                            }
                             a1[g] = fadd2(a1[g], xv);
                             a2[g] = ffma2(xv, xv, a2[g]);
                         }
@@ -1356,6 +1371,9 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                             s2[g] += a2[g].x + a2[g].y;
                         }
                     }
+                // rows of one sample share `sl` across all 4 warps (and both M-blocks); the summation
+                // order depends on the tile shape, which run_layer chooses from the trajectory count
+                // alone, so every batch on the same side of that threshold gives the same bits
 #pragma unroll
                 for (int off = 16; off >= 1; off >>= 1)
                     if (off >= nb)
@@ -1364,31 +1382,47 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                             s1[g] += __shfl_xor_sync(PS_FULL, s1[g], off);
                             s2[g] += __shfl_xor_sync(PS_FULL, s2[g], off);
                         }
-                // partials of the 4 warps -> smem (double-buffered by tile parity, so one barrier
-                // suffices); the tile's FiLM rows are staged before the same barrier
-                float* redj = red + (j & 1) * (UT_EPI_WG * 4 * 32 * 2 * NG);
+                float* redj = red + (jn & 1) * (UT_EPI_WG * 4 * 32 * 2 * NG);
                 if (lane < nb)
 #pragma unroll
                     for (int g = 0; g < NG; ++g) {
                         redj[(q * 32 + sl) * 2 * NG + g] = s1[g];
                         redj[(q * 32 + sl) * 2 * NG + NG + g] = s2[g];
                     }
-                bool film_staged = false;
                 if constexpr (EPI == EPI_GN_FILM) {
-                    float* sf = s_film + ((j & 1) * UT_EPI_WG + wg) * (TC_FILM_P * 2 * NC);
-                    if (f_n > 0) {
+                    float* sf = s_film + ((jn % 3) * UT_EPI_WG + wg) * (TC_FILM_P * 2 * NC);
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            const int i = r + 128 * u;
-                            if (i < f_n) {
-                                const int pp = i / (2 * NC), w = i % (2 * NC);
-                                sf[pp * 2 * NC + w] = w < NC ? 1.f + fpre[u] : fpre[u];
-                            }
+                    for (int u = 0; u < 2; ++u) {
+                        const int i = r + 128 * u;
+                        if (i < f_n) {
+                            const int pp = i / (2 * NC), w = i % (2 * NC);
+                            sf[pp * 2 * NC + w] = w < NC ? 1.f + fpre[u] : fpre[u];
                         }
-                        film_staged = true;
                     }
                 }
-                asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+                mbar_arrive(&gnb[jn & 1]);
+            };
+            // pipelining holds two accumulator buffers in the epilogue: only with 4 buffers (with 2 the
+            // MMAs of the next tile could not start before the normalise pass of this one ends)
+            constexpr bool PIPE = NBUF >= 4;
+            if (PIPE && my_tiles > 0) stats(0);
+            for (int j = 0; j < my_tiles; ++j) {
+                if (!PIPE) stats(j);
+                const int tile = tile_of(j);
+                cur_tile = tile;
+                cur_noff = slice_of(j) * N;
+                // this item's channel slice of the per-channel vectors
+                const float* s_bias = s_bias_all + cur_noff;
+                const float* s_gamma = s_gamma_all + cur_noff;
+                const float* s_beta = s_beta_all + cur_noff;
+                const float* s_rbias = s_rbias_all + cur_noff;
+                const int buf = j % NBUF;
+                const int b = tile * nb + sl;
+                const bool valid = b < a.B;
+                const uint32_t t_lane0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC + cbase);
+                mbar_wait(&gnb[j & 1], (uint32_t)(j >> 1) & 1u);
+                float mean[NG], rstd[NG];
+                const float* redj = red + (j & 1) * (UT_EPI_WG * 4 * 32 * 2 * NG);
 #pragma unroll
                 for (int g = 0; g < NG; ++g) {
                     float a1 = 0.f, a2 = 0.f;
@@ -1400,119 +1434,96 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     mean[g] = a1 * inv_n;
                     rstd[g] = rsqrtf(fmaxf(fmaf(a2, inv_n, -mean[g] * mean[g]), 0.f) + 1e-5f);
                 }
-
-                const int p = b / a.S;
-                {
-                    // per-tile FiLM rows staged as (1 + scale, shift) for this warpgroup's columns
-                    const float* fs1 = nullptr;
-                    const float* fsh = nullptr;
-                    if constexpr (EPI == EPI_GN_FILM) {
-                        if (film_staged) {
-                            const int p_lo = (tile * nb) / a.S;
-                            fs1 = s_film + ((j & 1) * UT_EPI_WG + wg) * (TC_FILM_P * 2 * NC) + (p - p_lo) * 2 * NC;
-                            fsh = fs1 + NC;
-                        }
-                    }
-                    float nmr[NG];
-#pragma unroll
-                    for (int g = 0; g < NG; ++g) nmr[g] = -mean[g] * rstd[g];
-                    // no early-out on `valid`: tcgen05.ld is .sync.aligned and lanes of one warp
-                    // belong to different samples, so only global accesses are predicated
-                    {
-                      // kept 16-channel slices with a projection residual: both M-blocks' residual
-                      // accumulators loaded before one wait
-                      uint32_t rq_all[KEEP && RES ? MB : 1][16];
-                      if constexpr (KEEP && RES) {
-#pragma unroll
-                          for (int mb = 0; mb < MB; ++mb) tmem_ld16(t_lane0 + (uint32_t)(mb * ACC1) + N, rq_all[mb]);
-                          tmem_wait_ld();
-                      }
-#pragma unroll
-                      for (int mb = 0; mb < MB; ++mb) {
-                        const int grow = b * Tv + t0 + mb * tstep;
-                        const uint32_t t_lane = t_lane0 + (uint32_t)(mb * ACC1);
-#pragma unroll
-                        for (int cc = 0; cc < NC; cc += 16) {
-                            const int c0 = cbase + cc;
-                            uint32_t rr[16], rq[16];
-                            if constexpr (!KEEP) {
-                                tmem_ld16(t_lane + cc, rr);
-                                if constexpr (RES) tmem_ld16(t_lane + N + cc, rq);
-                                tmem_wait_ld();
-                            }
-                            const int gi = cc / CG;
-                            const float rs = sel(rstd, gi), nm = sel(nmr, gi);
-                            const float rs2 = CG < 16 ? sel(rstd, gi + 1) : rs;
-                            const float nm2 = CG < 16 ? sel(nmr, gi + 1) : nm;
-                            float y[16];
-#pragma unroll
-                            for (int jj = 0; jj < 16; jj += 4) {
-                                const float4 bi = *reinterpret_cast<const float4*>(s_bias + c0 + jj);
-                                const float4 ga = *reinterpret_cast<const float4*>(s_gamma + c0 + jj);
-                                const float4 be = *reinterpret_cast<const float4*>(s_beta + c0 + jj);
-                                // packed pairs: (jj, jj+1) and (jj+2, jj+3) lie in one group each
-                                const bool hi = CG < 16 && jj >= CG;
-                                const float2 rsv = hi ? f2(rs2, rs2) : f2(rs, rs), nmv = hi ? f2(nm2, nm2) : f2(nm, nm);
-                                float2 x0, x1;
-                                if constexpr (KEEP) {
-                                    x0 = f2(kv[KEEP ? mb : 0][jj], kv[KEEP ? mb : 0][jj + 1]);
-                                    x1 = f2(kv[KEEP ? mb : 0][jj + 2], kv[KEEP ? mb : 0][jj + 3]);
-                                } else {
-                                    x0 = fadd2(f2(__uint_as_float(rr[jj]), __uint_as_float(rr[jj + 1])), f2(bi.x, bi.y));
-                                    x1 = fadd2(f2(__uint_as_float(rr[jj + 2]), __uint_as_float(rr[jj + 3])), f2(bi.z, bi.w));
-                                }
-                                const float2 z0 = ffma2(ffma2(x0, rsv, nmv), f2(ga.x, ga.y), f2(be.x, be.y));
-                                const float2 z1 = ffma2(ffma2(x1, rsv, nmv), f2(ga.z, ga.w), f2(be.z, be.w));
-                                float2 y0, y1;
-                                if (a.dbg & 32) {   // attribution only: Mish without its SFU ops
-                                    y0 = fmul2(z0, f2(0.5f, 0.5f));
-                                    y1 = fmul2(z1, f2(0.5f, 0.5f));
-                                } else {
-                                    y0 = mish2(z0);
-                                    y1 = mish2(z1);
-                                }
-                                y[jj] = y0.x; y[jj + 1] = y0.y; y[jj + 2] = y1.x; y[jj + 3] = y1.y;
-                            }
-                            if constexpr (EPI == EPI_GN_FILM) {
-                                if (fs1 && valid) {
-#pragma unroll
-                                    for (int jj = 0; jj < 16; jj += 4) {
-                                        const float4 m1 = *reinterpret_cast<const float4*>(fs1 + cc + jj);
-                                        const float4 sh = *reinterpret_cast<const float4*>(fsh + cc + jj);
-                                        const float2 u0 = ffma2(f2(y[jj], y[jj + 1]), f2(m1.x, m1.y), f2(sh.x, sh.y));
-                                        const float2 u1 = ffma2(f2(y[jj + 2], y[jj + 3]), f2(m1.z, m1.w), f2(sh.z, sh.w));
-                                        y[jj] = u0.x; y[jj + 1] = u0.y; y[jj + 2] = u1.x; y[jj + 3] = u1.y;
-                                    }
-                                } else if (valid) {
-                                    const float* fr = a.film + (size_t)p * 3584 + a.film_col + cur_noff;
-#pragma unroll
-                                    for (int jj = 0; jj < 16; ++jj)
-                                        y[jj] = fmaf(y[jj], 1.f + __ldg(fr + c0 + jj), __ldg(fr + NF + c0 + jj));
-                                }
-                            } else if constexpr (RES) {
-                                const uint32_t* rqp = KEEP ? rq_all[KEEP && RES ? mb : 0] : rq;
-#pragma unroll
-                                for (int jj = 0; jj < 16; ++jj) y[jj] += __uint_as_float(rqp[jj]) + s_rbias[c0 + jj];
-                            } else {
-                                stage_store_res(y, c0, mb, j, mb * (NC / 16) + cc / 16);
-                                continue;
-                            }
-                                {
-                                __align__(16) __nv_bfloat162 pk[8];
-#pragma unroll
-                                for (int u = 0; u < 8; ++u) pk[u] = __floats2bfloat162_rn(y[2 * u], y[2 * u + 1]);
-                                stage_store(pk, c0, mb);
-                            }
-                        }
-                      }
+                if (PIPE && j + 1 < my_tiles) stats(j + 1);
+                const int p = div_s(a, b);
+                // per-tile FiLM rows staged as (1 + scale, shift) for this warpgroup's columns
+                const float* fs1 = nullptr;
+                const float* fsh = nullptr;
+                if constexpr (EPI == EPI_GN_FILM) {
+                    int p_lo, p_hi;
+                    film_rows(tile, p_lo, p_hi);
+                    if (p_hi - p_lo < TC_FILM_P) {
+                        fs1 = s_film + ((j % 3) * UT_EPI_WG + wg) * (TC_FILM_P * 2 * NC) + (p - p_lo) * 2 * NC;
+                        fsh = fs1 + NC;
                     }
                 }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if (PAIR && !leader) mbar_arrive_remote(leader_addr(&tempty[buf]));
-                else mbar_arrive(&tempty[buf]);
+                float nmr[NG];
+#pragma unroll
+                for (int g = 0; g < NG; ++g) nmr[g] = -mean[g] * rstd[g];
+                // no early-out on `valid`: tcgen05.ld is .sync.aligned and lanes of one warp
+                // belong to different samples, so only global accesses are predicated
+#pragma unroll
+                for (int mb = 0; mb < MB; ++mb) {
+                    const uint32_t t_lane = t_lane0 + (uint32_t)(mb * ACC1);
+#pragma unroll
+                    for (int cc = 0; cc < NC; cc += 16) {
+                        const int c0 = cbase + cc;
+                        uint32_t rr[16], rq[16];
+                        tmem_ld16(t_lane + cc, rr);
+                        if constexpr (RES) tmem_ld16(t_lane + N + cc, rq);
+                        tmem_wait_ld();
+                        const int gi = cc / CG;
+                        const float rs = sel(rstd, gi), nm = sel(nmr, gi);
+                        const float rs2 = CG < 16 ? sel(rstd, gi + 1) : rs;
+                        const float nm2 = CG < 16 ? sel(nmr, gi + 1) : nm;
+                        float y[16];
+#pragma unroll
+                        for (int jj = 0; jj < 16; jj += 4) {
+                            const float4 bi = *reinterpret_cast<const float4*>(s_bias + c0 + jj);
+                            const float4 ga = *reinterpret_cast<const float4*>(s_gamma + c0 + jj);
+                            const float4 be = *reinterpret_cast<const float4*>(s_beta + c0 + jj);
+                            // packed pairs: (jj, jj+1) and (jj+2, jj+3) lie in one group each
+                            const bool hi = CG < 16 && jj >= CG;
+                            const float2 rsv = hi ? f2(rs2, rs2) : f2(rs, rs), nmv = hi ? f2(nm2, nm2) : f2(nm, nm);
+                            const float2 x0 = fadd2(f2(__uint_as_float(rr[jj]), __uint_as_float(rr[jj + 1])), f2(bi.x, bi.y));
+                            const float2 x1 = fadd2(f2(__uint_as_float(rr[jj + 2]), __uint_as_float(rr[jj + 3])), f2(bi.z, bi.w));
+                            const float2 z0 = ffma2(ffma2(x0, rsv, nmv), f2(ga.x, ga.y), f2(be.x, be.y));
+                            const float2 z1 = ffma2(ffma2(x1, rsv, nmv), f2(ga.z, ga.w), f2(be.z, be.w));
+                            float2 y0, y1;
+                            if (a.dbg & 32) {   // attribution only: Mish without its SFU ops
+                                y0 = fmul2(z0, f2(0.5f, 0.5f));
+                                y1 = fmul2(z1, f2(0.5f, 0.5f));
+                            } else {
+                                y0 = mish2(z0);
+                                y1 = mish2(z1);
+                            }
+                            y[jj] = y0.x; y[jj + 1] = y0.y; y[jj + 2] = y1.x; y[jj + 3] = y1.y;
+                        }
+                        if constexpr (EPI == EPI_GN_FILM) {
+                            if (fs1 && valid) {
+#pragma unroll
+                                for (int jj = 0; jj < 16; jj += 4) {
+                                    const float4 m1 = *reinterpret_cast<const float4*>(fs1 + cc + jj);
+                                    const float4 sh = *reinterpret_cast<const float4*>(fsh + cc + jj);
+                                    const float2 u0 = ffma2(f2(y[jj], y[jj + 1]), f2(m1.x, m1.y), f2(sh.x, sh.y));
+                                    const float2 u1 = ffma2(f2(y[jj + 2], y[jj + 3]), f2(m1.z, m1.w), f2(sh.z, sh.w));
+                                    y[jj] = u0.x; y[jj + 1] = u0.y; y[jj + 2] = u1.x; y[jj + 3] = u1.y;
+                                }
+                            } else if (valid) {
+                                const float* fr = a.film + (size_t)p * 3584 + a.film_col + cur_noff;
+#pragma unroll
+                                for (int jj = 0; jj < 16; ++jj)
+                                    y[jj] = fmaf(y[jj], 1.f + __ldg(fr + c0 + jj), __ldg(fr + NF + c0 + jj));
+                            }
+                        } else if constexpr (RES) {
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj) y[jj] += __uint_as_float(rq[jj]) + s_rbias[c0 + jj];
+                        } else {
+                            stage_store_res(y, c0, mb, j, mb * (NC / 16) + cc / 16);
+                            continue;
+                        }
+                        __align__(16) __nv_bfloat162 pk[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) pk[u] = __floats2bfloat162_rn(y[2 * u], y[2 * u + 1]);
+                        stage_store(pk, c0, mb);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (PAIR && !leader) mbar_arrive_remote(leader_addr(&tempty[buf]));
+                    else mbar_arrive(&tempty[buf]);
+                }
             }
         }
         if (!FIN && lane == 0) bulk_wait0();   // output stores complete before the grid ends
@@ -1573,7 +1584,7 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     // staged FiLM, tap tables
     constexpr int NSPLIT_ = UT_EPI_WG;
     constexpr int NG_ = 8 / (SPLIT * NSPLIT_), NC_ = N / NSPLIT_;
-    const size_t vec = (size_t)(4 * N * SPLIT + 7 * 64 + ut_red_floats<EPI, NG_>() + 2 * UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
+    const size_t vec = (size_t)(4 * N * SPLIT + 7 * 64 + ut_red_floats<EPI, NG_>() + 3 * UT_EPI_WG * TC_FILM_P * 2 * NC_) * 4 +
                        UT_MAXG * sizeof(UtGroup) + UT_MAXTAP * sizeof(UtTap) + 64;
     const size_t fin = EPI == EPI_FINAL ? UT_EPI_WG * (16384 + 128 * U_DOF * 4) + 2048 : (size_t)UT_EPI_WG * 2 * 4096;
     const size_t budget = 225 * 1024 - vec - 2048 - fin;
@@ -1593,7 +1604,7 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
     }
     if (a.sb_stages < 2 && !a.resident) return PS_FAIL(PS_ERR_SHAPE);
     const size_t smem = 1024 + (size_t)a.sa_stages * A_BYTES + (size_t)a.sb_stages * B_BYTES + fin +
-                        (2 * (a.sa_stages + a.sb_stages) + 20 + 8 * UT_EPI_WG) * 8 + 16 + vec;
+                        (2 * (a.sa_stages + a.sb_stages) + 20 + 10 * UT_EPI_WG) * 8 + 16 + vec;
     auto kern = unet_tc_kernel<N, EPI, RES, MB, PAIR, SPLIT>;
     static int set_bytes = 0;
     if ((int)smem > set_bytes) {
@@ -1725,6 +1736,7 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
     a.Tv = ly.Tv;
     a.nb = nb;
     a.S = S;
+    a.s_magic = ((1ull << 40) + (unsigned long long)S - 1) / (unsigned long long)S;
     const float* side = L.side(packed);
     a.bias = side + c.b_off;
     if (c.g_off >= 0) {
