@@ -619,6 +619,9 @@ struct UtTap {
 };
 
 constexpr int UT_EPI_WG = 4;                       // U-Net epilogue warpgroups
+#ifndef PS_GN_PIPE
+#define PS_GN_PIPE 0   // 1: GroupNorm statistics pipelined one tile ahead (4 TMEM buffers); measured 0.7% slower
+#endif
 constexpr int UT_THREADS = 64 + 128 * UT_EPI_WG;
 // GroupNorm partials in shared memory: [2 tile parity][WG][4 quadrants][32 samples][2 * NG];
 // FINAL (one warpgroup per tile, all 8 groups): [WG][4 quadrants][32 samples][16]
@@ -1292,6 +1295,13 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
             // after that arrival, are triple-buffered.  Same arithmetic and summation order as the
             // unpipelined epilogue.  (PS_TC_DBG bit 1 is ignored here.)
             uint64_t* gnb = gnbar + wg * 2;
+            // pipelining holds two accumulator buffers in the epilogue: only with 4 buffers (with 2 the
+            // MMAs of the next tile could not start before the normalise pass of this one ends)
+            constexpr bool PIPE = PS_GN_PIPE && NBUF >= 4;
+            // KEEP (unpipelined 16-channel slices): the biased accumulator values stay in registers
+            // between the statistics and the normalise pass (one TMEM read per tile)
+            constexpr bool KEEP = !PIPE && NC == 16;
+            float kv[KEEP ? MB : 1][16];
             auto film_rows = [&](int tile_, int& plo, int& phi) {
                 plo = div_s(a, tile_ * nb);
                 phi = div_s(a, min(tile_ * nb + nb - 1, a.B - 1));
@@ -1362,6 +1372,10 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                             const int g = (cc + jj) / CG;
                             const float2 bb = *reinterpret_cast<const float2*>(sb_n + cbase + cc + jj);
                             const float2 xv = fadd2(f2(v[jj], v[jj + 1]), bb);
+                            if constexpr (KEEP) {
+                                kv[KEEP ? mb : 0][(cc + jj) & 15] = xv.x;
+                                kv[KEEP ? mb : 0][(cc + jj + 1) & 15] = xv.y;
+                            }
                             a1[g] = fadd2(a1[g], xv);
                             a2[g] = ffma2(xv, xv, a2[g]);
                         }
@@ -1402,9 +1416,6 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                 }
                 mbar_arrive(&gnb[jn & 1]);
             };
-            // pipelining holds two accumulator buffers in the epilogue: only with 4 buffers (with 2 the
-            // MMAs of the next tile could not start before the normalise pass of this one ends)
-            constexpr bool PIPE = NBUF >= 4;
             if (PIPE && my_tiles > 0) stats(0);
             for (int j = 0; j < my_tiles; ++j) {
                 if (!PIPE) stats(j);
@@ -1459,9 +1470,9 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     for (int cc = 0; cc < NC; cc += 16) {
                         const int c0 = cbase + cc;
                         uint32_t rr[16], rq[16];
-                        tmem_ld16(t_lane + cc, rr);
+                        if constexpr (!KEEP) tmem_ld16(t_lane + cc, rr);
                         if constexpr (RES) tmem_ld16(t_lane + N + cc, rq);
-                        tmem_wait_ld();
+                        if constexpr (!KEEP || RES) tmem_wait_ld();
                         const int gi = cc / CG;
                         const float rs = sel(rstd, gi), nm = sel(nmr, gi);
                         const float rs2 = CG < 16 ? sel(rstd, gi + 1) : rs;
@@ -1475,8 +1486,14 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                             // packed pairs: (jj, jj+1) and (jj+2, jj+3) lie in one group each
                             const bool hi = CG < 16 && jj >= CG;
                             const float2 rsv = hi ? f2(rs2, rs2) : f2(rs, rs), nmv = hi ? f2(nm2, nm2) : f2(nm, nm);
-                            const float2 x0 = fadd2(f2(__uint_as_float(rr[jj]), __uint_as_float(rr[jj + 1])), f2(bi.x, bi.y));
-                            const float2 x1 = fadd2(f2(__uint_as_float(rr[jj + 2]), __uint_as_float(rr[jj + 3])), f2(bi.z, bi.w));
+                            float2 x0, x1;
+                            if constexpr (KEEP) {
+                                x0 = f2(kv[KEEP ? mb : 0][jj], kv[KEEP ? mb : 0][jj + 1]);
+                                x1 = f2(kv[KEEP ? mb : 0][jj + 2], kv[KEEP ? mb : 0][jj + 3]);
+                            } else {
+                                x0 = fadd2(f2(__uint_as_float(rr[jj]), __uint_as_float(rr[jj + 1])), f2(bi.x, bi.y));
+                                x1 = fadd2(f2(__uint_as_float(rr[jj + 2]), __uint_as_float(rr[jj + 3])), f2(bi.z, bi.w));
+                            }
                             const float2 z0 = ffma2(ffma2(x0, rsv, nmv), f2(ga.x, ga.y), f2(be.x, be.y));
                             const float2 z1 = ffma2(ffma2(x1, rsv, nmv), f2(ga.z, ga.w), f2(be.z, be.w));
                             float2 y0, y1;
