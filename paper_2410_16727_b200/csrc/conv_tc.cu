@@ -1496,14 +1496,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                             }
                             const float2 z0 = ffma2(ffma2(x0, rsv, nmv), f2(ga.x, ga.y), f2(be.x, be.y));
                             const float2 z1 = ffma2(ffma2(x1, rsv, nmv), f2(ga.z, ga.w), f2(be.z, be.w));
-                            float2 y0, y1;
-                            if (a.dbg & 32) {   // attribution only: Mish without its SFU ops
-                                y0 = fmul2(z0, f2(0.5f, 0.5f));
-                                y1 = fmul2(z1, f2(0.5f, 0.5f));
-                            } else {
-                                y0 = mish2(z0);
-                                y1 = mish2(z1);
-                            }
+                            const float2 y0 = mish2(z0), y1 = mish2(z1);
                             y[jj] = y0.x; y[jj + 1] = y0.y; y[jj + 2] = y1.x; y[jj + 3] = y1.y;
                         }
                         if constexpr (EPI == EPI_GN_FILM) {
