@@ -23,6 +23,9 @@ outs = (torch.empty_like(q), torch.empty(2048, device="cuda"), torch.empty(2048,
 ms = timeit(lambda: bl.refine(q, esdf[0], 2048, robot, grid, cost, out=outs))
 res["cfg2_refine_ms"] = ms
 res["cfg2_GBps_alg"] = 2048 * 10 * 52992 / (ms * 1e-3) / 1e9
+esdf_b = bl.esdf_build(boxes, grid, layout=bl.ESDF_BRICKED)
+ms_b = timeit(lambda: bl.refine(q, esdf_b[0], 2048, robot, grid, cost, out=outs, esdf_layout=bl.ESDF_BRICKED))
+res["cfg2_bricked_refine_ms"] = ms_b
 esdf_q = bl.esdf_build(boxes, grid, layout=bl.ESDF_QUAD)
 ms_q = timeit(lambda: bl.refine(q, esdf_q[0], 2048, robot, grid, cost, out=outs, esdf_layout=bl.ESDF_QUAD))
 res["cfg2_quad_refine_ms"] = ms_q
