@@ -516,13 +516,6 @@ __global__ void xb_kernel(const float* __restrict__ x, size_t rows, __nv_bfloat1
     reinterpret_cast<uint4*>(xb)[i] = *reinterpret_cast<uint4*>(v);
 }
 
-__global__ void film_step_kernel(const float* __restrict__ fa, const float* __restrict__ fb, int P,
-                                 float* __restrict__ out) {
-    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (size_t)P * 3584) return;
-    out[i] = fa[i] + fb[i % 3584];
-}
-
 // ---------------------------------------------------------------------------
 // host side: tensor maps and launches
 // ---------------------------------------------------------------------------
@@ -648,9 +641,11 @@ struct UtArgs {
     const float* beta;
     const float* rbias;
     const __nv_bfloat16* res_src;
-    const float* film;
+    const float* film;        // per-problem FiLM part [P][3584]
+    const float* film_b;      // this step's per-step part [3584], added when the tile's rows are staged
     int film_col;
     __nv_bfloat16* out;
+    __nv_bfloat16* xb_next;   // FINAL: bf16 view of the updated state for the next step's first layer
     const float* wout;
     const float* bout;
     float* x;
@@ -1143,6 +1138,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     for (int d = 0; d < U_DOF; ++d) a.eps_out[(size_t)grow * U_DOF + d] = eps[d];
                 } else {
                     const float* zr = sZw + sl * Tv * U_DOF + t * U_DOF;
+                    __align__(16) __nv_bfloat16 xv8[8];
+                    xv8[7] = __float2bfloat16_rn(0.f);
 #pragma unroll
                     for (int d = 0; d < U_DOF; ++d) {
                         const float xv = xs[d];
@@ -1151,12 +1148,15 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                         if (sc.last) {
                             a.traj[(size_t)grow * U_DOF + d] =
                                 (t == 0) ? a.q_start[(size_t)p * U_DOF + d] : a.lo + x0 * (a.hi - a.lo);
-                        } else if (sc.ddpm) {
-                            xr[d] = sc.c0 * x0 + sc.c1 * xv + sc.sig * zr[d];
                         } else {
-                            xr[d] = sc.sqn * x0 + sc.sq1mn * eps[d];
+                            const float xn = sc.ddpm ? sc.c0 * x0 + sc.c1 * xv + sc.sig * zr[d]
+                                                     : sc.sqn * x0 + sc.sq1mn * eps[d];
+                            xr[d] = xn;
+                            xv8[d] = __float2bfloat16_rn(xn);
                         }
                     }
+                    if (!sc.last && a.xb_next)
+                        *reinterpret_cast<uint4*>(a.xb_next + (size_t)grow * 8) = *reinterpret_cast<const uint4*>(xv8);
                 }
             }
         }
@@ -1327,8 +1327,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                             if (i < f_n) {
                                 const int pp = i / (2 * NC), w = i % (2 * NC);
                                 const int c = cbase + (w < NC ? w : w - NC);
-                                fpre[u] = __ldg(a.film + (size_t)(f_plo + pp) * 3584 + a.film_col + noff_n +
-                                                (w < NC ? c : NF + c));
+                                const int col = a.film_col + noff_n + (w < NC ? c : NF + c);
+                                fpre[u] = __ldg(a.film + (size_t)(f_plo + pp) * 3584 + col) + __ldg(a.film_b + col);
                             }
                         }
                     }
@@ -1511,9 +1511,11 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                                 }
                             } else if (valid) {
                                 const float* fr = a.film + (size_t)p * 3584 + a.film_col + cur_noff;
+                                const float* fq = a.film_b + a.film_col + cur_noff;
 #pragma unroll
                                 for (int jj = 0; jj < 16; ++jj)
-                                    y[jj] = fmaf(y[jj], 1.f + __ldg(fr + c0 + jj), __ldg(fr + NF + c0 + jj));
+                                    y[jj] = fmaf(y[jj], 1.f + (__ldg(fr + c0 + jj) + __ldg(fq + c0 + jj)),
+                                                 __ldg(fr + NF + c0 + jj) + __ldg(fq + NF + c0 + jj));
                             }
                         } else if constexpr (RES) {
 #pragma unroll
@@ -1648,7 +1650,8 @@ static int launch_ut(UtArgs& a, cudaStream_t st) {
 
 
 static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int B, int S, const float* film,
-                     float* x, const TcStep* step, float* eps_out, cudaStream_t st) {
+                     const float* film_b, float* x, __nv_bfloat16* xb_next, const TcStep* step, float* eps_out,
+                     cudaStream_t st) {
     UtArgs a;
     memset(&a, 0, sizeof(a));
     const PConv& c = *ly.c;
@@ -1756,12 +1759,14 @@ static int run_layer(const Layout& L, const char* packed, const TcLayer& ly, int
     if (ly.res) a.rbias = side + ly.res->b_off;
     a.res_src = ly.res_src;
     a.film = film;
+    a.film_b = film_b;
     a.film_col = c.film_col;
     a.out = ly.out;
     if (ly.epi == EPI_FINAL) {
         a.wout = side + L.outw_f32;
         a.bout = side + L.out.b_off;
         a.x = x;
+        a.xb_next = xb_next;
         a.eps_out = eps_out;
         if (step) {
             a.sc = step->sc;
@@ -1918,19 +1923,17 @@ int unet_eval_tc(const Layout& L, const char* packed, float* x, int B, int T, in
                  const float* film_b_row, float* ws, float* eps, const TcStep* step, cudaStream_t st) {
     if (!get_encoder()) return PS_FAIL(PS_ERR_CUDA);
     if (L.mode != 1) return PS_FAIL(PS_ERR_SHAPE);
-    const int P = B / S;
     const UnetSlots u = unet_slots(ws, B, T);
-    {
-        const size_t n = (size_t)P * 3584;
-        film_step_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(film_a, film_b_row, P, u.film);
-        PS_CHECK_LAUNCH();
-        PS_TRY_TC(tc_xb(x, (size_t)B * T, u.a0, st));
-    }
+    // the FiLM layers add this step's per-step part to the per-problem rows as they stage them; the
+    // state's bf16 view comes from the previous step's FINAL epilogue when the caller says so
+    static const bool no_fuse = std::getenv("PS_NO_XB_FUSE") != nullptr;   // A/B knob
+    if (!step || !step->xb_ready || no_fuse) PS_TRY_TC(tc_xb(x, (size_t)B * T, u.a0, st));
     std::vector<TcLayer> layers;
     unet_layer_list(L, T, u, true, layers);
     for (const TcLayer& ly : layers) {
         const bool fin = ly.epi == EPI_FINAL;
-        PS_TRY_TC(run_layer(L, packed, ly, B, S, u.film, x, fin ? step : nullptr, fin && !step ? eps : nullptr, st));
+        PS_TRY_TC(run_layer(L, packed, ly, B, S, film_a, film_b_row, x, fin && step && !no_fuse ? u.a0 : nullptr,
+                            fin ? step : nullptr, fin && !step ? eps : nullptr, st));
     }
     return PS_OK;
 }

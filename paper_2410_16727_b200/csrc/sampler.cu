@@ -1141,7 +1141,7 @@ static int sample_loop(const void* packed, int mode, const void* packed_hp, int 
                                                                              q_start, traj, lo, hi);
             PS_CHECK_LAUNCH();
         } else {
-            TcStep ts{sc, p0, noise_key, q_start, traj, lo, hi};
+            TcStep ts{sc, p0, noise_key, q_start, traj, lo, hi, i > n_hp ? 1 : 0};
             PS_TRY(unet_eval_tc(L, pk, x, B, T, S, film_a, fb, act, eps, &ts, st));
         }
     }

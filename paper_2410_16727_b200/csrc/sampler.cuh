@@ -47,6 +47,7 @@ struct TcStep {
     const float* q_start;
     float* traj;
     float lo, hi;
+    int xb_ready = 0;   // the bf16 state view already holds x (written by the previous step's FINAL epilogue)
 };
 
 // One conv layer of the tcgen05 U-Net.  src[0..2]: activation views (bf16 [B][Tv][ld]); the
