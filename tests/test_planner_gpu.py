@@ -281,3 +281,56 @@ def test_bf16_layered_pipeline_horizon64(torch_cuda, params, oracle_lib):
     want = un.sample(params, ARCH, cond, pb.q_start[:1], S, T=64, problems=np.array([pb.p0]))
     d = seeds[:S] - want
     assert np.sqrt((d ** 2).mean()) < 2e-2 and np.abs(d).max() < 0.2
+
+
+class TestRequestApi:
+    """plan_diffusion_batch / plan_diffusion (planseed's call shape, pipeline.py) over the same
+    planner: the same bits as plan_batch, planseed's PlanResult fields, any request split."""
+
+    P = 3
+
+    @pytest.fixture(scope="class")
+    def run(self, torch_cuda, params):
+        from paper_2410_16727_b200.pipeline import plan_diffusion_batch, requests_from_problems
+        pl = _planner(params, 1, self.P)
+        pb = synth.config3_problems(self.P, p0=7, seed=0)
+        res = plan_diffusion_batch(pl, requests_from_problems(pb), p0=pb.p0)
+        host = pl.plan_batch(pb.images, pb.q_start, pb.goal, pb.boxes, p0=pb.p0)
+        return pl, pb, res, host
+
+    def test_same_bits_as_plan_batch(self, run):
+        pl, pb, res, host = run
+        traj = np.asarray(host.trajectories).reshape(self.P, S, -1, 7)
+        for p, r in enumerate(res):
+            assert r.seeder == "diffusion" and len(r.results) == S and len(r.successes) == S
+            assert r.best_index == int(np.asarray(host.best_index)[p])
+            assert np.array_equal(np.stack([o.trajectory for o in r.results]).astype(np.float32), traj[p])
+            assert np.array_equal(np.array([o.cost for o in r.results], dtype=np.float32),
+                                  np.asarray(host.cost)[p * S:(p + 1) * S])
+            assert r.successes == [bool(f) for f in np.asarray(host.feasible)[p * S:(p + 1) * S]]
+            assert np.array_equal(r.trajectory, r.results[r.best_index].trajectory)
+            assert r.seed_trajectories.shape == (S, 32, 7)
+            assert np.array_equal(r.seed_trajectories[:, 0], np.repeat(pb.q_start[p:p + 1], S, 0).astype(np.float64))
+            assert r.plan_time > r.esdf_time > 0
+
+    def test_breakdown_and_serialisation(self, run):
+        import json
+        pl, pb, res, host = run
+        for r in res:
+            for o in r.results:
+                b = o.breakdown
+                assert list(b) == ["goal_pos", "goal_rot", "smooth", "self", "world"]
+                assert b["world"] >= 0 and b["smooth"] >= 0
+                assert abs(b["smooth"] + b["world"] - o.cost) <= 1e-5 * max(1.0, o.cost)
+                assert o.iterations == pl.cost.n_iters and not o.converged
+            d = json.loads(r.to_json())
+            assert d["best_index"] == r.best_index and len(d["planner_successes"]) == S
+
+    def test_single_request_equals_batch_element(self, run):
+        from paper_2410_16727_b200.pipeline import plan_diffusion, requests_from_problems
+        pl, pb, res, _ = run
+        reqs = requests_from_problems(pb)
+        one = plan_diffusion(pl, reqs[1], p0=pb.p0 + 1)
+        assert one.best_index == res[1].best_index
+        assert np.array_equal(one.trajectory, res[1].trajectory)
+        assert one.successes == res[1].successes
