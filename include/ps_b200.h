@@ -281,6 +281,20 @@ int ps_ref_metrics(const double* trajs, int S, int T, int D, const double* lengt
                    void* stream);
 int ps_ref_denorm_pin(const double* x0, int B, int T, int D, const double* lo, const double* hi,
                       const double* q0, double* traj, void* stream);
+/* The same denoiser / sampler building blocks with a scalar-type switch (float64 is
+ * the parity mode, float32 the fast mode): dtype 0 = double, 1 = float; every pointer of that
+ * type.  The plain entry points above are the dtype-0 forms. */
+int ps_ref_linear_dt(int dtype, const void* x, int ldx, const void* W, const void* b, int R, int K, int N, int act,
+                     void* y, int ldy, void* stream);
+int ps_ref_film_dt(int dtype, void* h, const void* scale, const void* shift, int R, int N, void* stream);
+int ps_ref_conv1d_silu_dt(int dtype, const void* x, int C, int L, const void* w, const void* b, int O, int K,
+                          int stride, void* y, void* stream);
+int ps_ref_sinusoid_dt(int dtype, double k, int half, void* out, void* stream);
+int ps_ref_div_dt(int dtype, const void* x, int n, double d, void* y, void* stream);
+int ps_ref_ddim_update_dt(int dtype, void* x, const void* eps, int n, double ab, double ab_next, int has_next,
+                          double clip_lo, double clip_hi, void* x0_out, void* stream);
+int ps_ref_denorm_pin_dt(int dtype, const void* x0, int B, int T, int D, const void* lo, const void* hi,
+                         const void* q0, void* traj, void* stream);
 
 /* ================= Reference profile: training (csrc/ref_train.cu, float64) ================
  * The layer-level kernels of loss_eq2 / train (src/diffusion.py:415-508, src/autodiff.py): the host

@@ -89,6 +89,13 @@ _SIGS = {
     "ps_ref_metrics": [_vp, _c_int, _c_int, _c_int, _vp, _c_d, _c_d, _vp, _c_int, _vp, _c_int, _vp, _c_int, _c_d,
                        _c_d, _c_d, _c_d, _vp, _vp, _vp, _vp, _c_int, _vp, _vp],
     "ps_ref_denorm_pin": [_vp, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp],
+    "ps_ref_linear_dt": [_c_int, _vp, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp],
+    "ps_ref_film_dt": [_c_int, _vp, _vp, _vp, _c_int, _c_int, _vp],
+    "ps_ref_conv1d_silu_dt": [_c_int, _vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _vp, _vp],
+    "ps_ref_sinusoid_dt": [_c_int, _c_d, _c_int, _vp, _vp],
+    "ps_ref_div_dt": [_c_int, _vp, _c_int, _c_d, _vp, _vp],
+    "ps_ref_ddim_update_dt": [_c_int, _vp, _vp, _c_int, _c_d, _c_d, _c_int, _c_d, _c_d, _vp, _vp],
+    "ps_ref_denorm_pin_dt": [_c_int, _vp, _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _vp],
     "ps_train_gemm": [_vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp],
     "ps_train_bias_act": [_vp, _c_int, _vp, _c_int, _c_int, _c_int, _vp, _vp],
     "ps_train_silu_bwd": [_vp, _c_int, _vp, _c_int, _c_int, _vp],

@@ -783,54 +783,59 @@ __global__ void planner_success_kernel(const __grid_constant__ ArmGrid<double> A
 // ---------------------------------------------------------------------------
 // FC denoiser (src/diffusion.py:272-300) and scan encoder (:246-269), fp64
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double silu(double x) { return x * (1.0 / (1.0 + exp(-x))); }
+// Templated on the scalar type: float64 is planseed's parity mode, float32 the fast mode
+// (SURVEY §7.2); the arithmetic is the same expression in either type.
+template <typename F>
+__device__ __forceinline__ F silu(F x) { return x * (F(1) / (F(1) + exp(-x))); }
 
 // y[r, n] = act(b[n] + sum_k x[r, k] W[k, n]); W (K, N) row-major ("in, out")
-__global__ void linear_f64_kernel(const double* __restrict__ x, int ldx, const double* __restrict__ W,
-                                  const double* __restrict__ b, int R, int K, int N, int act,
-                                  double* __restrict__ y, int ldy) {
+template <typename F>
+__global__ void linear_kernel(const F* __restrict__ x, int ldx, const F* __restrict__ W, const F* __restrict__ b,
+                              int R, int K, int N, int act, F* __restrict__ y, int ldy) {
     const int n = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
     if (n >= N || r >= R) return;
-    double acc = 0;
-    const double* xr = x + (size_t)r * ldx;
+    F acc = 0;
+    const F* xr = x + (size_t)r * ldx;
     for (int k = 0; k < K; ++k) acc += xr[k] * W[(size_t)k * N + n];
     acc += b[n];
     y[(size_t)r * ldy + n] = act ? silu(acc) : acc;
 }
 
 // h = h * (1 + scale) + shift, scale/shift rows broadcast (mod is shared by the batch)
-__global__ void film_f64_kernel(double* __restrict__ h, const double* __restrict__ scale,
-                                const double* __restrict__ shift, int R, int N) {
+template <typename F>
+__global__ void film_kernel(F* __restrict__ h, const F* __restrict__ scale, const F* __restrict__ shift, int R,
+                            int N) {
     const int n = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
     if (n >= N || r >= R) return;
-    double& v = h[(size_t)r * N + n];
-    v = v * (1.0 + scale[n]) + shift[n];
+    F& v = h[(size_t)r * N + n];
+    v = v * (F(1) + scale[n]) + shift[n];
 }
 
 // conv1d valid, stride s: (C_in, L) x (C_out, C_in, K) -> silu -> (C_out, Lo); one block
-__global__ void conv1d_silu_kernel(const double* __restrict__ x, int C, int L, const double* __restrict__ w,
-                                   const double* __restrict__ b, int O, int Kk, int stride,
-                                   double* __restrict__ y) {
+template <typename F>
+__global__ void conv1d_silu_kernel(const F* __restrict__ x, int C, int L, const F* __restrict__ w,
+                                   const F* __restrict__ b, int O, int Kk, int stride, F* __restrict__ y) {
     const int Lo = (L - Kk) / stride + 1;
     for (int idx = threadIdx.x; idx < O * Lo; idx += blockDim.x) {
         const int o = idx / Lo, j = idx % Lo;
-        double acc = 0;
+        F acc = 0;
         for (int c = 0; c < C; ++c)
             for (int t = 0; t < Kk; ++t) acc += w[((size_t)o * C + c) * Kk + t] * x[(size_t)c * L + j * stride + t];
         y[idx] = silu(acc + b[o]);
     }
 }
 
-// DDIM update (src/diffusion.py:547-555) on the normalised state
-__global__ void ddim_update_kernel(double* __restrict__ x, const double* __restrict__ eps, int n, double ab,
-                                   double ab_next, int has_next, double clip_lo, double clip_hi,
-                                   double* __restrict__ x0_out) {
+// DDIM update (src/diffusion.py:547-555) on the normalised state; the schedule coefficients are
+// formed in float64 on the host and rounded once to F
+template <typename F>
+__global__ void ddim_update_kernel(F* __restrict__ x, const F* __restrict__ eps, int n, F sq1m, F rsq, F sqn,
+                                   F sq1mn, int has_next, F clip_lo, F clip_hi, F* __restrict__ x0_out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double x0 = (x[i] - sqrt(1.0 - ab) * eps[i]) / sqrt(ab);
+    F x0 = (x[i] - sq1m * eps[i]) / rsq;
     x0 = fmin(fmax(x0, clip_lo), clip_hi);
     x0_out[i] = x0;
-    if (has_next) x[i] = sqrt(ab_next) * x0 + sqrt(1.0 - ab_next) * eps[i];
+    if (has_next) x[i] = sqn * x0 + sq1mn * eps[i];
 }
 
 }  // namespace ref
@@ -1052,34 +1057,77 @@ extern "C" int ps_ref_planner_success(const double* trajs, int S, int T, int D, 
     return PS_OK;
 }
 
+// dtype: 0 float64 (parity mode), 1 float32 (fast mode); pointers of that type
+extern "C" int ps_ref_linear_dt(int dtype, const void* x, int ldx, const void* W, const void* b, int R, int K, int N,
+                                int act, void* y, int ldy, void* stream) {
+    if (R <= 0 || K <= 0 || N <= 0 || (dtype != 0 && dtype != 1)) return PS_FAIL(PS_ERR_SHAPE);
+    const dim3 g((N + 127) / 128, R);
+    if (dtype == 0)
+        linear_kernel<double><<<g, 128, 0, (cudaStream_t)stream>>>((const double*)x, ldx, (const double*)W,
+                                                                    (const double*)b, R, K, N, act, (double*)y, ldy);
+    else
+        linear_kernel<float><<<g, 128, 0, (cudaStream_t)stream>>>((const float*)x, ldx, (const float*)W,
+                                                                   (const float*)b, R, K, N, act, (float*)y, ldy);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
 extern "C" int ps_ref_linear(const double* x, int ldx, const double* W, const double* b, int R, int K, int N, int act,
                              double* y, int ldy, void* stream) {
-    if (R <= 0 || K <= 0 || N <= 0) return PS_FAIL(PS_ERR_SHAPE);
-    linear_f64_kernel<<<dim3((N + 127) / 128, R), 128, 0, (cudaStream_t)stream>>>(x, ldx, W, b, R, K, N, act, y, ldy);
+    return ps_ref_linear_dt(0, x, ldx, W, b, R, K, N, act, y, ldy, stream);
+}
+
+extern "C" int ps_ref_film_dt(int dtype, void* h, const void* scale, const void* shift, int R, int N, void* stream) {
+    if (R <= 0 || N <= 0 || (dtype != 0 && dtype != 1)) return PS_FAIL(PS_ERR_SHAPE);
+    const dim3 g((N + 127) / 128, R);
+    if (dtype == 0)
+        film_kernel<double><<<g, 128, 0, (cudaStream_t)stream>>>((double*)h, (const double*)scale,
+                                                                  (const double*)shift, R, N);
+    else
+        film_kernel<float><<<g, 128, 0, (cudaStream_t)stream>>>((float*)h, (const float*)scale, (const float*)shift,
+                                                                 R, N);
     PS_CHECK_LAUNCH();
     return PS_OK;
 }
-
 extern "C" int ps_ref_film(double* h, const double* scale, const double* shift, int R, int N, void* stream) {
-    film_f64_kernel<<<dim3((N + 127) / 128, R), 128, 0, (cudaStream_t)stream>>>(h, scale, shift, R, N);
+    return ps_ref_film_dt(0, h, scale, shift, R, N, stream);
+}
+
+extern "C" int ps_ref_conv1d_silu_dt(int dtype, const void* x, int C, int L, const void* w, const void* b, int O,
+                                     int K, int stride, void* y, void* stream) {
+    if (L < K || (dtype != 0 && dtype != 1)) return PS_FAIL(PS_ERR_SHAPE);
+    if (dtype == 0)
+        conv1d_silu_kernel<double><<<1, 256, 0, (cudaStream_t)stream>>>((const double*)x, C, L, (const double*)w,
+                                                                         (const double*)b, O, K, stride, (double*)y);
+    else
+        conv1d_silu_kernel<float><<<1, 256, 0, (cudaStream_t)stream>>>((const float*)x, C, L, (const float*)w,
+                                                                        (const float*)b, O, K, stride, (float*)y);
     PS_CHECK_LAUNCH();
     return PS_OK;
 }
-
 extern "C" int ps_ref_conv1d_silu(const double* x, int C, int L, const double* w, const double* b, int O, int K,
                                   int stride, double* y, void* stream) {
-    if (L < K) return PS_FAIL(PS_ERR_SHAPE);
-    conv1d_silu_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(x, C, L, w, b, O, K, stride, y);
+    return ps_ref_conv1d_silu_dt(0, x, C, L, w, b, O, K, stride, y, stream);
+}
+
+extern "C" int ps_ref_ddim_update_dt(int dtype, void* x, const void* eps, int n, double ab, double ab_next,
+                                     int has_next, double clip_lo, double clip_hi, void* x0_out, void* stream) {
+    if (n <= 0 || (dtype != 0 && dtype != 1)) return PS_FAIL(PS_ERR_SHAPE);
+    const double sq1m = sqrt(1.0 - ab), rsq = sqrt(ab), sqn = sqrt(ab_next), sq1mn = sqrt(1.0 - ab_next);
+    const unsigned g = (unsigned)((n + 255) / 256);
+    if (dtype == 0)
+        ddim_update_kernel<double><<<g, 256, 0, (cudaStream_t)stream>>>((double*)x, (const double*)eps, n, sq1m, rsq,
+                                                                         sqn, sq1mn, has_next, clip_lo, clip_hi,
+                                                                         (double*)x0_out);
+    else
+        ddim_update_kernel<float><<<g, 256, 0, (cudaStream_t)stream>>>(
+            (float*)x, (const float*)eps, n, (float)sq1m, (float)rsq, (float)sqn, (float)sq1mn, has_next,
+            (float)clip_lo, (float)clip_hi, (float*)x0_out);
     PS_CHECK_LAUNCH();
     return PS_OK;
 }
-
 extern "C" int ps_ref_ddim_update(double* x, const double* eps, int n, double ab, double ab_next, int has_next,
                                   double clip_lo, double clip_hi, double* x0_out, void* stream) {
-    ddim_update_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(x, eps, n, ab, ab_next, has_next, clip_lo,
-                                                                           clip_hi, x0_out);
-    PS_CHECK_LAUNCH();
-    return PS_OK;
+    return ps_ref_ddim_update_dt(0, x, eps, n, ab, ab_next, has_next, clip_lo, clip_hi, x0_out, stream);
 }
 
 // ---------------------------------------------------------------------------
@@ -1088,22 +1136,25 @@ extern "C" int ps_ref_ddim_update(double* x, const double* eps, int n, double ab
 namespace ps {
 namespace ref {
 // sinusoid of a 1-based step (src/diffusion.py:228-234): freq_i = exp(-ln(1e4) i / max(half-1, 1))
-__global__ void sinusoid_f64_kernel(double k, int half, double* __restrict__ out) {
+// (the angle in float64 for both types, rounded once: the features match to the last bit of F)
+template <typename F>
+__global__ void sinusoid_kernel(double k, int half, F* __restrict__ out) {
     const int i = threadIdx.x;
     if (i >= half) return;
     const double freq = exp(-log(10000.0) * (double)i / (double)(half > 1 ? half - 1 : 1));
     const double ang = k * freq;
-    out[i] = sin(ang);
-    out[half + i] = cos(ang);
+    out[i] = (F)sin(ang);
+    out[half + i] = (F)cos(ang);
 }
-__global__ void div_f64_kernel(const double* __restrict__ x, int n, double d, double* __restrict__ y) {
+template <typename F>
+__global__ void div_kernel(const F* __restrict__ x, int n, F d, F* __restrict__ y) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) y[i] = x[i] / d;
 }
 // traj = lo + x0 * (hi - lo); row 0 := q0  (src/diffusion.py:559-569, arm.py:200-201)
-__global__ void denorm_pin_kernel(const double* __restrict__ x0, int B, int T, int D, const double* __restrict__ lo,
-                                  const double* __restrict__ hi, const double* __restrict__ q0,
-                                  double* __restrict__ traj) {
+template <typename F>
+__global__ void denorm_pin_kernel(const F* __restrict__ x0, int B, int T, int D, const F* __restrict__ lo,
+                                  const F* __restrict__ hi, const F* __restrict__ q0, F* __restrict__ traj) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= B * T * D) return;
     const int d = i % D, t = (i / D) % T;
@@ -1131,23 +1182,46 @@ __global__ void select_f64_kernel(const double* __restrict__ cost, const uint8_t
 }  // namespace ref
 }  // namespace ps
 
+extern "C" int ps_ref_sinusoid_dt(int dtype, double k, int half, void* out, void* stream) {
+    if (half < 1 || half > 1024 || (dtype != 0 && dtype != 1)) return PS_FAIL(PS_ERR_SHAPE);
+    if (dtype == 0) sinusoid_kernel<double><<<1, half, 0, (cudaStream_t)stream>>>(k, half, (double*)out);
+    else sinusoid_kernel<float><<<1, half, 0, (cudaStream_t)stream>>>(k, half, (float*)out);
+    PS_CHECK_LAUNCH();
+    return PS_OK;
+}
 extern "C" int ps_ref_sinusoid(double k, int half, double* out, void* stream) {
-    if (half < 1 || half > 1024) return PS_FAIL(PS_ERR_SHAPE);
-    sinusoid_f64_kernel<<<1, half, 0, (cudaStream_t)stream>>>(k, half, out);
+    return ps_ref_sinusoid_dt(0, k, half, out, stream);
+}
+extern "C" int ps_ref_div_dt(int dtype, const void* x, int n, double d, void* y, void* stream) {
+    if (n <= 0 || (dtype != 0 && dtype != 1)) return PS_FAIL(PS_ERR_SHAPE);
+    const unsigned g = (unsigned)((n + 255) / 256);
+    if (dtype == 0) div_kernel<double><<<g, 256, 0, (cudaStream_t)stream>>>((const double*)x, n, d, (double*)y);
+    else div_kernel<float><<<g, 256, 0, (cudaStream_t)stream>>>((const float*)x, n, (float)d, (float*)y);
     PS_CHECK_LAUNCH();
     return PS_OK;
 }
 extern "C" int ps_ref_div(const double* x, int n, double d, double* y, void* stream) {
-    div_f64_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(x, n, d, y);
+    return ps_ref_div_dt(0, x, n, d, y, stream);
+}
+extern "C" int ps_ref_denorm_pin_dt(int dtype, const void* x0, int B, int T, int D, const void* lo, const void* hi,
+                                    const void* q0, void* traj, void* stream) {
+    const int n = B * T * D;
+    if (n <= 0 || (dtype != 0 && dtype != 1)) return PS_FAIL(PS_ERR_SHAPE);
+    const unsigned g = (unsigned)((n + 255) / 256);
+    if (dtype == 0)
+        denorm_pin_kernel<double><<<g, 256, 0, (cudaStream_t)stream>>>((const double*)x0, B, T, D, (const double*)lo,
+                                                                        (const double*)hi, (const double*)q0,
+                                                                        (double*)traj);
+    else
+        denorm_pin_kernel<float><<<g, 256, 0, (cudaStream_t)stream>>>((const float*)x0, B, T, D, (const float*)lo,
+                                                                       (const float*)hi, (const float*)q0,
+                                                                       (float*)traj);
     PS_CHECK_LAUNCH();
     return PS_OK;
 }
 extern "C" int ps_ref_denorm_pin(const double* x0, int B, int T, int D, const double* lo, const double* hi,
                                  const double* q0, double* traj, void* stream) {
-    const int n = B * T * D;
-    denorm_pin_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(x0, B, T, D, lo, hi, q0, traj);
-    PS_CHECK_LAUNCH();
-    return PS_OK;
+    return ps_ref_denorm_pin_dt(0, x0, B, T, D, lo, hi, q0, traj, stream);
 }
 extern "C" int ps_ref_select(const double* cost, const uint8_t* ok, int P, int S, int* best, void* stream) {
     if (P <= 0 || S <= 0) return PS_FAIL(PS_ERR_SHAPE);

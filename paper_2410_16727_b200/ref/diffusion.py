@@ -149,18 +149,37 @@ def _host_params(net) -> Dict[str, np.ndarray]:
     return {k: np.asarray(getattr(v, "data", v), dtype=np.float64) for k, v in net.params.items()}
 
 
-def _dev_params(net):
-    """Device float64 copies of the weights, cached on the net object."""
+# scalar type of the device path: "fp64" is planseed's parity mode, "fp32" the fast mode
+_DTN = {"fp64": 0, "fp32": 1}
+
+
+def _tdt(dtype: str):
     torch = _lib.require_cuda()
+    if dtype not in _DTN:
+        raise ValueError("dtype must be 'fp64' or 'fp32'")
+    return torch.float64 if dtype == "fp64" else torch.float32
+
+
+def _dt_of(t) -> int:
+    torch = _lib.require_cuda()
+    return 0 if t.dtype == torch.float64 else 1
+
+
+def _dev_params(net, dtype: str = "fp64"):
+    """Device copies of the weights in `dtype` (rounded once from float64), cached on the net object."""
+    torch = _lib.require_cuda()
+    tdt = _tdt(dtype)
     cache = getattr(net, "_ps_dev", None)
     if cache is None:
-        cache = {k: torch.as_tensor(np.ascontiguousarray(v), device="cuda")
-                 for k, v in _host_params(net).items()}
+        cache = {}
         try:
             object.__setattr__(net, "_ps_dev", cache)
         except Exception:
             pass
-    return cache
+    if dtype not in cache:
+        cache[dtype] = {k: torch.as_tensor(np.ascontiguousarray(v), device="cuda").to(tdt)
+                        for k, v in _host_params(net).items()}
+    return cache[dtype]
 
 
 # ----------------------------------------------------------------------------- features
@@ -195,9 +214,9 @@ def _linear(x, W, b, act: int, out=None):
     torch = _lib.require_cuda()
     R, K = x.shape
     N = W.shape[1]
-    y = out if out is not None else torch.empty((R, N), dtype=torch.float64, device="cuda")
-    _lib.check(_lib.lib().ps_ref_linear(_lib.ptr(x), x.stride(0), _lib.ptr(W), _lib.ptr(b), R, K, N, act,
-                                        _lib.ptr(y), y.stride(0), _lib.stream_handle()), "linear")
+    y = out if out is not None else torch.empty((R, N), dtype=x.dtype, device="cuda")
+    _lib.check(_lib.lib().ps_ref_linear_dt(_dt_of(x), _lib.ptr(x), x.stride(0), _lib.ptr(W), _lib.ptr(b), R, K, N,
+                                           act, _lib.ptr(y), y.stride(0), _lib.stream_handle()), "linear")
     return y
 
 
@@ -206,58 +225,63 @@ def _mlp2(p, prefix, x):
                    p[f"{prefix}_fc2_w"], p[f"{prefix}_fc2_b"], 0)
 
 
-def condition_device(net, depths, prob_feats, pose_feats):
+def condition_device(net, depths, prob_feats, pose_feats, dtype: str = "fp64"):
     """condition_graph (src/diffusion.py:246-257) for one observation -> (1, cond_dim) device."""
     torch = _lib.require_cuda()
-    cfg, p = net.config, _dev_params(net)
+    tdt = _tdt(dtype)
+    cfg, p = net.config, _dev_params(net, dtype)
     L = _lib.lib()
-    d = torch.as_tensor(np.asarray(depths, dtype=np.float64), device="cuda").contiguous()
+    dt = _DTN[dtype]
+    d = torch.as_tensor(np.asarray(depths, dtype=np.float64), device="cuda").to(tdt).contiguous()
     h = torch.empty_like(d)
-    _lib.check(L.ps_ref_div(_lib.ptr(d), d.numel(), float(cfg.max_range), _lib.ptr(h),
-                            _lib.stream_handle()), "scan_features")
+    _lib.check(L.ps_ref_div_dt(dt, _lib.ptr(d), d.numel(), float(cfg.max_range), _lib.ptr(h),
+                               _lib.stream_handle()), "scan_features")
     C, Ln = 1, cfg.n_rays
     for i, (c, kk, ss) in enumerate(zip(cfg.scan_channels, cfg.scan_kernels, cfg.scan_strides)):
         lo = (Ln - kk) // ss + 1
-        y = torch.empty(c * lo, dtype=torch.float64, device="cuda")
-        _lib.check(L.ps_ref_conv1d_silu(_lib.ptr(h), C, Ln, _lib.ptr(p[f"scan_conv{i}_w"]),
-                                        _lib.ptr(p[f"scan_conv{i}_b"]), c, kk, ss, _lib.ptr(y),
-                                        _lib.stream_handle()), "conv1d")
+        y = torch.empty(c * lo, dtype=tdt, device="cuda")
+        _lib.check(L.ps_ref_conv1d_silu_dt(dt, _lib.ptr(h), C, Ln, _lib.ptr(p[f"scan_conv{i}_w"]),
+                                           _lib.ptr(p[f"scan_conv{i}_b"]), c, kk, ss, _lib.ptr(y),
+                                           _lib.stream_handle()), "conv1d")
         h, C, Ln = y, c, lo
     scan_emb = _linear(h.view(1, -1), p["scan_fc_w"], p["scan_fc_b"], 0)
-    pf = torch.as_tensor(np.asarray(prob_feats, dtype=np.float64)[None], device="cuda")
-    qf = torch.as_tensor(np.asarray(pose_feats, dtype=np.float64)[None], device="cuda")
+    pf = torch.as_tensor(np.asarray(prob_feats, dtype=np.float64)[None], device="cuda").to(tdt)
+    qf = torch.as_tensor(np.asarray(pose_feats, dtype=np.float64)[None], device="cuda").to(tdt)
     return torch.cat([scan_emb, _mlp2(p, "prob", pf), _mlp2(p, "pose", qf)], dim=1)
 
 
-def encode_condition(net, scan, q0, goal) -> np.ndarray:
-    """src/diffusion.py:260-269."""
+def encode_condition(net, scan, q0, goal, dtype: str = "fp64") -> np.ndarray:
+    """src/diffusion.py:260-269 (float64 result; dtype="fp32" runs the fast mode)."""
     cfg = net.config
-    c = condition_device(net, scan.depths, problem_features(cfg, q0, goal), pose_features(cfg, scan.pose))
-    return c.cpu().numpy()[0]
+    c = condition_device(net, scan.depths, problem_features(cfg, q0, goal), pose_features(cfg, scan.pose), dtype)
+    return c.cpu().numpy().astype(np.float64)[0]
 
 
 def predict_noise_device(net, x, k: int, cond):
-    """predict_noise_graph (src/diffusion.py:272-285); x (B,T,D) device f64, cond (1,C) device."""
+    """predict_noise_graph (src/diffusion.py:272-285); x (B,T,D) and cond (1,C) device tensors of
+    one scalar type (float64 parity mode or float32 fast mode)."""
     torch = _lib.require_cuda()
-    cfg, p = net.config, _dev_params(net)
+    dtype = "fp64" if x.dtype == torch.float64 else "fp32"
+    cfg, p = net.config, _dev_params(net, dtype)
     L = _lib.lib()
     B = x.shape[0]
     half = cfg.t_embed // 2
-    tf = torch.empty((1, cfg.t_embed), dtype=torch.float64, device="cuda")
-    _lib.check(L.ps_ref_sinusoid(float(k), half, _lib.ptr(tf), _lib.stream_handle()), "sinusoid")
+    tf = torch.empty((1, cfg.t_embed), dtype=x.dtype, device="cuda")
+    _lib.check(L.ps_ref_sinusoid_dt(_DTN[dtype], float(k), half, _lib.ptr(tf), _lib.stream_handle()), "sinusoid")
     t_emb = _mlp2(p, "t", tf)
+    cond = cond.to(x.dtype)
     mod = torch.cat([cond, t_emb], dim=1)
     h = torch.cat([x.reshape(B, cfg.x_dim), cond.expand(B, -1), t_emb.expand(B, -1)], dim=1).contiguous()
     for i in range(cfg.n_hidden):
         h = _linear(h, p[f"trunk{i}_w"], p[f"trunk{i}_b"], 1)
         sc = _linear(mod, p[f"trunk{i}_scale_w"], p[f"trunk{i}_scale_b"], 0)
         sh = _linear(mod, p[f"trunk{i}_shift_w"], p[f"trunk{i}_shift_b"], 0)
-        _lib.check(L.ps_ref_film(_lib.ptr(h), _lib.ptr(sc), _lib.ptr(sh), B, h.shape[1],
-                                 _lib.stream_handle()), "film")
+        _lib.check(L.ps_ref_film_dt(_DTN[dtype], _lib.ptr(h), _lib.ptr(sc), _lib.ptr(sh), B, h.shape[1],
+                                    _lib.stream_handle()), "film")
     return _linear(h, p["trunk_out_w"], p["trunk_out_b"], 0).view(B, cfg.t_len, cfg.dof)
 
 
-def predict_noise(net, x_k, k, cond, K: int = 100) -> np.ndarray:
+def predict_noise(net, x_k, k, cond, K: int = 100, dtype: str = "fp64") -> np.ndarray:
     """src/diffusion.py:288-300: x_k (T,D) or (B,T,D), one cond row broadcast."""
     torch = _lib.require_cuda()
     x = np.asarray(x_k, dtype=np.float64)
@@ -269,23 +293,27 @@ def predict_noise(net, x_k, k, cond, K: int = 100) -> np.ndarray:
     c = np.atleast_2d(np.asarray(cond, dtype=np.float64))
     if c.shape[0] != 1:
         raise ValueError("one condition row per call (the reference broadcasts a single row)")
-    xd = torch.as_tensor(x, device="cuda")
-    cd = torch.as_tensor(c, device="cuda")
-    out = predict_noise_device(net, xd, int(k), cd).cpu().numpy()
+    tdt = _tdt(dtype)
+    xd = torch.as_tensor(x, device="cuda").to(tdt)
+    cd = torch.as_tensor(c, device="cuda").to(tdt)
+    out = predict_noise_device(net, xd, int(k), cd).cpu().numpy().astype(np.float64)
     return out[0] if single else out
 
 
-def ddim_sample_device(net, schedule, cond, x_K, q0, arm, n_steps: int = 5):
-    """_ddim_core + ddim_sample (src/diffusion.py:535-569) on device float64."""
+def ddim_sample_device(net, schedule, cond, x_K, q0, arm, n_steps: int = 5, dtype: str = "fp64"):
+    """_ddim_core + ddim_sample (src/diffusion.py:535-569) on the device, in float64 (parity mode)
+    or float32 (fast mode); the schedule coefficients are formed in float64 either way."""
     torch = _lib.require_cuda()
+    tdt = _tdt(dtype)
+    dt = _DTN[dtype]
     L = _lib.lib()
     ks = ddim_steps(schedule.K, n_steps)
-    x = torch.as_tensor(np.array(x_K, dtype=np.float64), device="cuda")
+    x = torch.as_tensor(np.array(x_K, dtype=np.float64), device="cuda").to(tdt)
     single = x.dim() == 2
     if single:
         x = x[None]
     x = x.contiguous()
-    cd = torch.as_tensor(np.atleast_2d(np.asarray(cond, dtype=np.float64)), device="cuda")
+    cd = torch.as_tensor(np.atleast_2d(np.asarray(cond, dtype=np.float64)), device="cuda").to(tdt)
     x0 = torch.empty_like(x)
     n = x.numel()
     for i, k in enumerate(ks):
@@ -293,22 +321,25 @@ def ddim_sample_device(net, schedule, cond, x_K, q0, arm, n_steps: int = 5):
         eps = predict_noise_device(net, x, int(k), cd)
         has_next = i + 1 < len(ks)
         ab_next = float(schedule.alpha_bar(int(ks[i + 1]))) if has_next else 1.0
-        _lib.check(L.ps_ref_ddim_update(_lib.ptr(x), _lib.ptr(eps), n, ab, ab_next, int(has_next),
-                                        X0_CLIP[0], X0_CLIP[1], _lib.ptr(x0), _lib.stream_handle()),
+        _lib.check(L.ps_ref_ddim_update_dt(dt, _lib.ptr(x), _lib.ptr(eps), n, ab, ab_next, int(has_next),
+                                           X0_CLIP[0], X0_CLIP[1], _lib.ptr(x0), _lib.stream_handle()),
                    "ddim_update")
     B, T, D = x0.shape
-    lo = torch.as_tensor(np.asarray(arm.lo, dtype=np.float64), device="cuda")
-    hi = torch.as_tensor(np.asarray(arm.hi, dtype=np.float64), device="cuda")
-    q = torch.as_tensor(np.asarray(q0, dtype=np.float64), device="cuda")
+    lo = torch.as_tensor(np.asarray(arm.lo, dtype=np.float64), device="cuda").to(tdt)
+    hi = torch.as_tensor(np.asarray(arm.hi, dtype=np.float64), device="cuda").to(tdt)
+    q = torch.as_tensor(np.asarray(q0, dtype=np.float64), device="cuda").to(tdt)
     traj = torch.empty_like(x0)
-    _lib.check(L.ps_ref_denorm_pin(_lib.ptr(x0), B, T, D, _lib.ptr(lo), _lib.ptr(hi), _lib.ptr(q),
-                                   _lib.ptr(traj), _lib.stream_handle()), "denormalize")
+    _lib.check(L.ps_ref_denorm_pin_dt(dt, _lib.ptr(x0), B, T, D, _lib.ptr(lo), _lib.ptr(hi), _lib.ptr(q),
+                                      _lib.ptr(traj), _lib.stream_handle()), "denormalize")
     return traj[0] if single else traj
 
 
-def ddim_sample(net, schedule, cond, x_K, q0, arm, n_steps: int = 5) -> np.ndarray:
-    """src/diffusion.py:559-569: denoise x_K (T,D) or (B,T,D); row 0 pinned to q0."""
-    return ddim_sample_device(net, schedule, cond, x_K, q0, arm, n_steps).cpu().numpy()
+def ddim_sample(net, schedule, cond, x_K, q0, arm, n_steps: int = 5, dtype: str = "fp64") -> np.ndarray:
+    """src/diffusion.py:559-569: denoise x_K (T,D) or (B,T,D); row 0 pinned to q0 (float64 result;
+    dtype="fp32" runs the fast mode; its row 0 is re-pinned to the float64 q0)."""
+    out = ddim_sample_device(net, schedule, cond, x_K, q0, arm, n_steps, dtype).cpu().numpy().astype(np.float64)
+    out[..., 0, :] = np.asarray(q0, dtype=np.float64)
+    return out
 
 
 class PlannerCost:

@@ -139,8 +139,9 @@ def select_best(results: Sequence[OptResult], successes: Sequence[bool]) -> int:
 
 
 def plan_diffusion(arm, net, schedule, req: PlanRequest, weights: CostWeights = CostWeights(),
-                   guidance: Optional[GuidanceParams] = None) -> PlanResult:
-    """src/pipeline.py:172-209."""
+                   guidance: Optional[GuidanceParams] = None, dtype: str = "fp64") -> PlanResult:
+    """src/pipeline.py:172-209.  dtype="fp32" runs the encoder, the unguided sampler and the
+    optimizer in float32 (the fast mode; guidance stays float64)."""
     torch = _lib.require_cuda()
     t0 = time.perf_counter()
     esdf = build_planner_esdf(req.bounds, req.scan, req.esdf_cell)
@@ -148,7 +149,7 @@ def plan_diffusion(arm, net, schedule, req: PlanRequest, weights: CostWeights = 
 
     t1 = time.perf_counter()
     rng = np.random.default_rng(req.seed)
-    cond = encode_condition(net, req.scan, req.q_start, req.goal)
+    cond = encode_condition(net, req.scan, req.q_start, req.goal, dtype=dtype)
     x_K = rng.standard_normal((req.n_trajs, net.config.t_len, net.config.dof))
     if guidance is not None and guidance.alpha_guide != 0.0:
         cost_fn = PlannerCost(arm, esdf, req.goal, weights)
@@ -158,8 +159,9 @@ def plan_diffusion(arm, net, schedule, req: PlanRequest, weights: CostWeights = 
         seeds = seeds.cpu().numpy()
     else:
         seeds = ddim_sample_device(net, schedule, cond, x_K, req.q_start, arm,
-                                   n_steps=req.n_denoising).cpu().numpy()
-    results = optimize(arm, esdf, req.goal, list(seeds), req.n_iters, weights)
+                                   n_steps=req.n_denoising, dtype=dtype).cpu().numpy().astype(np.float64)
+        seeds[:, 0] = np.asarray(req.q_start, dtype=np.float64)
+    results = optimize(arm, esdf, req.goal, list(seeds), req.n_iters, weights, dtype=dtype)
     successes = [bool(s) for s in planner_success_batch(arm, esdf, req.goal,
                                                         np.stack([r.trajectory for r in results]),
                                                         req.delta_t, req.delta_r_deg)]

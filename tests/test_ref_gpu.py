@@ -291,3 +291,37 @@ def test_render_depth_scan(ref):
             assert got.shape == want.shape
             assert np.array_equal(got == pose.max_range, want == pose.max_range), (wi, pi)
             _close(got, want, rtol=1e-12, atol=1e-12)
+
+
+def test_fast_mode_fp32_sampler_and_plan(ref):
+    # the fp32 instantiation of the denoiser / encoder / DDIM kernels (SURVEY §7.2 fast mode) against
+    # planseed's float64 outputs: encoder and noise prediction within 1e-5 (measured 6e-8 / 1e-7),
+    # DDIM trajectories and plan_diffusion's seeds within the north-star 1e-4 rad (measured 3.5e-6 /
+    # 2.6e-6), and end to end with the fp32 optimizer the same successes and best seed as planseed
+    from golden_net import golden_net
+    z = np.load(GOLD / "ref_sampler.npz")
+    arm = ref.types.default_arm()
+    net = golden_net(arm)
+    goal = ref.types.Pose2((z["goal"][0], z["goal"][1]), z["goal"][2])
+    cond = ref.diffusion.encode_condition(net, _scan(ref, z), z["q0"], goal, dtype="fp32")
+    e_cond = np.abs(cond - z["cond"]).max()
+    eps = ref.diffusion.predict_noise(net, z["x"], int(z["k"]), z["cond"], dtype="fp32")
+    e_eps = np.abs(eps - z["eps"]).max()
+    sched = ref.diffusion.NoiseSchedule(betas=z["betas"])
+    traj = ref.diffusion.ddim_sample(net, sched, z["cond"], z["x_K"], z["q0"], arm, n_steps=5, dtype="fp32")
+    e_traj = np.abs(traj - z["traj"]).max()
+    print(f"fp32 fast mode: cond {e_cond:.2e} eps {e_eps:.2e} ddim traj {e_traj:.2e} rad")
+    assert e_cond < 1e-5 and e_eps < 1e-5
+    assert e_traj < 1e-4
+    assert np.array_equal(traj[:, 0], np.repeat(z["q0"][None], traj.shape[0], 0))
+    zp = np.load(GOLD / "ref_plan.npz")
+    goal = ref.types.Pose2((zp["goal"][0], zp["goal"][1]), zp["goal"][2])
+    req = ref.pipeline.PlanRequest(q_start=zp["q0"], goal=goal, scan=_scan(ref, zp), n_trajs=int(zp["n_trajs"]),
+                                   n_iters=int(zp["n_iters"]), n_denoising=5, seed=int(zp["seed"]))
+    res = ref.pipeline.plan_diffusion(arm, net, ref.diffusion.make_schedule(), req, dtype="fp32")
+    e_seed = np.abs(res.seed_trajectories - zp["seed_trajectories"]).max()
+    print(f"fp32 plan: seeds {e_seed:.2e} rad, successes {res.successes == list(zp['successes'])}, "
+          f"best {res.best_index} vs {int(zp['best_index'])}")
+    assert e_seed < 1e-4
+    assert res.successes == list(zp["successes"])
+    assert res.best_index == int(zp["best_index"])
