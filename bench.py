@@ -291,6 +291,25 @@ def main():
         finite = bool(torch.isfinite(outs[0]).all().item() and torch.isfinite(outs[1]).all().item())
         if not finite:
             raise RuntimeError("non-finite trajectories or costs in the benchmark outputs")
+    # ... and right: this rank's first two problems re-sampled by the OTHER sampler strategy (the
+    # persistent small-batch kernel when the step ran the layered kernels, and vice versa; same
+    # noise keys) must agree with the step's seeds within the bf16 bound (a wrong-but-finite path
+    # fails here; skipped for the numerically unqualified bf16 strided DDIM from k = 100)
+    seed_check = None
+    if args.schedule == "ddpm100" and P >= 1:
+        n_chk = min(2, P)
+        other = "0" if P * S * T <= 8192 else "1"
+        os.environ["PS_PERSIST"] = other
+        try:
+            alt = planner.sampler.sample(planner.film_a[:n_chk], d_q[:n_chk], S, T, p0=p0).float()
+        finally:
+            os.environ.pop("PS_PERSIST", None)
+        got = planner.seeds[:n_chk * S].float()
+        rms = float(torch.sqrt(((alt - got) ** 2).mean()).item())
+        seed_check = {"problems": n_chk, "other_path": "persistent" if other == "1" else "layered",
+                      "rms_rad": rms, "bound_rad": 3e-2}
+        if not rms < 3e-2:
+            raise RuntimeError(f"benchmark seeds disagree with the {seed_check['other_path']} sampler: RMS {rms:.3e} rad")
 
     # end-to-end through the public API from pinned host buffers: H2D of this rank's inputs, the
     # planning call, the NCCL gather and rank 0's read-back of the whole job's results
@@ -380,7 +399,7 @@ def main():
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "bf16" if mode == 1 else "f32", "data": "synthetic (seeded; MpiNet absent)",
         "config": _config(args), "roofline": roof, "roofline_refine": roof_refine, "cpu_baseline": cpu,
-        "e2e": e2e, "gpu_launches": int(launches), "outputs_finite": True, "clocks": clk,
+        "e2e": e2e, "gpu_launches": int(launches), "outputs_finite": True, "seed_check": seed_check, "clocks": clk,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
