@@ -1518,8 +1518,17 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                                                  __ldg(fr + NF + c0 + jj) + __ldg(fq + NF + c0 + jj));
                             }
                         } else if constexpr (RES) {
+                            // packed, with 16-B loads of the projection bias (4 LDS wavefronts per 16
+                            // channels instead of 16)
 #pragma unroll
-                            for (int jj = 0; jj < 16; ++jj) y[jj] += __uint_as_float(rq[jj]) + s_rbias[c0 + jj];
+                            for (int jj = 0; jj < 16; jj += 4) {
+                                const float4 rb = *reinterpret_cast<const float4*>(s_rbias + c0 + jj);
+                                const float2 u0 = fadd2(f2(y[jj], y[jj + 1]),
+                                                        fadd2(f2(__uint_as_float(rq[jj]), __uint_as_float(rq[jj + 1])), f2(rb.x, rb.y)));
+                                const float2 u1 = fadd2(f2(y[jj + 2], y[jj + 3]),
+                                                        fadd2(f2(__uint_as_float(rq[jj + 2]), __uint_as_float(rq[jj + 3])), f2(rb.z, rb.w)));
+                                y[jj] = u0.x; y[jj + 1] = u0.y; y[jj + 2] = u1.x; y[jj + 3] = u1.y;
+                            }
                         } else {
                             stage_store_res(y, c0, mb, j, mb * (NC / 16) + cc / 16);
                             continue;
