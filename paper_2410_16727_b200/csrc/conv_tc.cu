@@ -2087,42 +2087,75 @@ extern "C" int ps_encoder_pack(const float* blob, int H, int W, int n_layers, vo
 
 // layer 1 (1 -> 32 channels) in fp32 SIMT: one output pixel x 32 channels per thread,
 // input depth scaled by 1/2 (spec.DEPTH_SCALE), NHWC bf16 output with even-padded rows.
+// Two horizontally adjacent output pixels per thread: the weights sit in shared memory as
+// [tap][32 channels], so one 16-B broadcast load feeds 8 FMAs (4 channels x 2 pixels) instead of
+// one load per FMA; the FMA order per output is unchanged (bias, then taps dy-major).
 __global__ void enc_l1_kernel(const float* __restrict__ img, int n_img, int H, int W, const float* __restrict__ w,
                               const float* __restrict__ bias, int Ho, int Wo, int Ho_p,
                               __nv_bfloat16* __restrict__ out) {
-    __shared__ float sw[32 * 9], sb[32];
-    for (int i = threadIdx.x; i < 32 * 9; i += blockDim.x) sw[i] = w[i];
+    __shared__ __align__(16) float sw[9 * 32];
+    __shared__ __align__(16) float sb[32];
+    for (int i = threadIdx.x; i < 32 * 9; i += blockDim.x) sw[(i % 9) * 32 + i / 9] = w[i];   // w: [o][tap]
     for (int i = threadIdx.x; i < 32; i += blockDim.x) sb[i] = bias[i];
     __syncthreads();
+    const int Wp = (Wo + 1) / 2;   // pixel pairs per row
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const size_t n = (size_t)n_img * Ho_p * Wo;
+    const size_t n = (size_t)n_img * Ho_p * Wp;
     if (idx >= n) return;
-    const int x = (int)(idx % Wo), y = (int)((idx / Wo) % Ho_p), m = (int)(idx / ((size_t)Wo * Ho_p));
-    float acc[32];
+    const int xp = (int)(idx % Wp), y = (int)((idx / Wp) % Ho_p), m = (int)(idx / ((size_t)Wp * Ho_p));
+    const int x0 = 2 * xp;
+    const bool has1 = x0 + 1 < Wo;
+    float a0[32], a1[32];
 #pragma unroll
-    for (int o = 0; o < 32; ++o) acc[o] = sb[o];
+    for (int o = 0; o < 32; o += 4) {
+        const float4 b4 = *reinterpret_cast<const float4*>(sb + o);
+        a0[o] = a1[o] = b4.x; a0[o + 1] = a1[o + 1] = b4.y; a0[o + 2] = a1[o + 2] = b4.z; a0[o + 3] = a1[o + 3] = b4.w;
+    }
     if (y < Ho) {
         const float* ib = img + (size_t)m * H * W;
 #pragma unroll
         for (int dy = 0; dy < 3; ++dy) {
             const int yy = 2 * y + dy - 1;
+            const bool rowok = yy >= 0 && yy < H;
+            // input columns 2 x0 - 1 .. 2 x0 + 3 cover both pixels' 3 taps
+            float v[5];
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+                const int xx = 2 * x0 - 1 + c;
+                v[c] = (rowok && xx >= 0 && xx < W) ? ib[(size_t)yy * W + xx] * 0.5f : 0.f;
+            }
 #pragma unroll
             for (int dx = 0; dx < 3; ++dx) {
-                const int xx = 2 * x + dx - 1;
-                const float v = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? ib[(size_t)yy * W + xx] * 0.5f : 0.f;
+                const float* wt = sw + (dy * 3 + dx) * 32;
+                const float p0 = v[dx], p1 = v[dx + 2];
 #pragma unroll
-                for (int o = 0; o < 32; ++o) acc[o] = fmaf(v, sw[o * 9 + dy * 3 + dx], acc[o]);
+                for (int o = 0; o < 32; o += 4) {
+                    const float4 w4 = *reinterpret_cast<const float4*>(wt + o);
+                    a0[o] = fmaf(p0, w4.x, a0[o]); a0[o + 1] = fmaf(p0, w4.y, a0[o + 1]);
+                    a0[o + 2] = fmaf(p0, w4.z, a0[o + 2]); a0[o + 3] = fmaf(p0, w4.w, a0[o + 3]);
+                    a1[o] = fmaf(p1, w4.x, a1[o]); a1[o + 1] = fmaf(p1, w4.y, a1[o + 1]);
+                    a1[o + 2] = fmaf(p1, w4.z, a1[o + 2]); a1[o + 3] = fmaf(p1, w4.w, a1[o + 3]);
+                }
             }
         }
     }
+    const size_t pix = ((size_t)m * Ho_p + y) * Wo + x0;
     __align__(16) __nv_bfloat162 pk[16];
 #pragma unroll
     for (int o = 0; o < 16; ++o)
-        pk[o] = y < Ho ? __floats2bfloat162_rn(fmaxf(acc[2 * o], 0.f), fmaxf(acc[2 * o + 1], 0.f))
+        pk[o] = y < Ho ? __floats2bfloat162_rn(fmaxf(a0[2 * o], 0.f), fmaxf(a0[2 * o + 1], 0.f))
                        : __floats2bfloat162_rn(0.f, 0.f);
-    uint4* dst = reinterpret_cast<uint4*>(out + idx * 32);
+    uint4* dst = reinterpret_cast<uint4*>(out + pix * 32);
 #pragma unroll
     for (int i = 0; i < 4; ++i) dst[i] = reinterpret_cast<uint4*>(pk)[i];
+    if (has1) {
+#pragma unroll
+        for (int o = 0; o < 16; ++o)
+            pk[o] = y < Ho ? __floats2bfloat162_rn(fmaxf(a1[2 * o], 0.f), fmaxf(a1[2 * o + 1], 0.f))
+                           : __floats2bfloat162_rn(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[4 + i] = reinterpret_cast<uint4*>(pk)[i];
+    }
 }
 
 // global average pool of the last layer (NHWC bf16) averaged over each problem's images,
@@ -2187,7 +2220,7 @@ extern "C" int ps_encode_tc(const float* images, int P, int n_img, int H, int W,
     const float* w1 = side + bias_tot;
     {
         const EncLayerGeo& e = g[0];
-        const size_t n = (size_t)NI * e.Ho_p * e.Wo;
+        const size_t n = (size_t)NI * e.Ho_p * ((e.Wo + 1) / 2);
         enc_l1_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(images, NI, H, W, w1, side + e.b_off, e.Ho,
                                                                     e.Wo, e.Ho_p, buf[0]);
         PS_CHECK_LAUNCH();
