@@ -91,7 +91,9 @@ def plan_diffusion_batch(planner, reqs: Sequence[BLPlanRequest], p0: int = 0,
     torch = _lib.require_cuda()
     images, q_start, goal, boxes = (_stack(reqs, f) for f in ("images", "q_start", "goal", "boxes"))
     P, S, T = len(reqs), planner.S, planner.T
-    pin = [torch.from_numpy(a).pin_memory() for a in (images, q_start, goal, boxes)]
+    # host tensors over the stacked arrays (pageable: pinning ~0.6 GB per call would cost more than
+    # the staged copy; BLPlanner.plan_batch with caller-pinned buffers is the zero-copy path)
+    pin = [torch.from_numpy(a) for a in (images, q_start, goal, boxes)]
     ev = {k: torch.cuda.Event(enable_timing=True)
           for k in ("start", "sample_start", "sample_end", "refine_start", "refine_end", "end")}
     t0 = time.perf_counter()
