@@ -424,7 +424,11 @@ def _traffic(n_evals, P, S, T):
     if not cands or (P, S, T) != (1024, 32, 32):
         return None, None
     d = json.loads(cands[-1].read_text())
-    return d["dram_bytes_per_forward"] * n_evals, f"{cands[-1].name} x {n_evals} forwards"
+    # the U-Net layers only (the capture's once-per-call state conversion is not a per-step cost)
+    layers = [x for x in d.get("per_launch", []) if x["kernel"].startswith("unet_tc")]
+    per_fwd = (sum(x["dram_read_bytes"] + x["dram_write_bytes"] for x in layers) if layers
+               else d["dram_bytes_per_forward"])
+    return per_fwd * n_evals, f"{cands[-1].name} x {n_evals} forwards"
 
 
 def _peaks():

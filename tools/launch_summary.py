@@ -1,6 +1,6 @@
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) of `bench.py
 --steps 1 --warmup W`: per-kernel device time over the LAST step (the timed one), found as
-the launches after the last esdf build, and each kernel's share of that step.
+the launches from the last esdf build to its select, and each kernel's share of that step.
 
     python tools/launch_summary.py gpurun_out/launches.csv [out.csv]
 """
@@ -29,7 +29,9 @@ def short(name):
 def main():
     rows = load(sys.argv[1])
     starts = [i for i, (_, n, _) in enumerate(rows) if short(n).startswith("esdf_")]
-    step = rows[starts[-1]:]
+    # ... up to its select launch (bench.py's post-run seed check samples again after the step)
+    ends = [i for i, (_, n, _) in enumerate(rows) if i >= starts[-1] and short(n).startswith("select_kernel")]
+    step = rows[starts[-1]:(ends[-1] + 1 if ends else len(rows))]
     tot = sum(t for _, _, t in step)
     agg = OrderedDict()
     for _, n, t in step:
