@@ -415,9 +415,13 @@ struct ConvArgs {
     const float* W;      // [K][N]
     const float* bias;   // [N]
     float* out;          // [rows][N]
+    float* part;         // split-K: [n_chunks][rows][N] chunk partials (null: one pass over K)
 };
 
-constexpr int CB_M = 64, CB_N = 64, CB_K = 16;
+// K is summed in fixed chunks of F32_KC: each chunk's products are accumulated from zero and the
+// chunk sums are added in chunk order, so one block over all of K (large batches) and one block
+// per chunk + the ordered reduction (small batches, split-K for parallelism) give the same bits
+constexpr int CB_M = 64, CB_N = 64, CB_K = 16, F32_KC = 128;
 
 __global__ void __launch_bounds__(256) conv_gemm_f32_kernel(const __grid_constant__ ConvArgs a) {
     __shared__ float As[CB_K][CB_M + 4];
@@ -425,14 +429,19 @@ __global__ void __launch_bounds__(256) conv_gemm_f32_kernel(const __grid_constan
     const int tid = threadIdx.x;
     const int m0 = blockIdx.x * CB_M, n0 = blockIdx.y * CB_N;
     const int tr = tid / 16, tc = tid % 16;  // 16x16 threads, 4x4 outputs each
+    const int n_chunks = (a.K + F32_KC - 1) / F32_KC;
+    const int ch0 = a.part ? (int)blockIdx.z : 0, ch1 = a.part ? (int)blockIdx.z + 1 : n_chunks;
+    float tot[4][4] = {};
+    for (int ch = ch0; ch < ch1; ++ch) {
     float acc[4][4] = {};
-    for (int k0 = 0; k0 < a.K; k0 += CB_K) {
+    const int kend = min(a.K, (ch + 1) * F32_KC);
+    for (int k0 = ch * F32_KC; k0 < kend; k0 += CB_K) {
         // A tile: 64 rows x 16 k
         for (int i = tid; i < CB_M * CB_K; i += 256) {
             const int r = i / CB_K, kk = i % CB_K;
             const int row = m0 + r, k = k0 + kk;
             float v = 0.f;
-            if (row < a.rows && k < a.K) {
+            if (row < a.rows && k < kend) {
                 int s = 0;
                 while (s + 1 < a.n_seg && k >= a.seg[s + 1].k0) ++s;
                 const PSeg sg = a.seg[s];
@@ -445,7 +454,7 @@ __global__ void __launch_bounds__(256) conv_gemm_f32_kernel(const __grid_constan
         for (int i = tid; i < CB_K * CB_N; i += 256) {
             const int kk = i / CB_N, n = i % CB_N;
             const int k = k0 + kk, col = n0 + n;
-            Bs[kk][n] = (k < a.K && col < a.N) ? a.W[(size_t)k * a.N + col] : 0.f;
+            Bs[kk][n] = (k < kend && col < a.N) ? a.W[(size_t)k * a.N + col] : 0.f;
         }
         __syncthreads();
 #pragma unroll
@@ -463,15 +472,31 @@ __global__ void __launch_bounds__(256) conv_gemm_f32_kernel(const __grid_constan
         __syncthreads();
     }
 #pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tot[i][j] += acc[i][j];
+    }
+    float* dst = a.part ? a.part + (size_t)blockIdx.z * a.rows * a.N : a.out;
+#pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int row = m0 + tr * 4 + i;
         if (row >= a.rows) continue;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int col = n0 + tc * 4 + j;
-            if (col < a.N) a.out[(size_t)row * a.N + col] = acc[i][j] + a.bias[col];
+            if (col < a.N) dst[(size_t)row * a.N + col] = a.part ? tot[i][j] : tot[i][j] + a.bias[col];
         }
     }
+}
+
+// split-K epilogue: out = ((0 + part_0) + part_1 + ...) + bias, the chunk order of the one-pass kernel
+__global__ void conv_f32_reduce_kernel(const float* __restrict__ part, int n_chunks, size_t n, int N,
+                                       const float* __restrict__ bias, float* __restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float t = 0.f;
+    for (int c = 0; c < n_chunks; ++c) t += part[(size_t)c * n + i];
+    out[i] = t + bias[i % N];
 }
 
 // GroupNorm + Mish (+ FiLM) (+ residual) over one (sample, group) per block.
@@ -595,6 +620,10 @@ __global__ void cond_kernel(const float* __restrict__ feat, int n_img, int C, in
 // host orchestration
 // ---------------------------------------------------------------------------
 
+// split-K scratch of the fp32 network (floats), after its 8 activation slots in the workspace
+constexpr size_t F32_SPLIT_SCRATCH = (size_t)4 << 20;
+static thread_local float* split_scratch = nullptr;
+
 static int launch_conv_f32(const Layout& L, const PConv& c, const char* packed, const float* s0, int ld0,
                            const float* s1, int ld1, int Tv, int rows, float* out, cudaStream_t st) {
     ConvArgs a{};
@@ -612,6 +641,20 @@ static int launch_conv_f32(const Layout& L, const PConv& c, const char* packed, 
     a.bias = L.side(packed) + c.b_off;
     a.out = out;
     dim3 grid((rows + CB_M - 1) / CB_M, (c.N + CB_N - 1) / CB_N);
+    // small batches: one block per K chunk when the (rows x N) grid would leave most SMs idle and
+    // the chunk partials fit the split-K scratch (same bits either way, see F32_KC)
+    const int n_chunks = (c.K + F32_KC - 1) / F32_KC;
+    const size_t n_out = (size_t)rows * c.N;
+    if (split_scratch && n_chunks > 1 && grid.x * grid.y < 148 && (size_t)n_chunks * n_out <= F32_SPLIT_SCRATCH) {
+        a.part = split_scratch;
+        grid.z = n_chunks;
+        conv_gemm_f32_kernel<<<grid, 256, 0, st>>>(a);
+        PS_CHECK_LAUNCH();
+        conv_f32_reduce_kernel<<<(unsigned)((n_out + 255) / 256), 256, 0, st>>>(split_scratch, n_chunks, n_out, c.N,
+                                                                               a.bias, out);
+        PS_CHECK_LAUNCH();
+        return PS_OK;
+    }
     conv_gemm_f32_kernel<<<grid, 256, 0, st>>>(a);
     PS_CHECK_LAUNCH();
     return PS_OK;
@@ -651,6 +694,7 @@ int unet_eval_f32(const Layout& L, const char* packed, const float* x, int B, in
     const size_t SL = f32_slot_elems(B, T);
     float* slot[8];
     for (int i = 0; i < 8; ++i) slot[i] = ws + i * SL;
+    split_scratch = ws + 8 * SL;
     float *pre = slot[0], *h = slot[1], *r = slot[2], *skip1 = slot[6], *skip2 = slot[7];
     float* cur = slot[3];
     float* nxt = slot[4];
@@ -751,7 +795,7 @@ extern "C" long long ps_sample_workspace_bytes(int B, int T, int P, int n_steps,
     const size_t state = 2 * (size_t)B * T * U_DOF;
     size_t act;
     if (mode == 0)
-        act = 8 * f32_slot_elems(B, T) * 4;
+        act = (8 * f32_slot_elems(B, T) + F32_SPLIT_SCRATCH) * 4;
     else
         act = tc_workspace_bytes(B, T);
     return (long long)((film + state) * 4 + act + 4096);
