@@ -421,7 +421,7 @@ struct ConvArgs {
 // K is summed in fixed chunks of F32_KC: each chunk's products are accumulated from zero and the
 // chunk sums are added in chunk order, so one block over all of K (large batches) and one block
 // per chunk + the ordered reduction (small batches, split-K for parallelism) give the same bits
-constexpr int CB_M = 64, CB_N = 64, CB_K = 16, F32_KC = 128;
+constexpr int CB_M = 64, CB_N = 64, CB_K = 16, F32_KC = 64;
 
 __global__ void __launch_bounds__(256) conv_gemm_f32_kernel(const __grid_constant__ ConvArgs a) {
     __shared__ float As[CB_K][CB_M + 4];
