@@ -136,6 +136,18 @@ class TestSample:
         assert np.array_equal(full, again)
         del steps
 
+    def test_split_k_invariance(self, sampler, torch_cuda):
+        # the fp32 network sums K in fixed chunks; small grids split the chunks over blocks with an
+        # ordered reduction, large ones loop over them in one block: 2 problems alone (split-K) and
+        # inside a 64-problem batch (one pass) give the same bits
+        P, S = 64, 32
+        cond = _cond(P, 21)
+        x = np.random.default_rng(22).standard_normal((P * S, 32, 7)).astype(np.float32)
+        fa = sampler.film(cond)
+        big = sampler.predict_noise(x, 60, fa, S).cpu().numpy()
+        small = sampler.predict_noise(x[:2 * S], 60, fa[:2], S).cpu().numpy()
+        assert np.array_equal(big[:2 * S], small)
+
     def test_config0_pipeline_encode_then_sample(self, sampler, params):
         pb = synth.config0_problems(1, seed=0)
         cond = sampler.encode(pb.images, pb.q_start, pb.goal)
