@@ -115,6 +115,8 @@ class BLPlanner:
         P = int(q_start.shape[0])
         if P > self.Pmax:
             raise ValueError("batch larger than max_problems")
+        if P == 0:
+            raise ValueError("need at least one problem")   # planseed: "need at least one seed"
         B = P * self.S
         esdf = self.esdf[:P]
         self._esdf_build(boxes, esdf)

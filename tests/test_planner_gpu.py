@@ -334,3 +334,19 @@ class TestRequestApi:
         assert one.best_index == res[1].best_index
         assert np.array_equal(one.trajectory, res[1].trajectory)
         assert one.successes == res[1].successes
+
+
+def test_edge_shapes_one_seed_and_empty(torch_cuda, params, oracle_lib):
+    # one seed per problem (S = 1: select has nothing to choose) through the whole planner, refined
+    # bit-exactly against the C oracle on the GPU's own seeds; an empty batch raises like planseed
+    from paper_2410_16727_b200.planner import BLPlanner
+    pl = BLPlanner(params, ENC, mode=1, S=1, max_problems=3)
+    pb = synth.config3_problems(3, p0=11, seed=0)
+    host = pl.plan_batch(pb.images, pb.q_start, pb.goal, pb.boxes, p0=pb.p0)
+    assert np.array_equal(np.asarray(host.best_index), np.zeros(3, np.int32))
+    seeds = pl.seeds[:3].cpu().numpy()
+    ps = oracle_lib.BLProblemSet(pl.robot, pl.grid, pl.cost, _unbrick(pl, 3), pl.grid.n_nodes)
+    q, c, f, cl = oracle_lib.bl_refine(ps, seeds, 1, pl.cost.n_iters)
+    assert np.array_equal(np.asarray(host.trajectories), q) and np.array_equal(np.asarray(host.cost), c)
+    with pytest.raises(ValueError):
+        pl.plan_batch(pb.images[:0], pb.q_start[:0], pb.goal[:0], pb.boxes[:0])
