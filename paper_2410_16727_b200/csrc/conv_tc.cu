@@ -533,16 +533,6 @@ bool get_encoder() {
     return g_encode != nullptr;
 }
 
-// activation view [B][Tv][C] bf16, box {64, Tv, 128/Tv}
-static bool make_act_map(CUtensorMap* tm, const void* base, int B, int Tv, int C) {
-    cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)Tv, (cuuint64_t)B};
-    cuuint64_t strides[2] = {(cuuint64_t)C * 2, (cuuint64_t)Tv * C * 2};
-    cuuint32_t box[3] = {64, (cuuint32_t)Tv, (cuuint32_t)(128 / Tv)};
-    cuuint32_t es[3] = {1, 1, 1};
-    return g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 // weights [N][Kp] bf16, box {64, N}
 bool make_w_map(CUtensorMap* tm, const void* base, int N, int Kp, int box_rows) {
     cuuint64_t dims[2] = {(cuuint64_t)Kp, (cuuint64_t)N};
@@ -885,7 +875,6 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
                     if (++sa == SA) { sa = 0; pa ^= 1u; }
                     if (resident) continue;
                     for (int k = 0; k < gr.ntap; ++k, ++issued) {
-                        const UtTap tp = s_tap[gr.tap0 + k];
                         if (issued < pre) {   // sent before the dependency wait
                             if (++sb == SB) { sb = 0; pb ^= 1u; }
                             continue;
@@ -1165,7 +1154,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         const int wg = (warp - 2) >> 2;
         const int q = warp & 3;
         const int r = q * 32 + lane;
-        const int t0 = r / nb, sl = r % nb;  // tile row = (time, sample); M-block mb adds 128/nb steps
+        const int sl = r % nb;  // tile row = (time, sample); M-block mb adds 128/nb time steps
         const int tstep = 128 / nb;
         const float inv_n = 1.0f / (float)(Tv * CG);
         float* red = s_red + wg * (4 * 32 * 2 * NG);
@@ -1200,7 +1189,8 @@ __global__ void __launch_bounds__(UT_THREADS, 1) unet_tc_kernel(const __grid_con
         constexpr bool IDRES = EPI == EPI_GN_RES && !RES;
         const int n_slab = MB * (NC / 16);
         auto res_load = [&](uint32_t o, int tile_, int slab, int noff_) {
-            const int mb_ = slab / (NC / 16), c_ = noff_ + cbase + (slab % (NC / 16)) * 16;
+            constexpr int SPM = NC >= 16 ? NC / 16 : 1;   // 16-channel slabs per M-block
+            const int mb_ = slab / SPM, c_ = noff_ + cbase + (slab % SPM) * 16;
             uint64_t* bar = &rbar[ew * 2 + (o & 1u)];
             mbar_expect_tx(bar, 1024u);
             tma_load_3d(sOut + (size_t)(ew * 2 + (o & 1u)) * 1024, &a.tmRes, bar, c_, tile_ * nb,
